@@ -1,0 +1,143 @@
+/*
+ * lsv.h — C ABI of liblsv, the B200 (sm_100a) mixed-rank LoRA delta path.
+ *
+ * What it replaces.  The reference (LoRAServe simulator, /root/reference/pkg/src/lorasim)
+ * has no tensor arithmetic: "apply this co-batched prefill's LoRA deltas" exists only as
+ * the cost callback
+ *     costmodel.prefill_time(prompt_lengths, ranks, params, resident_max_rank)
+ *         /root/reference/pkg/src/lorasim/costmodel.py:83-105
+ *     costmodel.decode_iter_time(context_lengths, ranks, params)      costmodel.py:108-123
+ *     costmodel.fetch_latency(size_bytes, "remote_rdma", params)      costmodel.py:129-143
+ * called by schedule_server (simengine.py:139,146) on the batch it formed FIFO under the
+ * token budget (simengine.py:96-152).  The entry points below are what that callback's
+ * batch actually needs done on a GPU: for every segment s (the tokens of one adapter,
+ * contiguous after a stable sort by adapter slot)
+ *
+ *     y[t, :] += (x[t, :] · A_s^T) · B_s^T            t in [seg_indptr[s], seg_indptr[s+1])
+ *
+ * with A_s = lora_A [rank_s, h_in] and B_s = lora_B [h_out, rank_s] (PEFT layout), bf16
+ * operands, fp32 accumulation, bf16 y updated in place.  Each segment pays for its own
+ * rank (the B200 path deliberately does NOT reproduce costmodel.py:104's "whole batch pays
+ * the max rank").  A_s/B_s pointers may be local HBM or NVLink peer addresses: the
+ * reference's remote fetch (pool.py:101-132 plan_fetch → fetch_remote, priced by
+ * fetch_latency(..., "remote_rdma")) becomes a peer load inside the kernel.
+ *
+ * Conventions (mirroring the reference's error behaviour, costmodel.py:95-103, pool.py:75-80):
+ *   - every call returns LSV_OK (0) or an error code; lsv_last_error() returns a
+ *     thread-local message for the last nonzero return;
+ *   - LSV_EINVAL / LSV_EWORKSPACE map to Python ValueError, LSV_ECUDA / LSV_EUNSUPPORTED
+ *     to RuntimeError in the shim (paper_2511_22880_b200/native.py);
+ *   - all device work is asynchronous on the caller's stream; the library never
+ *     allocates in lsv_lora_apply and keeps no mutable global state besides cached
+ *     device attributes and driver entry points.
+ */
+#ifndef LSV_H_
+#define LSV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSV_ABI_VERSION 1
+
+#define LSV_OK 0
+#define LSV_EINVAL 1
+#define LSV_ECUDA 2
+#define LSV_EUNSUPPORTED 3
+#define LSV_EWORKSPACE 4
+
+#define LSV_DTYPE_BF16 0
+
+/* Tier policy for lsv_plan_build: AUTO chooses per segment (SIMT warp-shuffle tier for
+ * short segments, tcgen05 tier otherwise); the forced policies exist for tests/benchmarks. */
+#define LSV_TIER_AUTO 0
+#define LSV_TIER_SIMT 1
+#define LSV_TIER_TC 2
+
+typedef void* lsv_stream_t; /* a cudaStream_t */
+
+/* ABI version (LSV_ABI_VERSION). */
+int lsv_version(void);
+
+/* Message for the last nonzero return on this thread ("" if none). */
+const char* lsv_last_error(void);
+
+/* ---- adapter slab format -------------------------------------------------------------
+ * Replaces the reference's "adapter is GPU-resident in a slot" notion
+ * (pool.py:88-99 touch_gpu / is_gpu_resident; gpu_slots config.py:29): an adapter in a GPU
+ * slot is a pair of tiled buffers in HBM, packed once at load time so the kernels can
+ * move them with single bulk copies. */
+size_t lsv_adapter_a_bytes(int32_t rank, int32_t h_in);
+size_t lsv_adapter_b_bytes(int32_t rank, int32_t h_out);
+
+/* Pack PEFT-layout device tensors lora_A [rank][h_in] and lora_B [h_out][rank] (bf16,
+ * row-major, contiguous) into the tiled slab buffers a_tiled / b_tiled (device).
+ * rank must be a multiple of 8 in [8, 256]; h_in, h_out multiples of 128. */
+int lsv_pack_adapter(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in,
+                     int32_t h_out, void* a_tiled, void* b_tiled, lsv_stream_t stream);
+
+/* Inverse of lsv_pack_adapter (used by tests and by peer copy-on-first-use checks). */
+int lsv_unpack_adapter(const void* a_tiled, const void* b_tiled, int32_t rank, int32_t h_in,
+                       int32_t h_out, void* lora_a, void* lora_b, lsv_stream_t stream);
+
+/* ---- plan ------------------------------------------------------------------------------
+ * Host-side work planning for one (batch, projection shape).  seg_indptr [S+1] and
+ * seg_rank [S] are HOST arrays (the segment indexer's output); seg_indptr[0] must be 0,
+ * non-decreasing, seg_rank[s] in {8,16,...,256}.  The plan is a self-describing int32
+ * blob: segment table, per-segment tier, the LPT-ordered shrink and expand work lists
+ * and the workspace layout.  Copy it to the device once and reuse it for every layer
+ * and projection of the same shape. */
+int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                  int32_t h_in, int32_t h_out, int32_t tier_policy, size_t* plan_bytes,
+                  size_t* workspace_bytes);
+
+int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                   int32_t h_in, int32_t h_out, int32_t tier_policy, void* plan_host,
+                   size_t plan_bytes);
+
+/* Fill out[0..7] from a host plan: {num_segments, num_tokens, h_in, h_out,
+ * n_simt_segments, n_tc_mtiles, n_shrink_items, n_expand_items}. */
+int lsv_plan_summary(const void* plan_host, int32_t* out8);
+
+/* ---- apply -----------------------------------------------------------------------------
+ * y[t,:] += (x[t,:]·A_s^T)·B_s^T for every segment of the plan.
+ *   x  : [num_tokens][h_in] bf16, row stride ldx elements (device, 16-byte aligned rows)
+ *   y  : [num_tokens][h_out] bf16, row stride ldy elements (device), updated in place
+ *   a_ptrs, b_ptrs : device arrays [num_segments] of device pointers to the segment's
+ *        tiled A/B (lsv_pack_adapter format); local or NVLink-peer addresses
+ *   plan_dev / plan_host : the same plan blob, on device and on host
+ *   workspace : device scratch of at least the planned workspace_bytes, zero-filled once
+ *        at allocation (the kernels leave their counters zeroed again on exit). */
+int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype,
+                   int32_t num_tokens, int32_t h_in, int32_t h_out, const void* const* a_ptrs,
+                   const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                   void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* Shrink only: writes the per-segment bf16 intermediate v (x·A^T) into the workspace
+ * v-image area.  Together with lsv_lora_expand this splits lsv_lora_apply around an
+ * exchange (tensor-parallel all-gather of v). */
+int lsv_lora_shrink(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in,
+                    const void* const* a_ptrs, const void* plan_dev, const void* plan_host,
+                    void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out,
+                    const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                    void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* ---- NVLink peers ----------------------------------------------------------------------
+ * Replaces the reference's GPUDirect-RDMA remote fetch (pool.py:101-132, costmodel.py:139-140)
+ * for single-process multi-GPU use: enable direct peer loads from `peer`'s HBM on `dev`.
+ * Returns LSV_EUNSUPPORTED if the pair cannot access each other. */
+int lsv_enable_peer(int32_t dev, int32_t peer);
+
+/* Number of SMs the planner assumes (queried from device 0 once; 148 on B200). */
+int lsv_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LSV_H_ */

@@ -1,0 +1,454 @@
+// lsv_api.cu — liblsv C ABI: planner, adapter packing, apply / shrink / expand, peers.
+// See include/lsv.h for the reference interfaces each entry point replaces.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "../../include/lsv.h"
+#include "lsv_common.cuh"
+#include "lsv_plan.h"
+#include "lsv_simt.cuh"
+#include "lsv_tc.cuh"
+
+using namespace lsv;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define LSV_CUDA_CHECK(expr)                                                        \
+  do {                                                                              \
+    cudaError_t e__ = (expr);                                                       \
+    if (e__ != cudaSuccess)                                                         \
+      return fail(LSV_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e__));       \
+  } while (0)
+
+// ---- planner knobs ------------------------------------------------------------------------
+// AUTO tier rule: segments of at most kAutoSimtMaxTok tokens (decode / tiny prefill) or
+// rank > 128 go to the SIMT tier; everything else is tcgen05.  Justified by the per-tier
+// measurements in DESIGN.md §4 (profiles/).
+constexpr int kAutoSimtMaxTok = 8;
+constexpr int64_t kMinItemBytes = 96 * 1024;  // smallest shrink k-split worth a pipeline fill
+
+int num_sms_cached() {
+  static int sms = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) {
+      int dev = 0, v = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+    }
+    cudaGetLastError();
+    if (sms <= 0) sms = kNumSmsDefault;
+  });
+  return sms;
+}
+
+struct PlanBuilder {
+  PlanHeader h{};
+  std::vector<int32_t> indptr, rank, tier;
+  std::vector<SimtItem> simt;
+  std::vector<MTile> mtiles;
+  std::vector<ShrinkItem> shrink;
+  std::vector<ExpandItem> expand;
+};
+
+int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t h_out) {
+  if (S < 0) return fail(LSV_EINVAL, "num_segments must be >= 0, got %d", S);
+  if (S > 0 && (!indptr || !rank)) return fail(LSV_EINVAL, "seg_indptr/seg_rank must be non-null");
+  if (h_in <= 0 || h_in % 128) return fail(LSV_EINVAL, "h_in must be a positive multiple of 128, got %d", h_in);
+  if (h_out <= 0 || h_out % 128) return fail(LSV_EINVAL, "h_out must be a positive multiple of 128, got %d", h_out);
+  if (S > 0 && indptr[0] != 0) return fail(LSV_EINVAL, "seg_indptr[0] must be 0, got %d", indptr[0]);
+  for (int s = 0; s < S; ++s) {
+    if (indptr[s + 1] < indptr[s])
+      return fail(LSV_EINVAL, "seg_indptr must be non-decreasing (segment %d: %d < %d)", s, indptr[s + 1], indptr[s]);
+    if (rank[s] < 8 || rank[s] > 256 || rank[s] % 8)
+      return fail(LSV_EINVAL, "segment %d: rank must be a multiple of 8 in [8, 256], got %d", s, rank[s]);
+  }
+  return LSV_OK;
+}
+
+int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t h_out,
+               int32_t policy) {
+  if (int rc = validate_segments(S, indptr, rank, h_in, h_out)) return rc;
+  if (policy != LSV_TIER_AUTO && policy != LSV_TIER_SIMT && policy != LSV_TIER_TC)
+    return fail(LSV_EINVAL, "unknown tier policy %d", policy);
+  const int N = S > 0 ? indptr[S] : 0;
+  pb.indptr.assign(indptr, indptr + S + 1);
+  if (S == 0) pb.indptr.assign(1, 0);
+  pb.rank.assign(rank, rank + S);
+  pb.tier.assign(S, kTierNone);
+  const int nsm = num_sms_cached();
+
+  // tier per segment
+  int64_t v_off = 0;
+  for (int s = 0; s < S; ++s) {
+    const int n = indptr[s + 1] - indptr[s];
+    if (n == 0) continue;
+    bool simt;
+    if (policy == LSV_TIER_SIMT) simt = true;
+    else if (policy == LSV_TIER_TC) simt = rank[s] > 128;
+    else simt = n <= kAutoSimtMaxTok || rank[s] > 128;
+    pb.tier[s] = simt ? kTierSimt : kTierTc;
+    if (simt) {
+      for (int tb = 0; tb < n; tb += kSimtMaxTok) {
+        const int nt = std::min(kSimtMaxTok, n - tb);
+        pb.simt.push_back(SimtItem{s, indptr[s] + tb, nt, (int32_t)v_off});
+        v_off += (int64_t)nt * rank[s];
+      }
+    } else {
+      for (int tb = 0; tb < n; tb += kTileM) {
+        MTile mt{};
+        mt.seg = s; mt.tok_begin = indptr[s] + tb; mt.ntok = std::min(kTileM, n - tb); mt.rank = rank[s];
+        pb.mtiles.push_back(mt);
+      }
+    }
+  }
+  // shrink splits: balance bytes across ~2 waves of the SMs
+  const int chunks = h_in / kChunk;
+  std::vector<int64_t> row_bytes(pb.mtiles.size()), kch(pb.mtiles.size());
+  int64_t total = 0;
+  for (size_t i = 0; i < pb.mtiles.size(); ++i) {
+    const MTile& mt = pb.mtiles[i];
+    row_bytes[i] = (int64_t)(round_up(mt.ntok, 8) + mt.rank) * 128;
+    kch[i] = std::max<int64_t>(1, std::min<int64_t>(4, kShrinkSlotBytes / row_bytes[i]));
+    total += row_bytes[i] * chunks;
+  }
+  const int64_t target = std::max<int64_t>(kMinItemBytes, total / std::max(1, 2 * nsm));
+  int64_t part_off = 0, vimg_off = 0;
+  int counter = 0;
+  struct Costed { int64_t cost; int key; };
+  std::vector<std::pair<int64_t, ShrinkItem>> shrink_costed;
+  for (size_t i = 0; i < pb.mtiles.size(); ++i) {
+    MTile& mt = pb.mtiles[i];
+    const int stages = (chunks + kch[i] - 1) / kch[i];
+    const int64_t mt_bytes = row_bytes[i] * chunks;
+    int nsplit = (int)std::min<int64_t>(stages, std::max<int64_t>(1, (mt_bytes + target - 1) / target));
+    const int sps = (stages + nsplit - 1) / nsplit;  // stages per split
+    nsplit = (stages + sps - 1) / sps;
+    mt.nsplit = nsplit;
+    mt.part_off = (int32_t)part_off;
+    if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * mt.rank;
+    const int kp16 = std::max(16, mt.rank);
+    mt.vimg_off = (int32_t)vimg_off;
+    vimg_off += (int64_t)round_up(mt.ntok, 16) * kp16 * 2;
+    mt.counter = counter++;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      ShrinkItem it{};
+      it.mtile = (int32_t)i;
+      it.chunk_begin = (int32_t)(sp * sps * kch[i]);
+      it.chunk_end = (int32_t)std::min<int64_t>(chunks, (int64_t)(sp + 1) * sps * kch[i]);
+      it.split_kch = sp | (int32_t)(kch[i] << 16);
+      shrink_costed.push_back({row_bytes[i] * (it.chunk_end - it.chunk_begin), it});
+    }
+  }
+  std::stable_sort(shrink_costed.begin(), shrink_costed.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  for (auto& c : shrink_costed) pb.shrink.push_back(c.second);
+
+  std::vector<std::pair<int64_t, ExpandItem>> expand_costed;
+  for (size_t i = 0; i < pb.mtiles.size(); ++i) {
+    const MTile& mt = pb.mtiles[i];
+    const int64_t cost = 128LL * mt.rank * 2 + (int64_t)mt.ntok * 128 * 4;
+    for (int jt = 0; jt < h_out / kExpandW; ++jt) expand_costed.push_back({cost, ExpandItem{(int32_t)i, jt}});
+  }
+  std::stable_sort(expand_costed.begin(), expand_costed.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  for (auto& c : expand_costed) pb.expand.push_back(c.second);
+
+  // header + workspace layout
+  PlanHeader& h = pb.h;
+  h.magic = kPlanMagic; h.version = kPlanVersion;
+  h.num_segments = S; h.num_tokens = N; h.h_in = h_in; h.h_out = h_out;
+  h.n_simt_items = (int32_t)pb.simt.size();
+  h.n_mtiles = (int32_t)pb.mtiles.size();
+  h.n_shrink_items = (int32_t)pb.shrink.size();
+  h.n_expand_items = (int32_t)pb.expand.size();
+  h.shrink_grid = std::min(h.n_shrink_items, nsm);
+  h.expand_grid = std::min(h.n_expand_items, nsm);
+  int32_t off = sizeof(PlanHeader) / 4;
+  h.off_seg_indptr = off; off += S + 1;
+  h.off_seg_rank = off; off += S;
+  h.off_seg_tier = off; off += S;
+  off = round_up(off, 4);
+  h.off_simt_items = off; off += 4 * h.n_simt_items;
+  h.off_mtiles = off; off += 8 * h.n_mtiles;
+  h.off_shrink_items = off; off += 4 * h.n_shrink_items;
+  h.off_expand_items = off; off += 2 * h.n_expand_items;
+  h.total_ints = off;
+  int64_t ws = 0;
+  h.ws_counters = 0; ws += round_up(std::max(1, counter) * 4, 256);
+  h.ws_partials = (int32_t)ws; ws += (part_off * 4 + 255) / 256 * 256;
+  h.ws_vimg = (int32_t)ws; ws += (vimg_off + 1023) / 1024 * 1024;
+  h.ws_simt_v = (int32_t)ws; ws += (v_off * 4 + 255) / 256 * 256;
+  if (ws > INT32_MAX) return fail(LSV_EUNSUPPORTED, "workspace of %lld bytes exceeds 2 GiB", (long long)ws);
+  h.ws_bytes = (int32_t)ws;
+  h.n_counters = counter;
+  int simt_segs = 0;
+  for (int s = 0; s < S; ++s) simt_segs += pb.tier[s] == kTierSimt;
+  h.simt_segments = simt_segs;
+  return LSV_OK;
+}
+
+const PlanHeader* check_plan(const void* plan_host) {
+  const PlanHeader* h = static_cast<const PlanHeader*>(plan_host);
+  if (!h || h->magic != kPlanMagic || h->version != kPlanVersion) return nullptr;
+  return h;
+}
+
+// ---- driver entry point for TMA descriptors (no link-time libcuda dependency) -------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+int make_x_maps(CUtensorMap* maps, const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  for (int b = 0; b < 5; ++b) {
+    const cuuint64_t dims[2] = {(cuuint64_t)h_in, (cuuint64_t)num_tokens};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)(8 << b)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) for box rows %d", (int)r, 8 << b);
+  }
+  return LSV_OK;
+}
+
+int ensure_smem_attrs() {
+  static int rc = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaError_t e1 = cudaFuncSetAttribute(shrink_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          shrink_smem_bytes());
+    cudaError_t e2 = cudaFuncSetAttribute(expand_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          expand_smem_bytes());
+    rc = (e1 == cudaSuccess && e2 == cudaSuccess) ? LSV_OK : LSV_ECUDA;
+    if (rc) fail(LSV_ECUDA, "cudaFuncSetAttribute(smem) failed: %s / %s", cudaGetErrorString(e1), cudaGetErrorString(e2));
+  });
+  return rc;
+}
+
+int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_dev, const void* ws) {
+  if (!h) return fail(LSV_EINVAL, "plan_host is not a liblsv plan");
+  if (!plan_dev) return fail(LSV_EINVAL, "plan_dev is null");
+  if (workspace_bytes < (size_t)h->ws_bytes)
+    return fail(LSV_EWORKSPACE, "workspace of %zu bytes is smaller than the planned %d", workspace_bytes, h->ws_bytes);
+  if (h->ws_bytes > 0 && !ws) return fail(LSV_EINVAL, "workspace is null");
+  return LSV_OK;
+}
+
+int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
+               const int32_t* plan, uint8_t* ws, cudaStream_t st) {
+  if (h->n_simt_items > 0) {
+    simt_shrink_kernel<<<h->n_simt_items, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
+                                                        h->off_simt_items, h->off_seg_rank, a_ptrs,
+                                                        reinterpret_cast<float*>(ws + h->ws_simt_v));
+    LSV_CUDA_CHECK(cudaGetLastError());
+  }
+  if (h->n_shrink_items > 0) {
+    if (int rc = ensure_smem_attrs()) return rc;
+    ShrinkParams p{};
+    if (int rc = make_x_maps(p.xmap, x, ldx, num_tokens, h->h_in)) return rc;
+    p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
+    p.n_items = h->n_shrink_items; p.off_items = h->off_shrink_items; p.off_mtiles = h->off_mtiles;
+    p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg; p.ws_counters = h->ws_counters;
+    shrink_tc_kernel<<<h->shrink_grid, kTcThreads, shrink_smem_bytes(), st>>>(p);
+    LSV_CUDA_CHECK(cudaGetLastError());
+  }
+  return LSV_OK;
+}
+
+int run_expand(const PlanHeader* h, void* y, int64_t ldy, const void* const* b_ptrs, const int32_t* plan, uint8_t* ws,
+               cudaStream_t st) {
+  if (h->n_simt_items > 0) {
+    simt_expand_kernel<<<dim3(h->n_simt_items, h->h_out / 128), 64, 0, st>>>(
+        static_cast<__nv_bfloat16*>(y), ldy, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
+        reinterpret_cast<const float*>(ws + h->ws_simt_v));
+    LSV_CUDA_CHECK(cudaGetLastError());
+  }
+  if (h->n_expand_items > 0) {
+    if (int rc = ensure_smem_attrs()) return rc;
+    ExpandParams p{};
+    p.plan = plan; p.b_ptrs = b_ptrs; p.ws = ws; p.y = static_cast<__nv_bfloat16*>(y); p.ldy = ldy;
+    p.n_items = h->n_expand_items; p.off_items = h->off_expand_items; p.off_mtiles = h->off_mtiles;
+    p.ws_vimg = h->ws_vimg;
+    expand_tc_kernel<<<h->expand_grid, kTcThreads, expand_smem_bytes(), st>>>(p);
+    LSV_CUDA_CHECK(cudaGetLastError());
+  }
+  return LSV_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int lsv_version(void) { return LSV_ABI_VERSION; }
+const char* lsv_last_error(void) { return g_err; }
+int lsv_num_sms(void) { return num_sms_cached(); }
+
+size_t lsv_adapter_a_bytes(int32_t rank, int32_t h_in) {
+  return (rank > 0 && h_in > 0) ? (size_t)rank * h_in * 2 : 0;
+}
+size_t lsv_adapter_b_bytes(int32_t rank, int32_t h_out) {
+  return (rank > 0 && h_out > 0) ? (size_t)rank * h_out * 2 : 0;
+}
+
+static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in, int32_t h_out,
+                       void* a_tiled, void* b_tiled, lsv_stream_t stream, int unpack) {
+  if (rank < 8 || rank > 256 || rank % 8) return fail(LSV_EINVAL, "rank must be a multiple of 8 in [8, 256], got %d", rank);
+  if (h_in <= 0 || h_in % 128 || h_out <= 0 || h_out % 128)
+    return fail(LSV_EINVAL, "h_in/h_out must be positive multiples of 128 (got %d, %d)", h_in, h_out);
+  if (!lora_a || !lora_b || !a_tiled || !b_tiled) return fail(LSV_EINVAL, "null buffer");
+  if (!aligned16(lora_a) || !aligned16(lora_b) || !aligned16(a_tiled) || !aligned16(b_tiled))
+    return fail(LSV_EINVAL, "buffers must be 16-byte aligned");
+  const int64_t units = ((int64_t)rank * h_in + (int64_t)h_out * rank) / 8;
+  const int blocks = (int)std::min<int64_t>(4096, (units + 255) / 256);
+  pack_adapter_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(lora_a), static_cast<const uint8_t*>(lora_b), rank, h_in, h_out,
+      static_cast<uint8_t*>(a_tiled), static_cast<uint8_t*>(b_tiled), unpack);
+  LSV_CUDA_CHECK(cudaGetLastError());
+  return LSV_OK;
+}
+
+int lsv_pack_adapter(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in, int32_t h_out,
+                     void* a_tiled, void* b_tiled, lsv_stream_t stream) {
+  return pack_common(lora_a, lora_b, rank, h_in, h_out, a_tiled, b_tiled, stream, 0);
+}
+
+int lsv_unpack_adapter(const void* a_tiled, const void* b_tiled, int32_t rank, int32_t h_in, int32_t h_out,
+                       void* lora_a, void* lora_b, lsv_stream_t stream) {
+  return pack_common(lora_a, lora_b, rank, h_in, h_out, const_cast<void*>(a_tiled), const_cast<void*>(b_tiled),
+                     stream, 1);
+}
+
+int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                  int32_t h_out, int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes) {
+  PlanBuilder pb;
+  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, h_out, tier_policy)) return rc;
+  if (plan_bytes) *plan_bytes = (size_t)pb.h.total_ints * 4;
+  if (workspace_bytes) *workspace_bytes = (size_t)pb.h.ws_bytes;
+  return LSV_OK;
+}
+
+int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                   int32_t h_out, int32_t tier_policy, void* plan_host, size_t plan_bytes) {
+  PlanBuilder pb;
+  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, h_out, tier_policy)) return rc;
+  const PlanHeader& h = pb.h;
+  if (!plan_host) return fail(LSV_EINVAL, "plan_host is null");
+  if (plan_bytes < (size_t)h.total_ints * 4)
+    return fail(LSV_EINVAL, "plan buffer of %zu bytes is smaller than %d", plan_bytes, h.total_ints * 4);
+  int32_t* out = static_cast<int32_t*>(plan_host);
+  std::memset(out, 0, (size_t)h.total_ints * 4);
+  std::memcpy(out, &h, sizeof(h));
+  std::copy(pb.indptr.begin(), pb.indptr.end(), out + h.off_seg_indptr);
+  std::copy(pb.rank.begin(), pb.rank.end(), out + h.off_seg_rank);
+  std::copy(pb.tier.begin(), pb.tier.end(), out + h.off_seg_tier);
+  std::memcpy(out + h.off_simt_items, pb.simt.data(), pb.simt.size() * sizeof(SimtItem));
+  std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
+  std::memcpy(out + h.off_shrink_items, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkItem));
+  std::memcpy(out + h.off_expand_items, pb.expand.data(), pb.expand.size() * sizeof(ExpandItem));
+  return LSV_OK;
+}
+
+int lsv_plan_summary(const void* plan_host, int32_t* out8) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (!h || !out8) return fail(LSV_EINVAL, "not a liblsv plan");
+  const int32_t v[8] = {h->num_segments, h->num_tokens, h->h_in, h->h_out,
+                        h->simt_segments, h->n_mtiles, h->n_shrink_items, h->n_expand_items};
+  std::memcpy(out8, v, sizeof(v));
+  return LSV_OK;
+}
+
+int lsv_lora_shrink(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in, const void* const* a_ptrs,
+                    const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                    lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (h->h_in != h_in) return fail(LSV_EINVAL, "h_in %d does not match the plan's %d", h_in, h->h_in);
+  if (num_tokens < h->num_tokens)
+    return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (h->num_tokens == 0) return LSV_OK;
+  if (!x || !a_ptrs) return fail(LSV_EINVAL, "x / a_ptrs must be non-null");
+  if (!aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "x must be 16-byte aligned with ldx %% 8 == 0, ldx >= h_in");
+  return run_shrink(h, x, ldx, num_tokens, a_ptrs, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, const void* const* b_ptrs,
+                    const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                    lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (h->h_out != h_out) return fail(LSV_EINVAL, "h_out %d does not match the plan's %d", h_out, h->h_out);
+  if (num_tokens < h->num_tokens)
+    return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (h->num_tokens == 0) return LSV_OK;
+  if (!y || !b_ptrs) return fail(LSV_EINVAL, "y / b_ptrs must be non-null");
+  if (!aligned16(y) || ldy % 8 || ldy < h_out) return fail(LSV_EINVAL, "y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out");
+  return run_expand(h, y, ldy, b_ptrs, static_cast<const int32_t*>(plan_dev), static_cast<uint8_t*>(workspace),
+                    static_cast<cudaStream_t>(stream));
+}
+
+int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype, int32_t num_tokens, int32_t h_in,
+                   int32_t h_out, const void* const* a_ptrs, const void* const* b_ptrs, const void* plan_dev,
+                   const void* plan_host, void* workspace, size_t workspace_bytes, lsv_stream_t stream) {
+  if (dtype != LSV_DTYPE_BF16) return fail(LSV_EUNSUPPORTED, "only LSV_DTYPE_BF16 is supported, got %d", dtype);
+  if (int rc = lsv_lora_shrink(x, ldx, num_tokens, h_in, a_ptrs, plan_dev, plan_host, workspace, workspace_bytes,
+                               stream))
+    return rc;
+  return lsv_lora_expand(y, ldy, num_tokens, h_out, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes, stream);
+}
+
+int lsv_enable_peer(int32_t dev, int32_t peer) {
+  if (dev == peer) return LSV_OK;
+  int can = 0;
+  LSV_CUDA_CHECK(cudaDeviceCanAccessPeer(&can, dev, peer));
+  if (!can) return fail(LSV_EUNSUPPORTED, "device %d cannot access peer %d", dev, peer);
+  int cur = 0;
+  LSV_CUDA_CHECK(cudaGetDevice(&cur));
+  LSV_CUDA_CHECK(cudaSetDevice(dev));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); e = cudaSuccess; }
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(LSV_ECUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", dev, peer, cudaGetErrorString(e));
+  return LSV_OK;
+}
+
+}  // extern "C"

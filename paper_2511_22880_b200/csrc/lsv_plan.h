@@ -1,0 +1,65 @@
+// lsv_plan.h — the int32 plan blob shared by the host planner (lsv_plan.cpp) and the kernels.
+//
+// One plan covers one co-batched token batch (the reference's prefill batch,
+// simengine.py:96-152 schedule_server) for one projection shape (h_in, h_out).  It is
+// built on the host from the segment indexer's output and copied to HBM once; every
+// layer/projection of that shape reuses it.
+#pragma once
+#include <stdint.h>
+
+namespace lsv {
+
+constexpr int32_t kPlanMagic = 0x5056534c;  // "LSVP"
+constexpr int32_t kPlanVersion = 1;
+
+enum Tier : int32_t { kTierNone = 0, kTierSimt = 1, kTierTc = 2 };
+
+struct PlanHeader {            // 64 int32
+  int32_t magic, version;
+  int32_t num_segments, num_tokens, h_in, h_out;
+  int32_t n_simt_items;        // SIMT tier work items: <= kSimtMaxTok tokens of one segment
+  int32_t n_mtiles;            // tcgen05 tier 128-token tiles
+  int32_t n_shrink_items;      // tcgen05 shrink work items (mtile, k-range)
+  int32_t n_expand_items;      // tcgen05 expand work items (mtile, 128-wide h_out tile)
+  int32_t shrink_grid, expand_grid;
+  // int32 offsets of the arrays inside the blob
+  int32_t off_seg_indptr, off_seg_rank, off_seg_tier;
+  int32_t off_simt_items, off_mtiles, off_shrink_items, off_expand_items;
+  int32_t total_ints;
+  // workspace layout, byte offsets (workspace < 2 GiB)
+  int32_t ws_counters, ws_partials, ws_vimg, ws_simt_v, ws_bytes;
+  int32_t n_counters;
+  int32_t simt_segments;
+  int32_t reserved[64 - 27];
+};
+static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
+
+struct SimtItem {              // 4 int32
+  int32_t seg, tok_begin, ntok, v_off;  // v_off: float index of this item's fp32 v [ntok][rank]
+};
+
+struct MTile {                 // 8 int32
+  int32_t seg, tok_begin, ntok, rank;
+  int32_t nsplit;              // shrink k-splits reduced by the last-arriving CTA
+  int32_t part_off;            // float index of partials [nsplit][ntok][rank] (if nsplit > 1)
+  int32_t vimg_off;            // byte offset of the bf16 v image (16-byte aligned)
+  int32_t counter;             // index of this tile's split-arrival counter
+};
+
+struct ShrinkItem {            // 4 int32
+  int32_t mtile, chunk_begin, chunk_end;  // k-range in 64-element chunks of h_in
+  int32_t split_kch;           // split index (low 16 bits) | chunks per pipeline stage << 16
+};
+
+struct ExpandItem {            // 2 int32
+  int32_t mtile, jtile;        // h_out columns [jtile*128, jtile*128+128)
+};
+
+// Pipeline geometry (bytes of shared memory).
+constexpr int kShrinkSlotBytes = 48 * 1024;
+constexpr int kShrinkSlots = 4;
+constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past short token tiles
+constexpr int kExpandSlotBytes = 64 * 1024;
+constexpr int kExpandSlots = 3;
+
+}  // namespace lsv

@@ -1,0 +1,134 @@
+// lsv_simt.cuh — CUDA-core (warp-shuffle) tier and the adapter pack/unpack kernels.
+//
+// The SIMT tier serves segments too short to fill a 128-row tcgen05 tile: decode steps
+// (one token per request, the reference's decode_iter_time regime, costmodel.py:108-123)
+// and tiny prefill segments.  Shrink: one warp per rank row, lanes stride h_in with 16-byte
+// loads of x and of the tiled A row, warp-shuffle reduction.  Expand: one thread per two
+// h_out columns, bf16x2 read-modify-write of y.
+#pragma once
+#include "lsv_common.cuh"
+#include "lsv_plan.h"
+
+namespace lsv {
+
+__device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
+  float s = bf16_lo(a.x) * bf16_lo(b.x);
+  s = fmaf(bf16_hi(a.x), bf16_hi(b.x), s);
+  s = fmaf(bf16_lo(a.y), bf16_lo(b.y), s);
+  s = fmaf(bf16_hi(a.y), bf16_hi(b.y), s);
+  s = fmaf(bf16_lo(a.z), bf16_lo(b.z), s);
+  s = fmaf(bf16_hi(a.z), bf16_hi(b.z), s);
+  s = fmaf(bf16_lo(a.w), bf16_lo(b.w), s);
+  s = fmaf(bf16_hi(a.w), bf16_hi(b.w), s);
+  return s;
+}
+
+// grid = n_simt_items, block = 256 (8 warps).  v[item] = x[tokens] · A^T, fp32 [ntok][rank].
+__global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                          int h_in, const int32_t* __restrict__ plan,
+                                                          int off_items, int off_rank,
+                                                          const void* const* __restrict__ a_ptrs,
+                                                          float* __restrict__ simt_v) {
+  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
+  const int r = plan[off_rank + it.seg];
+  const uint8_t* a = static_cast<const uint8_t*>(a_ptrs[it.seg]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint8_t* xrow[kSimtMaxTok];
+#pragma unroll
+  for (int t = 0; t < kSimtMaxTok; ++t)
+    xrow[t] = reinterpret_cast<const uint8_t*>(x + (int64_t)(it.tok_begin + min(t, it.ntok - 1)) * ldx);
+  for (int k = warp; k < r; k += 8) {
+    float acc[kSimtMaxTok];
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
+    for (int i0 = lane * 8; i0 < h_in; i0 += 256) {
+      const uint4 av = __ldg(reinterpret_cast<const uint4*>(a + a_tiled_off(k, i0, r)));
+#pragma unroll
+      for (int t = 0; t < kSimtMaxTok; ++t) {
+        if (t < it.ntok) {
+          const uint4 xv = __ldg(reinterpret_cast<const uint4*>(xrow[t] + (size_t)i0 * 2));
+          acc[t] += dot8_bf16(av, xv);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < kSimtMaxTok; ++t)
+        if (t < it.ntok) simt_v[it.v_off + t * r + k] = acc[t];
+    }
+  }
+}
+
+// grid = (n_simt_items, h_out/128), block = 64: thread owns h_out columns j, j+1.
+__global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy,
+                                                         const int32_t* __restrict__ plan, int off_items,
+                                                         int off_rank, const void* const* __restrict__ b_ptrs,
+                                                         const float* __restrict__ simt_v) {
+  __shared__ float vs[kSimtMaxTok * 256];
+  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
+  const int r = plan[off_rank + it.seg];
+  const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
+  for (int e = threadIdx.x; e < it.ntok * r; e += blockDim.x) vs[e] = simt_v[it.v_off + e];
+  __syncthreads();
+  const int j = blockIdx.y * 128 + threadIdx.x * 2;
+  float acc0[kSimtMaxTok], acc1[kSimtMaxTok];
+#pragma unroll
+  for (int t = 0; t < kSimtMaxTok; ++t) acc0[t] = acc1[t] = 0.f;
+  for (int kc = 0; kc < r; kc += 8) {
+    const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, kc, r)));
+    const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j + 1, kc, r)));
+    const float w0[8] = {bf16_lo(b0.x), bf16_hi(b0.x), bf16_lo(b0.y), bf16_hi(b0.y),
+                         bf16_lo(b0.z), bf16_hi(b0.z), bf16_lo(b0.w), bf16_hi(b0.w)};
+    const float w1[8] = {bf16_lo(b1.x), bf16_hi(b1.x), bf16_lo(b1.y), bf16_hi(b1.y),
+                         bf16_lo(b1.z), bf16_hi(b1.z), bf16_lo(b1.w), bf16_hi(b1.w)};
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) {
+      if (t < it.ntok) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float vv = vs[t * r + kc + e];
+          acc0[t] = fmaf(vv, w0[e], acc0[t]);
+          acc1[t] = fmaf(vv, w1[e], acc1[t]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kSimtMaxTok; ++t) {
+    if (t < it.ntok) {
+      uint32_t* py = reinterpret_cast<uint32_t*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
+      const uint32_t yv = *py;
+      *py = pack_bf16x2(bf16_lo(yv) + acc0[t], bf16_hi(yv) + acc1[t]);
+    }
+  }
+}
+
+// ---- adapter slab packing ---------------------------------------------------------------
+// lora_a [rank][h_in] -> A tiled; lora_b [h_out][rank] -> B tiled.  One thread per 16 bytes.
+__global__ void pack_adapter_kernel(const uint8_t* __restrict__ lora_a, const uint8_t* __restrict__ lora_b,
+                                    int rank, int h_in, int h_out, uint8_t* __restrict__ a_t,
+                                    uint8_t* __restrict__ b_t, int unpack) {
+  const int64_t na = (int64_t)rank * h_in / 8, nb = (int64_t)h_out * rank / 8;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < na + nb;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    if (u < na) {
+      const int k = (int)(u / (h_in / 8)), i = (int)(u % (h_in / 8)) * 8;
+      uint4* plain = reinterpret_cast<uint4*>(const_cast<uint8_t*>(lora_a) + ((int64_t)k * h_in + i) * 2);
+      uint4* tiled = reinterpret_cast<uint4*>(a_t + a_tiled_off(k, i, rank));
+      if (unpack) *plain = *tiled; else *tiled = *plain;
+    } else {
+      const int64_t w = u - na;
+      const int j = (int)(w / (rank / 8)), k = (int)(w % (rank / 8)) * 8;
+      uint4* plain = reinterpret_cast<uint4*>(const_cast<uint8_t*>(lora_b) + ((int64_t)j * rank + k) * 2);
+      uint4* tiled = reinterpret_cast<uint4*>(b_t + b_tiled_off(j, k, rank));
+      if (unpack) *plain = *tiled; else *tiled = *plain;
+    }
+  }
+}
+
+}  // namespace lsv

@@ -1,0 +1,87 @@
+"""ctypes binding of liblsv (include/lsv.h).
+
+Nonzero returns become the exception types the reference raises at the boundary this path
+replaces: ValueError for bad shapes / metadata / workspace (costmodel.py:95-103 raises
+ValueError for an empty batch, length mismatch or budget overflow) and RuntimeError for CUDA
+failures.  There is no fallback: if liblsv.so is missing the import of this module's
+functions raises, so a GPU run can never silently take a CPU or PyTorch path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_NAME = "liblsv.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+LSV_OK, LSV_EINVAL, LSV_ECUDA, LSV_EUNSUPPORTED, LSV_EWORKSPACE = 0, 1, 2, 3, 4
+LSV_DTYPE_BF16 = 0
+TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
+
+# every symbol include/lsv.h declares (tests/test_native_abi.py checks the library exports them)
+EXPORTED_SYMBOLS = (
+    "lsv_version", "lsv_last_error", "lsv_adapter_a_bytes", "lsv_adapter_b_bytes",
+    "lsv_pack_adapter", "lsv_unpack_adapter", "lsv_plan_size", "lsv_plan_build",
+    "lsv_plan_summary", "lsv_lora_apply", "lsv_lora_shrink", "lsv_lora_expand",
+    "lsv_enable_peer", "lsv_num_sms",
+)
+
+_lib = None
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_SIGNATURES = {
+    "lsv_version": (ctypes.c_int, []),
+    "lsv_last_error": (ctypes.c_char_p, []),
+    "lsv_num_sms": (ctypes.c_int, []),
+    "lsv_adapter_a_bytes": (_sz, [_i32, _i32]),
+    "lsv_adapter_b_bytes": (_sz, [_i32, _i32]),
+    "lsv_pack_adapter": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "lsv_unpack_adapter": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "lsv_plan_size": (ctypes.c_int, [_i32, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_sz),
+                                     ctypes.POINTER(_sz)]),
+    "lsv_plan_build": (ctypes.c_int, [_i32, _vp, _vp, _i32, _i32, _i32, _vp, _sz]),
+    "lsv_plan_summary": (ctypes.c_int, [_vp, _vp]),
+    "lsv_lora_apply": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                      _vp, _vp, _sz, _vp]),
+    "lsv_lora_shrink": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "lsv_lora_expand": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "lsv_enable_peer": (ctypes.c_int, [_i32, _i32]),
+}
+
+
+class LsvError(RuntimeError):
+    """CUDA-side failure inside liblsv."""
+
+
+def load():
+    """Load liblsv.so (built in-tree by paper_2511_22880_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback for the LoRA delta path)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.lsv_version() != 1:
+            raise RuntimeError(f"liblsv ABI version {lib.lsv_version()} != 1")
+        _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == LSV_OK:
+        return
+    msg = load().lsv_last_error().decode(errors="replace")
+    if rc in (LSV_EINVAL, LSV_EWORKSPACE):
+        raise ValueError(msg)
+    raise LsvError(msg)
+
+
+def lib():
+    return load()

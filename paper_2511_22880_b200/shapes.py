@@ -1,0 +1,73 @@
+"""Model projection shapes for the benchmark configurations (BASELINE.json ``configs``).
+
+Each projection a LoRA adapter attaches to is (name, h_in, h_out).  Llama-2 7B/13B use MHA
+(k/v out = hidden); Llama-3 70B uses GQA with 8 KV heads of 128 (k/v out = 1024).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Projection:
+    name: str
+    h_in: int
+    h_out: int
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    layers: int
+    projections: tuple[Projection, ...]
+
+    def shapes(self) -> list[tuple[int, int]]:
+        """Distinct (h_in, h_out) pairs, in first-use order (one plan each)."""
+        seen: list[tuple[int, int]] = []
+        for p in self.projections:
+            if (p.h_in, p.h_out) not in seen:
+                seen.append((p.h_in, p.h_out))
+        return seen
+
+    def rank_units_bytes(self) -> int:
+        """bf16 bytes of one rank unit of an adapter across every layer/projection."""
+        return self.layers * sum(2 * (p.h_in + p.h_out) for p in self.projections)
+
+
+def _llama(name: str, hidden: int, inter: int, layers: int, kv_out: int | None = None) -> ModelShape:
+    kv = hidden if kv_out is None else kv_out
+    return ModelShape(name, layers, (
+        Projection("q_proj", hidden, hidden),
+        Projection("k_proj", hidden, kv),
+        Projection("v_proj", hidden, kv),
+        Projection("o_proj", hidden, hidden),
+        Projection("gate_proj", hidden, inter),
+        Projection("up_proj", hidden, inter),
+        Projection("down_proj", inter, hidden),
+    ))
+
+
+LLAMA2_7B = _llama("llama-2-7b", 4096, 11008, 32)
+LLAMA2_13B = _llama("llama-2-13b", 5120, 13824, 40)
+LLAMA3_70B = _llama("llama-3-70b", 8192, 28672, 80, kv_out=1024)
+LLAMA7B_QPROJ = ModelShape("llama-7b-q_proj", 1, (Projection("q_proj", 4096, 4096),))
+
+MODELS = {m.name: m for m in (LLAMA2_7B, LLAMA2_13B, LLAMA3_70B, LLAMA7B_QPROJ)}
+
+
+def tp_shard(model: ModelShape, tp: int) -> ModelShape:
+    """Per-GPU projection shapes under S-LoRA-style tensor parallelism (column-parallel
+    q/k/v/gate/up shard h_out, row-parallel o/down shard h_in)."""
+    col = {"q_proj", "k_proj", "v_proj", "gate_proj", "up_proj"}
+    projs = []
+    for p in model.projections:
+        if p.name in col:
+            if p.h_out % (tp * 128):
+                raise ValueError(f"{p.name}: h_out {p.h_out} not divisible into {tp} shards of 128")
+            projs.append(Projection(p.name, p.h_in, p.h_out // tp))
+        else:
+            if p.h_in % (tp * 128):
+                raise ValueError(f"{p.name}: h_in {p.h_in} not divisible into {tp} shards of 128")
+            projs.append(Projection(p.name, p.h_in // tp, p.h_out))
+    return ModelShape(f"{model.name}-tp{tp}", model.layers, tuple(projs))

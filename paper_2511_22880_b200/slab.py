@@ -1,0 +1,161 @@
+"""HBM adapter slab: the B200 form of the reference's per-server GPU adapter slots.
+
+Reference: ``AdapterPool`` keeps, per server, an LRU set of GPU-resident adapters
+(pool.py:88-99 ``touch_gpu``/``is_gpu_resident``, capacity ``gpu_slots`` config.py:29,
+pool.py:20) and prices making one resident (``plan_fetch`` pool.py:101-132,
+``fetch_latency`` costmodel.py:129-143).  Here a resident adapter is real memory: for every
+layer and projection of the model, its lora_A/lora_B packed once into the tiled layouts the
+kernels move with single bulk copies (include/lsv.h ``lsv_pack_adapter``).  Slots are
+allocated from one large device buffer sized for B200's 180 GB of HBM; a segment's A/B
+pointers are ``base + offset`` — or an NVLink peer address when the adapter lives in another
+GPU's slab (the reference's ``fetch_remote``).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import native
+from .shapes import ModelShape
+
+
+@dataclass
+class SlotInfo:
+    slot: int
+    adapter_id: str
+    rank: int
+    offset: int        # byte offset of the slot inside the slab buffer
+    nbytes: int
+
+
+class AdapterSlab:
+    """Adapters of one model resident in one GPU's HBM."""
+
+    ALIGN = 1024
+
+    def __init__(self, model: ModelShape, capacity_bytes: int, device: torch.device | str):
+        self.model = model
+        self.device = torch.device(device)
+        self.capacity = int(capacity_bytes)
+        self.buffer = torch.empty(self.capacity, dtype=torch.uint8, device=self.device)
+        self.base = self.buffer.data_ptr()
+        self.slots: list[SlotInfo] = []
+        self.by_id: dict[str, int] = {}
+        self._cursor = 0
+        P = len(model.projections)
+        # per (layer, projection): byte offset of A and B inside a slot of rank 1 scaled by rank
+        a_unit = np.zeros((model.layers, P), dtype=np.int64)
+        b_unit = np.zeros((model.layers, P), dtype=np.int64)
+        off = 0
+        for l in range(model.layers):
+            for p, proj in enumerate(model.projections):
+                a_unit[l, p] = off
+                off += 2 * proj.h_in
+                b_unit[l, p] = off
+                off += 2 * proj.h_out
+        self._a_unit, self._b_unit, self._unit_bytes = a_unit, b_unit, off
+        self._a_off_rows: list[np.ndarray] = []
+        self._b_off_rows: list[np.ndarray] = []
+        self._slot_offsets_dev: tuple[torch.Tensor, torch.Tensor] | None = None
+
+    # -- allocation --------------------------------------------------------------------
+    def slot_bytes(self, rank: int) -> int:
+        return rank * self._unit_bytes
+
+    def free_bytes(self) -> int:
+        return self.capacity - self._cursor
+
+    def allocate(self, adapter_id: str, rank: int) -> int:
+        if adapter_id in self.by_id:
+            raise ValueError(f"adapter {adapter_id!r} already resident")
+        if rank < 8 or rank % 8 or rank > 256:
+            raise ValueError(f"adapter {adapter_id!r}: rank must be a multiple of 8 in [8, 256], got {rank}")
+        nbytes = self.slot_bytes(rank)
+        start = (self._cursor + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        if start + nbytes > self.capacity:
+            raise MemoryError(f"slab full: adapter {adapter_id!r} needs {nbytes} bytes, "
+                              f"{self.capacity - start} free")
+        slot = len(self.slots)
+        self.slots.append(SlotInfo(slot, adapter_id, rank, start, nbytes))
+        self.by_id[adapter_id] = slot
+        self._a_off_rows.append(start + rank * self._a_unit)
+        self._b_off_rows.append(start + rank * self._b_unit)
+        self._cursor = start + nbytes
+        self._slot_offsets_dev = None
+        return slot
+
+    def a_offset(self, slot: int, layer: int, proj: int) -> int:
+        return int(self._a_off_rows[slot][layer, proj])
+
+    def b_offset(self, slot: int, layer: int, proj: int) -> int:
+        return int(self._b_off_rows[slot][layer, proj])
+
+    # -- weights -----------------------------------------------------------------------
+    def load(self, slot: int, layer: int, proj: int, lora_a: torch.Tensor, lora_b: torch.Tensor,
+             stream: torch.cuda.Stream | None = None) -> None:
+        """Pack PEFT-layout lora_A [r, h_in] / lora_B [h_out, r] (bf16, on this device)."""
+        info = self.slots[slot]
+        pr = self.model.projections[proj]
+        r = info.rank
+        if tuple(lora_a.shape) != (r, pr.h_in) or tuple(lora_b.shape) != (pr.h_out, r):
+            raise ValueError(f"expected lora_A {(r, pr.h_in)} and lora_B {(pr.h_out, r)}, got "
+                             f"{tuple(lora_a.shape)} and {tuple(lora_b.shape)}")
+        if lora_a.dtype != torch.bfloat16 or lora_b.dtype != torch.bfloat16:
+            raise ValueError("lora weights must be bfloat16")
+        lora_a = lora_a.contiguous()
+        lora_b = lora_b.contiguous()
+        st = stream or torch.cuda.current_stream(self.device)
+        native.check(native.lib().lsv_pack_adapter(
+            lora_a.data_ptr(), lora_b.data_ptr(), r, pr.h_in, pr.h_out,
+            self.base + self.a_offset(slot, layer, proj), self.base + self.b_offset(slot, layer, proj),
+            st.cuda_stream))
+
+    def read(self, slot: int, layer: int, proj: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """Unpack a resident adapter back to PEFT layout (tests, migration checks)."""
+        info = self.slots[slot]
+        pr = self.model.projections[proj]
+        a = torch.empty((info.rank, pr.h_in), dtype=torch.bfloat16, device=self.device)
+        b = torch.empty((pr.h_out, info.rank), dtype=torch.bfloat16, device=self.device)
+        native.check(native.lib().lsv_unpack_adapter(
+            self.base + self.a_offset(slot, layer, proj), self.base + self.b_offset(slot, layer, proj),
+            info.rank, pr.h_in, pr.h_out, a.data_ptr(), b.data_ptr(),
+            torch.cuda.current_stream(self.device).cuda_stream))
+        return a, b
+
+    def fill_random(self, slot: int, seed: int, layers: range | None = None) -> None:
+        """Random-init adapter weights on the device: A ~ N(0, 1/h_in), B ~ N(0, 1/r)
+        (B non-zero so the delta is not trivially 0).  Deterministic per seed."""
+        info = self.slots[slot]
+        gen = torch.Generator(device=self.device)
+        gen.manual_seed(seed)
+        for layer in (layers if layers is not None else range(self.model.layers)):
+            for p, pr in enumerate(self.model.projections):
+                a = (torch.randn((info.rank, pr.h_in), generator=gen, device=self.device)
+                     * (1.0 / math.sqrt(pr.h_in))).to(torch.bfloat16)
+                b = (torch.randn((pr.h_out, info.rank), generator=gen, device=self.device)
+                     * (1.0 / math.sqrt(info.rank))).to(torch.bfloat16)
+                self.load(slot, layer, p, a, b)
+
+    # -- pointer tables ----------------------------------------------------------------
+    def pointer_tables(self, seg_slots: np.ndarray, peer_slabs: dict[int, "AdapterSlab"] | None = None,
+                       seg_owner: np.ndarray | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """Device int64 tables [layers*projections, S] of A and B pointers for the segments.
+
+        ``seg_owner[s]`` (optional) names the GPU whose slab holds segment s; entries other than
+        this slab's device resolve through ``peer_slabs`` to NVLink peer addresses."""
+        L, P = self.model.layers, len(self.model.projections)
+        S = len(seg_slots)
+        a = np.empty((L * P, S), dtype=np.int64)
+        b = np.empty((L * P, S), dtype=np.int64)
+        for s, slot in enumerate(np.asarray(seg_slots)):
+            slab = self
+            if seg_owner is not None and peer_slabs is not None and int(seg_owner[s]) in peer_slabs:
+                slab = peer_slabs[int(seg_owner[s])]
+            a[:, s] = (slab.base + slab._a_off_rows[int(slot)]).reshape(-1)
+            b[:, s] = (slab.base + slab._b_off_rows[int(slot)]).reshape(-1)
+        return (torch.from_numpy(a).to(self.device, non_blocking=False),
+                torch.from_numpy(b).to(self.device, non_blocking=False))

@@ -1,0 +1,118 @@
+"""liblsv C ABI on the CPU: the library loads, exports every symbol include/lsv.h declares, and
+the host planner (no GPU needed) validates input and emits consistent work lists."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2511_22880_b200 import native
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_header_symbols():
+    lib = native.load()
+    header = (ROOT / "include" / "lsv.h").read_text()
+    declared = set(re.findall(r"\b(lsv_[a-z0-9_]+)\s*\(", header))
+    assert declared == set(native.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.lsv_version() == 1
+
+
+def _plan(indptr, ranks, h_in=4096, h_out=4096, policy=0):
+    lib = native.load()
+    indptr = np.asarray(indptr, dtype=np.int32)
+    ranks = np.asarray(ranks, dtype=np.int32)
+    pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
+    native.check(lib.lsv_plan_size(len(ranks), indptr.ctypes.data, ranks.ctypes.data, h_in, h_out, policy,
+                                   ctypes.byref(pb), ctypes.byref(wb)))
+    blob = np.zeros(pb.value // 4, dtype=np.int32)
+    native.check(lib.lsv_plan_build(len(ranks), indptr.ctypes.data, ranks.ctypes.data, h_in, h_out, policy,
+                                    blob.ctypes.data, pb.value))
+    return blob, wb.value
+
+
+def _decode(blob):
+    h = blob[:64]
+    names = ["magic", "version", "S", "N", "h_in", "h_out", "n_simt", "n_mtiles", "n_shrink", "n_expand",
+             "shrink_grid", "expand_grid", "off_indptr", "off_rank", "off_tier", "off_simt", "off_mtiles",
+             "off_shrink", "off_expand", "total_ints"]
+    d = {k: int(h[i]) for i, k in enumerate(names)}
+    d["mtiles"] = blob[d["off_mtiles"]:d["off_mtiles"] + 8 * d["n_mtiles"]].reshape(-1, 8)
+    d["shrink"] = blob[d["off_shrink"]:d["off_shrink"] + 4 * d["n_shrink"]].reshape(-1, 4)
+    d["expand"] = blob[d["off_expand"]:d["off_expand"] + 2 * d["n_expand"]].reshape(-1, 2)
+    d["simt"] = blob[d["off_simt"]:d["off_simt"] + 4 * d["n_simt"]].reshape(-1, 4)
+    d["tier"] = blob[d["off_tier"]:d["off_tier"] + d["S"]]
+    return d
+
+
+@pytest.mark.parametrize("h_in,h_out", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_plan_covers_every_chunk_and_tile(h_in, h_out):
+    rng = np.random.default_rng(0)
+    ranks = [8] * 44 + [16] * 22 + [32] * 14 + [64] * 11 + [128] * 9
+    lens = np.bincount(rng.integers(0, 100, 4096), minlength=100)
+    lens[3] = 0
+    lens[5] = 2    # SIMT-tier segment
+    lens[7] = 300  # three tensor-core tiles
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    blob, ws = _plan(indptr, ranks, h_in, h_out)
+    d = _decode(blob)
+    assert d["magic"] == 0x5056534C and d["N"] == int(indptr[-1])
+    chunks = h_in // 64
+    # every mtile's k-range is covered exactly once by its splits
+    cover = {}
+    for mt, cb, ce, sk in d["shrink"]:
+        cover.setdefault(int(mt), []).append((int(cb), int(ce), int(sk) & 0xFFFF))
+    for i, mt in enumerate(d["mtiles"]):
+        parts = sorted(cover[i])
+        assert parts[0][0] == 0 and parts[-1][1] == chunks
+        assert all(parts[j][1] == parts[j + 1][0] for j in range(len(parts) - 1))
+        assert sorted(p[2] for p in parts) == list(range(int(mt[4])))   # split ids 0..nsplit-1
+    # every (mtile, h_out tile) appears exactly once in the expand list
+    pairs = {(int(a), int(b)) for a, b in d["expand"]}
+    assert len(pairs) == len(d["expand"]) == d["n_mtiles"] * (h_out // 128)
+    # tokens: mtiles + simt items tile every non-empty segment exactly
+    covered = np.zeros(d["N"], dtype=int)
+    for seg, tb, nt, *_ in d["mtiles"]:
+        covered[tb:tb + nt] += 1
+    for seg, tb, nt, _ in d["simt"]:
+        covered[tb:tb + nt] += 1
+    assert np.all(covered == 1)
+    assert d["tier"][3] == 0 and d["tier"][5] == 1 and d["tier"][7] == 2
+    # LPT: shrink items sorted by non-increasing cost
+    row = {i: (int(-(-mt[2] // 8) * 8) + int(mt[3])) * 128 for i, mt in enumerate(d["mtiles"])}
+    costs = [row[int(m)] * (int(e) - int(b)) for m, b, e, _ in d["shrink"]]
+    assert costs == sorted(costs, reverse=True)
+    assert ws > 0
+
+
+def test_plan_rejects_bad_input():
+    with pytest.raises(ValueError, match="multiple of 128"):
+        _plan([0, 4], [8], h_in=1000)
+    with pytest.raises(ValueError, match="rank"):
+        _plan([0, 4], [12])
+    with pytest.raises(ValueError, match="non-decreasing"):
+        _plan([0, 4, 2], [8, 8])
+    with pytest.raises(ValueError, match="seg_indptr\\[0\\]"):
+        _plan([1, 4], [8])
+
+
+def test_forced_policies():
+    d = _decode(_plan([0, 64, 128], [8, 128], policy=native.TIER_SIMT)[0])
+    assert d["n_mtiles"] == 0 and d["n_simt"] == 16
+    d = _decode(_plan([0, 2, 130], [8, 256], policy=native.TIER_TC)[0])
+    assert d["n_mtiles"] == 1 and list(d["tier"]) == [2, 1]   # rank 256 stays on SIMT
+
+
+def test_apply_rejects_missing_plan():
+    lib = native.load()
+    rc = lib.lsv_lora_apply(None, 0, None, 0, 0, 0, 4096, 4096, None, None, None, None, None, 0, None)
+    with pytest.raises(ValueError):
+        native.check(rc)
+    rc = lib.lsv_lora_apply(None, 0, None, 0, 7, 0, 4096, 4096, None, None, None, None, None, 0, None)
+    with pytest.raises(RuntimeError):
+        native.check(rc)
