@@ -6,9 +6,12 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <queue>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/lsv.h"
@@ -22,6 +25,9 @@ using namespace lsv;
 namespace {
 
 thread_local char g_err[512] = "";
+uint64_t* g_trace = nullptr;  // debug timeline buffer (lsv_debug_set_trace)
+int g_trace_items = 0;
+int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -66,9 +72,37 @@ struct PlanBuilder {
   std::vector<int32_t> indptr, rank, tier;
   std::vector<SimtItem> simt;
   std::vector<MTile> mtiles;
-  std::vector<ShrinkItem> shrink;
-  std::vector<ExpandItem> expand;
+  std::vector<ShrinkRec> shrink;     // grouped per CTA
+  std::vector<int32_t> shrink_cta;   // [grid+1]
+  std::vector<ExpandRec> expand;
+  std::vector<int32_t> expand_cta;
 };
+
+// LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
+// CTA's list keeps that order.  Returns records regrouped per CTA and the [grid+1] offsets.
+template <typename Rec>
+void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, std::vector<Rec>& out,
+                std::vector<int32_t>& cta_off) {
+  std::vector<int64_t> load(grid, 0);
+  std::vector<std::vector<Rec>> per(grid);
+  using Slot = std::pair<int64_t, int>;
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  for (int c = 0; c < grid; ++c) heap.push({0, c});
+  for (const auto& cr : costed) {
+    Slot sl = heap.top();
+    heap.pop();
+    per[sl.second].push_back(cr.second);
+    sl.first += cr.first;
+    heap.push(sl);
+  }
+  out.clear();
+  cta_off.assign(grid + 1, 0);
+  for (int c = 0; c < grid; ++c) {
+    cta_off[c] = (int32_t)out.size();
+    out.insert(out.end(), per[c].begin(), per[c].end());
+  }
+  cta_off[grid] = (int32_t)out.size();
+}
 
 int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t h_out) {
   if (S < 0) return fail(LSV_EINVAL, "num_segments must be >= 0, got %d", S);
@@ -134,8 +168,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int64_t target = std::max<int64_t>(kMinItemBytes, total / std::max(1, 2 * nsm));
   int64_t part_off = 0, vimg_off = 0;
   int counter = 0;
-  struct Costed { int64_t cost; int key; };
-  std::vector<std::pair<int64_t, ShrinkItem>> shrink_costed;
+  std::vector<std::pair<int64_t, ShrinkRec>> shrink_costed;
   for (size_t i = 0; i < pb.mtiles.size(); ++i) {
     MTile& mt = pb.mtiles[i];
     const int stages = (chunks + kch[i] - 1) / kch[i];
@@ -151,27 +184,39 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     vimg_off += (int64_t)round_up(mt.ntok, 16) * kp16 * 2;
     mt.counter = counter++;
     for (int sp = 0; sp < nsplit; ++sp) {
-      ShrinkItem it{};
-      it.mtile = (int32_t)i;
-      it.chunk_begin = (int32_t)(sp * sps * kch[i]);
-      it.chunk_end = (int32_t)std::min<int64_t>(chunks, (int64_t)(sp + 1) * sps * kch[i]);
-      it.split_kch = sp | (int32_t)(kch[i] << 16);
-      shrink_costed.push_back({row_bytes[i] * (it.chunk_end - it.chunk_begin), it});
+      ShrinkRec r{};
+      r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
+      r.chunk_begin = (int32_t)(sp * sps * kch[i]);
+      r.chunk_end = (int32_t)std::min<int64_t>(chunks, (int64_t)(sp + 1) * sps * kch[i]);
+      r.kch = (int32_t)kch[i]; r.split = sp;
+      r.nsplit = nsplit; r.part_off = mt.part_off; r.vimg_off = mt.vimg_off; r.counter = mt.counter;
+      r.mtile = (int32_t)i;
+      // bytes moved + a fixed per-item cost (pipeline fill, epilogue, split reduction)
+      const int64_t cost = row_bytes[i] * (r.chunk_end - r.chunk_begin) + 24 * 1024 +
+                           (nsplit > 1 ? (int64_t)mt.ntok * mt.rank * 8 : 0);
+      shrink_costed.push_back({cost, r});
     }
   }
   std::stable_sort(shrink_costed.begin(), shrink_costed.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (auto& c : shrink_costed) pb.shrink.push_back(c.second);
 
-  std::vector<std::pair<int64_t, ExpandItem>> expand_costed;
+  std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
   for (size_t i = 0; i < pb.mtiles.size(); ++i) {
     const MTile& mt = pb.mtiles[i];
-    const int64_t cost = 128LL * mt.rank * 2 + (int64_t)mt.ntok * 128 * 4;
-    for (int jt = 0; jt < h_out / kExpandW; ++jt) expand_costed.push_back({cost, ExpandItem{(int32_t)i, jt}});
+    const int64_t cost = 128LL * mt.rank * 2 + (int64_t)mt.ntok * 128 * 4 + 8 * 1024;
+    for (int jt = 0; jt < h_out / kExpandW; ++jt) {
+      ExpandRec r{};
+      r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
+      r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i;
+      expand_costed.push_back({cost, r});
+    }
   }
   std::stable_sort(expand_costed.begin(), expand_costed.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (auto& c : expand_costed) pb.expand.push_back(c.second);
+  const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
+  const int expand_grid = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
+  lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta);
+  lpt_assign(expand_costed, std::max(expand_grid, 1), pb.expand, pb.expand_cta);
 
   // header + workspace layout
   PlanHeader& h = pb.h;
@@ -181,8 +226,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.n_mtiles = (int32_t)pb.mtiles.size();
   h.n_shrink_items = (int32_t)pb.shrink.size();
   h.n_expand_items = (int32_t)pb.expand.size();
-  h.shrink_grid = std::min(h.n_shrink_items, nsm);
-  h.expand_grid = std::min(h.n_expand_items, nsm);
+  h.shrink_grid = shrink_grid;
+  h.expand_grid = expand_grid;
   int32_t off = sizeof(PlanHeader) / 4;
   h.off_seg_indptr = off; off += S + 1;
   h.off_seg_rank = off; off += S;
@@ -190,8 +235,11 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   off = round_up(off, 4);
   h.off_simt_items = off; off += 4 * h.n_simt_items;
   h.off_mtiles = off; off += 8 * h.n_mtiles;
-  h.off_shrink_items = off; off += 4 * h.n_shrink_items;
-  h.off_expand_items = off; off += 2 * h.n_expand_items;
+  h.off_shrink_recs = off; off += 16 * h.n_shrink_items;
+  h.off_shrink_cta = off; off += (int32_t)pb.shrink_cta.size();
+  off = round_up(off, 4);
+  h.off_expand_recs = off; off += 8 * h.n_expand_items;
+  h.off_expand_cta = off; off += (int32_t)pb.expand_cta.size();
   h.total_ints = off;
   int64_t ws = 0;
   h.ws_counters = 0; ws += round_up(std::max(1, counter) * 4, 256);
@@ -232,19 +280,58 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-int make_x_maps(CUtensorMap* maps, const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in) {
+// Tensor maps are pure functions of (pointer, row stride, rows, cols); encoding costs ~1 µs of
+// host time, so they are cached (a model step reuses the same activation buffers every layer).
+struct MapKey {
+  uintptr_t ptr; int64_t ld; int32_t rows, cols, kind;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && ld == o.ld && rows == o.rows && cols == o.cols && kind == o.kind;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<uintptr_t>()(k.ptr);
+    h ^= std::hash<int64_t>()(k.ld * 1315423911LL + k.rows) + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()((int64_t)k.cols * 31 + k.kind) + (h << 6) + (h >> 2);
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, std::vector<CUtensorMap>, MapKeyHash> g_map_cache;
+
+// kind 0: x maps (5 boxes of 64 cols x 8<<b rows, SWIZZLE_128B)
+// kind 1: y maps (8 boxes of 128 cols x 1<<b rows, no swizzle)
+int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t rows, int32_t cols) {
+  const MapKey key{reinterpret_cast<uintptr_t>(ptr), ld, rows, cols, kind};
+  const int nmaps = kind == 0 ? 5 : 8;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_map_cache.find(key);
+    if (it != g_map_cache.end()) {
+      std::memcpy(out, it->second.data(), sizeof(CUtensorMap) * nmaps);
+      return LSV_OK;
+    }
+  }
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  for (int b = 0; b < 5; ++b) {
-    const cuuint64_t dims[2] = {(cuuint64_t)h_in, (cuuint64_t)num_tokens};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)kChunk, (cuuint32_t)(8 << b)};
+  std::vector<CUtensorMap> maps(nmaps);
+  for (int b = 0; b < nmaps; ++b) {
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)kChunk : (cuuint32_t)kExpandW,
+                               kind == 0 ? (cuuint32_t)(8 << b) : (cuuint32_t)(1 << b)};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) for box rows %d", (int)r, 8 << b);
+    CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) kind %d box %d", (int)r, kind, b);
   }
+  std::memcpy(out, maps.data(), sizeof(CUtensorMap) * nmaps);
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_map_cache.size() > 8192) g_map_cache.clear();
+  g_map_cache.emplace(key, std::move(maps));
   return LSV_OK;
 }
 
@@ -260,6 +347,23 @@ int ensure_smem_attrs() {
     if (rc) fail(LSV_ECUDA, "cudaFuncSetAttribute(smem) failed: %s / %s", cudaGetErrorString(e1), cudaGetErrorString(e2));
   });
   return rc;
+}
+
+// Programmatic dependent launch: the kernel may start while the previous kernel in the stream
+// drains; it calls griddepcontrol.wait before touching anything that kernel wrote.
+template <typename Params>
+cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t st, const Params& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
 int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_dev, const void* ws) {
@@ -282,17 +386,17 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
   if (h->n_shrink_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
     ShrinkParams p{};
-    if (int rc = make_x_maps(p.xmap, x, ldx, num_tokens, h->h_in)) return rc;
+    if (int rc = get_maps(p.xmap, 0, x, ldx, num_tokens, h->h_in)) return rc;
     p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
-    p.n_items = h->n_shrink_items; p.off_items = h->off_shrink_items; p.off_mtiles = h->off_mtiles;
+    p.off_recs = h->off_shrink_recs; p.off_cta = h->off_shrink_cta;
     p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg; p.ws_counters = h->ws_counters;
-    shrink_tc_kernel<<<h->shrink_grid, kTcThreads, shrink_smem_bytes(), st>>>(p);
-    LSV_CUDA_CHECK(cudaGetLastError());
+    p.trace = g_trace; p.trace_items = g_trace_items;
+    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p));
   }
   return LSV_OK;
 }
 
-int run_expand(const PlanHeader* h, void* y, int64_t ldy, const void* const* b_ptrs, const int32_t* plan, uint8_t* ws,
+int run_expand(const PlanHeader* h, void* y, int64_t ldy, int32_t num_tokens, const void* const* b_ptrs, const int32_t* plan, uint8_t* ws,
                cudaStream_t st) {
   if (h->n_simt_items > 0) {
     simt_expand_kernel<<<dim3(h->n_simt_items, h->h_out / 128), 64, 0, st>>>(
@@ -303,10 +407,13 @@ int run_expand(const PlanHeader* h, void* y, int64_t ldy, const void* const* b_p
   if (h->n_expand_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
     ExpandParams p{};
+    if (int rc = get_maps(p.ymap, 1, y, ldy, num_tokens, h->h_out)) return rc;
     p.plan = plan; p.b_ptrs = b_ptrs; p.ws = ws; p.y = static_cast<__nv_bfloat16*>(y); p.ldy = ldy;
-    p.n_items = h->n_expand_items; p.off_items = h->off_expand_items; p.off_mtiles = h->off_mtiles;
+    p.off_recs = h->off_expand_recs; p.off_cta = h->off_expand_cta;
     p.ws_vimg = h->ws_vimg;
-    expand_tc_kernel<<<h->expand_grid, kTcThreads, expand_smem_bytes(), st>>>(p);
+    p.dbg = g_debug_expand;
+    p.trace = g_trace; p.trace_items = g_trace_items;
+    LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, h->expand_grid, expand_smem_bytes(), st, p));
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   return LSV_OK;
@@ -382,8 +489,10 @@ int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_
   std::copy(pb.tier.begin(), pb.tier.end(), out + h.off_seg_tier);
   std::memcpy(out + h.off_simt_items, pb.simt.data(), pb.simt.size() * sizeof(SimtItem));
   std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
-  std::memcpy(out + h.off_shrink_items, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkItem));
-  std::memcpy(out + h.off_expand_items, pb.expand.data(), pb.expand.size() * sizeof(ExpandItem));
+  std::memcpy(out + h.off_shrink_recs, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkRec));
+  std::copy(pb.shrink_cta.begin(), pb.shrink_cta.end(), out + h.off_shrink_cta);
+  std::memcpy(out + h.off_expand_recs, pb.expand.data(), pb.expand.size() * sizeof(ExpandRec));
+  std::copy(pb.expand_cta.begin(), pb.expand_cta.end(), out + h.off_expand_cta);
   return LSV_OK;
 }
 
@@ -422,7 +531,7 @@ int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, con
   if (h->num_tokens == 0) return LSV_OK;
   if (!y || !b_ptrs) return fail(LSV_EINVAL, "y / b_ptrs must be non-null");
   if (!aligned16(y) || ldy % 8 || ldy < h_out) return fail(LSV_EINVAL, "y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out");
-  return run_expand(h, y, ldy, b_ptrs, static_cast<const int32_t*>(plan_dev), static_cast<uint8_t*>(workspace),
+  return run_expand(h, y, ldy, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev), static_cast<uint8_t*>(workspace),
                     static_cast<cudaStream_t>(stream));
 }
 
@@ -434,6 +543,14 @@ int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dty
                                stream))
     return rc;
   return lsv_lora_expand(y, ldy, num_tokens, h_out, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes, stream);
+}
+
+// Debug only (not part of include/lsv.h): route per-item globaltimer stamps of the tcgen05
+// kernels into `buf` ([148][items][8] uint64); nullptr turns tracing off.
+int lsv_debug_set_trace(void* buf, int32_t items_per_cta) {
+  g_trace = static_cast<uint64_t*>(buf);
+  g_trace_items = buf ? items_per_cta : 0;
+  return LSV_OK;
 }
 
 int lsv_enable_peer(int32_t dev, int32_t peer) {

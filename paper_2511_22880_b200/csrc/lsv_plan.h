@@ -24,13 +24,15 @@ struct PlanHeader {            // 64 int32
   int32_t shrink_grid, expand_grid;
   // int32 offsets of the arrays inside the blob
   int32_t off_seg_indptr, off_seg_rank, off_seg_tier;
-  int32_t off_simt_items, off_mtiles, off_shrink_items, off_expand_items;
+  int32_t off_simt_items, off_mtiles;
+  int32_t off_shrink_recs, off_shrink_cta;   // records grouped per CTA + [grid+1] CTA offsets
+  int32_t off_expand_recs, off_expand_cta;
   int32_t total_ints;
   // workspace layout, byte offsets (workspace < 2 GiB)
   int32_t ws_counters, ws_partials, ws_vimg, ws_simt_v, ws_bytes;
   int32_t n_counters;
   int32_t simt_segments;
-  int32_t reserved[64 - 27];
+  int32_t reserved[64 - 29];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -46,20 +48,27 @@ struct MTile {                 // 8 int32
   int32_t counter;             // index of this tile's split-arrival counter
 };
 
-struct ShrinkItem {            // 4 int32
-  int32_t mtile, chunk_begin, chunk_end;  // k-range in 64-element chunks of h_in
-  int32_t split_kch;           // split index (low 16 bits) | chunks per pipeline stage << 16
+// Fully decoded work records: the host assigns them to CTAs (LPT greedy on estimated bytes)
+// and stores each CTA's list contiguously, so the kernels need no atomics and no dependent
+// descriptor loads on their critical path.
+struct ShrinkRec {             // 16 int32
+  int32_t seg, tok_begin, ntok, rank;
+  int32_t chunk_begin, chunk_end, kch, split;   // k-range in 64-element chunks of h_in
+  int32_t nsplit, part_off, vimg_off, counter;
+  int32_t mtile, pad[3];
 };
 
-struct ExpandItem {            // 2 int32
-  int32_t mtile, jtile;        // h_out columns [jtile*128, jtile*128+128)
+struct ExpandRec {             // 8 int32
+  int32_t seg, tok_begin, ntok, rank;
+  int32_t jtile, vimg_off, mtile, pad;          // h_out columns [jtile*128, jtile*128+128)
 };
 
 // Pipeline geometry (bytes of shared memory).
 constexpr int kShrinkSlotBytes = 48 * 1024;
 constexpr int kShrinkSlots = 4;
 constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past short token tiles
-constexpr int kExpandSlotBytes = 64 * 1024;
-constexpr int kExpandSlots = 3;
+constexpr int kExpandRingBytes = 200 * 1024;   // variable-size items, allocated in issue order
+constexpr int kExpandGuardBytes = 2 * 1024;    // rank-8 K=16 MMA reads one k-core past its tile
+constexpr int kExpandInflight = 8;
 
 }  // namespace lsv

@@ -40,11 +40,13 @@ def _decode(blob):
     h = blob[:64]
     names = ["magic", "version", "S", "N", "h_in", "h_out", "n_simt", "n_mtiles", "n_shrink", "n_expand",
              "shrink_grid", "expand_grid", "off_indptr", "off_rank", "off_tier", "off_simt", "off_mtiles",
-             "off_shrink", "off_expand", "total_ints"]
+             "off_shrink", "off_shrink_cta", "off_expand", "off_expand_cta", "total_ints"]
     d = {k: int(h[i]) for i, k in enumerate(names)}
     d["mtiles"] = blob[d["off_mtiles"]:d["off_mtiles"] + 8 * d["n_mtiles"]].reshape(-1, 8)
-    d["shrink"] = blob[d["off_shrink"]:d["off_shrink"] + 4 * d["n_shrink"]].reshape(-1, 4)
-    d["expand"] = blob[d["off_expand"]:d["off_expand"] + 2 * d["n_expand"]].reshape(-1, 2)
+    d["shrink"] = blob[d["off_shrink"]:d["off_shrink"] + 16 * d["n_shrink"]].reshape(-1, 16)
+    d["shrink_cta"] = blob[d["off_shrink_cta"]:d["off_shrink_cta"] + d["shrink_grid"] + 1]
+    d["expand"] = blob[d["off_expand"]:d["off_expand"] + 8 * d["n_expand"]].reshape(-1, 8)
+    d["expand_cta"] = blob[d["off_expand_cta"]:d["off_expand_cta"] + d["expand_grid"] + 1]
     d["simt"] = blob[d["off_simt"]:d["off_simt"] + 4 * d["n_simt"]].reshape(-1, 4)
     d["tier"] = blob[d["off_tier"]:d["off_tier"] + d["S"]]
     return d
@@ -63,18 +65,24 @@ def test_plan_covers_every_chunk_and_tile(h_in, h_out):
     d = _decode(blob)
     assert d["magic"] == 0x5056534C and d["N"] == int(indptr[-1])
     chunks = h_in // 64
-    # every mtile's k-range is covered exactly once by its splits
+    # every mtile's k-range is covered exactly once by its splits (records: ShrinkRec, 16 int32)
     cover = {}
-    for mt, cb, ce, sk in d["shrink"]:
-        cover.setdefault(int(mt), []).append((int(cb), int(ce), int(sk) & 0xFFFF))
+    for rec in d["shrink"]:
+        cover.setdefault(int(rec[12]), []).append((int(rec[4]), int(rec[5]), int(rec[7])))
     for i, mt in enumerate(d["mtiles"]):
         parts = sorted(cover[i])
         assert parts[0][0] == 0 and parts[-1][1] == chunks
         assert all(parts[j][1] == parts[j + 1][0] for j in range(len(parts) - 1))
         assert sorted(p[2] for p in parts) == list(range(int(mt[4])))   # split ids 0..nsplit-1
-    # every (mtile, h_out tile) appears exactly once in the expand list
-    pairs = {(int(a), int(b)) for a, b in d["expand"]}
+    # every (mtile, h_out tile) appears exactly once in the expand records
+    pairs = {(int(r[6]), int(r[4])) for r in d["expand"]}
     assert len(pairs) == len(d["expand"]) == d["n_mtiles"] * (h_out // 128)
+    # per-CTA record lists partition the record arrays
+    for key in ("shrink_cta", "expand_cta"):
+        off = d[key]
+        assert off[0] == 0 and np.all(np.diff(off) >= 0)
+    assert d["shrink_cta"][-1] == d["n_shrink"] and d["expand_cta"][-1] == d["n_expand"]
+    assert d["shrink_grid"] <= 148 and d["expand_grid"] <= 148
     # tokens: mtiles + simt items tile every non-empty segment exactly
     covered = np.zeros(d["N"], dtype=int)
     for seg, tb, nt, *_ in d["mtiles"]:
@@ -83,10 +91,10 @@ def test_plan_covers_every_chunk_and_tile(h_in, h_out):
         covered[tb:tb + nt] += 1
     assert np.all(covered == 1)
     assert d["tier"][3] == 0 and d["tier"][5] == 1 and d["tier"][7] == 2
-    # LPT: shrink items sorted by non-increasing cost
-    row = {i: (int(-(-mt[2] // 8) * 8) + int(mt[3])) * 128 for i, mt in enumerate(d["mtiles"])}
-    costs = [row[int(m)] * (int(e) - int(b)) for m, b, e, _ in d["shrink"]]
-    assert costs == sorted(costs, reverse=True)
+    # LPT balance: the most-loaded CTA carries at most ~2x the mean estimated bytes
+    row = np.array([(int(-(-r[2] // 8) * 8) + int(r[3])) * 128 * (int(r[5]) - int(r[4])) for r in d["shrink"]])
+    per_cta = np.add.reduceat(row, d["shrink_cta"][:-1]) if len(row) else row
+    assert per_cta.max() <= 2.0 * per_cta.mean() + 1.5 * row.max()
     assert ws > 0
 
 

@@ -1,0 +1,27 @@
+"""Minimal C2 one-layer workload for ncu captures: q_proj apply x3 (the last two are profiled)."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+from paper_2511_22880_b200.slab import AdapterSlab
+from paper_2511_22880_b200.lora import LoraDeltaEngine
+from paper_2511_22880_b200.segments import index_tokens
+
+proj = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections)
+dev = torch.device("cuda:0")
+ranks = [8]*44+[16]*22+[32]*14+[64]*11+[128]*9
+slab = AdapterSlab(model, sum(r*model.rank_units_bytes() for r in ranks) + (1 << 24), dev)
+for i, r in enumerate(ranks):
+    s = slab.allocate(f"a{i}", r); slab.fill_random(s, 1000+i)
+seg = index_tokens(np.random.default_rng(0).integers(0, 100, 4096), ranks)
+eng = LoraDeltaEngine(slab)
+bp = eng.prepare(seg)
+pr = model.projections[proj]
+x = torch.randn(4096, pr.h_in, device=dev).to(torch.bfloat16)
+y = torch.zeros(4096, pr.h_out, device=dev, dtype=torch.bfloat16)
+for _ in range(3):
+    eng.apply(bp, 0, proj, x, y)
+torch.cuda.synchronize()
+print("ok")
