@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 mixed-rank LoRA delta path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1]
+
+One step = the delta path over one co-batched batch through every layer and projection of
+the model (config c2: Llama-2-7B, 32 layers x 7 projections, 100 power-law adapters
+r=8..128, 4096 tokens; synthetic inputs, random-init adapters).  ``value`` is whole-job
+tokens/s with inputs resident in HBM (CUDA-graph replay, CUDA events, max over ranks);
+``e2e`` is the same metric through the public API (host segment indexing + planning, plan
+upload, H2D of the batch's input activations from pinned memory, eager kernel launches for
+all layers, D2H of the final projection's output).  ``--impl reference`` times the CPU
+restatement (oracle/, test infrastructure) on this box's host cores: the reference itself has
+no tensor code, so its CPU "implementation" of this path is that restatement.
+Under torchrun every rank runs its own full batch (weak scaling; the path has no exchange
+step in data-parallel serving — SURVEY §8e).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mixed-rank LoRA tokens/s at 1/2/4/8 B200; % HBM roofline; remote-fetch overhead"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c2", "c1"), default="c2")
+    ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args(argv)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampled during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        def reader():
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=1)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+                for name, flag in zip(names, r[5:9]):
+                    if flag.strip().lower() in ("active", "1"):
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_layer_sample(wl, x_layer0: dict, adapters_l0: dict, budget_s: float):
+    """Time the CPU oracle on one full layer (all projections) of the workload; returns
+    (seconds per layer (median over reps), reps, threads)."""
+    from oracle import oracle
+    from paper_2511_22880_b200.lora import input_group
+    seg = wl.segments
+    threads = oracle.cpu_threads()
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        for p, pr in enumerate(wl.model.projections):
+            a_list = [adapters_l0[(int(slot), p)][0] for slot in seg.seg_slot]
+            b_list = [adapters_l0[(int(slot), p)][1] for slot in seg.seg_slot]
+            oracle.delta_c(x_layer0[input_group(pr.name)], seg.seg_indptr, seg.seg_rank, a_list, b_list,
+                           pr.h_out, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s * 0.5 or len(times) >= 10:
+            break
+    return statistics.median(times), len(times), threads
+
+
+def host_layer_inputs(wl, seed=0):
+    """CPU-generated layer-0 inputs for the reference arm (x and adapters, bf16 bit patterns)."""
+    import torch
+    from paper_2511_22880_b200.lora import input_group
+    g = torch.Generator().manual_seed(seed)
+    n = wl.segments.num_tokens
+    xs = {}
+    for pr in wl.model.projections:
+        grp = input_group(pr.name)
+        if grp not in xs:
+            xs[grp] = torch.randn(n, pr.h_in, generator=g).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    ads = {}
+    for slot, r in enumerate(wl.ranks):
+        ga = torch.Generator().manual_seed(1000 + slot)
+        for p, pr in enumerate(wl.model.projections):
+            a = (torch.randn(r, pr.h_in, generator=ga) / pr.h_in ** 0.5).to(torch.bfloat16)
+            b = (torch.randn(pr.h_out, r, generator=ga) / r ** 0.5).to(torch.bfloat16)
+            ads[(slot, p)] = (a.view(torch.int16).numpy().view(np.uint16), b.view(torch.int16).numpy().view(np.uint16))
+    return xs, ads
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU restatement on the host cores, bounded sample per step."""
+    from paper_2511_22880_b200 import synth
+    if rank != 0:
+        return None
+    wl = synth.WORKLOADS[args.config]()
+    xs, ads = host_layer_inputs(wl)
+    layers = wl.model.layers
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        t_layer, _, threads = cpu_layer_sample(wl, xs, ads, budget_s=0.0)  # one layer per step
+        if i >= args.warmup:
+            per_step.append(t_layer)
+    t_layer = statistics.median(per_step)
+    value = wl.segments.num_tokens / (t_layer * layers)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * layers * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in, fp32 accumulate",
+        "data": "synthetic", "config": {"workload": wl.description, "sample": "1 layer per step, x layers"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"1 of {layers} layers (all {len(wl.model.projections)} projections) per step, "
+                                   f"extrapolated x{layers}"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2511_22880_b200 import native, synth
+    from paper_2511_22880_b200.lora import (LoraDeltaEngine, algorithmic_bytes, algorithmic_flops,
+                                            input_group)
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.slab import AdapterSlab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    tier = {"auto": native.TIER_AUTO, "simt": native.TIER_SIMT, "tc": native.TIER_TC}[args.tier]
+    wl = synth.WORKLOADS[args.config]()
+    model = wl.model
+    seg = wl.segments
+    N = seg.num_tokens
+
+    # adapters resident in HBM (random-init, seeded per adapter)
+    slab_bytes = sum(r * model.rank_units_bytes() for r in wl.ranks) + 1024 * (len(wl.ranks) + 4)
+    slab = AdapterSlab(model, slab_bytes, dev)
+    for i, (aid, r) in enumerate(zip(wl.adapter_ids, wl.ranks)):
+        slab.fill_random(slab.allocate(aid, r), 1000 + i)
+    eng = LoraDeltaEngine(slab, tier_policy=tier)
+    bp = eng.prepare(seg)
+
+    # per-layer activations (distinct buffers; every step moves far more than the 126 MB L2)
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    groups = {}
+    for pr in model.projections:
+        groups.setdefault(input_group(pr.name), pr.h_in)
+    xs = [{grp: torch.randn(N, h, device=dev, generator=g).to(torch.bfloat16) for grp, h in groups.items()}
+          for _ in range(model.layers)]
+    ys = [{pr.name: torch.randn(N, pr.h_out, device=dev, generator=g).to(torch.bfloat16) for pr in model.projections}
+          for _ in range(model.layers)]
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident throughput: CUDA-graph replay of the whole step ----
+    with torch.cuda.stream(stream):
+        eng.forward(bp, xs, ys, stream)   # warm the tensor-map cache before capture
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        eng.forward(bp, xs, ys, stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            graph.replay()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = N * world / (ms / 1e3)
+
+    # launches per step (our kernels only)
+    launches = 0
+    for (h_in, h_out), sp in bp.shape_plans.items():
+        per = (1 if sp.summary[6] else 0) + (1 if sp.summary[7] else 0) + (2 if sp.summary[4] else 0)
+        launches += per * sum(1 for pr in model.projections if (pr.h_in, pr.h_out) == (h_in, h_out))
+    launches *= model.layers
+
+    # ---- algorithmic bytes / flops of the step ----
+    step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
+    step_flops = sum(algorithmic_flops(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
+    hbm_peak, peak_src = peaks()
+
+    # ---- dominant kernel roofline: expand (tcgen05) on the largest projection, CUDA events ----
+    big = max(range(len(model.projections)), key=lambda p: model.projections[p].h_out * model.projections[p].h_in)
+    pr = model.projections[big]
+    n_l = seg.lengths().astype(np.int64)
+    r_l = seg.seg_rank.astype(np.int64)
+    exp_bytes = int(np.sum(2 * r_l * pr.h_out + 4 * n_l * pr.h_out))
+    shr_bytes = int(np.sum(2 * n_l * pr.h_in + 2 * r_l * pr.h_in))
+    reps = 20
+    with torch.cuda.stream(stream):
+        eng.shrink(bp, 0, big, xs[0][input_group(pr.name)], stream)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        for _ in range(reps):
+            eng.expand(bp, 0, big, ys[0][pr.name], stream)
+        k1.record(stream)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(reps):
+            eng.shrink(bp, 0, big, xs[0][input_group(pr.name)], stream)
+        s1.record(stream)
+    torch.cuda.synchronize(dev)
+    exp_us = k0.elapsed_time(k1) / reps * 1e3
+    shr_us = s0.elapsed_time(s1) / reps * 1e3
+    achieved = exp_bytes / (exp_us * 1e-6) / 1e9
+
+    # ---- e2e through the public API with host buffers ----
+    from paper_2511_22880_b200.segments import index_tokens as _ix
+    tok_slots_host = np.repeat(seg.seg_slot, seg.lengths())   # the batch as the host sees it
+    x_host = torch.empty((N, model.projections[0].h_in), dtype=torch.bfloat16, pin_memory=True)
+    x_host.copy_(xs[0][input_group(model.projections[0].name)].cpu())
+    last = model.projections[-1]
+    y_host = torch.empty((N, last.h_out), dtype=torch.bfloat16, pin_memory=True)
+    x_dev0 = xs[0][input_group(model.projections[0].name)]
+    e2e_times = []
+    h2d_bytes = x_host.numel() * 2
+    d2h_bytes = y_host.numel() * 2
+    plan_bytes = 0
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            seg_i = _ix(tok_slots_host, wl.ranks)                  # host segment indexing
+            bp_i = eng.prepare(seg_i)                              # host planning + plan/pointer upload
+            x_dev0.copy_(x_host, non_blocking=True)                # H2D of the batch's input
+            eng.forward(bp_i, xs, ys, stream)
+            y_host.copy_(ys[-1][last.name], non_blocking=True)     # D2H of the result
+        stream.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+        if i == 0:
+            plan_bytes = sum(sp.plan_host.nbytes for sp in bp_i.shape_plans.values()) + \
+                bp_i.a_ptrs.numel() * 8 * 2
+    e2e_s = statistics.median(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = N * world / e2e_s
+
+    # ---- CPU baseline (rank 0, N=1 only): the oracle on one full layer, extrapolated ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        x_l0 = {grp: t.view(torch.int16).cpu().numpy().view(np.uint16) for grp, t in xs[0].items()}
+        ads = {}
+        for slot in seg.seg_slot:
+            for p in range(len(model.projections)):
+                a, b = slab.read(int(slot), 0, p)
+                ads[(int(slot), p)] = (a.view(torch.int16).cpu().numpy().view(np.uint16),
+                                       b.view(torch.int16).cpu().numpy().view(np.uint16))
+        t_layer, reps_cpu, threads = cpu_layer_sample(wl, x_l0, ads, args.cpu_budget_s)
+        cpu = {"value": N / (t_layer * model.layers), "unit": "tokens/s", "cores": threads, "kind": "port",
+               "sample": f"layer 0 of {model.layers} (all {len(model.projections)} projections, {N} tokens), "
+                         f"median of {reps_cpu} reps, extrapolated x{model.layers}"}
+
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapters, N(0,1) activations)",
+        "config": {"workload": wl.description, "config": args.config, "tier_policy": args.tier,
+                   "l2": "inputs larger than L2 (per-layer activation buffers; %.1f GB moved per step)" % (step_bytes / 1e9),
+                   "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
+        "step_hbm": {"algorithmic_bytes": step_bytes, "achieved_GBs": step_bytes / (ms * 1e-3) / 1e9,
+                     "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak, "flops": step_flops},
+        "roofline": {"bound": "hbm", "kernel": f"expand_tc_kernel ({pr.name} {pr.h_in}->{pr.h_out})",
+                     "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "launch_us": exp_us,
+                     "algorithmic_bytes_per_launch": exp_bytes,
+                     "shrink": {"launch_us": shr_us, "algorithmic_bytes_per_launch": shr_bytes,
+                                "achieved": shr_bytes / (shr_us * 1e-6) / 1e9}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d_bytes + plan_bytes,
+                "d2h_bytes_per_step": d2h_bytes,
+                "path": "index_tokens -> LoraDeltaEngine.prepare -> H2D x -> forward (eager) -> D2H y"},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    return line
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return 0
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
