@@ -204,7 +204,7 @@ def run_ours(args, rank, world, local_rank):
     N = seg.num_tokens
 
     # adapters resident in HBM (random-init, seeded per adapter)
-    slab_bytes = sum(r * model.rank_units_bytes() for r in wl.ranks) + 1024 * (len(wl.ranks) + 4)
+    slab_bytes = AdapterSlab.capacity_for(model, wl.ranks)
     slab = AdapterSlab(model, slab_bytes, dev)
     for i, (aid, r) in enumerate(zip(wl.adapter_ids, wl.ranks)):
         slab.fill_random(slab.allocate(aid, r), 1000 + i)

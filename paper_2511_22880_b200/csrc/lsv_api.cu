@@ -49,7 +49,8 @@ int fail(int code, const char* fmt, ...) {
 // rank > 128 go to the SIMT tier; everything else is tcgen05.  Justified by the per-tier
 // measurements in DESIGN.md §4 (profiles/).
 constexpr int kAutoSimtMaxTok = 8;
-constexpr int64_t kMinItemBytes = 96 * 1024;  // smallest shrink k-split worth a pipeline fill
+constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
+constexpr int kShrinkWaves = 4;               // target shrink items per SM (balance vs split cost)
 
 int num_sms_cached() {
   static int sms = -1;
@@ -76,6 +77,9 @@ struct PlanBuilder {
   std::vector<int32_t> shrink_cta;   // [grid+1]
   std::vector<ExpandRec> expand;
   std::vector<int32_t> expand_cta;
+  std::vector<int32_t> red;          // {mtile, first unit} per split tile
+  int32_t red_units = 0;
+  std::vector<int32_t> red_cta;
 };
 
 // LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
@@ -165,7 +169,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     kch[i] = std::max<int64_t>(1, std::min<int64_t>(4, kShrinkSlotBytes / row_bytes[i]));
     total += row_bytes[i] * chunks;
   }
-  const int64_t target = std::max<int64_t>(kMinItemBytes, total / std::max(1, 2 * nsm));
+  const int64_t target = std::max<int64_t>(kMinItemBytes, total / std::max(1, kShrinkWaves * nsm));
   int64_t part_off = 0, vimg_off = 0;
   int counter = 0;
   std::vector<std::pair<int64_t, ShrinkRec>> shrink_costed;
@@ -179,10 +183,14 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     mt.nsplit = nsplit;
     mt.part_off = (int32_t)part_off;
     if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * mt.rank;
-    const int kp16 = std::max(16, mt.rank);
-    mt.vimg_off = (int32_t)vimg_off;
-    vimg_off += (int64_t)round_up(mt.ntok, 16) * kp16 * 2;
+    mt.vimg_off = (int32_t)vimg_off;  // 1024-aligned: the v image's swizzle atoms are address-based
+    vimg_off += round_up((int)((int64_t)round_up(mt.ntok, 16) * kpad(mt.rank) * 2), 1024);
     mt.counter = counter++;
+    if (nsplit > 1) {  // reduction units: (token, 8 padded-k) of this tile, reduced grid-wide
+      pb.red.push_back((int32_t)i);
+      pb.red.push_back(pb.red_units);
+      pb.red_units += mt.ntok * (kpad(mt.rank) / 8);
+    }
     for (int sp = 0; sp < nsplit; ++sp) {
       ShrinkRec r{};
       r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
@@ -203,8 +211,9 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
   for (size_t i = 0; i < pb.mtiles.size(); ++i) {
     const MTile& mt = pb.mtiles[i];
-    const int64_t cost = 128LL * mt.rank * 2 + (int64_t)mt.ntok * 128 * 4 + 8 * 1024;
-    for (int jt = 0; jt < h_out / kExpandW; ++jt) {
+    const int tw = b_tile_width(h_out);
+    const int64_t cost = (int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024;
+    for (int jt = 0; jt < h_out / tw; ++jt) {
       ExpandRec r{};
       r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
       r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i;
@@ -240,9 +249,22 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   off = round_up(off, 4);
   h.off_expand_recs = off; off += 8 * h.n_expand_items;
   h.off_expand_cta = off; off += (int32_t)pb.expand_cta.size();
+  h.off_red = off; off += (int32_t)pb.red.size();
+  h.n_red = (int32_t)pb.red.size() / 2;
+  h.red_units = pb.red_units;
+  // split-K reduction: CTA c reduces units [c*U/G, (c+1)*U/G); record the entry holding its first
+  std::vector<int32_t> red_cta(shrink_grid + 1, 0);
+  for (int c = 0; c <= shrink_grid; ++c) {
+    const int64_t u0 = shrink_grid > 0 ? (int64_t)pb.red_units * c / shrink_grid : 0;
+    int e = 0;
+    while (e + 1 < h.n_red && pb.red[2 * (e + 1) + 1] <= u0) ++e;
+    red_cta[c] = e;
+  }
+  h.off_red_cta = off; off += (int32_t)red_cta.size();
+  pb.red_cta = red_cta;
   h.total_ints = off;
   int64_t ws = 0;
-  h.ws_counters = 0; ws += round_up(std::max(1, counter) * 4, 256);
+  h.ws_counters = 0; ws += round_up((counter + 2) * 4, 256);  // + grid barrier {arrive, done}
   h.ws_partials = (int32_t)ws; ws += (part_off * 4 + 255) / 256 * 256;
   h.ws_vimg = (int32_t)ws; ws += (vimg_off + 1023) / 1024 * 1024;
   h.ws_simt_v = (int32_t)ws; ws += (v_off * 4 + 255) / 256 * 256;
@@ -318,7 +340,7 @@ int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t ro
   for (int b = 0; b < nmaps; ++b) {
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)kChunk : (cuuint32_t)kExpandW,
+    const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)kChunk : (cuuint32_t)128,
                                kind == 0 ? (cuuint32_t)(8 << b) : (cuuint32_t)(1 << b)};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
@@ -390,6 +412,9 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
     p.off_recs = h->off_shrink_recs; p.off_cta = h->off_shrink_cta;
     p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg; p.ws_counters = h->ws_counters;
+    p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
+    p.off_red_cta = h->off_red_cta;
+    p.grid_bar = h->n_counters;
     p.trace = g_trace; p.trace_items = g_trace_items;
     LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p));
   }
@@ -399,18 +424,19 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
 int run_expand(const PlanHeader* h, void* y, int64_t ldy, int32_t num_tokens, const void* const* b_ptrs, const int32_t* plan, uint8_t* ws,
                cudaStream_t st) {
   if (h->n_simt_items > 0) {
-    simt_expand_kernel<<<dim3(h->n_simt_items, h->h_out / 128), 64, 0, st>>>(
-        static_cast<__nv_bfloat16*>(y), ldy, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
+    simt_expand_kernel<<<dim3(h->n_simt_items, (h->h_out + 511) / 512), 64, 0, st>>>(
+        static_cast<__nv_bfloat16*>(y), ldy, h->h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
         reinterpret_cast<const float*>(ws + h->ws_simt_v));
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   if (h->n_expand_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
     ExpandParams p{};
-    if (int rc = get_maps(p.ymap, 1, y, ldy, num_tokens, h->h_out)) return rc;
+    if (int rc = get_maps(p.ymap, 0, y, ldy, num_tokens, h->h_out)) return rc;
     p.plan = plan; p.b_ptrs = b_ptrs; p.ws = ws; p.y = static_cast<__nv_bfloat16*>(y); p.ldy = ldy;
     p.off_recs = h->off_expand_recs; p.off_cta = h->off_expand_cta;
     p.ws_vimg = h->ws_vimg;
+    p.tw = b_tile_width(h->h_out);
     p.dbg = g_debug_expand;
     p.trace = g_trace; p.trace_items = g_trace_items;
     LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, h->expand_grid, expand_smem_bytes(), st, p));
@@ -433,7 +459,7 @@ size_t lsv_adapter_a_bytes(int32_t rank, int32_t h_in) {
   return (rank > 0 && h_in > 0) ? (size_t)rank * h_in * 2 : 0;
 }
 size_t lsv_adapter_b_bytes(int32_t rank, int32_t h_out) {
-  return (rank > 0 && h_out > 0) ? (size_t)rank * h_out * 2 : 0;
+  return (rank > 0 && h_out > 0) ? (size_t)kpad(rank) * h_out * 2 : 0;  // rows padded to 16
 }
 
 static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in, int32_t h_out,
@@ -444,7 +470,7 @@ static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int
   if (!lora_a || !lora_b || !a_tiled || !b_tiled) return fail(LSV_EINVAL, "null buffer");
   if (!aligned16(lora_a) || !aligned16(lora_b) || !aligned16(a_tiled) || !aligned16(b_tiled))
     return fail(LSV_EINVAL, "buffers must be 16-byte aligned");
-  const int64_t units = ((int64_t)rank * h_in + (int64_t)h_out * rank) / 8;
+  const int64_t units = ((int64_t)rank * h_in + (int64_t)h_out * kpad(rank)) / 8;
   const int blocks = (int)std::min<int64_t>(4096, (units + 255) / 256);
   pack_adapter_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(lora_a), static_cast<const uint8_t*>(lora_b), rank, h_in, h_out,
@@ -493,6 +519,8 @@ int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_
   std::copy(pb.shrink_cta.begin(), pb.shrink_cta.end(), out + h.off_shrink_cta);
   std::memcpy(out + h.off_expand_recs, pb.expand.data(), pb.expand.size() * sizeof(ExpandRec));
   std::copy(pb.expand_cta.begin(), pb.expand_cta.end(), out + h.off_expand_cta);
+  std::copy(pb.red.begin(), pb.red.end(), out + h.off_red);
+  std::copy(pb.red_cta.begin(), pb.red_cta.end(), out + h.off_red_cta);
   return LSV_OK;
 }
 

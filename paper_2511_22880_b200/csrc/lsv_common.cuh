@@ -7,14 +7,14 @@
 //      swizzle atom: 16-byte unit u of row k lives at unit u ^ (k & 7).  Any run of
 //      consecutive chunks is contiguous, so one stage of the shrink is one bulk copy.
 //
-//  B tiled  (lora_B [h_out][rank] viewed as B^T rows j=h_out, cols k=rank; operand A of the
-//      tcgen05 expand, K-major, no swizzle "interleaved" core matrices)
-//      [h_out/8 row groups][rank/8 k-cores][8 rows][8 elems]; a 128-row h_out tile is
-//      128*rank*2 contiguous bytes.
+//  B tiled  (lora_B [h_out][rank]; operand B of the tcgen05 expand, MN-major SWIZZLE_128B)
+//      per tw-wide h_out tile (tw = 256, or 128 when h_out is not a multiple of 256):
+//      [kp/8 k-groups][tw/64 x 64 h_out][8 k][64 h_out] with kp = rank padded to 16 (zero rows);
+//      a tile is tw*kp*2 contiguous bytes, one bulk copy.
 //
-//  v image  (x·A^T of one 128-token tile, operand B of the expand, K-major interleaved)
-//      [n_pad16/8 token groups][kp16/8 k-cores][8][8], kp16 = max(16, rank); k-cores
-//      past the rank are zero so a rank-8 adapter can feed a K=16 MMA.
+//  v image  (x·A^T of one 128-token tile, operand A of the expand, K-major, SWIZZLE_32/64/128B
+//      by padded rank kp = round_up(max(rank,16),16)); k past the rank is zero so a rank-8
+//      adapter feeds a K=16 MMA.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -25,21 +25,46 @@ namespace lsv {
 constexpr int kNumSmsDefault = 148;
 constexpr int kChunk = 64;          // elements per 128-byte swizzle row
 constexpr int kTileM = 128;         // tokens per tcgen05 m-tile
-constexpr int kExpandW = 128;       // h_out columns per expand item
 constexpr int kSimtMaxTok = 8;      // tokens per SIMT item
 
 __host__ __device__ __forceinline__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // ---- layout address functions (byte offsets) -------------------------------------------
+// Hardware swizzle of a byte offset inside a region aligned to the pattern period
+// (SWIZZLE_32B/64B/128B = rows of 32/64/128 bytes): 16-byte unit bits [4..6] ^= bits [7..9].
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t off, int row_bytes) {
+  const uint32_t mask = row_bytes == 128 ? 0x70u : row_bytes == 64 ? 0x30u : row_bytes == 32 ? 0x10u : 0u;
+  return off ^ ((off >> 3) & mask);
+}
+// K padded for the 16-wide MMA K step (rank 8 -> 16, 24 -> 32, ...)
+__host__ __device__ __forceinline__ int kpad(int rank) { return round_up(rank < 16 ? 16 : rank, 16); }
+// v-image / K-major operand row width: the widest swizzle whose element run divides kp
+__host__ __device__ __forceinline__ int kmajor_row_bytes(int kp) { return kp % 64 == 0 ? 128 : kp % 32 == 0 ? 64 : 32; }
+__host__ __device__ __forceinline__ uint32_t umma_layout(int row_bytes) {
+  return row_bytes == 128 ? 2u : row_bytes == 64 ? 4u : 6u;  // SWIZZLE_128B / 64B / 32B
+}
+
+// A tiled (shrink B operand, K-major SW128): [h_in/64][rank][64]
 __host__ __device__ __forceinline__ size_t a_tiled_off(int k, int i, int rank) {
   const int c = i >> 6, e = i & 63;
   return (size_t)c * rank * 128 + (size_t)k * 128 + ((((e >> 3) ^ (k & 7)) << 4) | ((e & 7) << 1));
 }
-__host__ __device__ __forceinline__ size_t b_tiled_off(int j, int k, int rank) {
-  return (size_t)(j >> 3) * rank * 16 + (size_t)(k >> 3) * 128 + (j & 7) * 16 + (k & 7) * 2;
+// B tiled (expand B operand, MN-major SW128): per tw-wide h_out tile (tw = b_tile_width(h_out))
+// [kp/8 k-groups][tw/64 blocks of 64 h_out][8 k rows][64 h_out], 1024-byte swizzle atoms;
+// kp = kpad(rank) rows, the rows past the rank are zero so a K=16 MMA step never reads stale data.
+__host__ __device__ __forceinline__ int b_tile_width(int h_out) { return h_out % 256 == 0 ? 256 : 128; }
+__host__ __device__ __forceinline__ size_t b_tiled_off(int j, int k, int rank, int tw) {
+  const int jt = j / tw, jj = j % tw;
+  const uint32_t in_atom = (uint32_t)((k & 7) * 128 + (jj & 63) * 2);
+  return (size_t)jt * kpad(rank) * tw * 2 + (size_t)(k >> 3) * (tw / 64) * 1024 + (jj >> 6) * 1024 +
+         swz(in_atom, 128);
 }
-__host__ __device__ __forceinline__ int vimg_off(int t, int k, int kp16) {
-  return (t >> 3) * kp16 * 16 + (k >> 3) * 128 + (t & 7) * 16 + (k & 7) * 2;
+// v image (expand A operand, K-major, swizzle by kmajor_row_bytes(kp)): rows = tokens (rows_pad =
+// ntok rounded to 16), K = kp; K split in chunks of row_bytes/2 elements laid out chunk-major.
+__host__ __device__ __forceinline__ uint32_t vimg_off(int t, int k, int kp, int rows_pad) {
+  const int S = kmajor_row_bytes(kp), ck = S / 2;
+  const uint32_t off = (uint32_t)((k / ck) * rows_pad * S + t * S + (k % ck) * 2);
+  return swz(off, S);
 }
 
 // ---- small device helpers ----------------------------------------------------------------
@@ -180,9 +205,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
   d |= (uint64_t)layout << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major.
-__host__ __device__ __forceinline__ uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: kind::f16, A=B=bf16, D=f32; A K-major; B K-major (b_mn_major=0) or
+// MN-major (b_mn_major=1, bit 16).
+__host__ __device__ __forceinline__ uint32_t idesc_bf16(int M, int N, int b_mn_major = 0) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(b_mn_major & 1) << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -206,6 +233,24 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 lanes x 32 columns: thread i gets TMEM lane (base + i), 32 consecutive fp32 columns.
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_global_v4_if(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool pred) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p st.global.v4.b32 [%0], {%1, %2, %3, %4};\n\t}\n" ::"l"(ptr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"((uint32_t)pred)
+               : "memory");
 }
 
 }  // namespace lsv

@@ -32,7 +32,9 @@ struct PlanHeader {            // 64 int32
   int32_t ws_counters, ws_partials, ws_vimg, ws_simt_v, ws_bytes;
   int32_t n_counters;
   int32_t simt_segments;
-  int32_t reserved[64 - 29];
+  int32_t off_red, n_red, red_units;   // split-K reduction table: [n_red] {mtile, unit prefix}
+  int32_t off_red_cta;                 // [shrink_grid + 1] first reduction entry of each CTA's unit range
+  int32_t reserved[64 - 33];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -60,7 +62,7 @@ struct ShrinkRec {             // 16 int32
 
 struct ExpandRec {             // 8 int32
   int32_t seg, tok_begin, ntok, rank;
-  int32_t jtile, vimg_off, mtile, pad;          // h_out columns [jtile*128, jtile*128+128)
+  int32_t jtile, vimg_off, mtile, pad;          // h_out columns [jtile*tw, jtile*tw+tw)
 };
 
 // Pipeline geometry (bytes of shared memory).

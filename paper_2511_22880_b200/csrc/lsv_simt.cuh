@@ -3,8 +3,8 @@
 // The SIMT tier serves segments too short to fill a 128-row tcgen05 tile: decode steps
 // (one token per request, the reference's decode_iter_time regime, costmodel.py:108-123)
 // and tiny prefill segments.  Shrink: one warp per rank row, lanes stride h_in with 16-byte
-// loads of x and of the tiled A row, warp-shuffle reduction.  Expand: one thread per two
-// h_out columns, bf16x2 read-modify-write of y.
+// loads of x and of the tiled A row, warp-shuffle reduction.  Expand: one thread per eight
+// h_out columns (a 16-byte unit of the B tile), 16-byte read-modify-write of y.
 #pragma once
 #include "lsv_common.cuh"
 #include "lsv_plan.h"
@@ -64,8 +64,10 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   }
 }
 
-// grid = (n_simt_items, h_out/128), block = 64: thread owns h_out columns j, j+1.
-__global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy,
+// grid = (n_simt_items, ceil(h_out/512)), block = 64: thread owns 8 consecutive h_out columns
+// (one 16-byte unit of a B-tile row), so each k costs one 16-byte load of B and the y update is a
+// 16-byte read-modify-write per token.
+__global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy, int h_out,
                                                          const int32_t* __restrict__ plan, int off_items,
                                                          int off_rank, const void* const* __restrict__ b_ptrs,
                                                          const float* __restrict__ simt_v) {
@@ -75,45 +77,50 @@ __global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restri
   const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
   for (int e = threadIdx.x; e < it.ntok * r; e += blockDim.x) vs[e] = simt_v[it.v_off + e];
   __syncthreads();
-  const int j = blockIdx.y * 128 + threadIdx.x * 2;
-  float acc0[kSimtMaxTok], acc1[kSimtMaxTok];
+  const int j = (blockIdx.y * 64 + threadIdx.x) * 8;
+  if (j >= h_out) return;
+  const int tw = b_tile_width(h_out);
+  float acc[kSimtMaxTok][8];
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t) acc0[t] = acc1[t] = 0.f;
-  for (int kc = 0; kc < r; kc += 8) {
-    const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, kc, r)));
-    const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j + 1, kc, r)));
-    const float w0[8] = {bf16_lo(b0.x), bf16_hi(b0.x), bf16_lo(b0.y), bf16_hi(b0.y),
-                         bf16_lo(b0.z), bf16_hi(b0.z), bf16_lo(b0.w), bf16_hi(b0.w)};
-    const float w1[8] = {bf16_lo(b1.x), bf16_hi(b1.x), bf16_lo(b1.y), bf16_hi(b1.y),
-                         bf16_lo(b1.z), bf16_hi(b1.z), bf16_lo(b1.w), bf16_hi(b1.w)};
+  for (int t = 0; t < kSimtMaxTok; ++t)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
+  for (int k = 0; k < r; ++k) {
+    const uint4 bw = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, k, r, tw)));
+    const float w[8] = {bf16_lo(bw.x), bf16_hi(bw.x), bf16_lo(bw.y), bf16_hi(bw.y),
+                        bf16_lo(bw.z), bf16_hi(bw.z), bf16_lo(bw.w), bf16_hi(bw.w)};
 #pragma unroll
     for (int t = 0; t < kSimtMaxTok; ++t) {
       if (t < it.ntok) {
+        const float vv = vs[t * r + k];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float vv = vs[t * r + kc + e];
-          acc0[t] = fmaf(vv, w0[e], acc0[t]);
-          acc1[t] = fmaf(vv, w1[e], acc1[t]);
-        }
+        for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
       }
     }
   }
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t) {
     if (t < it.ntok) {
-      uint32_t* py = reinterpret_cast<uint32_t*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
-      const uint32_t yv = *py;
-      *py = pack_bf16x2(bf16_lo(yv) + acc0[t], bf16_hi(yv) + acc1[t]);
+      uint4* py = reinterpret_cast<uint4*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
+      const uint4 yv = *py;
+      uint4 o;
+      o.x = pack_bf16x2(bf16_lo(yv.x) + acc[t][0], bf16_hi(yv.x) + acc[t][1]);
+      o.y = pack_bf16x2(bf16_lo(yv.y) + acc[t][2], bf16_hi(yv.y) + acc[t][3]);
+      o.z = pack_bf16x2(bf16_lo(yv.z) + acc[t][4], bf16_hi(yv.z) + acc[t][5]);
+      o.w = pack_bf16x2(bf16_lo(yv.w) + acc[t][6], bf16_hi(yv.w) + acc[t][7]);
+      *py = o;
     }
   }
 }
 
 // ---- adapter slab packing ---------------------------------------------------------------
-// lora_a [rank][h_in] -> A tiled; lora_b [h_out][rank] -> B tiled.  One thread per 16 bytes.
+// lora_a [rank][h_in] -> A tiled; lora_b [h_out][rank] -> B tiled.  One thread per 16 bytes of
+// the tiled buffers.
 __global__ void pack_adapter_kernel(const uint8_t* __restrict__ lora_a, const uint8_t* __restrict__ lora_b,
                                     int rank, int h_in, int h_out, uint8_t* __restrict__ a_t,
                                     uint8_t* __restrict__ b_t, int unpack) {
-  const int64_t na = (int64_t)rank * h_in / 8, nb = (int64_t)h_out * rank / 8;
+  const int kp = kpad(rank);
+  const int64_t na = (int64_t)rank * h_in / 8, nb = (int64_t)h_out * kp / 8;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < na + nb;
        u += (int64_t)gridDim.x * blockDim.x) {
     if (u < na) {
@@ -122,11 +129,20 @@ __global__ void pack_adapter_kernel(const uint8_t* __restrict__ lora_a, const ui
       uint4* tiled = reinterpret_cast<uint4*>(a_t + a_tiled_off(k, i, rank));
       if (unpack) *plain = *tiled; else *tiled = *plain;
     } else {
+      // one 16-byte unit of B tiled = lora_b[j .. j+7][k] (a strided column gather of lora_B);
+      // k in [rank, kp) is the zero padding
       const int64_t w = u - na;
-      const int j = (int)(w / (rank / 8)), k = (int)(w % (rank / 8)) * 8;
-      uint4* plain = reinterpret_cast<uint4*>(const_cast<uint8_t*>(lora_b) + ((int64_t)j * rank + k) * 2);
-      uint4* tiled = reinterpret_cast<uint4*>(b_t + b_tiled_off(j, k, rank));
-      if (unpack) *plain = *tiled; else *tiled = *plain;
+      const int k = (int)(w % kp), j = (int)(w / kp) * 8;
+      uint16_t* plain = reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(lora_b)) + (int64_t)j * rank + k;
+      uint16_t* tiled = reinterpret_cast<uint16_t*>(b_t + b_tiled_off(j, k, rank, b_tile_width(h_out)));
+      if (unpack) {
+        if (k < rank)
+          for (int e = 0; e < 8; ++e) plain[(int64_t)e * rank] = tiled[e];
+      } else {
+        alignas(16) uint16_t v[8];
+        for (int e = 0; e < 8; ++e) v[e] = k < rank ? plain[(int64_t)e * rank] : (uint16_t)0;
+        *reinterpret_cast<uint4*>(tiled) = *reinterpret_cast<const uint4*>(v);
+      }
     }
   }
 }

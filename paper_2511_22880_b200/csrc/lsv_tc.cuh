@@ -5,12 +5,11 @@
 //   64-column chunk, composed from 128/64/32/16/8-row boxes; A_s: one cp.async.bulk of a
 //   pre-swizzled [kch chunks][rank][64] slab run.  Rows past the segment / columns past the
 //   rank are garbage in, garbage out (row i of D only reads row i of x; column j only
-//   row j of A) and are never stored.  k-splits are reduced deterministically by the
-//   last-arriving CTA (fixed summation order) into the bf16 "v image".
-// Expand  D[128 h_out × N=ntok16] = B_s^T[128 × rank16] · v^T            (swap-AB)
-//   B tile and v image: one cp.async.bulk each; the item's y rows arrive by TMA (exact row
-//   count, boxes of 128..1 rows) into the same ring allocation, so the y read is prefetched as
-//   deep as the ring; the epilogue adds D and writes bf16x2 words straight back to HBM.
+//   row j of A) and are never stored.  k-split partials are reduced after a grid barrier by
+//   all CTAs in parallel (fixed summation order per element) into the bf16 "v image".
+// Expand  D[128 tok × 128 h_out] = v·B_s^T + I·y                         (y added on the tensor core)
+//   B tile and v image: one cp.async.bulk each; the item's y rows: TMA into an MN-major
+//   SWIZZLE_128B operand; the epilogue is LDTM -> cvt -> 16-byte row stores.
 //
 // Both kernels: 192 threads, one persistent CTA per SM, each streaming its own list of fully
 // decoded work records (the host planner assigns records to CTAs LPT-greedy on estimated bytes,
@@ -27,7 +26,8 @@
 namespace lsv {
 
 constexpr int kTcThreads = 192;
-constexpr int kTmemCols = 256;  // two 128-column accumulators (double buffer)
+constexpr int kTmemCols = 512;  // four 128-column accumulators
+constexpr int kAccBufs = 4;
 constexpr int kItemQ = 8;       // expand: ring allocations in flight
 
 struct alignas(64) ShrinkParams {
@@ -36,18 +36,20 @@ struct alignas(64) ShrinkParams {
   const void* const* a_ptrs;
   uint8_t* ws;
   int off_recs, off_cta, ws_partials, ws_vimg, ws_counters;
+  int off_mtiles, off_red, n_red, red_units, grid_bar, off_red_cta;   // grid-wide split-K reduction
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
 };
 
 struct alignas(64) ExpandParams {
-  CUtensorMap ymap[8];          // y [num_tokens][h_out], boxes {128 cols × 1<<b rows}, no swizzle
+  CUtensorMap ymap[5];          // y [num_tokens][h_out], boxes {64 cols × 8<<b rows}, SWIZZLE_128B
   const int32_t* plan;
   const void* const* b_ptrs;
   uint8_t* ws;
   __nv_bfloat16* y;
   int64_t ldy;
   int off_recs, off_cta, ws_vimg;
+  int tw;                       // h_out tile width of the B slab layout (128 or 256)
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -59,54 +61,91 @@ __device__ __forceinline__ void trace_stamp(uint64_t* trace, int trace_items, in
     trace[((size_t)cta * trace_items + i) * 16 + 8 + k] = clock64();
   }
 }
+// CTA-level phase stamps land in the last item slot of the trace buffer.
+__device__ __forceinline__ void phase_stamp(uint64_t* trace, int trace_items, int cta, int k) {
+  if (trace != nullptr) trace_stamp(trace, trace_items, cta, trace_items - 1, k);
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Streams one CTA's record list with a one-record lookahead (the next load is in flight while
-// the current record is processed).
-template <typename Rec>
-struct RecStream {
+// Warp-cooperative stream over one CTA's record list: every lane of the warp calls pop(); a
+// refill loads the next CH records (one per lane) plus each record's adapter pointer into the
+// warp's shared-memory buffer, so the dependent global loads cost one latency per CH items
+// instead of one per item.
+template <typename Rec, int CH>
+struct WarpRecBuf {
+  Rec rec[CH];
+  const uint8_t* ptr[CH];
+};
+
+template <typename Rec, int CH>
+struct WarpRecStream {
+  WarpRecBuf<Rec, CH>* buf;
   const Rec* recs;
-  int k, end;
-  Rec next;
-  __device__ __forceinline__ RecStream(const int32_t* plan, int off_recs, int off_cta, int cta) {
+  const void* const* ptrs;
+  int next, end, j, n;
+  __device__ __forceinline__ WarpRecStream(WarpRecBuf<Rec, CH>* b, const int32_t* plan, int off_recs, int off_cta,
+                                           int cta, const void* const* adapter_ptrs) {
+    buf = b;
     recs = reinterpret_cast<const Rec*>(plan + off_recs);
-    k = plan[off_cta + cta];
+    ptrs = adapter_ptrs;
+    next = plan[off_cta + cta];
     end = plan[off_cta + cta + 1];
-    if (k < end) next = recs[k];
+    j = n = 0;
   }
-  __device__ __forceinline__ bool pop(Rec& r) {
-    if (k >= end) return false;
-    r = next;
-    if (++k < end) next = recs[k];
+  // all 32 lanes must call; returns the same record on every lane
+  __device__ __forceinline__ bool pop(Rec& r, const uint8_t*& ptr) {
+    if (j == n) {
+      if (next >= end) return false;
+      __syncwarp();
+      const int lane = threadIdx.x & 31;
+      n = min(CH, end - next);
+      if (lane < n) {
+        const Rec rr = recs[next + lane];
+        buf->rec[lane] = rr;
+        buf->ptr[lane] = ptrs ? static_cast<const uint8_t*>(ptrs[rr.seg]) : nullptr;
+      }
+      __syncwarp();
+      next += n;
+      j = 0;
+    }
+    r = buf->rec[j];
+    ptr = buf->ptr[j];
+    ++j;
     return true;
   }
 };
 
+constexpr int kShrinkRecCh = 16;
+constexpr int kExpandRecCh = 32;
+using ShrinkRecBuf = WarpRecBuf<ShrinkRec, kShrinkRecCh>;
+using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
+
 __host__ __device__ constexpr int shrink_smem_bytes() {
-  return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 1024;
+  return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
 }
 __host__ __device__ constexpr int expand_smem_bytes() {
-  return 1024 + kExpandRingBytes + kExpandGuardBytes + 1024;
+  return 1024 + kExpandRingBytes + kExpandGuardBytes + 256 * 16 * 2 + 6 * (int)sizeof(ExpandRecBuf) + 1024;
 }
 
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
+  ShrinkRecBuf* recbuf = reinterpret_cast<ShrinkRecBuf*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + 6);
   uint64_t* empty = full + kShrinkSlots;
   uint64_t* tfull = empty + kShrinkSlots;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* tempty = tfull + kAccBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_mbar_init();
     for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
   }
@@ -116,49 +155,55 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int cta = blockIdx.x;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
   pdl_wait();                 // x, workspace and counters are written by earlier launches
   pdl_launch_dependents();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer
-      RecStream<ShrinkRec> rs(p.plan, p.off_recs, p.off_cta, cta);
-      ShrinkRec inf;
-      int slot = 0; uint32_t phase = 0;
-      for (int k = 0; rs.pop(inf); ++k) {
-        trace_stamp(p.trace, p.trace_items, cta, k, 0);
-        const int r = inf.rank, np8 = round_up(inf.ntok, 8), kch = inf.kch;
-        const uint8_t* a = static_cast<const uint8_t*>(p.a_ptrs[inf.seg]);
-        for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
-          const int kc = min(kch, inf.chunk_end - g);
+  if (warp == 0) {  // ---------------- producer: lane 0 owns the slot ring, lanes issue the copies
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, p.a_ptrs);
+    ShrinkRec inf;
+    const uint8_t* a;
+    int slot = 0; uint32_t phase = 0;
+    for (int k = 0; rs.pop(inf, a); ++k) {
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+      const int r = inf.rank, np8 = round_up(inf.ntok, 8), kch = inf.kch;
+      const int m = np8 >> 3, pc = __popc(m);   // x boxes per chunk: one per set bit of np8/8
+      for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
+        const int kc = min(kch, inf.chunk_end - g);
+        if (lane == 0) {
           mbar_wait(&empty[slot], phase ^ 1);
-          uint8_t* dst = ring + slot * kShrinkSlotBytes;
           mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (np8 + r) * 128));
-          for (int c = 0; c < kc; ++c) {
-            int row = 0;
-            for (int b = 4; b >= 0; --b) {
-              const int R = 8 << b;
-              if (np8 - row >= R) {
-                tma_load_2d(dst + (c * np8 + row) * 128, &p.xmap[b], &full[slot], (g + c) * kChunk,
-                            inf.tok_begin + row);
-                row += R;
-              }
-            }
-          }
-          bulk_load(dst + kc * np8 * 128, a + (size_t)g * r * 128, (uint32_t)(kc * r * 128), &full[slot]);
-          if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
         }
-        trace_stamp(p.trace, p.trace_items, cta, k, 1);
+        __syncwarp();
+        uint8_t* dst = ring + slot * kShrinkSlotBytes;
+        if (lane == 0) {
+          bulk_load(dst + kc * np8 * 128, a + (size_t)g * r * 128, (uint32_t)(kc * r * 128), &full[slot]);
+        } else if (lane - 1 < kc * pc) {
+          const int c = (lane - 1) / pc, i = (lane - 1) % pc;
+          int mm = m, row = 0, bb = -1;
+          for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
+            bb = 31 - __clz(mm);
+            if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
+          }
+          tma_load_2d(dst + (c * np8 + row) * 128, &p.xmap[bb], &full[slot], (g + c) * kChunk,
+                      inf.tok_begin + row);
+        }
+        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+      __syncwarp();
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      RecStream<ShrinkRec> rs(p.plan, p.off_recs, p.off_cta, cta);
-      ShrinkRec inf;
-      int slot = 0; uint32_t phase = 0;
-      for (int k = 0; rs.pop(inf); ++k) {
+  } else if (warp == 1) {  // ---------------- MMA issuer (lane 0)
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[1], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+    ShrinkRec inf;
+    const uint8_t* unused;
+    int slot = 0; uint32_t phase = 0;
+    for (int k = 0; rs.pop(inf, unused); ++k) {
+      if (lane == 0) {
         const int r = inf.rank, np8 = round_up(inf.ntok, 8), kch = inf.kch;
-        const int buf = k & 1;
-        mbar_wait(&tempty[buf], ((k >> 1) & 1) ^ 1);
+        const int buf = k % kAccBufs;
+        mbar_wait(&tempty[buf], ((k / kAccBufs) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + buf * 128;
         const uint32_t idesc = idesc_bf16(128, max(16, round_up(r, 16)));
@@ -184,17 +229,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
         umma_commit(&tfull[buf]);
         trace_stamp(p.trace, p.trace_items, cta, k, 2);
       }
+      __syncwarp();
     }
   } else {  // ---------------------------- epilogue (warps 2..5)
     const int q = warp & 3, row = q * 32 + lane, etid = threadIdx.x - 64;
     float* partials = reinterpret_cast<float*>(p.ws + p.ws_partials);
-    int* counters = reinterpret_cast<int*>(p.ws + p.ws_counters);
-    RecStream<ShrinkRec> rs(p.plan, p.off_recs, p.off_cta, cta);
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
-    for (int k = 0; rs.pop(inf); ++k) {
-      const int r = inf.rank, nt = inf.ntok, kp16 = max(16, r);
-      const int buf = k & 1;
-      mbar_wait(&tfull[buf], (k >> 1) & 1);
+    const uint8_t* unused;
+    for (int k = 0; rs.pop(inf, unused); ++k) {
+      const int r = inf.rank, nt = inf.ntok, kp = kpad(r), np16 = round_up(nt, 16);
+      const int buf = k % kAccBufs;
+      mbar_wait(&tfull[buf], (k / kAccBufs) & 1);
       tc_fence_after();
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 128;
@@ -213,7 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
               w.y = pack_bf16x2(k0 + 2 < r ? v[h * 8 + 2] : 0.f, k0 + 3 < r ? v[h * 8 + 3] : 0.f);
               w.z = pack_bf16x2(k0 + 4 < r ? v[h * 8 + 4] : 0.f, k0 + 5 < r ? v[h * 8 + 5] : 0.f);
               w.w = pack_bf16x2(k0 + 6 < r ? v[h * 8 + 6] : 0.f, k0 + 7 < r ? v[h * 8 + 7] : 0.f);
-              if (k0 < kp16) *reinterpret_cast<uint4*>(vimg + vimg_off(row, k0, kp16)) = w;
+              if (k0 < kp) *reinterpret_cast<uint4*>(vimg + vimg_off(row, k0, kp, np16)) = w;
             }
           } else {
             float4* dst = reinterpret_cast<float4*>(part + (size_t)row * r + cc);
@@ -226,92 +272,110 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
-      if (inf.nsplit > 1) {
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (etid == 0) *last_flag = (atomicAdd(&counters[inf.counter], 1) == inf.nsplit - 1);
-        named_bar_sync(1, 128);
-        if (*last_flag) {
-          __threadfence();
-          const float* base = partials + inf.part_off;
-          const size_t stride = (size_t)nt * r;
-          // one thread per (token, 8-rank unit), four units in flight per thread; fixed-order sum
-          const int upr = kp16 / 8, units = nt * upr;
-          for (int u0 = etid; u0 < units; u0 += 4 * 128) {
-            float s[4][8];
-#pragma unroll
-            for (int g = 0; g < 4; ++g)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) s[g][e] = 0.f;
-            for (int j = 0; j < inf.nsplit; ++j) {
-              float4 lo[4], hi[4];
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                const int u = u0 + g * 128, t = u / upr, k0 = (u % upr) * 8;
-                if (u < units && k0 < r) {
-                  const float4* src = reinterpret_cast<const float4*>(base + j * stride + (size_t)t * r + k0);
-                  lo[g] = __ldcg(src);
-                  hi[g] = __ldcg(src + 1);
-                } else {
-                  lo[g] = hi[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-              }
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                s[g][0] += lo[g].x; s[g][1] += lo[g].y; s[g][2] += lo[g].z; s[g][3] += lo[g].w;
-                s[g][4] += hi[g].x; s[g][5] += hi[g].y; s[g][6] += hi[g].z; s[g][7] += hi[g].w;
-              }
-            }
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const int u = u0 + g * 128, t = u / upr, k0 = (u % upr) * 8;
-              if (u < units) {
-                uint4 w;
-                w.x = pack_bf16x2(s[g][0], s[g][1]); w.y = pack_bf16x2(s[g][2], s[g][3]);
-                w.z = pack_bf16x2(s[g][4], s[g][5]); w.w = pack_bf16x2(s[g][6], s[g][7]);
-                *reinterpret_cast<uint4*>(vimg + vimg_off(t, k0, kp16)) = w;
-              }
-            }
-          }
-          if (etid == 0) counters[inf.counter] = 0;  // leave the workspace clean for the next call
-        }
-        named_bar_sync(1, 128);
-      }
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
   }
   tc_fence_before();
+  __threadfence();             // partials visible device-wide before the grid barrier
   __syncthreads();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (p.n_red == 0) return;
+
+  // ---- grid-wide split-K reduction (all CTAs are co-resident: grid <= SMs, 1 CTA per SM) ----
+  // Every (token, 8-wide k unit) of every split tile is summed over its splits in fixed split
+  // order by one thread, so results are bit-identical from run to run.
+  int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+  if (threadIdx.x == 0) {
+    atomicAdd(&bar[0], 1);
+    int seen = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(&bar[0]) : "memory");
+      if (seen < (int)gridDim.x) __nanosleep(64);
+    } while (seen < (int)gridDim.x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 4);
+  const MTile* mtiles = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
+  const int32_t* red = p.plan + p.off_red;
+  const float* partials = reinterpret_cast<const float*>(p.ws + p.ws_partials);
+  // CTA c owns units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host recorded the
+  // table entry holding its first unit, so each thread only walks forward a step or two.
+  const int u0 = (int)((int64_t)p.red_units * blockIdx.x / gridDim.x);
+  const int u1 = (int)((int64_t)p.red_units * (blockIdx.x + 1) / gridDim.x);
+  const int e0 = p.plan[p.off_red_cta + blockIdx.x];
+  for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+    int e = e0;
+    while (e + 1 < p.n_red && red[2 * (e + 1) + 1] <= u) ++e;
+    const MTile mt = mtiles[red[2 * e]];
+    const int kp = kpad(mt.rank), upr = kp / 8, v = u - red[2 * e + 1], np16 = round_up(mt.ntok, 16);
+    const int t = v / upr, k0 = (v % upr) * 8;
+    float s8[8];
+#pragma unroll
+    for (int q8 = 0; q8 < 8; ++q8) s8[q8] = 0.f;
+    if (k0 < mt.rank) {
+      const size_t stride = (size_t)mt.ntok * mt.rank;
+      const float* base = partials + mt.part_off + (size_t)t * mt.rank + k0;
+      for (int j = 0; j < mt.nsplit; ++j) {
+        const float4 lo4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride));
+        const float4 hi4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride) + 1);
+        s8[0] += lo4.x; s8[1] += lo4.y; s8[2] += lo4.z; s8[3] += lo4.w;
+        s8[4] += hi4.x; s8[5] += hi4.y; s8[6] += hi4.z; s8[7] += hi4.w;
+      }
+    }
+    uint4 w;
+    w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
+    w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
+    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 5);
+  if (threadIdx.x == 0 && atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) {
+    bar[0] = 0;                // every CTA is past the barrier: re-arm it for the next launch
+    bar[1] = 0;
+  }
 }
 
 // ------------------------------------------------------------------------------------------
-// Expand: per item (m-tile, 128-wide h_out tile) the producer moves B tile + v image (bulk
-// copies) and the item's y rows (TMA, exact row count) into a variable-size byte ring; the
-// epilogue adds D (TMEM) to the prefetched y rows and stores bf16x2 words back to HBM.
+// Expand: per item (m-tile of <=128 tokens, tw-wide h_out tile, tw = 256 or 128):
+//     D[tok x tw] = v[tok x K=kp] . B_s[K x tw]  +  I[tok x K=tok16] . y[K=tok16 x tw]
+// The first MMA group is the LoRA expand (A = v image, K-major swizzled; B = the B tile, MN-major
+// SWIZZLE_128B); the second adds the current y rows on the tensor core: A = a 0/1 identity
+// block, B = the y tile TMA-loaded as an MN-major SWIZZLE_128B operand.  TMEM lane = token,
+// columns = h_out, so the epilogue is LDTM -> cvt.bf16x2 -> 16-byte stores of contiguous row
+// pieces (~0.7 instructions per element), and the ring bytes are released as soon as the MMAs
+// have read them.  The producer warp issues an item's copies from several lanes at once.
+constexpr int kIdentRows = 256;  // identity block at rows [128, 144) of a zero [256 x 16] A tile
+
 __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(ring + kExpandRingBytes + kExpandGuardBytes);  // [kItemQ]
+  uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                    // 8 KB
+  ExpandRecBuf* recbuf = reinterpret_cast<ExpandRecBuf*>(ident + kIdentRows * 16 * 2);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 6);                       // [kItemQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
   uint64_t* empty = full + kItemQ;
   uint64_t* tfull = empty + kItemQ;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kAccBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // The K=16 MMA of a rank-8 adapter reads one 8-wide k-core past its B tile (multiplied by the
-  // zero k-padding of v): zero the ring once so that memory is never NaN.
-  for (int i = threadIdx.x; i < (kExpandRingBytes + kExpandGuardBytes) / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
+  const int tw = p.tw, nb = tw / 64;         // h_out tile width and its 64-column blocks
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
+  const int nbuf = kTmemCols / tw;           // TMEM accumulators in flight
+  // No ring zeroing is needed: B tiles are stored padded to kp rows (zeros past the rank) and
+  // every other over-read (v rows past the tile's tokens) only feeds discarded D rows.
+  // identity A tile, K-major SWIZZLE_32B [256 rows][16 k]: 1.0 at (128 + k, k)
+  for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {
+    const int t = i / 16, k = i % 16;
+    reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
+  }
   fence_proxy_async_smem();
-  // Ring allocations in flight: full[s] = the item's bytes landed (the producer's arrive also
-  // publishes offs[s]), empty[s] = the 4 epilogue warps are done with them.
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 4); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_mbar_init();
-    for (int b = 0; b < 8; ++b) prefetch_tmap(&p.ymap[b]);
+    for (int b = 0; b < 5; ++b) prefetch_tmap(&p.ymap[b]);
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
@@ -319,21 +383,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int cta = blockIdx.x;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
   pdl_wait();                 // v images come from the shrink launch; y from earlier work
   pdl_launch_dependents();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer: byte-ring allocation in list order
-      RecStream<ExpandRec> rs(p.plan, p.off_recs, p.off_cta, cta);
-      ExpandRec inf;
-      uint32_t head = 0, tail = 0;
-      uint32_t vbegin[kItemQ];
-      int retired = 0;
-      for (int k = 0; rs.pop(inf); ++k) {
-        const int kp16 = max(16, inf.rank), np16 = round_up(inf.ntok, 16);
-        const uint32_t bbytes = 128 * inf.rank * 2, vbytes = np16 * kp16 * 2, ybytes = inf.ntok * 256;
-        const uint32_t size = round_up(bbytes, 128) + round_up(vbytes, 128) + round_up(ybytes, 128);
-        if ((head % kExpandRingBytes) + size > kExpandRingBytes)
+  if (warp == 0) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
+    ExpandRec inf;
+    const uint8_t* b;
+    uint32_t head = 0, tail = 0;
+    uint32_t vbegin[kItemQ];
+    int retired = 0;
+    for (int k = 0; rs.pop(inf, b); ++k) {
+      const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
+      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2, ybytes = nb * np16 * 128;
+      const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
+      const uint32_t size = yoff + ybytes;
+      const int qs = k % kItemQ;
+      uint32_t ring_off = 0;
+      if (lane == 0) {
+        // the M=128 MMA reads 128 v rows per K chunk (rows >= ntok only feed discarded D rows):
+        // the item must sit where that read stays inside the ring + guard
+        const uint32_t extent = max(size, voff + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
+        head = round_up(head, 1024);
+        if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
           head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
         trace_stamp(p.trace, p.trace_items, cta, k, 0);
         // retire in FIFO order until an allocation slot and the ring bytes are free
@@ -342,121 +416,118 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
           ++retired;
           tail = retired < k ? vbegin[retired % kItemQ] : head;
         }
-        const int qs = k % kItemQ;
         vbegin[qs] = head;
-        const uint32_t ring_off = head % kExpandRingBytes;
+        ring_off = head % kExpandRingBytes;
         offs[qs] = ring_off;
-        trace_stamp(p.trace, p.trace_items, cta, k, 1);
-        uint8_t* dst = ring + ring_off;
-        const uint8_t* b = static_cast<const uint8_t*>(p.b_ptrs[inf.seg]);
-        mbar_arrive_expect_tx(&full[qs], bbytes + vbytes + ybytes);
-        bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
-        uint8_t* vdst = dst + round_up(bbytes, 128);
-        bulk_load(vdst, p.ws + p.ws_vimg + inf.vimg_off, vbytes, &full[qs]);
-        uint8_t* ydst = vdst + round_up(vbytes, 128);
-        int row = 0;
-        for (int bb = 7; bb >= 0; --bb) {
-          if (inf.ntok - row >= (1 << bb)) {
-            tma_load_2d(ydst + row * 256, &p.ymap[bb], &full[qs], inf.jtile * 128, inf.tok_begin + row);
-            row += 1 << bb;
-          }
-        }
         head += size;
+        const int dbg = p.dbg;
+        mbar_arrive_expect_tx(&full[qs], ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) + ((dbg & 8) ? 0 : ybytes));
+        trace_stamp(p.trace, p.trace_items, cta, k, 1);
       }
+      ring_off = __shfl_sync(0xffffffffu, ring_off, 0);
+      uint8_t* dst = ring + ring_off;
+      const int dbg = p.dbg;
+      if (lane == 0) {
+        if (!(dbg & 16)) bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
+      } else if (lane == 1) {
+        if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg + inf.vimg_off, vbytes, &full[qs]);
+      } else if (!(dbg & 8)) {
+        // y rows [tok_begin, tok_begin + np16) as nb 64-column SWIZZLE_128B blocks; each block is
+        // np16/8 = sum of powers of two 8-row groups -> one TMA box per set bit, one lane per box
+        const int m = np16 >> 3, pc = __popc(m), box = lane - 2;
+        if (box < nb * pc) {
+          const int h = box / pc, i = box % pc;
+          int mm = m, row = 0, bb = -1;
+          for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
+            bb = 31 - __clz(mm);
+            if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
+          }
+          tma_load_2d(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[bb], &full[qs],
+                      inf.jtile * tw + h * 64, inf.tok_begin + row);
+        }
+      }
+      __syncwarp();
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      RecStream<ExpandRec> rs(p.plan, p.off_recs, p.off_cta, cta);
-      ExpandRec inf;
-      for (int k = 0; rs.pop(inf); ++k) {
+  } else if (warp == 1) {  // ---------------- MMA issuer (lane 0)
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[1], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+    ExpandRec inf;
+    const uint8_t* unused;
+    const uint32_t ib = smem_u32(ident);
+    const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
+    for (int k = 0; rs.pop(inf, unused); ++k) {
+      if (lane == 0) {
         const int qs = k % kItemQ;
-        const int r = inf.rank, kp16 = max(16, r), np16 = round_up(inf.ntok, 16);
-        const int buf = k & 1;
-        mbar_wait(&tempty[buf], ((k >> 1) & 1) ^ 1);
+        const int r = inf.rank, kp = kpad(r), np16 = round_up(inf.ntok, 16);
+        const int S = kmajor_row_bytes(kp), ck = S / 2;
+        const uint32_t vlay = umma_layout(S);
+        const int buf = k % nbuf;
+        mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
+        trace_stamp(p.trace, p.trace_items, cta, k, 5);
         mbar_wait(&full[qs], (k / kItemQ) & 1);
+        trace_stamp(p.trace, p.trace_items, cta, k, 6);
         tc_fence_after();
         const uint32_t bb = smem_u32(ring + offs[qs]);
-        const uint32_t vb = bb + round_up(128 * r * 2, 128);
-        const uint32_t idesc = idesc_bf16(128, np16);
-        const uint32_t d = tmem_base + buf * 128;
-        for (int ks = 0; ks < kp16 / 16; ++ks) {
-          const uint64_t adesc = smem_desc(bb + ks * 256, 128, r * 16, 0);
-          const uint64_t bdesc = smem_desc(vb + ks * 256, 128, kp16 * 16, 0);
-          umma_bf16(d, adesc, bdesc, idesc, ks > 0 ? 1u : 0u);
+        const uint32_t voff = round_up(tw * kp * 2, 1024);
+        const uint32_t vb = bb + voff;
+        const uint32_t yb = bb + round_up(voff + np16 * kp * 2, 1024);
+        const uint32_t d = tmem_base + buf * tw;
+        // D = v . B : A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128)
+        const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
+        for (int ks = 0; ks < nv; ++ks) {
+          const int kk = ks * 16;
+          const uint64_t adesc = smem_desc(vb + (kk / ck) * np16 * S + (kk % ck) * 2, 16, 8 * S, vlay);
+          const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
+          umma_bf16(d, adesc, bdesc, idesc_mn, ks > 0 ? 1u : 0u);
         }
+        // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
+        for (int ks = 0; ks < ny; ++ks) {
+          const uint64_t adesc = smem_desc(ib + (128 - 16 * ks) * 32, 16, 256, 6);
+          const uint64_t bdesc = smem_desc(yb + ks * 2048, np16 * 128, 1024, 2);
+          umma_bf16(d, adesc, bdesc, idesc_mn, 1u);
+        }
+        trace_stamp(p.trace, p.trace_items, cta, k, 7);
+        umma_commit(&empty[qs]);   // ring bytes free once these MMAs have read them
         umma_commit(&tfull[buf]);
         trace_stamp(p.trace, p.trace_items, cta, k, 2);
       }
+      __syncwarp();
     }
-  } else {  // ---------------------------- epilogue (warps 2..5)
+  } else {  // ---------------------------- epilogue (warps 2..5): thread = token row
     const int q = warp & 3, etid = threadIdx.x - 64;
-    // Lane pairs (2m, 2m+1) own columns (c, c+1), c = 32q + 2m.  For each token pair (t, t+1)
-    // one shuffle gives the even lane both columns of token t and the odd lane both columns of
-    // token t+1, so every y access is a 32-bit word: LDS from the TMA-prefetched tile, STG of
-    // the updated pair straight to HBM (fire-and-forget).
-    const bool odd = lane & 1;
-    const int c = q * 32 + (lane & ~1);
-    const int64_t ldw = p.ldy >> 1;  // row stride in 32-bit words
-    RecStream<ExpandRec> rs(p.plan, p.off_recs, p.off_cta, cta);
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ExpandRec inf;
-    for (int k = 0; rs.pop(inf); ++k) {
-      const int qs = k % kItemQ;
-      const int nt = inf.ntok, r = inf.rank, kp16 = max(16, r), np16 = round_up(nt, 16);
-      const int buf = k & 1;
-      mbar_wait(&tfull[buf], (k >> 1) & 1);
-      mbar_wait(&full[qs], (k / kItemQ) & 1);  // y rows landed (TMA writes visible)
+    const uint8_t* unused;
+    for (int k = 0; rs.pop(inf, unused); ++k) {
+      const int buf = k % nbuf;
+      mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 128;
-      const uint8_t* ytile = ring + offs[qs] + round_up(128 * r * 2, 128) + round_up(np16 * kp16 * 2, 128);
-      const uint32_t* ysm = reinterpret_cast<const uint32_t*>(ytile) + (c >> 1);
-      uint32_t* yg = reinterpret_cast<uint32_t*>(p.y + (int64_t)inf.tok_begin * p.ldy + inf.jtile * 128 + c);
-      for (int c0 = 0; c0 < nt; c0 += 32) {
-        if (etid == 0 && c0 == 32) trace_stamp(p.trace, p.trace_items, cta, k, 5);
-        float v[32];
-        if (!(p.dbg & 4)) {
-          tmem_ld_32x32b_x16(taddr + c0, v);
-          tmem_ld_32x32b_x16(taddr + c0 + 16, v + 16);
-        } else {
+      const int t = q * 32 + lane;
+      if (q * 32 < inf.ntok) {   // warp-uniform: quadrants past the tile's tokens have no rows
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * tw;
+        const bool valid = t < inf.ntok && !(p.dbg & 1);
+        __nv_bfloat16* yrow = p.y + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy + inf.jtile * tw;
+#pragma unroll 1
+        for (int cc = 0; cc < tw; cc += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cc, r);
+          uint32_t w[16];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] = 0.f;
-        }
-        const int rows = min(32, nt - c0);
-        uint32_t yw[16], out[16];
+          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int tl = 2 * u + (odd ? 1 : 0);
-          yw[u] = ld_shared_b32_if(ysm + (c0 + tl) * 64, tl < rows && !(p.dbg & 2));
-        }
-        // shuffle phase: no control flow, so the warp stays converged without reconvergence code
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const float send = odd ? v[2 * u] : v[2 * u + 1];
-          const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-          const float d0 = odd ? recv : v[2 * u];          // column c
-          const float d1 = odd ? v[2 * u + 1] : recv;      // column c+1
-          out[u] = pack_bf16x2(bf16_lo(yw[u]) + d0, bf16_hi(yw[u]) + d1);
-        }
-        // store phase: branch-free predicated 32-bit stores
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int tl = 2 * u + (odd ? 1 : 0);
-          st_global_b32_if(yg + (int64_t)(c0 + tl) * ldw, out[u], tl < rows && !(p.dbg & 1));
+          for (int u = 0; u < 4; ++u)
+            st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
         }
       }
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 6);
       tc_fence_before();
       __syncwarp();
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 7);
-      if (lane == 0) {
-        mbar_arrive(&tempty[buf]);
-        mbar_arrive(&empty[qs]);  // this warp is done with the item's ring bytes
-      }
+      if (lane == 0) mbar_arrive(&tempty[buf]);
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
 }
 

@@ -34,6 +34,16 @@ class ModelShape:
         """bf16 bytes of one rank unit of an adapter across every layer/projection."""
         return self.layers * sum(2 * (p.h_in + p.h_out) for p in self.projections)
 
+    def adapter_bytes(self, rank: int) -> int:
+        """HBM bytes of one resident adapter in the slab format (B rows padded to 16, include/lsv.h)."""
+        kp = kpad(rank)
+        return self.layers * sum(2 * (rank * p.h_in + kp * p.h_out) for p in self.projections)
+
+
+def kpad(rank: int) -> int:
+    """Rank padded to the 16-wide tensor-core K step (lsv_common.cuh kpad)."""
+    return max(16, (rank + 15) // 16 * 16)
+
 
 def _llama(name: str, hidden: int, inter: int, layers: int, kv_out: int | None = None) -> ModelShape:
     kv = hidden if kv_out is None else kv_out

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import native
-from .shapes import ModelShape
+from .shapes import ModelShape, kpad
 
 
 @dataclass
@@ -46,25 +46,18 @@ class AdapterSlab:
         self.slots: list[SlotInfo] = []
         self.by_id: dict[str, int] = {}
         self._cursor = 0
-        P = len(model.projections)
-        # per (layer, projection): byte offset of A and B inside a slot of rank 1 scaled by rank
-        a_unit = np.zeros((model.layers, P), dtype=np.int64)
-        b_unit = np.zeros((model.layers, P), dtype=np.int64)
-        off = 0
-        for l in range(model.layers):
-            for p, proj in enumerate(model.projections):
-                a_unit[l, p] = off
-                off += 2 * proj.h_in
-                b_unit[l, p] = off
-                off += 2 * proj.h_out
-        self._a_unit, self._b_unit, self._unit_bytes = a_unit, b_unit, off
-        self._a_off_rows: list[np.ndarray] = []
+        self._a_off_rows: list[np.ndarray] = []   # per slot: [layers, projections] byte offsets
         self._b_off_rows: list[np.ndarray] = []
         self._slot_offsets_dev: tuple[torch.Tensor, torch.Tensor] | None = None
 
     # -- allocation --------------------------------------------------------------------
     def slot_bytes(self, rank: int) -> int:
-        return rank * self._unit_bytes
+        return self.model.adapter_bytes(rank)
+
+    @staticmethod
+    def capacity_for(model: ModelShape, ranks) -> int:
+        """Slab bytes for a roster of adapter ranks (with slot alignment)."""
+        return sum(model.adapter_bytes(int(r)) + AdapterSlab.ALIGN for r in ranks) + AdapterSlab.ALIGN
 
     def free_bytes(self) -> int:
         return self.capacity - self._cursor
@@ -82,8 +75,20 @@ class AdapterSlab:
         slot = len(self.slots)
         self.slots.append(SlotInfo(slot, adapter_id, rank, start, nbytes))
         self.by_id[adapter_id] = slot
-        self._a_off_rows.append(start + rank * self._a_unit)
-        self._b_off_rows.append(start + rank * self._b_unit)
+        L, P = self.model.layers, len(self.model.projections)
+        a_off = np.empty((L, P), dtype=np.int64)
+        b_off = np.empty((L, P), dtype=np.int64)
+        cur = start
+        kp = kpad(rank)
+        for l in range(L):
+            for p, pr in enumerate(self.model.projections):
+                a_off[l, p] = cur
+                cur += 2 * rank * pr.h_in
+                b_off[l, p] = cur
+                cur += 2 * kp * pr.h_out
+        assert cur - start == nbytes
+        self._a_off_rows.append(a_off)
+        self._b_off_rows.append(b_off)
         self._cursor = start + nbytes
         self._slot_offsets_dev = None
         return slot

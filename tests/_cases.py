@@ -52,7 +52,7 @@ class Case:
     def run_gpu(self, tier_policy=0, device="cuda:0", repeat=1):
         from paper_2511_22880_b200.lora import LoraDeltaEngine
         from paper_2511_22880_b200.slab import AdapterSlab
-        slab_bytes = sum(r * (2 * self.h_in + 2 * self.h_out) for r in self.ranks) + 1024 * (len(self.ranks) + 1)
+        slab_bytes = AdapterSlab.capacity_for(self.model, self.ranks)
         slab = AdapterSlab(self.model, slab_bytes, device)
         for s, r in enumerate(self.ranks):
             slot = slab.allocate(f"a{s}", r)

@@ -40,7 +40,7 @@ def test_config1_qproj_4_adapters(tier):
         assert summ[5] == 4  # four 64-token tiles on tcgen05
 
 
-@pytest.mark.parametrize("h_in,h_out", [(4096, 11008), (11008, 4096), (5120, 13824), (8192, 1024)])
+@pytest.mark.parametrize("h_in,h_out", [(4096, 11008), (11008, 4096), (5120, 13824), (8192, 1024), (4096, 1152)])
 def test_llama_projection_shapes(h_in, h_out):
     case = Case(h_in, h_out, [41, 7, 130, 64, 1, 256], [128, 8, 32, 16, 64, 8], seed=2)
     _check(case)
@@ -53,6 +53,16 @@ def test_ragged_segments_both_tiers():
     err, bp = _check(case)
     s = bp.shape_plans[(4096, 4096)].summary
     assert s[4] > 0 and s[5] > 0  # both tiers used
+
+
+@pytest.mark.parametrize("tier", [AUTO, TC])
+def test_every_rank_class_on_tensor_cores(tier):
+    """Ranks that are not multiples of 16/32/64 exercise the K padding and each v-image swizzle."""
+    ranks = [8, 16, 24, 32, 40, 48, 56, 64, 72, 96, 112, 128]
+    lengths = [9, 17, 33, 64, 100, 128, 129, 20, 47, 5, 61, 90]
+    case = Case(4096, 1024, lengths, ranks, seed=8)
+    err, bp = _check(case, tier)
+    assert bp.shape_plans[(4096, 1024)].summary[5] >= 10
 
 
 def test_accumulates_into_y_and_leaves_other_rows():
@@ -86,7 +96,8 @@ def test_many_segments_splitk():
 def test_pack_roundtrip():
     from paper_2511_22880_b200.shapes import ModelShape, Projection
     from paper_2511_22880_b200.slab import AdapterSlab
-    model = ModelShape("m", 2, (Projection("p", 4096, 11008), Projection("q", 11008, 4096)))
+    model = ModelShape("m", 2, (Projection("p", 4096, 11008), Projection("q", 11008, 4096),
+                                Projection("o", 1024, 1152)))
     slab = AdapterSlab(model, 64 << 20, "cuda:0")
     g = torch.Generator(device="cuda:0").manual_seed(0)
     for r in (8, 24, 128):

@@ -76,7 +76,8 @@ def test_plan_covers_every_chunk_and_tile(h_in, h_out):
         assert sorted(p[2] for p in parts) == list(range(int(mt[4])))   # split ids 0..nsplit-1
     # every (mtile, h_out tile) appears exactly once in the expand records
     pairs = {(int(r[6]), int(r[4])) for r in d["expand"]}
-    assert len(pairs) == len(d["expand"]) == d["n_mtiles"] * (h_out // 128)
+    tw = 256 if h_out % 256 == 0 else 128
+    assert len(pairs) == len(d["expand"]) == d["n_mtiles"] * (h_out // tw)
     # per-CTA record lists partition the record arrays
     for key in ("shrink_cta", "expand_cta"):
         off = d[key]

@@ -13,7 +13,7 @@ layers = 2
 model = ModelShape("l7b-2l", layers, LLAMA2_7B.projections)
 dev = torch.device("cuda:0")
 ranks = [8]*44+[16]*22+[32]*14+[64]*11+[128]*9
-slab = AdapterSlab(model, sum(r*model.rank_units_bytes()//1 for r in ranks) // 1 + (1<<24), dev)
+slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
 t=time.time()
 for i, r in enumerate(ranks):
     s = slab.allocate(f"a{i}", r); slab.fill_random(s, 1000+i)

@@ -14,7 +14,7 @@ kind = sys.argv[2] if len(sys.argv) > 2 else "expand"
 model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections)
 dev = torch.device("cuda:0")
 ranks = [8]*44+[16]*22+[32]*14+[64]*11+[128]*9
-slab = AdapterSlab(model, sum(r*model.rank_units_bytes() for r in ranks) + (1 << 24), dev)
+slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
 for i, r in enumerate(ranks):
     s = slab.allocate(f"a{i}", r); slab.fill_random(s, 1000+i)
 seg = index_tokens(np.random.default_rng(0).integers(0, 100, 4096), ranks)
