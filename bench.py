@@ -26,6 +26,7 @@ import subprocess
 import sys
 import threading
 import time
+import zlib
 from pathlib import Path
 
 import numpy as np
@@ -43,7 +44,9 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1"), default="c2")
+    ap.add_argument("--config", choices=("c2", "c1", "dp"), default="c2",
+                    help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
+                         "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -198,16 +201,17 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     tier = {"auto": native.TIER_AUTO, "simt": native.TIER_SIMT, "tc": native.TIER_TC}[args.tier]
-    wl = synth.WORKLOADS[args.config]()
+    config = args.config if not (world > 1 and args.config == "c2") else "dp"
+    wl = synth.dp_workloads(world)[rank] if config == "dp" else synth.WORKLOADS[config]()
     model = wl.model
     seg = wl.segments
     N = seg.num_tokens
 
-    # adapters resident in HBM (random-init, seeded per adapter)
+    # adapters resident in this GPU's HBM slab (random-init, seeded per adapter id)
     slab_bytes = AdapterSlab.capacity_for(model, wl.ranks)
     slab = AdapterSlab(model, slab_bytes, dev)
-    for i, (aid, r) in enumerate(zip(wl.adapter_ids, wl.ranks)):
-        slab.fill_random(slab.allocate(aid, r), 1000 + i)
+    for aid, r in zip(wl.adapter_ids, wl.ranks):
+        slab.fill_random(slab.allocate(aid, r), 1000 + zlib.crc32(aid.encode()) % 100000)
     eng = LoraDeltaEngine(slab, tier_policy=tier)
     bp = eng.prepare(seg)
 
@@ -250,11 +254,16 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = ms_local
+    tokens_all = N * world
+    per_rank = [[ms_local, N]]
     if world > 1:
-        t = torch.tensor([ms_local], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    value = N * world / (ms / 1e3)
+        t = torch.tensor([ms_local, float(N)], device=dev)
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(gathered, t)
+        per_rank = [g.tolist() for g in gathered]
+        ms = max(p[0] for p in per_rank)
+        tokens_all = int(sum(p[1] for p in per_rank))
+    value = tokens_all / (ms / 1e3)
 
     # launches per step (our kernels only)
     launches = 0
@@ -266,6 +275,10 @@ def run_ours(args, rank, world, local_rank):
     # ---- algorithmic bytes / flops of the step ----
     step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
     step_flops = sum(algorithmic_flops(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
+    if world > 1:   # whole-job bytes/flops: every rank's own batch
+        t = torch.tensor([float(step_bytes), float(step_flops)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t)
+        step_bytes, step_flops = int(t[0].item()), int(t[1].item())
     hbm_peak, peak_src = peaks()
 
     # ---- dominant kernel roofline: expand (tcgen05) on the largest projection, CUDA events ----
@@ -328,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = N * world / e2e_s
+    e2e_value = tokens_all / e2e_s
 
     # ---- CPU baseline (rank 0, N=1 only): the oracle on one full layer, extrapolated ----
     cpu = None
@@ -351,11 +364,13 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapters, N(0,1) activations)",
-        "config": {"workload": wl.description, "config": args.config, "tier_policy": args.tier,
+        "config": {"workload": wl.description, "config": config, "tier_policy": args.tier,
+                   "per_gpu": [{"ms": p[0], "tokens": int(p[1])} for p in per_rank] if world > 1 else None,
                    "l2": "inputs larger than L2 (per-layer activation buffers; %.1f GB moved per step)" % (step_bytes / 1e9),
                    "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
         "step_hbm": {"algorithmic_bytes": step_bytes, "achieved_GBs": step_bytes / (ms * 1e-3) / 1e9,
-                     "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak, "flops": step_flops},
+                     "frac": step_bytes / (ms * 1e-3) / 1e9 / (hbm_peak * world), "flops": step_flops,
+                     "note": "whole-job algorithmic bytes / step time / (peak x GPUs)"},
         "roofline": {"bound": "hbm", "kernel": f"expand_tc_kernel ({pr.name} {pr.h_in}->{pr.h_out})",
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None, "launch_us": exp_us,
