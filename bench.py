@@ -44,7 +44,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1", "dp"), default="c2",
+    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote"), default="c2",
                     help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
                          "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
@@ -387,6 +387,101 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
+def time_graph(torch, eng, bp, xs, ys, stream, steps, warmup, dev):
+    """CUDA-graph the whole step once, replay warmup + steps, return ms per step (CUDA events)."""
+    with torch.cuda.stream(stream):
+        eng.forward(bp, xs, ys, stream)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        eng.forward(bp, xs, ys, stream)
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / steps
+
+
+def run_remote(args, rank, world, local_rank):
+    """Config 4: 30% of each GPU's tokens hit adapters owned by a peer GPU, read in-kernel over
+    NVLink through CUDA-IPC-mapped peer slabs (no copy, no NCCL).  Reports tokens/s with the
+    remote reads and the overhead against the same batch with every adapter local."""
+    import torch
+    from paper_2511_22880_b200 import synth
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, algorithmic_bytes, input_group
+    from paper_2511_22880_b200.slab import AdapterSlab
+    if world < 2:
+        raise SystemExit("--config remote needs >= 2 ranks (torchrun)")
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    wl, owner = synth.remote_workload(world, rank)
+    model, seg = wl.model, wl.segments
+    N = seg.num_tokens
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, wl.ranks), dev)
+    for aid, r in zip(wl.adapter_ids, wl.ranks):
+        slab.fill_random(slab.allocate(aid, r), 1000 + zlib.crc32(aid.encode()) % 100000)
+    torch.cuda.synchronize(dev)
+    handles = [None] * world
+    torch.distributed.all_gather_object(handles, slab.ipc_handle())
+    roster = list(zip(wl.adapter_ids, wl.ranks))
+    peers = {r: AdapterSlab.open_peer(model, handles[r], roster, dev) for r in range(world) if r != rank}
+    eng = LoraDeltaEngine(slab)
+    bp_local = eng.prepare(seg)
+    bp_remote = eng.prepare(seg, seg_owner=owner, peer_slabs=peers)
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    groups = {}
+    for pr in model.projections:
+        groups.setdefault(input_group(pr.name), pr.h_in)
+    xs = [{k: torch.randn(N, h, device=dev, generator=g).to(torch.bfloat16) for k, h in groups.items()}
+          for _ in range(model.layers)]
+    ys = [{pr.name: torch.randn(N, pr.h_out, device=dev, generator=g).to(torch.bfloat16) for pr in model.projections}
+          for _ in range(model.layers)]
+    # remote reads produce bit-identical deltas (same weights, same math)
+    y_l = torch.zeros(N, model.projections[0].h_out, device=dev, dtype=torch.bfloat16)
+    y_r = torch.zeros_like(y_l)
+    eng.apply(bp_local, 0, 0, xs[0][input_group(model.projections[0].name)], y_l)
+    eng.apply(bp_remote, 0, 0, xs[0][input_group(model.projections[0].name)], y_r)
+    torch.cuda.synchronize(dev)
+    identical = bool(torch.equal(y_l, y_r))
+    stream = torch.cuda.Stream(dev)
+    torch.distributed.barrier()
+    ms_local = time_graph(torch, eng, bp_local, xs, ys, stream, args.steps, args.warmup, dev)
+    torch.distributed.barrier()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    ms_remote = time_graph(torch, eng, bp_remote, xs, ys, stream, args.steps, args.warmup, dev)
+    clocks = sampler.stop()
+    t = torch.tensor([ms_local, ms_remote, float(identical)], device=dev, dtype=torch.float64)
+    per = [torch.zeros_like(t) for _ in range(world)]
+    torch.distributed.all_gather(per, t)
+    per = [p.tolist() for p in per]
+    ms_l = max(p[0] for p in per)
+    ms_r = max(p[1] for p in per)
+    remote_frac = float(np.sum(seg.lengths()[owner != rank])) / N
+    step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
+    hbm_peak, peak_src = peaks()
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": N * world / (ms_r / 1e3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_r, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapters)",
+        "config": {"workload": wl.description, "config": "remote", "remote_token_fraction": remote_frac,
+                   "per_gpu": [{"ms_local": p[0], "ms_remote": p[1], "bit_identical": bool(p[2])} for p in per],
+                   "timing": "CUDA-graph replay, CUDA events, max over ranks"},
+        "remote_overhead": ms_r / ms_l - 1.0,
+        "all_local": {"ms_per_step": ms_l, "value": N * world / (ms_l / 1e3)},
+        "step_hbm": {"frac_local_bytes": step_bytes / (ms_r * 1e-3) / 1e9 / hbm_peak},
+        "clocks": clocks,
+    }
+
+
 def main(argv=None):
     args = parse_args(argv)
     rank = int(os.environ.get("RANK", "0"))
@@ -401,7 +496,8 @@ def main(argv=None):
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line = run_ours(args, rank, world, local_rank)
+    line = run_remote(args, rank, world, local_rank) if args.config == "remote" else \
+        run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -73,6 +73,10 @@ const char* lsv_last_error(void);
 size_t lsv_adapter_a_bytes(int32_t rank, int32_t h_in);
 size_t lsv_adapter_b_bytes(int32_t rank, int32_t h_out);
 
+/* Slab memory: one cudaMalloc on `device` (its base is what lsv_ipc_get_handle exports). */
+int lsv_slab_alloc(size_t bytes, int32_t device, void** dev_ptr_out);
+int lsv_slab_free(void* dev_ptr);
+
 /* Pack PEFT-layout device tensors lora_A [rank][h_in] and lora_B [h_out][rank] (bf16,
  * row-major, contiguous) into the tiled slab buffers a_tiled / b_tiled (device).
  * rank must be a multiple of 8 in [8, 256]; h_in, h_out multiples of 128. */
@@ -132,6 +136,13 @@ int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out,
  * for single-process multi-GPU use: enable direct peer loads from `peer`'s HBM on `dev`.
  * Returns LSV_EUNSUPPORTED if the pair cannot access each other. */
 int lsv_enable_peer(int32_t dev, int32_t peer);
+
+/* Cross-process form of the same: export a device allocation (a cudaMalloc base pointer) as a
+ * 64-byte CUDA IPC handle; open a peer process's handle in `device`'s context (mapping the
+ * peer GPU's HBM into this GPU's address space for direct NVLink loads); close it again. */
+int lsv_ipc_get_handle(void* dev_ptr, void* handle64_out);
+int lsv_ipc_open_handle(const void* handle64, int32_t device, void** dev_ptr_out);
+int lsv_ipc_close_handle(void* dev_ptr);
 
 /* Number of SMs the planner assumes (queried from device 0 once; 148 on B200). */
 int lsv_num_sms(void);

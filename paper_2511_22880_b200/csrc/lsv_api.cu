@@ -581,6 +581,51 @@ int lsv_debug_set_trace(void* buf, int32_t items_per_cta) {
   return LSV_OK;
 }
 
+int lsv_slab_alloc(size_t bytes, int32_t device, void** dev_ptr_out) {
+  if (!dev_ptr_out || bytes == 0) return fail(LSV_EINVAL, "lsv_slab_alloc: bad arguments");
+  int cur = 0;
+  LSV_CUDA_CHECK(cudaGetDevice(&cur));
+  LSV_CUDA_CHECK(cudaSetDevice(device));
+  const cudaError_t e = cudaMalloc(dev_ptr_out, bytes);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(LSV_ECUDA, "cudaMalloc(%zu) on device %d: %s", bytes, device, cudaGetErrorString(e));
+  return LSV_OK;
+}
+
+int lsv_slab_free(void* dev_ptr) {
+  if (!dev_ptr) return LSV_OK;
+  LSV_CUDA_CHECK(cudaFree(dev_ptr));
+  return LSV_OK;
+}
+
+int lsv_ipc_get_handle(void* dev_ptr, void* handle64_out) {
+  if (!dev_ptr || !handle64_out) return fail(LSV_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  LSV_CUDA_CHECK(cudaIpcGetMemHandle(&h, dev_ptr));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64_out, &h, sizeof(h));
+  return LSV_OK;
+}
+
+int lsv_ipc_open_handle(const void* handle64, int32_t device, void** dev_ptr_out) {
+  if (!handle64 || !dev_ptr_out) return fail(LSV_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  int cur = 0;
+  LSV_CUDA_CHECK(cudaGetDevice(&cur));
+  LSV_CUDA_CHECK(cudaSetDevice(device));
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(LSV_ECUDA, "cudaIpcOpenMemHandle on device %d: %s", device, cudaGetErrorString(e));
+  return LSV_OK;
+}
+
+int lsv_ipc_close_handle(void* dev_ptr) {
+  if (!dev_ptr) return fail(LSV_EINVAL, "null pointer");
+  LSV_CUDA_CHECK(cudaIpcCloseMemHandle(dev_ptr));
+  return LSV_OK;
+}
+
 int lsv_enable_peer(int32_t dev, int32_t peer) {
   if (dev == peer) return LSV_OK;
   int can = 0;

@@ -25,7 +25,8 @@ EXPORTED_SYMBOLS = (
     "lsv_version", "lsv_last_error", "lsv_adapter_a_bytes", "lsv_adapter_b_bytes",
     "lsv_pack_adapter", "lsv_unpack_adapter", "lsv_plan_size", "lsv_plan_build",
     "lsv_plan_summary", "lsv_lora_apply", "lsv_lora_shrink", "lsv_lora_expand",
-    "lsv_enable_peer", "lsv_num_sms",
+    "lsv_enable_peer", "lsv_num_sms", "lsv_ipc_get_handle", "lsv_ipc_open_handle", "lsv_ipc_close_handle",
+    "lsv_slab_alloc", "lsv_slab_free",
 )
 
 _lib = None
@@ -48,6 +49,11 @@ _SIGNATURES = {
     "lsv_lora_shrink": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "lsv_lora_expand": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "lsv_enable_peer": (ctypes.c_int, [_i32, _i32]),
+    "lsv_ipc_get_handle": (ctypes.c_int, [_vp, _vp]),
+    "lsv_slab_alloc": (ctypes.c_int, [_sz, _i32, ctypes.POINTER(_vp)]),
+    "lsv_slab_free": (ctypes.c_int, [_vp]),
+    "lsv_ipc_open_handle": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_vp)]),
+    "lsv_ipc_close_handle": (ctypes.c_int, [_vp]),
 }
 
 

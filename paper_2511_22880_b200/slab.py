@@ -13,6 +13,7 @@ GPU's slab (the reference's ``fetch_remote``).
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -37,12 +38,18 @@ class AdapterSlab:
 
     ALIGN = 1024
 
-    def __init__(self, model: ModelShape, capacity_bytes: int, device: torch.device | str):
+    def __init__(self, model: ModelShape, capacity_bytes: int, device: torch.device | str,
+                 _peer_base: int | None = None):
         self.model = model
         self.device = torch.device(device)
         self.capacity = int(capacity_bytes)
-        self.buffer = torch.empty(self.capacity, dtype=torch.uint8, device=self.device)
-        self.base = self.buffer.data_ptr()
+        self._owned = _peer_base is None
+        if self._owned:   # one cudaMalloc owned by liblsv: its base is exactly what IPC exports
+            ptr = ctypes.c_void_p()
+            native.check(native.lib().lsv_slab_alloc(self.capacity, self.device.index or 0, ctypes.byref(ptr)))
+            self.base = int(ptr.value)
+        else:             # a view of another process's slab, mapped over NVLink (open_peer)
+            self.base = int(_peer_base)
         self.slots: list[SlotInfo] = []
         self.by_id: dict[str, int] = {}
         self._cursor = 0
@@ -144,6 +151,44 @@ class AdapterSlab:
                 b = (torch.randn((pr.h_out, info.rank), generator=gen, device=self.device)
                      * (1.0 / math.sqrt(info.rank))).to(torch.bfloat16)
                 self.load(slot, layer, p, a, b)
+
+    # -- NVLink peers (the reference's remote holder, pool.py:101-132) -------------------
+    def ipc_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of the slab allocation, for peers to map it with ``open_peer``."""
+        buf = (ctypes.c_char * 64)()
+        native.check(native.lib().lsv_ipc_get_handle(self.base, ctypes.addressof(buf)))
+        return bytes(buf)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_owned", False) and self.base:
+                native.lib().lsv_slab_free(self.base)
+                self.base = 0
+            else:
+                self.close_peer()
+        except Exception:
+            pass
+
+    @classmethod
+    def open_peer(cls, model: ModelShape, handle, roster: list[tuple[str, int]], device) -> "AdapterSlab":
+        """Map a peer process's slab into this GPU's address space (CUDA IPC opened in this device's
+        context, peer access enabled) so kernels here read it over NVLink.  ``roster`` is the (id,
+        rank) allocation order the owner used, replayed to rebuild the slot offsets; no data moves."""
+        device = torch.device(device)
+        buf = (ctypes.c_char * 64).from_buffer_copy(handle)
+        ptr = ctypes.c_void_p()
+        native.check(native.lib().lsv_ipc_open_handle(ctypes.addressof(buf), device.index, ctypes.byref(ptr)))
+        size = sum(model.adapter_bytes(r) + cls.ALIGN for _, r in roster) + cls.ALIGN
+        view = cls(model, size, device, _peer_base=ptr.value)
+        view._ipc_base = ptr.value
+        for aid, rank in roster:
+            view.allocate(aid, rank)
+        return view
+
+    def close_peer(self) -> None:
+        if getattr(self, "_ipc_base", None):
+            native.check(native.lib().lsv_ipc_close_handle(self._ipc_base))
+            self._ipc_base = None
 
     # -- pointer tables ----------------------------------------------------------------
     def pointer_tables(self, seg_slots: np.ndarray, peer_slabs: dict[int, "AdapterSlab"] | None = None,

@@ -121,3 +121,23 @@ def dp_workloads(num_servers: int, model: shapes.ModelShape = shapes.LLAMA2_7B, 
                          f"{tokens_per_gpu} tokens/GPU from {prompt_len}-token requests"),
             server=srv, resident=resident, placement=asg, routed_tokens=routed[srv]))
     return out
+
+
+def remote_workload(num_gpus: int, rank: int, remote_frac: float = 0.3, n_tokens: int = 4096,
+                    n_adapters: int = 100, seed: int = 0):
+    """Config 4: the C2 roster/model on every GPU; adapter i is owned by GPU i % num_gpus.  The GPU's
+    4096-token batch draws ``remote_frac`` of its tokens from adapters owned by other GPUs (read
+    in-kernel over NVLink) and the rest from its own.  Returns (workload, seg_owner)."""
+    roster = traces.roster(n_adapters)
+    ranks = [a.rank for a in roster]
+    own = [i for i in range(n_adapters) if i % num_gpus == rank]
+    other = [i for i in range(n_adapters) if i % num_gpus != rank] or own
+    rng = random.Random(f"{seed}:remote:{rank}")
+    tok = [(rng.choice(other) if rng.random() < remote_frac else rng.choice(own)) for _ in range(n_tokens)]
+    seg = index_tokens(np.asarray(tok), ranks)
+    owner = np.asarray([int(s) % num_gpus for s in seg.seg_slot], dtype=np.int32)
+    remote_tokens = int(np.sum(seg.lengths()[owner != rank]))
+    wl = Workload(f"remote{num_gpus}_gpu{rank}", shapes.LLAMA2_7B, ranks, [a.id for a in roster], seg,
+                  f"llama-2-7b 32 layers x 7 proj, {n_adapters} adapters owned round-robin by {num_gpus} GPUs; "
+                  f"{n_tokens} tokens/GPU, {remote_tokens / n_tokens:.0%} on peer-owned adapters (NVLink loads)")
+    return wl, owner
