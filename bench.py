@@ -44,11 +44,13 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote"), default="c2",
+    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote", "tp"), default="c2",
                     help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
                          "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp-adapters", type=int, default=0,
+                    help="config tp: roster size (default 1000 at TP8, scaled by TP/8 below that to fit HBM)")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args(argv)
 
@@ -482,6 +484,100 @@ def run_remote(args, rank, world, local_rank):
     }
 
 
+def run_tp(args, rank, world, local_rank):
+    """Config 5: Llama-3-70B shapes tensor-parallel over the ranks (TP = world size); column-parallel
+    projections all-gather the rank-sharded shrink output with NCCL, row-parallel ones all-reduce
+    it.  value = tokens/s of the TP group (one batch over all ranks); the NCCL share is reported."""
+    import torch
+    from paper_2511_22880_b200 import shapes, traces
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.tp import TPLoraDeltaEngine, TPSlab
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    model = shapes.LLAMA3_70B
+    n_ad = args.tp_adapters or max(50, 1000 * world // 8)
+    roster = traces.roster(n_ad)
+    ranks = [a.rank for a in roster]
+    rng = np.random.default_rng(0)
+    tok = rng.integers(0, n_ad, 4096)
+    seg = index_tokens(tok, ranks)
+    slab = TPSlab(model, world, rank, ranks, dev)
+    for s_, r in enumerate(ranks):
+        slab.fill_random_shards(s_, 1000 + s_)
+    eng = TPLoraDeltaEngine(slab)
+    st = eng.prepare(seg)
+    N = seg.num_tokens
+    g = torch.Generator(device=dev).manual_seed(7)
+    xs, ys = [], []
+    for _ in range(model.layers):
+        xd, yd = {}, {}
+        for sp in eng.specs:
+            grp = sp.name if sp.name in ("o_proj", "down_proj") else \
+                ("attn_in" if sp.name in ("q_proj", "k_proj", "v_proj") else "mlp_in")
+            if grp not in xd:
+                xd[grp] = torch.randn(N, sp.h_in, device=dev, generator=g).to(torch.bfloat16)
+            yd[sp.name] = torch.zeros(N, sp.h_out, device=dev, dtype=torch.bfloat16)
+        xs.append(xd)
+        ys.append(yd)
+    from paper_2511_22880_b200.lora import INPUT_GROUPS
+    INPUT_GROUPS.update({"o_proj": "o_proj", "down_proj": "down_proj"})
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize(dev)
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            eng.forward(st, xs, ys, stream)
+    torch.cuda.synchronize(dev)
+    torch.distributed.barrier()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.forward(st, xs, ys, stream)
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    # NCCL share: the same number of collectives on the same v regions, alone
+    import torch.distributed as dist
+    coll = []
+    for p, sp in enumerate(eng.specs):
+        plan_a = st["plans"][p][0]
+        off, nb = eng._region(plan_a)
+        coll.append((sp.column, off, nb))
+    torch.cuda.synchronize(dev)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ws_a = st["ws"][0]
+    with torch.cuda.stream(stream):
+        c0.record(stream)
+        for _ in range(model.layers):
+            for col, off, nb in coll:
+                if col:
+                    dist.all_gather_into_tensor(st["gathered"][:world * nb], ws_a[off:off + nb])
+                else:
+                    dist.all_reduce(ws_a[off:off + nb].view(torch.bfloat16))
+        c1.record(stream)
+    torch.cuda.synchronize(dev)
+    coll_ms = c0.elapsed_time(c1)
+    t = torch.tensor([ms, coll_ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, coll_ms = t.tolist()
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": N / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapter shards)",
+        "config": {"workload": f"llama-3-70b 80 layers x 7 proj, TP{world} (S-LoRA sharding), {n_ad} adapters "
+                               f"{traces.assign_power_law_counts(n_ad, traces.DEFAULT_RANKS, 1.0)}, {N} tokens, "
+                               f"{seg.num_segments} active", "config": "tp",
+                   "timing": "eager launches incl. NCCL collectives, CUDA events, max over ranks"},
+        "nccl_ms_per_step": coll_ms, "nccl_share": coll_ms / ms,
+        "clocks": clocks,
+    }
+
+
 def main(argv=None):
     args = parse_args(argv)
     rank = int(os.environ.get("RANK", "0"))
@@ -492,16 +588,26 @@ def main(argv=None):
         if line is not None:
             print(json.dumps(line), flush=True)
         return 0
-    if world > 1:
+    if world > 1 or args.config == "tp":
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line = run_remote(args, rank, world, local_rank) if args.config == "remote" else \
-        run_ours(args, rank, world, local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            torch.distributed.init_process_group("nccl", rank=0, world_size=1,
+                                                 device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.config == "remote":
+        line = run_remote(args, rank, world, local_rank)
+    elif args.config == "tp":
+        line = run_tp(args, rank, world, local_rank)
+    else:
+        line = run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch
+    import torch
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0

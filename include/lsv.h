@@ -79,7 +79,9 @@ int lsv_slab_free(void* dev_ptr);
 
 /* Pack PEFT-layout device tensors lora_A [rank][h_in] and lora_B [h_out][rank] (bf16,
  * row-major, contiguous) into the tiled slab buffers a_tiled / b_tiled (device).
- * rank must be a multiple of 8 in [8, 256]; h_in, h_out multiples of 128. */
+ * rank must be a multiple of 8 in [8, 256]; h_in, h_out multiples of 128.  Passing null for
+ * both pointers of one half packs only the other (tensor-parallel shards keep A and B at
+ * different ranks). */
 int lsv_pack_adapter(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in,
                      int32_t h_out, void* a_tiled, void* b_tiled, lsv_stream_t stream);
 
@@ -130,6 +132,20 @@ int lsv_lora_shrink(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in
 int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out,
                     const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
                     void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* ---- tensor parallelism -------------------------------------------------------------------
+ * Column-parallel projections shard each adapter's rank over the TP group: rank t's shrink
+ * (plan built with the shard ranks) writes v images of K = rank/tp; after an NCCL all-gather of
+ * those workspace images into `gathered` ([tp][shard_region_bytes]), this rebuilds the full-rank
+ * v images the expand (plan built with the full ranks) reads.  Both plans must index the same
+ * segments.  region_bytes = the shard plan's workspace v-image region size
+ * (lsv_plan_vimg_region). */
+int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, const void* shard_plan_dev,
+                      const void* shard_plan_host, const void* full_plan_dev, const void* full_plan_host,
+                      void* full_workspace, lsv_stream_t stream);
+
+/* Byte offset and size of a plan's v-image region inside its workspace (what TP exchanges). */
+int lsv_plan_vimg_region(const void* plan_host, size_t* offset, size_t* bytes);
 
 /* ---- NVLink peers ----------------------------------------------------------------------
  * Replaces the reference's GPUDirect-RDMA remote fetch (pool.py:101-132, costmodel.py:139-140)

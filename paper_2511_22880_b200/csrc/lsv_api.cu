@@ -467,14 +467,16 @@ static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int
   if (rank < 8 || rank > 256 || rank % 8) return fail(LSV_EINVAL, "rank must be a multiple of 8 in [8, 256], got %d", rank);
   if (h_in <= 0 || h_in % 128 || h_out <= 0 || h_out % 128)
     return fail(LSV_EINVAL, "h_in/h_out must be positive multiples of 128 (got %d, %d)", h_in, h_out);
-  if (!lora_a || !lora_b || !a_tiled || !b_tiled) return fail(LSV_EINVAL, "null buffer");
-  if (!aligned16(lora_a) || !aligned16(lora_b) || !aligned16(a_tiled) || !aligned16(b_tiled))
+  const bool do_a = lora_a || a_tiled, do_b = lora_b || b_tiled;   // either half may be skipped
+  if ((do_a && !(lora_a && a_tiled)) || (do_b && !(lora_b && b_tiled)) || !(do_a || do_b))
+    return fail(LSV_EINVAL, "null buffer");
+  if ((do_a && (!aligned16(lora_a) || !aligned16(a_tiled))) || (do_b && (!aligned16(lora_b) || !aligned16(b_tiled))))
     return fail(LSV_EINVAL, "buffers must be 16-byte aligned");
-  const int64_t units = ((int64_t)rank * h_in + (int64_t)h_out * kpad(rank)) / 8;
+  const int64_t units = ((do_a ? (int64_t)rank * h_in : 0) + (do_b ? (int64_t)h_out * kpad(rank) : 0)) / 8;
   const int blocks = (int)std::min<int64_t>(4096, (units + 255) / 256);
   pack_adapter_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(lora_a), static_cast<const uint8_t*>(lora_b), rank, h_in, h_out,
-      static_cast<uint8_t*>(a_tiled), static_cast<uint8_t*>(b_tiled), unpack);
+      static_cast<const uint8_t*>(lora_a), static_cast<const uint8_t*>(lora_b), rank, do_a ? h_in : 0,
+      do_b ? h_out : 0, static_cast<uint8_t*>(a_tiled), static_cast<uint8_t*>(b_tiled), unpack);
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
@@ -595,6 +597,35 @@ int lsv_slab_alloc(size_t bytes, int32_t device, void** dev_ptr_out) {
 int lsv_slab_free(void* dev_ptr) {
   if (!dev_ptr) return LSV_OK;
   LSV_CUDA_CHECK(cudaFree(dev_ptr));
+  return LSV_OK;
+}
+
+int lsv_plan_vimg_region(const void* plan_host, size_t* offset, size_t* bytes) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (!h || !offset || !bytes) return fail(LSV_EINVAL, "not a liblsv plan");
+  *offset = (size_t)h->ws_vimg;
+  *bytes = (size_t)(h->ws_simt_v - h->ws_vimg);
+  return LSV_OK;
+}
+
+int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, const void* shard_plan_dev,
+                      const void* shard_plan_host, const void* full_plan_dev, const void* full_plan_host,
+                      void* full_workspace, lsv_stream_t stream) {
+  const PlanHeader* hs = check_plan(shard_plan_host);
+  const PlanHeader* hf = check_plan(full_plan_host);
+  if (!hs || !hf || !shard_plan_dev || !full_plan_dev) return fail(LSV_EINVAL, "not a liblsv plan");
+  if (hs->n_mtiles != hf->n_mtiles || hs->num_tokens != hf->num_tokens)
+    return fail(LSV_EINVAL, "shard and full plans index different tiles (%d vs %d)", hs->n_mtiles, hf->n_mtiles);
+  if (tp < 1 || !gathered || !full_workspace) return fail(LSV_EINVAL, "bad arguments");
+  if (hs->n_simt_items != 0 || hf->n_simt_items != 0)
+    return fail(LSV_EUNSUPPORTED, "TP assembly needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
+  if (hf->n_mtiles == 0) return LSV_OK;
+  const int32_t* sp = static_cast<const int32_t*>(shard_plan_dev);
+  const int32_t* fp = static_cast<const int32_t*>(full_plan_dev);
+  vimg_assemble_kernel<<<hf->n_mtiles, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(gathered), region_bytes, tp, sp, hs->off_mtiles, 0, fp, hf->off_mtiles,
+      static_cast<uint8_t*>(full_workspace), hf->ws_vimg);
+  LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
 

@@ -113,6 +113,30 @@ __global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restri
   }
 }
 
+// ---- tensor-parallel v assembly -------------------------------------------------------------
+// grid = n_mtiles; one thread per (token, 8-wide k unit) of the full-rank image.  Shard t of a
+// tile's rank holds k in [t*rs, (t+1)*rs); rs is a multiple of 8 so a unit never straddles shards.
+__global__ void __launch_bounds__(256) vimg_assemble_kernel(const uint8_t* __restrict__ gathered, size_t region,
+                                                            int tp, const int32_t* __restrict__ splan,
+                                                            int s_off_mtiles, int s_ws_vimg,
+                                                            const int32_t* __restrict__ fplan, int f_off_mtiles,
+                                                            uint8_t* __restrict__ fws, int f_ws_vimg) {
+  const MTile ms = reinterpret_cast<const MTile*>(splan + s_off_mtiles)[blockIdx.x];
+  const MTile mf = reinterpret_cast<const MTile*>(fplan + f_off_mtiles)[blockIdx.x];
+  const int rs = ms.rank, kps = kpad(rs), kpf = kpad(mf.rank), np16 = round_up(mf.ntok, 16);
+  const int upr = kpf / 8, units = mf.ntok * upr;
+  for (int u = threadIdx.x; u < units; u += blockDim.x) {
+    const int t = u / upr, k0 = (u % upr) * 8;
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (k0 < tp * rs) {
+      const int sh = k0 / rs, kk = k0 % rs;
+      const uint8_t* src = gathered + (size_t)sh * region + (ms.vimg_off) + vimg_off(t, kk, kps, np16);
+      w = *reinterpret_cast<const uint4*>(src);
+    }
+    *reinterpret_cast<uint4*>(fws + f_ws_vimg + mf.vimg_off + vimg_off(t, k0, kpf, np16)) = w;
+  }
+}
+
 // ---- adapter slab packing ---------------------------------------------------------------
 // lora_a [rank][h_in] -> A tiled; lora_b [h_out][rank] -> B tiled.  One thread per 16 bytes of
 // the tiled buffers.

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "lsv_pack_adapter", "lsv_unpack_adapter", "lsv_plan_size", "lsv_plan_build",
     "lsv_plan_summary", "lsv_lora_apply", "lsv_lora_shrink", "lsv_lora_expand",
     "lsv_enable_peer", "lsv_num_sms", "lsv_ipc_get_handle", "lsv_ipc_open_handle", "lsv_ipc_close_handle",
-    "lsv_slab_alloc", "lsv_slab_free",
+    "lsv_slab_alloc", "lsv_slab_free", "lsv_vimg_assemble", "lsv_plan_vimg_region",
 )
 
 _lib = None
@@ -52,6 +52,8 @@ _SIGNATURES = {
     "lsv_ipc_get_handle": (ctypes.c_int, [_vp, _vp]),
     "lsv_slab_alloc": (ctypes.c_int, [_sz, _i32, ctypes.POINTER(_vp)]),
     "lsv_slab_free": (ctypes.c_int, [_vp]),
+    "lsv_vimg_assemble": (ctypes.c_int, [_vp, _sz, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "lsv_plan_vimg_region": (ctypes.c_int, [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
     "lsv_ipc_open_handle": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_vp)]),
     "lsv_ipc_close_handle": (ctypes.c_int, [_vp]),
 }
