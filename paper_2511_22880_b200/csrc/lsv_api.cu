@@ -27,6 +27,7 @@ namespace {
 thread_local char g_err[512] = "";
 uint64_t* g_trace = nullptr;  // debug timeline buffer (lsv_debug_set_trace)
 int g_trace_items = 0;
+int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
 int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
@@ -415,6 +416,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
     p.off_red_cta = h->off_red_cta;
     p.grid_bar = h->n_counters;
+    p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
     LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p));
   }

@@ -39,6 +39,7 @@ struct alignas(64) ShrinkParams {
   int off_mtiles, off_red, n_red, red_units, grid_bar, off_red_cta;   // grid-wide split-K reduction
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
+  int dbg;                      // debug ablations (0 in production)
 };
 
 struct alignas(64) ExpandParams {
@@ -173,13 +174,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
         const int kc = min(kch, inf.chunk_end - g);
         if (lane == 0) {
           mbar_wait(&empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (np8 + r) * 128));
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : r)) * 128));
         }
         __syncwarp();
         uint8_t* dst = ring + slot * kShrinkSlotBytes;
         if (lane == 0) {
-          bulk_load(dst + kc * np8 * 128, a + (size_t)g * r * 128, (uint32_t)(kc * r * 128), &full[slot]);
-        } else if (lane - 1 < kc * pc) {
+          if (!(p.dbg & 2))
+            bulk_load(dst + kc * np8 * 128, a + (size_t)g * r * 128, (uint32_t)(kc * r * 128), &full[slot]);
+        } else if (!(p.dbg & 4) && lane - 1 < kc * pc) {
           const int c = (lane - 1) / pc, i = (lane - 1) % pc;
           int mm = m, row = 0, bb = -1;
           for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
@@ -194,42 +196,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
       __syncwarp();
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer (lane 0)
+  } else if (warp == 1) {  // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+    // values stay in uniform registers, so each MMA costs a few uniform adds), one lane issues
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[1], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
     const uint8_t* unused;
     int slot = 0; uint32_t phase = 0;
+    int dbg_stage = 0;
+    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
     for (int k = 0; rs.pop(inf, unused); ++k) {
-      if (lane == 0) {
-        const int r = inf.rank, np8 = round_up(inf.ntok, 8), kch = inf.kch;
-        const int buf = k % kAccBufs;
-        mbar_wait(&tempty[buf], ((k / kAccBufs) & 1) ^ 1);
+      const int r = __shfl_sync(0xffffffffu, inf.rank, 0);
+      const int np8 = round_up(__shfl_sync(0xffffffffu, inf.ntok, 0), 8);
+      const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
+      const int cb = __shfl_sync(0xffffffffu, inf.chunk_begin, 0), ce = __shfl_sync(0xffffffffu, inf.chunk_end, 0);
+      const int buf = k % kAccBufs;
+      mbar_wait(&tempty[buf], ((k / kAccBufs) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + buf * 128;
+      const uint32_t idesc = idesc_bf16(128, max(16, round_up(r, 16)));
+      const uint32_t xstep = (uint32_t)(np8 * 128) >> 4, astep = (uint32_t)(r * 128) >> 4;  // per chunk, desc units
+      uint32_t accumulate = 0;
+      for (int g = cb; g < ce; g += kch) {
+        const int kc = min(kch, ce - g);
+        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage, 6);
+        mbar_wait(&full[slot], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + buf * 128;
-        const uint32_t idesc = idesc_bf16(128, max(16, round_up(r, 16)));
-        uint32_t accumulate = 0;
-        for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
-          const int kc = min(kch, inf.chunk_end - g);
-          mbar_wait(&full[slot], phase);
-          tc_fence_after();
-          const uint32_t xb = smem_u32(ring + slot * kShrinkSlotBytes);
-          const uint32_t ab = xb + kc * np8 * 128;
-          for (int c = 0; c < kc; ++c) {
+        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage++, 7);
+        const uint32_t xb = ring_base + slot * kShrinkSlotBytes;
+        uint64_t adesc = smem_desc(xb, 16, 1024, 2);
+        uint64_t bdesc = smem_desc(xb + kc * np8 * 128, 16, 1024, 2);
+        for (int c = 0; c < kc; ++c) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t adesc = smem_desc(xb + c * np8 * 128 + kk * 32, 16, 1024, 2);
-              const uint64_t bdesc = smem_desc(ab + c * r * 128 + kk * 32, 16, 1024, 2);
-              umma_bf16(d, adesc, bdesc, idesc, accumulate);
-              accumulate = 1;
-            }
+          for (int kk = 0; kk < 4; ++kk) {   // K=16 steps inside the 128-byte swizzle row: +32 B = +2
+            umma_bf16_elect(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
+            accumulate = 1;
           }
-          umma_commit(&empty[slot]);
-          if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
+          adesc += xstep;
+          bdesc += astep;
         }
-        umma_commit(&tfull[buf]);
-        trace_stamp(p.trace, p.trace_items, cta, k, 2);
+        umma_commit_elect(&empty[slot]);
+        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
-      __syncwarp();
+      umma_commit_elect(&tfull[buf]);
+      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
     }
   } else {  // ---------------------------- epilogue (warps 2..5)
     const int q = warp & 3, row = q * 32 + lane, etid = threadIdx.x - 64;
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       tc_fence_after();
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 128;
-      const bool valid = row < nt;
+      const bool valid = row < nt && !(p.dbg & 8);
       uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;
       float* part = partials + inf.part_off + (size_t)inf.split * nt * r;
       for (int cc = 0; cc < r; cc += 16) {
