@@ -196,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2511_22880_b200 import native, synth
     from paper_2511_22880_b200.lora import (LoraDeltaEngine, algorithmic_bytes, algorithmic_flops,
-                                            input_group)
+                                            input_group, moved_bytes)
     from paper_2511_22880_b200.segments import index_tokens
     from paper_2511_22880_b200.slab import AdapterSlab
 
@@ -268,19 +268,18 @@ def run_ours(args, rank, world, local_rank):
     value = tokens_all / (ms / 1e3)
 
     # launches per step (our kernels only)
-    launches = 0
-    for (h_in, h_out), sp in bp.shape_plans.items():
-        per = (1 if sp.summary[6] else 0) + (1 if sp.summary[7] else 0) + (2 if sp.summary[4] else 0)
-        launches += per * sum(1 for pr in model.projections if (pr.h_in, pr.h_out) == (h_in, h_out))
-    launches *= model.layers
+    launches = eng.launches_per_step(bp)
 
     # ---- algorithmic bytes / flops of the step ----
+    # algorithmic: SURVEY §8d per projection (x counted once per projection); moved: what the
+    # input-group path actually has to move (x once per group: q/k/v and gate/up share it)
     step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
+    step_moved = moved_bytes(seg, model) * model.layers
     step_flops = sum(algorithmic_flops(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
     if world > 1:   # whole-job bytes/flops: every rank's own batch
-        t = torch.tensor([float(step_bytes), float(step_flops)], dtype=torch.float64, device=dev)
+        t = torch.tensor([float(step_bytes), float(step_flops), float(step_moved)], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t)
-        step_bytes, step_flops = int(t[0].item()), int(t[1].item())
+        step_bytes, step_flops, step_moved = int(t[0].item()), int(t[1].item()), int(t[2].item())
     hbm_peak, peak_src = peaks()
 
     # ---- dominant kernel roofline: expand (tcgen05) on the largest projection, CUDA events ----
@@ -289,7 +288,8 @@ def run_ours(args, rank, world, local_rank):
     n_l = seg.lengths().astype(np.int64)
     r_l = seg.seg_rank.astype(np.int64)
     exp_bytes = int(np.sum(2 * r_l * pr.h_out + 4 * n_l * pr.h_out))
-    shr_bytes = int(np.sum(2 * n_l * pr.h_in + 2 * r_l * pr.h_in))
+    n_members = len(next(m for _, m in model.groups() if big in m))   # the fused shrink covers the group
+    shr_bytes = int(np.sum(2 * n_l * pr.h_in + 2 * n_members * r_l * pr.h_in))
     reps = 20
     with torch.cuda.stream(stream):
         eng.shrink(bp, 0, big, xs[0][input_group(pr.name)], stream)
@@ -336,8 +336,8 @@ def run_ours(args, rank, world, local_rank):
         if i >= args.warmup:
             e2e_times.append(dt)
         if i == 0:
-            plan_bytes = sum(sp.plan_host.nbytes for sp in bp_i.shape_plans.values()) + \
-                bp_i.a_ptrs.numel() * 8 * 2
+            plan_bytes = sum(sp.plan_host.nbytes for sp in bp_i.group_plans) + \
+                (bp_i.a_ptrs.numel() + bp_i.b_ptrs.numel()) * 8
     e2e_s = statistics.median(e2e_times)
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
@@ -372,12 +372,15 @@ def run_ours(args, rank, world, local_rank):
                    "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
         "step_hbm": {"algorithmic_bytes": step_bytes, "achieved_GBs": step_bytes / (ms * 1e-3) / 1e9,
                      "frac": step_bytes / (ms * 1e-3) / 1e9 / (hbm_peak * world), "flops": step_flops,
-                     "note": "whole-job algorithmic bytes / step time / (peak x GPUs)"},
+                     "moved_bytes": step_moved, "moved_frac": step_moved / (ms * 1e-3) / 1e9 / (hbm_peak * world),
+                     "note": "whole-job algorithmic bytes (SURVEY 8d, x per projection) / step time / (peak x GPUs); "
+                             "moved: x once per input group (q/k/v, gate/up share one fused shrink)"},
         "roofline": {"bound": "hbm", "kernel": f"expand_tc_kernel ({pr.name} {pr.h_in}->{pr.h_out})",
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None, "launch_us": exp_us,
                      "algorithmic_bytes_per_launch": exp_bytes,
-                     "shrink": {"launch_us": shr_us, "algorithmic_bytes_per_launch": shr_bytes,
+                     "shrink": {"kernel": f"shrink_tc_kernel (fused {n_members}-projection group of {pr.name})",
+                                "launch_us": shr_us, "algorithmic_bytes_per_launch": shr_bytes,
                                 "achieved": shr_bytes / (shr_us * 1e-6) / 1e9}},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d_bytes + plan_bytes,
@@ -492,6 +495,7 @@ def run_tp(args, rank, world, local_rank):
     from paper_2511_22880_b200 import shapes, traces
     from paper_2511_22880_b200.segments import index_tokens
     from paper_2511_22880_b200.tp import TPLoraDeltaEngine, TPSlab
+    from paper_2511_22880_b200.lora import input_group
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     model = shapes.LLAMA3_70B
@@ -512,15 +516,12 @@ def run_tp(args, rank, world, local_rank):
     for _ in range(model.layers):
         xd, yd = {}, {}
         for sp in eng.specs:
-            grp = sp.name if sp.name in ("o_proj", "down_proj") else \
-                ("attn_in" if sp.name in ("q_proj", "k_proj", "v_proj") else "mlp_in")
+            grp = input_group(sp.name)
             if grp not in xd:
                 xd[grp] = torch.randn(N, sp.h_in, device=dev, generator=g).to(torch.bfloat16)
             yd[sp.name] = torch.zeros(N, sp.h_out, device=dev, dtype=torch.bfloat16)
         xs.append(xd)
         ys.append(yd)
-    from paper_2511_22880_b200.lora import INPUT_GROUPS
-    INPUT_GROUPS.update({"o_proj": "o_proj", "down_proj": "down_proj"})
     stream = torch.cuda.Stream(dev)
     torch.cuda.synchronize(dev)
     for _ in range(args.warmup):

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define LSV_ABI_VERSION 1
+#define LSV_ABI_VERSION 2
 
 #define LSV_OK 0
 #define LSV_EINVAL 1
@@ -89,6 +89,18 @@ int lsv_pack_adapter(const void* lora_a, const void* lora_b, int32_t rank, int32
 int lsv_unpack_adapter(const void* a_tiled, const void* b_tiled, int32_t rank, int32_t h_in,
                        int32_t h_out, void* lora_a, void* lora_b, lsv_stream_t stream);
 
+/* Input groups.  Projections that read the same activation (q/k/v of attention, gate/up of the
+ * MLP; all with the same h_in and, for one adapter, the same rank) keep their A matrices in one
+ * group tile of num_proj*rank rows per 64-column chunk, so one shrink reads x once for all of them
+ * (lsv_plan_build_group).  Member `proj` occupies rows [proj*rank, (proj+1)*rank).  B stays per
+ * projection (lsv_pack_adapter with lora_a = a_tiled = NULL).  num_proj = 1 is exactly the
+ * lsv_pack_adapter A layout. */
+size_t lsv_adapter_a_group_bytes(int32_t num_proj, int32_t rank, int32_t h_in);
+int lsv_pack_adapter_group(const void* lora_a, int32_t num_proj, int32_t proj, int32_t rank,
+                           int32_t h_in, void* a_group_tiled, lsv_stream_t stream);
+int lsv_unpack_adapter_group(const void* a_group_tiled, int32_t num_proj, int32_t proj, int32_t rank,
+                             int32_t h_in, void* lora_a, lsv_stream_t stream);
+
 /* ---- plan ------------------------------------------------------------------------------
  * Host-side work planning for one (batch, projection shape).  seg_indptr [S+1] and
  * seg_rank [S] are HOST arrays (the segment indexer's output); seg_indptr[0] must be 0,
@@ -103,6 +115,17 @@ int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t
 int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
                    int32_t h_in, int32_t h_out, int32_t tier_policy, void* plan_host,
                    size_t plan_bytes);
+
+/* Plan for an input group: num_proj projections with output widths h_outs[0..num_proj) that share
+ * x.  lsv_lora_shrink with this plan (a_ptrs = the segments' group A tiles) writes the v images of
+ * every member; lsv_lora_expand_proj(proj) then applies member proj.  lsv_plan_build is the
+ * num_proj = 1 case. */
+int lsv_plan_size_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                        int32_t h_in, int32_t num_proj, const int32_t* h_outs, int32_t tier_policy,
+                        size_t* plan_bytes, size_t* workspace_bytes);
+int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                         int32_t h_in, int32_t num_proj, const int32_t* h_outs, int32_t tier_policy,
+                         void* plan_host, size_t plan_bytes);
 
 /* Fill out[0..7] from a host plan: {num_segments, num_tokens, h_in, h_out,
  * n_simt_segments, n_tc_mtiles, n_shrink_items, n_expand_items}. */
@@ -132,6 +155,11 @@ int lsv_lora_shrink(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in
 int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out,
                     const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
                     void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* Expand of member `proj` of a group plan (lsv_lora_expand is proj = 0). */
+int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,
+                         const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                         void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
 /* ---- tensor parallelism -------------------------------------------------------------------
  * Column-parallel projections shard each adapter's rank over the TP group: rank t's shrink

@@ -76,8 +76,8 @@ struct PlanBuilder {
   std::vector<MTile> mtiles;
   std::vector<ShrinkRec> shrink;     // grouped per CTA
   std::vector<int32_t> shrink_cta;   // [grid+1]
-  std::vector<ExpandRec> expand;
-  std::vector<int32_t> expand_cta;
+  std::vector<ExpandRec> expand[kMaxProj];
+  std::vector<int32_t> expand_cta[kMaxProj];
   std::vector<int32_t> red;          // {mtile, first unit} per split tile
   int32_t red_units = 0;
   std::vector<int32_t> red_cta;
@@ -109,11 +109,16 @@ void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, st
   cta_off[grid] = (int32_t)out.size();
 }
 
-int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t h_out) {
+int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
+                      const int32_t* h_outs) {
   if (S < 0) return fail(LSV_EINVAL, "num_segments must be >= 0, got %d", S);
   if (S > 0 && (!indptr || !rank)) return fail(LSV_EINVAL, "seg_indptr/seg_rank must be non-null");
   if (h_in <= 0 || h_in % 128) return fail(LSV_EINVAL, "h_in must be a positive multiple of 128, got %d", h_in);
-  if (h_out <= 0 || h_out % 128) return fail(LSV_EINVAL, "h_out must be a positive multiple of 128, got %d", h_out);
+  if (P < 1 || P > kMaxProj) return fail(LSV_EINVAL, "num_proj must be in [1, %d], got %d", kMaxProj, P);
+  if (!h_outs) return fail(LSV_EINVAL, "h_outs must be non-null");
+  for (int p = 0; p < P; ++p)
+    if (h_outs[p] <= 0 || h_outs[p] % 128)
+      return fail(LSV_EINVAL, "h_out must be a positive multiple of 128, got %d", h_outs[p]);
   if (S > 0 && indptr[0] != 0) return fail(LSV_EINVAL, "seg_indptr[0] must be 0, got %d", indptr[0]);
   for (int s = 0; s < S; ++s) {
     if (indptr[s + 1] < indptr[s])
@@ -124,9 +129,13 @@ int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int
   return LSV_OK;
 }
 
-int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t h_out,
-               int32_t policy) {
-  if (int rc = validate_segments(S, indptr, rank, h_in, h_out)) return rc;
+// Projections [p0, p0+np) of one record: the widest prefix whose rows (np*rank) fit one
+// M=128 tcgen05 MMA (N <= 256).
+int subset_np(int P, int p0, int r) { return std::max(1, std::min(P - p0, 256 / r)); }
+
+int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
+               const int32_t* h_outs, int32_t policy) {
+  if (int rc = validate_segments(S, indptr, rank, h_in, P, h_outs)) return rc;
   if (policy != LSV_TIER_AUTO && policy != LSV_TIER_SIMT && policy != LSV_TIER_TC)
     return fail(LSV_EINVAL, "unknown tier policy %d", policy);
   const int N = S > 0 ? indptr[S] : 0;
@@ -160,15 +169,18 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
       }
     }
   }
-  // shrink splits: balance bytes across ~2 waves of the SMs
+  // shrink: every m-tile is cut into projection subsets (N = np*rank <= 256) and k-splits that
+  // balance bytes across ~kShrinkWaves waves of the SMs
   const int chunks = h_in / kChunk;
-  std::vector<int64_t> row_bytes(pb.mtiles.size()), kch(pb.mtiles.size());
   int64_t total = 0;
-  for (size_t i = 0; i < pb.mtiles.size(); ++i) {
-    const MTile& mt = pb.mtiles[i];
-    row_bytes[i] = (int64_t)(round_up(mt.ntok, 8) + mt.rank) * 128;
-    kch[i] = std::max<int64_t>(1, std::min<int64_t>(4, kShrinkSlotBytes / row_bytes[i]));
-    total += row_bytes[i] * chunks;
+  int acc_cols = 128;
+  for (const MTile& mt : pb.mtiles) {
+    const int np8 = round_up(mt.ntok, 8);
+    for (int p0 = 0; p0 < P; p0 += subset_np(P, p0, mt.rank)) {
+      const int rows = subset_np(P, p0, mt.rank) * mt.rank;
+      total += (int64_t)(np8 + rows) * 128 * chunks;
+      if (round_up(rows, 16) > 128) acc_cols = 256;
+    }
   }
   const int64_t target = std::max<int64_t>(kMinItemBytes, total / std::max(1, kShrinkWaves * nsm));
   int64_t part_off = 0, vimg_off = 0;
@@ -176,68 +188,78 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   std::vector<std::pair<int64_t, ShrinkRec>> shrink_costed;
   for (size_t i = 0; i < pb.mtiles.size(); ++i) {
     MTile& mt = pb.mtiles[i];
-    const int stages = (chunks + kch[i] - 1) / kch[i];
-    const int64_t mt_bytes = row_bytes[i] * chunks;
-    int nsplit = (int)std::min<int64_t>(stages, std::max<int64_t>(1, (mt_bytes + target - 1) / target));
-    const int sps = (stages + nsplit - 1) / nsplit;  // stages per split
-    nsplit = (stages + sps - 1) / sps;
+    const int r = mt.rank, G = P * r, np8 = round_up(mt.ntok, 8);
+    const int64_t mt_bytes = (int64_t)(np8 + G) * 128 * chunks;
+    int nsplit = (int)std::min<int64_t>(chunks, std::max<int64_t>(1, (mt_bytes + target - 1) / target));
+    int cps = (chunks + nsplit - 1) / nsplit;          // chunks per split, whole 4-chunk stages
+    if (nsplit > 1) cps = std::min(chunks, round_up(cps, 4));
+    nsplit = (chunks + cps - 1) / cps;
     mt.nsplit = nsplit;
     mt.part_off = (int32_t)part_off;
-    if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * mt.rank;
+    if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * G;
     mt.vimg_off = (int32_t)vimg_off;  // 1024-aligned: the v image's swizzle atoms are address-based
-    vimg_off += round_up((int)((int64_t)round_up(mt.ntok, 16) * kpad(mt.rank) * 2), 1024);
+    vimg_off += round_up((int)((int64_t)round_up(mt.ntok, 16) * kpad(r) * 2), 1024);
     mt.counter = counter++;
-    if (nsplit > 1) {  // reduction units: (token, 8 padded-k) of this tile, reduced grid-wide
+    if (nsplit > 1) {  // reduction units: (token, projection, 8 padded-k) of this tile, reduced grid-wide
       pb.red.push_back((int32_t)i);
       pb.red.push_back(pb.red_units);
-      pb.red_units += mt.ntok * (kpad(mt.rank) / 8);
+      pb.red_units += mt.ntok * P * (kpad(r) / 8);
     }
-    for (int sp = 0; sp < nsplit; ++sp) {
-      ShrinkRec r{};
-      r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
-      r.chunk_begin = (int32_t)(sp * sps * kch[i]);
-      r.chunk_end = (int32_t)std::min<int64_t>(chunks, (int64_t)(sp + 1) * sps * kch[i]);
-      r.kch = (int32_t)kch[i]; r.split = sp;
-      r.nsplit = nsplit; r.part_off = mt.part_off; r.vimg_off = mt.vimg_off; r.counter = mt.counter;
-      r.mtile = (int32_t)i;
-      // bytes moved + a fixed per-item cost (pipeline fill, epilogue, split reduction)
-      const int64_t cost = row_bytes[i] * (r.chunk_end - r.chunk_begin) + 24 * 1024 +
-                           (nsplit > 1 ? (int64_t)mt.ntok * mt.rank * 8 : 0);
-      shrink_costed.push_back({cost, r});
+    for (int p0 = 0; p0 < P; p0 += subset_np(P, p0, r)) {
+      const int np = subset_np(P, p0, r), rows = np * r;
+      const int64_t row_bytes = (int64_t)(np8 + rows) * 128;
+      const int kch = (int)std::max<int64_t>(1, std::min<int64_t>(4, kShrinkSlotBytes / row_bytes));
+      for (int sp = 0; sp < nsplit; ++sp) {
+        ShrinkRec rc{};
+        rc.seg = mt.seg; rc.tok_begin = mt.tok_begin; rc.ntok = mt.ntok; rc.rank = r;
+        rc.chunk_begin = sp * cps;
+        rc.chunk_end = std::min(chunks, (sp + 1) * cps);
+        rc.kch = kch; rc.split = sp;
+        rc.nsplit = nsplit; rc.part_off = mt.part_off; rc.vimg_off = mt.vimg_off; rc.counter = mt.counter;
+        rc.mtile = (int32_t)i; rc.p0 = p0; rc.np = np;
+        // bytes moved + a fixed per-item cost (pipeline fill, epilogue, split reduction)
+        const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + 24 * 1024 +
+                             (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0);
+        shrink_costed.push_back({cost, rc});
+      }
     }
   }
   std::stable_sort(shrink_costed.begin(), shrink_costed.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-
-  std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
-  for (size_t i = 0; i < pb.mtiles.size(); ++i) {
-    const MTile& mt = pb.mtiles[i];
-    const int tw = b_tile_width(h_out);
-    const int64_t cost = (int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024;
-    for (int jt = 0; jt < h_out / tw; ++jt) {
-      ExpandRec r{};
-      r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
-      r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i;
-      expand_costed.push_back({cost, r});
-    }
-  }
-  std::stable_sort(expand_costed.begin(), expand_costed.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
   const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
-  const int expand_grid = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
   lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta);
-  lpt_assign(expand_costed, std::max(expand_grid, 1), pb.expand, pb.expand_cta);
+
+  // expand: per projection, items = (m-tile, tw-wide h_out tile)
+  int expand_grid[kMaxProj] = {0, 0, 0, 0};
+  for (int p = 0; p < P; ++p) {
+    std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
+    const int tw = b_tile_width(h_outs[p]);
+    for (size_t i = 0; i < pb.mtiles.size(); ++i) {
+      const MTile& mt = pb.mtiles[i];
+      const int64_t cost = (int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024;
+      for (int jt = 0; jt < h_outs[p] / tw; ++jt) {
+        ExpandRec r{};
+        r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
+        r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i;
+        expand_costed.push_back({cost, r});
+      }
+    }
+    std::stable_sort(expand_costed.begin(), expand_costed.end(),
+                     [](const auto& a, const auto& b) { return a.first > b.first; });
+    expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
+    lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p]);
+  }
 
   // header + workspace layout
   PlanHeader& h = pb.h;
   h.magic = kPlanMagic; h.version = kPlanVersion;
-  h.num_segments = S; h.num_tokens = N; h.h_in = h_in; h.h_out = h_out;
+  h.num_segments = S; h.num_tokens = N; h.h_in = h_in; h.h_out = h_outs[0];
+  h.num_proj = P;
+  h.acc_cols = acc_cols;
   h.n_simt_items = (int32_t)pb.simt.size();
   h.n_mtiles = (int32_t)pb.mtiles.size();
   h.n_shrink_items = (int32_t)pb.shrink.size();
-  h.n_expand_items = (int32_t)pb.expand.size();
   h.shrink_grid = shrink_grid;
-  h.expand_grid = expand_grid;
   int32_t off = sizeof(PlanHeader) / 4;
   h.off_seg_indptr = off; off += S + 1;
   h.off_seg_rank = off; off += S;
@@ -247,9 +269,18 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.off_mtiles = off; off += 8 * h.n_mtiles;
   h.off_shrink_recs = off; off += 16 * h.n_shrink_items;
   h.off_shrink_cta = off; off += (int32_t)pb.shrink_cta.size();
-  off = round_up(off, 4);
-  h.off_expand_recs = off; off += 8 * h.n_expand_items;
-  h.off_expand_cta = off; off += (int32_t)pb.expand_cta.size();
+  for (int p = 0; p < P; ++p) {
+    off = round_up(off, 4);
+    h.h_outs[p] = h_outs[p];
+    h.n_expand_items_p[p] = (int32_t)pb.expand[p].size();
+    h.expand_grid_p[p] = expand_grid[p];
+    h.off_expand_recs_p[p] = off; off += 8 * h.n_expand_items_p[p];
+    h.off_expand_cta_p[p] = off; off += (int32_t)pb.expand_cta[p].size();
+  }
+  h.n_expand_items = h.n_expand_items_p[0];
+  h.expand_grid = h.expand_grid_p[0];
+  h.off_expand_recs = h.off_expand_recs_p[0];
+  h.off_expand_cta = h.off_expand_cta_p[0];
   h.off_red = off; off += (int32_t)pb.red.size();
   h.n_red = (int32_t)pb.red.size() / 2;
   h.red_units = pb.red_units;
@@ -267,9 +298,12 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   int64_t ws = 0;
   h.ws_counters = 0; ws += round_up((counter + 2) * 4, 256);  // + grid barrier {arrive, done}
   h.ws_partials = (int32_t)ws; ws += (part_off * 4 + 255) / 256 * 256;
-  h.ws_vimg = (int32_t)ws; ws += (vimg_off + 1023) / 1024 * 1024;
-  h.ws_simt_v = (int32_t)ws; ws += (v_off * 4 + 255) / 256 * 256;
+  const int64_t vstride = (vimg_off + 1023) / 1024 * 1024;
+  h.ws_vimg = (int32_t)ws; ws += vstride * P;
+  h.simt_stride = (int32_t)((v_off + 63) / 64 * 64);
+  h.ws_simt_v = (int32_t)ws; ws += (int64_t)h.simt_stride * 4 * P;
   if (ws > INT32_MAX) return fail(LSV_EUNSUPPORTED, "workspace of %lld bytes exceeds 2 GiB", (long long)ws);
+  h.vimg_stride = (int32_t)vstride;
   h.ws_bytes = (int32_t)ws;
   h.n_counters = counter;
   int simt_segs = 0;
@@ -403,7 +437,8 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
   if (h->n_simt_items > 0) {
     simt_shrink_kernel<<<h->n_simt_items, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
                                                         h->off_simt_items, h->off_seg_rank, a_ptrs,
-                                                        reinterpret_cast<float*>(ws + h->ws_simt_v));
+                                                        reinterpret_cast<float*>(ws + h->ws_simt_v), h->num_proj,
+                                                        h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   if (h->n_shrink_items > 0) {
@@ -416,6 +451,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
     p.off_red_cta = h->off_red_cta;
     p.grid_bar = h->n_counters;
+    p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
     LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p));
@@ -423,25 +459,26 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
   return LSV_OK;
 }
 
-int run_expand(const PlanHeader* h, void* y, int64_t ldy, int32_t num_tokens, const void* const* b_ptrs, const int32_t* plan, uint8_t* ws,
-               cudaStream_t st) {
+int run_expand(const PlanHeader* h, int proj, void* y, int64_t ldy, int32_t num_tokens, const void* const* b_ptrs,
+               const int32_t* plan, uint8_t* ws, cudaStream_t st) {
+  const int h_out = h->h_outs[proj];
   if (h->n_simt_items > 0) {
-    simt_expand_kernel<<<dim3(h->n_simt_items, (h->h_out + 511) / 512), 64, 0, st>>>(
-        static_cast<__nv_bfloat16*>(y), ldy, h->h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
-        reinterpret_cast<const float*>(ws + h->ws_simt_v));
+    simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 511) / 512), 64, 0, st>>>(
+        static_cast<__nv_bfloat16*>(y), ldy, h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
+        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)proj * h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
-  if (h->n_expand_items > 0) {
+  if (h->n_expand_items_p[proj] > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
     ExpandParams p{};
-    if (int rc = get_maps(p.ymap, 0, y, ldy, num_tokens, h->h_out)) return rc;
+    if (int rc = get_maps(p.ymap, 0, y, ldy, num_tokens, h_out)) return rc;
     p.plan = plan; p.b_ptrs = b_ptrs; p.ws = ws; p.y = static_cast<__nv_bfloat16*>(y); p.ldy = ldy;
-    p.off_recs = h->off_expand_recs; p.off_cta = h->off_expand_cta;
-    p.ws_vimg = h->ws_vimg;
-    p.tw = b_tile_width(h->h_out);
+    p.off_recs = h->off_expand_recs_p[proj]; p.off_cta = h->off_expand_cta_p[proj];
+    p.ws_vimg = h->ws_vimg + proj * h->vimg_stride;
+    p.tw = b_tile_width(h_out);
     p.dbg = g_debug_expand;
     p.trace = g_trace; p.trace_items = g_trace_items;
-    LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, h->expand_grid, expand_smem_bytes(), st, p));
+    LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, h->expand_grid_p[proj], expand_smem_bytes(), st, p));
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   return LSV_OK;
@@ -465,11 +502,14 @@ size_t lsv_adapter_b_bytes(int32_t rank, int32_t h_out) {
 }
 
 static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int32_t h_in, int32_t h_out,
-                       void* a_tiled, void* b_tiled, lsv_stream_t stream, int unpack) {
+                       void* a_tiled, void* b_tiled, lsv_stream_t stream, int unpack, int32_t nproj = 1,
+                       int32_t proj = 0) {
   if (rank < 8 || rank > 256 || rank % 8) return fail(LSV_EINVAL, "rank must be a multiple of 8 in [8, 256], got %d", rank);
-  if (h_in <= 0 || h_in % 128 || h_out <= 0 || h_out % 128)
-    return fail(LSV_EINVAL, "h_in/h_out must be positive multiples of 128 (got %d, %d)", h_in, h_out);
+  if (nproj < 1 || nproj > kMaxProj || proj < 0 || proj >= nproj)
+    return fail(LSV_EINVAL, "projection %d of a group of %d (max %d)", proj, nproj, kMaxProj);
   const bool do_a = lora_a || a_tiled, do_b = lora_b || b_tiled;   // either half may be skipped
+  if ((do_a && (h_in <= 0 || h_in % 128)) || (do_b && (h_out <= 0 || h_out % 128)))
+    return fail(LSV_EINVAL, "h_in/h_out must be positive multiples of 128 (got %d, %d)", h_in, h_out);
   if ((do_a && !(lora_a && a_tiled)) || (do_b && !(lora_b && b_tiled)) || !(do_a || do_b))
     return fail(LSV_EINVAL, "null buffer");
   if ((do_a && (!aligned16(lora_a) || !aligned16(a_tiled))) || (do_b && (!aligned16(lora_b) || !aligned16(b_tiled))))
@@ -478,7 +518,8 @@ static int pack_common(const void* lora_a, const void* lora_b, int32_t rank, int
   const int blocks = (int)std::min<int64_t>(4096, (units + 255) / 256);
   pack_adapter_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(lora_a), static_cast<const uint8_t*>(lora_b), rank, do_a ? h_in : 0,
-      do_b ? h_out : 0, static_cast<uint8_t*>(a_tiled), static_cast<uint8_t*>(b_tiled), unpack);
+      do_b ? h_out : 0, static_cast<uint8_t*>(a_tiled), static_cast<uint8_t*>(b_tiled), unpack, nproj * rank,
+      proj * rank);
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
@@ -494,19 +535,22 @@ int lsv_unpack_adapter(const void* a_tiled, const void* b_tiled, int32_t rank, i
                      stream, 1);
 }
 
-int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
-                  int32_t h_out, int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes) {
-  PlanBuilder pb;
-  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, h_out, tier_policy)) return rc;
-  if (plan_bytes) *plan_bytes = (size_t)pb.h.total_ints * 4;
-  if (workspace_bytes) *workspace_bytes = (size_t)pb.h.ws_bytes;
-  return LSV_OK;
+size_t lsv_adapter_a_group_bytes(int32_t num_proj, int32_t rank, int32_t h_in) {
+  return (num_proj > 0 && rank > 0 && h_in > 0) ? (size_t)num_proj * rank * h_in * 2 : 0;
 }
 
-int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
-                   int32_t h_out, int32_t tier_policy, void* plan_host, size_t plan_bytes) {
-  PlanBuilder pb;
-  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, h_out, tier_policy)) return rc;
+int lsv_pack_adapter_group(const void* lora_a, int32_t num_proj, int32_t proj, int32_t rank, int32_t h_in,
+                           void* a_group_tiled, lsv_stream_t stream) {
+  return pack_common(lora_a, nullptr, rank, h_in, 0, a_group_tiled, nullptr, stream, 0, num_proj, proj);
+}
+
+int lsv_unpack_adapter_group(const void* a_group_tiled, int32_t num_proj, int32_t proj, int32_t rank, int32_t h_in,
+                             void* lora_a, lsv_stream_t stream) {
+  return pack_common(lora_a, nullptr, rank, h_in, 0, const_cast<void*>(a_group_tiled), nullptr, stream, 1, num_proj,
+                     proj);
+}
+
+static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes) {
   const PlanHeader& h = pb.h;
   if (!plan_host) return fail(LSV_EINVAL, "plan_host is null");
   if (plan_bytes < (size_t)h.total_ints * 4)
@@ -521,11 +565,43 @@ int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_
   std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
   std::memcpy(out + h.off_shrink_recs, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkRec));
   std::copy(pb.shrink_cta.begin(), pb.shrink_cta.end(), out + h.off_shrink_cta);
-  std::memcpy(out + h.off_expand_recs, pb.expand.data(), pb.expand.size() * sizeof(ExpandRec));
-  std::copy(pb.expand_cta.begin(), pb.expand_cta.end(), out + h.off_expand_cta);
+  for (int p = 0; p < h.num_proj; ++p) {
+    std::memcpy(out + h.off_expand_recs_p[p], pb.expand[p].data(), pb.expand[p].size() * sizeof(ExpandRec));
+    std::copy(pb.expand_cta[p].begin(), pb.expand_cta[p].end(), out + h.off_expand_cta_p[p]);
+  }
   std::copy(pb.red.begin(), pb.red.end(), out + h.off_red);
   std::copy(pb.red_cta.begin(), pb.red_cta.end(), out + h.off_red_cta);
   return LSV_OK;
+}
+
+int lsv_plan_size_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                        int32_t num_proj, const int32_t* h_outs, int32_t tier_policy, size_t* plan_bytes,
+                        size_t* workspace_bytes) {
+  PlanBuilder pb;
+  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy)) return rc;
+  if (plan_bytes) *plan_bytes = (size_t)pb.h.total_ints * 4;
+  if (workspace_bytes) *workspace_bytes = (size_t)pb.h.ws_bytes;
+  return LSV_OK;
+}
+
+int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                         int32_t num_proj, const int32_t* h_outs, int32_t tier_policy, void* plan_host,
+                         size_t plan_bytes) {
+  PlanBuilder pb;
+  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy)) return rc;
+  return plan_write(pb, plan_host, plan_bytes);
+}
+
+int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                  int32_t h_out, int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes) {
+  return lsv_plan_size_group(num_segments, seg_indptr, seg_rank, h_in, 1, &h_out, tier_policy, plan_bytes,
+                             workspace_bytes);
+}
+
+int lsv_plan_build(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
+                   int32_t h_out, int32_t tier_policy, void* plan_host, size_t plan_bytes) {
+  return lsv_plan_build_group(num_segments, seg_indptr, seg_rank, h_in, 1, &h_out, tier_policy, plan_host,
+                              plan_bytes);
 }
 
 int lsv_plan_summary(const void* plan_host, int32_t* out8) {
@@ -552,19 +628,28 @@ int lsv_lora_shrink(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in
                     static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
 }
 
-int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, const void* const* b_ptrs,
-                    const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
-                    lsv_stream_t stream) {
+int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,
+                         const void* const* b_ptrs, const void* plan_dev, const void* plan_host, void* workspace,
+                         size_t workspace_bytes, lsv_stream_t stream) {
   const PlanHeader* h = check_plan(plan_host);
   if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
-  if (h->h_out != h_out) return fail(LSV_EINVAL, "h_out %d does not match the plan's %d", h_out, h->h_out);
+  if (proj < 0 || proj >= h->num_proj) return fail(LSV_EINVAL, "projection %d of a plan for %d", proj, h->num_proj);
+  if (h->h_outs[proj] != h_out)
+    return fail(LSV_EINVAL, "h_out %d does not match the plan's %d", h_out, h->h_outs[proj]);
   if (num_tokens < h->num_tokens)
     return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
   if (h->num_tokens == 0) return LSV_OK;
   if (!y || !b_ptrs) return fail(LSV_EINVAL, "y / b_ptrs must be non-null");
   if (!aligned16(y) || ldy % 8 || ldy < h_out) return fail(LSV_EINVAL, "y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out");
-  return run_expand(h, y, ldy, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev), static_cast<uint8_t*>(workspace),
-                    static_cast<cudaStream_t>(stream));
+  return run_expand(h, proj, y, ldy, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, const void* const* b_ptrs,
+                    const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                    lsv_stream_t stream) {
+  return lsv_lora_expand_proj(y, ldy, num_tokens, h_out, 0, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes,
+                              stream);
 }
 
 int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype, int32_t num_tokens, int32_t h_in,
@@ -605,8 +690,8 @@ int lsv_slab_free(void* dev_ptr) {
 int lsv_plan_vimg_region(const void* plan_host, size_t* offset, size_t* bytes) {
   const PlanHeader* h = check_plan(plan_host);
   if (!h || !offset || !bytes) return fail(LSV_EINVAL, "not a liblsv plan");
-  *offset = (size_t)h->ws_vimg;
-  *bytes = (size_t)(h->ws_simt_v - h->ws_vimg);
+  *offset = (size_t)h->ws_vimg;           // projection 0's v images (TP plans have one projection)
+  *bytes = (size_t)h->vimg_stride;
   return LSV_OK;
 }
 
@@ -619,6 +704,7 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
   if (hs->n_mtiles != hf->n_mtiles || hs->num_tokens != hf->num_tokens)
     return fail(LSV_EINVAL, "shard and full plans index different tiles (%d vs %d)", hs->n_mtiles, hf->n_mtiles);
   if (tp < 1 || !gathered || !full_workspace) return fail(LSV_EINVAL, "bad arguments");
+  if (hs->num_proj != 1 || hf->num_proj != 1) return fail(LSV_EINVAL, "TP assembly takes single-projection plans");
   if (hs->n_simt_items != 0 || hf->n_simt_items != 0)
     return fail(LSV_EUNSUPPORTED, "TP assembly needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
   if (hf->n_mtiles == 0) return LSV_OK;

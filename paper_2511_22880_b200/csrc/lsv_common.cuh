@@ -45,10 +45,14 @@ __host__ __device__ __forceinline__ uint32_t umma_layout(int row_bytes) {
 }
 
 // A tiled (shrink B operand, K-major SW128): [h_in/64][rank][64]
-__host__ __device__ __forceinline__ size_t a_tiled_off(int k, int i, int rank) {
+// Group form: the A tiles of an input group's projections (same h_in, same rank) interleaved per
+// chunk, [h_in/64][grows = nproj*rank rows][64]; member p's rows start at p*rank (a multiple of 8,
+// so every member keeps the swizzle phase it has alone).  nproj = 1 is the single-adapter layout.
+__host__ __device__ __forceinline__ size_t a_tiled_off_g(int row, int i, int grows) {
   const int c = i >> 6, e = i & 63;
-  return (size_t)c * rank * 128 + (size_t)k * 128 + ((((e >> 3) ^ (k & 7)) << 4) | ((e & 7) << 1));
+  return (size_t)c * grows * 128 + (size_t)row * 128 + ((((e >> 3) ^ (row & 7)) << 4) | ((e & 7) << 1));
 }
+__host__ __device__ __forceinline__ size_t a_tiled_off(int k, int i, int rank) { return a_tiled_off_g(k, i, rank); }
 // B tiled (expand B operand, MN-major SW128): per tw-wide h_out tile (tw = b_tile_width(h_out))
 // [kp/8 k-groups][tw/64 blocks of 64 h_out][8 k rows][64 h_out], 1024-byte swizzle atoms;
 // kp = kpad(rank) rows, the rows past the rank are zero so a K=16 MMA step never reads stale data.

@@ -10,7 +10,8 @@
 namespace lsv {
 
 constexpr int32_t kPlanMagic = 0x5056534c;  // "LSVP"
-constexpr int32_t kPlanVersion = 1;
+constexpr int32_t kPlanVersion = 2;
+constexpr int kMaxProj = 4;    // projections per input group (q/k/v = 3)
 
 enum Tier : int32_t { kTierNone = 0, kTierSimt = 1, kTierTc = 2 };
 
@@ -34,7 +35,16 @@ struct PlanHeader {            // 64 int32
   int32_t simt_segments;
   int32_t off_red, n_red, red_units;   // split-K reduction table: [n_red] {mtile, unit prefix}
   int32_t off_red_cta;                 // [shrink_grid + 1] first reduction entry of each CTA's unit range
-  int32_t reserved[64 - 33];
+  // input groups: num_proj projections share x (q/k/v, gate/up) and are shrunk together from a
+  // group A tile [chunk][num_proj*rank rows][64]; each has its own h_out, expand list and v images
+  int32_t num_proj;
+  int32_t vimg_stride;                 // bytes between the v-image regions of consecutive projections
+  int32_t simt_stride;                 // floats between the SIMT v regions of consecutive projections
+  int32_t acc_cols;                    // shrink TMEM accumulator width (128 or 256 columns)
+  int32_t h_outs[kMaxProj];
+  int32_t off_expand_recs_p[kMaxProj], off_expand_cta_p[kMaxProj];
+  int32_t expand_grid_p[kMaxProj], n_expand_items_p[kMaxProj];
+  int32_t reserved[64 - 57];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -57,7 +67,7 @@ struct ShrinkRec {             // 16 int32
   int32_t seg, tok_begin, ntok, rank;
   int32_t chunk_begin, chunk_end, kch, split;   // k-range in 64-element chunks of h_in
   int32_t nsplit, part_off, vimg_off, counter;
-  int32_t mtile, pad[3];
+  int32_t mtile, p0, np, pad;                   // projections [p0, p0+np) of the group: N = np*rank
 };
 
 struct ExpandRec {             // 8 int32

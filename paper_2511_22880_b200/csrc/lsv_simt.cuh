@@ -28,21 +28,23 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
                                                           int h_in, const int32_t* __restrict__ plan,
                                                           int off_items, int off_rank,
                                                           const void* const* __restrict__ a_ptrs,
-                                                          float* __restrict__ simt_v) {
+                                                          float* __restrict__ simt_v, int nproj, int simt_stride) {
+  // the group's nproj projections are one rank-(nproj*r) adapter in the group A layout; row k of
+  // it is projection k / r, whose v lands in that projection's region
   const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
-  const int r = plan[off_rank + it.seg];
+  const int r = plan[off_rank + it.seg], G = nproj * r;
   const uint8_t* a = static_cast<const uint8_t*>(a_ptrs[it.seg]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint8_t* xrow[kSimtMaxTok];
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t)
     xrow[t] = reinterpret_cast<const uint8_t*>(x + (int64_t)(it.tok_begin + min(t, it.ntok - 1)) * ldx);
-  for (int k = warp; k < r; k += 8) {
+  for (int k = warp; k < G; k += 8) {
     float acc[kSimtMaxTok];
 #pragma unroll
     for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
     for (int i0 = lane * 8; i0 < h_in; i0 += 256) {
-      const uint4 av = __ldg(reinterpret_cast<const uint4*>(a + a_tiled_off(k, i0, r)));
+      const uint4 av = __ldg(reinterpret_cast<const uint4*>(a + a_tiled_off_g(k, i0, G)));
 #pragma unroll
       for (int t = 0; t < kSimtMaxTok; ++t) {
         if (t < it.ntok) {
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
     if (lane == 0) {
 #pragma unroll
       for (int t = 0; t < kSimtMaxTok; ++t)
-        if (t < it.ntok) simt_v[it.v_off + t * r + k] = acc[t];
+        if (t < it.ntok) simt_v[(size_t)(k / r) * simt_stride + it.v_off + t * r + k % r] = acc[t];
     }
   }
 }
@@ -142,7 +144,8 @@ __global__ void __launch_bounds__(256) vimg_assemble_kernel(const uint8_t* __res
 // the tiled buffers.
 __global__ void pack_adapter_kernel(const uint8_t* __restrict__ lora_a, const uint8_t* __restrict__ lora_b,
                                     int rank, int h_in, int h_out, uint8_t* __restrict__ a_t,
-                                    uint8_t* __restrict__ b_t, int unpack) {
+                                    uint8_t* __restrict__ b_t, int unpack, int grows, int row0) {
+  // A goes to rows [row0, row0 + rank) of a group tile of grows rows per chunk (a_tiled_off_g)
   const int kp = kpad(rank);
   const int64_t na = (int64_t)rank * h_in / 8, nb = (int64_t)h_out * kp / 8;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < na + nb;
@@ -150,7 +153,7 @@ __global__ void pack_adapter_kernel(const uint8_t* __restrict__ lora_a, const ui
     if (u < na) {
       const int k = (int)(u / (h_in / 8)), i = (int)(u % (h_in / 8)) * 8;
       uint4* plain = reinterpret_cast<uint4*>(const_cast<uint8_t*>(lora_a) + ((int64_t)k * h_in + i) * 2);
-      uint4* tiled = reinterpret_cast<uint4*>(a_t + a_tiled_off(k, i, rank));
+      uint4* tiled = reinterpret_cast<uint4*>(a_t + a_tiled_off_g(row0 + k, i, grows));
       if (unpack) *plain = *tiled; else *tiled = *plain;
     } else {
       // one 16-byte unit of B tiled = lora_b[j .. j+7][k] (a strided column gather of lora_B);

@@ -37,6 +37,8 @@ struct alignas(64) ShrinkParams {
   uint8_t* ws;
   int off_recs, off_cta, ws_partials, ws_vimg, ws_counters;
   int off_mtiles, off_red, n_red, red_units, grid_bar, off_red_cta;   // grid-wide split-K reduction
+  int num_proj, vimg_stride;    // input group: projections shrunk together, bytes between their v images
+  int acc_cols;                 // TMEM accumulator width (128 -> 4 buffers, 256 -> 2)
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -168,19 +170,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     int slot = 0; uint32_t phase = 0;
     for (int k = 0; rs.pop(inf, a); ++k) {
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
-      const int r = inf.rank, np8 = round_up(inf.ntok, 8), kch = inf.kch;
+      // rows [p0*r, (p0+np)*r) of the group A tile (G = num_proj*r rows per 64-column chunk)
+      const int r = inf.rank, G = p.num_proj * r, rows = inf.np * r, np8 = round_up(inf.ntok, 8), kch = inf.kch;
+      const uint8_t* asub = a + (size_t)inf.p0 * r * 128;
       const int m = np8 >> 3, pc = __popc(m);   // x boxes per chunk: one per set bit of np8/8
       for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
         const int kc = min(kch, inf.chunk_end - g);
         if (lane == 0) {
           mbar_wait(&empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : r)) * 128));
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : rows)) * 128));
         }
         __syncwarp();
         uint8_t* dst = ring + slot * kShrinkSlotBytes;
         if (lane == 0) {
-          if (!(p.dbg & 2))
-            bulk_load(dst + kc * np8 * 128, a + (size_t)g * r * 128, (uint32_t)(kc * r * 128), &full[slot]);
+          if (!(p.dbg & 2)) {
+            if (rows == G) {       // whole group: the kc chunks are one contiguous run
+              bulk_load(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), &full[slot]);
+            } else {               // projection subset: one copy per chunk
+              for (int c = 0; c < kc; ++c)
+                bulk_load(dst + (kc * np8 + c * rows) * 128, asub + (size_t)(g + c) * G * 128, (uint32_t)(rows * 128),
+                          &full[slot]);
+            }
+          }
         } else if (!(p.dbg & 4) && lane - 1 < kc * pc) {
           const int c = (lane - 1) / pc, i = (lane - 1) % pc;
           int mm = m, row = 0, bb = -1;
@@ -204,17 +215,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     int slot = 0; uint32_t phase = 0;
     int dbg_stage = 0;
     const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+    const int nbuf = kTmemCols / p.acc_cols;
     for (int k = 0; rs.pop(inf, unused); ++k) {
-      const int r = __shfl_sync(0xffffffffu, inf.rank, 0);
+      const int rows = __shfl_sync(0xffffffffu, inf.rank * inf.np, 0);
       const int np8 = round_up(__shfl_sync(0xffffffffu, inf.ntok, 0), 8);
       const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
       const int cb = __shfl_sync(0xffffffffu, inf.chunk_begin, 0), ce = __shfl_sync(0xffffffffu, inf.chunk_end, 0);
-      const int buf = k % kAccBufs;
-      mbar_wait(&tempty[buf], ((k / kAccBufs) & 1) ^ 1);
+      const int buf = k % nbuf;
+      mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem_base + buf * 128;
-      const uint32_t idesc = idesc_bf16(128, max(16, round_up(r, 16)));
-      const uint32_t xstep = (uint32_t)(np8 * 128) >> 4, astep = (uint32_t)(r * 128) >> 4;  // per chunk, desc units
+      const uint32_t d = tmem_base + buf * p.acc_cols;
+      const uint32_t idesc = idesc_bf16(128, max(16, round_up(rows, 16)));
+      const uint32_t xstep = (uint32_t)(np8 * 128) >> 4, astep = (uint32_t)(rows * 128) >> 4;  // per chunk, desc units
       uint32_t accumulate = 0;
       for (int g = cb; g < ce; g += kch) {
         const int kc = min(kch, ce - g);
@@ -246,36 +258,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
     const uint8_t* unused;
+    const int nbuf = kTmemCols / p.acc_cols;
     for (int k = 0; rs.pop(inf, unused); ++k) {
       const int r = inf.rank, nt = inf.ntok, kp = kpad(r), np16 = round_up(nt, 16);
-      const int buf = k % kAccBufs;
-      mbar_wait(&tfull[buf], (k / kAccBufs) & 1);
+      const int G = p.num_proj * r, rows = inf.np * r;
+      const int buf = k % nbuf;
+      mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
       const bool valid = row < nt && !(p.dbg & 8);
-      uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;
-      float* part = partials + inf.part_off + (size_t)inf.split * nt * r;
-      for (int cc = 0; cc < r; cc += 16) {
+      uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
+      float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
+      for (int cc = 0; cc < rows; cc += 16) {
         float v[16];
         tmem_ld_32x32b_x16(taddr + cc, v);
         if (valid) {
-          if (inf.nsplit == 1) {
-            for (int h = 0; h < 2; ++h) {
-              uint4 w;
-              const int k0 = cc + h * 8;
-              w.x = pack_bf16x2(k0 + 0 < r ? v[h * 8 + 0] : 0.f, k0 + 1 < r ? v[h * 8 + 1] : 0.f);
-              w.y = pack_bf16x2(k0 + 2 < r ? v[h * 8 + 2] : 0.f, k0 + 3 < r ? v[h * 8 + 3] : 0.f);
-              w.z = pack_bf16x2(k0 + 4 < r ? v[h * 8 + 4] : 0.f, k0 + 5 < r ? v[h * 8 + 5] : 0.f);
-              w.w = pack_bf16x2(k0 + 6 < r ? v[h * 8 + 6] : 0.f, k0 + 7 < r ? v[h * 8 + 7] : 0.f);
-              if (k0 < kp) *reinterpret_cast<uint4*>(vimg + vimg_off(row, k0, kp, np16)) = w;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j0 = cc + h * 8;          // 8 columns, all of projection p0 + j0 / r (r % 8 == 0)
+            if (j0 < rows) {
+              if (inf.nsplit == 1) {
+                uint4 w;
+                w.x = pack_bf16x2(v[h * 8 + 0], v[h * 8 + 1]);
+                w.y = pack_bf16x2(v[h * 8 + 2], v[h * 8 + 3]);
+                w.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
+                w.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
+                const int pp = inf.p0 + j0 / r;
+                *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
+              } else {
+                float4* dst = reinterpret_cast<float4*>(part + j0);
+                dst[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
+                dst[1] = make_float4(v[h * 8 + 4], v[h * 8 + 5], v[h * 8 + 6], v[h * 8 + 7]);
+              }
             }
-          } else {
-            float4* dst = reinterpret_cast<float4*>(part + (size_t)row * r + cc);
-            const int nvec = min(16, r - cc) / 4;
-            for (int u = 0; u < nvec; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
           }
         }
+      }
+      if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
+        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp)
+          *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16)) = make_uint4(0, 0, 0, 0);
       }
       tc_fence_before();
       __syncwarp();
@@ -318,13 +340,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     while (e + 1 < p.n_red && red[2 * (e + 1) + 1] <= u) ++e;
     const MTile mt = mtiles[red[2 * e]];
     const int kp = kpad(mt.rank), upr = kp / 8, v = u - red[2 * e + 1], np16 = round_up(mt.ntok, 16);
-    const int t = v / upr, k0 = (v % upr) * 8;
+    const int G = p.num_proj * mt.rank, upt = p.num_proj * upr;   // units per token: projections x k units
+    const int t = v / upt, pp = (v % upt) / upr, k0 = (v % upr) * 8;
     float s8[8];
 #pragma unroll
     for (int q8 = 0; q8 < 8; ++q8) s8[q8] = 0.f;
     if (k0 < mt.rank) {
-      const size_t stride = (size_t)mt.ntok * mt.rank;
-      const float* base = partials + mt.part_off + (size_t)t * mt.rank + k0;
+      const size_t stride = (size_t)mt.ntok * G;
+      const float* base = partials + mt.part_off + (size_t)t * G + pp * mt.rank + k0;
       for (int j = 0; j < mt.nsplit; ++j) {
         const float4 lo4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride));
         const float4 hi4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride) + 1);
@@ -335,7 +358,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     uint4 w;
     w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
     w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
-    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
   }
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 5);

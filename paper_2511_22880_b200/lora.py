@@ -3,9 +3,11 @@
 This is the operator the reference only prices: ``schedule_server`` forms a prefill batch
 (simengine.py:96-152) and calls ``costmodel.prefill_time(lengths, ranks, params)``
 (costmodel.py:83-105), which charges the whole batch the maximum rank.  Here the batch is
-indexed into adapter segments (segments.py), planned once per projection shape by liblsv's
-host planner (per-segment tier + LPT work lists), and every layer/projection is one
-``lsv_lora_apply`` call: y[t] += (x[t]·A_s^T)·B_s^T with each segment paying its own rank.
+indexed into adapter segments (segments.py) and planned once per input group by liblsv's host
+planner (per-segment tier + LPT work lists).  Per layer, each input group (q/k/v, o, gate/up,
+down) is one fused ``lsv_lora_shrink`` (x read once, v = x·A_s^T for every member) followed by
+one ``lsv_lora_expand_proj`` per member (y += v·B_s^T): y[t] += (x[t]·A_s^T)·B_s^T with each
+segment paying its own rank.
 """
 
 from __future__ import annotations
@@ -18,26 +20,30 @@ import torch
 
 from . import native
 from .segments import Segments
-from .shapes import ModelShape
+from .shapes import INPUT_GROUPS, ModelShape, input_group  # noqa: F401  (re-exported)
 from .slab import AdapterSlab
 
 
 @dataclass
 class ShapePlan:
+    """One liblsv plan: an input group's fused shrink + each member's expand (h_outs[i]); a single
+    projection is the one-member case (h_out = h_outs[0])."""
     h_in: int
     h_out: int
     plan_host: np.ndarray       # int32 blob (liblsv plan)
     plan_dev: torch.Tensor      # same blob in HBM
     workspace_bytes: int
     summary: tuple[int, ...]    # (S, N, h_in, h_out, simt_segs, mtiles, shrink_items, expand_items)
+    h_outs: tuple[int, ...] = ()
+    members: tuple[int, ...] = ()
 
 
 @dataclass
 class BatchPlan:
     segments: Segments
-    shape_plans: dict[tuple[int, int], ShapePlan]
-    a_ptrs: torch.Tensor        # int64 [layers*projections, S]
-    b_ptrs: torch.Tensor
+    group_plans: list[ShapePlan]   # one per model.groups() entry
+    a_ptrs: torch.Tensor        # int64 [layers*groups, S]: group A tiles
+    b_ptrs: torch.Tensor        # int64 [layers*projections, S]
     workspace: torch.Tensor     # uint8, zero-filled once
     tier_policy: int = native.TIER_AUTO
     extra: dict = field(default_factory=dict)
@@ -46,28 +52,47 @@ class BatchPlan:
     def num_tokens(self) -> int:
         return self.segments.num_tokens
 
+    @property
+    def shape_plans(self) -> dict[tuple[int, int], ShapePlan]:
+        """(h_in, h_out) -> the plan of the first group with a member of that shape."""
+        out: dict[tuple[int, int], ShapePlan] = {}
+        for gp in self.group_plans:
+            for h in gp.h_outs:
+                out.setdefault((gp.h_in, h), gp)
+        return out
 
-def build_shape_plan(seg: Segments, h_in: int, h_out: int, tier_policy: int,
-                     device: torch.device) -> ShapePlan:
+
+def build_group_plan(seg: Segments, h_in: int, h_outs, tier_policy: int, device: torch.device,
+                     members: tuple[int, ...] = ()) -> ShapePlan:
     lib = native.lib()
     S = seg.num_segments
     indptr = np.ascontiguousarray(seg.seg_indptr, dtype=np.int32)
     ranks = np.ascontiguousarray(seg.seg_rank, dtype=np.int32)
+    hs = np.ascontiguousarray(h_outs, dtype=np.int32)
     pb = ctypes.c_size_t()
     wb = ctypes.c_size_t()
-    native.check(lib.lsv_plan_size(S, indptr.ctypes.data, ranks.ctypes.data, h_in, h_out, tier_policy,
-                                   ctypes.byref(pb), ctypes.byref(wb)))
+    native.check(lib.lsv_plan_size_group(S, indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs), hs.ctypes.data,
+                                         tier_policy, ctypes.byref(pb), ctypes.byref(wb)))
     blob = np.zeros(pb.value // 4, dtype=np.int32)
-    native.check(lib.lsv_plan_build(S, indptr.ctypes.data, ranks.ctypes.data, h_in, h_out, tier_policy,
-                                    blob.ctypes.data, pb.value))
+    native.check(lib.lsv_plan_build_group(S, indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs), hs.ctypes.data,
+                                          tier_policy, blob.ctypes.data, pb.value))
     summ = np.zeros(8, dtype=np.int32)
     native.check(lib.lsv_plan_summary(blob.ctypes.data, summ.ctypes.data))
     dev = torch.from_numpy(blob).to(device)
-    return ShapePlan(h_in, h_out, blob, dev, int(wb.value), tuple(int(v) for v in summ))
+    return ShapePlan(h_in, int(hs[0]), blob, dev, int(wb.value), tuple(int(v) for v in summ),
+                     tuple(int(h) for h in hs), tuple(members))
+
+
+def build_shape_plan(seg: Segments, h_in: int, h_out: int, tier_policy: int,
+                     device: torch.device) -> ShapePlan:
+    return build_group_plan(seg, h_in, [h_out], tier_policy, device)
 
 
 class LoraDeltaEngine:
-    """Mixed-rank LoRA delta over all layers/projections of one model on one GPU."""
+    """Mixed-rank LoRA delta over all layers/projections of one model on one GPU.
+
+    Per layer and input group (model.groups(): q/k/v, o, gate/up, down) one fused shrink reads
+    the group's x once and writes every member's v images; each member's expand follows."""
 
     def __init__(self, slab: AdapterSlab, tier_policy: int = native.TIER_AUTO):
         native.load()
@@ -75,18 +100,22 @@ class LoraDeltaEngine:
         self.model: ModelShape = slab.model
         self.device = slab.device
         self.tier_policy = tier_policy
+        self.groups = self.model.groups()
+        self._member = {p: (gi, i) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self._workspace: torch.Tensor | None = None
 
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
                 peer_slabs: dict[int, AdapterSlab] | None = None) -> BatchPlan:
-        """Plan a batch: one liblsv plan per distinct projection shape + pointer tables."""
-        plans = {}
+        """Plan a batch: one liblsv plan per input group + pointer tables."""
+        plans = []
         ws_need = 0
-        for (h_in, h_out) in self.model.shapes():
-            sp = build_shape_plan(seg, h_in, h_out, self.tier_policy, self.device)
-            plans[(h_in, h_out)] = sp
-            ws_need = max(ws_need, sp.workspace_bytes)
+        projs = self.model.projections
+        for _, members in self.groups:
+            gp = build_group_plan(seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
+                                  self.tier_policy, self.device, members)
+            plans.append(gp)
+            ws_need = max(ws_need, gp.workspace_bytes)
         if self._workspace is None or self._workspace.numel() < ws_need:
             # zero-filled once: the kernels leave their split counters at zero on exit
             self._workspace = torch.zeros(max(ws_need, 256), dtype=torch.uint8, device=self.device)
@@ -96,47 +125,60 @@ class LoraDeltaEngine:
     # -- execution ---------------------------------------------------------------------
     def apply(self, bp: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor,
               stream: torch.cuda.Stream | None = None) -> None:
-        """y[:N] += delta for one (layer, projection); x [N, h_in], y [N, h_out] bf16."""
+        """y[:N] += delta for one (layer, projection); x [N, h_in], y [N, h_out] bf16.  (Runs the
+        projection's whole group shrink; ``forward`` shares it across the group.)"""
         pr = self.model.projections[proj]
-        sp = bp.shape_plans[(pr.h_in, pr.h_out)]
         self._check_io(x, y, pr.h_in, pr.h_out, bp.num_tokens)
-        S = bp.segments.num_segments
-        row = layer * len(self.model.projections) + proj
-        st = stream or torch.cuda.current_stream(self.device)
-        native.check(native.lib().lsv_lora_apply(
-            x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0), native.LSV_DTYPE_BF16, x.shape[0],
-            pr.h_in, pr.h_out, bp.a_ptrs.data_ptr() + row * S * 8, bp.b_ptrs.data_ptr() + row * S * 8,
-            sp.plan_dev.data_ptr(), sp.plan_host.ctypes.data, bp.workspace.data_ptr(),
-            bp.workspace.numel(), st.cuda_stream))
+        self.shrink(bp, layer, proj, x, stream)
+        self.expand(bp, layer, proj, y, stream)
 
     def shrink(self, bp: BatchPlan, layer: int, proj: int, x: torch.Tensor, stream=None) -> None:
-        pr = self.model.projections[proj]
-        sp = bp.shape_plans[(pr.h_in, pr.h_out)]
+        """Fused shrink of proj's input group (v images of every member)."""
+        gi, _ = self._member[proj]
+        gp = bp.group_plans[gi]
         S = bp.segments.num_segments
-        row = layer * len(self.model.projections) + proj
+        row = layer * len(self.groups) + gi
         st = stream or torch.cuda.current_stream(self.device)
         native.check(native.lib().lsv_lora_shrink(
-            x.data_ptr(), x.stride(0), x.shape[0], pr.h_in, bp.a_ptrs.data_ptr() + row * S * 8,
-            sp.plan_dev.data_ptr(), sp.plan_host.ctypes.data, bp.workspace.data_ptr(),
+            x.data_ptr(), x.stride(0), x.shape[0], gp.h_in, bp.a_ptrs.data_ptr() + row * S * 8,
+            gp.plan_dev.data_ptr(), gp.plan_host.ctypes.data, bp.workspace.data_ptr(),
             bp.workspace.numel(), st.cuda_stream))
 
     def expand(self, bp: BatchPlan, layer: int, proj: int, y: torch.Tensor, stream=None) -> None:
         pr = self.model.projections[proj]
-        sp = bp.shape_plans[(pr.h_in, pr.h_out)]
+        gi, idx = self._member[proj]
+        gp = bp.group_plans[gi]
         S = bp.segments.num_segments
         row = layer * len(self.model.projections) + proj
         st = stream or torch.cuda.current_stream(self.device)
-        native.check(native.lib().lsv_lora_expand(
-            y.data_ptr(), y.stride(0), y.shape[0], pr.h_out, bp.b_ptrs.data_ptr() + row * S * 8,
-            sp.plan_dev.data_ptr(), sp.plan_host.ctypes.data, bp.workspace.data_ptr(),
+        native.check(native.lib().lsv_lora_expand_proj(
+            y.data_ptr(), y.stride(0), y.shape[0], pr.h_out, idx, bp.b_ptrs.data_ptr() + row * S * 8,
+            gp.plan_dev.data_ptr(), gp.plan_host.ctypes.data, bp.workspace.data_ptr(),
             bp.workspace.numel(), st.cuda_stream))
 
     def forward(self, bp: BatchPlan, xs: list[dict[str, torch.Tensor]], ys: list[dict[str, torch.Tensor]],
                 stream=None) -> None:
         """Every layer and projection: xs[l][input_group], ys[l][proj_name]."""
+        projs = self.model.projections
         for layer in range(self.model.layers):
-            for p, pr in enumerate(self.model.projections):
-                self.apply(bp, layer, p, xs[layer][input_group(pr.name)], ys[layer][pr.name], stream)
+            for gname, members in self.groups:
+                x = xs[layer][gname]
+                for p in members:
+                    self._check_io(x, ys[layer][projs[p].name], projs[p].h_in, projs[p].h_out, bp.num_tokens)
+                self.shrink(bp, layer, members[0], x, stream)
+                for p in members:
+                    self.expand(bp, layer, p, ys[layer][projs[p].name], stream)
+
+    def launches_per_step(self, bp: BatchPlan) -> int:
+        """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand
+        per member)."""
+        n = 0
+        for gp in bp.group_plans:
+            simt = 1 if gp.summary[4] else 0
+            h = gp.plan_host[:64]
+            n += simt + (1 if gp.summary[6] else 0)
+            n += sum(simt + (1 if int(h[53 + i]) else 0) for i in range(len(gp.h_outs)))
+        return n * self.model.layers
 
     @staticmethod
     def _check_io(x: torch.Tensor, y: torch.Tensor, h_in: int, h_out: int, n: int) -> None:
@@ -150,13 +192,18 @@ class LoraDeltaEngine:
             raise ValueError("x and y rows must be contiguous")
 
 
-INPUT_GROUPS = {"q_proj": "attn_in", "k_proj": "attn_in", "v_proj": "attn_in", "o_proj": "attn_out",
-                "gate_proj": "mlp_in", "up_proj": "mlp_in", "down_proj": "mlp_mid"}
-
-
-def input_group(proj_name: str) -> str:
-    """Which activation a projection reads (q/k/v share the attention input, gate/up the MLP input)."""
-    return INPUT_GROUPS.get(proj_name, proj_name)
+def moved_bytes(seg: Segments, model: ModelShape) -> int:
+    """Bytes one layer moves with input-group fusion: x read once per group, A/B once per segment,
+    y read+write per projection (v and metadata excluded)."""
+    n = seg.lengths().astype(np.int64)
+    r = seg.seg_rank.astype(np.int64)
+    total = 0
+    for _, members in model.groups():
+        total += int(np.sum(2 * n * model.projections[members[0]].h_in))
+        for p in members:
+            pr = model.projections[p]
+            total += int(np.sum(2 * r * pr.h_in + 2 * r * pr.h_out + 4 * n * pr.h_out))
+    return total
 
 
 def algorithmic_bytes(seg: Segments, h_in: int, h_out: int) -> int:

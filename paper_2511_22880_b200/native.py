@@ -14,10 +14,12 @@ import os
 from pathlib import Path
 
 LIB_NAME = "liblsv.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+# LSV_LIB_PATH: development override (A/B timing of two builds of the same library on one box)
+LIB_PATH = Path(os.environ.get("LSV_LIB_PATH") or Path(__file__).resolve().parent / LIB_NAME)
 
 LSV_OK, LSV_EINVAL, LSV_ECUDA, LSV_EUNSUPPORTED, LSV_EWORKSPACE = 0, 1, 2, 3, 4
 LSV_DTYPE_BF16 = 0
+ABI_VERSION = 2
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 
 # every symbol include/lsv.h declares (tests/test_native_abi.py checks the library exports them)
@@ -27,6 +29,8 @@ EXPORTED_SYMBOLS = (
     "lsv_plan_summary", "lsv_lora_apply", "lsv_lora_shrink", "lsv_lora_expand",
     "lsv_enable_peer", "lsv_num_sms", "lsv_ipc_get_handle", "lsv_ipc_open_handle", "lsv_ipc_close_handle",
     "lsv_slab_alloc", "lsv_slab_free", "lsv_vimg_assemble", "lsv_plan_vimg_region",
+    "lsv_adapter_a_group_bytes", "lsv_pack_adapter_group", "lsv_unpack_adapter_group",
+    "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj",
 )
 
 _lib = None
@@ -56,6 +60,13 @@ _SIGNATURES = {
     "lsv_plan_vimg_region": (ctypes.c_int, [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
     "lsv_ipc_open_handle": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_vp)]),
     "lsv_ipc_close_handle": (ctypes.c_int, [_vp]),
+    "lsv_adapter_a_group_bytes": (_sz, [_i32, _i32, _i32]),
+    "lsv_pack_adapter_group": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "lsv_unpack_adapter_group": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "lsv_plan_size_group": (ctypes.c_int, [_i32, _vp, _vp, _i32, _i32, _vp, _i32, ctypes.POINTER(_sz),
+                                           ctypes.POINTER(_sz)]),
+    "lsv_plan_build_group": (ctypes.c_int, [_i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _sz]),
+    "lsv_lora_expand_proj": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
 
 
@@ -76,8 +87,8 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.lsv_version() != 1:
-            raise RuntimeError(f"liblsv ABI version {lib.lsv_version()} != 1")
+        if lib.lsv_version() != ABI_VERSION:
+            raise RuntimeError(f"liblsv ABI version {lib.lsv_version()} != {ABI_VERSION}")
         _lib = lib
     return _lib
 

@@ -16,11 +16,32 @@ class Projection:
     h_out: int
 
 
+# Which activation each projection reads: q/k/v share the attention input, gate/up the MLP input.
+INPUT_GROUPS = {"q_proj": "attn_in", "k_proj": "attn_in", "v_proj": "attn_in", "o_proj": "attn_out",
+                "gate_proj": "mlp_in", "up_proj": "mlp_in", "down_proj": "mlp_mid"}
+
+
+def input_group(proj_name: str) -> str:
+    return INPUT_GROUPS.get(proj_name, proj_name)
+
+
 @dataclass(frozen=True)
 class ModelShape:
     name: str
     layers: int
     projections: tuple[Projection, ...]
+
+    def groups(self) -> list[tuple[str, tuple[int, ...]]]:
+        """Input groups: runs of consecutive projections that read the same activation (same h_in).
+        Their A matrices share one slab tile and one shrink (include/lsv.h, lsv_plan_build_group)."""
+        out: list[tuple[str, list[int]]] = []
+        for i, p in enumerate(self.projections):
+            g = input_group(p.name)
+            if out and out[-1][0] == g and self.projections[out[-1][1][0]].h_in == p.h_in and len(out[-1][1]) < 4:
+                out[-1][1].append(i)
+            else:
+                out.append((g, [i]))
+        return [(g, tuple(m)) for g, m in out]
 
     def shapes(self) -> list[tuple[int, int]]:
         """Distinct (h_in, h_out) pairs, in first-use order (one plan each)."""

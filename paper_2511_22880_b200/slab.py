@@ -5,7 +5,9 @@ Reference: ``AdapterPool`` keeps, per server, an LRU set of GPU-resident adapter
 pool.py:20) and prices making one resident (``plan_fetch`` pool.py:101-132,
 ``fetch_latency`` costmodel.py:129-143).  Here a resident adapter is real memory: for every
 layer and projection of the model, its lora_A/lora_B packed once into the tiled layouts the
-kernels move with single bulk copies (include/lsv.h ``lsv_pack_adapter``).  Slots are
+kernels move with single bulk copies (include/lsv.h ``lsv_pack_adapter``).  The A matrices of the
+projections that read the same activation (q/k/v, gate/up: ``ModelShape.groups``) share one group
+tile per layer (``lsv_pack_adapter_group``), so one shrink reads x once for all of them.  Slots are
 allocated from one large device buffer sized for B200's 180 GB of HBM; a segment's A/B
 pointers are ``base + offset`` — or an NVLink peer address when the adapter lives in another
 GPU's slab (the reference's ``fetch_remote``).
@@ -54,6 +56,8 @@ class AdapterSlab:
         self.by_id: dict[str, int] = {}
         self._cursor = 0
         self._a_off_rows: list[np.ndarray] = []   # per slot: [layers, projections] byte offsets
+        self._g_off_rows: list[np.ndarray] = []   # per slot: [layers, input groups] group A tiles
+        self._member = {p: (gi, i, len(m)) for gi, (_, m) in enumerate(model.groups()) for i, p in enumerate(m)}
         self._b_off_rows: list[np.ndarray] = []
         self._slot_offsets_dev: tuple[torch.Tensor, torch.Tensor] | None = None
 
@@ -83,25 +87,36 @@ class AdapterSlab:
         self.slots.append(SlotInfo(slot, adapter_id, rank, start, nbytes))
         self.by_id[adapter_id] = slot
         L, P = self.model.layers, len(self.model.projections)
+        groups = self.model.groups()
         a_off = np.empty((L, P), dtype=np.int64)
+        g_off = np.empty((L, len(groups)), dtype=np.int64)
         b_off = np.empty((L, P), dtype=np.int64)
         cur = start
         kp = kpad(rank)
         for l in range(L):
-            for p, pr in enumerate(self.model.projections):
-                a_off[l, p] = cur
-                cur += 2 * rank * pr.h_in
-                b_off[l, p] = cur
-                cur += 2 * kp * pr.h_out
+            for gi, (_, members) in enumerate(groups):
+                # one group A tile [h_in/64][len(members)*rank][64]: member i's rows start at i*rank
+                g_off[l, gi] = cur
+                for i, p in enumerate(members):
+                    a_off[l, p] = cur + i * rank * 128
+                cur += 2 * len(members) * rank * self.model.projections[members[0]].h_in
+                for p in members:
+                    b_off[l, p] = cur
+                    cur += 2 * kp * self.model.projections[p].h_out
         assert cur - start == nbytes
         self._a_off_rows.append(a_off)
+        self._g_off_rows.append(g_off)
         self._b_off_rows.append(b_off)
         self._cursor = start + nbytes
         self._slot_offsets_dev = None
         return slot
 
     def a_offset(self, slot: int, layer: int, proj: int) -> int:
+        """Offset of proj's first A row inside its group tile (rows repeat every group*rank rows)."""
         return int(self._a_off_rows[slot][layer, proj])
+
+    def a_group_offset(self, slot: int, layer: int, proj: int) -> int:
+        return int(self._g_off_rows[slot][layer, self._member[proj][0]])
 
     def b_offset(self, slot: int, layer: int, proj: int) -> int:
         return int(self._b_off_rows[slot][layer, proj])
@@ -121,10 +136,12 @@ class AdapterSlab:
         lora_a = lora_a.contiguous()
         lora_b = lora_b.contiguous()
         st = stream or torch.cuda.current_stream(self.device)
-        native.check(native.lib().lsv_pack_adapter(
-            lora_a.data_ptr(), lora_b.data_ptr(), r, pr.h_in, pr.h_out,
-            self.base + self.a_offset(slot, layer, proj), self.base + self.b_offset(slot, layer, proj),
-            st.cuda_stream))
+        _, idx, nproj = self._member[proj]
+        lib = native.lib()
+        native.check(lib.lsv_pack_adapter_group(lora_a.data_ptr(), nproj, idx, r, pr.h_in,
+                                                self.base + self.a_group_offset(slot, layer, proj), st.cuda_stream))
+        native.check(lib.lsv_pack_adapter(None, lora_b.data_ptr(), r, pr.h_in, pr.h_out, None,
+                                          self.base + self.b_offset(slot, layer, proj), st.cuda_stream))
 
     def read(self, slot: int, layer: int, proj: int) -> tuple[torch.Tensor, torch.Tensor]:
         """Unpack a resident adapter back to PEFT layout (tests, migration checks)."""
@@ -132,10 +149,13 @@ class AdapterSlab:
         pr = self.model.projections[proj]
         a = torch.empty((info.rank, pr.h_in), dtype=torch.bfloat16, device=self.device)
         b = torch.empty((pr.h_out, info.rank), dtype=torch.bfloat16, device=self.device)
-        native.check(native.lib().lsv_unpack_adapter(
-            self.base + self.a_offset(slot, layer, proj), self.base + self.b_offset(slot, layer, proj),
-            info.rank, pr.h_in, pr.h_out, a.data_ptr(), b.data_ptr(),
-            torch.cuda.current_stream(self.device).cuda_stream))
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _, idx, nproj = self._member[proj]
+        lib = native.lib()
+        native.check(lib.lsv_unpack_adapter_group(self.base + self.a_group_offset(slot, layer, proj), nproj, idx,
+                                                  info.rank, pr.h_in, a.data_ptr(), st))
+        native.check(lib.lsv_unpack_adapter(None, self.base + self.b_offset(slot, layer, proj), info.rank, pr.h_in,
+                                            pr.h_out, None, b.data_ptr(), st))
         return a, b
 
     def fill_random(self, slot: int, seed: int, layers: range | None = None) -> None:
@@ -193,19 +213,20 @@ class AdapterSlab:
     # -- pointer tables ----------------------------------------------------------------
     def pointer_tables(self, seg_slots: np.ndarray, peer_slabs: dict[int, "AdapterSlab"] | None = None,
                        seg_owner: np.ndarray | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-        """Device int64 tables [layers*projections, S] of A and B pointers for the segments.
+        """Device int64 tables for the segments: group A tiles [layers*groups, S] (model.groups())
+        and B tiles [layers*projections, S].
 
         ``seg_owner[s]`` (optional) names the GPU whose slab holds segment s; entries other than
         this slab's device resolve through ``peer_slabs`` to NVLink peer addresses."""
-        L, P = self.model.layers, len(self.model.projections)
+        L, P, G = self.model.layers, len(self.model.projections), len(self.model.groups())
         S = len(seg_slots)
-        a = np.empty((L * P, S), dtype=np.int64)
+        a = np.empty((L * G, S), dtype=np.int64)
         b = np.empty((L * P, S), dtype=np.int64)
         for s, slot in enumerate(np.asarray(seg_slots)):
             slab = self
             if seg_owner is not None and peer_slabs is not None and int(seg_owner[s]) in peer_slabs:
                 slab = peer_slabs[int(seg_owner[s])]
-            a[:, s] = (slab.base + slab._a_off_rows[int(slot)]).reshape(-1)
+            a[:, s] = (slab.base + slab._g_off_rows[int(slot)]).reshape(-1)
             b[:, s] = (slab.base + slab._b_off_rows[int(slot)]).reshape(-1)
         return (torch.from_numpy(a).to(self.device, non_blocking=False),
                 torch.from_numpy(b).to(self.device, non_blocking=False))

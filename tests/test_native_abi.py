@@ -20,7 +20,7 @@ def test_library_exports_header_symbols():
     assert declared == set(native.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.lsv_version() == 1
+    assert lib.lsv_version() == native.ABI_VERSION
 
 
 def _plan(indptr, ranks, h_in=4096, h_out=4096, policy=0):
@@ -125,3 +125,76 @@ def test_apply_rejects_missing_plan():
     rc = lib.lsv_lora_apply(None, 0, None, 0, 7, 0, 4096, 4096, None, None, None, None, None, 0, None)
     with pytest.raises(RuntimeError):
         native.check(rc)
+
+
+def _plan_group(indptr, ranks, h_in, h_outs, policy=0):
+    lib = native.load()
+    indptr = np.asarray(indptr, dtype=np.int32)
+    ranks = np.asarray(ranks, dtype=np.int32)
+    hs = np.asarray(h_outs, dtype=np.int32)
+    pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
+    native.check(lib.lsv_plan_size_group(len(ranks), indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs),
+                                         hs.ctypes.data, policy, ctypes.byref(pb), ctypes.byref(wb)))
+    blob = np.zeros(pb.value // 4, dtype=np.int32)
+    native.check(lib.lsv_plan_build_group(len(ranks), indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs),
+                                          hs.ctypes.data, policy, blob.ctypes.data, pb.value))
+    return blob, wb.value
+
+
+def test_group_plan_covers_every_projection():
+    """A q/k/v group plan (Llama-3-70B-like widths: k/v narrower): every (m-tile, projection,
+    chunk) is shrunk exactly once, records never exceed one N=256 MMA, rank 128 x 3 splits into
+    {q,k} + {v}, and each projection has its own expand list over its own h_out tiles."""
+    rng = np.random.default_rng(1)
+    ranks = [8] * 20 + [16] * 10 + [64] * 5 + [128] * 5
+    lens = rng.integers(9, 90, len(ranks))
+    lens[2] = 3                                  # SIMT
+    lens[-1] = 200                               # two m-tiles
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    h_outs = [4096, 1024, 1024]
+    blob, ws = _plan_group(indptr, ranks, 4096, h_outs)
+    h = blob[:64]
+    P = int(h[33])
+    assert P == 3 and list(h[37:40]) == h_outs
+    d = _decode(blob)
+    chunks = 4096 // 64
+    seen = {}
+    for rec in d["shrink"]:
+        mt, p0, npj, r = int(rec[12]), int(rec[13]), int(rec[14]), int(rec[3])
+        assert 1 <= npj and p0 + npj <= P and npj * r <= 256
+        for pp in range(p0, p0 + npj):
+            seen.setdefault((mt, pp), []).append((int(rec[4]), int(rec[5])))
+    for i, mt in enumerate(d["mtiles"]):
+        r = int(mt[3])
+        for pp in range(P):
+            parts = sorted(seen[(i, pp)])
+            assert parts[0][0] == 0 and parts[-1][1] == chunks
+            assert all(parts[j][1] == parts[j + 1][0] for j in range(len(parts) - 1))
+        subsets = {(int(rec[13]), int(rec[14])) for rec in d["shrink"] if int(rec[12]) == i}
+        assert subsets == ({(0, 2), (2, 1)} if r == 128 else {(0, 3)})
+    off_recs, off_cta, grids, nitems = h[41:45], h[45:49], h[49:53], h[53:57]
+    for pp in range(P):
+        tw = 256 if h_outs[pp] % 256 == 0 else 128
+        recs = blob[off_recs[pp]:off_recs[pp] + 8 * nitems[pp]].reshape(-1, 8)
+        assert {(int(r[6]), int(r[4])) for r in recs} == {(i, j) for i in range(d["n_mtiles"]) for j in range(h_outs[pp] // tw)}
+        cta = blob[off_cta[pp]:off_cta[pp] + grids[pp] + 1]
+        assert cta[0] == 0 and cta[-1] == nitems[pp]
+    # workspace: P v-image regions of vimg_stride bytes each
+    assert int(h[34]) % 1024 == 0 and ws >= int(h[34]) * P
+
+
+def test_group_plan_of_one_is_the_single_plan():
+    ranks = [8, 16, 64, 128]
+    indptr = [0, 40, 90, 130, 300]
+    a, wa = _plan(indptr, ranks, 4096, 11008)
+    b, wb = _plan_group(indptr, ranks, 4096, [11008])
+    assert wa == wb and np.array_equal(a, b)
+
+
+def test_group_pack_rejects_bad_member():
+    lib = native.load()
+    with pytest.raises(ValueError):
+        native.check(lib.lsv_pack_adapter_group(None, 3, 3, 8, 4096, None, None))
+    with pytest.raises(ValueError):
+        native.check(lib.lsv_pack_adapter_group(None, 5, 0, 8, 4096, None, None))
+    assert lib.lsv_adapter_a_group_bytes(3, 16, 4096) == 3 * 16 * 4096 * 2

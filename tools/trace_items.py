@@ -1,0 +1,35 @@
+"""All per-item stamps of one expand launch for one CTA (clock64 cycles, relative): producer start /
+issued, MMA got tempty / got full / MMAs issued / committed, epilogue got tfull / done."""
+import sys, ctypes
+import numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2511_22880_b200 import native
+from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+from paper_2511_22880_b200.slab import AdapterSlab
+from paper_2511_22880_b200.lora import LoraDeltaEngine
+from paper_2511_22880_b200.segments import index_tokens
+model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections); dev = torch.device("cuda:0")
+ranks = [8]*44+[16]*22+[32]*14+[64]*11+[128]*9
+slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+for i, r in enumerate(ranks):
+    s = slab.allocate(f"a{i}", r); slab.fill_random(s, 1000+i)
+seg = index_tokens(np.random.default_rng(0).integers(0, 100, 4096), ranks)
+eng = LoraDeltaEngine(slab); bp = eng.prepare(seg)
+lib = native.lib(); lib.lsv_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+ITEMS = 64
+proj = int(sys.argv[1]); pr = model.projections[proj]
+x = torch.randn(4096, pr.h_in, device=dev).to(torch.bfloat16); y = torch.zeros(4096, pr.h_out, device=dev, dtype=torch.bfloat16)
+for _ in range(3): eng.apply(bp, 0, proj, x, y)
+torch.cuda.synchronize()
+buf = torch.zeros(148 * ITEMS * 16, dtype=torch.int64, device=dev)
+lib.lsv_debug_set_trace(buf.data_ptr(), ITEMS)
+eng.expand(bp, 0, proj, y); torch.cuda.synchronize(); lib.lsv_debug_set_trace(None, 0)
+tr = buf.view(148, ITEMS, 16).cpu().numpy().astype(np.int64)
+for c in (0, 77):
+    cyc = tr[c, :ITEMS - 1, 8:16]
+    n = int((cyc[:, 0] > 0).sum()); t0 = cyc[0, 0]
+    print(f"cta {c}: {n} items (cycles rel. to item0 producer start)")
+    print("   k  prod0  prod1 | mma_te mma_fu mma_is mma_cm | epi_in epi_out")
+    for i in range(min(n, 14)):
+        v = cyc[i] - t0
+        print(f"  {i:2d} {v[0]:6d} {v[1]:6d} | {v[5]:6d} {v[6]:6d} {v[7]:6d} {v[2]:6d} | {v[3]:6d} {v[4]:6d}")
