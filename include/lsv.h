@@ -156,6 +156,13 @@ int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out,
                     const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
                     void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
+/* Expand of every member of a group plan in one launch (one LPT work list over all members'
+ * items): ys / ldys / b_ptrs are HOST arrays of num_proj entries (member i's y, its row stride and
+ * its device table of per-segment B pointers). */
+int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_tokens,
+                          const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                          void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
 /* Expand of member `proj` of a group plan (lsv_lora_expand is proj = 0). */
 int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,
                          const void* const* b_ptrs, const void* plan_dev, const void* plan_host,

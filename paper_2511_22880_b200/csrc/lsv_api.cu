@@ -78,6 +78,8 @@ struct PlanBuilder {
   std::vector<int32_t> shrink_cta;   // [grid+1]
   std::vector<ExpandRec> expand[kMaxProj];
   std::vector<int32_t> expand_cta[kMaxProj];
+  std::vector<ExpandRec> expand_all;   // every member's items, one LPT assignment
+  std::vector<int32_t> expand_all_cta;
   std::vector<int32_t> red;          // {mtile, first unit} per split tile
   int32_t red_units = 0;
   std::vector<int32_t> red_cta;
@@ -229,8 +231,9 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
   lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta);
 
-  // expand: per projection, items = (m-tile, tw-wide h_out tile)
+  // expand: per projection, items = (m-tile, tw-wide h_out tile); plus all members in one list
   int expand_grid[kMaxProj] = {0, 0, 0, 0};
+  std::vector<std::pair<int64_t, ExpandRec>> all_costed;
   for (int p = 0; p < P; ++p) {
     std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
     const int tw = b_tile_width(h_outs[p]);
@@ -240,15 +243,19 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
       for (int jt = 0; jt < h_outs[p] / tw; ++jt) {
         ExpandRec r{};
         r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
-        r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i;
+        r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i; r.proj = p;
         expand_costed.push_back({cost, r});
       }
     }
+    all_costed.insert(all_costed.end(), expand_costed.begin(), expand_costed.end());
     std::stable_sort(expand_costed.begin(), expand_costed.end(),
                      [](const auto& a, const auto& b) { return a.first > b.first; });
     expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
     lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p]);
   }
+  std::stable_sort(all_costed.begin(), all_costed.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  const int expand_grid_all = (int)std::min<size_t>(all_costed.size(), (size_t)nsm);
+  lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta);
 
   // header + workspace layout
   PlanHeader& h = pb.h;
@@ -277,6 +284,11 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     h.off_expand_recs_p[p] = off; off += 8 * h.n_expand_items_p[p];
     h.off_expand_cta_p[p] = off; off += (int32_t)pb.expand_cta[p].size();
   }
+  off = round_up(off, 4);
+  h.n_expand_all = (int32_t)pb.expand_all.size();
+  h.expand_grid_all = expand_grid_all;
+  h.off_expand_recs_all = off; off += 8 * h.n_expand_all;
+  h.off_expand_cta_all = off; off += (int32_t)pb.expand_all_cta.size();
   h.n_expand_items = h.n_expand_items_p[0];
   h.expand_grid = h.expand_grid_p[0];
   h.off_expand_recs = h.off_expand_recs_p[0];
@@ -459,28 +471,43 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
   return LSV_OK;
 }
 
-int run_expand(const PlanHeader* h, int proj, void* y, int64_t ldy, int32_t num_tokens, const void* const* b_ptrs,
-               const int32_t* plan, uint8_t* ws, cudaStream_t st) {
-  const int h_out = h->h_outs[proj];
-  if (h->n_simt_items > 0) {
+// Expand of members [p0, p0 + np) of a plan: np == num_proj uses the combined list (one launch
+// for every member), np == 1 member p0's own list.
+int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys, int32_t num_tokens,
+               const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st) {
+  for (int i = 0; i < np && h->n_simt_items > 0; ++i) {
+    const int pp = p0 + i, h_out = h->h_outs[pp];
     simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 511) / 512), 64, 0, st>>>(
-        static_cast<__nv_bfloat16*>(y), ldy, h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs,
-        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)proj * h->simt_stride);
+        static_cast<__nv_bfloat16*>(ys[i]), ldys[i], h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs[i],
+        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
-  if (h->n_expand_items_p[proj] > 0) {
-    if (int rc = ensure_smem_attrs()) return rc;
-    ExpandParams p{};
-    if (int rc = get_maps(p.ymap, 0, y, ldy, num_tokens, h_out)) return rc;
-    p.plan = plan; p.b_ptrs = b_ptrs; p.ws = ws; p.y = static_cast<__nv_bfloat16*>(y); p.ldy = ldy;
-    p.off_recs = h->off_expand_recs_p[proj]; p.off_cta = h->off_expand_cta_p[proj];
-    p.ws_vimg = h->ws_vimg + proj * h->vimg_stride;
-    p.tw = b_tile_width(h_out);
-    p.dbg = g_debug_expand;
-    p.trace = g_trace; p.trace_items = g_trace_items;
-    LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, h->expand_grid_p[proj], expand_smem_bytes(), st, p));
-    LSV_CUDA_CHECK(cudaGetLastError());
+  const bool all = np == h->num_proj && np > 1;
+  const int n_items = all ? h->n_expand_all : h->n_expand_items_p[p0];
+  if (n_items == 0) return LSV_OK;
+  if (int rc = ensure_smem_attrs()) return rc;
+  ExpandParams p{};
+  int tw_max = 0;
+  for (int pp = 0; pp < h->num_proj; ++pp) {
+    const int i = all ? pp : (pp == p0 ? 0 : -1);
+    if (i < 0) continue;
+    if (int rc = get_maps(p.ymap[pp], 0, ys[i], ldys[i], num_tokens, h->h_outs[pp])) return rc;
+    p.y[pp] = static_cast<__nv_bfloat16*>(ys[i]);
+    p.ldy[pp] = ldys[i];
+    p.b_ptrs[pp] = b_ptrs[i];
+    p.tws[pp] = b_tile_width(h->h_outs[pp]);
+    p.ws_vimg[pp] = h->ws_vimg + pp * h->vimg_stride;
+    tw_max = std::max(tw_max, p.tws[pp]);
   }
+  p.plan = plan; p.ws = ws;
+  p.off_recs = all ? h->off_expand_recs_all : h->off_expand_recs_p[p0];
+  p.off_cta = all ? h->off_expand_cta_all : h->off_expand_cta_p[p0];
+  p.tw_max = tw_max;
+  p.dbg = g_debug_expand;
+  p.trace = g_trace; p.trace_items = g_trace_items;
+  LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, all ? h->expand_grid_all : h->expand_grid_p[p0], expand_smem_bytes(),
+                            st, p));
+  LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
 
@@ -569,6 +596,8 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
     std::memcpy(out + h.off_expand_recs_p[p], pb.expand[p].data(), pb.expand[p].size() * sizeof(ExpandRec));
     std::copy(pb.expand_cta[p].begin(), pb.expand_cta[p].end(), out + h.off_expand_cta_p[p]);
   }
+  std::memcpy(out + h.off_expand_recs_all, pb.expand_all.data(), pb.expand_all.size() * sizeof(ExpandRec));
+  std::copy(pb.expand_all_cta.begin(), pb.expand_all_cta.end(), out + h.off_expand_cta_all);
   std::copy(pb.red.begin(), pb.red.end(), out + h.off_red);
   std::copy(pb.red_cta.begin(), pb.red_cta.end(), out + h.off_red_cta);
   return LSV_OK;
@@ -641,7 +670,28 @@ int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out
   if (h->num_tokens == 0) return LSV_OK;
   if (!y || !b_ptrs) return fail(LSV_EINVAL, "y / b_ptrs must be non-null");
   if (!aligned16(y) || ldy % 8 || ldy < h_out) return fail(LSV_EINVAL, "y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out");
-  return run_expand(h, proj, y, ldy, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev),
+  void* ys[1] = {y};
+  const int64_t ldys[1] = {ldy};
+  const void* const* bt[1] = {b_ptrs};
+  return run_expand(h, proj, 1, ys, ldys, num_tokens, bt, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_tokens, const void* const* const* b_ptrs,
+                          const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                          lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (!ys || !ldys || !b_ptrs) return fail(LSV_EINVAL, "ys / ldys / b_ptrs must be non-null host arrays");
+  if (num_tokens < h->num_tokens)
+    return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (h->num_tokens == 0) return LSV_OK;
+  for (int pp = 0; pp < h->num_proj; ++pp) {
+    if (!ys[pp] || !b_ptrs[pp]) return fail(LSV_EINVAL, "member %d: y / b_ptrs must be non-null", pp);
+    if (!aligned16(ys[pp]) || ldys[pp] % 8 || ldys[pp] < h->h_outs[pp])
+      return fail(LSV_EINVAL, "member %d: y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out", pp);
+  }
+  return run_expand(h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev),
                     static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
 }
 

@@ -44,7 +44,8 @@ struct PlanHeader {            // 64 int32
   int32_t h_outs[kMaxProj];
   int32_t off_expand_recs_p[kMaxProj], off_expand_cta_p[kMaxProj];
   int32_t expand_grid_p[kMaxProj], n_expand_items_p[kMaxProj];
-  int32_t reserved[64 - 57];
+  int32_t off_expand_recs_all, off_expand_cta_all, expand_grid_all, n_expand_all;  // every member, one LPT list
+  int32_t reserved[64 - 61];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -72,7 +73,7 @@ struct ShrinkRec {             // 16 int32
 
 struct ExpandRec {             // 8 int32
   int32_t seg, tok_begin, ntok, rank;
-  int32_t jtile, vimg_off, mtile, pad;          // h_out columns [jtile*tw, jtile*tw+tw)
+  int32_t jtile, vimg_off, mtile, proj;         // member proj's h_out columns [jtile*tw, jtile*tw+tw)
 };
 
 // Pipeline geometry (bytes of shared memory).

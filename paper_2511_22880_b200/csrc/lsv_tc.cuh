@@ -45,14 +45,16 @@ struct alignas(64) ShrinkParams {
 };
 
 struct alignas(64) ExpandParams {
-  CUtensorMap ymap[5];          // y [num_tokens][h_out], boxes {64 cols × 8<<b rows}, SWIZZLE_128B
+  CUtensorMap ymap[kMaxProj][5];   // per member: y [num_tokens][h_out], boxes {64 cols x 8<<b rows}, SW128
   const int32_t* plan;
-  const void* const* b_ptrs;
+  const void* const* b_ptrs[kMaxProj];
   uint8_t* ws;
-  __nv_bfloat16* y;
-  int64_t ldy;
-  int off_recs, off_cta, ws_vimg;
-  int tw;                       // h_out tile width of the B slab layout (128 or 256)
+  __nv_bfloat16* y[kMaxProj];
+  int64_t ldy[kMaxProj];
+  int ws_vimg[kMaxProj];        // byte offset of each member's v images
+  int tws[kMaxProj];            // each member's h_out tile width (its B slab layout: 128 or 256)
+  int tw_max;                   // TMEM accumulator width
+  int off_recs, off_cta;
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -83,17 +85,20 @@ struct WarpRecBuf {
   const uint8_t* ptr[CH];
 };
 
+__device__ __forceinline__ int rec_table(const ShrinkRec&) { return 0; }
+__device__ __forceinline__ int rec_table(const ExpandRec& r) { return r.proj; }
+
 template <typename Rec, int CH>
 struct WarpRecStream {
   WarpRecBuf<Rec, CH>* buf;
   const Rec* recs;
-  const void* const* ptrs;
+  const void* const* const* tables;   // adapter pointer table of each member (nullptr: no pointers)
   int next, end, j, n;
   __device__ __forceinline__ WarpRecStream(WarpRecBuf<Rec, CH>* b, const int32_t* plan, int off_recs, int off_cta,
-                                           int cta, const void* const* adapter_ptrs) {
+                                           int cta, const void* const* const* adapter_tables) {
     buf = b;
     recs = reinterpret_cast<const Rec*>(plan + off_recs);
-    ptrs = adapter_ptrs;
+    tables = adapter_tables;
     next = plan[off_cta + cta];
     end = plan[off_cta + cta + 1];
     j = n = 0;
@@ -108,7 +113,7 @@ struct WarpRecStream {
       if (lane < n) {
         const Rec rr = recs[next + lane];
         buf->rec[lane] = rr;
-        buf->ptr[lane] = ptrs ? static_cast<const uint8_t*>(ptrs[rr.seg]) : nullptr;
+        buf->ptr[lane] = tables ? static_cast<const uint8_t*>(tables[rec_table(rr)][rr.seg]) : nullptr;
       }
       __syncwarp();
       next += n;
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
   if (warp == 0) {  // ---------------- producer: lane 0 owns the slot ring, lanes issue the copies
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, p.a_ptrs);
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
     ShrinkRec inf;
     const uint8_t* a;
     int slot = 0; uint32_t phase = 0;
@@ -392,9 +397,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tw = p.tw, nb = tw / 64;         // h_out tile width and its 64-column blocks
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
-  const int nbuf = kTmemCols / tw;           // TMEM accumulators in flight
+  const int nbuf = kTmemCols / p.tw_max;     // TMEM accumulators in flight
   // No ring zeroing is needed: B tiles are stored padded to kp rows (zeros past the rank) and
   // every other over-read (v rows past the tile's tokens) only feeds discarded D rows.
   // identity A tile, K-major SWIZZLE_32B [256 rows][16 k]: 1.0 at (128 + k, k)
@@ -407,7 +411,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
     for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_mbar_init();
-    for (int b = 0; b < 5; ++b) prefetch_tmap(&p.ymap[b]);
+    for (int pp = 0; pp < kMaxProj; ++pp)
+      if (p.y[pp])
+        for (int b = 0; b < 5; ++b) prefetch_tmap(&p.ymap[pp][b]);
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
@@ -428,6 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
     uint32_t vbegin[kItemQ];
     int retired = 0;
     for (int k = 0; rs.pop(inf, b); ++k) {
+      const int tw = p.tws[inf.proj], nb = tw / 64;
       const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
       const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2, ybytes = nb * np16 * 128;
       const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
       if (lane == 0) {
         if (!(dbg & 16)) bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
       } else if (lane == 1) {
-        if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg + inf.vimg_off, vbytes, &full[qs]);
+        if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, &full[qs]);
       } else if (!(dbg & 8)) {
         // y rows [tok_begin, tok_begin + np16) as nb 64-column SWIZZLE_128B blocks; each block is
         // np16/8 = sum of powers of two 8-row groups -> one TMA box per set bit, one lane per box
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
             bb = 31 - __clz(mm);
             if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
           }
-          tma_load_2d(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[bb], &full[qs],
+          tma_load_2d(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
                       inf.jtile * tw + h * 64, inf.tok_begin + row);
         }
       }
@@ -485,9 +492,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
     ExpandRec inf;
     const uint8_t* unused;
     const uint32_t ib = smem_u32(ident);
-    const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
     for (int k = 0; rs.pop(inf, unused); ++k) {
       if (lane == 0) {
+        const int tw = p.tws[inf.proj], nb = tw / 64;
+        const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
         const int qs = k % kItemQ;
         const int r = inf.rank, kp = kpad(r), np16 = round_up(inf.ntok, 16);
         const int S = kmajor_row_bytes(kp), ck = S / 2;
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
         const uint32_t voff = round_up(tw * kp * 2, 1024);
         const uint32_t vb = bb + voff;
         const uint32_t yb = bb + round_up(voff + np16 * kp * 2, 1024);
-        const uint32_t d = tmem_base + buf * tw;
+        const uint32_t d = tmem_base + buf * p.tw_max;
         // D = v . B : A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128)
         const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
         for (int ks = 0; ks < nv; ++ks) {
@@ -536,9 +544,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
       if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const int t = q * 32 + lane;
       if (q * 32 < inf.ntok) {   // warp-uniform: quadrants past the tile's tokens have no rows
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * tw;
+        const int tw = p.tws[inf.proj];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
         const bool valid = t < inf.ntok && !(p.dbg & 1);
-        __nv_bfloat16* yrow = p.y + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy + inf.jtile * tw;
+        __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
 #pragma unroll 1
         for (int cc = 0; cc < tw; cc += 32) {
           uint32_t r[32];

@@ -156,18 +156,34 @@ class LoraDeltaEngine:
             gp.plan_dev.data_ptr(), gp.plan_host.ctypes.data, bp.workspace.data_ptr(),
             bp.workspace.numel(), st.cuda_stream))
 
+    def expand_group(self, bp: BatchPlan, layer: int, gi: int, ys: list[torch.Tensor], stream=None) -> None:
+        """Every member of input group gi in one launch (one LPT list over all members' items)."""
+        gp = bp.group_plans[gi]
+        members = self.groups[gi][1]
+        S = bp.segments.num_segments
+        P = len(self.model.projections)
+        st = stream or torch.cuda.current_stream(self.device)
+        n = len(members)
+        y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+        ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys])
+        b_arr = (ctypes.c_void_p * n)(*[bp.b_ptrs.data_ptr() + (layer * P + p) * S * 8 for p in members])
+        native.check(native.lib().lsv_lora_expand_group(
+            ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys[0].shape[0], ctypes.addressof(b_arr),
+            gp.plan_dev.data_ptr(), gp.plan_host.ctypes.data, bp.workspace.data_ptr(), bp.workspace.numel(),
+            st.cuda_stream))
+
     def forward(self, bp: BatchPlan, xs: list[dict[str, torch.Tensor]], ys: list[dict[str, torch.Tensor]],
                 stream=None) -> None:
         """Every layer and projection: xs[l][input_group], ys[l][proj_name]."""
         projs = self.model.projections
         for layer in range(self.model.layers):
-            for gname, members in self.groups:
+            for gi, (gname, members) in enumerate(self.groups):
                 x = xs[layer][gname]
-                for p in members:
-                    self._check_io(x, ys[layer][projs[p].name], projs[p].h_in, projs[p].h_out, bp.num_tokens)
+                yl = [ys[layer][projs[p].name] for p in members]
+                for p, y in zip(members, yl):
+                    self._check_io(x, y, projs[p].h_in, projs[p].h_out, bp.num_tokens)
                 self.shrink(bp, layer, members[0], x, stream)
-                for p in members:
-                    self.expand(bp, layer, p, ys[layer][projs[p].name], stream)
+                self.expand_group(bp, layer, gi, yl, stream)
 
     def launches_per_step(self, bp: BatchPlan) -> int:
         """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand
@@ -176,8 +192,8 @@ class LoraDeltaEngine:
         for gp in bp.group_plans:
             simt = 1 if gp.summary[4] else 0
             h = gp.plan_host[:64]
-            n += simt + (1 if gp.summary[6] else 0)
-            n += sum(simt + (1 if int(h[53 + i]) else 0) for i in range(len(gp.h_outs)))
+            n += simt + (1 if gp.summary[6] else 0)                     # shrink
+            n += simt * len(gp.h_outs) + (1 if int(h[60]) else 0)       # expand: SIMT per member + one tcgen05
         return n * self.model.layers
 
     @staticmethod

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "lsv_enable_peer", "lsv_num_sms", "lsv_ipc_get_handle", "lsv_ipc_open_handle", "lsv_ipc_close_handle",
     "lsv_slab_alloc", "lsv_slab_free", "lsv_vimg_assemble", "lsv_plan_vimg_region",
     "lsv_adapter_a_group_bytes", "lsv_pack_adapter_group", "lsv_unpack_adapter_group",
-    "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj",
+    "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
 )
 
 _lib = None
@@ -67,6 +67,7 @@ _SIGNATURES = {
                                            ctypes.POINTER(_sz)]),
     "lsv_plan_build_group": (ctypes.c_int, [_i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _sz]),
     "lsv_lora_expand_proj": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "lsv_lora_expand_group": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
 
 

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-2
 
 
-def _run_group(cases, tier, dev="cuda:0"):
+def _run_group(cases, tier, dev="cuda:0", one_launch=False):
     from paper_2511_22880_b200 import native
     lib = native.load()
     P = len(cases)
@@ -61,13 +61,23 @@ def _run_group(cases, tier, dev="cuda:0"):
     x = c0.x.to(dev)
     native.check(lib.lsv_lora_shrink(x.data_ptr(), x.stride(0), x.shape[0], h_in, a_ptrs.data_ptr(),
                                      plan_dev.data_ptr(), plan.ctypes.data, ws.data_ptr(), ws.numel(), st))
-    outs = []
+    outs, tables = [], []
     for p, c in enumerate(cases):
         b_ptrs = torch.tensor([b_bufs[s][p].data_ptr() for s in range(S)], dtype=torch.int64, device=dev)
+        tables.append(b_ptrs)
         y = torch.zeros(c.n_tok, c.h_out, dtype=torch.bfloat16, device=dev)
-        native.check(lib.lsv_lora_expand_proj(y.data_ptr(), y.stride(0), y.shape[0], c.h_out, p, b_ptrs.data_ptr(),
-                                              plan_dev.data_ptr(), plan.ctypes.data, ws.data_ptr(), ws.numel(), st))
+        if not one_launch:
+            native.check(lib.lsv_lora_expand_proj(y.data_ptr(), y.stride(0), y.shape[0], c.h_out, p,
+                                                  b_ptrs.data_ptr(), plan_dev.data_ptr(), plan.ctypes.data,
+                                                  ws.data_ptr(), ws.numel(), st))
         outs.append(y)
+    if one_launch:   # lsv_lora_expand_group: every member in one launch
+        ya = (ctypes.c_void_p * P)(*[y.data_ptr() for y in outs])
+        la = (ctypes.c_int64 * P)(*[y.stride(0) for y in outs])
+        ba = (ctypes.c_void_p * P)(*[t.data_ptr() for t in tables])
+        native.check(lib.lsv_lora_expand_group(ctypes.addressof(ya), ctypes.addressof(la), outs[0].shape[0],
+                                               ctypes.addressof(ba), plan_dev.data_ptr(), plan.ctypes.data,
+                                               ws.data_ptr(), ws.numel(), st))
     torch.cuda.synchronize()
     return [o.float().cpu().numpy() for o in outs], plan
 
@@ -83,12 +93,12 @@ def _cases(lengths, ranks, seed, h_outs=(4096, 1024, 1024), h_in=4096):
     return cases
 
 
-@pytest.mark.parametrize("tier", [0, 1, 2])
-def test_qkv_group_matches_oracle(tier):
+@pytest.mark.parametrize("tier,one_launch", [(0, False), (1, False), (2, False), (0, True), (2, True)])
+def test_qkv_group_matches_oracle(tier, one_launch):
     lengths = [41, 3, 130, 64, 17, 9, 200, 0, 45]
     ranks = [8, 16, 128, 64, 24, 32, 128, 8, 40]
     cases = _cases(lengths, ranks, seed=11)
-    outs, plan = _run_group(cases, tier)
+    outs, plan = _run_group(cases, tier, one_launch=one_launch)
     n = cases[0].seg.num_tokens
     for p, c in enumerate(cases):
         err = oracle.max_rel_err(outs[p][:n], c.oracle_delta()[:n])
@@ -101,7 +111,7 @@ def test_gate_up_group_split_k():
     lengths = [128, 128, 96, 64]
     ranks = [128, 64, 16, 8]
     cases = _cases(lengths, ranks, seed=12, h_outs=(11008, 11008))
-    outs, plan = _run_group(cases, 0)
+    outs, plan = _run_group(cases, 0, one_launch=True)
     n = cases[0].seg.num_tokens
     assert int(plan[30]) > 0   # n_red: split tiles present
     for p, c in enumerate(cases):
