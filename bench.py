@@ -282,31 +282,41 @@ def run_ours(args, rank, world, local_rank):
         step_bytes, step_flops, step_moved = int(t[0].item()), int(t[1].item()), int(t[2].item())
     hbm_peak, peak_src = peaks()
 
-    # ---- dominant kernel roofline: expand (tcgen05) on the largest projection, CUDA events ----
-    big = max(range(len(model.projections)), key=lambda p: model.projections[p].h_out * model.projections[p].h_in)
-    pr = model.projections[big]
+    # ---- dominant kernel roofline: the one-launch expand of the input group with the most expand
+    # bytes (gate/up on Llama), timed with CUDA events on its stream; its group's fused shrink beside it
     n_l = seg.lengths().astype(np.int64)
     r_l = seg.seg_rank.astype(np.int64)
-    exp_bytes = int(np.sum(2 * r_l * pr.h_out + 4 * n_l * pr.h_out))
-    n_members = len(next(m for _, m in model.groups() if big in m))   # the fused shrink covers the group
-    shr_bytes = int(np.sum(2 * n_l * pr.h_in + 2 * n_members * r_l * pr.h_in))
+    groups = model.groups()
+
+    def grp_expand_bytes(members):
+        return sum(int(np.sum(2 * r_l * model.projections[p].h_out + 4 * n_l * model.projections[p].h_out))
+                   for p in members)
+    gi = max(range(len(groups)), key=lambda i: grp_expand_bytes(groups[i][1]))
+    gname, members = groups[gi]
+    exp_bytes = grp_expand_bytes(members)
+    h_in = model.projections[members[0]].h_in
+    shr_bytes = int(np.sum(2 * n_l * h_in + 2 * len(members) * r_l * h_in))
+    names = "/".join(model.projections[p].name for p in members)
+    ylist = [ys[0][model.projections[p].name] for p in members]
     reps = 20
     with torch.cuda.stream(stream):
-        eng.shrink(bp, 0, big, xs[0][input_group(pr.name)], stream)
+        eng.shrink(bp, 0, members[0], xs[0][gname], stream)
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k0.record(stream)
         for _ in range(reps):
-            eng.expand(bp, 0, big, ys[0][pr.name], stream)
+            eng.expand_group(bp, 0, gi, ylist, stream)
         k1.record(stream)
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(reps):
-            eng.shrink(bp, 0, big, xs[0][input_group(pr.name)], stream)
+            eng.shrink(bp, 0, members[0], xs[0][gname], stream)
         s1.record(stream)
     torch.cuda.synchronize(dev)
     exp_us = k0.elapsed_time(k1) / reps * 1e3
     shr_us = s0.elapsed_time(s1) / reps * 1e3
     achieved = exp_bytes / (exp_us * 1e-6) / 1e9
+    exp_label = f"expand_tc_kernel ({names}, one launch)"
+    traffic = measured_traffic(config, exp_label)
 
     # ---- e2e through the public API with host buffers ----
     from paper_2511_22880_b200.segments import index_tokens as _ix
@@ -375,11 +385,13 @@ def run_ours(args, rank, world, local_rank):
                      "moved_bytes": step_moved, "moved_frac": step_moved / (ms * 1e-3) / 1e9 / (hbm_peak * world),
                      "note": "whole-job algorithmic bytes (SURVEY 8d, x per projection) / step time / (peak x GPUs); "
                              "moved: x once per input group (q/k/v, gate/up share one fused shrink)"},
-        "roofline": {"bound": "hbm", "kernel": f"expand_tc_kernel ({pr.name} {pr.h_in}->{pr.h_out})",
+        "roofline": {"bound": "hbm", "kernel": exp_label,
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "launch_us": exp_us,
+                     "frac": achieved / hbm_peak, "traffic": traffic, "launch_us": exp_us,
                      "algorithmic_bytes_per_launch": exp_bytes,
-                     "shrink": {"kernel": f"shrink_tc_kernel (fused {n_members}-projection group of {pr.name})",
+                     "traffic_source": "profiles/traffic_r1.json: dram__bytes_read.sum + dram__bytes_write.sum of the "
+                                       "same launch from one ncu --set full capture (tools/prof_one.py)",
+                     "shrink": {"kernel": f"shrink_tc_kernel (fused {len(members)}-projection group {names})",
                                 "launch_us": shr_us, "algorithmic_bytes_per_launch": shr_bytes,
                                 "achieved": shr_bytes / (shr_us * 1e-6) / 1e9}},
         "cpu_baseline": cpu,
@@ -390,6 +402,16 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
     }
     return line
+
+
+def measured_traffic(config, label):
+    """DRAM bytes per launch of the roofline kernel, from the committed ncu capture (or None)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r1.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config, {}).get(label)
+    except (OSError, ValueError):
+        return None
 
 
 def time_graph(torch, eng, bp, xs, ys, stream, steps, warmup, dev):

@@ -163,6 +163,17 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
                           const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host,
                           void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
+/* A whole model step for one batch: for every layer l and input group g (in order), the group's
+ * fused shrink then its one-launch expand.  plans_* [num_groups] (group plans of the same batch),
+ * xs/ldxs [num_layers*num_groups], ys/ldys [num_layers*num_projections] (host arrays of device
+ * pointers / row strides; projections numbered group by group), a_ptrs [num_layers*num_groups][S]
+ * and b_ptrs [num_layers*num_projections][S] device tables.  Equivalent to the per-group calls,
+ * with no per-launch host round trips. */
+int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
+                     const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
+                     void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
+                     int32_t num_tokens, void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
 /* Expand of member `proj` of a group plan (lsv_lora_expand is proj = 0). */
 int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,
                          const void* const* b_ptrs, const void* plan_dev, const void* plan_host,

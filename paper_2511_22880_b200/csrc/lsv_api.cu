@@ -4,10 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <queue>
@@ -87,28 +89,46 @@ struct PlanBuilder {
 
 // LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
 // CTA's list keeps that order.  Returns records regrouped per CTA and the [grid+1] offsets.
+// Least-loaded CTA with the lowest index among equals, via a tournament tree over the CTA loads:
+// the root holds the winner, an update replays one leaf-to-root path (log2(grid) compares).
+struct LoadTree {
+  int n = 1;
+  std::vector<int64_t> load;
+  std::vector<int32_t> win;   // [2n): win[1] is the overall least-loaded CTA
+  explicit LoadTree(int grid) {
+    while (n < grid) n <<= 1;
+    load.assign(n, INT64_MAX);
+    for (int c = 0; c < grid; ++c) load[c] = 0;
+    win.assign(2 * n, 0);
+    for (int i = 0; i < n; ++i) win[n + i] = i;
+    for (int i = n - 1; i >= 1; --i) win[i] = better(win[2 * i], win[2 * i + 1]);
+  }
+  int better(int a, int b) const { return (load[b] < load[a] || (load[b] == load[a] && b < a)) ? b : a; }
+  int top() const { return win[1]; }
+  void add(int c, int64_t v) {
+    load[c] += v;
+    for (int i = (n + c) >> 1; i >= 1; i >>= 1) win[i] = better(win[2 * i], win[2 * i + 1]);
+  }
+};
+
+// LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
+// CTA's list keeps that order.  Returns records regrouped per CTA and the [grid+1] offsets.
 template <typename Rec>
 void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, std::vector<Rec>& out,
                 std::vector<int32_t>& cta_off) {
-  std::vector<int64_t> load(grid, 0);
-  std::vector<std::vector<Rec>> per(grid);
-  using Slot = std::pair<int64_t, int>;
-  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
-  for (int c = 0; c < grid; ++c) heap.push({0, c});
-  for (const auto& cr : costed) {
-    Slot sl = heap.top();
-    heap.pop();
-    per[sl.second].push_back(cr.second);
-    sl.first += cr.first;
-    heap.push(sl);
+  std::vector<int32_t> owner(costed.size());
+  LoadTree tree(grid);
+  for (size_t i = 0; i < costed.size(); ++i) {
+    const int c = tree.top();
+    owner[i] = c;
+    tree.add(c, costed[i].first);
   }
-  out.clear();
   cta_off.assign(grid + 1, 0);
-  for (int c = 0; c < grid; ++c) {
-    cta_off[c] = (int32_t)out.size();
-    out.insert(out.end(), per[c].begin(), per[c].end());
-  }
-  cta_off[grid] = (int32_t)out.size();
+  for (int32_t o : owner) ++cta_off[o + 1];
+  for (int c = 0; c < grid; ++c) cta_off[c + 1] += cta_off[c];
+  out.resize(costed.size());
+  std::vector<int32_t> fill(cta_off.begin(), cta_off.end() - 1);
+  for (size_t i = 0; i < costed.size(); ++i) out[fill[owner[i]]++] = costed[i].second;   // keeps LPT order per CTA
 }
 
 int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
@@ -231,29 +251,44 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
   lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta);
 
-  // expand: per projection, items = (m-tile, tw-wide h_out tile); plus all members in one list
-  int expand_grid[kMaxProj] = {0, 0, 0, 0};
-  std::vector<std::pair<int64_t, ExpandRec>> all_costed;
-  for (int p = 0; p < P; ++p) {
-    std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
-    const int tw = b_tile_width(h_outs[p]);
-    for (size_t i = 0; i < pb.mtiles.size(); ++i) {
-      const MTile& mt = pb.mtiles[i];
-      const int64_t cost = (int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024;
-      for (int jt = 0; jt < h_outs[p] / tw; ++jt) {
+  // expand: per projection, items = (m-tile, tw-wide h_out tile); plus all members in one list.
+  // An item's cost depends only on (m-tile, member), so the (m-tile, member) classes are sorted
+  // (stable, a few hundred) and their h_out tiles emitted in that order: the LPT input order of a
+  // stable sort of the items, without sorting the items.
+  struct ItemClass { int64_t cost; int32_t mt, p; };
+  auto emit = [&](const std::vector<ItemClass>& cls, std::vector<std::pair<int64_t, ExpandRec>>& out) {
+    for (const ItemClass& c : cls) {
+      const MTile& mt = pb.mtiles[c.mt];
+      const int tw = b_tile_width(h_outs[c.p]);
+      for (int jt = 0; jt < h_outs[c.p] / tw; ++jt) {
         ExpandRec r{};
         r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
-        r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = (int32_t)i; r.proj = p;
-        expand_costed.push_back({cost, r});
+        r.jtile = jt; r.vimg_off = mt.vimg_off; r.mtile = c.mt; r.proj = c.p;
+        out.push_back({c.cost, r});
       }
     }
-    all_costed.insert(all_costed.end(), expand_costed.begin(), expand_costed.end());
-    std::stable_sort(expand_costed.begin(), expand_costed.end(),
-                     [](const auto& a, const auto& b) { return a.first > b.first; });
+  };
+  auto by_cost = [](const ItemClass& a, const ItemClass& b) { return a.cost > b.cost; };
+  int expand_grid[kMaxProj] = {0, 0, 0, 0};
+  std::vector<ItemClass> all_cls;
+  for (int p = 0; p < P; ++p) {
+    const int tw = b_tile_width(h_outs[p]);
+    std::vector<ItemClass> cls;
+    for (size_t i = 0; i < pb.mtiles.size(); ++i) {
+      const MTile& mt = pb.mtiles[i];
+      cls.push_back({(int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024, (int32_t)i, p});
+    }
+    all_cls.insert(all_cls.end(), cls.begin(), cls.end());
+    std::stable_sort(cls.begin(), cls.end(), by_cost);
+    std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
+    expand_costed.reserve((size_t)pb.mtiles.size() * (h_outs[p] / tw));
+    emit(cls, expand_costed);
     expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
     lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p]);
   }
-  std::stable_sort(all_costed.begin(), all_costed.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::stable_sort(all_cls.begin(), all_cls.end(), by_cost);
+  std::vector<std::pair<int64_t, ExpandRec>> all_costed;
+  emit(all_cls, all_costed);
   const int expand_grid_all = (int)std::min<size_t>(all_costed.size(), (size_t)nsm);
   lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta);
 
@@ -603,22 +638,55 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   return LSV_OK;
 }
 
+// The usual call pattern is lsv_plan_size_group then lsv_plan_build_group with the same inputs:
+// the last plan built on this thread is kept so the second call does not plan again.
+struct PlanKey {
+  std::vector<int32_t> v;
+  PlanKey() = default;
+  PlanKey(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P, const int32_t* h_outs,
+          int32_t policy) {
+    v = {S, h_in, P, policy, num_sms_cached()};
+    if (h_outs) v.insert(v.end(), h_outs, h_outs + std::max(0, std::min(P, kMaxProj)));
+    if (S > 0 && indptr && rank) {
+      v.insert(v.end(), indptr, indptr + S + 1);
+      v.insert(v.end(), rank, rank + S);
+    }
+  }
+};
+thread_local PlanKey g_last_key;
+thread_local std::unique_ptr<PlanBuilder> g_last_plan;
+
+int plan_cached(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P, const int32_t* h_outs,
+                int32_t policy, const PlanBuilder** out) {
+  PlanKey key(S, indptr, rank, h_in, P, h_outs, policy);
+  if (g_last_plan && key.v == g_last_key.v) {
+    *out = g_last_plan.get();
+    return LSV_OK;
+  }
+  auto pb = std::make_unique<PlanBuilder>();
+  if (int rc = build_plan(*pb, S, indptr, rank, h_in, P, h_outs, policy)) return rc;
+  g_last_key = std::move(key);
+  g_last_plan = std::move(pb);
+  *out = g_last_plan.get();
+  return LSV_OK;
+}
+
 int lsv_plan_size_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
                         int32_t num_proj, const int32_t* h_outs, int32_t tier_policy, size_t* plan_bytes,
                         size_t* workspace_bytes) {
-  PlanBuilder pb;
-  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy)) return rc;
-  if (plan_bytes) *plan_bytes = (size_t)pb.h.total_ints * 4;
-  if (workspace_bytes) *workspace_bytes = (size_t)pb.h.ws_bytes;
+  const PlanBuilder* pb = nullptr;
+  if (int rc = plan_cached(num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy, &pb)) return rc;
+  if (plan_bytes) *plan_bytes = (size_t)pb->h.total_ints * 4;
+  if (workspace_bytes) *workspace_bytes = (size_t)pb->h.ws_bytes;
   return LSV_OK;
 }
 
 int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
                          int32_t num_proj, const int32_t* h_outs, int32_t tier_policy, void* plan_host,
                          size_t plan_bytes) {
-  PlanBuilder pb;
-  if (int rc = build_plan(pb, num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy)) return rc;
-  return plan_write(pb, plan_host, plan_bytes);
+  const PlanBuilder* pb = nullptr;
+  if (int rc = plan_cached(num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy, &pb)) return rc;
+  return plan_write(*pb, plan_host, plan_bytes);
 }
 
 int lsv_plan_size(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank, int32_t h_in,
@@ -700,6 +768,45 @@ int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, con
                     lsv_stream_t stream) {
   return lsv_lora_expand_proj(y, ldy, num_tokens, h_out, 0, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes,
                               stream);
+}
+
+int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* plans_dev, const void* const* plans_host,
+                     const void* const* xs, const int64_t* ldxs, void* const* ys, const int64_t* ldys,
+                     const void* a_ptrs, const void* b_ptrs, int32_t num_tokens, void* workspace,
+                     size_t workspace_bytes, lsv_stream_t stream) {
+  if (num_layers < 0 || num_groups < 1 || num_groups > 64)
+    return fail(LSV_EINVAL, "num_layers %d / num_groups %d out of range", num_layers, num_groups);
+  if (!plans_dev || !plans_host || !xs || !ldxs || !ys || !ldys || !a_ptrs || !b_ptrs)
+    return fail(LSV_EINVAL, "lsv_lora_forward: null argument");
+  const PlanHeader* hs[64];
+  int nproj = 0, S = -1;
+  for (int g = 0; g < num_groups; ++g) {
+    hs[g] = check_plan(plans_host[g]);
+    if (int rc = check_common(hs[g], workspace_bytes, plans_dev[g], workspace)) return rc;
+    if (S >= 0 && hs[g]->num_segments != S) return fail(LSV_EINVAL, "group plans index different batches");
+    S = hs[g]->num_segments;
+    nproj += hs[g]->num_proj;
+  }
+  const void* const* at = static_cast<const void* const*>(a_ptrs);
+  const void* const* bt = static_cast<const void* const*>(b_ptrs);
+  for (int l = 0; l < num_layers; ++l) {
+    int p0 = 0;
+    for (int g = 0; g < num_groups; ++g) {
+      const PlanHeader* h = hs[g];
+      const int np = h->num_proj;
+      if (int rc = lsv_lora_shrink(xs[l * num_groups + g], ldxs[l * num_groups + g], num_tokens, h->h_in,
+                                   at + ((size_t)l * num_groups + g) * S, plans_dev[g], plans_host[g], workspace,
+                                   workspace_bytes, stream))
+        return rc;
+      const void* const* btab[kMaxProj];
+      for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
+      if (int rc = lsv_lora_expand_group(ys + (size_t)l * nproj + p0, ldys + (size_t)l * nproj + p0, num_tokens,
+                                         btab, plans_dev[g], plans_host[g], workspace, workspace_bytes, stream))
+        return rc;
+      p0 += np;
+    }
+  }
+  return LSV_OK;
 }
 
 int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype, int32_t num_tokens, int32_t h_in,

@@ -174,16 +174,32 @@ class LoraDeltaEngine:
 
     def forward(self, bp: BatchPlan, xs: list[dict[str, torch.Tensor]], ys: list[dict[str, torch.Tensor]],
                 stream=None) -> None:
-        """Every layer and projection: xs[l][input_group], ys[l][proj_name]."""
+        """Every layer and projection: xs[l][input_group], ys[l][proj_name] — one native call
+        (lsv_lora_forward) that issues each layer's group shrinks and group expands in order."""
         projs = self.model.projections
-        for layer in range(self.model.layers):
-            for gi, (gname, members) in enumerate(self.groups):
+        L, G = self.model.layers, len(self.groups)
+        order = [p for _, m in self.groups for p in m]
+        if order != list(range(len(projs))):
+            raise ValueError("projections must be numbered group by group")
+        xl, ldx, yl, ldy = [], [], [], []
+        for layer in range(L):
+            for gname, members in self.groups:
                 x = xs[layer][gname]
-                yl = [ys[layer][projs[p].name] for p in members]
-                for p, y in zip(members, yl):
+                xl.append(x.data_ptr()); ldx.append(x.stride(0))
+                for p in members:
+                    y = ys[layer][projs[p].name]
                     self._check_io(x, y, projs[p].h_in, projs[p].h_out, bp.num_tokens)
-                self.shrink(bp, layer, members[0], x, stream)
-                self.expand_group(bp, layer, gi, yl, stream)
+                    yl.append(y.data_ptr()); ldy.append(y.stride(0))
+        arr = lambda t, v: (t * len(v))(*v)   # noqa: E731
+        pd = arr(ctypes.c_void_p, [gp.plan_dev.data_ptr() for gp in bp.group_plans])
+        ph = arr(ctypes.c_void_p, [gp.plan_host.ctypes.data for gp in bp.group_plans])
+        xa, la, ya, lya = (arr(ctypes.c_void_p, xl), arr(ctypes.c_int64, ldx), arr(ctypes.c_void_p, yl),
+                           arr(ctypes.c_int64, ldy))
+        st = stream or torch.cuda.current_stream(self.device)
+        native.check(native.lib().lsv_lora_forward(
+            L, G, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
+            ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr(), bp.b_ptrs.data_ptr(),
+            xs[0][self.groups[0][0]].shape[0], bp.workspace.data_ptr(), bp.workspace.numel(), st.cuda_stream))
 
     def launches_per_step(self, bp: BatchPlan) -> int:
         """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand

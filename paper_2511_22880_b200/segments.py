@@ -74,7 +74,10 @@ def index_requests(slots: Sequence[int], lengths: Sequence[int], ranks: Sequence
         raise ValueError("an adapter slot appears with two different ranks in one batch")
     seg_tokens = np.add.reduceat(lens_a[order], group_first)
     seg_indptr = np.concatenate(([0], np.cumsum(seg_tokens)))
-    perm = np.concatenate([np.arange(starts[i], starts[i] + lens_a[i]) for i in order])
+    # tokens of request order[k] are starts[order[k]] + 0..len-1, laid out request after request
+    lens_o = lens_a[order]
+    excl = np.concatenate(([0], np.cumsum(lens_o)[:-1]))
+    perm = np.arange(int(lens_o.sum()), dtype=np.int64) + np.repeat(starts[order] - excl, lens_o)
     return Segments(
         perm=perm.astype(np.int32),
         seg_indptr=seg_indptr.astype(np.int32),

@@ -211,6 +211,18 @@ class AdapterSlab:
             self._ipc_base = None
 
     # -- pointer tables ----------------------------------------------------------------
+    def _offset_tables(self) -> tuple[np.ndarray, np.ndarray]:
+        """Per-slot offset rows stacked into [slots, L, groups] / [slots, L, projections] (cached)."""
+        n = len(self.slots)
+        if getattr(self, "_tables_n", -1) != n:
+            L = self.model.layers
+            self._g_tab = (np.stack(self._g_off_rows) if n else
+                           np.zeros((0, L, len(self.model.groups())), dtype=np.int64))
+            self._b_tab = (np.stack(self._b_off_rows) if n else
+                           np.zeros((0, L, len(self.model.projections)), dtype=np.int64))
+            self._tables_n = n
+        return self._g_tab, self._b_tab
+
     def pointer_tables(self, seg_slots: np.ndarray, peer_slabs: dict[int, "AdapterSlab"] | None = None,
                        seg_owner: np.ndarray | None = None) -> tuple[torch.Tensor, torch.Tensor]:
         """Device int64 tables for the segments: group A tiles [layers*groups, S] (model.groups())
@@ -219,14 +231,20 @@ class AdapterSlab:
         ``seg_owner[s]`` (optional) names the GPU whose slab holds segment s; entries other than
         this slab's device resolve through ``peer_slabs`` to NVLink peer addresses."""
         L, P, G = self.model.layers, len(self.model.projections), len(self.model.groups())
-        S = len(seg_slots)
-        a = np.empty((L * G, S), dtype=np.int64)
-        b = np.empty((L * P, S), dtype=np.int64)
-        for s, slot in enumerate(np.asarray(seg_slots)):
-            slab = self
-            if seg_owner is not None and peer_slabs is not None and int(seg_owner[s]) in peer_slabs:
-                slab = peer_slabs[int(seg_owner[s])]
-            a[:, s] = (slab.base + slab._g_off_rows[int(slot)]).reshape(-1)
-            b[:, s] = (slab.base + slab._b_off_rows[int(slot)]).reshape(-1)
+        slots = np.asarray(seg_slots, dtype=np.int64)
+        S = len(slots)
+        g_all, b_all = self._offset_tables()
+        a = g_all[slots].reshape(S, L * G).T + self.base        # [L*G, S]
+        b = b_all[slots].reshape(S, L * P).T + self.base
+        if seg_owner is not None and peer_slabs is not None:
+            for s in range(S):     # segments whose adapter lives in a peer GPU's slab (its own slots)
+                owner = int(seg_owner[s])
+                if owner in peer_slabs and peer_slabs[owner] is not self:
+                    peer = peer_slabs[owner]
+                    pg, pb_ = peer._offset_tables()
+                    a[:, s] = pg[slots[s]].reshape(-1) + peer.base
+                    b[:, s] = pb_[slots[s]].reshape(-1) + peer.base
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
         return (torch.from_numpy(a).to(self.device, non_blocking=False),
                 torch.from_numpy(b).to(self.device, non_blocking=False))

@@ -13,9 +13,9 @@ if timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_o
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?"
 fi
-if timeout 300 python tools/prof_one.py 4 > gpurun_out/prof_one_$TAG.log 2>&1; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_kernel|simt_" -s 3 -c 3 \
-    -o gpurun_out/full_$TAG -f python tools/prof_one.py 4 > gpurun_out/ncu_full_$TAG.log 2>&1
+if timeout 300 python tools/prof_one.py 2 > gpurun_out/prof_one_$TAG.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_kernel|simt_" -s 4 -c 2 \
+    -o gpurun_out/full_$TAG -f python tools/prof_one.py 2 > gpurun_out/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?"
 fi
 lscpu | head -20 > gpurun_out/lscpu_$TAG.txt

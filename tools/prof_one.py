@@ -1,4 +1,5 @@
-"""Minimal C2 one-layer workload for ncu captures: q_proj apply x3 (the last two are profiled)."""
+"""Minimal C2 one-layer workload for ncu captures: the step's mlp_in kernels (fused gate/up shrink
++ one-launch gate/up expand), three times; profile the last pair with -s 4 -c 2."""
 import sys
 import numpy as np
 import torch
@@ -8,7 +9,6 @@ from paper_2511_22880_b200.slab import AdapterSlab
 from paper_2511_22880_b200.lora import LoraDeltaEngine
 from paper_2511_22880_b200.segments import index_tokens
 
-proj = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections)
 dev = torch.device("cuda:0")
 ranks = [8]*44+[16]*22+[32]*14+[64]*11+[128]*9
@@ -18,10 +18,12 @@ for i, r in enumerate(ranks):
 seg = index_tokens(np.random.default_rng(0).integers(0, 100, 4096), ranks)
 eng = LoraDeltaEngine(slab)
 bp = eng.prepare(seg)
-pr = model.projections[proj]
-x = torch.randn(4096, pr.h_in, device=dev).to(torch.bfloat16)
-y = torch.zeros(4096, pr.h_out, device=dev, dtype=torch.bfloat16)
+gi = int(sys.argv[1]) if len(sys.argv) > 1 else 2          # 2 = mlp_in (gate/up)
+gname, members = eng.groups[gi]
+x = torch.randn(4096, model.projections[members[0]].h_in, device=dev).to(torch.bfloat16)
+ys = [torch.zeros(4096, model.projections[p].h_out, device=dev, dtype=torch.bfloat16) for p in members]
 for _ in range(3):
-    eng.apply(bp, 0, proj, x, y)
+    eng.shrink(bp, 0, members[0], x)
+    eng.expand_group(bp, 0, gi, ys)
 torch.cuda.synchronize()
 print("ok")
