@@ -168,11 +168,16 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
  * xs/ldxs [num_layers*num_groups], ys/ldys [num_layers*num_projections] (host arrays of device
  * pointers / row strides; projections numbered group by group), a_ptrs [num_layers*num_groups][S]
  * and b_ptrs [num_layers*num_projections][S] device tables.  Equivalent to the per-group calls,
- * with no per-launch host round trips. */
+ * with no per-launch host round trips.  The workspace holds one slice per (layer, group)
+ * (lsv_lora_forward_workspace bytes, zero-filled once), so each group's shrink may start while
+ * the previous group's expand drains. */
 int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
                      const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
                      void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
                      int32_t num_tokens, void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* Workspace bytes lsv_lora_forward needs for these group plans (0 on bad input). */
+size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const void* const* plans_host);
 
 /* Expand of member `proj` of a group plan (lsv_lora_expand is proj = 0). */
 int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,

@@ -456,7 +456,7 @@ int ensure_smem_attrs() {
 // Programmatic dependent launch: the kernel may start while the previous kernel in the stream
 // drains; it calls griddepcontrol.wait before touching anything that kernel wrote.
 template <typename Params>
-cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t st, const Params& p) {
+cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t st, const Params& p, bool pdl = true) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTcThreads);
@@ -466,7 +466,7 @@ cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;     // without it the launch waits for all earlier work in the stream
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
@@ -479,8 +479,11 @@ int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_d
   return LSV_OK;
 }
 
+// wait_prev = 0: the previous launch neither writes what this shrink reads nor reads what it
+// writes (lsv_lora_forward's per-(layer, group) workspace slices), so it need not wait for it;
+// pdl = false: a plain launch, ordered after all earlier work in the stream.
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
-               const int32_t* plan, uint8_t* ws, cudaStream_t st) {
+               const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true) {
   if (h->n_simt_items > 0) {
     simt_shrink_kernel<<<h->n_simt_items, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
                                                         h->off_simt_items, h->off_seg_rank, a_ptrs,
@@ -499,9 +502,10 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.off_red_cta = h->off_red_cta;
     p.grid_bar = h->n_counters;
     p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
+    p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
-    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p));
+    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl));
   }
   return LSV_OK;
 }
@@ -778,35 +782,68 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
     return fail(LSV_EINVAL, "num_layers %d / num_groups %d out of range", num_layers, num_groups);
   if (!plans_dev || !plans_host || !xs || !ldxs || !ys || !ldys || !a_ptrs || !b_ptrs)
     return fail(LSV_EINVAL, "lsv_lora_forward: null argument");
+  // every (layer, group) gets its own workspace slice: nothing a shrink writes is read by any
+  // other launch of this call but its own group's expand, so a shrink need not wait for the
+  // expand before it (it fills the SMs that expand's tail frees).  The first launch of the call
+  // is a plain one: it waits for everything earlier in the stream, including a previous call.
   const PlanHeader* hs[64];
+  size_t ws_off[65];
   int nproj = 0, S = -1;
+  ws_off[0] = 0;
   for (int g = 0; g < num_groups; ++g) {
     hs[g] = check_plan(plans_host[g]);
-    if (int rc = check_common(hs[g], workspace_bytes, plans_dev[g], workspace)) return rc;
+    if (!hs[g]) return fail(LSV_EINVAL, "plans_host[%d] is not a liblsv plan", g);
+    if (!plans_dev[g]) return fail(LSV_EINVAL, "plans_dev[%d] is null", g);
     if (S >= 0 && hs[g]->num_segments != S) return fail(LSV_EINVAL, "group plans index different batches");
     S = hs[g]->num_segments;
     nproj += hs[g]->num_proj;
+    ws_off[g + 1] = ws_off[g] + ((size_t)hs[g]->ws_bytes + 255) / 256 * 256;
   }
+  const size_t per_layer = ws_off[num_groups];
+  if (workspace_bytes < per_layer * (size_t)num_layers)
+    return fail(LSV_EWORKSPACE, "workspace of %zu bytes is smaller than the %zu the forward needs "
+                "(lsv_lora_forward_workspace)", workspace_bytes, per_layer * (size_t)num_layers);
+  if (per_layer > 0 && !workspace) return fail(LSV_EINVAL, "workspace is null");
   const void* const* at = static_cast<const void* const*>(a_ptrs);
   const void* const* bt = static_cast<const void* const*>(b_ptrs);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (int l = 0; l < num_layers; ++l) {
     int p0 = 0;
+    uint8_t* wsl = static_cast<uint8_t*>(workspace) + per_layer * (size_t)l;
     for (int g = 0; g < num_groups; ++g) {
       const PlanHeader* h = hs[g];
       const int np = h->num_proj;
-      if (int rc = lsv_lora_shrink(xs[l * num_groups + g], ldxs[l * num_groups + g], num_tokens, h->h_in,
-                                   at + ((size_t)l * num_groups + g) * S, plans_dev[g], plans_host[g], workspace,
-                                   workspace_bytes, stream))
-        return rc;
+      const int64_t ldx = ldxs[l * num_groups + g];
+      const void* x = xs[l * num_groups + g];
+      const bool first = l == 0 && g == 0;
+      if (h->num_tokens > 0) {
+        if (!x || !aligned16(x) || ldx % 8 || ldx < h->h_in || num_tokens < h->num_tokens)
+          return fail(LSV_EINVAL, "layer %d group %d: bad x", l, g);
+        if (int rc = run_shrink(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S,
+                                static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st, first ? 1 : 0, !first))
+          return rc;
+      }
       const void* const* btab[kMaxProj];
       for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
       if (int rc = lsv_lora_expand_group(ys + (size_t)l * nproj + p0, ldys + (size_t)l * nproj + p0, num_tokens,
-                                         btab, plans_dev[g], plans_host[g], workspace, workspace_bytes, stream))
+                                         btab, plans_dev[g], plans_host[g], wsl + ws_off[g],
+                                         ws_off[g + 1] - ws_off[g], stream))
         return rc;
       p0 += np;
     }
   }
   return LSV_OK;
+}
+
+size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const void* const* plans_host) {
+  if (num_layers < 0 || num_groups < 1 || !plans_host) return 0;
+  size_t per_layer = 0;
+  for (int g = 0; g < num_groups; ++g) {
+    const PlanHeader* h = check_plan(plans_host[g]);
+    if (!h) return 0;
+    per_layer += ((size_t)h->ws_bytes + 255) / 256 * 256;
+  }
+  return per_layer * (size_t)num_layers;
 }
 
 int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype, int32_t num_tokens, int32_t h_in,

@@ -39,6 +39,8 @@ struct alignas(64) ShrinkParams {
   int off_mtiles, off_red, n_red, red_units, grid_bar, off_red_cta;   // grid-wide split-K reduction
   int num_proj, vimg_stride;    // input group: projections shrunk together, bytes between their v images
   int acc_cols;                 // TMEM accumulator width (128 -> 4 buffers, 256 -> 2)
+  int wait_prev;                // 0: the previous launch is another input group's expand, which this
+                                // launch neither reads nor overwrites: start without waiting for it
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   const uint32_t tmem_base = *tmem_slot;
   const int cta = blockIdx.x;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
-  pdl_wait();                 // x, workspace and counters are written by earlier launches
+  if (p.wait_prev) pdl_wait();   // x, workspace and counters are written by earlier launches
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 

@@ -115,7 +115,9 @@ class LoraDeltaEngine:
             gp = build_group_plan(seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
                                   self.tier_policy, self.device, members)
             plans.append(gp)
-            ws_need = max(ws_need, gp.workspace_bytes)
+        # forward: one workspace slice per (layer, group) (lsv_lora_forward_workspace)
+        ph = (ctypes.c_void_p * len(plans))(*[gp.plan_host.ctypes.data for gp in plans])
+        ws_need = native.lib().lsv_lora_forward_workspace(self.model.layers, len(plans), ctypes.addressof(ph))
         if self._workspace is None or self._workspace.numel() < ws_need:
             # zero-filled once: the kernels leave their split counters at zero on exit
             self._workspace = torch.zeros(max(ws_need, 256), dtype=torch.uint8, device=self.device)
