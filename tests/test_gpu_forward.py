@@ -1,0 +1,90 @@
+"""Whole-step path (lsv_lora_forward: every layer's input groups, fused shrinks + one-launch group
+expands, per-(layer, group) workspace slices, shrinks overlapping the previous expand's tail)
+against the CPU oracle, on a 2-layer Llama-shaped model with all four input groups, and
+bit-identical to issuing the same work group by group."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle
+from tests._cases import bf16_bits
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+def _setup(dev, tier=0):
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import ModelShape, Projection
+    from paper_2511_22880_b200.slab import AdapterSlab
+    h, inter, kv = 1024, 2816, 256
+    model = ModelShape("mini", 2, (Projection("q_proj", h, h), Projection("k_proj", h, kv), Projection("v_proj", h, kv),
+                                    Projection("o_proj", h, h), Projection("gate_proj", h, inter),
+                                    Projection("up_proj", h, inter), Projection("down_proj", inter, h)))
+    ranks = [8, 16, 128, 64, 24, 32, 8, 128]
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+    for i, r in enumerate(ranks):
+        slab.fill_random(slab.allocate(f"a{i}", r), 500 + i)
+    rng = np.random.default_rng(5)
+    tok = np.concatenate([np.full(n, s) for s, n in enumerate([41, 3, 150, 64, 17, 0, 90, 33])])
+    rng.shuffle(tok)
+    seg = index_tokens(tok, ranks)
+    eng = LoraDeltaEngine(slab, tier_policy=tier)
+    bp = eng.prepare(seg)
+    N = seg.num_tokens
+    g = torch.Generator().manual_seed(9)
+    xs = [{name: torch.randn(N, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16).to(dev)
+           for name, m in model.groups()} for _ in range(model.layers)]
+    return model, slab, seg, eng, bp, xs
+
+
+@pytest.mark.parametrize("tier", [0, 2])
+def test_forward_matches_oracle_and_per_group_calls(tier):
+    dev = torch.device("cuda:0")
+    model, slab, seg, eng, bp, xs = _setup(dev, tier)
+    N = seg.num_tokens
+    ys = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device=dev) for p in model.projections}
+          for _ in range(model.layers)]
+    eng.forward(bp, xs, ys)
+    torch.cuda.synchronize()
+    # the same work issued group by group (shrink + expand_group per group)
+    ys2 = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device=dev) for p in model.projections}
+           for _ in range(model.layers)]
+    for layer in range(model.layers):
+        for gi, (name, members) in enumerate(model.groups()):
+            eng.shrink(bp, layer, members[0], xs[layer][name])
+            eng.expand_group(bp, layer, gi, [ys2[layer][model.projections[p].name] for p in members])
+    torch.cuda.synchronize()
+    for layer in range(model.layers):
+        for p, pr in enumerate(model.projections):
+            got = ys[layer][pr.name]
+            assert torch.equal(got, ys2[layer][pr.name]), (layer, pr.name)
+            a_list, b_list = [], []
+            for slot in seg.seg_slot:
+                a, b = slab.read(int(slot), layer, p)
+                a_list.append(bf16_bits(a.cpu()))
+                b_list.append(bf16_bits(b.cpu()))
+            x = xs[layer][[n for n, m in model.groups() if p in m][0]]
+            ref = oracle.delta_c(bf16_bits(x.cpu()), seg.seg_indptr, seg.seg_rank, a_list, b_list, pr.h_out)
+            err = oracle.max_rel_err(got.float().cpu().numpy()[:N], ref[:N])
+            assert err <= TOL, (layer, pr.name, err)
+
+
+def test_forward_repeats_bit_identical():
+    """Two back-to-back steps on the same inputs (the second reuses the workspace slices, whose
+    split counters the kernels re-arm) give bit-identical outputs."""
+    dev = torch.device("cuda:0")
+    model, slab, seg, eng, bp, xs = _setup(dev)
+    N = seg.num_tokens
+    outs = []
+    for _ in range(2):
+        ys = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device=dev) for p in model.projections}
+              for _ in range(model.layers)]
+        eng.forward(bp, xs, ys)
+        torch.cuda.synchronize()
+        outs.append(ys)
+    for layer in range(model.layers):
+        for pr in model.projections:
+            assert torch.equal(outs[0][layer][pr.name], outs[1][layer][pr.name])
