@@ -485,7 +485,12 @@ int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_d
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
                const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true) {
   if (h->n_simt_items > 0) {
-    simt_shrink_kernel<<<h->n_simt_items, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
+    // grid.y covers the widest SIMT group (num_proj x the largest SIMT rank) in 8-row blocks
+    const int32_t* hp = reinterpret_cast<const int32_t*>(h);
+    int max_r = 8;
+    for (int s = 0; s < h->num_segments; ++s)
+      if (hp[h->off_seg_tier + s] == kTierSimt) max_r = std::max(max_r, (int)hp[h->off_seg_rank + s]);
+    simt_shrink_kernel<<<dim3(h->n_simt_items, h->num_proj * max_r / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
                                                         h->off_simt_items, h->off_seg_rank, a_ptrs,
                                                         reinterpret_cast<float*>(ws + h->ws_simt_v), h->num_proj,
                                                         h->simt_stride);
@@ -516,7 +521,7 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
                const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st) {
   for (int i = 0; i < np && h->n_simt_items > 0; ++i) {
     const int pp = p0 + i, h_out = h->h_outs[pp];
-    simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 511) / 512), 64, 0, st>>>(
+    simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 255) / 256), 128, 0, st>>>(
         static_cast<__nv_bfloat16*>(ys[i]), ldys[i], h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs[i],
         reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());

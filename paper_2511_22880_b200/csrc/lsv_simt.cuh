@@ -23,94 +23,143 @@ __device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
   return s;
 }
 
-// grid = n_simt_items, block = 256 (8 warps).  v[item] = x[tokens] · A^T, fp32 [ntok][rank].
+// Shrink: grid = (n_simt_items, G / 8), block = 256: one block per (item, 8 rows of the item's
+// group A, G = nproj * rank rows).  The 8 warps split the 64-column chunks of h_in (warp w takes
+// chunks w, w + 8, ...); lane = (row of 8, quarter of a chunk), so a warp reads each chunk's 8 rows
+// as 1 KB contiguous, four chunks in flight.  Quarters reduce by shuffle, warps through shared
+// memory in a fixed order (deterministic).  v (fp32) lands in the row's projection region.
+constexpr int kSimtUnroll = 4;
 __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                           int h_in, const int32_t* __restrict__ plan,
                                                           int off_items, int off_rank,
                                                           const void* const* __restrict__ a_ptrs,
                                                           float* __restrict__ simt_v, int nproj, int simt_stride) {
-  // the group's nproj projections are one rank-(nproj*r) adapter in the group A layout; row k of
-  // it is projection k / r, whose v lands in that projection's region
+  __shared__ float red[8][8][kSimtMaxTok];   // [warp][row][token]
   const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
   const int r = plan[off_rank + it.seg], G = nproj * r;
-  const uint8_t* a = static_cast<const uint8_t*>(a_ptrs[it.seg]);
+  if ((int)blockIdx.y * 8 >= G) return;      // block-uniform (G % 8 == 0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint8_t* xrow[kSimtMaxTok];
+  const int rl = lane >> 2, k = blockIdx.y * 8 + rl, q4 = lane & 3;
+  const uint8_t* arow = static_cast<const uint8_t*>(a_ptrs[it.seg]) + (size_t)k * 128;
+  const uint32_t u0 = (uint32_t)((2 * q4) ^ (k & 7)) << 4, u1 = (uint32_t)((2 * q4 + 1) ^ (k & 7)) << 4;
+  const size_t cstride = (size_t)G * 128;            // bytes between consecutive chunks of a row
+  const int chunks = h_in / 64, nt = it.ntok;
+  float acc[kSimtMaxTok];
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t)
-    xrow[t] = reinterpret_cast<const uint8_t*>(x + (int64_t)(it.tok_begin + min(t, it.ntok - 1)) * ldx);
-  for (int k = warp; k < G; k += 8) {
-    float acc[kSimtMaxTok];
+  for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
+  for (int c0 = warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
+    uint4 a0[kSimtUnroll], a1[kSimtUnroll];
 #pragma unroll
-    for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
-    for (int i0 = lane * 8; i0 < h_in; i0 += 256) {
-      const uint4 av = __ldg(reinterpret_cast<const uint4*>(a + a_tiled_off_g(k, i0, G)));
-#pragma unroll
-      for (int t = 0; t < kSimtMaxTok; ++t) {
-        if (t < it.ntok) {
-          const uint4 xv = __ldg(reinterpret_cast<const uint4*>(xrow[t] + (size_t)i0 * 2));
-          acc[t] += dot8_bf16(av, xv);
-        }
+    for (int u = 0; u < kSimtUnroll; ++u) {
+      const int c = c0 + 8 * u;
+      if (c < chunks) {
+        const uint8_t* ap = arow + (size_t)c * cstride;
+        a0[u] = __ldg(reinterpret_cast<const uint4*>(ap + u0));
+        a1[u] = __ldg(reinterpret_cast<const uint4*>(ap + u1));
       }
     }
 #pragma unroll
-    for (int t = 0; t < kSimtMaxTok; ++t) {
+    for (int u = 0; u < kSimtUnroll; ++u) {
+      const int c = c0 + 8 * u;
+      if (c < chunks) {
+        const int col = c * 64 + q4 * 16;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int t = 0; t < kSimtMaxTok; ++t)
-        if (t < it.ntok) simt_v[(size_t)(k / r) * simt_stride + it.v_off + t * r + k % r] = acc[t];
-    }
-  }
-}
-
-// grid = (n_simt_items, ceil(h_out/512)), block = 64: thread owns 8 consecutive h_out columns
-// (one 16-byte unit of a B-tile row), so each k costs one 16-byte load of B and the y update is a
-// 16-byte read-modify-write per token.
-__global__ void __launch_bounds__(64) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy, int h_out,
-                                                         const int32_t* __restrict__ plan, int off_items,
-                                                         int off_rank, const void* const* __restrict__ b_ptrs,
-                                                         const float* __restrict__ simt_v) {
-  __shared__ float vs[kSimtMaxTok * 256];
-  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
-  const int r = plan[off_rank + it.seg];
-  const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
-  for (int e = threadIdx.x; e < it.ntok * r; e += blockDim.x) vs[e] = simt_v[it.v_off + e];
-  __syncthreads();
-  const int j = (blockIdx.y * 64 + threadIdx.x) * 8;
-  if (j >= h_out) return;
-  const int tw = b_tile_width(h_out);
-  float acc[kSimtMaxTok][8];
-#pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
-  for (int k = 0; k < r; ++k) {
-    const uint4 bw = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, k, r, tw)));
-    const float w[8] = {bf16_lo(bw.x), bf16_hi(bw.x), bf16_lo(bw.y), bf16_hi(bw.y),
-                        bf16_lo(bw.z), bf16_hi(bw.z), bf16_lo(bw.w), bf16_hi(bw.w)};
-#pragma unroll
-    for (int t = 0; t < kSimtMaxTok; ++t) {
-      if (t < it.ntok) {
-        const float vv = vs[t * r + k];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
+        for (int t = 0; t < kSimtMaxTok; ++t) {
+          if (t < nt) {
+            const uint4* xp = reinterpret_cast<const uint4*>(x + (int64_t)(it.tok_begin + t) * ldx + col);
+            acc[t] += dot8_bf16(a0[u], __ldg(xp)) + dot8_bf16(a1[u], __ldg(xp + 1));
+          }
+        }
       }
     }
   }
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t) {
-    if (t < it.ntok) {
-      uint4* py = reinterpret_cast<uint4*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
-      const uint4 yv = *py;
-      uint4 o;
-      o.x = pack_bf16x2(bf16_lo(yv.x) + acc[t][0], bf16_hi(yv.x) + acc[t][1]);
-      o.y = pack_bf16x2(bf16_lo(yv.y) + acc[t][2], bf16_hi(yv.y) + acc[t][3]);
-      o.z = pack_bf16x2(bf16_lo(yv.z) + acc[t][4], bf16_hi(yv.z) + acc[t][5]);
-      o.w = pack_bf16x2(bf16_lo(yv.w) + acc[t][6], bf16_hi(yv.w) + acc[t][7]);
-      *py = o;
+    acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 1);
+    acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 2);
+  }
+  if (q4 == 0) {
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) red[warp][rl][t] = acc[t];
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 * kSimtMaxTok) {
+    const int row = threadIdx.x / kSimtMaxTok, t = threadIdx.x % kSimtMaxTok, kk = blockIdx.y * 8 + row;
+    if (t < nt) {
+      float sum = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += red[w][row][t];
+      simt_v[(size_t)(kk / r) * simt_stride + it.v_off + t * r + kk % r] = sum;
+    }
+  }
+}
+
+// Expand: grid = (n_simt_items, ceil(h_out / 256)), block = 128 (warp w: 64 columns of the 256).
+// Lane = (k row of 4, 16-byte unit of 8 columns): a warp reads four 128-byte B atom rows per
+// load (four loads in flight), accumulates [tokens][8 columns] in registers over k, reduces the
+// four k lanes by shuffle and updates y with row-contiguous 16-byte read-modify-writes.
+__global__ void __launch_bounds__(128) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy, int h_out,
+                                                          const int32_t* __restrict__ plan, int off_items,
+                                                          int off_rank, const void* const* __restrict__ b_ptrs,
+                                                          const float* __restrict__ simt_v) {
+  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
+  const int r = plan[off_rank + it.seg];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.y * 256 + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
+  if (blockIdx.y * 256 + warp * 64 >= h_out) return;            // warp-uniform (h_out % 64 == 0)
+  const int ks = lane >> 3, nt = it.ntok;
+  const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
+  const int tw = b_tile_width(h_out);
+  const float* vp = simt_v + it.v_off;
+  float acc[kSimtMaxTok][8];
+#pragma unroll
+  for (int t = 0; t < kSimtMaxTok; ++t)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
+  for (int k0 = 0; k0 < r; k0 += 4 * kSimtUnroll) {
+    uint4 bw[kSimtUnroll];
+#pragma unroll
+    for (int u = 0; u < kSimtUnroll; ++u) {
+      const int k = k0 + u * 4 + ks;
+      if (k < r) bw[u] = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, k, r, tw)));
+    }
+#pragma unroll
+    for (int u = 0; u < kSimtUnroll; ++u) {
+      const int k = k0 + u * 4 + ks;
+      if (k < r) {
+        const float w[8] = {bf16_lo(bw[u].x), bf16_hi(bw[u].x), bf16_lo(bw[u].y), bf16_hi(bw[u].y),
+                            bf16_lo(bw[u].z), bf16_hi(bw[u].z), bf16_lo(bw[u].w), bf16_hi(bw[u].w)};
+#pragma unroll
+        for (int t = 0; t < kSimtMaxTok; ++t) {
+          if (t < nt) {
+            const float vv = __ldg(vp + t * r + k);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kSimtMaxTok; ++t)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 8);
+      acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 16);
+    }
+  if (ks == 0) {
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) {
+      if (t < nt) {
+        uint4* py = reinterpret_cast<uint4*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
+        const uint4 yv = *py;
+        uint4 o;
+        o.x = pack_bf16x2(bf16_lo(yv.x) + acc[t][0], bf16_hi(yv.x) + acc[t][1]);
+        o.y = pack_bf16x2(bf16_lo(yv.y) + acc[t][2], bf16_hi(yv.y) + acc[t][3]);
+        o.z = pack_bf16x2(bf16_lo(yv.z) + acc[t][4], bf16_hi(yv.z) + acc[t][5]);
+        o.w = pack_bf16x2(bf16_lo(yv.w) + acc[t][6], bf16_hi(yv.w) + acc[t][7]);
+        *py = o;
+      }
     }
   }
 }
