@@ -44,7 +44,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote", "tp"), default="c2",
+    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote", "tp", "decode"), default="c2",
                     help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
                          "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")

@@ -48,7 +48,21 @@ def c2_llama2_7b(n_tokens: int = 4096, n_adapters: int = 100, seed: int = 0) -> 
                     f"llama-2-7b 32 layers x 7 proj, {n_adapters} adapters {counts}, {n_tokens} tokens")
 
 
-WORKLOADS = {"c1": c1_qproj, "c2": c2_llama2_7b}
+def decode_llama2_7b(n_requests: int = 128, n_adapters: int = 100, seed: int = 0) -> Workload:
+    """Decode step (the reference's decode_iter_time regime, costmodel.py:108-123): C2's roster and
+    shapes, ``n_requests`` requests each decoding one token (one token per request, so segments of
+    a few tokens: the SIMT tier)."""
+    roster = traces.roster(n_adapters)
+    ranks = [a.rank for a in roster]
+    rng = random.Random(seed)
+    tok = [rng.randrange(n_adapters) for _ in range(n_requests)]
+    seg = index_tokens(np.asarray(tok), ranks)
+    return Workload("decode_llama2_7b", shapes.LLAMA2_7B, ranks, [a.id for a in roster], seg,
+                    f"llama-2-7b 32 layers x 7 proj decode step: {n_requests} requests x 1 token over "
+                    f"{n_adapters} adapters ({seg.num_segments} active)")
+
+
+WORKLOADS = {"c1": c1_qproj, "c2": c2_llama2_7b, "decode": decode_llama2_7b}
 
 
 # ---- data-parallel serving across GPUs (configs 3/4): placement + routing decide each GPU's batch
