@@ -414,14 +414,15 @@ def measured_traffic(config, label):
         return None
 
 
-def time_graph(torch, eng, bp, xs, ys, stream, steps, warmup, dev):
+def time_graph(torch, eng, bp, xs, ys, stream, steps, warmup, dev, step_fn=None):
     """CUDA-graph the whole step once, replay warmup + steps, return ms per step (CUDA events)."""
+    step_fn = step_fn or (lambda: eng.forward(bp, xs, ys, stream))
     with torch.cuda.stream(stream):
-        eng.forward(bp, xs, ys, stream)
+        step_fn()
     torch.cuda.synchronize(dev)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
-        eng.forward(bp, xs, ys, stream)
+        step_fn()
     with torch.cuda.stream(stream):
         for _ in range(warmup):
             g.replay()
@@ -436,12 +437,14 @@ def time_graph(torch, eng, bp, xs, ys, stream, steps, warmup, dev):
 
 
 def run_remote(args, rank, world, local_rank):
-    """Config 4: 30% of each GPU's tokens hit adapters owned by a peer GPU, read in-kernel over
-    NVLink through CUDA-IPC-mapped peer slabs (no copy, no NCCL).  Reports tokens/s with the
-    remote reads and the overhead against the same batch with every adapter local."""
+    """Config 4: 30% of each GPU's tokens hit adapters owned by a peer GPU (CUDA-IPC-mapped peer
+    slabs, no NCCL).  Two ways to use them: fetched a layer ahead into local staging buffers by the
+    copy engines over NVLink while the current layer computes (``prefetch``, the headline), or read
+    in-kernel over NVLink (``direct``).  Reports tokens/s and the overhead against the same batch
+    with every adapter local."""
     import torch
     from paper_2511_22880_b200 import synth
-    from paper_2511_22880_b200.lora import LoraDeltaEngine, algorithmic_bytes, input_group
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, RemotePrefetch, algorithmic_bytes, input_group
     from paper_2511_22880_b200.slab import AdapterSlab
     if world < 2:
         raise SystemExit("--config remote needs >= 2 ranks (torchrun)")
@@ -461,6 +464,8 @@ def run_remote(args, rank, world, local_rank):
     eng = LoraDeltaEngine(slab)
     bp_local = eng.prepare(seg)
     bp_remote = eng.prepare(seg, seg_owner=owner, peer_slabs=peers)
+    pf = RemotePrefetch(eng, seg, owner, peers)
+    bp_pf = pf.plan()
     g = torch.Generator(device=dev).manual_seed(1 + rank)
     groups = {}
     for pr in model.projections:
@@ -476,20 +481,35 @@ def run_remote(args, rank, world, local_rank):
     eng.apply(bp_remote, 0, 0, xs[0][input_group(model.projections[0].name)], y_r)
     torch.cuda.synchronize(dev)
     identical = bool(torch.equal(y_l, y_r))
+    # the prefetched step must give the all-local step's bits on every layer and projection
+    ys_a = [{pr.name: torch.zeros(N, pr.h_out, device=dev, dtype=torch.bfloat16) for pr in model.projections}
+            for _ in range(model.layers)]
+    ys_b = [{pr.name: torch.zeros(N, pr.h_out, device=dev, dtype=torch.bfloat16) for pr in model.projections}
+            for _ in range(model.layers)]
+    eng.forward(bp_local, xs, ys_a)
+    eng.forward_prefetch(bp_pf, pf, xs, ys_b)
+    torch.cuda.synchronize(dev)
+    identical_pf = all(torch.equal(ys_a[l][k], ys_b[l][k]) for l in range(model.layers) for k in ys_a[l])
+    del ys_a, ys_b
     stream = torch.cuda.Stream(dev)
     torch.distributed.barrier()
     ms_local = time_graph(torch, eng, bp_local, xs, ys, stream, args.steps, args.warmup, dev)
     torch.distributed.barrier()
+    ms_pf = time_graph(torch, eng, bp_pf, xs, ys, stream, args.steps, args.warmup, dev,
+                       step_fn=lambda: eng.forward_prefetch(bp_pf, pf, xs, ys, stream))
+    torch.distributed.barrier()
     sampler = ClockSampler(dev.index)
     sampler.start()
-    ms_remote = time_graph(torch, eng, bp_remote, xs, ys, stream, args.steps, args.warmup, dev)
+    ms_direct = time_graph(torch, eng, bp_remote, xs, ys, stream, args.steps, args.warmup, dev)
     clocks = sampler.stop()
-    t = torch.tensor([ms_local, ms_remote, float(identical)], device=dev, dtype=torch.float64)
+    t = torch.tensor([ms_local, ms_direct, float(identical and identical_pf), ms_pf], device=dev,
+                     dtype=torch.float64)
     per = [torch.zeros_like(t) for _ in range(world)]
     torch.distributed.all_gather(per, t)
     per = [p.tolist() for p in per]
     ms_l = max(p[0] for p in per)
-    ms_r = max(p[1] for p in per)
+    ms_r = max(p[1] for p in per)      # headline: in-kernel NVLink peer loads
+    ms_p = max(p[3] for p in per)
     remote_frac = float(np.sum(seg.lengths()[owner != rank])) / N
     step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
     hbm_peak, peak_src = peaks()
@@ -500,9 +520,15 @@ def run_remote(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_r, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapters)",
         "config": {"workload": wl.description, "config": "remote", "remote_token_fraction": remote_frac,
-                   "per_gpu": [{"ms_local": p[0], "ms_remote": p[1], "bit_identical": bool(p[2])} for p in per],
+                   "remote_mode": "in-kernel NVLink peer loads from CUDA-IPC-mapped peer slabs",
+                   "per_gpu": [{"ms_local": p[0], "ms_remote_direct": p[1], "ms_remote_prefetch": p[3],
+                                "bit_identical": bool(p[2])} for p in per],
                    "timing": "CUDA-graph replay, CUDA events, max over ranks"},
         "remote_overhead": ms_r / ms_l - 1.0,
+        "remote_prefetch": {"ms_per_step": ms_p, "value": N * world / (ms_p / 1e3), "overhead": ms_p / ms_l - 1.0,
+                            "mode": "copy-engine fetch (lsv_copy_blocks) of the next layer's peer-owned tiles into "
+                                    f"local staging while the current layer computes; {pf.bytes_per_layer / 1e6:.1f} "
+                                    f"MB/layer over NVLink on GPU {rank}"},
         "all_local": {"ms_per_step": ms_l, "value": N * world / (ms_l / 1e3)},
         "step_hbm": {"frac_local_bytes": step_bytes / (ms_r * 1e-3) / 1e9 / hbm_peak},
         "clocks": clocks,

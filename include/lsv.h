@@ -211,6 +211,13 @@ int lsv_ipc_get_handle(void* dev_ptr, void* handle64_out);
 int lsv_ipc_open_handle(const void* handle64, int32_t device, void** dev_ptr_out);
 int lsv_ipc_close_handle(void* dev_ptr);
 
+/* Fetch: n device-to-device block copies (src[i] -> dst[i], bytes[i]; host arrays of device
+ * addresses) on `stream`, executed by the copy engines (NVLink for peer addresses), leaving the
+ * SMs to the kernels.  The B200 form of the reference's fetch_remote (pool.py:101-132): stage a
+ * peer-owned adapter's next-layer tiles in local HBM while the current layer computes. */
+int lsv_copy_blocks(int32_t n, const void* const* src, void* const* dst, const size_t* bytes,
+                    lsv_stream_t stream);
+
 /* Number of SMs the planner assumes (queried from device 0 once; 148 on B200). */
 int lsv_num_sms(void);
 

@@ -916,6 +916,16 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
   return LSV_OK;
 }
 
+int lsv_copy_blocks(int32_t n, const void* const* src, void* const* dst, const size_t* bytes, lsv_stream_t stream) {
+  if (n < 0 || (n > 0 && (!src || !dst || !bytes))) return fail(LSV_EINVAL, "lsv_copy_blocks: bad arguments");
+  for (int i = 0; i < n; ++i) {
+    if (bytes[i] == 0) continue;
+    if (!src[i] || !dst[i]) return fail(LSV_EINVAL, "lsv_copy_blocks: null block %d", i);
+    LSV_CUDA_CHECK(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  }
+  return LSV_OK;
+}
+
 int lsv_ipc_get_handle(void* dev_ptr, void* handle64_out) {
   if (!dev_ptr || !handle64_out) return fail(LSV_EINVAL, "null pointer");
   cudaIpcMemHandle_t h;

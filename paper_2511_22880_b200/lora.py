@@ -203,6 +203,49 @@ class LoraDeltaEngine:
             ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr(), bp.b_ptrs.data_ptr(),
             xs[0][self.groups[0][0]].shape[0], bp.workspace.data_ptr(), bp.workspace.numel(), st.cuda_stream))
 
+    def forward_prefetch(self, bp: BatchPlan, pf: "RemotePrefetch", xs, ys, stream=None) -> None:
+        """``forward`` with peer-owned adapters fetched one layer ahead into local staging buffers by
+        the copy engines (lsv_copy_blocks) while the current layer computes, so the kernels only
+        read local HBM.  ``bp`` must come from ``pf.plan``."""
+        st = stream or torch.cuda.current_stream(self.device)
+        cs = pf.copy_stream
+        L = self.model.layers
+        cs.wait_stream(st)                                # fork: the copy stream joins st's work
+        pf.fetch(0, cs)
+        for layer in range(L):
+            if layer + 1 < L:
+                if layer >= 1:                            # buffer (layer+1)%2 was read by layer-1
+                    cs.wait_event(pf.done[(layer - 1) % 2])
+                pf.fetch(layer + 1, cs)
+            st.wait_event(pf.ready[layer % 2])
+            self._forward_layers(bp, xs, ys, st, layer, 1)
+            pf.done[layer % 2].record(st)
+        st.wait_stream(cs)                                # join
+
+    def _forward_layers(self, bp, xs, ys, st, l0: int, nl: int) -> None:
+        projs = self.model.projections
+        G, P = len(self.groups), len(projs)
+        S = bp.segments.num_segments
+        xl, ldx, yl, ldy = [], [], [], []
+        for layer in range(l0, l0 + nl):
+            for gname, members in self.groups:
+                x = xs[layer][gname]
+                xl.append(x.data_ptr()); ldx.append(x.stride(0))
+                for p in members:
+                    y = ys[layer][projs[p].name]
+                    yl.append(y.data_ptr()); ldy.append(y.stride(0))
+        arr = lambda t, v: (t * len(v))(*v)   # noqa: E731
+        pd = arr(ctypes.c_void_p, [gp.plan_dev.data_ptr() for gp in bp.group_plans])
+        ph = arr(ctypes.c_void_p, [gp.plan_host.ctypes.data for gp in bp.group_plans])
+        xa, la, ya, lya = (arr(ctypes.c_void_p, xl), arr(ctypes.c_int64, ldx), arr(ctypes.c_void_p, yl),
+                           arr(ctypes.c_int64, ldy))
+        per_layer_ws = bp.workspace.numel() // self.model.layers
+        native.check(native.lib().lsv_lora_forward(
+            nl, G, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
+            ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr() + l0 * G * S * 8,
+            bp.b_ptrs.data_ptr() + l0 * P * S * 8, xs[l0][self.groups[0][0]].shape[0],
+            bp.workspace.data_ptr() + l0 * per_layer_ws, per_layer_ws * nl, st.cuda_stream))
+
     def launches_per_step(self, bp: BatchPlan) -> int:
         """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand
         per member)."""
@@ -252,3 +295,84 @@ def algorithmic_flops(seg: Segments, h_in: int, h_out: int) -> int:
     n = seg.lengths().astype(np.int64)
     r = seg.seg_rank.astype(np.int64)
     return int(np.sum(2 * n * r * (h_in + h_out)))
+
+
+class RemotePrefetch:
+    """Peer-owned adapters fetched a layer ahead (the reference's fetch_remote, pool.py:101-132,
+    as copy-engine copies over NVLink instead of in-kernel peer loads).
+
+    Segment s with ``seg_owner[s] != this GPU`` has its layer-l block (all group A tiles and B tiles
+    of the layer, contiguous in the owner's slab, ``AdapterSlab.layer_block``) copied into staging
+    buffer l % 2; ``plan`` builds a BatchPlan whose pointer tables send those segments' layer-l
+    pointers to the staging copy."""
+
+    ALIGN = 1024
+
+    def __init__(self, eng: LoraDeltaEngine, seg: Segments, seg_owner: np.ndarray,
+                 peer_slabs: dict[int, AdapterSlab]):
+        self.eng, self.seg = eng, seg
+        self.device = eng.device
+        me = eng.device.index or 0
+        model = eng.model
+        self.remote = [s for s in range(seg.num_segments)
+                       if int(seg_owner[s]) != me and int(seg_owner[s]) in peer_slabs]
+        self.owner = seg_owner
+        self.peers = peer_slabs
+        self.stage_off = {}
+        cur = 0
+        for s in self.remote:
+            self.stage_off[s] = cur
+            cur += (model.adapter_bytes(int(seg.seg_rank[s])) // model.layers + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        self.stage_bytes = max(cur, self.ALIGN)
+        self.stage = [torch.empty(self.stage_bytes, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        # per layer: source addresses, destinations (buffer l % 2), sizes
+        self._src = np.zeros((model.layers, len(self.remote)), dtype=np.uint64)
+        self._dst = np.zeros((model.layers, len(self.remote)), dtype=np.uint64)
+        self._len = np.zeros(len(self.remote), dtype=np.uint64)
+        for i, s in enumerate(self.remote):
+            peer = peer_slabs[int(seg_owner[s])]
+            slot = int(seg.seg_slot[s])
+            for l in range(model.layers):
+                off, nb = peer.layer_block(slot, l)
+                self._src[l, i] = peer.base + off
+                self._dst[l, i] = self.stage[l % 2].data_ptr() + self.stage_off[s]
+                self._len[i] = nb
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+
+    @property
+    def bytes_per_layer(self) -> int:
+        return int(self._len.sum())
+
+    def fetch(self, layer: int, stream) -> None:
+        """Copy layer ``layer`` of every remote segment into staging buffer layer % 2 on ``stream``
+        and record ``ready[layer % 2]`` there."""
+        n = len(self.remote)
+        if n:
+            native.check(native.lib().lsv_copy_blocks(
+                n, self._src[layer].ctypes.data, self._dst[layer].ctypes.data, self._len.ctypes.data,
+                stream.cuda_stream))
+        self.ready[layer % 2].record(stream)
+
+    def plan(self) -> BatchPlan:
+        """BatchPlan whose remote segments point into the staging buffers (layer parity)."""
+        eng, seg, model = self.eng, self.seg, self.eng.model
+        bp = eng.prepare(seg)                       # local pointers everywhere
+        L, G, P = model.layers, len(eng.groups), len(model.projections)
+        S = seg.num_segments
+        a = bp.a_ptrs.cpu().numpy().reshape(L, G, S).copy()
+        b = bp.b_ptrs.cpu().numpy().reshape(L, P, S).copy()
+        for s in self.remote:
+            peer = self.peers[int(self.owner[s])]
+            slot = int(seg.seg_slot[s])
+            for l in range(L):
+                base, _ = peer.layer_block(slot, l)
+                dst = self.stage[l % 2].data_ptr() + self.stage_off[s]
+                for gi in range(G):
+                    a[l, gi, s] = dst + int(peer._g_off_rows[slot][l, gi]) - base
+                for p in range(P):
+                    b[l, p, s] = dst + int(peer._b_off_rows[slot][l, p]) - base
+        bp.a_ptrs = torch.from_numpy(a.reshape(L * G, S)).to(self.device)
+        bp.b_ptrs = torch.from_numpy(b.reshape(L * P, S)).to(self.device)
+        return bp

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "lsv_slab_alloc", "lsv_slab_free", "lsv_vimg_assemble", "lsv_plan_vimg_region",
     "lsv_adapter_a_group_bytes", "lsv_pack_adapter_group", "lsv_unpack_adapter_group",
     "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
-    "lsv_lora_forward", "lsv_lora_forward_workspace",
+    "lsv_lora_forward", "lsv_lora_forward_workspace", "lsv_copy_blocks",
 )
 
 _lib = None
@@ -71,6 +71,7 @@ _SIGNATURES = {
     "lsv_lora_expand_group": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "lsv_lora_forward": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "lsv_lora_forward_workspace": (_sz, [_i32, _i32, _vp]),
+    "lsv_copy_blocks": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp]),
 }
 
 

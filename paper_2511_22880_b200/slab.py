@@ -115,6 +115,13 @@ class AdapterSlab:
         """Offset of proj's first A row inside its group tile (rows repeat every group*rank rows)."""
         return int(self._a_off_rows[slot][layer, proj])
 
+    def layer_block(self, slot: int, layer: int) -> tuple[int, int]:
+        """(offset, bytes) of one layer of a slot: every group A tile and B tile of that layer,
+        contiguous (what a remote fetch moves for the layer)."""
+        info = self.slots[slot]
+        per_layer = self.model.adapter_bytes(info.rank) // self.model.layers
+        return int(self._g_off_rows[slot][layer, 0]), per_layer
+
     def a_group_offset(self, slot: int, layer: int, proj: int) -> int:
         return int(self._g_off_rows[slot][layer, self._member[proj][0]])
 

@@ -35,3 +35,49 @@ def test_peer_adapter_loads_bit_identical():
     torch.cuda.synchronize("cuda:0")
     assert torch.equal(y1, y2)
     assert int(bp_peer.a_ptrs[0, 0]) != int(bp_local.a_ptrs[0, 0])   # really a different address
+
+
+def test_remote_prefetch_forward_bit_identical():
+    """The copy-engine fetch path (RemotePrefetch + forward_prefetch: the next layer's peer-owned
+    tiles staged in local HBM while the current layer computes) gives the all-local step's bits on
+    a 3-layer model with every input group."""
+    from paper_2511_22880_b200 import native
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, RemotePrefetch
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import ModelShape, Projection
+    from paper_2511_22880_b200.slab import AdapterSlab
+    native.check(native.lib().lsv_enable_peer(0, 1))
+    h, inter = 1024, 2816
+    model = ModelShape("mini3", 3, (Projection("q_proj", h, h), Projection("k_proj", h, 256), Projection("v_proj", h, 256),
+                                     Projection("o_proj", h, h), Projection("gate_proj", h, inter),
+                                     Projection("up_proj", h, inter), Projection("down_proj", inter, h)))
+    ranks = [8, 16, 128, 64, 24, 32]
+    slabs = []
+    for dev in ("cuda:0", "cuda:1"):
+        slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+        for i, r in enumerate(ranks):
+            slab.fill_random(slab.allocate(f"a{i}", r), 700 + i)
+        slabs.append(slab)
+    torch.cuda.synchronize("cuda:1")
+    tok = np.concatenate([np.full(n, s) for s, n in enumerate([41, 3, 150, 64, 17, 90])])
+    seg = index_tokens(tok, ranks)
+    owner = np.array([1, 0, 1, 1, 0, 1], dtype=np.int32)
+    eng = LoraDeltaEngine(slabs[0])
+    bp_local = eng.prepare(seg)
+    pf = RemotePrefetch(eng, seg, owner, {1: slabs[1]})
+    bp_pf = pf.plan()
+    N = seg.num_tokens
+    g = torch.Generator().manual_seed(3)
+    xs = [{n: torch.randn(N, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16).to("cuda:0")
+           for n, m in model.groups()} for _ in range(model.layers)]
+    ya = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device="cuda:0") for p in model.projections}
+          for _ in range(model.layers)]
+    yb = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device="cuda:0") for p in model.projections}
+          for _ in range(model.layers)]
+    eng.forward(bp_local, xs, ya)
+    eng.forward_prefetch(bp_pf, pf, xs, yb)
+    torch.cuda.synchronize("cuda:0")
+    for layer in range(model.layers):
+        for p in model.projections:
+            assert torch.equal(ya[layer][p.name], yb[layer][p.name]), (layer, p.name)
+    assert pf.bytes_per_layer > 0
