@@ -214,7 +214,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     const int64_t mt_bytes = (int64_t)(np8 + G) * 128 * chunks;
     int nsplit = (int)std::min<int64_t>(chunks, std::max<int64_t>(1, (mt_bytes + target - 1) / target));
     int cps = (chunks + nsplit - 1) / nsplit;          // chunks per split, whole 4-chunk stages
-    if (nsplit > 1) cps = std::min(chunks, round_up(cps, 4));
+    if (nsplit > 1) cps = std::min(chunks, round_up(cps, kShrinkMaxKch));
     nsplit = (chunks + cps - 1) / cps;
     mt.nsplit = nsplit;
     mt.part_off = (int32_t)part_off;
@@ -230,7 +230,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     for (int p0 = 0; p0 < P; p0 += subset_np(P, p0, r)) {
       const int np = subset_np(P, p0, r), rows = np * r;
       const int64_t row_bytes = (int64_t)(np8 + rows) * 128;
-      const int kch = (int)std::max<int64_t>(1, std::min<int64_t>(4, kShrinkSlotBytes / row_bytes));
+      const int kch = (int)std::max<int64_t>(1, std::min<int64_t>(kShrinkMaxKch, kShrinkSlotBytes / row_bytes));
       for (int sp = 0; sp < nsplit; ++sp) {
         ShrinkRec rc{};
         rc.seg = mt.seg; rc.tok_begin = mt.tok_begin; rc.ntok = mt.ntok; rc.rank = r;

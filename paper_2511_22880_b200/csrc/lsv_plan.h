@@ -77,8 +77,16 @@ struct ExpandRec {             // 8 int32
 };
 
 // Pipeline geometry (bytes of shared memory).
-constexpr int kShrinkSlotBytes = 48 * 1024;
-constexpr int kShrinkSlots = 4;
+#ifndef LSV_SHRINK_SLOT_KB
+#define LSV_SHRINK_SLOT_KB 64
+#define LSV_SHRINK_SLOTS 3
+#endif
+#ifndef LSV_SHRINK_MAX_KCH
+#define LSV_SHRINK_MAX_KCH 16
+#endif
+constexpr int kShrinkMaxKch = LSV_SHRINK_MAX_KCH;   // 64-column chunks per pipeline stage, at most
+constexpr int kShrinkSlotBytes = LSV_SHRINK_SLOT_KB * 1024;
+constexpr int kShrinkSlots = LSV_SHRINK_SLOTS;
 constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past short token tiles
 constexpr int kExpandRingBytes = 200 * 1024;   // variable-size items, allocated in issue order
 constexpr int kExpandGuardBytes = 2 * 1024;    // rank-8 K=16 MMA reads one k-core past its tile

@@ -199,15 +199,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
                           &full[slot]);
             }
           }
-        } else if (!(p.dbg & 4) && lane - 1 < kc * pc) {
-          const int c = (lane - 1) / pc, i = (lane - 1) % pc;
-          int mm = m, row = 0, bb = -1;
-          for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
-            bb = 31 - __clz(mm);
-            if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
+        } else if (!(p.dbg & 4)) {
+          for (int bx = lane - 1; bx < kc * pc; bx += 31) {   // kc * pc may exceed the 31 lanes
+            const int c = bx / pc, i = bx % pc;
+            int mm = m, row = 0, bb = -1;
+            for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
+              bb = 31 - __clz(mm);
+              if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
+            }
+            tma_load_2d(dst + (c * np8 + row) * 128, &p.xmap[bb], &full[slot], (g + c) * kChunk,
+                        inf.tok_begin + row);
           }
-          tma_load_2d(dst + (c * np8 + row) * 128, &p.xmap[bb], &full[slot], (g + c) * kChunk,
-                      inf.tok_begin + row);
         }
         if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
