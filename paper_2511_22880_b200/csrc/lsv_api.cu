@@ -53,7 +53,10 @@ int fail(int code, const char* fmt, ...) {
 // measurements in DESIGN.md §4 (profiles/).
 constexpr int kAutoSimtMaxTok = 8;
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
-constexpr int kShrinkWaves = 4;               // target shrink items per SM (balance vs split cost)
+#ifndef LSV_SHRINK_WAVES
+#define LSV_SHRINK_WAVES 8
+#endif
+constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost)
 
 int num_sms_cached() {
   static int sms = -1;

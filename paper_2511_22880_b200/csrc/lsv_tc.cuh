@@ -28,7 +28,10 @@ namespace lsv {
 constexpr int kTcThreads = 192;
 constexpr int kTmemCols = 512;  // four 128-column accumulators
 constexpr int kAccBufs = 4;
-constexpr int kItemQ = 8;       // expand: ring allocations in flight
+#ifndef LSV_EXPAND_ITEMQ
+#define LSV_EXPAND_ITEMQ 6
+#endif
+constexpr int kItemQ = LSV_EXPAND_ITEMQ;   // expand: ring allocations in flight
 
 struct alignas(64) ShrinkParams {
   CUtensorMap xmap[5];          // x [num_tokens][h_in], boxes {64 cols × 8<<b rows}, SWIZZLE_128B
