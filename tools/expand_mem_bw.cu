@@ -16,6 +16,8 @@ struct Args {
   const uint8_t* bsrc;
   int rows, cols, ntiles_m, ntiles_j, bkb, ns, slot;
   size_t bbytes_total;
+  __nv_bfloat16* y;
+  int stg;   // 1: write y back like the expand epilogue (thread = row, 16-byte stores) instead of TMA
 };
 
 __device__ __forceinline__ void tma_store_2d_(const void* tmap, const void* src, int c0, int c1) {
@@ -23,14 +25,14 @@ __device__ __forceinline__ void tma_store_2d_(const void* tmap, const void* src,
                "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
 }
 
-__global__ void __launch_bounds__(64, 1) kern(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(192, 1) kern(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + a.ns * a.slot);
   uint64_t* empty = full + 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < a.ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < a.ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], a.stg ? 4 : 1); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -56,7 +58,26 @@ __global__ void __launch_bounds__(64, 1) kern(const __grid_constant__ Args a) {
       }
       if (++slot == a.ns) { slot = 0; ph ^= 1; }
     }
-  } else if (lane == 0) {   // "consumer": stores the y tile back, then frees the slot
+  } else if (a.stg && warp >= 2) {   // 4 warps: thread = row (48 rows), 32 x 16-byte STG per row
+    const int t = (warp - 2) * 32 + lane;
+    int slot = 0; uint32_t ph = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int m = it / a.ntiles_j, j = it % a.ntiles_j;
+      mbar_wait(&full[slot], ph);
+      const uint8_t* src = ring + slot * a.slot;
+      if (t < 48) {
+        __nv_bfloat16* yrow = a.y + (size_t)(m * 48 + t) * a.cols + j * 256;
+        for (int h = 0; h < 4; ++h)
+          for (int c = 0; c < 8; ++c) {
+            const uint4 w = *reinterpret_cast<const uint4*>(src + h * 48 * 128 + t * 128 + ((c ^ (t & 7)) << 4));
+            *reinterpret_cast<uint4*>(yrow + h * 64 + c * 8) = w;
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == a.ns) { slot = 0; ph ^= 1; }
+    }
+  } else if (!a.stg && warp == 1 && lane == 0) {   // "consumer": stores the y tile back, then frees the slot
     int slot = 0; uint32_t ph = 0;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       const int m = it / a.ntiles_j, j = it % a.ntiles_j;
@@ -91,8 +112,9 @@ int main() {
   int nsm = 0; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int bkb : {8, 32, 64}) for (int ns : {2, 3, 4, 6}) {
+  for (int stg : {0, 1}) for (int bkb : {8, 32, 64}) for (int ns : {2, 3, 4}) {
     Args a{};
+    a.stg = stg; a.y = reinterpret_cast<__nv_bfloat16*>(y);
     a.rows = rows; a.cols = cols; a.bsrc = b; a.bbytes_total = bt; a.bkb = bkb; a.ns = ns;
     a.slot = ((4 * 48 * 128 + bkb * 1024) + 1023) / 1024 * 1024;
     if (ns * a.slot + 1024 + 256 > 220 * 1024) continue;
@@ -107,14 +129,14 @@ int main() {
     float best = 1e9;
     for (int it = 0; it < 5; ++it) {
       cudaEventRecord(e0);
-      kern<<<nsm, 64, smem>>>(a);
+      kern<<<nsm, 192, smem>>>(a);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       if (it > 0 && ms < best) best = ms;
     }
     const double items = (double)a.ntiles_m * a.ntiles_j;
     const double bytes = items * (2.0 * 4 * 48 * 128 + bkb * 1024.0);
-    printf("B tile %2d KB, %d slots x %3d KB: %7.1f us, %7.1f GB/s (%s)\n", bkb, ns, a.slot / 1024, best * 1e3,
+    printf("%s B tile %2d KB, %d slots x %3d KB: %7.1f us, %7.1f GB/s (%s)\n", stg ? "STG" : "TMA", bkb, ns, a.slot / 1024, best * 1e3,
            bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
