@@ -44,7 +44,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c2", "c1", "dp", "remote", "tp", "decode"), default="c2",
+    ap.add_argument("--config", choices=("c2", "c1", "dp", "c3", "remote", "tp", "decode"), default="c2",
                     help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
                          "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
@@ -204,7 +204,13 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     tier = {"auto": native.TIER_AUTO, "simt": native.TIER_SIMT, "tc": native.TIER_TC}[args.tier]
     config = args.config if not (world > 1 and args.config == "c2") else "dp"
-    wl = synth.dp_workloads(world)[rank] if config == "dp" else synth.WORKLOADS[config]()
+    if config == "dp":
+        wl = synth.dp_workloads(world)[rank]
+    elif config == "c3":      # BASELINE config 3: Llama-2-13B shapes, LoRAServe placement + routing
+        from paper_2511_22880_b200 import shapes as _shapes
+        wl = synth.dp_workloads(world, model=_shapes.LLAMA2_13B)[rank]
+    else:
+        wl = synth.WORKLOADS[config]()
     model = wl.model
     seg = wl.segments
     N = seg.num_tokens
