@@ -578,9 +578,25 @@ def run_tp(args, rank, world, local_rank):
         ys.append(yd)
     stream = torch.cuda.Stream(dev)
     torch.cuda.synchronize(dev)
-    for _ in range(args.warmup):
-        with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):
+        eng.forward(st, xs, ys, stream)          # warm tensor maps / NCCL before capture
+    torch.cuda.synchronize(dev)
+    torch.distributed.barrier()
+    # the whole step (kernels and NCCL collectives) as one CUDA graph, replayed
+    graph = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(graph, stream=stream):
             eng.forward(st, xs, ys, stream)
+        timing = "CUDA-graph replay of the whole step incl. NCCL collectives, CUDA events, max over ranks"
+        step = graph.replay
+    except Exception as exc:   # capture unsupported here: time the eager step
+        print(f"[bench] TP graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+        torch.cuda.synchronize(dev)
+        timing = "eager launches incl. NCCL collectives, CUDA events, max over ranks"
+        step = lambda: eng.forward(st, xs, ys, stream)   # noqa: E731
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
     torch.cuda.synchronize(dev)
     torch.distributed.barrier()
     sampler = ClockSampler(dev.index)
@@ -589,7 +605,7 @@ def run_tp(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         e0.record(stream)
         for _ in range(args.steps):
-            eng.forward(st, xs, ys, stream)
+            step()
         e1.record(stream)
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
@@ -627,7 +643,7 @@ def run_tp(args, rank, world, local_rank):
         "config": {"workload": f"llama-3-70b 80 layers x 7 proj, TP{world} (S-LoRA sharding), {n_ad} adapters "
                                f"{traces.assign_power_law_counts(n_ad, traces.DEFAULT_RANKS, 1.0)}, {N} tokens, "
                                f"{seg.num_segments} active", "config": "tp",
-                   "timing": "eager launches incl. NCCL collectives, CUDA events, max over ranks"},
+                   "timing": timing},
         "nccl_ms_per_step": coll_ms, "nccl_share": coll_ms / ms,
         "clocks": clocks,
     }
