@@ -612,11 +612,11 @@ def run_tp(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1) / args.steps
     # NCCL share: the same number of collectives on the same v regions, alone
     import torch.distributed as dist
-    coll = []
-    for p, sp in enumerate(eng.specs):
-        plan_a = st["plans"][p][0]
+    coll = []       # one collective per input group: all-gather (column) / all-reduce (row) of its v images
+    for gi, (_, members) in enumerate(eng.groups):
+        plan_a = st["plans"][gi][0]
         off, nb = eng._region(plan_a)
-        coll.append((sp.column, off, nb))
+        coll.append((eng.specs[members[0]].column, off, nb))
     torch.cuda.synchronize(dev)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ws_a = st["ws"][0]

@@ -195,7 +195,9 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
                       const void* shard_plan_host, const void* full_plan_dev, const void* full_plan_host,
                       void* full_workspace, lsv_stream_t stream);
 
-/* Byte offset and size of a plan's v-image region inside its workspace (what TP exchanges). */
+/* Byte offset and size of a plan's v-image region inside its workspace (what TP exchanges): every
+ * member's images, member p at p * (size / num_proj).  lsv_vimg_assemble handles group plans
+ * member by member (both plans must have the same members). */
 int lsv_plan_vimg_region(const void* plan_host, size_t* offset, size_t* bytes);
 
 /* ---- NVLink peers ----------------------------------------------------------------------

@@ -892,8 +892,8 @@ int lsv_slab_free(void* dev_ptr) {
 int lsv_plan_vimg_region(const void* plan_host, size_t* offset, size_t* bytes) {
   const PlanHeader* h = check_plan(plan_host);
   if (!h || !offset || !bytes) return fail(LSV_EINVAL, "not a liblsv plan");
-  *offset = (size_t)h->ws_vimg;           // projection 0's v images (TP plans have one projection)
-  *bytes = (size_t)h->vimg_stride;
+  *offset = (size_t)h->ws_vimg;           // every member's v images, contiguous (member p at p * vimg_stride)
+  *bytes = (size_t)h->vimg_stride * h->num_proj;
   return LSV_OK;
 }
 
@@ -906,16 +906,18 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
   if (hs->n_mtiles != hf->n_mtiles || hs->num_tokens != hf->num_tokens)
     return fail(LSV_EINVAL, "shard and full plans index different tiles (%d vs %d)", hs->n_mtiles, hf->n_mtiles);
   if (tp < 1 || !gathered || !full_workspace) return fail(LSV_EINVAL, "bad arguments");
-  if (hs->num_proj != 1 || hf->num_proj != 1) return fail(LSV_EINVAL, "TP assembly takes single-projection plans");
+  if (hs->num_proj != hf->num_proj) return fail(LSV_EINVAL, "shard and full plans have different members");
   if (hs->n_simt_items != 0 || hf->n_simt_items != 0)
     return fail(LSV_EUNSUPPORTED, "TP assembly needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
   if (hf->n_mtiles == 0) return LSV_OK;
   const int32_t* sp = static_cast<const int32_t*>(shard_plan_dev);
   const int32_t* fp = static_cast<const int32_t*>(full_plan_dev);
-  vimg_assemble_kernel<<<hf->n_mtiles, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(gathered), region_bytes, tp, sp, hs->off_mtiles, 0, fp, hf->off_mtiles,
-      static_cast<uint8_t*>(full_workspace), hf->ws_vimg);
-  LSV_CUDA_CHECK(cudaGetLastError());
+  for (int pp = 0; pp < hf->num_proj; ++pp) {   // member pp: its shard images and its full-rank images
+    vimg_assemble_kernel<<<hf->n_mtiles, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(gathered) + (size_t)pp * hs->vimg_stride, region_bytes, tp, sp, hs->off_mtiles, 0,
+        fp, hf->off_mtiles, static_cast<uint8_t*>(full_workspace), hf->ws_vimg + pp * hf->vimg_stride);
+    LSV_CUDA_CHECK(cudaGetLastError());
+  }
   return LSV_OK;
 }
 

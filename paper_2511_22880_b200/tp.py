@@ -27,7 +27,7 @@ import torch
 import torch.distributed as dist
 
 from . import native
-from .lora import build_shape_plan, input_group
+from .lora import build_group_plan, input_group  # noqa: F401
 from .segments import Segments
 from .shapes import ModelShape, Projection, kpad
 
@@ -86,28 +86,34 @@ def shard_adapter(lora_a: torch.Tensor, lora_b: torch.Tensor, sp: ShardSpec, tp:
 
 
 class TPSlab:
-    """One rank's shard of every adapter: A and B tiles at their own (shard) ranks."""
+    """One rank's shard of every adapter.  Per layer and input group (model.groups(): column groups
+    q/k/v and gate/up, row groups o and down) one group A tile of the members' A shards at their
+    shard rank (lsv_pack_adapter_group), and per projection its B shard at the B rank."""
 
     ALIGN = 1024
 
     def __init__(self, model: ModelShape, tp: int, rank: int, ranks: list[int], device):
         self.model, self.tp, self.rank = model, tp, rank
         self.specs = shard_specs(model, tp)
+        self.groups = model.groups()
+        self._member = {p: (gi, i, len(m)) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self.device = torch.device(device)
         self.ranks = list(ranks)
-        L, P = model.layers, len(self.specs)
-        self.a_off = np.zeros((len(ranks), L, P), dtype=np.int64)
+        L, P, G = model.layers, len(self.specs), len(self.groups)
+        self.g_off = np.zeros((len(ranks), L, G), dtype=np.int64)
         self.b_off = np.zeros((len(ranks), L, P), dtype=np.int64)
         cur = 0
         for s, r in enumerate(ranks):
             cur = (cur + self.ALIGN - 1) // self.ALIGN * self.ALIGN
             for l in range(L):
-                for p, sp in enumerate(self.specs):
-                    ra, rb = sp.a_rank(r, tp), sp.b_rank(r, tp)
-                    self.a_off[s, l, p] = cur
-                    cur += 2 * ra * sp.h_in
-                    self.b_off[s, l, p] = cur
-                    cur += 2 * kpad(rb) * sp.h_out
+                for gi, (_, members) in enumerate(self.groups):
+                    sp0 = self.specs[members[0]]
+                    self.g_off[s, l, gi] = cur
+                    cur += 2 * len(members) * sp0.a_rank(r, tp) * sp0.h_in
+                    for p in members:
+                        sp = self.specs[p]
+                        self.b_off[s, l, p] = cur
+                        cur += 2 * kpad(sp.b_rank(r, tp)) * sp.h_out
         self.capacity = cur + self.ALIGN
         ptr = ctypes.c_void_p()
         native.check(native.lib().lsv_slab_alloc(self.capacity, self.device.index or 0, ctypes.byref(ptr)))
@@ -119,19 +125,24 @@ class TPSlab:
         except Exception:
             pass
 
+    def _pack(self, slot: int, layer: int, proj: int, a_sh: torch.Tensor, b_sh: torch.Tensor, st) -> None:
+        sp = self.specs[proj]
+        r = self.ranks[slot]
+        gi, idx, nproj = self._member[proj]
+        ra, rb = sp.a_rank(r, self.tp), sp.b_rank(r, self.tp)
+        lib = native.lib()
+        native.check(lib.lsv_pack_adapter_group(a_sh.data_ptr(), nproj, idx, ra, sp.h_in,
+                                                self.base + int(self.g_off[slot, layer, gi]), st))
+        native.check(lib.lsv_pack_adapter(None, b_sh.data_ptr(), rb, sp.h_in, sp.h_out, None,
+                                          self.base + int(self.b_off[slot, layer, proj]), st))
+
     def load_full(self, slot: int, layer: int, proj: int, lora_a: torch.Tensor, lora_b: torch.Tensor,
                   stream=None) -> None:
         """Pack this rank's shard of a full PEFT-layout adapter (lora_A [r, h_in], lora_B [h_out, r])."""
-        sp, tp, t = self.specs[proj], self.tp, self.rank
-        r = self.ranks[slot]
+        sp = self.specs[proj]
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        a_sh, b_sh = shard_adapter(lora_a.to(self.device), lora_b.to(self.device), sp, tp, t)
-        ra, rb = sp.a_rank(r, tp), sp.b_rank(r, tp)
-        lib = native.lib()
-        native.check(lib.lsv_pack_adapter(a_sh.data_ptr(), None, ra, sp.h_in, sp.h_out,
-                                          self.base + int(self.a_off[slot, layer, proj]), None, st))
-        native.check(lib.lsv_pack_adapter(None, b_sh.data_ptr(), rb, sp.h_in, sp.h_out, None,
-                                          self.base + int(self.b_off[slot, layer, proj]), st))
+        a_sh, b_sh = shard_adapter(lora_a.to(self.device), lora_b.to(self.device), sp, self.tp, self.rank)
+        self._pack(slot, layer, proj, a_sh.contiguous(), b_sh.contiguous(), st)
 
     def fill_random_full(self, slot: int, seed: int, full: ModelShape) -> None:
         """Seeded full adapter (same on every rank), this rank's shard packed."""
@@ -149,55 +160,58 @@ class TPSlab:
         r = self.ranks[slot]
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
-        lib = native.lib()
         st = torch.cuda.current_stream(self.device).cuda_stream
         for l in range(self.model.layers):
             for p, sp in enumerate(self.specs):
                 ra, rb = sp.a_rank(r, self.tp), sp.b_rank(r, self.tp)
                 a = (torch.randn((ra, sp.h_in), generator=g, device=self.device) * 0.02).to(torch.bfloat16)
                 b = (torch.randn((sp.h_out, rb), generator=g, device=self.device) * 0.1).to(torch.bfloat16)
-                native.check(lib.lsv_pack_adapter(a.data_ptr(), None, ra, sp.h_in, sp.h_out,
-                                                  self.base + int(self.a_off[slot, l, p]), None, st))
-                native.check(lib.lsv_pack_adapter(None, b.data_ptr(), rb, sp.h_in, sp.h_out, None,
-                                                  self.base + int(self.b_off[slot, l, p]), st))
+                self._pack(slot, l, p, a, b, st)
 
     def pointer_tables(self, seg_slots) -> tuple[torch.Tensor, torch.Tensor]:
-        L, P = self.model.layers, len(self.specs)
+        """Device tables: group A tiles [layers*groups, S], B tiles [layers*projections, S]."""
+        L, P, G = self.model.layers, len(self.specs), len(self.groups)
         slots = np.asarray(seg_slots, dtype=np.int64)
-        a = (self.base + self.a_off[slots]).reshape(len(slots), L * P).T.copy()
+        a = (self.base + self.g_off[slots]).reshape(len(slots), L * G).T.copy()
         b = (self.base + self.b_off[slots]).reshape(len(slots), L * P).T.copy()
         return torch.from_numpy(a).to(self.device), torch.from_numpy(b).to(self.device)
 
 
 class TPLoraDeltaEngine:
-    """Delta path of one TP rank: shrink -> NCCL exchange of v -> (assemble) -> expand."""
+    """Delta path of one TP rank, per layer and input group: fused shrink of the group's A shards
+    -> one NCCL exchange of every member's v images (all-gather for a column group, all-reduce for
+    a row group) -> (column: lsv_vimg_assemble to full rank) -> one-launch group expand."""
 
     def __init__(self, slab: TPSlab, group=None):
         native.load()
         self.slab, self.group = slab, group
         self.tp, self.rank, self.device = slab.tp, slab.rank, slab.device
         self.specs = slab.specs
+        self.groups = slab.groups
+        self._member = {p: (gi, i) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
 
     def prepare(self, seg: Segments) -> dict:
-        """Per projection: shrink plan (A ranks) and expand plan (B ranks); all tensor-core tier so
-        every rank's plans tile the batch identically."""
+        """Per input group: shrink plan (A shard ranks) and expand plan (B ranks; the same plan for
+        a row group); all tensor-core tier so every rank's plans tile the batch identically."""
         tp = self.tp
         plans = {}
-        ws_need = 0
-        for p, sp in enumerate(self.specs):
-            ra = np.array([sp.a_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
-            rb = np.array([sp.b_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
-            key_a = (sp.h_in, sp.h_out, tuple(ra))
-            key_b = (sp.h_in, sp.h_out, tuple(rb))
-            for key, rr in ((key_a, ra), (key_b, rb)):
-                if key not in plans:
-                    s2 = Segments(seg.perm, seg.seg_indptr, seg.seg_slot, rr, seg.request_order)
-                    plans[key] = build_shape_plan(s2, sp.h_in, sp.h_out, native.TIER_TC, self.device)
-                    ws_need = max(ws_need, plans[key].workspace_bytes)
-            plans[p] = (plans[key_a], plans[key_b])
-        ws = [torch.zeros(max(ws_need, 256), dtype=torch.uint8, device=self.device) for _ in range(2)]
+        ws_a_need = ws_b_need = 0
+        for gi, (_, members) in enumerate(self.groups):
+            sp0 = self.specs[members[0]]
+            ra = np.array([sp0.a_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
+            rb = np.array([sp0.b_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
+            h_outs = [self.specs[p].h_out for p in members]
+            mk = lambda rr: build_group_plan(Segments(seg.perm, seg.seg_indptr, seg.seg_slot, rr, seg.request_order),  # noqa: E731
+                                             sp0.h_in, h_outs, native.TIER_TC, self.device, members)
+            plan_a = mk(ra)
+            plan_b = mk(rb) if sp0.column else plan_a
+            plans[gi] = (plan_a, plan_b)
+            ws_a_need = max(ws_a_need, plan_a.workspace_bytes)
+            ws_b_need = max(ws_b_need, plan_b.workspace_bytes)
+        ws = [torch.zeros(max(ws_a_need, 256), dtype=torch.uint8, device=self.device),
+              torch.zeros(max(ws_b_need, 256), dtype=torch.uint8, device=self.device)]
         a_ptrs, b_ptrs = self.slab.pointer_tables(seg.seg_slot)
-        region = max(self._region(plans[p][0])[1] for p in range(len(self.specs)))
+        region = max(self._region(plans[gi][0])[1] for gi in range(len(self.groups)))
         gathered = torch.empty(self.tp * max(region, 16), dtype=torch.uint8, device=self.device)
         return {"seg": seg, "plans": plans, "ws": ws, "a_ptrs": a_ptrs, "b_ptrs": b_ptrs, "gathered": gathered}
 
@@ -207,39 +221,62 @@ class TPLoraDeltaEngine:
         native.check(native.lib().lsv_plan_vimg_region(sp.plan_host.ctypes.data, ctypes.byref(off), ctypes.byref(nb)))
         return off.value, nb.value
 
-    def apply(self, st: dict, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
-        """x: this rank's input (full h_in for column-parallel, its h_in slice for row-parallel);
-        y: this rank's h_out slice."""
+    def _shrink_exchange(self, st: dict, layer: int, gi: int, x: torch.Tensor, strm) -> torch.Tensor:
+        """Fused shrink of group gi + its NCCL exchange; returns the workspace the expand reads."""
         lib = native.lib()
-        sp = self.specs[proj]
-        plan_a, plan_b = st["plans"][proj]
-        seg = st["seg"]
-        S = seg.num_segments
-        row = layer * len(self.specs) + proj
-        strm = stream or torch.cuda.current_stream(self.device)
+        members = self.groups[gi][1]
+        sp0 = self.specs[members[0]]
+        plan_a, plan_b = st["plans"][gi]
+        S = st["seg"].num_segments
+        row = layer * len(self.groups) + gi
         ws_a, ws_b = st["ws"]
-        native.check(lib.lsv_lora_shrink(x.data_ptr(), x.stride(0), x.shape[0], sp.h_in,
+        native.check(lib.lsv_lora_shrink(x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
                                          st["a_ptrs"].data_ptr() + row * S * 8, plan_a.plan_dev.data_ptr(),
                                          plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(), strm.cuda_stream))
         off, nb = self._region(plan_a)
         with torch.cuda.stream(strm):
-            if sp.column:
-                src = ws_a[off:off + nb]
+            if sp0.column:
                 dst = st["gathered"][:self.tp * nb]
-                dist.all_gather_into_tensor(dst, src, group=self.group)
+                dist.all_gather_into_tensor(dst, ws_a[off:off + nb], group=self.group)
                 native.check(lib.lsv_vimg_assemble(dst.data_ptr(), nb, self.tp, plan_a.plan_dev.data_ptr(),
                                                    plan_a.plan_host.ctypes.data, plan_b.plan_dev.data_ptr(),
                                                    plan_b.plan_host.ctypes.data, ws_b.data_ptr(), strm.cuda_stream))
-                ws_e = ws_b
-            else:
-                v = ws_a[off:off + nb].view(torch.bfloat16)
-                dist.all_reduce(v, group=self.group)     # sum of the per-rank partial v images
-                ws_e = ws_a
-        native.check(lib.lsv_lora_expand(y.data_ptr(), y.stride(0), y.shape[0], sp.h_out,
-                                         st["b_ptrs"].data_ptr() + row * S * 8, plan_b.plan_dev.data_ptr(),
-                                         plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(), strm.cuda_stream))
+                return ws_b
+            dist.all_reduce(ws_a[off:off + nb].view(torch.bfloat16), group=self.group)   # partial v sums
+            return ws_a
+
+    def apply_group(self, st: dict, layer: int, gi: int, x: torch.Tensor, ys: list[torch.Tensor], stream=None) -> None:
+        """Every member of input group gi: x is this rank's input (full h_in for a column group, its
+        h_in slice for a row group); ys[i] member i's h_out slice."""
+        strm = stream or torch.cuda.current_stream(self.device)
+        ws_e = self._shrink_exchange(st, layer, gi, x, strm)
+        members = self.groups[gi][1]
+        plan_b = st["plans"][gi][1]
+        S = st["seg"].num_segments
+        P = len(self.specs)
+        n = len(members)
+        y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+        ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys])
+        b_arr = (ctypes.c_void_p * n)(*[st["b_ptrs"].data_ptr() + (layer * P + p) * S * 8 for p in members])
+        native.check(native.lib().lsv_lora_expand_group(
+            ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys[0].shape[0], ctypes.addressof(b_arr),
+            plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(), strm.cuda_stream))
+
+    def apply(self, st: dict, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor, stream=None) -> None:
+        """One projection (its group's shrink and exchange, then its own expand)."""
+        strm = stream or torch.cuda.current_stream(self.device)
+        gi, idx = self._member[proj]
+        ws_e = self._shrink_exchange(st, layer, gi, x, strm)
+        plan_b = st["plans"][gi][1]
+        S = st["seg"].num_segments
+        row = layer * len(self.specs) + proj
+        sp = self.specs[proj]
+        native.check(native.lib().lsv_lora_expand_proj(
+            y.data_ptr(), y.stride(0), y.shape[0], sp.h_out, idx, st["b_ptrs"].data_ptr() + row * S * 8,
+            plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(), strm.cuda_stream))
 
     def forward(self, st: dict, xs, ys, stream=None) -> None:
         for layer in range(self.slab.model.layers):
-            for p, sp in enumerate(self.specs):
-                self.apply(st, layer, p, xs[layer][input_group(sp.name)], ys[layer][sp.name], stream)
+            for gi, (gname, members) in enumerate(self.groups):
+                self.apply_group(st, layer, gi, xs[layer][gname], [ys[layer][self.specs[p].name] for p in members],
+                                 stream)

@@ -85,3 +85,97 @@ def test_tp2_column_and_row_parallel():
     yq, yo, refq, refo = res
     assert oracle.max_rel_err(yq, refq) <= TOL
     assert oracle.max_rel_err(yo, refo) <= TOL
+
+
+def _worker_groups(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        from oracle import oracle
+        from tests._cases import bf16_bits
+        from paper_2511_22880_b200.segments import index_tokens
+        from paper_2511_22880_b200.shapes import ModelShape, Projection
+        from paper_2511_22880_b200.tp import TPLoraDeltaEngine, TPSlab
+        h, kv, inter = 1024, 256, 2816
+        model = ModelShape("tp-mini", 2, (Projection("q_proj", h, h), Projection("k_proj", h, kv),
+                                          Projection("v_proj", h, kv), Projection("o_proj", h, h),
+                                          Projection("gate_proj", h, inter), Projection("up_proj", h, inter),
+                                          Projection("down_proj", inter, h)))
+        ranks = [8, 24, 128, 64, 16]
+        tok = np.concatenate([np.full(n, s) for s, n in enumerate([41, 130, 17, 64, 9])])
+        seg = index_tokens(tok, ranks)
+        N = seg.num_tokens
+        g = torch.Generator().manual_seed(17)
+        full = {}
+        for s_, r in enumerate(ranks):           # the same full adapters on every rank
+            for l in range(model.layers):
+                for p, pr in enumerate(model.projections):
+                    full[(s_, l, p)] = ((torch.randn(r, pr.h_in, generator=g) / pr.h_in ** 0.5).to(torch.bfloat16),
+                                        (torch.randn(pr.h_out, r, generator=g) / r ** 0.5).to(torch.bfloat16))
+        slab = TPSlab(model, world, rank, ranks, dev)
+        for (s_, l, p), (a, b) in full.items():
+            slab.load_full(s_, l, p, a, b)
+        eng = TPLoraDeltaEngine(slab)
+        st = eng.prepare(seg)
+        xs_full = [{n: torch.randn(N, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16)
+                    for n, m in model.groups()} for _ in range(model.layers)]
+        xs, ys = [], []
+        for l in range(model.layers):
+            xd, yd = {}, {}
+            for n, m in model.groups():
+                sp0 = slab.specs[m[0]]
+                xf = xs_full[l][n]
+                xd[n] = (xf if sp0.column else xf[:, rank * sp0.h_in:(rank + 1) * sp0.h_in]).contiguous().to(dev)
+                for p in m:
+                    yd[model.projections[p].name] = torch.zeros(N, slab.specs[p].h_out, dtype=torch.bfloat16, device=dev)
+            xs.append(xd)
+            ys.append(yd)
+        eng.forward(st, xs, ys)
+        torch.cuda.synchronize()
+        errs = []
+        for l in range(model.layers):
+            for p, pr in enumerate(model.projections):
+                parts = [torch.zeros_like(ys[l][pr.name]) for _ in range(world)]
+                dist.all_gather(parts, ys[l][pr.name])
+                if rank == 0:
+                    got = torch.cat(parts, 1).float().cpu().numpy()
+                    grp = [n for n, m in model.groups() if p in m][0]
+                    ref = oracle.delta_c(bf16_bits(xs_full[l][grp]), seg.seg_indptr, seg.seg_rank,
+                                         [bf16_bits(full[(int(sl), l, p)][0]) for sl in seg.seg_slot],
+                                         [bf16_bits(full[(int(sl), l, p)][1]) for sl in seg.seg_slot], pr.h_out)
+                    errs.append((l, pr.name, oracle.max_rel_err(got[:N], ref[:N])))
+        if rank == 0:
+            q.put(errs)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_tp2_forward_input_groups():
+    """TP2 forward over every input group of a 2-layer mini Llama: fused q/k/v and gate/up shrinks of
+    rank-sharded A shards, one all-gather per column group + assembly, one all-reduce per row group,
+    one-launch group expands — every projection within the bf16 tolerance of the unsharded oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_groups, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    import queue as _queue
+    res = None
+    for _ in range(600):
+        try:
+            res = q.get(timeout=1)
+            break
+        except _queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res is not None and len(res) == 14
+    for layer, name, err in res:
+        assert err <= TOL, (layer, name, err)
