@@ -612,11 +612,13 @@ def run_tp(args, rank, world, local_rank):
     ms = e0.elapsed_time(e1) / args.steps
     # NCCL share: the same number of collectives on the same v regions, alone
     import torch.distributed as dist
-    coll = []       # one collective per input group: all-gather (column) / all-reduce (row) of its v images
+    coll = []       # the NCCL collectives the step still issues: all-reduce of each row group's partial v
+    fused = st.get("fused") is not None   # column groups exchange inside the kernels (NVLink stores)
     for gi, (_, members) in enumerate(eng.groups):
         plan_a = st["plans"][gi][0]
         off, nb = eng._region(plan_a)
-        coll.append((eng.specs[members[0]].column, off, nb))
+        if not (fused and eng.specs[members[0]].column):
+            coll.append((eng.specs[members[0]].column, off, nb))
     torch.cuda.synchronize(dev)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ws_a = st["ws"][0]
@@ -645,6 +647,9 @@ def run_tp(args, rank, world, local_rank):
                                f"{seg.num_segments} active", "config": "tp",
                    "timing": timing},
         "nccl_ms_per_step": coll_ms, "nccl_share": coll_ms / ms,
+        "exchange": ("column groups (q/k/v, gate/up): shrink epilogue stores each shard into every rank's full-rank "
+                     "v image over NVLink + flag (no NCCL); row groups (o, down): NCCL all-reduce") if fused
+                    else "NCCL all-gather (column groups) / all-reduce (row groups)",
         "clocks": clocks,
     }
 

@@ -195,6 +195,27 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
                       const void* shard_plan_host, const void* full_plan_dev, const void* full_plan_host,
                       void* full_workspace, lsv_stream_t stream);
 
+/* Fused compute + collective for column-parallel groups (the NCCL all-gather + assembly in one
+ * kernel, over NVLink): the shrink of this rank's rank-shard plan writes every (token, member,
+ * 8-column) unit of its v straight into column tp_rank*rs + k of the member's full-rank image on
+ * every rank (vfull_dst[d]: rank d's image base for this layer/group, device addresses mapped with
+ * lsv_ipc_open_handle; member p at p * full vimg_stride, m-tile at the full plan's offsets), then
+ * its last CTA adds 1 to flags[d] on every rank (system-scope release).  full_plan: the full-rank
+ * plan (same segments and members).  Tensor-core tier only (LSV_TIER_TC plans). */
+int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in,
+                               const void* const* a_ptrs, const void* plan_dev, const void* plan_host,
+                               void* workspace, size_t workspace_bytes, int32_t tp, int32_t tp_rank,
+                               void* const* vfull_dst, const void* full_plan_dev,
+                               const void* full_plan_host, int32_t* const* flags, lsv_stream_t stream);
+
+/* The matching expand: waits until flag[0] == expect (every rank's shard has landed in vimg_base),
+ * re-arms flag[0..1] for the next use, and expands every member from vimg_base (member p's images
+ * at p * vimg_stride of plan). */
+int lsv_lora_expand_group_tp(void* const* ys, const int64_t* ldys, int32_t num_tokens,
+                             const void* const* const* b_ptrs, const void* plan_dev,
+                             const void* plan_host, const void* vimg_base, int32_t* flag,
+                             int32_t expect, lsv_stream_t stream);
+
 /* Byte offset and size of a plan's v-image region inside its workspace (what TP exchanges): every
  * member's images, member p at p * (size / num_proj).  lsv_vimg_assemble handles group plans
  * member by member (both plans must have the same members). */

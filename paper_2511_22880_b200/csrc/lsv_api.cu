@@ -485,8 +485,17 @@ int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_d
 // wait_prev = 0: the previous launch neither writes what this shrink reads nor reads what it
 // writes (lsv_lora_forward's per-(layer, group) workspace slices), so it need not wait for it;
 // pdl = false: a plain launch, ordered after all earlier work in the stream.
+struct TpScatter {
+  int tp = 0, tp_rank = 0;
+  const PlanHeader* fh = nullptr;
+  const int32_t* fplan = nullptr;
+  void* const* vdst = nullptr;
+  int32_t* const* flags = nullptr;
+};
+
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
-               const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true) {
+               const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true,
+               const TpScatter* tps = nullptr) {
   if (h->n_simt_items > 0) {
     // grid.y covers the widest SIMT group (num_proj x the largest SIMT rank) in 8-row blocks
     const int32_t* hp = reinterpret_cast<const int32_t*>(h);
@@ -511,6 +520,14 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.grid_bar = h->n_counters;
     p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
+    if (tps != nullptr) {
+      p.tp = tps->tp; p.tp_rank = tps->tp_rank;
+      p.fplan = tps->fplan; p.f_off_mtiles = tps->fh->off_mtiles; p.vstride_f = tps->fh->vimg_stride;
+      for (int d = 0; d < tps->tp; ++d) {
+        p.vdst[d] = static_cast<uint8_t*>(tps->vdst[d]);
+        p.flags[d] = tps->flags[d];
+      }
+    }
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
     LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl));
@@ -521,7 +538,8 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
 // Expand of members [p0, p0 + np) of a plan: np == num_proj uses the combined list (one launch
 // for every member), np == 1 member p0's own list.
 int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys, int32_t num_tokens,
-               const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st) {
+               const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st,
+               const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0) {
   for (int i = 0; i < np && h->n_simt_items > 0; ++i) {
     const int pp = p0 + i, h_out = h->h_outs[pp];
     simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 255) / 256), 128, 0, st>>>(
@@ -543,10 +561,11 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
     p.ldy[pp] = ldys[i];
     p.b_ptrs[pp] = b_ptrs[i];
     p.tws[pp] = b_tile_width(h->h_outs[pp]);
-    p.ws_vimg[pp] = h->ws_vimg + pp * h->vimg_stride;
+    p.ws_vimg[pp] = (vimg_base ? 0 : h->ws_vimg) + pp * h->vimg_stride;
     tw_max = std::max(tw_max, p.tws[pp]);
   }
-  p.plan = plan; p.ws = ws;
+  p.plan = plan; p.ws = vimg_base ? const_cast<uint8_t*>(vimg_base) : ws;
+  p.wait_flag = wait_flag; p.wait_target = wait_target;
   p.off_recs = all ? h->off_expand_recs_all : h->off_expand_recs_p[p0];
   p.off_cta = all ? h->off_expand_cta_all : h->off_expand_cta_p[p0];
   p.tw_max = tw_max;
@@ -841,6 +860,45 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
     }
   }
   return LSV_OK;
+}
+
+int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in, const void* const* a_ptrs,
+                               const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                               int32_t tp, int32_t tp_rank, void* const* vfull_dst, const void* full_plan_dev,
+                               const void* full_plan_host, int32_t* const* flags, lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  const PlanHeader* fh = check_plan(full_plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (!fh || !full_plan_dev) return fail(LSV_EINVAL, "full_plan is not a liblsv plan");
+  if (tp < 1 || tp > kMaxTp || tp_rank < 0 || tp_rank >= tp || !vfull_dst || !flags)
+    return fail(LSV_EINVAL, "lsv_lora_shrink_tp_scatter: bad tp / rank / destinations");
+  if (fh->n_mtiles != h->n_mtiles || fh->num_proj != h->num_proj || fh->num_tokens != h->num_tokens)
+    return fail(LSV_EINVAL, "shard and full plans index different tiles");
+  if (h->n_simt_items != 0 || fh->n_simt_items != 0)
+    return fail(LSV_EUNSUPPORTED, "TP scatter needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
+  if (h->h_in != h_in) return fail(LSV_EINVAL, "h_in %d does not match the plan's %d", h_in, h->h_in);
+  if (h->num_tokens == 0) return LSV_OK;
+  if (!x || !a_ptrs || !aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "bad x / a_ptrs");
+  for (int d = 0; d < tp; ++d)
+    if (!vfull_dst[d] || !flags[d]) return fail(LSV_EINVAL, "rank %d: null destination or flag", d);
+  TpScatter tps;
+  tps.tp = tp; tps.tp_rank = tp_rank; tps.fh = fh; tps.fplan = static_cast<const int32_t*>(full_plan_dev);
+  tps.vdst = vfull_dst; tps.flags = flags;
+  return run_shrink(h, x, ldx, num_tokens, a_ptrs, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream), 1, true, &tps);
+}
+
+int lsv_lora_expand_group_tp(void* const* ys, const int64_t* ldys, int32_t num_tokens, const void* const* const* b_ptrs,
+                             const void* plan_dev, const void* plan_host, const void* vimg_base, int32_t* flag,
+                             int32_t expect, lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (!h || !plan_dev) return fail(LSV_EINVAL, "not a liblsv plan");
+  if (!ys || !ldys || !b_ptrs || !vimg_base || !flag) return fail(LSV_EINVAL, "lsv_lora_expand_group_tp: null argument");
+  if (num_tokens < h->num_tokens) return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (h->n_simt_items != 0) return fail(LSV_EUNSUPPORTED, "TP expand needs every segment on the tensor-core tier");
+  if (h->num_tokens == 0) return LSV_OK;
+  return run_expand(h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev), nullptr,
+                    static_cast<cudaStream_t>(stream), static_cast<const uint8_t*>(vimg_base), flag, expect);
 }
 
 size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const void* const* plans_host) {

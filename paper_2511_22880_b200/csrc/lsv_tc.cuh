@@ -26,6 +26,7 @@
 namespace lsv {
 
 constexpr int kTcThreads = 192;
+constexpr int kMaxTp = 8;       // tensor-parallel ranks a scatter shrink writes to
 constexpr int kTmemCols = 512;  // four 128-column accumulators
 constexpr int kAccBufs = 4;
 #ifndef LSV_EXPAND_ITEMQ
@@ -44,6 +45,14 @@ struct alignas(64) ShrinkParams {
   int acc_cols;                 // TMEM accumulator width (128 -> 4 buffers, 256 -> 2)
   int wait_prev;                // 0: the previous launch is another input group's expand, which this
                                 // launch neither reads nor overwrites: start without waiting for it
+  // tensor-parallel scatter (tp > 0): instead of this rank's shard images, every (token, member,
+  // 8-column) unit goes to column tp_rank*rs + k of the member's full-rank image on every rank
+  // (vdst[d]: rank d's image base for this layer/group, CUDA-IPC-mapped); the last CTA then bumps
+  // every rank's flag.  fplan: the full-rank plan (same m-tiles) on the device.
+  int tp, tp_rank, vstride_f, f_off_mtiles;
+  const int32_t* fplan;
+  uint8_t* vdst[kMaxTp];
+  int* flags[kMaxTp];
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -60,6 +69,8 @@ struct alignas(64) ExpandParams {
   int tws[kMaxProj];            // each member's h_out tile width (its B slab layout: 128 or 256)
   int tw_max;                   // TMEM accumulator width
   int off_recs, off_cta;
+  int* wait_flag;               // TP: wait until *wait_flag == wait_target (every rank's shard written),
+  int wait_target;              //     then the last CTA through re-arms it ([0] flag, [1] pass counter)
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -135,6 +146,33 @@ constexpr int kShrinkRecCh = 16;
 constexpr int kExpandRecCh = 32;
 using ShrinkRecBuf = WarpRecBuf<ShrinkRec, kShrinkRecCh>;
 using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
+
+// TP scatter of one 16-byte unit (8 k of member pp, token t of m-tile mtile; k local to the shard)
+// into every rank's full-rank image: column tp_rank * rs + k of K = kpad(full rank).
+__device__ __forceinline__ void tp_scatter(const ShrinkParams& p, int mtile, int pp, int t, int k, int rs, int np16,
+                                           const uint4& w) {
+  const MTile mf = reinterpret_cast<const MTile*>(p.fplan + p.f_off_mtiles)[mtile];
+  const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, p.tp_rank * rs + k, kpad(mf.rank), np16);
+  for (int d = 0; d < p.tp; ++d) *reinterpret_cast<uint4*>(p.vdst[d] + off) = w;
+}
+// The full image's k pad (full rank % 16 == 8) is written as zeros by the last shard's rank.
+__device__ __forceinline__ void tp_scatter_pad(const ShrinkParams& p, int mtile, int pp, int t, int np16) {
+  const MTile mf = reinterpret_cast<const MTile*>(p.fplan + p.f_off_mtiles)[mtile];
+  const int kpf = kpad(mf.rank);
+  if (p.tp_rank != p.tp - 1 || kpf == mf.rank) return;
+  const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, mf.rank, kpf, np16);
+  for (int d = 0; d < p.tp; ++d) *reinterpret_cast<uint4*>(p.vdst[d] + off) = make_uint4(0, 0, 0, 0);
+}
+// No split tiles: the CTAs count themselves out (counter slot after the grid barrier's) and the
+// last one signals every rank.
+__device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
+  if (threadIdx.x != 0) return;
+  int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+  if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) {
+    bar[1] = 0;
+    for (int d = 0; d < p.tp; ++d) red_release_sys_add(p.flags[d], 1);
+  }
+}
 
 __host__ __device__ constexpr int shrink_smem_bytes() {
   return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
@@ -297,7 +335,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
                 w.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
                 w.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
                 const int pp = inf.p0 + j0 / r;
-                *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
+                if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w);
+                else *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
               } else {
                 float4* dst = reinterpret_cast<float4*>(part + j0);
                 dst[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
@@ -307,7 +346,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
           }
         }
       }
-      if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
+      if (valid && inf.nsplit == 1 && p.tp > 0) {
+        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
+      } else if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
         for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp)
           *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16)) = make_uint4(0, 0, 0, 0);
       }
@@ -320,10 +361,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   }
   tc_fence_before();
   __threadfence();             // partials visible device-wide before the grid barrier
+  if (p.tp > 0) __threadfence_system();   // scattered images visible to the peers
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
-  if (p.n_red == 0) return;
+  if (p.n_red == 0) {
+    if (p.tp > 0) tp_signal(p);
+    return;
+  }
 
   // ---- grid-wide split-K reduction (all CTAs are co-resident: grid <= SMs, 1 CTA per SM) ----
   // Every (token, 8-wide k unit) of every split tile is summed over its splits in fixed split
@@ -370,13 +415,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     uint4 w;
     w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
     w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
-    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+    if (p.tp > 0) {
+      if (k0 < mt.rank) tp_scatter(p, red[2 * e], pp, t, k0, mt.rank, np16, w);
+      if (k0 == 0) tp_scatter_pad(p, red[2 * e], pp, t, np16);   // once per (token, member)
+    } else {
+      *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+    }
   }
+  if (p.tp > 0) __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 5);
   if (threadIdx.x == 0 && atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) {
     bar[0] = 0;                // every CTA is past the barrier: re-arm it for the next launch
     bar[1] = 0;
+    if (p.tp > 0)              // the last CTA out: every rank's copy of this group is complete
+      for (int d = 0; d < p.tp; ++d) red_release_sys_add(p.flags[d], 1);
   }
 }
 
@@ -430,6 +483,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
   const int cta = blockIdx.x;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
   pdl_wait();                 // v images come from the shrink launch; y from earlier work
+  if (p.wait_flag != nullptr) {   // TP: the peers' shards of the v images have landed here too
+    if (threadIdx.x == 0) {
+      while (ld_acquire_sys(p.wait_flag) < p.wait_target) __nanosleep(32);
+      fence_proxy_async_global();
+      if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
+        p.wait_flag[1] = 0;
+        p.wait_flag[0] = 0;
+      }
+    }
+    __syncthreads();
+  }
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 

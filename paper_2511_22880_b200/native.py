@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "lsv_adapter_a_group_bytes", "lsv_pack_adapter_group", "lsv_unpack_adapter_group",
     "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
     "lsv_lora_forward", "lsv_lora_forward_workspace", "lsv_copy_blocks",
+    "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
 )
 
 _lib = None
@@ -72,6 +73,9 @@ _SIGNATURES = {
     "lsv_lora_forward": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
     "lsv_lora_forward_workspace": (_sz, [_i32, _i32, _vp]),
     "lsv_copy_blocks": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp]),
+    "lsv_lora_shrink_tp_scatter": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
+                                                  _vp, _vp, _vp, _vp, _vp]),
+    "lsv_lora_expand_group_tp": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
 }
 
 

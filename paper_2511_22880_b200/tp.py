@@ -213,7 +213,72 @@ class TPLoraDeltaEngine:
         a_ptrs, b_ptrs = self.slab.pointer_tables(seg.seg_slot)
         region = max(self._region(plans[gi][0])[1] for gi in range(len(self.groups)))
         gathered = torch.empty(self.tp * max(region, 16), dtype=torch.uint8, device=self.device)
-        return {"seg": seg, "plans": plans, "ws": ws, "a_ptrs": a_ptrs, "b_ptrs": b_ptrs, "gathered": gathered}
+        # pipelined forward: every group has its own shrink/exchange/expand buffers, so group g's
+        # collective runs on the side stream while group g-1's assembly and expand compute
+        per_group = []
+        for gi in range(len(self.groups)):
+            pa, pb = plans[gi]
+            per_group.append({
+                "ws_a": torch.zeros(max(pa.workspace_bytes, 256), dtype=torch.uint8, device=self.device),
+                "ws_b": (torch.zeros(max(pb.workspace_bytes, 256), dtype=torch.uint8, device=self.device)
+                         if pb is not pa else None),
+                "gathered": torch.empty(self.tp * max(self._region(pa)[1], 16), dtype=torch.uint8, device=self.device),
+            })
+        st = {"seg": seg, "plans": plans, "ws": ws, "a_ptrs": a_ptrs, "b_ptrs": b_ptrs, "gathered": gathered,
+              "per_group": per_group, "comm": torch.cuda.Stream(self.device)}
+        self._prepare_fused(st)
+        return st
+
+    def _prepare_fused(self, st: dict) -> None:
+        """Fused column-group exchange: one CUDA-IPC-exportable buffer per rank holding the full-rank v
+        images of every (layer, column group) and a flag pair per (layer, group); every rank maps
+        every other rank's buffer, so a shrink can store its shard straight into all of them."""
+        if self.tp > 8 or not dist.is_available() or not dist.is_initialized():
+            st["fused"] = None
+            return
+        L, G = self.slab.model.layers, len(self.groups)
+        col_off, per_layer = {}, 0
+        for gi, (_, members) in enumerate(self.groups):
+            if self.specs[members[0]].column:
+                col_off[gi] = per_layer
+                _, nb = self._region(st["plans"][gi][1])
+                per_layer += (nb + 1023) // 1024 * 1024
+        flags_off = per_layer * L
+        nbytes = flags_off + L * G * 8 + 1024
+        lib = native.lib()
+        ptr = ctypes.c_void_p()
+        native.check(lib.lsv_slab_alloc(nbytes, self.device.index or 0, ctypes.byref(ptr)))
+        base = int(ptr.value)
+        torch.cuda.synchronize(self.device)
+        flags = torch.zeros(L * G * 2, dtype=torch.int32, device=self.device)    # zero the flag area
+        native.check(lib.lsv_copy_blocks(1, (ctypes.c_void_p * 1)(flags.data_ptr()),
+                                         (ctypes.c_void_p * 1)(base + flags_off),
+                                         (ctypes.c_size_t * 1)(flags.numel() * 4),
+                                         torch.cuda.current_stream(self.device).cuda_stream))
+        torch.cuda.synchronize(self.device)
+        handle = (ctypes.c_char * 64)()
+        native.check(lib.lsv_ipc_get_handle(base, ctypes.addressof(handle)))
+        handles = [None] * self.tp
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        bases = []
+        for d, h in enumerate(handles):
+            if d == self.rank:
+                bases.append(base)
+                continue
+            hb = (ctypes.c_char * 64).from_buffer_copy(h)
+            peer = ctypes.c_void_p()
+            native.check(lib.lsv_ipc_open_handle(ctypes.addressof(hb), self.device.index or 0, ctypes.byref(peer)))
+            bases.append(int(peer.value))
+        st["fused"] = {"base": base, "bases": bases, "col_off": col_off, "per_layer": per_layer,
+                       "flags_off": flags_off, "G": G}
+
+    def _fused_addrs(self, st: dict, layer: int, gi: int):
+        f = st["fused"]
+        off = layer * f["per_layer"] + f["col_off"][gi]
+        foff = f["flags_off"] + (layer * f["G"] + gi) * 8
+        vdst = (ctypes.c_void_p * self.tp)(*[b + off for b in f["bases"]])
+        flags = (ctypes.c_void_p * self.tp)(*[b + foff for b in f["bases"]])
+        return vdst, flags, f["base"] + off, f["base"] + foff
 
     @staticmethod
     def _region(sp) -> tuple[int, int]:
@@ -275,8 +340,106 @@ class TPLoraDeltaEngine:
             y.data_ptr(), y.stride(0), y.shape[0], sp.h_out, idx, st["b_ptrs"].data_ptr() + row * S * 8,
             plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(), strm.cuda_stream))
 
-    def forward(self, st: dict, xs, ys, stream=None) -> None:
+    def forward(self, st: dict, xs, ys, stream=None, fused: bool = True) -> None:
+        """Every layer and group.  fused (default when prepared with peers mapped): column groups
+        exchange inside the kernels — the shrink stores its shard of v into every rank's full-rank
+        image over NVLink and signals, the expand waits for every rank's signal (no NCCL, no
+        assembly); row groups all-reduce with NCCL.  fused=False: every group through NCCL,
+        software-pipelined (group g's collective on a side stream under group g-1's expand)."""
+        if fused and st.get("fused"):
+            return self._forward_fused(st, xs, ys, stream)
+        return self._forward_nccl(st, xs, ys, stream)
+
+    def _forward_fused(self, st: dict, xs, ys, stream=None) -> None:
+        lib = native.lib()
+        strm = stream or torch.cuda.current_stream(self.device)
+        S = st["seg"].num_segments
+        P, G = len(self.specs), len(self.groups)
         for layer in range(self.slab.model.layers):
             for gi, (gname, members) in enumerate(self.groups):
-                self.apply_group(st, layer, gi, xs[layer][gname], [ys[layer][self.specs[p].name] for p in members],
-                                 stream)
+                sp0 = self.specs[members[0]]
+                ys_m = [ys[layer][self.specs[p].name] for p in members]
+                if not sp0.column:
+                    self.apply_group(st, layer, gi, xs[layer][gname], ys_m, strm)
+                    continue
+                plan_a, plan_b = st["plans"][gi]
+                ws_a = st["per_group"][gi]["ws_a"]
+                x = xs[layer][gname]
+                vdst, flags, vimg, flag = self._fused_addrs(st, layer, gi)
+                native.check(lib.lsv_lora_shrink_tp_scatter(
+                    x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
+                    st["a_ptrs"].data_ptr() + (layer * G + gi) * S * 8, plan_a.plan_dev.data_ptr(),
+                    plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(), self.tp, self.rank,
+                    ctypes.addressof(vdst), plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data,
+                    ctypes.addressof(flags), strm.cuda_stream))
+                n = len(members)
+                y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys_m])
+                ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys_m])
+                b_arr = (ctypes.c_void_p * n)(*[st["b_ptrs"].data_ptr() + (layer * P + p) * S * 8 for p in members])
+                native.check(lib.lsv_lora_expand_group_tp(
+                    ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys_m[0].shape[0], ctypes.addressof(b_arr),
+                    plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, vimg, flag, self.tp, strm.cuda_stream))
+
+    def _forward_nccl(self, st: dict, xs, ys, stream=None) -> None:
+        """Every layer and group, software-pipelined: the shrink of group g and its NCCL collective
+        (side stream) overlap the assembly + expand of group g-1 on the compute stream."""
+        lib = native.lib()
+        comp = stream or torch.cuda.current_stream(self.device)
+        comm = st["comm"]
+        S = st["seg"].num_segments
+        P, G = len(self.specs), len(self.groups)
+        pending = None
+
+        def finish(item):
+            layer, gi, ev = item
+            members = self.groups[gi][1]
+            sp0 = self.specs[members[0]]
+            plan_a, plan_b = st["plans"][gi]
+            buf = st["per_group"][gi]
+            comp.wait_event(ev)
+            if sp0.column:
+                off, nb = self._region(plan_a)
+                native.check(lib.lsv_vimg_assemble(buf["gathered"].data_ptr(), nb, self.tp, plan_a.plan_dev.data_ptr(),
+                                                   plan_a.plan_host.ctypes.data, plan_b.plan_dev.data_ptr(),
+                                                   plan_b.plan_host.ctypes.data, buf["ws_b"].data_ptr(), comp.cuda_stream))
+                ws_e = buf["ws_b"]
+            else:
+                ws_e = buf["ws_a"]
+            ys_m = [ys[layer][self.specs[p].name] for p in members]
+            n = len(members)
+            y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys_m])
+            ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys_m])
+            b_arr = (ctypes.c_void_p * n)(*[st["b_ptrs"].data_ptr() + (layer * P + p) * S * 8 for p in members])
+            native.check(lib.lsv_lora_expand_group(
+                ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys_m[0].shape[0], ctypes.addressof(b_arr),
+                plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(),
+                comp.cuda_stream))
+
+        for layer in range(self.slab.model.layers):
+            for gi, (gname, members) in enumerate(self.groups):
+                sp0 = self.specs[members[0]]
+                plan_a = st["plans"][gi][0]
+                buf = st["per_group"][gi]
+                x = xs[layer][gname]
+                ws_a = buf["ws_a"]
+                native.check(lib.lsv_lora_shrink(x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
+                                                 st["a_ptrs"].data_ptr() + (layer * G + gi) * S * 8,
+                                                 plan_a.plan_dev.data_ptr(), plan_a.plan_host.ctypes.data,
+                                                 ws_a.data_ptr(), ws_a.numel(), comp.cuda_stream))
+                shrunk = torch.cuda.Event()
+                shrunk.record(comp)
+                off, nb = self._region(plan_a)
+                with torch.cuda.stream(comm):
+                    comm.wait_event(shrunk)
+                    if sp0.column:
+                        dist.all_gather_into_tensor(buf["gathered"][:self.tp * nb], ws_a[off:off + nb], group=self.group)
+                    else:
+                        dist.all_reduce(ws_a[off:off + nb].view(torch.bfloat16), group=self.group)
+                    exchanged = torch.cuda.Event()
+                    exchanged.record(comm)
+                if pending is not None:
+                    finish(pending)
+                pending = (layer, gi, exchanged)
+        if pending is not None:
+            finish(pending)
+        comp.wait_stream(comm)

@@ -133,9 +133,13 @@ def _worker_groups(rank, world, port, q):
                     yd[model.projections[p].name] = torch.zeros(N, slab.specs[p].h_out, dtype=torch.bfloat16, device=dev)
             xs.append(xd)
             ys.append(yd)
-        eng.forward(st, xs, ys)
+        eng.forward(st, xs, ys)                      # fused column-group exchange (NVLink stores)
+        ys2 = [{k: torch.zeros_like(v) for k, v in yd.items()} for yd in ys]
+        eng.forward(st, xs, ys2, fused=False)        # every group through NCCL
         torch.cuda.synchronize()
-        errs = []
+        assert st.get("fused") is not None
+        same = all(torch.equal(ys[l][k], ys2[l][k]) for l in range(model.layers) for k in ys[l])
+        errs = [("fused == nccl", same)]
         for l in range(model.layers):
             for p, pr in enumerate(model.projections):
                 parts = [torch.zeros_like(ys[l][pr.name]) for _ in range(world)]
@@ -156,8 +160,9 @@ def _worker_groups(rank, world, port, q):
 @pytest.mark.timeout(600)
 def test_tp2_forward_input_groups():
     """TP2 forward over every input group of a 2-layer mini Llama: fused q/k/v and gate/up shrinks of
-    rank-sharded A shards, one all-gather per column group + assembly, one all-reduce per row group,
-    one-launch group expands — every projection within the bf16 tolerance of the unsharded oracle."""
+    rank-sharded A shards whose epilogues store each shard into every rank's full-rank v image over
+    NVLink (no NCCL for column groups), one all-reduce per row group, one-launch group expands —
+    bit-identical to the all-NCCL path and within the bf16 tolerance of the unsharded oracle."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -176,6 +181,7 @@ def test_tp2_forward_input_groups():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res is not None and len(res) == 14
-    for layer, name, err in res:
+    assert res is not None and len(res) == 15
+    assert res[0] == ("fused == nccl", True)      # the in-kernel NVLink exchange gives NCCL's bits
+    for layer, name, err in res[1:]:
         assert err <= TOL, (layer, name, err)
