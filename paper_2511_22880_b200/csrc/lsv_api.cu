@@ -57,6 +57,16 @@ constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a
 #define LSV_SHRINK_WAVES 8
 #endif
 constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost)
+// LPT cost of an item = its bytes + a fixed per-item cost (pipeline fill, barrier round trips,
+// epilogue), in byte-equivalents
+#ifndef LSV_EXPAND_ITEM_FIXED_KB
+#define LSV_EXPAND_ITEM_FIXED_KB 8
+#endif
+#ifndef LSV_SHRINK_REC_FIXED_KB
+#define LSV_SHRINK_REC_FIXED_KB 24
+#endif
+constexpr int64_t kExpandItemFixed = (int64_t)LSV_EXPAND_ITEM_FIXED_KB * 1024;
+constexpr int64_t kShrinkRecFixed = (int64_t)LSV_SHRINK_REC_FIXED_KB * 1024;
 
 int num_sms_cached() {
   static int sms = -1;
@@ -243,7 +253,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         rc.nsplit = nsplit; rc.part_off = mt.part_off; rc.vimg_off = mt.vimg_off; rc.counter = mt.counter;
         rc.mtile = (int32_t)i; rc.p0 = p0; rc.np = np;
         // bytes moved + a fixed per-item cost (pipeline fill, epilogue, split reduction)
-        const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + 24 * 1024 +
+        const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + kShrinkRecFixed +
                              (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0);
         shrink_costed.push_back({cost, rc});
       }
@@ -279,7 +289,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     std::vector<ItemClass> cls;
     for (size_t i = 0; i < pb.mtiles.size(); ++i) {
       const MTile& mt = pb.mtiles[i];
-      cls.push_back({(int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + 8 * 1024, (int32_t)i, p});
+      cls.push_back({(int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + kExpandItemFixed, (int32_t)i, p});
     }
     all_cls.insert(all_cls.end(), cls.begin(), cls.end());
     std::stable_sort(cls.begin(), cls.end(), by_cost);
