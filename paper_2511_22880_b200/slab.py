@@ -60,6 +60,7 @@ class AdapterSlab:
         self._member = {p: (gi, i, len(m)) for gi, (_, m) in enumerate(model.groups()) for i, p in enumerate(m)}
         self._b_off_rows: list[np.ndarray] = []
         self._slot_offsets_dev: tuple[torch.Tensor, torch.Tensor] | None = None
+        self._free: dict[int, list[int]] = {}      # rank -> freed slots (reused by allocate)
 
     # -- allocation --------------------------------------------------------------------
     def slot_bytes(self, rank: int) -> int:
@@ -74,10 +75,18 @@ class AdapterSlab:
         return self.capacity - self._cursor
 
     def allocate(self, adapter_id: str, rank: int) -> int:
+        """A slot for the adapter: a freed slot of the same rank (same size, same offsets) if there is
+        one (pool.py:91-99: an evicted GPU slot is reused), else new space after the last slot."""
         if adapter_id in self.by_id:
             raise ValueError(f"adapter {adapter_id!r} already resident")
         if rank < 8 or rank % 8 or rank > 256:
             raise ValueError(f"adapter {adapter_id!r}: rank must be a multiple of 8 in [8, 256], got {rank}")
+        free = self._free.get(rank)
+        if free:
+            slot = free.pop()
+            self.slots[slot].adapter_id = adapter_id
+            self.by_id[adapter_id] = slot
+            return slot
         nbytes = self.slot_bytes(rank)
         start = (self._cursor + self.ALIGN - 1) // self.ALIGN * self.ALIGN
         if start + nbytes > self.capacity:
@@ -110,6 +119,27 @@ class AdapterSlab:
         self._cursor = start + nbytes
         self._slot_offsets_dev = None
         return slot
+
+    def free(self, adapter_id: str) -> int:
+        """Evict an adapter (the reference's LRU eviction of a GPU slot, pool.py:91-99): its slot
+        joins the free list of its rank.  Returns the slot."""
+        if adapter_id not in self.by_id:
+            raise KeyError(f"adapter {adapter_id!r} is not resident")
+        slot = self.by_id.pop(adapter_id)
+        info = self.slots[slot]
+        info.adapter_id = ""
+        self._free.setdefault(info.rank, []).append(slot)
+        return slot
+
+    def load_from_host(self, slot: int, weights, stream: torch.cuda.Stream | None = None) -> None:
+        """Make an adapter resident from host memory (the reference's load_from_host fetch,
+        pool.py:119-124): weights[(layer, proj)] = (lora_A [r, h_in], lora_B [h_out, r]) bf16 CPU
+        tensors (pinned for asynchronous copies); each pair is copied to the device and packed."""
+        st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            for (layer, proj), (a, b) in weights.items():
+                self.load(slot, layer, proj, a.to(self.device, non_blocking=True),
+                          b.to(self.device, non_blocking=True), st)
 
     def a_offset(self, slot: int, layer: int, proj: int) -> int:
         """Offset of proj's first A row inside its group tile (rows repeat every group*rank rows)."""
