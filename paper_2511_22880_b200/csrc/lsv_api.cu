@@ -469,10 +469,11 @@ int ensure_smem_attrs() {
 // Programmatic dependent launch: the kernel may start while the previous kernel in the stream
 // drains; it calls griddepcontrol.wait before touching anything that kernel wrote.
 template <typename Params>
-cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t st, const Params& p, bool pdl = true) {
+cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t st, const Params& p, bool pdl = true,
+                       int threads = kTcThreads) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -582,7 +583,7 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   p.dbg = g_debug_expand;
   p.trace = g_trace; p.trace_items = g_trace_items;
   LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, all ? h->expand_grid_all : h->expand_grid_p[p0], expand_smem_bytes(),
-                            st, p));
+                            st, p, true, kExpandThreads));
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }

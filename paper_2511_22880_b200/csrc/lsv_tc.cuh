@@ -177,8 +177,13 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 __host__ __device__ constexpr int shrink_smem_bytes() {
   return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
 }
+#ifndef LSV_EXPAND_EPI_WARPS
+#define LSV_EXPAND_EPI_WARPS 4
+#endif
+constexpr int kExpandEpiWarps = LSV_EXPAND_EPI_WARPS;   // 4: one per TMEM lane quadrant; 8: two, each half the columns
+constexpr int kExpandThreads = 64 + 32 * kExpandEpiWarps;
 __host__ __device__ constexpr int expand_smem_bytes() {
-  return 1024 + kExpandRingBytes + kExpandGuardBytes + 256 * 16 * 2 + 6 * (int)sizeof(ExpandRecBuf) + 1024;
+  return 1024 + kExpandRingBytes + kExpandGuardBytes + 256 * 16 * 2 + (2 + kExpandEpiWarps) * (int)sizeof(ExpandRecBuf) + 1024;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -444,12 +449,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
 // have read them.  The producer warp issues an item's copies from several lanes at once.
 constexpr int kIdentRows = 256;  // identity block at rows [128, 144) of a zero [256 x 16] A tile
 
-__global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
+__global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                    // 8 KB
   ExpandRecBuf* recbuf = reinterpret_cast<ExpandRecBuf*>(ident + kIdentRows * 16 * 2);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 6);                       // [kItemQ]
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 2 + kExpandEpiWarps);     // [kItemQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
   uint64_t* empty = full + kItemQ;
   uint64_t* tfull = empty + kItemQ;
@@ -469,7 +474,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
     fence_mbar_init();
     for (int pp = 0; pp < kMaxProj; ++pp)
       if (p.y[pp])
@@ -603,8 +608,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
       }
       __syncwarp();
     }
-  } else {  // ---------------------------- epilogue (warps 2..5): thread = token row
+  } else {  // ---------------------------- epilogue (warps 2..): thread = token row
     const int q = warp & 3, etid = threadIdx.x - 64;
+    const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ExpandRec inf;
     const uint8_t* unused;
@@ -619,8 +625,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) expand_tc_kernel(const __grid_c
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
         const bool valid = t < inf.ntok && !(p.dbg & 1);
         __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
+        const int c_lo = kExpandEpiWarps == 8 ? half * (tw / 2) : 0, c_hi = kExpandEpiWarps == 8 ? c_lo + tw / 2 : tw;
 #pragma unroll 1
-        for (int cc = 0; cc < tw; cc += 32) {
+        for (int cc = c_lo; cc < c_hi; cc += 32) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cc, r);
           uint32_t w[16];
