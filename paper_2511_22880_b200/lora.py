@@ -62,8 +62,44 @@ class BatchPlan:
         return out
 
 
+class _PinnedRing:
+    """Pinned host arenas for asynchronous uploads, reused round robin: an arena is refilled only
+    after the event recorded behind its last copies has completed (normally long ago), so the host
+    never allocates pinned memory or waits for the GPU in steady state."""
+
+    def __init__(self, slots: int = 4):
+        self.buf: list[torch.Tensor | None] = [None] * slots
+        self.ev: list[torch.cuda.Event | None] = [None] * slots
+        self.i = 0
+
+    def upload(self, arrays: list[np.ndarray], device: torch.device, stream) -> list[torch.Tensor]:
+        offs, total = [], 0
+        for a in arrays:
+            offs.append(total)
+            total += (a.nbytes + 255) // 256 * 256
+        k = self.i
+        self.i = (self.i + 1) % len(self.buf)
+        if self.ev[k] is not None:
+            self.ev[k].synchronize()
+        if self.buf[k] is None or self.buf[k].numel() < total:
+            self.buf[k] = torch.empty(max(total, 1 << 20) * 3 // 2, dtype=torch.uint8, pin_memory=True)
+        host = self.buf[k].numpy()
+        outs = []
+        with torch.cuda.stream(stream):
+            for a, o in zip(arrays, offs):
+                host[o:o + a.nbytes] = np.frombuffer(np.ascontiguousarray(a).tobytes(), dtype=np.uint8)
+                src = self.buf[k][o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype).view(a.shape)
+                dst = torch.empty(a.shape, dtype=src.dtype, device=device)
+                dst.copy_(src, non_blocking=True)
+                outs.append(dst)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self.ev[k] = ev
+        return outs
+
+
 def build_group_plan(seg: Segments, h_in: int, h_outs, tier_policy: int, device: torch.device,
-                     members: tuple[int, ...] = ()) -> ShapePlan:
+                     members: tuple[int, ...] = (), upload: bool = True) -> ShapePlan:
     lib = native.lib()
     S = seg.num_segments
     indptr = np.ascontiguousarray(seg.seg_indptr, dtype=np.int32)
@@ -78,7 +114,7 @@ def build_group_plan(seg: Segments, h_in: int, h_outs, tier_policy: int, device:
                                           tier_policy, blob.ctypes.data, pb.value))
     summ = np.zeros(8, dtype=np.int32)
     native.check(lib.lsv_plan_summary(blob.ctypes.data, summ.ctypes.data))
-    dev = torch.from_numpy(blob).to(device)
+    dev = torch.from_numpy(blob).to(device) if upload else None
     return ShapePlan(h_in, int(hs[0]), blob, dev, int(wb.value), tuple(int(v) for v in summ),
                      tuple(int(h) for h in hs), tuple(members))
 
@@ -103,17 +139,20 @@ class LoraDeltaEngine:
         self.groups = self.model.groups()
         self._member = {p: (gi, i) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self._workspace: torch.Tensor | None = None
+        self._ring = _PinnedRing()
 
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
-                peer_slabs: dict[int, AdapterSlab] | None = None) -> BatchPlan:
-        """Plan a batch: one liblsv plan per input group + pointer tables."""
+                peer_slabs: dict[int, AdapterSlab] | None = None, stream=None) -> BatchPlan:
+        """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
+        uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
+        k+1 on the host while batch k still runs there."""
         plans = []
         ws_need = 0
         projs = self.model.projections
         for _, members in self.groups:
             gp = build_group_plan(seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
-                                  self.tier_policy, self.device, members)
+                                  self.tier_policy, self.device, members, upload=stream is None)
             plans.append(gp)
         # forward: one workspace slice per (layer, group) (lsv_lora_forward_workspace)
         ph = (ctypes.c_void_p * len(plans))(*[gp.plan_host.ctypes.data for gp in plans])
@@ -121,8 +160,16 @@ class LoraDeltaEngine:
         if self._workspace is None or self._workspace.numel() < ws_need:
             # zero-filled once: the kernels leave their split counters at zero on exit
             self._workspace = torch.zeros(max(ws_need, 256), dtype=torch.uint8, device=self.device)
-        a_ptrs, b_ptrs = self.slab.pointer_tables(seg.seg_slot, peer_slabs=peer_slabs, seg_owner=seg_owner)
-        return BatchPlan(seg, plans, a_ptrs, b_ptrs, self._workspace, self.tier_policy)
+        a_tab, b_tab = self.slab.pointer_tables(seg.seg_slot, peer_slabs=peer_slabs, seg_owner=seg_owner,
+                                                as_numpy=True)
+        if stream is None:
+            a_dev, b_dev = torch.from_numpy(a_tab).to(self.device), torch.from_numpy(b_tab).to(self.device)
+        else:    # everything through one pinned arena, asynchronously on the stream
+            up = self._ring.upload([gp.plan_host for gp in plans] + [a_tab, b_tab], self.device, stream)
+            for gp, t in zip(plans, up):
+                gp.plan_dev = t
+            a_dev, b_dev = up[-2], up[-1]
+        return BatchPlan(seg, plans, a_dev, b_dev, self._workspace, self.tier_policy)
 
     # -- execution ---------------------------------------------------------------------
     def apply(self, bp: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor,

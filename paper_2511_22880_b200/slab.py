@@ -261,7 +261,7 @@ class AdapterSlab:
         return self._g_tab, self._b_tab
 
     def pointer_tables(self, seg_slots: np.ndarray, peer_slabs: dict[int, "AdapterSlab"] | None = None,
-                       seg_owner: np.ndarray | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+                       seg_owner: np.ndarray | None = None, as_numpy: bool = False):
         """Device int64 tables for the segments: group A tiles [layers*groups, S] (model.groups())
         and B tiles [layers*projections, S].
 
@@ -283,5 +283,7 @@ class AdapterSlab:
                     b[:, s] = pb_[slots[s]].reshape(-1) + peer.base
         a = np.ascontiguousarray(a)
         b = np.ascontiguousarray(b)
+        if as_numpy:
+            return a, b
         return (torch.from_numpy(a).to(self.device, non_blocking=False),
                 torch.from_numpy(b).to(self.device, non_blocking=False))
