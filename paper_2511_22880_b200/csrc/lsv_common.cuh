@@ -156,6 +156,19 @@ __device__ __forceinline__ void red_release_sys_add(int* p, int v) {
   asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Bounded cross-GPU wait: traps after ~4 s instead of hanging the GPU on a missing signal.
+__device__ __forceinline__ void wait_flag_geq(const int* flag, int target) {
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0; ld_acquire_sys(flag) < target; ++spin) {
+    __nanosleep(32);
+    if ((spin & 1023u) == 1023u) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+}
 
 // ---- async copies (TMA / bulk) -------------------------------------------------------------
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {

@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   pdl_wait();                 // v images come from the shrink launch; y from earlier work
   if (p.wait_flag != nullptr) {   // TP: the peers' shards of the v images have landed here too
     if (threadIdx.x == 0) {
-      while (ld_acquire_sys(p.wait_flag) < p.wait_target) __nanosleep(32);
+      wait_flag_geq(p.wait_flag, p.wait_target);
       fence_proxy_async_global();
       if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
         p.wait_flag[1] = 0;
