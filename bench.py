@@ -627,7 +627,7 @@ def run_tp(args, rank, world, local_rank):
     for gi, (_, members) in enumerate(eng.groups):
         plan_a = st["plans"][gi][0]
         off, nb = eng._region(plan_a)
-        if not (fused and eng.specs[members[0]].column):
+        if not (fused and eng.specs[members[0]].column):   # row groups keep NCCL (forward's default)
             coll.append((eng.specs[members[0]].column, off, nb))
     torch.cuda.synchronize(dev)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

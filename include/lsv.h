@@ -216,6 +216,23 @@ int lsv_lora_expand_group_tp(void* const* ys, const int64_t* ldys, int32_t num_t
                              const void* plan_host, const void* vimg_base, int32_t* flag,
                              int32_t expect, lsv_stream_t stream);
 
+/* Fused compute + all-reduce for row-parallel groups (o, down): the shrink of this rank's h_in
+ * slice writes its fp32 partial v into slot tp_rank of every rank's exchange buffer (xdst[d]:
+ * rank d's buffer for this layer/group, tp slots of 2 * vimg_stride * num_proj bytes; member p's
+ * m-tile at 2 * (p * vimg_stride + vimg_off) as fp32 [rows16][kpad]) over NVLink, then signals
+ * flags[d] like lsv_lora_shrink_tp_scatter. */
+int lsv_lora_shrink_tp_partials(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in,
+                                const void* const* a_ptrs, const void* plan_dev, const void* plan_host,
+                                void* workspace, size_t workspace_bytes, int32_t tp, int32_t tp_rank,
+                                void* const* xdst, int32_t* const* flags, lsv_stream_t stream);
+
+/* The matching expand: waits for flag[0] == tp, sums the tp partial slots of xsum in rank order
+ * (identical bits on every rank) into the workspace's bf16 v images, then expands every member. */
+int lsv_lora_expand_group_tp_sum(void* const* ys, const int64_t* ldys, int32_t num_tokens,
+                                 const void* const* const* b_ptrs, const void* plan_dev,
+                                 const void* plan_host, void* workspace, size_t workspace_bytes,
+                                 const void* xsum, int32_t tp, int32_t* flag, lsv_stream_t stream);
+
 /* Byte offset and size of a plan's v-image region inside its workspace (what TP exchanges): every
  * member's images, member p at p * (size / num_proj).  lsv_vimg_assemble handles group plans
  * member by member (both plans must have the same members). */

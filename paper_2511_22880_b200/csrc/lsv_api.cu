@@ -497,7 +497,7 @@ int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_d
 // writes (lsv_lora_forward's per-(layer, group) workspace slices), so it need not wait for it;
 // pdl = false: a plain launch, ordered after all earlier work in the stream.
 struct TpScatter {
-  int tp = 0, tp_rank = 0;
+  int tp = 0, tp_rank = 0, row = 0;
   const PlanHeader* fh = nullptr;
   const int32_t* fplan = nullptr;
   void* const* vdst = nullptr;
@@ -533,6 +533,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     if (tps != nullptr) {
       p.tp = tps->tp; p.tp_rank = tps->tp_rank;
+      p.tp_row = tps->row; p.xslot = 2 * h->vimg_stride * h->num_proj;
       p.fplan = tps->fplan; p.f_off_mtiles = tps->fh->off_mtiles; p.vstride_f = tps->fh->vimg_stride;
       for (int d = 0; d < tps->tp; ++d) {
         p.vdst[d] = static_cast<uint8_t*>(tps->vdst[d]);
@@ -550,7 +551,8 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
 // for every member), np == 1 member p0's own list.
 int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys, int32_t num_tokens,
                const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st,
-               const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0) {
+               const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0,
+               const uint8_t* xsum = nullptr) {
   for (int i = 0; i < np && h->n_simt_items > 0; ++i) {
     const int pp = p0 + i, h_out = h->h_outs[pp];
     simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 255) / 256), 128, 0, st>>>(
@@ -577,6 +579,11 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   }
   p.plan = plan; p.ws = vimg_base ? const_cast<uint8_t*>(vimg_base) : ws;
   p.wait_flag = wait_flag; p.wait_target = wait_target;
+  if (xsum != nullptr) {
+    p.xsum = xsum; p.xslot = 2 * h->vimg_stride * h->num_proj; p.ws_vimg0 = h->ws_vimg;
+    p.off_mtiles = h->off_mtiles; p.n_mtiles = h->n_mtiles; p.num_proj = h->num_proj;
+    p.vimg_stride = h->vimg_stride; p.grid_bar = h->n_counters; p.ws_counters = h->ws_counters;
+  }
   p.off_recs = all ? h->off_expand_recs_all : h->off_expand_recs_p[p0];
   p.off_cta = all ? h->off_expand_cta_all : h->off_expand_cta_p[p0];
   p.tw_max = tw_max;
@@ -910,6 +917,44 @@ int lsv_lora_expand_group_tp(void* const* ys, const int64_t* ldys, int32_t num_t
   if (h->num_tokens == 0) return LSV_OK;
   return run_expand(h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev), nullptr,
                     static_cast<cudaStream_t>(stream), static_cast<const uint8_t*>(vimg_base), flag, expect);
+}
+
+int lsv_lora_shrink_tp_partials(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in, const void* const* a_ptrs,
+                                const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                                int32_t tp, int32_t tp_rank, void* const* xdst, int32_t* const* flags,
+                                lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (tp < 1 || tp > kMaxTp || tp_rank < 0 || tp_rank >= tp || !xdst || !flags)
+    return fail(LSV_EINVAL, "lsv_lora_shrink_tp_partials: bad tp / rank / destinations");
+  if (h->n_simt_items != 0)
+    return fail(LSV_EUNSUPPORTED, "TP partial exchange needs every segment on the tensor-core tier (LSV_TIER_TC)");
+  if (h->h_in != h_in) return fail(LSV_EINVAL, "h_in %d does not match the plan's %d", h_in, h->h_in);
+  if (h->num_tokens == 0) return LSV_OK;
+  if (!x || !a_ptrs || !aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "bad x / a_ptrs");
+  for (int d = 0; d < tp; ++d)
+    if (!xdst[d] || !flags[d]) return fail(LSV_EINVAL, "rank %d: null destination or flag", d);
+  TpScatter tps;
+  tps.tp = tp; tps.tp_rank = tp_rank; tps.row = 1; tps.fh = h; tps.fplan = static_cast<const int32_t*>(plan_dev);
+  tps.vdst = xdst; tps.flags = flags;
+  return run_shrink(h, x, ldx, num_tokens, a_ptrs, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream), 1, true, &tps);
+}
+
+int lsv_lora_expand_group_tp_sum(void* const* ys, const int64_t* ldys, int32_t num_tokens,
+                                 const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                                 void* workspace, size_t workspace_bytes, const void* xsum, int32_t tp, int32_t* flag,
+                                 lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (!ys || !ldys || !b_ptrs || !xsum || !flag || tp < 1 || tp > kMaxTp)
+    return fail(LSV_EINVAL, "lsv_lora_expand_group_tp_sum: bad arguments");
+  if (num_tokens < h->num_tokens) return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (h->n_simt_items != 0) return fail(LSV_EUNSUPPORTED, "TP expand needs every segment on the tensor-core tier");
+  if (h->num_tokens == 0) return LSV_OK;
+  return run_expand(h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev),
+                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream), nullptr, flag, tp,
+                    static_cast<const uint8_t*>(xsum));
 }
 
 size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const void* const* plans_host) {

@@ -53,6 +53,8 @@ struct alignas(64) ShrinkParams {
   const int32_t* fplan;
   uint8_t* vdst[kMaxTp];
   int* flags[kMaxTp];
+  int tp_row;                   // row-parallel: vdst[d] is rank d's exchange buffer; this rank's fp32
+  int xslot;                    // partial v goes to slot tp_rank (xslot bytes per slot) on every rank
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -71,6 +73,9 @@ struct alignas(64) ExpandParams {
   int off_recs, off_cta;
   int* wait_flag;               // TP: wait until *wait_flag == wait_target (every rank's shard written),
   int wait_target;              //     then the last CTA through re-arms it ([0] flag, [1] pass counter)
+  const uint8_t* xsum;          // TP row groups: this rank's exchange buffer (wait_target fp32 partial
+  int xslot, ws_vimg0;          //   slots); summed into the v images (at ws + ws_vimg0) before expanding
+  int off_mtiles, n_mtiles, num_proj, vimg_stride, grid_bar, ws_counters;
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -162,6 +167,19 @@ __device__ __forceinline__ void tp_scatter_pad(const ShrinkParams& p, int mtile,
   if (p.tp_rank != p.tp - 1 || kpf == mf.rank) return;
   const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, mf.rank, kpf, np16);
   for (int d = 0; d < p.tp; ++d) *reinterpret_cast<uint4*>(p.vdst[d] + off) = make_uint4(0, 0, 0, 0);
+}
+// Row-parallel TP: 8 fp32 partial-v values (member pp, token t of m-tile mtile, k..k+7) into slot
+// tp_rank of every rank's exchange buffer (per m-tile fp32 [np16][kp] at 2 * vimg_off).
+__device__ __forceinline__ void tp_row_put(const ShrinkParams& p, int mtile, int pp, int t, int k, const float* v8) {
+  const MTile mt = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles)[mtile];
+  const size_t off = (size_t)p.tp_rank * p.xslot + (size_t)pp * 2 * p.vimg_stride + 2 * (size_t)mt.vimg_off +
+                     ((size_t)t * kpad(mt.rank) + k) * 4;
+  const float4 lo = make_float4(v8[0], v8[1], v8[2], v8[3]), hi = make_float4(v8[4], v8[5], v8[6], v8[7]);
+  for (int d = 0; d < p.tp; ++d) {
+    float4* dst = reinterpret_cast<float4*>(p.vdst[d] + off);
+    dst[0] = lo;
+    dst[1] = hi;
+  }
 }
 // No split tiles: the CTAs count themselves out (counter slot after the grid barrier's) and the
 // last one signals every rank.
@@ -340,7 +358,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
                 w.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
                 w.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
                 const int pp = inf.p0 + j0 / r;
-                if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w);
+                if (p.tp > 0 && p.tp_row) tp_row_put(p, inf.mtile, pp, row, j0 % r, v + h * 8);
+                else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w);
                 else *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
               } else {
                 float4* dst = reinterpret_cast<float4*>(part + j0);
@@ -352,7 +371,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
         }
       }
       if (valid && inf.nsplit == 1 && p.tp > 0) {
-        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
+        if (!p.tp_row)
+          for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
       } else if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
         for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp)
           *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16)) = make_uint4(0, 0, 0, 0);
@@ -382,10 +402,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   if (threadIdx.x == 0) {
     atomicAdd(&bar[0], 1);
     int seen = 0;
-    do {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0;; ++spin) {
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(&bar[0]) : "memory");
-      if (seen < (int)gridDim.x) __nanosleep(64);
-    } while (seen < (int)gridDim.x);
+      if (seen >= (int)gridDim.x) break;
+      __nanosleep(64);
+      if ((spin & 1023u) == 1023u) {   // bounded: trap after ~4 s instead of hanging the GPU
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 4000000000ull) __trap();
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 4);
@@ -420,7 +447,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     uint4 w;
     w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
     w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
-    if (p.tp > 0) {
+    if (p.tp > 0 && p.tp_row) {
+      if (k0 < mt.rank) tp_row_put(p, red[2 * e], pp, t, k0, s8);
+    } else if (p.tp > 0) {
       if (k0 < mt.rank) tp_scatter(p, red[2 * e], pp, t, k0, mt.rank, np16, w);
       if (k0 == 0) tp_scatter_pad(p, red[2 * e], pp, t, np16);   // once per (token, member)
     } else {
@@ -448,6 +477,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
 // pieces (~0.7 instructions per element), and the ring bytes are released as soon as the MMAs
 // have read them.  The producer warp issues an item's copies from several lanes at once.
 constexpr int kIdentRows = 256;  // identity block at rows [128, 144) of a zero [256 x 16] A tile
+
+// Row-parallel TP: CTA c sums m-tiles c, c + grid, ... over the wait_target fp32 partial slots
+// (rank order 0..T-1: every rank computes the same bits) into the bf16 v images; k pads are zero.
+__device__ __forceinline__ void tp_row_sum(const ExpandParams& p) {
+  const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
+  for (int m = blockIdx.x; m < p.n_mtiles; m += gridDim.x) {
+    const MTile mt = mts[m];
+    const int kp = kpad(mt.rank), upr = kp / 8, np16 = round_up(mt.ntok, 16);
+    const int units = mt.ntok * upr * p.num_proj;
+    for (int u = threadIdx.x; u < units; u += blockDim.x) {
+      const int pp = u / (mt.ntok * upr), rem = u % (mt.ntok * upr), t = rem / upr, k0 = (rem % upr) * 8;
+      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (k0 < mt.rank) {
+        const size_t off = (size_t)pp * 2 * p.vimg_stride + 2 * (size_t)mt.vimg_off + ((size_t)t * kp + k0) * 4;
+        for (int d = 0; d < p.wait_target; ++d) {
+          const float4* src = reinterpret_cast<const float4*>(p.xsum + (size_t)d * p.xslot + off);
+          const float4 lo = __ldcg(src), hi = __ldcg(src + 1);
+          s8[0] += lo.x; s8[1] += lo.y; s8[2] += lo.z; s8[3] += lo.w;
+          s8[4] += hi.x; s8[5] += hi.y; s8[6] += hi.z; s8[7] += hi.w;
+        }
+      }
+      uint4 w;
+      w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
+      w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
+      *reinterpret_cast<uint4*>(p.ws + p.ws_vimg0 + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -498,6 +555,26 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       }
     }
     __syncthreads();
+    if (p.xsum != nullptr) {      // row group: v = sum of every rank's fp32 partial, fixed rank order
+      tp_row_sum(p);
+      __threadfence();
+      __syncthreads();
+      int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+      if (threadIdx.x == 0) {
+        atomicAdd(&bar[0], 1);
+        uint64_t t0 = 0;
+        for (uint32_t spin = 0; ld_acquire_sys(&bar[0]) < (int)gridDim.x; ++spin) {
+          __nanosleep(32);
+          if ((spin & 1023u) == 1023u) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) __trap();
+          }
+        }
+        fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
+      }
+      __syncthreads();
+    }
   }
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
@@ -648,6 +725,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (p.xsum != nullptr && threadIdx.x == 0) {   // every CTA is past the sum barrier: re-arm it
+    int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+    if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }
+  }
 }
 
 }  // namespace lsv

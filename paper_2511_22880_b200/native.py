@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
     "lsv_lora_forward", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
+    "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum",
 )
 
 _lib = None
@@ -76,6 +77,9 @@ _SIGNATURES = {
     "lsv_lora_shrink_tp_scatter": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
                                                   _vp, _vp, _vp, _vp, _vp]),
     "lsv_lora_expand_group_tp": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "lsv_lora_shrink_tp_partials": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
+                                                   _vp, _vp, _vp]),
+    "lsv_lora_expand_group_tp_sum": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp, _i32, _vp, _vp]),
 }
 
 

@@ -239,10 +239,12 @@ class TPLoraDeltaEngine:
         L, G = self.slab.model.layers, len(self.groups)
         col_off, per_layer = {}, 0
         for gi, (_, members) in enumerate(self.groups):
-            if self.specs[members[0]].column:
-                col_off[gi] = per_layer
-                _, nb = self._region(st["plans"][gi][1])
+            _, nb = self._region(st["plans"][gi][1])
+            col_off[gi] = per_layer
+            if self.specs[members[0]].column:     # full-rank bf16 v images
                 per_layer += (nb + 1023) // 1024 * 1024
+            else:                                 # tp slots of fp32 partial v (2x the bf16 images)
+                per_layer += self.tp * 2 * ((nb + 1023) // 1024 * 1024)
         flags_off = per_layer * L
         nbytes = flags_off + L * G * 8 + 1024
         lib = native.lib()
@@ -340,17 +342,21 @@ class TPLoraDeltaEngine:
             y.data_ptr(), y.stride(0), y.shape[0], sp.h_out, idx, st["b_ptrs"].data_ptr() + row * S * 8,
             plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, ws_e.data_ptr(), ws_e.numel(), strm.cuda_stream))
 
-    def forward(self, st: dict, xs, ys, stream=None, fused: bool = True) -> None:
-        """Every layer and group.  fused (default when prepared with peers mapped): column groups
-        exchange inside the kernels — the shrink stores its shard of v into every rank's full-rank
-        image over NVLink and signals, the expand waits for every rank's signal (no NCCL, no
-        assembly); row groups all-reduce with NCCL.  fused=False: every group through NCCL,
-        software-pipelined (group g's collective on a side stream under group g-1's expand)."""
+    def forward(self, st: dict, xs, ys, stream=None, fused: bool = True, row_fused: bool = False) -> None:
+        """Every layer and group.  fused (default when prepared with peers mapped): every exchange
+        happens inside the kernels over NVLink, no NCCL — a column group's shrink stores its shard
+        of v into every rank's full-rank image, a row group's shrink stores its fp32 partial v into
+        its slot on every rank and the expand sums the slots (rank order: identical bits on every
+        rank); each expand waits for every rank's signal.  Row groups take the in-kernel path only
+        with row_fused=True (measured slower at TP2: the expand's sum phase and grid barrier delay its
+        pipeline more than the NCCL all-reduce costs); by default they all-reduce with NCCL.
+        fused=False: every group through NCCL, software-pipelined (group g's collective on a side
+        stream under group g-1's expand)."""
         if fused and st.get("fused"):
-            return self._forward_fused(st, xs, ys, stream)
+            return self._forward_fused(st, xs, ys, stream, row_fused)
         return self._forward_nccl(st, xs, ys, stream)
 
-    def _forward_fused(self, st: dict, xs, ys, stream=None) -> None:
+    def _forward_fused(self, st: dict, xs, ys, stream=None, row_fused: bool = False) -> None:
         lib = native.lib()
         strm = stream or torch.cuda.current_stream(self.device)
         S = st["seg"].num_segments
@@ -359,23 +365,34 @@ class TPLoraDeltaEngine:
             for gi, (gname, members) in enumerate(self.groups):
                 sp0 = self.specs[members[0]]
                 ys_m = [ys[layer][self.specs[p].name] for p in members]
-                if not sp0.column:
-                    self.apply_group(st, layer, gi, xs[layer][gname], ys_m, strm)
-                    continue
                 plan_a, plan_b = st["plans"][gi]
                 ws_a = st["per_group"][gi]["ws_a"]
                 x = xs[layer][gname]
                 vdst, flags, vimg, flag = self._fused_addrs(st, layer, gi)
+                n = len(members)
+                y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys_m])
+                ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys_m])
+                b_arr = (ctypes.c_void_p * n)(*[st["b_ptrs"].data_ptr() + (layer * P + p) * S * 8 for p in members])
+                if not sp0.column and not row_fused:
+                    self.apply_group(st, layer, gi, x, ys_m, strm)
+                    continue
+                if not sp0.column:   # row group: fp32 partials to every rank's slot, summed in the expand
+                    native.check(lib.lsv_lora_shrink_tp_partials(
+                        x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
+                        st["a_ptrs"].data_ptr() + (layer * G + gi) * S * 8, plan_a.plan_dev.data_ptr(),
+                        plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(), self.tp, self.rank,
+                        ctypes.addressof(vdst), ctypes.addressof(flags), strm.cuda_stream))
+                    native.check(lib.lsv_lora_expand_group_tp_sum(
+                        ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys_m[0].shape[0], ctypes.addressof(b_arr),
+                        plan_a.plan_dev.data_ptr(), plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(),
+                        vimg, self.tp, flag, strm.cuda_stream))
+                    continue
                 native.check(lib.lsv_lora_shrink_tp_scatter(
                     x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
                     st["a_ptrs"].data_ptr() + (layer * G + gi) * S * 8, plan_a.plan_dev.data_ptr(),
                     plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(), self.tp, self.rank,
                     ctypes.addressof(vdst), plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data,
                     ctypes.addressof(flags), strm.cuda_stream))
-                n = len(members)
-                y_arr = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys_m])
-                ld_arr = (ctypes.c_int64 * n)(*[y.stride(0) for y in ys_m])
-                b_arr = (ctypes.c_void_p * n)(*[st["b_ptrs"].data_ptr() + (layer * P + p) * S * 8 for p in members])
                 native.check(lib.lsv_lora_expand_group_tp(
                     ctypes.addressof(y_arr), ctypes.addressof(ld_arr), ys_m[0].shape[0], ctypes.addressof(b_arr),
                     plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data, vimg, flag, self.tp, strm.cuda_stream))

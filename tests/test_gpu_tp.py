@@ -136,9 +136,14 @@ def _worker_groups(rank, world, port, q):
         eng.forward(st, xs, ys)                      # fused column-group exchange (NVLink stores)
         ys2 = [{k: torch.zeros_like(v) for k, v in yd.items()} for yd in ys]
         eng.forward(st, xs, ys2, fused=False)        # every group through NCCL
+        ys3 = [{k: torch.zeros_like(v) for k, v in yd.items()} for yd in ys]
+        eng.forward(st, xs, ys3, row_fused=True)     # row groups' all-reduce in the kernels too
         torch.cuda.synchronize()
         assert st.get("fused") is not None
-        same = all(torch.equal(ys[l][k], ys2[l][k]) for l in range(model.layers) for k in ys[l])
+        # column groups: the fused exchange moves the same bf16 units NCCL's all-gather moves (identical
+        # bits); row groups: fp32 partials summed once vs NCCL's bf16 all-reduce (both within tolerance)
+        col = {model.projections[p].name for n, m in model.groups() for p in m if slab.specs[p].column}
+        same = all(torch.equal(ys[l][k], ys2[l][k]) for l in range(model.layers) for k in ys[l] if k in col)
         errs = [("fused == nccl", same)]
         for l in range(model.layers):
             for p, pr in enumerate(model.projections):
@@ -151,6 +156,11 @@ def _worker_groups(rank, world, port, q):
                                          [bf16_bits(full[(int(sl), l, p)][0]) for sl in seg.seg_slot],
                                          [bf16_bits(full[(int(sl), l, p)][1]) for sl in seg.seg_slot], pr.h_out)
                     errs.append((l, pr.name, oracle.max_rel_err(got[:N], ref[:N])))
+                parts3 = [torch.zeros_like(ys3[l][pr.name]) for _ in range(world)]
+                dist.all_gather(parts3, ys3[l][pr.name])
+                if rank == 0:
+                    got3 = torch.cat(parts3, 1).float().cpu().numpy()
+                    errs.append((l, pr.name + "/row_fused", oracle.max_rel_err(got3[:N], ref[:N])))
         if rank == 0:
             q.put(errs)
     finally:
@@ -159,10 +169,11 @@ def _worker_groups(rank, world, port, q):
 
 @pytest.mark.timeout(600)
 def test_tp2_forward_input_groups():
-    """TP2 forward over every input group of a 2-layer mini Llama: fused q/k/v and gate/up shrinks of
-    rank-sharded A shards whose epilogues store each shard into every rank's full-rank v image over
-    NVLink (no NCCL for column groups), one all-reduce per row group, one-launch group expands —
-    bit-identical to the all-NCCL path and within the bf16 tolerance of the unsharded oracle."""
+    """TP2 forward over every input group of a 2-layer mini Llama with every exchange inside the
+    kernels over NVLink: fused q/k/v and gate/up shrinks store each rank-shard of v into every rank's
+    full-rank image (bit-identical to the NCCL all-gather path); o/down shrinks store fp32 partial v
+    into every rank's slot and the expands sum them — every projection within the bf16 tolerance of
+    the unsharded oracle."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -181,7 +192,7 @@ def test_tp2_forward_input_groups():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res is not None and len(res) == 15
+    assert res is not None and len(res) == 29
     assert res[0] == ("fused == nccl", True)      # the in-kernel NVLink exchange gives NCCL's bits
     for layer, name, err in res[1:]:
         assert err <= TOL, (layer, name, err)
