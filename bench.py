@@ -19,6 +19,7 @@ step in data-parallel serving — SURVEY §8e).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -331,33 +332,58 @@ def run_ours(args, rank, world, local_rank):
     x_host.copy_(xs[0][input_group(model.projections[0].name)].cpu())
     last = model.projections[-1]
     y_host = torch.empty((N, last.h_out), dtype=torch.bfloat16, pin_memory=True)
-    x_dev0 = xs[0][input_group(model.projections[0].name)]
+    g0 = input_group(model.projections[0].name)
     h2d_bytes = x_host.numel() * 2
     d2h_bytes = y_host.numel() * 2
+    # double-buffered layer-0 input and last-layer output, so the H2D of step k+1 and the D2H of
+    # step k run on the copy engines (own streams) while step k's kernels run
+    xs_buf = [xs, [dict(d) for d in xs]]
+    ys_buf = [ys, [dict(d) for d in ys]]
+    xs_buf[1][0][g0] = torch.empty_like(xs[0][g0])
+    ys_buf[1][-1][last.name] = torch.zeros_like(ys[-1][last.name])
+    h2d_st, d2h_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_h2d = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_fwd = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_d2h = [torch.cuda.Event(), torch.cuda.Event()]
+    for e in ev_fwd + ev_d2h:
+        e.record(stream)
+    step_no = [0]
 
     def e2e_step():
         """One step through the public API: index the host batch, plan it (uploads asynchronous on
         the compute stream), H2D of x, the whole-model delta, D2H of y.  Nothing waits for the GPU,
-        so the host work of step k+1 overlaps the GPU work of step k (a serving loop)."""
+        so the host work of step k+1 overlaps the GPU work of step k (a serving loop), and the
+        copies of neighbouring steps overlap step k's kernels."""
+        b = step_no[0] & 1
+        step_no[0] += 1
         seg_i = _ix(tok_slots_host, wl.ranks)                      # host segment indexing
         bp_i = eng.prepare(seg_i, stream=stream)                   # host planning + async plan/pointer upload
-        with torch.cuda.stream(stream):
-            x_dev0.copy_(x_host, non_blocking=True)                # H2D of the batch's input
-            eng.forward(bp_i, xs, ys, stream)
-            y_host.copy_(ys[-1][last.name], non_blocking=True)     # D2H of the result
+        h2d_st.wait_event(ev_fwd[b])                               # step k-2 done reading this x buffer
+        with torch.cuda.stream(h2d_st):
+            xs_buf[b][0][g0].copy_(x_host, non_blocking=True)      # H2D of the batch's input
+            ev_h2d[b].record(h2d_st)
+        stream.wait_event(ev_h2d[b])
+        stream.wait_event(ev_d2h[b])                               # step k-2's result read out
+        eng.forward(bp_i, xs_buf[b], ys_buf[b], stream)
+        ev_fwd[b].record(stream)
+        d2h_st.wait_event(ev_fwd[b])
+        with torch.cuda.stream(d2h_st):
+            y_host.copy_(ys_buf[b][-1][last.name], non_blocking=True)   # D2H of the result
+            ev_d2h[b].record(d2h_st)
         return bp_i
 
     keep = []
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 8)):      # cycles every slot of the engine's upload ring
         keep.append(e2e_step())
-    stream.synchronize()
+    torch.cuda.synchronize(dev)
+    gc.collect()
     if world > 1:
         torch.distributed.barrier()
     keep.clear()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         keep.append(e2e_step())                                    # plans stay alive until the sync
-    stream.synchronize()
+    torch.cuda.synchronize(dev)
     e2e_s = (time.perf_counter() - t0) / args.steps
     bp_last = keep[-1]
     plan_bytes = sum(sp.plan_host.nbytes for sp in bp_last.group_plans) + \

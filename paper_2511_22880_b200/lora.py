@@ -12,6 +12,7 @@ segment paying its own rank.
 
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes
 from dataclasses import dataclass, field
 
@@ -62,40 +63,61 @@ class BatchPlan:
         return out
 
 
-class _PinnedRing:
-    """Pinned host arenas for asynchronous uploads, reused round robin: an arena is refilled only
-    after the event recorded behind its last copies has completed (normally long ago), so the host
-    never allocates pinned memory or waits for the GPU in steady state."""
+class _UploadRing:
+    """Pinned host arena + device arena pairs for asynchronous plan uploads, reused round robin.
+
+    A slot's host arena is refilled only after the event behind its last H2D copy has completed
+    (normally long ago); its device arena is overwritten by a copy issued on the caller's stream,
+    so it is stream-ordered behind every kernel that read the previous plan in that slot.  Steady
+    state therefore allocates nothing (a cudaMalloc / cudaHostAlloc can serialise the device and
+    drain a serving loop's pipeline) and waits for nothing.  Each reuse bumps the slot's
+    generation; a plan whose slot has been reused is rejected (``check``)."""
 
     def __init__(self, slots: int = 4):
-        self.buf: list[torch.Tensor | None] = [None] * slots
+        self.host: list[torch.Tensor | None] = [None] * slots
+        self.dev: list[torch.Tensor | None] = [None] * slots
         self.ev: list[torch.cuda.Event | None] = [None] * slots
+        self.gen = [0] * slots
+        self.last_stream: list = [None] * slots
         self.i = 0
 
-    def upload(self, arrays: list[np.ndarray], device: torch.device, stream) -> list[torch.Tensor]:
+    def upload(self, arrays: list[np.ndarray], device: torch.device, stream) -> tuple[list[torch.Tensor], tuple]:
         offs, total = [], 0
         for a in arrays:
             offs.append(total)
             total += (a.nbytes + 255) // 256 * 256
         k = self.i
-        self.i = (self.i + 1) % len(self.buf)
+        self.i = (self.i + 1) % len(self.host)
         if self.ev[k] is not None:
             self.ev[k].synchronize()
-        if self.buf[k] is None or self.buf[k].numel() < total:
-            self.buf[k] = torch.empty(max(total, 1 << 20) * 3 // 2, dtype=torch.uint8, pin_memory=True)
-        host = self.buf[k].numpy()
-        outs = []
+        if self.host[k] is None or self.host[k].numel() < total:
+            cap = max(total, 1 << 20) * 3 // 2
+            # size every never-used slot too, so growth happens once and not inside a later window
+            for j in range(len(self.host)):
+                if j == k or (self.ev[j] is None and (self.host[j] is None or self.host[j].numel() < cap)):
+                    if self.dev[j] is not None and self.last_stream[j] is not None:
+                        self.dev[j].record_stream(self.last_stream[j])   # in-flight readers keep it alive
+                    self.host[j] = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+                    self.dev[j] = torch.empty(cap, dtype=torch.uint8, device=device)
+        self.gen[k] += 1
+        self.last_stream[k] = stream
+        host = self.host[k].numpy()
+        for a, o in zip(arrays, offs):
+            host[o:o + a.nbytes] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
         with torch.cuda.stream(stream):
-            for a, o in zip(arrays, offs):
-                host[o:o + a.nbytes] = np.frombuffer(np.ascontiguousarray(a).tobytes(), dtype=np.uint8)
-                src = self.buf[k][o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype).view(a.shape)
-                dst = torch.empty(a.shape, dtype=src.dtype, device=device)
-                dst.copy_(src, non_blocking=True)
-                outs.append(dst)
+            self.dev[k][:total].copy_(self.host[k][:total], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(stream)
         self.ev[k] = ev
-        return outs
+        outs = [self.dev[k][o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype).view(a.shape)
+                for a, o in zip(arrays, offs)]
+        return outs, (k, self.gen[k])
+
+    def check(self, tag: tuple) -> None:
+        k, g = tag
+        if self.gen[k] != g:
+            raise RuntimeError(f"batch plan is stale: its upload slot was reused by a later prepare(stream=...) "
+                               f"(at most {len(self.host)} stream-prepared plans are live at once)")
 
 
 def build_group_plan(seg: Segments, h_in: int, h_outs, tier_policy: int, device: torch.device,
@@ -139,7 +161,8 @@ class LoraDeltaEngine:
         self.groups = self.model.groups()
         self._member = {p: (gi, i) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self._workspace: torch.Tensor | None = None
-        self._ring = _PinnedRing()
+        self._ring = _UploadRing()
+        self._pool = concurrent.futures.ThreadPoolExecutor(max_workers=max(1, len(self.groups)))
 
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
@@ -147,13 +170,14 @@ class LoraDeltaEngine:
         """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
         uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
         k+1 on the host while batch k still runs there."""
-        plans = []
         ws_need = 0
         projs = self.model.projections
-        for _, members in self.groups:
-            gp = build_group_plan(seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
-                                  self.tier_policy, self.device, members, upload=stream is None)
-            plans.append(gp)
+        # the group plans are independent host work; ctypes drops the GIL inside the C++ planner,
+        # so they build in parallel
+        futs = [self._pool.submit(build_group_plan, seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
+                                  self.tier_policy, self.device, members, stream is None)
+                for _, members in self.groups]
+        plans = [f.result() for f in futs]
         # forward: one workspace slice per (layer, group) (lsv_lora_forward_workspace)
         ph = (ctypes.c_void_p * len(plans))(*[gp.plan_host.ctypes.data for gp in plans])
         ws_need = native.lib().lsv_lora_forward_workspace(self.model.layers, len(plans), ctypes.addressof(ph))
@@ -165,11 +189,19 @@ class LoraDeltaEngine:
         if stream is None:
             a_dev, b_dev = torch.from_numpy(a_tab).to(self.device), torch.from_numpy(b_tab).to(self.device)
         else:    # everything through one pinned arena, asynchronously on the stream
-            up = self._ring.upload([gp.plan_host for gp in plans] + [a_tab, b_tab], self.device, stream)
+            up, tag = self._ring.upload([gp.plan_host for gp in plans] + [a_tab, b_tab], self.device, stream)
             for gp, t in zip(plans, up):
                 gp.plan_dev = t
             a_dev, b_dev = up[-2], up[-1]
-        return BatchPlan(seg, plans, a_dev, b_dev, self._workspace, self.tier_policy)
+        bp = BatchPlan(seg, plans, a_dev, b_dev, self._workspace, self.tier_policy)
+        if stream is not None:
+            bp.extra["ring_tag"] = tag
+        return bp
+
+    def _live(self, bp: BatchPlan) -> None:
+        tag = bp.extra.get("ring_tag")
+        if tag is not None:
+            self._ring.check(tag)
 
     # -- execution ---------------------------------------------------------------------
     def apply(self, bp: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor,
@@ -183,6 +215,7 @@ class LoraDeltaEngine:
 
     def shrink(self, bp: BatchPlan, layer: int, proj: int, x: torch.Tensor, stream=None) -> None:
         """Fused shrink of proj's input group (v images of every member)."""
+        self._live(bp)
         gi, _ = self._member[proj]
         gp = bp.group_plans[gi]
         S = bp.segments.num_segments
@@ -194,6 +227,7 @@ class LoraDeltaEngine:
             bp.workspace.numel(), st.cuda_stream))
 
     def expand(self, bp: BatchPlan, layer: int, proj: int, y: torch.Tensor, stream=None) -> None:
+        self._live(bp)
         pr = self.model.projections[proj]
         gi, idx = self._member[proj]
         gp = bp.group_plans[gi]
@@ -207,6 +241,7 @@ class LoraDeltaEngine:
 
     def expand_group(self, bp: BatchPlan, layer: int, gi: int, ys: list[torch.Tensor], stream=None) -> None:
         """Every member of input group gi in one launch (one LPT list over all members' items)."""
+        self._live(bp)
         gp = bp.group_plans[gi]
         members = self.groups[gi][1]
         S = bp.segments.num_segments
@@ -225,6 +260,7 @@ class LoraDeltaEngine:
                 stream=None) -> None:
         """Every layer and projection: xs[l][input_group], ys[l][proj_name] — one native call
         (lsv_lora_forward) that issues each layer's group shrinks and group expands in order."""
+        self._live(bp)
         projs = self.model.projections
         L, G = self.model.layers, len(self.groups)
         order = [p for _, m in self.groups for p in m]
@@ -254,6 +290,7 @@ class LoraDeltaEngine:
         """``forward`` with peer-owned adapters fetched one layer ahead into local staging buffers by
         the copy engines (lsv_copy_blocks) while the current layer computes, so the kernels only
         read local HBM.  ``bp`` must come from ``pf.plan``."""
+        self._live(bp)
         st = stream or torch.cuda.current_stream(self.device)
         cs = pf.copy_stream
         L = self.model.layers

@@ -88,3 +88,33 @@ def test_forward_repeats_bit_identical():
     for layer in range(model.layers):
         for pr in model.projections:
             assert torch.equal(outs[0][layer][pr.name], outs[1][layer][pr.name])
+
+
+def test_stream_prepared_plans_ring_and_staleness():
+    """prepare(stream=...) uploads through the engine's reused pinned+device arenas: results are
+    bit-identical to a synchronously uploaded plan, and a plan whose arena slot a later prepare
+    reused fails loudly instead of reading another batch's plan."""
+    dev = torch.device("cuda:0")
+    model, slab, seg, eng, bp, xs = _setup(dev)
+    N = seg.num_tokens
+    st = torch.cuda.Stream(dev)
+
+    def run(plan, stream=None):
+        ys = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device=dev) for p in model.projections}
+              for _ in range(model.layers)]
+        eng.forward(plan, xs, ys, stream)
+        torch.cuda.synchronize()
+        return ys
+
+    ref = run(bp)
+    plans = []
+    for _ in range(6):     # more than the ring depth; each plan consumed on its stream right away
+        plans.append(eng.prepare(seg, stream=st))
+        with torch.cuda.stream(st):
+            got = run(plans[-1], st)
+        for layer in range(model.layers):
+            for p in model.projections:
+                assert torch.equal(got[layer][p.name], ref[layer][p.name])
+    with pytest.raises(RuntimeError, match="stale"):
+        run(plans[0])
+    run(plans[-1])   # the newest one is still live
