@@ -439,7 +439,8 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h_bytes,
                 "path": "per step: index_tokens -> LoraDeltaEngine.prepare (async uploads) -> H2D x -> forward "
                         "(one lsv_lora_forward call) -> D2H y; steps issued back to back (host planning of step k+1 "
-                        "overlaps the GPU work of step k), wall clock over all steps after one final sync"},
+                        "overlaps the GPU work of step k; H2D/D2H on their own streams with double-buffered "
+                        "x/y overlap neighbouring steps' kernels), wall clock over all steps after one final sync"},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }
