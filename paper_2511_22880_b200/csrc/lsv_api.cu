@@ -574,6 +574,7 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
     p.ldy[pp] = ldys[i];
     p.b_ptrs[pp] = b_ptrs[i];
     p.tws[pp] = b_tile_width(h->h_outs[pp]);
+    p.st32[pp] = (reinterpret_cast<uintptr_t>(ys[i]) & 31) == 0 && ldys[i] % 16 == 0;
     p.ws_vimg[pp] = (vimg_base ? 0 : h->ws_vimg) + pp * h->vimg_stride;
     tw_max = std::max(tw_max, p.tws[pp]);
   }

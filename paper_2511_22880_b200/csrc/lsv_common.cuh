@@ -292,6 +292,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t* r) 
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// 32-byte store (sm_100 STG.256); ptr must be 32-byte aligned
+__device__ __forceinline__ void st_global_v8_if(void* ptr, const uint32_t* w, bool pred) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t@p st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t}\n" ::"l"(ptr),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"((int)pred)
+               : "memory");
+}
 __device__ __forceinline__ void st_global_v4_if(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool pred) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t@p st.global.v4.b32 [%0], {%1, %2, %3, %4};\n\t}\n" ::"l"(ptr),
                "r"(a), "r"(b), "r"(c), "r"(d), "r"((uint32_t)pred)

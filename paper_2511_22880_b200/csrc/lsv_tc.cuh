@@ -69,6 +69,7 @@ struct alignas(64) ExpandParams {
   int64_t ldy[kMaxProj];
   int ws_vimg[kMaxProj];        // byte offset of each member's v images
   int tws[kMaxProj];            // each member's h_out tile width (its B slab layout: 128 or 256)
+  int st32[kMaxProj];           // 1: y base and row stride are 32-byte aligned -> 32-byte (full sector) stores
   int tw_max;                   // TMEM accumulator width
   int off_recs, off_cta;
   int* wait_flag;               // TP: wait until *wait_flag == wait_target (every rank's shard written),
@@ -83,7 +84,9 @@ struct alignas(64) ExpandParams {
 
 __device__ __forceinline__ void trace_stamp(uint64_t* trace, int trace_items, int cta, int i, int k) {
   if (trace != nullptr && i < trace_items) {
+#ifndef LSV_TRACE_CLOCK_ONLY   // the globaltimer read is slow enough to perturb per-item timings
     trace[((size_t)cta * trace_items + i) * 16 + k] = globaltimer_ns();
+#endif
     trace[((size_t)cta * trace_items + i) * 16 + 8 + k] = clock64();
   }
 }
@@ -195,6 +198,9 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 __host__ __device__ constexpr int shrink_smem_bytes() {
   return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
 }
+#ifndef LSV_EXPAND_ST32
+#define LSV_EXPAND_ST32 1
+#endif
 #ifndef LSV_EXPAND_EPI_WARPS
 #define LSV_EXPAND_EPI_WARPS 4
 #endif
@@ -686,7 +692,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       __syncwarp();
     }
   } else {  // ---------------------------- epilogue (warps 2..): thread = token row
-    const int q = warp & 3, etid = threadIdx.x - 64;
+    const int q = warp & 3;
     const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ExpandRec inf;
@@ -695,7 +701,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       const int buf = k % nbuf;
       mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
+      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const int t = q * 32 + lane;
       if (q * 32 < inf.ntok) {   // warp-uniform: quadrants past the tile's tokens have no rows
         const int tw = p.tws[inf.proj];
@@ -703,6 +709,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         const bool valid = t < inf.ntok && !(p.dbg & 1);
         __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
         const int c_lo = kExpandEpiWarps == 8 ? half * (tw / 2) : 0, c_hi = kExpandEpiWarps == 8 ? c_lo + tw / 2 : tw;
+        // each lane writes its own token row: 32-byte stores are one full sector per row and half
+        // the store wavefronts of 16-byte ones (the epilogue is the expand's busiest stage)
+        const bool st32 = LSV_EXPAND_ST32 && p.st32[inf.proj];
 #pragma unroll 1
         for (int cc = c_lo; cc < c_hi; cc += 32) {
           uint32_t r[32];
@@ -710,15 +719,20 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           uint32_t w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+          if (st32) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
+            for (int u = 0; u < 2; ++u) st_global_v8_if(yrow + cc + u * 16, &w[8 * u], valid);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
     }
   }
   tc_fence_before();

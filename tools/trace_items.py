@@ -33,3 +33,19 @@ for c in (0, 77):
     for i in range(min(n, 14)):
         v = cyc[i] - t0
         print(f"  {i:2d} {v[0]:6d} {v[1]:6d} | {v[5]:6d} {v[6]:6d} {v[7]:6d} {v[2]:6d} | {v[3]:6d} {v[4]:6d}")
+
+# aggregate over all CTAs (cycles): which stage paces the pipeline
+st = {"epi_busy": [], "mma_wait_tempty": [], "mma_wait_full": [], "mma_issue": [], "item_period": [], "prod_wait": []}
+for c in range(148):
+    cyc = tr[c, :ITEMS - 1, 8:16]
+    n = int((cyc[:, 0] > 0).sum())
+    for i in range(1, n):
+        st["epi_busy"].append(cyc[i, 4] - cyc[i, 3])
+        st["mma_wait_tempty"].append(cyc[i, 5] - cyc[i - 1, 2])
+        st["mma_wait_full"].append(cyc[i, 6] - cyc[i, 5])
+        st["mma_issue"].append(cyc[i, 2] - cyc[i, 6])
+        st["item_period"].append(cyc[i, 4] - cyc[i - 1, 4])
+        st["prod_wait"].append(cyc[i, 1] - cyc[i, 0])
+for k, v in st.items():
+    v = np.array(v)
+    print(f"{k:16s} mean {v.mean():8.1f}  p50 {np.median(v):8.1f}  p90 {np.percentile(v, 90):8.1f}")
