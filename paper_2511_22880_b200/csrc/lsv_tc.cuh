@@ -90,6 +90,12 @@ __device__ __forceinline__ void trace_stamp(uint64_t* trace, int trace_items, in
     trace[((size_t)cta * trace_items + i) * 16 + 8 + k] = clock64();
   }
 }
+// Clock-only trace builds: extra per-item stamps in the (unused) globaltimer slots.
+__device__ __forceinline__ void trace_aux(uint64_t* trace, int trace_items, int cta, int i, int k) {
+#ifdef LSV_TRACE_CLOCK_ONLY
+  if (trace != nullptr && i < trace_items) trace[((size_t)cta * trace_items + i) * 16 + k] = clock64();
+#endif
+}
 // CTA-level phase stamps land in the last item slot of the trace buffer.
 __device__ __forceinline__ void phase_stamp(uint64_t* trace, int trace_items, int cta, int k) {
   if (trace != nullptr) trace_stamp(trace, trace_items, cta, trace_items - 1, k);
@@ -198,6 +204,9 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 __host__ __device__ constexpr int shrink_smem_bytes() {
   return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
 }
+#ifndef LSV_EXPAND_EPI_PIPE
+#define LSV_EXPAND_EPI_PIPE 1
+#endif
 #ifndef LSV_EXPAND_ST32
 #define LSV_EXPAND_ST32 1
 #endif
@@ -205,9 +214,26 @@ __host__ __device__ constexpr int shrink_smem_bytes() {
 #define LSV_EXPAND_EPI_WARPS 4
 #endif
 constexpr int kExpandEpiWarps = LSV_EXPAND_EPI_WARPS;   // 4: one per TMEM lane quadrant; 8: two, each half the columns
-constexpr int kExpandThreads = 64 + 32 * kExpandEpiWarps;
+// Expand warp roles.  An epilogue warp can only read its TMEM lane quadrant (warp % 4), and
+// tiles of <= 64 tokens (most of them) keep only quadrants 0 and 1 busy with LDTM + stores, which
+// congest their SM sub-partition's memory-instruction queue.  Layout 1 therefore puts the
+// producer and the MMA issuer (serial chains of shared-memory / mbarrier ops) on sub-partitions
+// 2 and 3: warps 0, 1, 6, 7 = epilogue quadrants 0..3, 2 = producer, 3 = MMA, 4 and 5 idle.
+// Layout 0: 0 = producer, 1 = MMA, 2.. = epilogue.
+#ifndef LSV_EXPAND_LAYOUT
+#define LSV_EXPAND_LAYOUT 1
+#endif
+#if LSV_EXPAND_LAYOUT
+static_assert(LSV_EXPAND_EPI_WARPS == 4, "layout 1 has one epilogue warp per quadrant");
+constexpr int kExpProdWarp = 2, kExpMmaWarp = 3, kExpandThreads = 256;
+__device__ __forceinline__ bool expand_epi_warp(int w) { return w < 2 || w >= 6; }
+#else
+constexpr int kExpProdWarp = 0, kExpMmaWarp = 1, kExpandThreads = 64 + 32 * kExpandEpiWarps;
+__device__ __forceinline__ bool expand_epi_warp(int w) { return w >= 2; }
+#endif
+constexpr int kExpRecBufs = kExpandThreads / 32;   // one record buffer per warp (indexed by warp)
 __host__ __device__ constexpr int expand_smem_bytes() {
-  return 1024 + kExpandRingBytes + kExpandGuardBytes + 256 * 16 * 2 + (2 + kExpandEpiWarps) * (int)sizeof(ExpandRecBuf) + 1024;
+  return 1024 + kExpandRingBytes + kExpandGuardBytes + 256 * 16 * 2 + kExpRecBufs * (int)sizeof(ExpandRecBuf) + 1024;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -517,7 +543,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                    // 8 KB
   ExpandRecBuf* recbuf = reinterpret_cast<ExpandRecBuf*>(ident + kIdentRows * 16 * 2);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 2 + kExpandEpiWarps);     // [kItemQ]
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + kExpRecBufs);     // [kItemQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
   uint64_t* empty = full + kItemQ;
   uint64_t* tfull = empty + kItemQ;
@@ -543,7 +569,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       if (p.y[pp])
         for (int b = 0; b < 5; ++b) prefetch_tmap(&p.ymap[pp][b]);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -585,8 +611,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == 0) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
+  if (warp == kExpProdWarp) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
     ExpandRec inf;
     const uint8_t* b;
     uint32_t head = 0, tail = 0;
@@ -646,13 +672,14 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       }
       __syncwarp();
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer (lane 0)
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[1], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  } else if (warp == kExpMmaWarp) {  // ---------------- MMA issuer (lane 0)
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ExpandRec inf;
     const uint8_t* unused;
     const uint32_t ib = smem_u32(ident);
     for (int k = 0; rs.pop(inf, unused); ++k) {
       if (lane == 0) {
+        trace_aux(p.trace, p.trace_items, cta, k, 1);
         const int tw = p.tws[inf.proj], nb = tw / 64;
         const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
         const int qs = k % kItemQ;
@@ -660,6 +687,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         const int S = kmajor_row_bytes(kp), ck = S / 2;
         const uint32_t vlay = umma_layout(S);
         const int buf = k % nbuf;
+        trace_aux(p.trace, p.trace_items, cta, k, 2);
         mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
         trace_stamp(p.trace, p.trace_items, cta, k, 5);
         mbar_wait(&full[qs], (k / kItemQ) & 1);
@@ -690,8 +718,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         trace_stamp(p.trace, p.trace_items, cta, k, 2);
       }
       __syncwarp();
+      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 0);
     }
-  } else {  // ---------------------------- epilogue (warps 2..): thread = token row
+  } else if (expand_epi_warp(warp)) {  // ---------------- epilogue: thread = token row of quadrant q
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
@@ -712,6 +741,33 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         // each lane writes its own token row: 32-byte stores are one full sector per row and half
         // the store wavefronts of 16-byte ones (the epilogue is the expand's busiest stage)
         const bool st32 = LSV_EXPAND_ST32 && p.st32[inf.proj];
+#if LSV_EXPAND_EPI_PIPE
+        // two 32-column chunks in flight: chunk i+1's TMEM load overlaps chunk i's convert + stores
+        auto put = [&](const uint32_t* r, int cc) {
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+          if (st32) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) st_global_v8_if(yrow + cc + u * 16, &w[8 * u], valid);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
+          }
+        };
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32_nowait(taddr + c_lo, ra);
+#pragma unroll 1
+        for (int cc = c_lo; cc < c_hi; cc += 64) {   // (c_hi - c_lo) is a multiple of 64
+          tmem_wait_ld_regs(ra);
+          tmem_ld_32x32b_x32_nowait(taddr + cc + 32, rb);
+          put(ra, cc);
+          tmem_wait_ld_regs(rb);
+          if (cc + 64 < c_hi) tmem_ld_32x32b_x32_nowait(taddr + cc + 64, ra);
+          put(rb, cc + 32);
+        }
+#else
 #pragma unroll 1
         for (int cc = c_lo; cc < c_hi; cc += 32) {
           uint32_t r[32];
@@ -728,6 +784,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
               st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
           }
         }
+#endif
       }
       tc_fence_before();
       __syncwarp();
@@ -738,7 +795,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
-  if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   if (p.xsum != nullptr && threadIdx.x == 0) {   // every CTA is past the sum barrier: re-arm it
     int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
     if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }

@@ -35,11 +35,17 @@ for c in (0, 77):
         print(f"  {i:2d} {v[0]:6d} {v[1]:6d} | {v[5]:6d} {v[6]:6d} {v[7]:6d} {v[2]:6d} | {v[3]:6d} {v[4]:6d}")
 
 # aggregate over all CTAs (cycles): which stage paces the pipeline
-st = {"epi_busy": [], "mma_wait_tempty": [], "mma_wait_full": [], "mma_issue": [], "item_period": [], "prod_wait": []}
+st = {"aux_commit_sync": [], "aux_sync_pop": [], "aux_pop_pre": [], "aux_pre_tempty": [], "epi_busy": [], "mma_wait_tempty": [], "mma_wait_full": [], "mma_issue": [], "item_period": [], "prod_wait": []}
 for c in range(148):
     cyc = tr[c, :ITEMS - 1, 8:16]
     n = int((cyc[:, 0] > 0).sum())
     for i in range(1, n):
+        ax = tr[c, i, :8]; axp = tr[c, i - 1, :8]
+        if ax[1] > 0:   # clock-only build: aux stamps (0 after the loop's syncwarp, 1 after pop, 2 before tempty wait)
+            st["aux_commit_sync"].append(axp[0] - cyc[i - 1, 2])
+            st["aux_sync_pop"].append(ax[1] - axp[0])
+            st["aux_pop_pre"].append(ax[2] - ax[1])
+            st["aux_pre_tempty"].append(cyc[i, 5] - ax[2])
         st["epi_busy"].append(cyc[i, 4] - cyc[i, 3])
         st["mma_wait_tempty"].append(cyc[i, 5] - cyc[i - 1, 2])
         st["mma_wait_full"].append(cyc[i, 6] - cyc[i, 5])
@@ -48,4 +54,5 @@ for c in range(148):
         st["prod_wait"].append(cyc[i, 1] - cyc[i, 0])
 for k, v in st.items():
     v = np.array(v)
+    if len(v) == 0: continue
     print(f"{k:16s} mean {v.mean():8.1f}  p50 {np.median(v):8.1f}  p90 {np.percentile(v, 90):8.1f}")
