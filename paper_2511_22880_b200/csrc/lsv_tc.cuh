@@ -538,6 +538,24 @@ __device__ __forceinline__ void tp_row_sum(const ExpandParams& p) {
   }
 }
 
+// y rows [tok_begin, tok_begin + np16) as nb 64-column SWIZZLE_128B blocks; each block is np16/8 =
+// a sum of powers of two 8-row groups -> one TMA box per set bit.  Box `box` (one per lane):
+// 64-column block h, first row `row`, box map index bb (8 << bb rows).  False: no such box.
+__device__ __forceinline__ bool y_box(int np16, int nb, int box, int& h, int& row, int& bb) {
+  const int m = np16 >> 3, pc = __popc(m);
+  if (box < 0 || box >= nb * pc) return false;
+  h = box / pc;
+  const int i = box % pc;
+  int mm = m;
+  row = 0;
+  bb = -1;
+  for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
+    bb = 31 - __clz(mm);
+    if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -656,19 +674,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       } else if (lane == 1) {
         if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, &full[qs]);
       } else if (!(dbg & 8)) {
-        // y rows [tok_begin, tok_begin + np16) as nb 64-column SWIZZLE_128B blocks; each block is
-        // np16/8 = sum of powers of two 8-row groups -> one TMA box per set bit, one lane per box
-        const int m = np16 >> 3, pc = __popc(m), box = lane - 2;
-        if (box < nb * pc) {
-          const int h = box / pc, i = box % pc;
-          int mm = m, row = 0, bb = -1;
-          for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
-            bb = 31 - __clz(mm);
-            if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
-          }
+        int h, row, bb;
+        if (y_box(np16, nb, lane - 2, h, row, bb))
           tma_load_2d(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
                       inf.jtile * tw + h * 64, inf.tok_begin + row);
-        }
       }
       __syncwarp();
     }
