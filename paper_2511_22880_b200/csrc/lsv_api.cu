@@ -542,7 +542,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     }
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
-    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl));
+    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl, kShrinkThreads));
   }
   return LSV_OK;
 }

@@ -201,8 +201,21 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
   }
 }
 
+// Shrink warp roles: as the expand's (below), layout 1 keeps the producer and the MMA issuer off
+// the sub-partitions of the busy epilogue quadrants 0 and 1.
+#ifndef LSV_SHRINK_LAYOUT
+#define LSV_SHRINK_LAYOUT 1
+#endif
+#if LSV_SHRINK_LAYOUT
+constexpr int kShrProdWarp = 2, kShrMmaWarp = 3, kShrinkThreads = 256;
+__device__ __forceinline__ bool shrink_epi_warp(int w) { return w < 2 || w >= 6; }
+#else
+constexpr int kShrProdWarp = 0, kShrMmaWarp = 1, kShrinkThreads = 192;
+__device__ __forceinline__ bool shrink_epi_warp(int w) { return w >= 2; }
+#endif
+constexpr int kShrinkRecBufs = kShrinkThreads / 32;
 __host__ __device__ constexpr int shrink_smem_bytes() {
-  return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + 6 * (int)sizeof(ShrinkRecBuf) + 1024;
+  return 1024 + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes + kShrinkRecBufs * (int)sizeof(ShrinkRecBuf) + 1024;
 }
 #ifndef LSV_EXPAND_EPI_PIPE
 #define LSV_EXPAND_EPI_PIPE 1
@@ -237,11 +250,11 @@ __host__ __device__ constexpr int expand_smem_bytes() {
 }
 
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
+__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ShrinkRecBuf* recbuf = reinterpret_cast<ShrinkRecBuf*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + 6);
+  uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + kShrinkRecBufs);
   uint64_t* empty = full + kShrinkSlots;
   uint64_t* tfull = empty + kShrinkSlots;
   uint64_t* tempty = tfull + kAccBufs;
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
     fence_mbar_init();
     for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kShrMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -266,8 +279,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == 0) {  // ---------------- producer: lane 0 owns the slot ring, lanes issue the copies
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[0], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
+  if (warp == kShrProdWarp) {  // ---------------- producer: lane 0 owns the slot ring, lanes issue the copies
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
     ShrinkRec inf;
     const uint8_t* a;
     int slot = 0; uint32_t phase = 0;
@@ -312,9 +325,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
       __syncwarp();
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+  } else if (warp == kShrMmaWarp) {  // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
     // values stay in uniform registers, so each MMA costs a few uniform adds), one lane issues
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[1], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
     const uint8_t* unused;
     int slot = 0; uint32_t phase = 0;
@@ -357,8 +370,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       umma_commit_elect(&tfull[buf]);
       if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
     }
-  } else {  // ---------------------------- epilogue (warps 2..5)
-    const int q = warp & 3, row = q * 32 + lane, etid = threadIdx.x - 64;
+  } else if (shrink_epi_warp(warp)) {  // ---------------- epilogue: thread = token row of quadrant q
+    const int q = warp & 3, row = q * 32 + lane;
     float* partials = reinterpret_cast<float*>(p.ws + p.ws_partials);
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       const int buf = k % nbuf;
       mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
+      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
       const bool valid = row < nt && !(p.dbg & 8);
       uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
@@ -394,9 +407,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
                 else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w);
                 else *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
               } else {
-                float4* dst = reinterpret_cast<float4*>(part + j0);
-                dst[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
-                dst[1] = make_float4(v[h * 8 + 4], v[h * 8 + 5], v[h * 8 + 6], v[h * 8 + 7]);
+                float* dst = part + j0;
+                if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {   // one full sector per row
+                  st_global_v8_if(dst, reinterpret_cast<const uint32_t*>(v + h * 8), true);
+                } else {
+                  reinterpret_cast<float4*>(dst)[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
+                  reinterpret_cast<float4*>(dst)[1] = make_float4(v[h * 8 + 4], v[h * 8 + 5], v[h * 8 + 6], v[h * 8 + 7]);
+                }
               }
             }
           }
@@ -412,8 +429,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
-      if (etid == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
+      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
   }
   tc_fence_before();
@@ -421,7 +438,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) shrink_tc_kernel(const __grid_c
   if (p.tp > 0) __threadfence_system();   // scattered images visible to the peers
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
-  if (warp == 1) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (warp == kShrMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   if (p.n_red == 0) {
     if (p.tp > 0) tp_signal(p);
     return;
