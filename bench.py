@@ -322,7 +322,13 @@ def run_ours(args, rank, world, local_rank):
     exp_us = k0.elapsed_time(k1) / reps * 1e3
     shr_us = s0.elapsed_time(s1) / reps * 1e3
     achieved = exp_bytes / (exp_us * 1e-6) / 1e9
-    exp_label = f"expand_tc_kernel ({names}, one launch)"
+    # which tier the group's work runs on (plan summary: [.., simt segments, m-tiles, ..])
+    gsum = bp.group_plans[gi].summary
+    simt_only = gsum[4] > 0 and gsum[5] == 0
+    if simt_only:     # decode-regime batches: every segment on the SIMT tier
+        exp_label = f"simt_expand_kernel ({names}, one launch per member)"
+    else:
+        exp_label = f"expand_tc_kernel ({names}, one launch)"
     traffic = measured_traffic(config, exp_label)
 
     # ---- e2e through the public API with host buffers ----
@@ -431,7 +437,8 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": exp_bytes,
                      "traffic_source": "profiles/traffic_r1.json: dram__bytes_read.sum + dram__bytes_write.sum of the "
                                        "same launch from one ncu --set full capture (tools/prof_one.py)",
-                     "shrink": {"kernel": f"shrink_tc_kernel (fused {len(members)}-projection group {names})",
+                     "shrink": {"kernel": (f"simt_shrink_kernel ({names}, one launch)" if simt_only else
+                                           f"shrink_tc_kernel (fused {len(members)}-projection group {names})"),
                                 "launch_us": shr_us, "algorithmic_bytes_per_launch": shr_bytes,
                                 "achieved": shr_bytes / (shr_us * 1e-6) / 1e9}},
         "cpu_baseline": cpu,

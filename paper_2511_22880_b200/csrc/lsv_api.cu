@@ -321,6 +321,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.off_seg_tier = off; off += S;
   off = round_up(off, 4);
   h.off_simt_items = off; off += 4 * h.n_simt_items;
+  off += h.n_simt_items > 0 ? h.n_simt_items + 1 : 0;   // SIMT row-block prefix (simt_rb_prefix)
+  off = round_up(off, 4);
   h.off_mtiles = off; off += 8 * h.n_mtiles;
   h.off_shrink_recs = off; off += 16 * h.n_shrink_items;
   h.off_shrink_cta = off; off += (int32_t)pb.shrink_cta.size();
@@ -361,7 +363,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int64_t vstride = (vimg_off + 1023) / 1024 * 1024;
   h.ws_vimg = (int32_t)ws; ws += vstride * P;
   h.simt_stride = (int32_t)((v_off + 63) / 64 * 64);
-  h.ws_simt_v = (int32_t)ws; ws += (int64_t)h.simt_stride * 4 * P;
+  h.ws_simt_v = (int32_t)ws; ws += (int64_t)h.simt_stride * 4 * P * simt_ksplit(h_in);
   if (ws > INT32_MAX) return fail(LSV_EUNSUPPORTED, "workspace of %lld bytes exceeds 2 GiB", (long long)ws);
   h.vimg_stride = (int32_t)vstride;
   h.ws_bytes = (int32_t)ws;
@@ -508,13 +510,12 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
                const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true,
                const TpScatter* tps = nullptr) {
   if (h->n_simt_items > 0) {
-    // grid.y covers the widest SIMT group (num_proj x the largest SIMT rank) in 8-row blocks
+    // one block per (8-row block of an item's group A, k-split): exactly the blocks with rows
     const int32_t* hp = reinterpret_cast<const int32_t*>(h);
-    int max_r = 8;
-    for (int s = 0; s < h->num_segments; ++s)
-      if (hp[h->off_seg_tier + s] == kTierSimt) max_r = std::max(max_r, (int)hp[h->off_seg_rank + s]);
-    simt_shrink_kernel<<<dim3(h->n_simt_items, h->num_proj * max_r / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
-                                                        h->off_simt_items, h->off_seg_rank, a_ptrs,
+    const int n_rb = hp[h->off_simt_items + 4 * h->n_simt_items + h->n_simt_items];
+    simt_shrink_kernel<<<dim3(n_rb, 1, simt_ksplit(h->h_in)), 256, 0, st>>>(
+                                                        static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
+                                                        h->off_simt_items, h->n_simt_items, h->off_seg_rank, a_ptrs,
                                                         reinterpret_cast<float*>(ws + h->ws_simt_v), h->num_proj,
                                                         h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());
@@ -557,7 +558,8 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
     const int pp = p0 + i, h_out = h->h_outs[pp];
     simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 255) / 256), 128, 0, st>>>(
         static_cast<__nv_bfloat16*>(ys[i]), ldys[i], h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs[i],
-        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride);
+        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride,
+        simt_ksplit(h->h_in), (int64_t)h->num_proj * h->simt_stride);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   const bool all = np == h->num_proj && np > 1;
@@ -674,6 +676,11 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   std::copy(pb.rank.begin(), pb.rank.end(), out + h.off_seg_rank);
   std::copy(pb.tier.begin(), pb.tier.end(), out + h.off_seg_tier);
   std::memcpy(out + h.off_simt_items, pb.simt.data(), pb.simt.size() * sizeof(SimtItem));
+  if (h.n_simt_items > 0) {   // prefix over the SIMT items of their 8-row blocks of the group A
+    int32_t* pre = out + h.off_simt_items + 4 * h.n_simt_items;
+    pre[0] = 0;
+    for (int i = 0; i < h.n_simt_items; ++i) pre[i + 1] = pre[i] + h.num_proj * pb.rank[pb.simt[i].seg] / 8;
+  }
   std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
   std::memcpy(out + h.off_shrink_recs, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkRec));
   std::copy(pb.shrink_cta.begin(), pb.shrink_cta.end(), out + h.off_shrink_cta);

@@ -23,31 +23,41 @@ __device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
   return s;
 }
 
-// Shrink: grid = (n_simt_items, G / 8), block = 256: one block per (item, 8 rows of the item's
-// group A, G = nproj * rank rows).  The 8 warps split the 64-column chunks of h_in (warp w takes
-// chunks w, w + 8, ...); lane = (row of 8, quarter of a chunk), so a warp reads each chunk's 8 rows
-// as 1 KB contiguous, four chunks in flight.  Quarters reduce by shuffle, warps through shared
-// memory in a fixed order (deterministic).  v (fp32) lands in the row's projection region.
+// Shrink: grid = (row blocks, 1, simt_ksplit(h_in)), block = 256: one block per (item, 8 rows of
+// the item's group A, G = nproj * rank rows, one range of h_in's 64-column chunks); the plan's
+// row-block prefix over the items maps blockIdx.x to (item, row block).  The 8
+// warps split the range's chunks (warp w takes chunks w, w + 8, ...); lane = (row of 8, quarter of
+// a chunk), so a warp reads each chunk's 8 rows as 1 KB contiguous, four chunks in flight.
+// Quarters reduce by shuffle, warps through shared memory in a fixed order (deterministic).  The
+// split's partial v (fp32) lands in its own copy of the row's projection region.
 constexpr int kSimtUnroll = 4;
 __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                           int h_in, const int32_t* __restrict__ plan,
-                                                          int off_items, int off_rank,
+                                                          int off_items, int n_items, int off_rank,
                                                           const void* const* __restrict__ a_ptrs,
                                                           float* __restrict__ simt_v, int nproj, int simt_stride) {
   __shared__ float red[8][8][kSimtMaxTok];   // [warp][row][token]
-  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
+  const int32_t* pre = plan + off_items + 4 * n_items;   // [n_items + 1] row-block prefix
+  int lo = 0, hi = n_items - 1;                          // last item with pre[item] <= blockIdx.x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[lo];
+  const int rb = blockIdx.x - pre[lo];
   const int r = plan[off_rank + it.seg], G = nproj * r;
-  if ((int)blockIdx.y * 8 >= G) return;      // block-uniform (G % 8 == 0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rl = lane >> 2, k = blockIdx.y * 8 + rl, q4 = lane & 3;
+  const int rl = lane >> 2, k = rb * 8 + rl, q4 = lane & 3;
   const uint8_t* arow = static_cast<const uint8_t*>(a_ptrs[it.seg]) + (size_t)k * 128;
   const uint32_t u0 = (uint32_t)((2 * q4) ^ (k & 7)) << 4, u1 = (uint32_t)((2 * q4 + 1) ^ (k & 7)) << 4;
   const size_t cstride = (size_t)G * 128;            // bytes between consecutive chunks of a row
-  const int chunks = h_in / 64, nt = it.ntok;
+  const int nchunks = h_in / 64, nt = it.ntok, ks_n = gridDim.z;
+  const int cps = (nchunks + ks_n - 1) / ks_n, cbeg = blockIdx.z * cps;
+  const int chunks = min(nchunks, cbeg + cps);   // this split: chunks [cbeg, chunks)
   float acc[kSimtMaxTok];
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
-  for (int c0 = warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
+  for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
     uint4 a0[kSimtUnroll], a1[kSimtUnroll];
 #pragma unroll
     for (int u = 0; u < kSimtUnroll; ++u) {
@@ -84,61 +94,85 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   }
   __syncthreads();
   if (threadIdx.x < 8 * kSimtMaxTok) {
-    const int row = threadIdx.x / kSimtMaxTok, t = threadIdx.x % kSimtMaxTok, kk = blockIdx.y * 8 + row;
+    const int row = threadIdx.x / kSimtMaxTok, t = threadIdx.x % kSimtMaxTok, kk = rb * 8 + row;
     if (t < nt) {
       float sum = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) sum += red[w][row][t];
-      simt_v[(size_t)(kk / r) * simt_stride + it.v_off + t * r + kk % r] = sum;
+      simt_v[((size_t)blockIdx.z * nproj + kk / r) * simt_stride + it.v_off + t * r + kk % r] = sum;
     }
   }
 }
 
 // Expand: grid = (n_simt_items, ceil(h_out / 256)), block = 128 (warp w: 64 columns of the 256).
 // Lane = (k row of 4, 16-byte unit of 8 columns): a warp reads four 128-byte B atom rows per
-// load (four loads in flight), accumulates [tokens][8 columns] in registers over k, reduces the
-// four k lanes by shuffle and updates y with row-contiguous 16-byte read-modify-writes.
+// load.  The item's v (<= 8 tokens x rank fp32) is staged in shared memory once, summing the
+// shrink's k-split partials in split order, and the B loads are double-buffered (round i+1's
+// kSimtExpUnroll loads are in flight while round i is multiplied), so a high-rank item costs about
+// rank/32 memory latencies instead of rank/16.  [tokens][8 columns] accumulate in registers over
+// k; the four k lanes reduce by shuffle and y is updated with row-contiguous 16-byte
+// read-modify-writes.
+#ifndef LSV_SIMT_EXP_UNROLL
+#define LSV_SIMT_EXP_UNROLL 4
+#endif
+constexpr int kSimtExpUnroll = LSV_SIMT_EXP_UNROLL;
 __global__ void __launch_bounds__(128) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy, int h_out,
                                                           const int32_t* __restrict__ plan, int off_items,
                                                           int off_rank, const void* const* __restrict__ b_ptrs,
-                                                          const float* __restrict__ simt_v) {
+                                                          const float* __restrict__ simt_v, int ksplit,
+                                                          int64_t split_stride) {
+  __shared__ float vs[kSimtMaxTok * 256];
   const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
   const int r = plan[off_rank + it.seg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.y * 256 + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
-  if (blockIdx.y * 256 + warp * 64 >= h_out) return;            // warp-uniform (h_out % 64 == 0)
+  const bool active = blockIdx.y * 256 + warp * 64 < h_out;      // warp-uniform (h_out % 64 == 0)
   const int ks = lane >> 3, nt = it.ntok;
   const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
   const int tw = b_tile_width(h_out);
+  constexpr int U = kSimtExpUnroll;
+  uint4 cur[U], nxt[U];
+  auto load = [&](uint4* dst, int k0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * 4 + ks;
+      if (active && k < r) dst[u] = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, k, r, tw)));
+    }
+  };
+  load(cur, 0);                                  // in flight while v is staged
   const float* vp = simt_v + it.v_off;
+  for (int i = threadIdx.x; i < nt * r; i += blockDim.x) {
+    float sum = 0.f;
+    for (int z = 0; z < ksplit; ++z) sum += __ldcg(vp + z * split_stride + i);
+    vs[i] = sum;
+  }
+  __syncthreads();
+  if (!active) return;
   float acc[kSimtMaxTok][8];
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
-  for (int k0 = 0; k0 < r; k0 += 4 * kSimtUnroll) {
-    uint4 bw[kSimtUnroll];
+  for (int k0 = 0; k0 < r; k0 += 4 * U) {
+    if (k0 + 4 * U < r) load(nxt, k0 + 4 * U);
 #pragma unroll
-    for (int u = 0; u < kSimtUnroll; ++u) {
-      const int k = k0 + u * 4 + ks;
-      if (k < r) bw[u] = __ldg(reinterpret_cast<const uint4*>(b + b_tiled_off(j, k, r, tw)));
-    }
-#pragma unroll
-    for (int u = 0; u < kSimtUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int k = k0 + u * 4 + ks;
       if (k < r) {
-        const float w[8] = {bf16_lo(bw[u].x), bf16_hi(bw[u].x), bf16_lo(bw[u].y), bf16_hi(bw[u].y),
-                            bf16_lo(bw[u].z), bf16_hi(bw[u].z), bf16_lo(bw[u].w), bf16_hi(bw[u].w)};
+        const float w[8] = {bf16_lo(cur[u].x), bf16_hi(cur[u].x), bf16_lo(cur[u].y), bf16_hi(cur[u].y),
+                            bf16_lo(cur[u].z), bf16_hi(cur[u].z), bf16_lo(cur[u].w), bf16_hi(cur[u].w)};
 #pragma unroll
         for (int t = 0; t < kSimtMaxTok; ++t) {
           if (t < nt) {
-            const float vv = __ldg(vp + t * r + k);
+            const float vv = vs[t * r + k];
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
           }
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
   }
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t)

@@ -250,6 +250,58 @@ __host__ __device__ constexpr int expand_smem_bytes() {
 }
 
 // ------------------------------------------------------------------------------------------
+// One split-K reduce unit: 8 k of member pp for token t of split tile e (entry in the plan's
+// reduce table).  Resolving it reads only static plan data.
+struct RedUnit {
+  MTile mt;
+  int e, t, pp, k0;
+};
+__device__ __forceinline__ RedUnit red_unit(const ShrinkParams& p, int u, int e) {
+  const int32_t* red = p.plan + p.off_red;
+  while (e + 1 < p.n_red && red[2 * (e + 1) + 1] <= u) ++e;
+  RedUnit ru;
+  ru.mt = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles)[red[2 * e]];
+  ru.e = e;
+  const int upr = kpad(ru.mt.rank) / 8, v = u - red[2 * e + 1];
+  const int upt = p.num_proj * upr;   // units per token: projections x k units
+  ru.t = v / upt;
+  ru.pp = (v % upt) / upr;
+  ru.k0 = (v % upr) * 8;
+  return ru;
+}
+// Sum of the unit's partials over its splits, in split order (bit-reproducible).
+__device__ __forceinline__ void red_sum(const ShrinkParams& p, const RedUnit& ru, float* s8) {
+#pragma unroll
+  for (int q8 = 0; q8 < 8; ++q8) s8[q8] = 0.f;
+  if (ru.k0 >= ru.mt.rank) return;
+  const float* partials = reinterpret_cast<const float*>(p.ws + p.ws_partials);
+  const int G = p.num_proj * ru.mt.rank;
+  const size_t stride = (size_t)ru.mt.ntok * G;
+  const float* base = partials + ru.mt.part_off + (size_t)ru.t * G + ru.pp * ru.mt.rank + ru.k0;
+  for (int j = 0; j < ru.mt.nsplit; ++j) {
+    const float4 lo4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride));
+    const float4 hi4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride) + 1);
+    s8[0] += lo4.x; s8[1] += lo4.y; s8[2] += lo4.z; s8[3] += lo4.w;
+    s8[4] += hi4.x; s8[5] += hi4.y; s8[6] += hi4.z; s8[7] += hi4.w;
+  }
+}
+__device__ __forceinline__ void red_store(const ShrinkParams& p, const RedUnit& ru, const float* s8) {
+  const int32_t* red = p.plan + p.off_red;
+  const int kp = kpad(ru.mt.rank), np16 = round_up(ru.mt.ntok, 16);
+  uint4 w;
+  w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
+  w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
+  if (p.tp > 0 && p.tp_row) {
+    if (ru.k0 < ru.mt.rank) tp_row_put(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, s8);
+  } else if (p.tp > 0) {
+    if (ru.k0 < ru.mt.rank) tp_scatter(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, ru.mt.rank, np16, w);
+    if (ru.k0 == 0) tp_scatter_pad(p, red[2 * ru.e], ru.pp, ru.t, np16);   // once per (token, member)
+  } else {
+    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)ru.pp * p.vimg_stride + ru.mt.vimg_off +
+                              vimg_off(ru.t, ru.k0, kp, np16)) = w;
+  }
+}
+
 __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -433,6 +485,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
   }
+  // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
+  // recorded the table entry holding its first unit.  Each thread resolves its first two units
+  // (static plan data, dependent loads) now, while other warps finish, so that after the grid
+  // barrier it only loads and sums partials.
+  const int u0 = (int)((int64_t)p.red_units * blockIdx.x / gridDim.x);
+  const int u1 = (int)((int64_t)p.red_units * (blockIdx.x + 1) / gridDim.x);
+  const int ua = u0 + threadIdx.x, ub = ua + blockDim.x;
+  RedUnit ra{}, rb{};
+  if (p.n_red > 0 && ua < u1) {
+    ra = red_unit(p, ua, p.plan[p.off_red_cta + blockIdx.x]);
+    if (ub < u1) rb = red_unit(p, ub, ra.e);
+  }
   tc_fence_before();
   __threadfence();             // partials visible device-wide before the grid barrier
   if (p.tp > 0) __threadfence_system();   // scattered images visible to the peers
@@ -465,44 +529,19 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   }
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 4);
-  const MTile* mtiles = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
-  const int32_t* red = p.plan + p.off_red;
-  const float* partials = reinterpret_cast<const float*>(p.ws + p.ws_partials);
-  // CTA c owns units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host recorded the
-  // table entry holding its first unit, so each thread only walks forward a step or two.
-  const int u0 = (int)((int64_t)p.red_units * blockIdx.x / gridDim.x);
-  const int u1 = (int)((int64_t)p.red_units * (blockIdx.x + 1) / gridDim.x);
-  const int e0 = p.plan[p.off_red_cta + blockIdx.x];
-  for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-    int e = e0;
-    while (e + 1 < p.n_red && red[2 * (e + 1) + 1] <= u) ++e;
-    const MTile mt = mtiles[red[2 * e]];
-    const int kp = kpad(mt.rank), upr = kp / 8, v = u - red[2 * e + 1], np16 = round_up(mt.ntok, 16);
-    const int G = p.num_proj * mt.rank, upt = p.num_proj * upr;   // units per token: projections x k units
-    const int t = v / upt, pp = (v % upt) / upr, k0 = (v % upr) * 8;
-    float s8[8];
-#pragma unroll
-    for (int q8 = 0; q8 < 8; ++q8) s8[q8] = 0.f;
-    if (k0 < mt.rank) {
-      const size_t stride = (size_t)mt.ntok * G;
-      const float* base = partials + mt.part_off + (size_t)t * G + pp * mt.rank + k0;
-      for (int j = 0; j < mt.nsplit; ++j) {
-        const float4 lo4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride));
-        const float4 hi4 = __ldcg(reinterpret_cast<const float4*>(base + j * stride) + 1);
-        s8[0] += lo4.x; s8[1] += lo4.y; s8[2] += lo4.z; s8[3] += lo4.w;
-        s8[4] += hi4.x; s8[5] += hi4.y; s8[6] += hi4.z; s8[7] += hi4.w;
-      }
-    }
-    uint4 w;
-    w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
-    w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
-    if (p.tp > 0 && p.tp_row) {
-      if (k0 < mt.rank) tp_row_put(p, red[2 * e], pp, t, k0, s8);
-    } else if (p.tp > 0) {
-      if (k0 < mt.rank) tp_scatter(p, red[2 * e], pp, t, k0, mt.rank, np16, w);
-      if (k0 == 0) tp_scatter_pad(p, red[2 * e], pp, t, np16);   // once per (token, member)
-    } else {
-      *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+  if (ua < u1) {
+    float sa[8], sb[8];
+    red_sum(p, ra, sa);                  // both units' loads in flight before either store
+    if (ub < u1) red_sum(p, rb, sb);
+    red_store(p, ra, sa);
+    if (ub < u1) red_store(p, rb, sb);
+    int e = ub < u1 ? rb.e : ra.e;
+    for (int u = ub + blockDim.x; u < u1; u += blockDim.x) {
+      const RedUnit ru = red_unit(p, u, e);
+      e = ru.e;
+      float s8[8];
+      red_sum(p, ru, s8);
+      red_store(p, ru, s8);
     }
   }
   if (p.tp > 0) __threadfence_system();
