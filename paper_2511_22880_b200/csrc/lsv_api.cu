@@ -321,7 +321,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.off_seg_tier = off; off += S;
   off = round_up(off, 4);
   h.off_simt_items = off; off += 4 * h.n_simt_items;
-  off += h.n_simt_items > 0 ? h.n_simt_items + 1 : 0;   // SIMT row-block prefix (simt_rb_prefix)
+  // SIMT tail: row-block prefix [n + 1] (shrink), small-item count, expand order [n]
+  off += h.n_simt_items > 0 ? 2 * h.n_simt_items + 2 : 0;
   off = round_up(off, 4);
   h.off_mtiles = off; off += 8 * h.n_mtiles;
   h.off_shrink_recs = off; off += 16 * h.n_shrink_items;
@@ -554,12 +555,23 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
                const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st,
                const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0,
                const uint8_t* xsum = nullptr) {
-  for (int i = 0; i < np && h->n_simt_items > 0; ++i) {
-    const int pp = p0 + i, h_out = h->h_outs[pp];
-    simt_expand_kernel<<<dim3(h->n_simt_items, (h_out + 255) / 256), 128, 0, st>>>(
-        static_cast<__nv_bfloat16*>(ys[i]), ldys[i], h_out, plan, h->off_simt_items, h->off_seg_rank, b_ptrs[i],
-        reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride,
-        simt_ksplit(h->h_in), (int64_t)h->num_proj * h->simt_stride);
+  if (h->n_simt_items > 0) {   // every member in one launch per token class (grid.z = member)
+    SimtExpandArgs a{};
+    int max_tiles = 0;
+    for (int i = 0; i < np; ++i) {
+      const int pp = p0 + i;
+      a.y[i] = static_cast<__nv_bfloat16*>(ys[i]);
+      a.ldy[i] = ldys[i];
+      a.h_out[i] = h->h_outs[pp];
+      a.b_ptrs[i] = b_ptrs[i];
+      a.v[i] = reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride;
+      max_tiles = std::max(max_tiles, (h->h_outs[pp] + 255) / 256);
+    }
+    a.plan = plan; a.off_items = h->off_simt_items; a.n_items = h->n_simt_items; a.off_rank = h->off_seg_rank;
+    a.ksplit = simt_ksplit(h->h_in); a.split_stride = (int64_t)h->num_proj * h->simt_stride;
+    // one launch: the small accumulator; larger items (rare in decode) in token-pair passes
+    a.item0 = 0;
+    simt_expand_kernel<kSimtSmallTok><<<dim3(h->n_simt_items, max_tiles, np), 128, 0, st>>>(a);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   const bool all = np == h->num_proj && np > 1;
@@ -676,10 +688,22 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   std::copy(pb.rank.begin(), pb.rank.end(), out + h.off_seg_rank);
   std::copy(pb.tier.begin(), pb.tier.end(), out + h.off_seg_tier);
   std::memcpy(out + h.off_simt_items, pb.simt.data(), pb.simt.size() * sizeof(SimtItem));
-  if (h.n_simt_items > 0) {   // prefix over the SIMT items of their 8-row blocks of the group A
-    int32_t* pre = out + h.off_simt_items + 4 * h.n_simt_items;
+  if (h.n_simt_items > 0) {
+    // shrink: prefix over the SIMT items (segment order) of their 8-row blocks of the group A;
+    // expand: the items with <= kSimtSmallTok tokens first (small register accumulator; decode
+    // batches are almost all 1-2 tokens per adapter), then the rest, and the small count
+    const int n = h.n_simt_items;
+    int32_t* pre = out + h.off_simt_items + 4 * n;
+    int32_t* order = pre + n + 2;
     pre[0] = 0;
-    for (int i = 0; i < h.n_simt_items; ++i) pre[i + 1] = pre[i] + h.num_proj * pb.rank[pb.simt[i].seg] / 8;
+    int n_small = 0;
+    for (int i = 0; i < n; ++i) {
+      pre[i + 1] = pre[i] + h.num_proj * pb.rank[pb.simt[i].seg] / 8;
+      if (pb.simt[i].ntok <= kSimtSmallTok) order[n_small++] = i;
+    }
+    for (int i = 0, k = n_small; i < n; ++i)
+      if (pb.simt[i].ntok > kSimtSmallTok) order[k++] = i;
+    pre[n + 1] = n_small;
   }
   std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
   std::memcpy(out + h.off_shrink_recs, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkRec));

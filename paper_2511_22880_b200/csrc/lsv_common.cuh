@@ -26,6 +26,10 @@ constexpr int kNumSmsDefault = 148;
 constexpr int kChunk = 64;          // elements per 128-byte swizzle row
 constexpr int kTileM = 128;         // tokens per tcgen05 m-tile
 constexpr int kSimtMaxTok = 8;      // tokens per SIMT item
+#ifndef LSV_SIMT_SMALL_TOK
+#define LSV_SIMT_SMALL_TOK 2
+#endif
+constexpr int kSimtSmallTok = LSV_SIMT_SMALL_TOK;    // SIMT items up to this many tokens use the small expand accumulator
 
 __host__ __device__ __forceinline__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
 

@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   }
 }
 
-// Expand: grid = (n_simt_items, ceil(h_out / 256)), block = 128 (warp w: 64 columns of the 256).
+// Expand: grid = (items of one token class, ceil(max h_out / 256), members), block = 128 (warp w:
+// 64 columns of the 256); one launch per token class (<= kSimtSmallTok tokens, the rest).
 // Lane = (k row of 4, 16-byte unit of 8 columns): a warp reads four 128-byte B atom rows per
 // load.  The item's v (<= 8 tokens x rank fp32) is staged in shared memory once, summing the
 // shrink's k-split partials in split order, and the B loads are double-buffered (round i+1's
@@ -116,19 +117,31 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
 #define LSV_SIMT_EXP_UNROLL 4
 #endif
 constexpr int kSimtExpUnroll = LSV_SIMT_EXP_UNROLL;
-__global__ void __launch_bounds__(128) simt_expand_kernel(__nv_bfloat16* __restrict__ y, int64_t ldy, int h_out,
-                                                          const int32_t* __restrict__ plan, int off_items,
-                                                          int off_rank, const void* const* __restrict__ b_ptrs,
-                                                          const float* __restrict__ simt_v, int ksplit,
-                                                          int64_t split_stride) {
+struct SimtExpandArgs {          // every member of an input group (grid.z = member)
+  __nv_bfloat16* y[kMaxProj];
+  int64_t ldy[kMaxProj];
+  int h_out[kMaxProj];
+  const void* const* b_ptrs[kMaxProj];
+  const float* v[kMaxProj];      // member's k-split-0 v region
+  const int32_t* plan;
+  int off_items, n_items, off_rank, item0, ksplit;
+  int64_t split_stride;          // floats between k-split copies of the v regions
+};
+template <int NT>                // accumulator rows: tokens per pass over the item's B tile
+__global__ void __launch_bounds__(128) simt_expand_kernel(const __grid_constant__ SimtExpandArgs a) {
   __shared__ float vs[kSimtMaxTok * 256];
-  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[blockIdx.x];
-  const int r = plan[off_rank + it.seg];
+  const int m = blockIdx.z, h_out = a.h_out[m];
+  if ((int)blockIdx.y * 256 >= h_out) return;    // block-uniform: past this member's columns
+  const int item = a.plan[a.off_items + 5 * a.n_items + 2 + a.item0 + blockIdx.x];   // expand order
+  const SimtItem it = reinterpret_cast<const SimtItem*>(a.plan + a.off_items)[item];
+  const int r = a.plan[a.off_rank + it.seg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.y * 256 + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
   const bool active = blockIdx.y * 256 + warp * 64 < h_out;      // warp-uniform (h_out % 64 == 0)
   const int ks = lane >> 3, nt = it.ntok;
-  const uint8_t* b = static_cast<const uint8_t*>(b_ptrs[it.seg]);
+  __nv_bfloat16* const y = a.y[m];
+  const int64_t ldy = a.ldy[m];
+  const uint8_t* b = static_cast<const uint8_t*>(a.b_ptrs[m][it.seg]);
   const int tw = b_tile_width(h_out);
   constexpr int U = kSimtExpUnroll;
   uint4 cur[U], nxt[U];
@@ -140,59 +153,63 @@ __global__ void __launch_bounds__(128) simt_expand_kernel(__nv_bfloat16* __restr
     }
   };
   load(cur, 0);                                  // in flight while v is staged
-  const float* vp = simt_v + it.v_off;
+  const float* vp = a.v[m] + it.v_off;
   for (int i = threadIdx.x; i < nt * r; i += blockDim.x) {
     float sum = 0.f;
-    for (int z = 0; z < ksplit; ++z) sum += __ldcg(vp + z * split_stride + i);
+    for (int z = 0; z < a.ksplit; ++z) sum += __ldcg(vp + z * a.split_stride + i);
     vs[i] = sum;
   }
   __syncthreads();
   if (!active) return;
-  float acc[kSimtMaxTok][8];
+  // NT tokens per pass; items with more tokens (rare in decode) re-read their B tile from L1/L2
+  for (int tb = 0; tb < nt; tb += NT) {
+    if (tb > 0) load(cur, 0);
+    float acc[NT][8];
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t)
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
-  for (int k0 = 0; k0 < r; k0 += 4 * U) {
-    if (k0 + 4 * U < r) load(nxt, k0 + 4 * U);
+      for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
+    for (int k0 = 0; k0 < r; k0 += 4 * U) {
+      if (k0 + 4 * U < r) load(nxt, k0 + 4 * U);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * 4 + ks;
-      if (k < r) {
-        const float w[8] = {bf16_lo(cur[u].x), bf16_hi(cur[u].x), bf16_lo(cur[u].y), bf16_hi(cur[u].y),
-                            bf16_lo(cur[u].z), bf16_hi(cur[u].z), bf16_lo(cur[u].w), bf16_hi(cur[u].w)};
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * 4 + ks;
+        if (k < r) {
+          const float w[8] = {bf16_lo(cur[u].x), bf16_hi(cur[u].x), bf16_lo(cur[u].y), bf16_hi(cur[u].y),
+                              bf16_lo(cur[u].z), bf16_hi(cur[u].z), bf16_lo(cur[u].w), bf16_hi(cur[u].w)};
 #pragma unroll
-        for (int t = 0; t < kSimtMaxTok; ++t) {
-          if (t < nt) {
-            const float vv = vs[t * r + k];
+          for (int t = 0; t < NT; ++t) {
+            if (tb + t < nt) {
+              const float vv = vs[(tb + t) * r + k];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
+              for (int e = 0; e < 8; ++e) acc[t][e] = fmaf(vv, w[e], acc[t][e]);
+            }
           }
         }
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-  }
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t)
+      for (int e = 0; e < 8; ++e) {
+        acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 8);
+        acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 16);
+      }
+    if (ks == 0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 8);
-      acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], 16);
-    }
-  if (ks == 0) {
-#pragma unroll
-    for (int t = 0; t < kSimtMaxTok; ++t) {
-      if (t < nt) {
-        uint4* py = reinterpret_cast<uint4*>(y + (int64_t)(it.tok_begin + t) * ldy + j);
-        const uint4 yv = *py;
-        uint4 o;
-        o.x = pack_bf16x2(bf16_lo(yv.x) + acc[t][0], bf16_hi(yv.x) + acc[t][1]);
-        o.y = pack_bf16x2(bf16_lo(yv.y) + acc[t][2], bf16_hi(yv.y) + acc[t][3]);
-        o.z = pack_bf16x2(bf16_lo(yv.z) + acc[t][4], bf16_hi(yv.z) + acc[t][5]);
-        o.w = pack_bf16x2(bf16_lo(yv.w) + acc[t][6], bf16_hi(yv.w) + acc[t][7]);
-        *py = o;
+      for (int t = 0; t < NT; ++t) {
+        if (tb + t < nt) {
+          uint4* py = reinterpret_cast<uint4*>(y + (int64_t)(it.tok_begin + tb + t) * ldy + j);
+          const uint4 yv = *py;
+          uint4 o;
+          o.x = pack_bf16x2(bf16_lo(yv.x) + acc[t][0], bf16_hi(yv.x) + acc[t][1]);
+          o.y = pack_bf16x2(bf16_lo(yv.y) + acc[t][2], bf16_hi(yv.y) + acc[t][3]);
+          o.z = pack_bf16x2(bf16_lo(yv.z) + acc[t][4], bf16_hi(yv.z) + acc[t][5]);
+          o.w = pack_bf16x2(bf16_lo(yv.w) + acc[t][6], bf16_hi(yv.w) + acc[t][7]);
+          *py = o;
+        }
       }
     }
   }

@@ -127,3 +127,18 @@ def test_shrink_expand_split_equals_apply():
     eng.expand(bp2, 0, 0, y)
     torch.cuda.synchronize()
     assert torch.equal(y.cpu(), y_ref)
+
+
+@pytest.mark.parametrize("h_in,h_out", [(11008, 4096), (4096, 11008), (1024, 2816)])
+def test_decode_regime_simt(h_in, h_out):
+    """Decode-shaped batches on the SIMT tier: 1-8-token segments (the expand's 2-token passes,
+    odd counts), ranks 8..256 (r > 128 is SIMT at any length), and h_in up to 11008 (several
+    shrink k-splits whose partials the expand sums in split order)."""
+    lengths = [1, 2, 3, 1, 5, 8, 1, 2, 7, 4, 1, 6, 2, 1]
+    ranks = [8, 16, 32, 64, 128, 256, 8, 200, 24, 40, 136, 16, 64, 8]
+    case = Case(h_in, h_out, lengths, ranks, seed=12)
+    err, bp = _check(case)
+    s = bp.shape_plans[(h_in, h_out)].summary
+    assert s[5] == 0   # every segment on the SIMT tier
+    outs, _ = case.run_gpu(repeat=2)
+    assert torch.equal(outs[0], outs[1])   # deterministic k-split sums
