@@ -487,6 +487,22 @@ cudaError_t launch_pdl(void (*kernel)(Params), int grid, int smem, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
+// The same for any kernel signature and grid shape (the SIMT kernels).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_any(void (*kernel)(KArgs...), dim3 grid, int threads, cudaStream_t st, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_dev, const void* ws) {
   if (!h) return fail(LSV_EINVAL, "plan_host is not a liblsv plan");
   if (!plan_dev) return fail(LSV_EINVAL, "plan_dev is null");
@@ -509,17 +525,15 @@ struct TpScatter {
 
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
                const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true,
-               const TpScatter* tps = nullptr) {
+               const TpScatter* tps = nullptr, bool simt_pdl = false) {
   if (h->n_simt_items > 0) {
     // one block per (8-row block of an item's group A, k-split): exactly the blocks with rows
     const int32_t* hp = reinterpret_cast<const int32_t*>(h);
     const int n_rb = hp[h->off_simt_items + 4 * h->n_simt_items + h->n_simt_items];
-    simt_shrink_kernel<<<dim3(n_rb, 1, simt_ksplit(h->h_in)), 256, 0, st>>>(
-                                                        static_cast<const __nv_bfloat16*>(x), ldx, h->h_in, plan,
-                                                        h->off_simt_items, h->n_simt_items, h->off_seg_rank, a_ptrs,
-                                                        reinterpret_cast<float*>(ws + h->ws_simt_v), h->num_proj,
-                                                        h->simt_stride);
-    LSV_CUDA_CHECK(cudaGetLastError());
+    LSV_CUDA_CHECK(launch_pdl_any(simt_shrink_kernel, dim3(n_rb, 1, simt_ksplit(h->h_in)), 256, st, simt_pdl,
+                                  static_cast<const __nv_bfloat16*>(x), ldx, (int)h->h_in, plan,
+                                  (int)h->off_simt_items, (int)h->n_simt_items, (int)h->off_seg_rank, a_ptrs,
+                                  reinterpret_cast<float*>(ws + h->ws_simt_v), (int)h->num_proj, (int)h->simt_stride));
   }
   if (h->n_shrink_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
@@ -554,7 +568,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
 int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys, int32_t num_tokens,
                const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st,
                const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0,
-               const uint8_t* xsum = nullptr) {
+               const uint8_t* xsum = nullptr, bool simt_pdl = false) {
   if (h->n_simt_items > 0) {   // every member in one launch per token class (grid.z = member)
     SimtExpandArgs a{};
     int max_tiles = 0;
@@ -571,8 +585,8 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
     a.ksplit = simt_ksplit(h->h_in); a.split_stride = (int64_t)h->num_proj * h->simt_stride;
     // one launch: the small accumulator; larger items (rare in decode) in token-pair passes
     a.item0 = 0;
-    simt_expand_kernel<kSimtSmallTok><<<dim3(h->n_simt_items, max_tiles, np), 128, 0, st>>>(a);
-    LSV_CUDA_CHECK(cudaGetLastError());
+    LSV_CUDA_CHECK(launch_pdl_any(simt_expand_kernel<kSimtSmallTok>, dim3(h->n_simt_items, max_tiles, np), 128, st,
+                                  simt_pdl, a));
   }
   const bool all = np == h->num_proj && np > 1;
   const int n_items = all ? h->n_expand_all : h->n_expand_items_p[p0];
@@ -826,9 +840,10 @@ int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out
                     static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
 }
 
-int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_tokens, const void* const* const* b_ptrs,
-                          const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
-                          lsv_stream_t stream) {
+namespace {
+int expand_group_checked(void* const* ys, const int64_t* ldys, int32_t num_tokens, const void* const* const* b_ptrs,
+                         const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                         cudaStream_t stream, bool simt_pdl) {
   const PlanHeader* h = check_plan(plan_host);
   if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
   if (!ys || !ldys || !b_ptrs) return fail(LSV_EINVAL, "ys / ldys / b_ptrs must be non-null host arrays");
@@ -841,7 +856,15 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
       return fail(LSV_EINVAL, "member %d: y must be 16-byte aligned with ldy %% 8 == 0, ldy >= h_out", pp);
   }
   return run_expand(h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, static_cast<const int32_t*>(plan_dev),
-                    static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
+                    static_cast<uint8_t*>(workspace), stream, nullptr, nullptr, 0, nullptr, simt_pdl);
+}
+}  // namespace
+
+int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_tokens, const void* const* const* b_ptrs,
+                          const void* plan_dev, const void* plan_host, void* workspace, size_t workspace_bytes,
+                          lsv_stream_t stream) {
+  return expand_group_checked(ys, ldys, num_tokens, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream), false);
 }
 
 int lsv_lora_expand(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, const void* const* b_ptrs,
@@ -896,15 +919,19 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
       if (h->num_tokens > 0) {
         if (!x || !aligned16(x) || ldx % 8 || ldx < h->h_in || num_tokens < h->num_tokens)
           return fail(LSV_EINVAL, "layer %d group %d: bad x", l, g);
+        // every launch after the first may start during its predecessor's tail (PDL): inside
+        // this call no kernel writes an adapter slab, so the SIMT kernels stream their first
+        // weights before griddepcontrol.wait
         if (int rc = run_shrink(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S,
-                                static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st, first ? 1 : 0, !first))
+                                static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st, first ? 1 : 0, !first,
+                                nullptr, !first))
           return rc;
       }
       const void* const* btab[kMaxProj];
       for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
-      if (int rc = lsv_lora_expand_group(ys + (size_t)l * nproj + p0, ldys + (size_t)l * nproj + p0, num_tokens,
-                                         btab, plans_dev[g], plans_host[g], wsl + ws_off[g],
-                                         ws_off[g + 1] - ws_off[g], stream))
+      if (int rc = expand_group_checked(ys + (size_t)l * nproj + p0, ldys + (size_t)l * nproj + p0, num_tokens,
+                                        btab, plans_dev[g], plans_host[g], wsl + ws_off[g],
+                                        ws_off[g + 1] - ws_off[g], st, true))
         return rc;
       p0 += np;
     }

@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   float acc[kSimtMaxTok];
 #pragma unroll
   for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
-  for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
-    uint4 a0[kSimtUnroll], a1[kSimtUnroll];
+  uint4 a0[kSimtUnroll], a1[kSimtUnroll];
+  auto load = [&](int c0) {
 #pragma unroll
     for (int u = 0; u < kSimtUnroll; ++u) {
       const int c = c0 + 8 * u;
@@ -68,6 +68,14 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
         a1[u] = __ldg(reinterpret_cast<const uint4*>(ap + u1));
       }
     }
+  };
+  load(cbeg + warp);
+  // PDL (lsv_lora_forward): the first A loads above may overlap the previous kernel's tail; x and
+  // the v partials are touched only after it has completed.  A no-op for a normal launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
+    if (c0 != cbeg + warp) load(c0);
 #pragma unroll
     for (int u = 0; u < kSimtUnroll; ++u) {
       const int c = c0 + 8 * u;
@@ -153,6 +161,10 @@ __global__ void __launch_bounds__(128) simt_expand_kernel(const __grid_constant_
     }
   };
   load(cur, 0);                                  // in flight while v is staged
+  // PDL (lsv_lora_forward): the B loads above may overlap the previous kernel's tail; v and y
+  // are read only after it has completed.  A no-op for a normally launched grid.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const float* vp = a.v[m] + it.v_off;
   for (int i = threadIdx.x; i < nt * r; i += blockDim.x) {
     float sum = 0.f;
