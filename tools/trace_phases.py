@@ -25,6 +25,12 @@ lib.lsv_debug_set_trace(buf.data_ptr(), ITEMS)
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record()
 if kind == "expand": eng.expand(bp, 0, proj, y)
+elif kind == "group":   # the one-launch expand of proj's whole input group (what forward runs)
+    gi, _ = eng._member[proj]
+    ysg = [torch.zeros(4096, model.projections[q].h_out, device=dev, dtype=torch.bfloat16) for q in eng.groups[gi][1]]
+    eng.expand_group(bp, 0, gi, ysg); torch.cuda.synchronize()
+    lib.lsv_debug_set_trace(buf.data_ptr(), ITEMS); e0.record()
+    eng.expand_group(bp, 0, gi, ysg)
 else: eng.shrink(bp, 0, proj, x)
 e1.record(); torch.cuda.synchronize(); lib.lsv_debug_set_trace(None, 0)
 ph = buf.view(148, ITEMS, 16)[:, ITEMS - 1, :8].cpu().numpy().astype(np.float64)
