@@ -193,7 +193,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     if (simt) {
       for (int tb = 0; tb < n; tb += kSimtMaxTok) {
         const int nt = std::min(kSimtMaxTok, n - tb);
-        pb.simt.push_back(SimtItem{s, indptr[s] + tb, nt, (int32_t)v_off});
+        pb.simt.push_back(SimtItem{s, indptr[s] + tb, nt | rank[s] << 16, (int32_t)v_off});
         v_off += (int64_t)nt * rank[s];
       }
     } else {
@@ -321,8 +321,12 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.off_seg_tier = off; off += S;
   off = round_up(off, 4);
   h.off_simt_items = off; off += 4 * h.n_simt_items;
-  // SIMT tail: row-block prefix [n + 1] (shrink), small-item count, expand order [n]
-  off += h.n_simt_items > 0 ? 2 * h.n_simt_items + 2 : 0;
+  // SIMT tail (lsv_plan.h): row-block prefix [n + 1], row-block map [n_rb]
+  if (h.n_simt_items > 0) {
+    int n_rb = 0;
+    for (const SimtItem& it : pb.simt) n_rb += P * simt_rank(it) / 8;
+    off += h.n_simt_items + 1 + n_rb;
+  }
   off = round_up(off, 4);
   h.off_mtiles = off; off += 8 * h.n_mtiles;
   h.off_shrink_recs = off; off += 16 * h.n_shrink_items;
@@ -532,7 +536,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     const int n_rb = hp[h->off_simt_items + 4 * h->n_simt_items + h->n_simt_items];
     LSV_CUDA_CHECK(launch_pdl_any(simt_shrink_kernel, dim3(n_rb, 1, simt_ksplit(h->h_in)), 256, st, simt_pdl,
                                   static_cast<const __nv_bfloat16*>(x), ldx, (int)h->h_in, plan,
-                                  (int)h->off_simt_items, (int)h->n_simt_items, (int)h->off_seg_rank, a_ptrs,
+                                  (int)h->off_simt_items, (int)h->n_simt_items, a_ptrs,
                                   reinterpret_cast<float*>(ws + h->ws_simt_v), (int)h->num_proj, (int)h->simt_stride));
   }
   if (h->n_shrink_items > 0) {
@@ -581,10 +585,9 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
       a.v[i] = reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride;
       max_tiles = std::max(max_tiles, (h->h_outs[pp] + 255) / 256);
     }
-    a.plan = plan; a.off_items = h->off_simt_items; a.n_items = h->n_simt_items; a.off_rank = h->off_seg_rank;
+    a.plan = plan; a.off_items = h->off_simt_items;
     a.ksplit = simt_ksplit(h->h_in); a.split_stride = (int64_t)h->num_proj * h->simt_stride;
     // one launch: the small accumulator; larger items (rare in decode) in token-pair passes
-    a.item0 = 0;
     LSV_CUDA_CHECK(launch_pdl_any(simt_expand_kernel<kSimtSmallTok>, dim3(h->n_simt_items, max_tiles, np), 128, st,
                                   simt_pdl, a));
   }
@@ -702,22 +705,16 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   std::copy(pb.rank.begin(), pb.rank.end(), out + h.off_seg_rank);
   std::copy(pb.tier.begin(), pb.tier.end(), out + h.off_seg_tier);
   std::memcpy(out + h.off_simt_items, pb.simt.data(), pb.simt.size() * sizeof(SimtItem));
-  if (h.n_simt_items > 0) {
-    // shrink: prefix over the SIMT items (segment order) of their 8-row blocks of the group A;
-    // expand: the items with <= kSimtSmallTok tokens first (small register accumulator; decode
-    // batches are almost all 1-2 tokens per adapter), then the rest, and the small count
+  if (h.n_simt_items > 0) {   // SIMT tail: row-block prefix over the items, then the row-block map
     const int n = h.n_simt_items;
     int32_t* pre = out + h.off_simt_items + 4 * n;
-    int32_t* order = pre + n + 2;
+    int32_t* rbmap = pre + n + 1;
     pre[0] = 0;
-    int n_small = 0;
     for (int i = 0; i < n; ++i) {
-      pre[i + 1] = pre[i] + h.num_proj * pb.rank[pb.simt[i].seg] / 8;
-      if (pb.simt[i].ntok <= kSimtSmallTok) order[n_small++] = i;
+      const int nrb = h.num_proj * simt_rank(pb.simt[i]) / 8;
+      for (int rb = 0; rb < nrb; ++rb) rbmap[pre[i] + rb] = i << 8 | rb;
+      pre[i + 1] = pre[i] + nrb;
     }
-    for (int i = 0, k = n_small; i < n; ++i)
-      if (pb.simt[i].ntok > kSimtSmallTok) order[k++] = i;
-    pre[n + 1] = n_small;
   }
   std::memcpy(out + h.off_mtiles, pb.mtiles.data(), pb.mtiles.size() * sizeof(MTile));
   std::memcpy(out + h.off_shrink_recs, pb.shrink.data(), pb.shrink.size() * sizeof(ShrinkRec));

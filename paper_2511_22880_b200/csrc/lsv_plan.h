@@ -50,8 +50,14 @@ struct PlanHeader {            // 64 int32
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
 struct SimtItem {              // 4 int32
-  int32_t seg, tok_begin, ntok, v_off;  // v_off: float index of this item's fp32 v [ntok][rank]
+  int32_t seg, tok_begin;
+  int32_t nt_rank;             // ntok | rank << 16: the kernels need both before their first weight load
+  int32_t v_off;               // float index of this item's fp32 v [ntok][rank]
 };
+__host__ __device__ inline int simt_nt(const SimtItem& it) { return it.nt_rank & 0xffff; }
+__host__ __device__ inline int simt_rank(const SimtItem& it) { return it.nt_rank >> 16; }
+// The SIMT tail of a plan, after the items: the shrink's row-block prefix [n + 1] over the items
+// (8-row blocks of each item's group A), then one int per row block: item << 8 | row block.
 
 struct MTile {                 // 8 int32
   int32_t seg, tok_begin, ntok, rank;

@@ -25,7 +25,7 @@ __device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
 
 // Shrink: grid = (row blocks, 1, simt_ksplit(h_in)), block = 256: one block per (item, 8 rows of
 // the item's group A, G = nproj * rank rows, one range of h_in's 64-column chunks); the plan's
-// row-block prefix over the items maps blockIdx.x to (item, row block).  The 8
+// row-block map gives blockIdx.x's (item, row block) in one load.  The 8
 // warps split the range's chunks (warp w takes chunks w, w + 8, ...); lane = (row of 8, quarter of
 // a chunk), so a warp reads each chunk's 8 rows as 1 KB contiguous, four chunks in flight.
 // Quarters reduce by shuffle, warps through shared memory in a fixed order (deterministic).  The
@@ -33,25 +33,20 @@ __device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
 constexpr int kSimtUnroll = 4;
 __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                           int h_in, const int32_t* __restrict__ plan,
-                                                          int off_items, int n_items, int off_rank,
+                                                          int off_items, int n_items,
                                                           const void* const* __restrict__ a_ptrs,
                                                           float* __restrict__ simt_v, int nproj, int simt_stride) {
   __shared__ float red[8][8][kSimtMaxTok];   // [warp][row][token]
-  const int32_t* pre = plan + off_items + 4 * n_items;   // [n_items + 1] row-block prefix
-  int lo = 0, hi = n_items - 1;                          // last item with pre[item] <= blockIdx.x
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
-  }
-  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[lo];
-  const int rb = blockIdx.x - pre[lo];
-  const int r = plan[off_rank + it.seg], G = nproj * r;
+  const int m = plan[off_items + 5 * n_items + 1 + blockIdx.x];   // row-block map: item << 8 | row block
+  const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[m >> 8];
+  const int rb = m & 255;
+  const int r = simt_rank(it), G = nproj * r;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rl = lane >> 2, k = rb * 8 + rl, q4 = lane & 3;
   const uint8_t* arow = static_cast<const uint8_t*>(a_ptrs[it.seg]) + (size_t)k * 128;
   const uint32_t u0 = (uint32_t)((2 * q4) ^ (k & 7)) << 4, u1 = (uint32_t)((2 * q4 + 1) ^ (k & 7)) << 4;
   const size_t cstride = (size_t)G * 128;            // bytes between consecutive chunks of a row
-  const int nchunks = h_in / 64, nt = it.ntok, ks_n = gridDim.z;
+  const int nchunks = h_in / 64, nt = simt_nt(it), ks_n = gridDim.z;
   const int cps = (nchunks + ks_n - 1) / ks_n, cbeg = blockIdx.z * cps;
   const int chunks = min(nchunks, cbeg + cps);   // this split: chunks [cbeg, chunks)
   float acc[kSimtMaxTok];
@@ -132,7 +127,7 @@ struct SimtExpandArgs {          // every member of an input group (grid.z = mem
   const void* const* b_ptrs[kMaxProj];
   const float* v[kMaxProj];      // member's k-split-0 v region
   const int32_t* plan;
-  int off_items, n_items, off_rank, item0, ksplit;
+  int off_items, ksplit;
   int64_t split_stride;          // floats between k-split copies of the v regions
 };
 template <int NT>                // accumulator rows: tokens per pass over the item's B tile
@@ -140,13 +135,12 @@ __global__ void __launch_bounds__(128) simt_expand_kernel(const __grid_constant_
   __shared__ float vs[kSimtMaxTok * 256];
   const int m = blockIdx.z, h_out = a.h_out[m];
   if ((int)blockIdx.y * 256 >= h_out) return;    // block-uniform: past this member's columns
-  const int item = a.plan[a.off_items + 5 * a.n_items + 2 + a.item0 + blockIdx.x];   // expand order
-  const SimtItem it = reinterpret_cast<const SimtItem*>(a.plan + a.off_items)[item];
-  const int r = a.plan[a.off_rank + it.seg];
+  const SimtItem it = reinterpret_cast<const SimtItem*>(a.plan + a.off_items)[blockIdx.x];
+  const int r = simt_rank(it);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.y * 256 + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
   const bool active = blockIdx.y * 256 + warp * 64 < h_out;      // warp-uniform (h_out % 64 == 0)
-  const int ks = lane >> 3, nt = it.ntok;
+  const int ks = lane >> 3, nt = simt_nt(it);
   __nv_bfloat16* const y = a.y[m];
   const int64_t ldy = a.ldy[m];
   const uint8_t* b = static_cast<const uint8_t*>(a.b_ptrs[m][it.seg]);

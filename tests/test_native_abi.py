@@ -88,7 +88,9 @@ def test_plan_covers_every_chunk_and_tile(h_in, h_out):
     covered = np.zeros(d["N"], dtype=int)
     for seg, tb, nt, *_ in d["mtiles"]:
         covered[tb:tb + nt] += 1
-    for seg, tb, nt, _ in d["simt"]:
+    for seg, tb, nt_rank, _ in d["simt"]:       # nt_rank = ntok | rank << 16
+        nt = int(nt_rank) & 0xFFFF
+        assert int(nt_rank) >> 16 == ranks[seg]
         covered[tb:tb + nt] += 1
     assert np.all(covered == 1)
     assert d["tier"][3] == 0 and d["tier"][5] == 1 and d["tier"][7] == 2
