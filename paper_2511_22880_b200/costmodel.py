@@ -226,3 +226,50 @@ class MeasuredCost:
         if key not in self._cache:
             self._cache[key] = self._measure([1] * len(ranks), list(ranks))
         return self._cache[key]
+
+
+# ------------------------------------------------------------------------------------------
+class FittedCost:
+    """The B200 measurements as a closed form, usable where no GPU is (the reference simulator,
+    ``profile_operating_points`` costmodel.py:215-281; tools/measured_op_points.py).
+
+    tools/measure_cost_fit.py times the delta path (MeasuredCost, Llama-2-7B, every request its
+    own segment) and fits, per regime,
+        delta = t0 + k_tok * sum(lengths) + k_rank * sum(ranks)
+    (the path is HBM-bound and moves X*sum(n) + W*sum(r) bytes).  The prefill /
+    decode prices keep the reference's base-model terms and replace its max-rank multiplier
+    (costmodel.py:104-105, :121) with that additive rank-aware delta, the rank term divided by
+    ``tp`` like ``rank_factor`` (costmodel.py:69-70).  Same signatures and errors as the modelled
+    functions."""
+
+    def __init__(self, prefill_fit: dict, decode_fit: dict):
+        self.prefill_fit = dict(prefill_fit)
+        self.decode_fit = dict(decode_fit)
+
+    @classmethod
+    def from_json(cls, path=None) -> "FittedCost":
+        import json
+        from pathlib import Path
+        p = Path(path) if path else Path(__file__).resolve().parent.parent / "tests" / "golden" / "b200_delta_cost.json"
+        d = json.loads(p.read_text())
+        return cls(d["prefill_fit"], d["decode_fit"])
+
+    @staticmethod
+    def _delta(fit: dict, lengths: Sequence[int], ranks: Sequence[int], tp: int) -> float:
+        return max(0.0, fit["t0_s"] + fit["k_tok_s"] * sum(lengths) + fit["k_rank_s"] * sum(ranks) / tp)
+
+    def prefill_time(self, prompt_lengths: Sequence[int], ranks: Sequence[int], params: CostParams,
+                     resident_max_rank: int = 0) -> float:
+        """Base-model prefill + the fitted B200 delta; ``resident_max_rank`` has no effect (a
+        co-scheduled decode's rank does not slow this batch on the B200 path)."""
+        _check_batch(prompt_lengths, ranks, "prefill")
+        tokens = sum(prompt_lengths)
+        if tokens > params.token_budget:
+            raise ValueError(f"prefill batch of {tokens} tokens exceeds token budget {params.token_budget}")
+        return params.prefill_base_s + params.prefill_token_s * tokens + \
+            self._delta(self.prefill_fit, prompt_lengths, ranks, params.tp)
+
+    def decode_iter_time(self, context_lengths: Sequence[int], ranks: Sequence[int], params: CostParams) -> float:
+        _check_batch(context_lengths, ranks, "decode")
+        return params.decode_base_s + params.decode_ctx_s * sum(context_lengths) + \
+            self._delta(self.decode_fit, [1] * len(ranks), ranks, params.tp)

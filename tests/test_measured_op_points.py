@@ -1,0 +1,110 @@
+"""the measured B200 cost as a closed form (costmodel.FittedCost) and the operating
+points Algorithm 1 gets from it (tools/measured_op_points.py, which runs the reference's own
+profile_operating_points with that cost).  CPU only: fixtures tests/golden/b200_delta_cost.json
+(measured on a B200 by tools/measure_cost_fit.py) and tests/golden/op_points_b200.json."""
+
+import json
+import sys
+from pathlib import Path
+
+import pytest
+
+from paper_2511_22880_b200 import costmodel
+from paper_2511_22880_b200.domain import OperatingPointTable
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+REF = Path("/root/reference/pkg/src")
+
+
+def _load(name):
+    return json.loads((GOLDEN / name).read_text())
+
+
+def test_fit_reproduces_the_b200_samples():
+    d = _load("b200_delta_cost.json")
+    assert d["device"].startswith("NVIDIA B200")
+    fitted = costmodel.FittedCost.from_json()
+    for key, fit in (("prefill_samples", fitted.prefill_fit), ("decode_samples", fitted.decode_fit)):
+        for s in d[key]:
+            pred = costmodel.FittedCost._delta(fit, s["lengths"], s["ranks"], 1)
+            assert abs(pred - s["seconds"]) <= 0.25 * s["seconds"], (key, s["sum_len"], s["sum_rank"])
+    # physically sensible: non-negative per-token and per-rank costs (HBM bytes grow with both)
+    assert fitted.prefill_fit["k_tok_s"] >= 0 and fitted.prefill_fit["k_rank_s"] > 0
+    assert fitted.decode_fit["k_rank_s"] > 0
+
+
+def test_fitted_cost_keeps_the_reference_contract():
+    f = costmodel.FittedCost.from_json()
+    p = costmodel.CostParams()
+    with pytest.raises(ValueError):
+        f.prefill_time([], [], p)
+    with pytest.raises(ValueError):
+        f.prefill_time([1, 2], [8], p)
+    with pytest.raises(ValueError):
+        f.prefill_time([8192, 1], [8, 8], p)
+    with pytest.raises(ValueError):
+        f.decode_iter_time([], [], p)
+    # rank-aware: one high-rank request no longer prices the whole batch at max rank
+    mixed = f.prefill_time([256] * 8, [8] * 7 + [128], p)
+    low = f.prefill_time([256] * 8, [8] * 8, p)
+    assert (mixed - low) / low < 0.05
+    m_mixed = costmodel.prefill_time([256] * 8, [8] * 7 + [128], p)
+    m_low = costmodel.prefill_time([256] * 8, [8] * 8, p)
+    assert (m_mixed - m_low) / m_low > 1.0        # the reference's max-rank model: > 2x
+    # resident_max_rank has no effect on the B200 price
+    assert f.prefill_time([64], [8], p, resident_max_rank=128) == f.prefill_time([64], [8], p)
+
+
+def test_operating_points_from_the_b200_cost():
+    d = _load("op_points_b200.json")
+    modelled = OperatingPointTable({int(r): v for r, v in d["modelled"].items()})
+    measured = OperatingPointTable({int(r): v for r, v in d["b200_measured"].items()})
+    ranks = modelled.ranks()
+    assert ranks == measured.ranks() == [8, 16, 32, 64, 128]
+    # the max-rank penalty the paper removes: modelled capacity falls ~3x from r8 to r128,
+    # the B200-priced capacity does not fall by more than 10%
+    assert modelled[8] / modelled[128] > 2.5
+    assert measured[8] / measured[128] < 1.1
+    assert all(measured[r] >= modelled[r] for r in ranks)
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not present (GPU box)")
+def test_op_points_fixture_matches_a_fresh_reference_run():
+    """Pins the fixture: the reference's profile_operating_points with the fitted cost patched in
+    reproduces it exactly (deterministic simulator, seed 0)."""
+    d = _load("op_points_b200.json")
+    sys.path.insert(0, str(REF))
+    try:
+        import lorasim.costmodel as rcm
+        fitted = costmodel.FittedCost.from_json()
+        saved = (rcm.prefill_time, rcm.decode_iter_time)
+        rcm.prefill_time, rcm.decode_iter_time = fitted.prefill_time, fitted.decode_iter_time
+        try:
+            table = rcm.profile_operating_points(rcm.CostParams(), d["slo_seconds"], d["ranks"],
+                                                 duration_seconds=d["duration_seconds"], seed=d["seed"])
+        finally:
+            rcm.prefill_time, rcm.decode_iter_time = saved
+        assert {str(r): table[r] for r in table.ranks()} == d["b200_measured"]
+        ref_table = rcm.profile_operating_points(rcm.CostParams(), d["slo_seconds"], d["ranks"],
+                                                 duration_seconds=d["duration_seconds"], seed=d["seed"])
+        assert {str(r): ref_table[r] for r in ref_table.ranks()} == d["modelled"]
+    finally:
+        sys.path.remove(str(REF))
+
+
+def test_placement_consumes_the_measured_table():
+    """Algorithm 1 (placement.place_from_demand) with the B200 operating points: every adapter is
+    placed, fractions sum to 1, and flat capacities spread high-rank adapters like low-rank ones."""
+    from paper_2511_22880_b200 import placement, traces
+    from paper_2511_22880_b200.demand import DemandEstimate
+    d = _load("op_points_b200.json")
+    table = OperatingPointTable({int(r): v for r, v in d["b200_measured"].items()})
+    roster = traces.roster(100)
+    demand = DemandEstimate({a.id: 50.0 + 10.0 * (i % 7) for i, a in enumerate(roster)})
+    asg = placement.place_from_demand(list(range(4)), roster, demand, table)
+    per_adapter = {}
+    for server, items in asg.per_server.items():
+        for aid, phi in items:
+            per_adapter[aid] = per_adapter.get(aid, 0.0) + phi
+    assert set(per_adapter) == {a.id for a in roster}
+    assert all(abs(v - 1.0) < 1e-9 for v in per_adapter.values())
