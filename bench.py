@@ -552,8 +552,30 @@ def run_remote(args, rank, world, local_rank):
     sampler.start()
     ms_direct = time_graph(torch, eng, bp_remote, xs, ys, stream, args.steps, args.warmup, dev)
     clocks = sampler.stop()
-    t = torch.tensor([ms_local, ms_direct, float(identical and identical_pf), ms_pf], device=dev,
-                     dtype=torch.float64)
+    # copy-on-first-use (the reference's commit_migration): every peer-owned adapter this GPU's
+    # batch uses, copied once into a local slab by the copy engines; afterwards the batch runs
+    # all-local (ms_local).  Break-even: how many steps of direct peer loads the copy costs.
+    peer_aids = sorted({(wl.adapter_ids[int(sl)], int(o)) for sl, o in zip(seg.seg_slot, owner) if int(o) != rank})
+    mig = AdapterSlab(model, AdapterSlab.capacity_for(model, [wl.ranks[wl.adapter_ids.index(a)] for a, _ in peer_aids]), dev)
+    torch.cuda.synchronize(dev)
+    torch.distributed.barrier()
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record(stream)
+    for aid, o in peer_aids:
+        mig.migrate_from_peer(aid, peers[o], stream)
+    m1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_mig = m0.elapsed_time(m1)
+    mig_bytes = sum(mig.slots[sl].nbytes for sl in mig.by_id.values())
+    L_, P_ = model.layers - 1, len(model.projections) - 1   # the slot's last bytes: A and B of the last layer
+
+    def _same(aid):
+        (a1, b1), (a2, b2) = mig.read(mig.by_id[aid], L_, P_), slab.read(slab.by_id[aid], L_, P_)
+        return torch.equal(a1, a2) and torch.equal(b1, b2)
+    mig_identical = all(_same(a) for a, _ in peer_aids[:4])
+    del mig
+    t = torch.tensor([ms_local, ms_direct, float(identical and identical_pf and mig_identical), ms_pf, ms_mig,
+                      float(mig_bytes)], device=dev, dtype=torch.float64)
     per = [torch.zeros_like(t) for _ in range(world)]
     torch.distributed.all_gather(per, t)
     per = [p.tolist() for p in per]
@@ -580,6 +602,11 @@ def run_remote(args, rank, world, local_rank):
                                     f"local staging while the current layer computes; {pf.bytes_per_layer / 1e6:.1f} "
                                     f"MB/layer over NVLink on GPU {rank}"},
         "all_local": {"ms_per_step": ms_l, "value": N * world / (ms_l / 1e3)},
+        "remote_migration": {"mode": "copy-on-first-use: every peer-owned adapter of the batch copied once into a "
+                                     "local slot (AdapterSlab.migrate_from_peer, lsv_copy_blocks over NVLink)",
+                             "ms": max(p[4] for p in per), "bytes_per_gpu": [int(p[5]) for p in per],
+                             "GBps": min(p[5] / (p[4] * 1e-3) / 1e9 for p in per),
+                             "break_even_steps": max(p[4] for p in per) / max(ms_r - ms_l, 1e-9)},
         "step_hbm": {"frac_local_bytes": step_bytes / (ms_r * 1e-3) / 1e9 / hbm_peak},
         "clocks": clocks,
     }

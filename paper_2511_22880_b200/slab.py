@@ -141,6 +141,20 @@ class AdapterSlab:
                 self.load(slot, layer, proj, a.to(self.device, non_blocking=True),
                           b.to(self.device, non_blocking=True), st)
 
+    def migrate_from_peer(self, adapter_id: str, peer: "AdapterSlab", stream: torch.cuda.Stream | None = None) -> int:
+        """Copy-on-first-use of a peer-owned adapter (the reference's commit_migration,
+        pool.py:134-162: the target becomes a holder): a local slot of the same rank, filled by one
+        copy-engine transfer of the peer slot's bytes over NVLink (slots of one model share their
+        internal layout, so the bytes move verbatim).  Returns the local slot."""
+        ps = peer.slots[peer.by_id[adapter_id]]
+        slot = self.allocate(adapter_id, ps.rank)
+        dst = self.slots[slot]
+        st = stream or torch.cuda.current_stream(self.device)
+        native.check(native.lib().lsv_copy_blocks(
+            1, (ctypes.c_void_p * 1)(peer.base + ps.offset), (ctypes.c_void_p * 1)(self.base + dst.offset),
+            (ctypes.c_size_t * 1)(ps.nbytes), st.cuda_stream))
+        return slot
+
     def a_offset(self, slot: int, layer: int, proj: int) -> int:
         """Offset of proj's first A row inside its group tile (rows repeat every group*rank rows)."""
         return int(self._a_off_rows[slot][layer, proj])

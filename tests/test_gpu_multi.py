@@ -81,3 +81,35 @@ def test_remote_prefetch_forward_bit_identical():
         for p in model.projections:
             assert torch.equal(ya[layer][p.name], yb[layer][p.name]), (layer, p.name)
     assert pf.bytes_per_layer > 0
+
+
+def test_migrate_from_peer_bit_identical():
+    """Copy-on-first-use (the reference's commit_migration, pool.py:134-162): a peer-owned adapter
+    copied into a local slot verbatim (one copy-engine transfer over NVLink) unpacks to the same
+    weights and gives the oracle's delta, whatever local slot order the copies land in."""
+    from paper_2511_22880_b200 import native
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.slab import AdapterSlab
+    native.check(native.lib().lsv_enable_peer(0, 1))
+    case = Case(4096, 4096, [64, 41, 200, 5, 130], [128, 8, 32, 16, 64], seed=23)
+    peer = AdapterSlab(case.model, AdapterSlab.capacity_for(case.model, case.ranks), "cuda:1")
+    for s, r in enumerate(case.ranks):
+        peer.load(peer.allocate(f"a{s}", r), 0, 0, case.a[s].to("cuda:1"), case.b[s].to("cuda:1"))
+    torch.cuda.synchronize("cuda:1")
+    local = AdapterSlab(case.model, AdapterSlab.capacity_for(case.model, case.ranks), "cuda:0")
+    # migrate in a different order than the peer's slots: offsets differ, bytes move verbatim
+    for s in reversed(range(len(case.ranks))):
+        local.migrate_from_peer(f"a{s}", peer)
+    torch.cuda.synchronize("cuda:0")
+    for s in range(len(case.ranks)):
+        a0, b0 = local.read(local.by_id[f"a{s}"], 0, 0)
+        assert torch.equal(a0.cpu(), case.a[s]) and torch.equal(b0.cpu(), case.b[s])
+    seg = case.seg
+    seg.seg_slot[:] = [local.by_id[f"a{s}"] for s in range(len(case.ranks))]
+    eng = LoraDeltaEngine(local)
+    y = torch.zeros(case.n_tok, 4096, dtype=torch.bfloat16, device="cuda:0")
+    eng.apply(eng.prepare(seg), 0, 0, case.x.to("cuda:0"), y)
+    torch.cuda.synchronize("cuda:0")
+    from oracle import oracle
+    err = oracle.max_rel_err(y.float().cpu().numpy()[:seg.num_tokens], case.oracle_delta()[:seg.num_tokens])
+    assert err <= 1e-2
