@@ -94,7 +94,10 @@ constexpr int kShrinkMaxKch = LSV_SHRINK_MAX_KCH;   // 64-column chunks per pipe
 constexpr int kShrinkSlotBytes = LSV_SHRINK_SLOT_KB * 1024;
 constexpr int kShrinkSlots = LSV_SHRINK_SLOTS;
 constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past short token tiles
-constexpr int kExpandRingBytes = 200 * 1024;   // variable-size items, allocated in issue order
+#ifndef LSV_EXPAND_RING_KB
+#define LSV_EXPAND_RING_KB 200
+#endif
+constexpr int kExpandRingBytes = LSV_EXPAND_RING_KB * 1024;   // variable-size items, allocated in issue order
 constexpr int kExpandGuardBytes = 2 * 1024;    // rank-8 K=16 MMA reads one k-core past its tile
 constexpr int kExpandInflight = 8;
 // SIMT shrink k-splits: h_in's 64-column chunks are split into ~32-chunk ranges (four per warp), one

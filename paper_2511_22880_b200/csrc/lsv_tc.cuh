@@ -157,7 +157,10 @@ struct WarpRecStream {
 };
 
 constexpr int kShrinkRecCh = 16;
-constexpr int kExpandRecCh = 32;
+#ifndef LSV_EXPAND_RECCH
+#define LSV_EXPAND_RECCH 32
+#endif
+constexpr int kExpandRecCh = LSV_EXPAND_RECCH;
 using ShrinkRecBuf = WarpRecBuf<ShrinkRec, kShrinkRecCh>;
 using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
 
