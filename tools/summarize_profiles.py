@@ -14,6 +14,11 @@ from collections import OrderedDict
 
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1e"
 OUT = sys.argv[2] if len(sys.argv) > 2 else TAG
+DECODE = len(sys.argv) > 3 and sys.argv[3] == "decode"
+WL = ("decode (C2 roster, 128 requests x 1 token, 73 active adapters; SIMT tier)" if DECODE else
+      "config 2 (Llama-2-7B shapes, 100 adapters, 4096 tokens)")
+CMD = "python bench.py --config decode --steps 1 --warmup 3 --no-cpu-baseline" if DECODE else \
+      "python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 GROUPS = ["attn_in (q/k/v fused)", "attn_out (o)", "mlp_in (gate/up fused)", "mlp_mid (down)"]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
@@ -30,7 +35,7 @@ def launches():
     scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}
     out = [(r["Kernel Name"].split("(")[0], float(r["Metric Value"].replace(",", "")) * scale[r["Metric Unit"]])
            for r in rows]
-    with open(f"profiles/{OUT}_launches_c2_step.csv", "w") as f:
+    with open(f"profiles/{OUT}_launches{'' if DECODE else '_c2'}_step.csv", "w") as f:
         f.write("launch,kernel,us\n")
         for i, (k, us) in enumerate(out):
             f.write(f"{i},{k},{us:.3f}\n")
@@ -39,14 +44,13 @@ def launches():
         n, t = agg.get(k, (0, 0.0))
         agg[k] = (n + 1, t + us)
     total = sum(t for _, t in agg.values())
-    lines = ["# ncu launch list, config 2 (Llama-2-7B shapes, 100 adapters, 4096 tokens), warm-up + one bench.py step",
+    lines = [f"# ncu launch list, {WL}, warm-up + one bench.py step",
              "# command: ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'tc_kernel|simt_|vimg' "
-             "-c 700 --csv \\",
-             "#          python bench.py --steps 1 --warmup 3 --no-cpu-baseline   (after the same command exited 0 "
-             "without ncu)",
+             "--csv \\",
+             f"#          {CMD}   (after the same command exited 0 without ncu)",
              "# ncu serialises launches and replays with cold caches: absolute times run above the CUDA-graph step;",
              "# the per-kernel SHARE of the step is what to compare.  Full list: "
-             f"profiles/{OUT}_launches_c2_step.csv", "",
+             f"profiles/{OUT}_launches{'' if DECODE else '_c2'}_step.csv", "",
              f"{'kernel':20s} {'launches':>8s} {'total_us':>10s} {'mean_us':>9s} {'share':>7s}"]
     for k, (n, t) in agg.items():
         lines.append(f"{k:20s} {n:8d} {t:10.1f} {t / n:9.2f} {t / total:7.3f}")
@@ -71,11 +75,17 @@ def full():
     rows = list(csv.reader(io.StringIO(raw[raw.index('"ID"'):])))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
-    lines = ["# ncu --set full --clock-control none --import-source on -k regex:'tc_kernel|simt_' -s 4 -c 2 "
-             "python tools/prof_one.py 2",
-             "# config 2, layer-0 mlp_in group: fused gate/up shrink + one-launch gate/up expand (the step's "
-             "largest pair);",
-             "# run only after `python tools/prof_one.py 2` exited 0 without ncu.  Cold-cache, serialised replay.", ""]
+    if DECODE:
+        lines = ["# ncu --set full --clock-control none --import-source on -k regex:'simt_' -s 16 -c 2 "
+                 "python tools/decode_one.py 128",
+                 "# decode batch (128 requests x 1 token), 2-layer Llama-2-7B: the 17th-18th SIMT launches",
+                 "# run only after `python tools/decode_one.py 128` exited 0 without ncu.  Cold-cache, serialised.", ""]
+    else:
+        lines = ["# ncu --set full --clock-control none --import-source on -k regex:'tc_kernel|simt_' -s 4 -c 2 "
+                 "python tools/prof_one.py 2",
+                 "# config 2, layer-0 mlp_in group: fused gate/up shrink + one-launch gate/up expand (the step's "
+                 "largest pair);",
+                 "# run only after `python tools/prof_one.py 2` exited 0 without ncu.  Cold-cache, serialised replay.", ""]
     traffic = {}
     for r in data:
         name = r[col["Kernel Name"]].split("(")[0]
@@ -90,8 +100,10 @@ def full():
         lines.append(f"  dram read+write bytes per launch: {b / 1e6:.1f} MB")
         lines.append("")
         traffic[name] = b
-    open(f"profiles/{OUT}_ncu_full_mlp_in.txt", "w").write("\n".join(lines) + "\n")
+    open(f"profiles/{OUT}_ncu_full{'' if DECODE else '_mlp_in'}.txt", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
+    if DECODE:
+        return
     tj = json.load(open("profiles/traffic_r1.json"))
     for k in tj["c2"]:
         kern = k.split(" ")[0]
