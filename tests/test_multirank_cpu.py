@@ -60,3 +60,20 @@ def test_dp_placement_consistent_across_ranks():
     wls = synth.dp_workloads(world)
     assert set(res[0][3]) | set(res[1][3]) == {a for w in wls for a in w.resident}
     assert all(w.segments.num_tokens <= 4096 for w in wls)
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_dp_workloads_at_scale(world):
+    """The driver's scaling run goes to 8 GPUs (gpurun reaches 4): every rank's batch is non-empty
+    and within the token budget, every segment's adapter is resident on that rank, and weak
+    scaling keeps tokens per GPU fixed."""
+    from paper_2511_22880_b200 import shapes, synth
+    for model in (shapes.LLAMA2_7B, shapes.LLAMA2_13B):
+        wls = synth.dp_workloads(world, model=model)
+        assert len(wls) == world
+        toks = {w.segments.num_tokens for w in wls}
+        assert len(toks) == 1 and 0 < toks.pop() <= 4096
+        for w in wls:
+            assert w.segments.num_segments > 0
+            used = {w.adapter_ids[int(s)] for s in w.segments.seg_slot}
+            assert used <= set(w.resident)
