@@ -324,7 +324,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   // SIMT tail (lsv_plan.h): row-block prefix [n + 1], row-block map [n_rb]
   if (h.n_simt_items > 0) {
     int n_rb = 0;
-    for (const SimtItem& it : pb.simt) n_rb += P * simt_rank(it) / 8;
+    for (const SimtItem& it : pb.simt) n_rb += (P * simt_rank(it) + kSimtShrRows - 1) / kSimtShrRows;
     off += h.n_simt_items + 1 + n_rb;
   }
   off = round_up(off, 4);
@@ -711,7 +711,7 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
     int32_t* rbmap = pre + n + 1;
     pre[0] = 0;
     for (int i = 0; i < n; ++i) {
-      const int nrb = h.num_proj * simt_rank(pb.simt[i]) / 8;
+      const int nrb = (h.num_proj * simt_rank(pb.simt[i]) + kSimtShrRows - 1) / kSimtShrRows;
       for (int rb = 0; rb < nrb; ++rb) rbmap[pre[i] + rb] = i << 8 | rb;
       pre[i + 1] = pre[i] + nrb;
     }

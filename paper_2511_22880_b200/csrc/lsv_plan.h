@@ -54,6 +54,10 @@ struct SimtItem {              // 4 int32
   int32_t nt_rank;             // ntok | rank << 16: the kernels need both before their first weight load
   int32_t v_off;               // float index of this item's fp32 v [ntok][rank]
 };
+#ifndef LSV_SIMT_SHR_ROWS
+#define LSV_SIMT_SHR_ROWS 16
+#endif
+constexpr int kSimtShrRows = LSV_SIMT_SHR_ROWS;   // group-A rows per SIMT shrink block (8 or 16)
 __host__ __device__ inline int simt_nt(const SimtItem& it) { return it.nt_rank & 0xffff; }
 __host__ __device__ inline int simt_rank(const SimtItem& it) { return it.nt_rank >> 16; }
 // The SIMT tail of a plan, after the items: the shrink's row-block prefix [n + 1] over the items

@@ -31,36 +31,50 @@ __device__ __forceinline__ float dot8_bf16(const uint4& a, const uint4& b) {
 // Quarters reduce by shuffle, warps through shared memory in a fixed order (deterministic).  The
 // split's partial v (fp32) lands in its own copy of the row's projection region.
 constexpr int kSimtUnroll = 4;
+#ifndef LSV_SIMT_SHR_UNROLL
+#define LSV_SIMT_SHR_UNROLL (LSV_SIMT_SHR_ROWS == 8 ? 4 : 2)
+#endif
+constexpr int kShrRH = kSimtShrRows / 8;          // 8-row halves per block; a lane owns row rl of each
+constexpr int kShrU = LSV_SIMT_SHR_UNROLL;        // chunks in flight per warp
 __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                           int h_in, const int32_t* __restrict__ plan,
                                                           int off_items, int n_items,
                                                           const void* const* __restrict__ a_ptrs,
                                                           float* __restrict__ simt_v, int nproj, int simt_stride) {
-  __shared__ float red[8][8][kSimtMaxTok];   // [warp][row][token]
+  __shared__ float red[8][kSimtShrRows][kSimtMaxTok];   // [warp][row][token]
   const int m = plan[off_items + 5 * n_items + 1 + blockIdx.x];   // row-block map: item << 8 | row block
   const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[m >> 8];
   const int rb = m & 255;
   const int r = simt_rank(it), G = nproj * r;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rl = lane >> 2, k = rb * 8 + rl, q4 = lane & 3;
+  const int rl = lane >> 2, k = rb * kSimtShrRows + rl, q4 = lane & 3;
   const uint8_t* arow = static_cast<const uint8_t*>(a_ptrs[it.seg]) + (size_t)k * 128;
+  // row k + 8h has the same swizzle phase as row k
   const uint32_t u0 = (uint32_t)((2 * q4) ^ (k & 7)) << 4, u1 = (uint32_t)((2 * q4 + 1) ^ (k & 7)) << 4;
+  bool half_ok[kShrRH];
+#pragma unroll
+  for (int h = 0; h < kShrRH; ++h) half_ok[h] = rb * kSimtShrRows + 8 * h < G;   // block-uniform
   const size_t cstride = (size_t)G * 128;            // bytes between consecutive chunks of a row
   const int nchunks = h_in / 64, nt = simt_nt(it), ks_n = gridDim.z;
   const int cps = (nchunks + ks_n - 1) / ks_n, cbeg = blockIdx.z * cps;
   const int chunks = min(nchunks, cbeg + cps);   // this split: chunks [cbeg, chunks)
-  float acc[kSimtMaxTok];
+  float acc[kShrRH][kSimtMaxTok];
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t) acc[t] = 0.f;
-  uint4 a0[kSimtUnroll], a1[kSimtUnroll];
+  for (int h = 0; h < kShrRH; ++h)
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) acc[h][t] = 0.f;
+  uint4 a0[kShrU][kShrRH], a1[kShrU][kShrRH];
   auto load = [&](int c0) {
 #pragma unroll
-    for (int u = 0; u < kSimtUnroll; ++u) {
+    for (int u = 0; u < kShrU; ++u) {
       const int c = c0 + 8 * u;
-      if (c < chunks) {
-        const uint8_t* ap = arow + (size_t)c * cstride;
-        a0[u] = __ldg(reinterpret_cast<const uint4*>(ap + u0));
-        a1[u] = __ldg(reinterpret_cast<const uint4*>(ap + u1));
+#pragma unroll
+      for (int h = 0; h < kShrRH; ++h) {
+        if (c < chunks && half_ok[h]) {
+          const uint8_t* ap = arow + (size_t)c * cstride + h * 8 * 128;
+          a0[u][h] = __ldg(reinterpret_cast<const uint4*>(ap + u0));
+          a1[u][h] = __ldg(reinterpret_cast<const uint4*>(ap + u1));
+        }
       }
     }
   };
@@ -69,10 +83,10 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   // the v partials are touched only after it has completed.  A no-op for a normal launch.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kSimtUnroll) {
+  for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kShrU) {
     if (c0 != cbeg + warp) load(c0);
 #pragma unroll
-    for (int u = 0; u < kSimtUnroll; ++u) {
+    for (int u = 0; u < kShrU; ++u) {
       const int c = c0 + 8 * u;
       if (c < chunks) {
         const int col = c * 64 + q4 * 16;
@@ -80,25 +94,32 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
         for (int t = 0; t < kSimtMaxTok; ++t) {
           if (t < nt) {
             const uint4* xp = reinterpret_cast<const uint4*>(x + (int64_t)(it.tok_begin + t) * ldx + col);
-            acc[t] += dot8_bf16(a0[u], __ldg(xp)) + dot8_bf16(a1[u], __ldg(xp + 1));
+            const uint4 x0 = __ldg(xp), x1 = __ldg(xp + 1);   // one x load feeds every row half
+#pragma unroll
+            for (int h = 0; h < kShrRH; ++h)
+              if (half_ok[h]) acc[h][t] += dot8_bf16(a0[u][h], x0) + dot8_bf16(a1[u][h], x1);
           }
         }
       }
     }
   }
 #pragma unroll
-  for (int t = 0; t < kSimtMaxTok; ++t) {
-    acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 1);
-    acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 2);
-  }
+  for (int h = 0; h < kShrRH; ++h)
+#pragma unroll
+    for (int t = 0; t < kSimtMaxTok; ++t) {
+      acc[h][t] += __shfl_xor_sync(0xffffffffu, acc[h][t], 1);
+      acc[h][t] += __shfl_xor_sync(0xffffffffu, acc[h][t], 2);
+    }
   if (q4 == 0) {
 #pragma unroll
-    for (int t = 0; t < kSimtMaxTok; ++t) red[warp][rl][t] = acc[t];
+    for (int h = 0; h < kShrRH; ++h)
+#pragma unroll
+      for (int t = 0; t < kSimtMaxTok; ++t) red[warp][8 * h + rl][t] = acc[h][t];
   }
   __syncthreads();
-  if (threadIdx.x < 8 * kSimtMaxTok) {
-    const int row = threadIdx.x / kSimtMaxTok, t = threadIdx.x % kSimtMaxTok, kk = rb * 8 + row;
-    if (t < nt) {
+  if (threadIdx.x < kSimtShrRows * kSimtMaxTok) {
+    const int row = threadIdx.x / kSimtMaxTok, t = threadIdx.x % kSimtMaxTok, kk = rb * kSimtShrRows + row;
+    if (t < nt && kk < G) {
       float sum = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) sum += red[w][row][t];
@@ -107,8 +128,8 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   }
 }
 
-// Expand: grid = (items of one token class, ceil(max h_out / 256), members), block = 128 (warp w:
-// 64 columns of the 256); one launch per token class (<= kSimtSmallTok tokens, the rest).
+// Expand: grid = (items, ceil(max h_out / 256), members), block = 128 (warp w: 64 columns of the
+// 256); one launch per input group.
 // Lane = (k row of 4, 16-byte unit of 8 columns): a warp reads four 128-byte B atom rows per
 // load.  The item's v (<= 8 tokens x rank fp32) is staged in shared memory once, summing the
 // shrink's k-split partials in split order, and the B loads are double-buffered (round i+1's
