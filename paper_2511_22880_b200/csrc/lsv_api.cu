@@ -63,10 +63,14 @@ constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (b
 #define LSV_EXPAND_ITEM_FIXED_KB 8
 #endif
 #ifndef LSV_SHRINK_REC_FIXED_KB
-#define LSV_SHRINK_REC_FIXED_KB 24
+#define LSV_SHRINK_REC_FIXED_KB 64
 #endif
 constexpr int64_t kExpandItemFixed = (int64_t)LSV_EXPAND_ITEM_FIXED_KB * 1024;
 constexpr int64_t kShrinkRecFixed = (int64_t)LSV_SHRINK_REC_FIXED_KB * 1024;
+#ifndef LSV_SHRINK_STAGE_FIXED_KB
+#define LSV_SHRINK_STAGE_FIXED_KB 96
+#endif
+constexpr int64_t kShrinkStageFixed = (int64_t)LSV_SHRINK_STAGE_FIXED_KB * 1024;
 
 int num_sms_cached() {
   static int sms = -1;
@@ -252,9 +256,13 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         rc.kch = kch; rc.split = sp;
         rc.nsplit = nsplit; rc.part_off = mt.part_off; rc.vimg_off = mt.vimg_off; rc.counter = mt.counter;
         rc.mtile = (int32_t)i; rc.p0 = p0; rc.np = np;
-        // bytes moved + a fixed per-item cost (pipeline fill, epilogue, split reduction)
+        // bytes moved + a fixed cost per pipeline stage and per record (pipeline fill, epilogue,
+        // split partials).  Measured per CTA (tools/shrink_balance.py), a stage costs a near
+        // fixed share of the load latency whatever its size (the ring holds 3), so stage counts
+        // predict a CTA's time better than its bytes.
+        const int nstage = (rc.chunk_end - rc.chunk_begin + kch - 1) / kch;
         const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + kShrinkRecFixed +
-                             (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0);
+                             kShrinkStageFixed * nstage + (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0);
         shrink_costed.push_back({cost, rc});
       }
     }
