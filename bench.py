@@ -165,28 +165,43 @@ def host_layer_inputs(wl, seed=0):
 
 
 def run_reference(args, rank):
-    """--impl reference: the CPU restatement on the host cores, bounded sample per step."""
-    from paper_2511_22880_b200 import synth
+    """--impl reference: the CPU restatement on the host cores, bounded sample per step.  Same
+    workload as our arm: under torchrun (N > 1) that is the data-parallel job (one LoRAServe-routed
+    batch per GPU), which rank 0 runs on its host cores batch after batch."""
+    from paper_2511_22880_b200 import shapes as _shapes, synth
     if rank != 0:
         return None
-    wl = synth.WORKLOADS[args.config]()
-    xs, ads = host_layer_inputs(wl)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    config = args.config if not (world > 1 and args.config == "c2") else "dp"
+    if config in ("dp", "c3"):
+        wls = synth.dp_workloads(world, model=_shapes.LLAMA2_13B if config == "c3" else _shapes.LLAMA2_7B)
+    else:
+        wls = [synth.WORKLOADS[config]()]
+    wl = wls[0]
+    inputs = [host_layer_inputs(w) for w in wls]
     layers = wl.model.layers
+    tokens = sum(w.segments.num_tokens for w in wls)
     per_step = []
     for i in range(args.warmup + args.steps):
-        t_layer, _, threads = cpu_layer_sample(wl, xs, ads, budget_s=0.0)  # one layer per step
+        t_layer = 0.0
+        for w, (xs, ads) in zip(wls, inputs):       # one layer of every batch per step
+            t, _, threads = cpu_layer_sample(w, xs, ads, budget_s=0.0)
+            t_layer += t
         if i >= args.warmup:
             per_step.append(t_layer)
     t_layer = statistics.median(per_step)
-    value = wl.segments.num_tokens / (t_layer * layers)
+    value = tokens / (t_layer * layers)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * layers * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in, fp32 accumulate",
-        "data": "synthetic", "config": {"workload": wl.description, "sample": "1 layer per step, x layers"},
+        "data": "synthetic",
+        "config": {"workload": wl.description if len(wls) == 1 else
+                   f"{config}: {len(wls)} per-GPU batches ({wl.model.name}, LoRAServe placement + routing)",
+                   "config": config, "sample": "1 layer per step of every batch, x layers"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"1 of {layers} layers (all {len(wl.model.projections)} projections) per step, "
-                                   f"extrapolated x{layers}"},
+                         "sample": f"1 of {layers} layers (all {len(wl.model.projections)} projections) of "
+                                   f"{len(wls)} batch(es) per step, extrapolated x{layers}"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
