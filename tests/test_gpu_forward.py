@@ -118,3 +118,43 @@ def test_stream_prepared_plans_ring_and_staleness():
     with pytest.raises(RuntimeError, match="stale"):
         run(plans[0])
     run(plans[-1])   # the newest one is still live
+
+
+def test_decode_groups_simt_ksplit_against_oracle():
+    """Decode-shaped batch (1-5 tokens per adapter) through lsv_lora_forward on a full-width
+    layer (h = 4096, inter = 11008): the SIMT tier's group shrinks (q/k/v: N = 3r rows in 16-row
+    blocks that straddle members) with several k-splits (2 for h_in 4096, 5 for 11008), and the
+    one-launch multi-member expands, against the oracle for every projection."""
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+    from paper_2511_22880_b200.slab import AdapterSlab
+    dev = torch.device("cuda:0")
+    model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections)
+    ranks = [8, 24, 128, 64, 16, 40, 256, 8]
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+    for i, r in enumerate(ranks):
+        slab.fill_random(slab.allocate(f"d{i}", r), 900 + i)
+    tok = np.concatenate([np.full(n, s) for s, n in enumerate([1, 2, 5, 1, 3, 1, 2, 4])])
+    np.random.default_rng(3).shuffle(tok)
+    seg = index_tokens(tok, ranks)
+    eng = LoraDeltaEngine(slab)
+    bp = eng.prepare(seg)
+    assert all(gp.summary[5] == 0 for gp in bp.group_plans)   # every segment on the SIMT tier
+    N = seg.num_tokens
+    g = torch.Generator().manual_seed(31)
+    xs = [{name: torch.randn(N, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16).to(dev)
+           for name, m in model.groups()}]
+    ys = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device=dev) for p in model.projections}]
+    eng.forward(bp, xs, ys)
+    torch.cuda.synchronize()
+    for p, pr in enumerate(model.projections):
+        a_list, b_list = [], []
+        for slot in seg.seg_slot:
+            a, b = slab.read(int(slot), 0, p)
+            a_list.append(bf16_bits(a.cpu()))
+            b_list.append(bf16_bits(b.cpu()))
+        x = xs[0][[n for n, m in model.groups() if p in m][0]]
+        ref = oracle.delta_c(bf16_bits(x.cpu()), seg.seg_indptr, seg.seg_rank, a_list, b_list, pr.h_out)
+        err = oracle.max_rel_err(ys[0][pr.name].float().cpu().numpy()[:N], ref[:N])
+        assert err <= TOL, (pr.name, err)
