@@ -142,3 +142,22 @@ def test_decode_regime_simt(h_in, h_out):
     assert s[5] == 0   # every segment on the SIMT tier
     outs, _ = case.run_gpu(repeat=2)
     assert torch.equal(outs[0], outs[1])   # deterministic k-split sums
+
+
+def test_full_token_budget_batch():
+    """The reference's token budget (CostParams.token_budget = 8192, costmodel.py:54): a batch of
+    8192 tokens over 60 power-law adapters on the gate projection shape."""
+    rng = np.random.default_rng(40)
+    ranks = [8] * 26 + [16] * 13 + [32] * 9 + [64] * 7 + [128] * 5
+    lengths = np.bincount(rng.integers(0, len(ranks), 8192), minlength=len(ranks)).tolist()
+    case = Case(4096, 11008, lengths, ranks, seed=40)
+    err, bp = _check(case)
+    assert bp.shape_plans[(4096, 11008)].summary[1] == 8192
+
+
+def test_one_adapter_owns_the_whole_batch():
+    """A single rank-128 adapter over 8192 tokens: 64 m-tiles of one segment (every tile the same
+    B tiles; split-K over the same A for each), on the down projection shape."""
+    case = Case(11008, 4096, [8192], [128], seed=41)
+    err, bp = _check(case)
+    assert bp.shape_plans[(11008, 4096)].summary[5] == 64
