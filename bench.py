@@ -722,6 +722,21 @@ def run_tp(args, rank, world, local_rank):
     t = torch.tensor([ms, coll_ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, coll_ms = t.tolist()
+    # algorithmic HBM bytes per GPU per step of ideal S-LoRA sharding (unpadded ranks; SURVEY 8d
+    # per shard: x once per projection, the rank- or h_in-shard of A, the h_out shard of B and y)
+    from paper_2511_22880_b200.tp import COLUMN_PARALLEL
+    n_s = seg.lengths().astype(np.float64)
+    r_s = seg.seg_rank.astype(np.float64)
+    per_layer = 0.0
+    for pr in model.projections:
+        ho = pr.h_out / world
+        if pr.name in COLUMN_PARALLEL:     # x full, A rank-shard
+            per_layer += np.sum(2 * n_s * pr.h_in + 2 * (r_s / world) * pr.h_in + 2 * r_s * ho + 4 * n_s * ho)
+        else:                              # x and A h_in-shards
+            hi = pr.h_in / world
+            per_layer += np.sum(2 * n_s * hi + 2 * r_s * hi + 2 * r_s * ho + 4 * n_s * ho)
+    gpu_bytes = per_layer * model.layers
+    hbm_peak, peak_src = peaks()
     if rank != 0:
         return None
     return {
@@ -733,6 +748,11 @@ def run_tp(args, rank, world, local_rank):
                                f"{seg.num_segments} active", "config": "tp",
                    "timing": timing},
         "nccl_ms_per_step": coll_ms, "nccl_share": coll_ms / ms,
+        "step_hbm": {"algorithmic_bytes_per_gpu": gpu_bytes, "achieved_GBs_per_gpu": gpu_bytes / (ms * 1e-3) / 1e9,
+                     "peak": hbm_peak, "peak_source": peak_src,
+                     "frac": gpu_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+                     "note": "ideal S-LoRA sharding with unpadded ranks; the implementation pads column-group "
+                             "ranks to a multiple of 8*TP (DESIGN.md section 8, item 5)"},
         "exchange": ("column groups (q/k/v, gate/up): shrink epilogue stores each shard into every rank's full-rank "
                      "v image over NVLink + flag (no NCCL); row groups (o, down): NCCL all-reduce") if fused
                     else "NCCL all-gather (column groups) / all-reduce (row groups)",
