@@ -591,12 +591,12 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
       a.h_out[i] = h->h_outs[pp];
       a.b_ptrs[i] = b_ptrs[i];
       a.v[i] = reinterpret_cast<const float*>(ws + h->ws_simt_v) + (size_t)pp * h->simt_stride;
-      max_tiles = std::max(max_tiles, (h->h_outs[pp] + 255) / 256);
+      max_tiles = std::max(max_tiles, (h->h_outs[pp] + kSimtExpCols - 1) / kSimtExpCols);
     }
     a.plan = plan; a.off_items = h->off_simt_items;
     a.ksplit = simt_ksplit(h->h_in); a.split_stride = (int64_t)h->num_proj * h->simt_stride;
     // one launch: the small accumulator; larger items (rare in decode) in token-pair passes
-    LSV_CUDA_CHECK(launch_pdl_any(simt_expand_kernel<kSimtSmallTok>, dim3(h->n_simt_items, max_tiles, np), 128, st,
+    LSV_CUDA_CHECK(launch_pdl_any(simt_expand_kernel<kSimtSmallTok>, dim3(h->n_simt_items, max_tiles, np), kSimtExpThreads, st,
                                   simt_pdl, a));
   }
   const bool all = np == h->num_proj && np > 1;

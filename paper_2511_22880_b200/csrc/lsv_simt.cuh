@@ -151,16 +151,21 @@ struct SimtExpandArgs {          // every member of an input group (grid.z = mem
   int off_items, ksplit;
   int64_t split_stride;          // floats between k-split copies of the v regions
 };
+#ifndef LSV_SIMT_EXP_COLS
+#define LSV_SIMT_EXP_COLS 256
+#endif
+constexpr int kSimtExpCols = LSV_SIMT_EXP_COLS;            // h_out columns per block (64 per warp)
+constexpr int kSimtExpThreads = kSimtExpCols / 64 * 32;
 template <int NT>                // accumulator rows: tokens per pass over the item's B tile
-__global__ void __launch_bounds__(128) simt_expand_kernel(const __grid_constant__ SimtExpandArgs a) {
+__global__ void __launch_bounds__(kSimtExpThreads) simt_expand_kernel(const __grid_constant__ SimtExpandArgs a) {
   __shared__ float vs[kSimtMaxTok * 256];
   const int m = blockIdx.z, h_out = a.h_out[m];
-  if ((int)blockIdx.y * 256 >= h_out) return;    // block-uniform: past this member's columns
+  if ((int)blockIdx.y * kSimtExpCols >= h_out) return;    // block-uniform: past this member's columns
   const SimtItem it = reinterpret_cast<const SimtItem*>(a.plan + a.off_items)[blockIdx.x];
   const int r = simt_rank(it);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.y * 256 + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
-  const bool active = blockIdx.y * 256 + warp * 64 < h_out;      // warp-uniform (h_out % 64 == 0)
+  const int j = blockIdx.y * kSimtExpCols + warp * 64 + (lane & 7) * 8;   // this lane's 8 columns
+  const bool active = blockIdx.y * kSimtExpCols + warp * 64 < h_out;      // warp-uniform (h_out % 64 == 0)
   const int ks = lane >> 3, nt = simt_nt(it);
   __nv_bfloat16* const y = a.y[m];
   const int64_t ldy = a.ldy[m];
