@@ -261,6 +261,11 @@ int lsv_copy_blocks(int32_t n, const void* const* src, void* const* dst, const s
 /* Number of SMs the planner assumes (queried from device 0 once; 148 on B200). */
 int lsv_num_sms(void);
 
+/* Development hook (tools/trace_*.py): kernels launched afterwards from the calling thread write
+ * per-CTA / per-item clock stamps into buf ([grid][items_per_cta][16] uint64, device memory);
+ * buf = NULL turns it off.  Not needed for any computation. */
+int lsv_debug_set_trace(void* buf, int32_t items_per_cta);
+
 #ifdef __cplusplus
 }
 #endif

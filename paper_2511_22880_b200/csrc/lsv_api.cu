@@ -27,10 +27,13 @@ using namespace lsv;
 namespace {
 
 thread_local char g_err[512] = "";
-uint64_t* g_trace = nullptr;  // debug timeline buffer (lsv_debug_set_trace)
-int g_trace_items = 0;
-int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
-int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
+// Development hooks, not part of any compute path's state: a per-thread trace buffer
+// (lsv_debug_set_trace: launches issued from the calling thread stamp it) and ablation bits read
+// once from the environment (0 in production).
+thread_local uint64_t* g_trace = nullptr;
+thread_local int g_trace_items = 0;
+const int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
+const int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;

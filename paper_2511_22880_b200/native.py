@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
     "lsv_lora_forward", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
-    "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum",
+    "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum", "lsv_debug_set_trace",
 )
 
 _lib = None
@@ -43,6 +43,7 @@ _SIGNATURES = {
     "lsv_version": (ctypes.c_int, []),
     "lsv_last_error": (ctypes.c_char_p, []),
     "lsv_num_sms": (ctypes.c_int, []),
+    "lsv_debug_set_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "lsv_adapter_a_bytes": (_sz, [_i32, _i32]),
     "lsv_adapter_b_bytes": (_sz, [_i32, _i32]),
     "lsv_pack_adapter": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
