@@ -200,3 +200,26 @@ def test_group_pack_rejects_bad_member():
     with pytest.raises(ValueError):
         native.check(lib.lsv_pack_adapter_group(None, 5, 0, 8, 4096, None, None))
     assert lib.lsv_adapter_a_group_bytes(3, 16, 4096) == 3 * 16 * 4096 * 2
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_simt_tail_row_block_map(P):
+    """The SIMT tier's plan tail (lsv_plan.h): items carry ntok | rank << 16; the row-block prefix
+    counts each item's 16-row blocks of its group A (P * rank rows); the map gives every shrink
+    block its (item, row block) in item order."""
+    ranks = [8, 24, 128, 256, 40, 16]
+    lens = [1, 3, 8, 2, 5, 1]
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    blob, _ = _plan_group(indptr, ranks, 4096, [1024] * P) if P > 1 else _plan(indptr, ranks, 4096, 1024)
+    d = _decode(blob)
+    n = d["n_simt"]
+    assert n == len(ranks) and d["n_mtiles"] == 0
+    items = d["simt"]
+    assert [int(it[2]) & 0xFFFF for it in items] == lens
+    assert [int(it[2]) >> 16 for it in items] == ranks
+    pre = blob[d["off_simt"] + 4 * n:d["off_simt"] + 5 * n + 1]
+    nrb = [-(-P * r // 16) for r in ranks]
+    assert list(np.diff(pre)) == nrb and pre[0] == 0
+    rbmap = blob[d["off_simt"] + 5 * n + 1:d["off_simt"] + 5 * n + 1 + int(pre[-1])]
+    want = [i << 8 | rb for i in range(n) for rb in range(nrb[i])]
+    assert list(rbmap) == want
