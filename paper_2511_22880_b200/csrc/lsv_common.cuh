@@ -318,6 +318,13 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
                : "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
                  "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
+// The same with the streaming (evict-first) cache hint: for outputs nothing re-reads soon, so
+// they do not displace L2 lines other traffic still needs.
+__device__ __forceinline__ void st_global_v8_cs_if(void* ptr, const uint32_t* w, bool pred) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t@p st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t}\n" ::"l"(ptr),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"((int)pred)
+               : "memory");
+}
 // 32-byte store (sm_100 STG.256); ptr must be 32-byte aligned
 __device__ __forceinline__ void st_global_v8_if(void* ptr, const uint32_t* w, bool pred) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %9, 0;\n\t@p st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t}\n" ::"l"(ptr),

@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
         const int c_lo = kExpandEpiWarps == 8 ? half * (tw / 2) : 0, c_hi = kExpandEpiWarps == 8 ? c_lo + tw / 2 : tw;
         // each lane writes its own token row: 32-byte stores are one full sector per row and half
-        // the store wavefronts of 16-byte ones (the epilogue is the expand's busiest stage)
+        // the store wavefronts of 16-byte ones; streaming (evict-first) since y is not re-read here
         const bool st32 = LSV_EXPAND_ST32 && p.st32[inf.proj];
 #if LSV_EXPAND_EPI_PIPE
         // two 32-column chunks in flight: chunk i+1's TMEM load overlaps chunk i's convert + stores
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
           if (st32) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) st_global_v8_if(yrow + cc + u * 16, &w[8 * u], valid);
+            for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
           } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
           if (st32) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) st_global_v8_if(yrow + cc + u * 16, &w[8 * u], valid);
+            for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
           } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
