@@ -226,6 +226,23 @@ __host__ __device__ constexpr int shrink_smem_bytes() {
 #ifndef LSV_EXPAND_ST32
 #define LSV_EXPAND_ST32 1
 #endif
+// Quadrant rotation of small expand tiles.  An M=128 MMA writes A row i to TMEM lane i, so an item
+// of <= 32 (<= 64) tokens whose A descriptors start 32*qb rows early lands in lane quadrant(s)
+// qb.. and is stored by that quadrant's epilogue warp.  Consecutive small items then drain on
+// different warps in parallel instead of queueing on the quadrant-0 warp.  0: off; 1: <= 32-token
+// items alternate quadrants 0/1; 2: <= 32-token items rotate over 0..3, <= 64-token over {0, 2}.
+#ifndef LSV_EXPAND_QROT
+#define LSV_EXPAND_QROT 0
+#endif
+__device__ __forceinline__ int expand_qbase(int k, int ntok) {
+#if LSV_EXPAND_QROT == 2
+  return ntok <= 32 ? (k & 3) : ntok <= 64 ? ((k & 1) << 1) : 0;
+#elif LSV_EXPAND_QROT == 1
+  return ntok <= 32 ? (k & 1) : 0;
+#else
+  return 0;
+#endif
+}
 #ifndef LSV_EXPAND_EPI_WARPS
 #define LSV_EXPAND_EPI_WARPS 4
 #endif
@@ -766,17 +783,20 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         const uint32_t vb = bb + voff;
         const uint32_t yb = bb + round_up(voff + np16 * kp * 2, 1024);
         const uint32_t d = tmem_base + buf * p.tw_max;
+        // quadrant rotation: A starts qrow rows early (whole swizzle atoms; the rows before the v
+        // image are this item's B tile, >= 96 * S bytes, and only feed discarded D lanes)
+        const int qrow = 32 * expand_qbase(k, inf.ntok);
         // D = v . B : A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128)
         const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
         for (int ks = 0; ks < nv; ++ks) {
           const int kk = ks * 16;
-          const uint64_t adesc = smem_desc(vb + (kk / ck) * np16 * S + (kk % ck) * 2, 16, 8 * S, vlay);
+          const uint64_t adesc = smem_desc(vb + (kk / ck) * np16 * S + (kk % ck) * 2 - qrow * S, 16, 8 * S, vlay);
           const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
           umma_bf16(d, adesc, bdesc, idesc_mn, ks > 0 ? 1u : 0u);
         }
         // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
         for (int ks = 0; ks < ny; ++ks) {
-          const uint64_t adesc = smem_desc(ib + (128 - 16 * ks) * 32, 16, 256, 6);
+          const uint64_t adesc = smem_desc(ib + (128 - 16 * ks - qrow) * 32, 16, 256, 6);
           const uint64_t bdesc = smem_desc(yb + ks * 2048, np16 * 128, 1024, 2);
           umma_bf16(d, adesc, bdesc, idesc_mn, 1u);
         }
@@ -799,8 +819,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
       if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
-      const int t = q * 32 + lane;
-      if (q * 32 < inf.ntok) {   // warp-uniform: quadrants past the tile's tokens have no rows
+      const int qr = q - expand_qbase(k, inf.ntok);   // this warp's quadrant within the item
+      const int t = qr * 32 + lane;
+      if (qr >= 0 && qr * 32 < inf.ntok) {   // warp-uniform: other quadrants have no rows
         const int tw = p.tws[inf.proj];
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
         const bool valid = t < inf.ntok && !(p.dbg & 1);
