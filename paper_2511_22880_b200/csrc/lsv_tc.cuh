@@ -243,7 +243,8 @@ __device__ __forceinline__ int expand_qbase(int k, int ntok) {
   return 0;
 #endif
 }
-// L2 evict-first hints on the expand's loads: 0 off; 1 B tiles; 2 B tiles and y rows.
+// L2 hints on the expand's loads: 0 off; 1 B evict-first; 2 B and y evict-first; 3 y evict-last;
+// 4 B evict-first and y evict-last.
 #ifndef LSV_EXPAND_EF
 #define LSV_EXPAND_EF 0
 #endif
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       uint8_t* dst = ring + ring_off;
       const int dbg = p.dbg;
       if (lane == 0) {
-#if LSV_EXPAND_EF >= 1
+#if LSV_EXPAND_EF == 1 || LSV_EXPAND_EF == 2 || LSV_EXPAND_EF == 4
         if (!(dbg & 16)) bulk_load_hint(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs], l2_evict_first_policy());
 #else
         if (!(dbg & 16)) bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
@@ -760,7 +761,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       } else if (!(dbg & 8)) {
         int h, row, bb;
         if (y_box(np16, nb, lane - 2, h, row, bb))
-#if LSV_EXPAND_EF >= 2
+#if LSV_EXPAND_EF >= 3
+          tma_load_2d_hint(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
+                           inf.jtile * tw + h * 64, inf.tok_begin + row, l2_evict_last_policy());
+#elif LSV_EXPAND_EF == 2
           tma_load_2d_hint(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
                            inf.jtile * tw + h * 64, inf.tok_begin + row, l2_evict_first_policy());
 #else
