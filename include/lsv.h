@@ -28,8 +28,12 @@
  *   - LSV_EINVAL / LSV_EWORKSPACE map to Python ValueError, LSV_ECUDA / LSV_EUNSUPPORTED
  *     to RuntimeError in the shim (paper_2511_22880_b200/native.py);
  *   - all device work is asynchronous on the caller's stream; the library never
- *     allocates in lsv_lora_apply and keeps no mutable global state besides cached
- *     device attributes and driver entry points.
+ *     allocates device memory in lsv_lora_apply.  Its host-side mutable state is limited to
+ *     caches whose contents are pure functions of their keys: cached device attributes and
+ *     driver entry points, a process-wide tensor-map cache keyed by (pointer, row stride,
+ *     rows, cols, box kind) under a mutex, and a per-thread cache of the last plan built
+ *     (keyed by every planner input, so lsv_plan_size_* followed by lsv_plan_build_* with the
+ *     same inputs plans once).  None of them changes a result.
  */
 #ifndef LSV_H_
 #define LSV_H_
@@ -175,6 +179,18 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
                      const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
                      void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
                      int32_t num_tokens, void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* lsv_lora_forward with flags.  By default a group's shrink may start while the previous group's
+ * expand drains (it reads nothing that expand writes), which is valid only when every y range of the
+ * call is disjoint from every other y range and from every x range; the library checks this and
+ * falls back to full serialisation otherwise.  LSV_FWD_SERIAL forces every launch to wait for its
+ * predecessor (what a model whose next input depends on the previous output gets). */
+#define LSV_FWD_SERIAL 1
+int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
+                        const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
+                        void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
+                        int32_t num_tokens, void* workspace, size_t workspace_bytes, int32_t flags,
+                        lsv_stream_t stream);
 
 /* Workspace bytes lsv_lora_forward needs for these group plans (0 on bad input). */
 size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const void* const* plans_host);

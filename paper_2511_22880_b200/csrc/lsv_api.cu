@@ -640,6 +640,40 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// lsv_lora_forward's cross-launch overlap is safe when every y range is disjoint from every other
+// y range and from every x range of the call (x ranges may overlap each other: read-only).
+bool forward_ranges_disjoint(int L, int G, const PlanHeader* const* hs, int nproj, const void* const* xs,
+                             const int64_t* ldxs, void* const* ys, const int64_t* ldys, int32_t num_tokens) {
+  if (num_tokens <= 0) return true;
+  struct Rng { uintptr_t lo, hi; bool is_y; };
+  std::vector<Rng> r;
+  r.reserve((size_t)L * (G + nproj));
+  for (int l = 0; l < L; ++l) {
+    int p0 = 0;
+    for (int g = 0; g < G; ++g) {
+      const PlanHeader* h = hs[g];
+      const uintptr_t x = reinterpret_cast<uintptr_t>(xs[(size_t)l * G + g]);
+      if (x) r.push_back({x, x + (uintptr_t)(((int64_t)(num_tokens - 1) * ldxs[(size_t)l * G + g] + h->h_in) * 2), false});
+      for (int i = 0; i < h->num_proj; ++i) {
+        const size_t k = (size_t)l * nproj + p0 + i;
+        const uintptr_t y = reinterpret_cast<uintptr_t>(ys[k]);
+        if (y) r.push_back({y, y + (uintptr_t)(((int64_t)(num_tokens - 1) * ldys[k] + h->h_outs[i]) * 2), true});
+      }
+      p0 += h->num_proj;
+    }
+  }
+  std::sort(r.begin(), r.end(), [](const Rng& a, const Rng& b) { return a.lo < b.lo; });
+  // sweep: an overlap involving a y range is a hazard; track the furthest-reaching x and y so far
+  uintptr_t x_end = 0, y_end = 0;
+  for (const Rng& q : r) {
+    if (q.lo < y_end) return false;                 // overlaps an earlier y
+    if (q.is_y && q.lo < x_end) return false;        // a y overlapping an earlier x
+    if (q.is_y) y_end = std::max(y_end, q.hi);
+    else x_end = std::max(x_end, q.hi);
+  }
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -886,6 +920,15 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
                      const void* const* xs, const int64_t* ldxs, void* const* ys, const int64_t* ldys,
                      const void* a_ptrs, const void* b_ptrs, int32_t num_tokens, void* workspace,
                      size_t workspace_bytes, lsv_stream_t stream) {
+  return lsv_lora_forward_ex(num_layers, num_groups, plans_dev, plans_host, xs, ldxs, ys, ldys, a_ptrs, b_ptrs,
+                             num_tokens, workspace, workspace_bytes, 0, stream);
+}
+
+int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
+                        const void* const* plans_host, const void* const* xs, const int64_t* ldxs, void* const* ys,
+                        const int64_t* ldys, const void* a_ptrs, const void* b_ptrs, int32_t num_tokens,
+                        void* workspace, size_t workspace_bytes, int32_t flags, lsv_stream_t stream) {
+  if (flags & ~LSV_FWD_SERIAL) return fail(LSV_EINVAL, "lsv_lora_forward_ex: unknown flags 0x%x", flags);
   if (num_layers < 0 || num_groups < 1 || num_groups > 64)
     return fail(LSV_EINVAL, "num_layers %d / num_groups %d out of range", num_layers, num_groups);
   if (!plans_dev || !plans_host || !xs || !ldxs || !ys || !ldys || !a_ptrs || !b_ptrs)
@@ -908,6 +951,10 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
     ws_off[g + 1] = ws_off[g] + ((size_t)hs[g]->ws_bytes + 255) / 256 * 256;
   }
   const size_t per_layer = ws_off[num_groups];
+  // A shrink may skip waiting for the previous launch only if nothing it reads is written by an
+  // earlier expand of this call and no two expands write overlapping y: otherwise (e.g. y buffers
+  // reused across layers) every launch waits for its predecessor.
+  const bool overlap_free = !(flags & LSV_FWD_SERIAL) && forward_ranges_disjoint(num_layers, num_groups, hs, nproj, xs, ldxs, ys, ldys, num_tokens);
   if (workspace_bytes < per_layer * (size_t)num_layers)
     return fail(LSV_EWORKSPACE, "workspace of %zu bytes is smaller than the %zu the forward needs "
                 "(lsv_lora_forward_workspace)", workspace_bytes, per_layer * (size_t)num_layers);
@@ -931,7 +978,8 @@ int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* 
         // this call no kernel writes an adapter slab, so the SIMT kernels stream their first
         // weights before griddepcontrol.wait
         if (int rc = run_shrink(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S,
-                                static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st, first ? 1 : 0, !first,
+                                static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st,
+                                (first || !overlap_free) ? 1 : 0, !first,
                                 nullptr, !first))
           return rc;
       }

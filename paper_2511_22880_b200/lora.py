@@ -182,8 +182,7 @@ class LoraDeltaEngine:
         ph = (ctypes.c_void_p * len(plans))(*[gp.plan_host.ctypes.data for gp in plans])
         ws_need = native.lib().lsv_lora_forward_workspace(self.model.layers, len(plans), ctypes.addressof(ph))
         if self._workspace is None or self._workspace.numel() < ws_need:
-            # zero-filled once: the kernels leave their split counters at zero on exit
-            self._workspace = torch.zeros(max(ws_need, 256), dtype=torch.uint8, device=self.device)
+            self._grow_workspace(ws_need, stream)
         a_tab, b_tab = self.slab.pointer_tables(seg.seg_slot, peer_slabs=peer_slabs, seg_owner=seg_owner,
                                                 as_numpy=True)
         if stream is None:
@@ -197,6 +196,26 @@ class LoraDeltaEngine:
         if stream is not None:
             bp.extra["ring_tag"] = tag
         return bp
+
+    def _grow_workspace(self, need: int, stream) -> None:
+        """Replace the shared workspace by a larger zero-filled one (growth only, rare).
+
+        The split-K / TP grid barriers need zeroed counters, so the memset must be ordered before
+        every kernel that uses the new buffer: it is issued on the stream the batch will run on
+        (``stream``, or the current stream for eager callers, which is then synchronised).  The old
+        buffer may still be read by kernels in flight on any stream, so the device is drained before
+        it goes back to the caching allocator."""
+        if self._workspace is not None:
+            torch.cuda.synchronize(self.device)
+            self._workspace = None
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            # zero-filled once: the kernels leave their split counters at zero on exit
+            ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+        ws.record_stream(st)
+        if stream is None:
+            st.synchronize()
+        self._workspace = ws
 
     def _live(self, bp: BatchPlan) -> None:
         tag = bp.extra.get("ring_tag")
@@ -257,9 +276,11 @@ class LoraDeltaEngine:
             st.cuda_stream))
 
     def forward(self, bp: BatchPlan, xs: list[dict[str, torch.Tensor]], ys: list[dict[str, torch.Tensor]],
-                stream=None) -> None:
+                stream=None, serial: bool = False) -> None:
         """Every layer and projection: xs[l][input_group], ys[l][proj_name] — one native call
-        (lsv_lora_forward) that issues each layer's group shrinks and group expands in order."""
+        (lsv_lora_forward_ex) that issues each layer's group shrinks and group expands in order.
+        ``serial``: every launch waits for the previous one (no shrink starting under the previous
+        group's expand), as in a model where each group's input depends on the previous output."""
         self._live(bp)
         projs = self.model.projections
         L, G = self.model.layers, len(self.groups)
@@ -281,10 +302,11 @@ class LoraDeltaEngine:
         xa, la, ya, lya = (arr(ctypes.c_void_p, xl), arr(ctypes.c_int64, ldx), arr(ctypes.c_void_p, yl),
                            arr(ctypes.c_int64, ldy))
         st = stream or torch.cuda.current_stream(self.device)
-        native.check(native.lib().lsv_lora_forward(
+        native.check(native.lib().lsv_lora_forward_ex(
             L, G, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
             ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr(), bp.b_ptrs.data_ptr(),
-            xs[0][self.groups[0][0]].shape[0], bp.workspace.data_ptr(), bp.workspace.numel(), st.cuda_stream))
+            xs[0][self.groups[0][0]].shape[0], bp.workspace.data_ptr(), bp.workspace.numel(),
+            native.FWD_SERIAL if serial else 0, st.cuda_stream))
 
     def forward_prefetch(self, bp: BatchPlan, pf: "RemotePrefetch", xs, ys, stream=None) -> None:
         """``forward`` with peer-owned adapters fetched one layer ahead into local staging buffers by

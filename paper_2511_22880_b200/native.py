@@ -21,6 +21,7 @@ LSV_OK, LSV_EINVAL, LSV_ECUDA, LSV_EUNSUPPORTED, LSV_EWORKSPACE = 0, 1, 2, 3, 4
 LSV_DTYPE_BF16 = 0
 ABI_VERSION = 2
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
+FWD_SERIAL = 1
 
 # every symbol include/lsv.h declares (tests/test_native_abi.py checks the library exports them)
 EXPORTED_SYMBOLS = (
@@ -31,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "lsv_slab_alloc", "lsv_slab_free", "lsv_vimg_assemble", "lsv_plan_vimg_region",
     "lsv_adapter_a_group_bytes", "lsv_pack_adapter_group", "lsv_unpack_adapter_group",
     "lsv_plan_size_group", "lsv_plan_build_group", "lsv_lora_expand_proj", "lsv_lora_expand_group",
-    "lsv_lora_forward", "lsv_lora_forward_workspace", "lsv_copy_blocks",
+    "lsv_lora_forward", "lsv_lora_forward_ex", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
     "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum", "lsv_debug_set_trace",
 )
@@ -73,6 +74,8 @@ _SIGNATURES = {
     "lsv_lora_expand_proj": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "lsv_lora_expand_group": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "lsv_lora_forward": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _vp]),
+    "lsv_lora_forward_ex": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _sz, _i32,
+                                           _vp]),
     "lsv_lora_forward_workspace": (_sz, [_i32, _i32, _vp]),
     "lsv_copy_blocks": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp]),
     "lsv_lora_shrink_tp_scatter": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,

@@ -227,6 +227,9 @@ class TPLoraDeltaEngine:
         st = {"seg": seg, "plans": plans, "ws": ws, "a_ptrs": a_ptrs, "b_ptrs": b_ptrs, "gathered": gathered,
               "per_group": per_group, "comm": torch.cuda.Stream(self.device)}
         self._prepare_fused(st)
+        # the workspaces' zero fills (their split counters and grid barriers start at zero) ran on
+        # the current stream; forward may run on any stream, so they must be complete first
+        torch.cuda.current_stream(self.device).synchronize()
         return st
 
     def _prepare_fused(self, st: dict) -> None:
