@@ -42,3 +42,24 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip_gpu)
         if "multigpu" in item.keywords and ngpu < 2:
             item.add_marker(skip_multi)
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Print every parity margin the GPU tests recorded (tests._cases.MARGINS) and save them to
+    gpurun_out/parity_margins.json (the worst error of each test against the 1e-2 contract)."""
+    try:
+        from tests._cases import MARGINS
+    except Exception:  # pragma: no cover
+        return
+    if not MARGINS:
+        return
+    import json
+    tr = terminalreporter
+    tr.write_sep("=", "parity margins (max|gpu-ref|/max|ref| vs the 1e-2 contract; ulps of ref)")
+    for m in MARGINS:
+        tr.write_line(f"{m.get('test', '?')[:60]:60s} {m.get('key', '')[:26]:26s} err {m['max_rel_err']:.3e} "
+                      f"(x{1e-2 / max(m['max_rel_err'], 1e-12):.1f} headroom)  ulps {m.get('max_ulps', float('nan')):.2f}  "
+                      f"rn-exact {m.get('frac_rn_exact', float('nan')):.4f}")
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / "parity_margins.json").write_text(json.dumps(MARGINS, indent=1))
