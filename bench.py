@@ -49,6 +49,8 @@ def parse_args(argv=None):
                     help="c2: the metric's 1-GPU config; dp: LoRAServe placement + routing across the ranks "
                          "(default when launched with more than one rank)")
     ap.add_argument("--tier", choices=("auto", "simt", "tc"), default="auto")
+    ap.add_argument("--v-bf16", action="store_true",
+                    help="tensor-core tier keeps v as one bf16 image (LSV_PLAN_V_BF16) instead of the hi/lo pair")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tp-adapters", type=int, default=0,
                     help="config tp: roster size (default 1000 at TP8, scaled by TP/8 below that to fit HBM)")
@@ -236,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
     slab = AdapterSlab(model, slab_bytes, dev)
     for aid, r in zip(wl.adapter_ids, wl.ranks):
         slab.fill_random(slab.allocate(aid, r), 1000 + zlib.crc32(aid.encode()) % 100000)
-    eng = LoraDeltaEngine(slab, tier_policy=tier)
+    eng = LoraDeltaEngine(slab, tier_policy=tier, v_bf16=args.v_bf16)
     bp = eng.prepare(seg)
 
     # per-layer activations (distinct buffers; every step moves far more than the 126 MB L2)
@@ -438,6 +440,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init adapters, N(0,1) activations)",
         "config": {"workload": wl.description, "config": config, "tier_policy": args.tier,
+                   "v_precision": "bf16" if args.v_bf16 else "bf16 hi/lo pair (~16 bits)",
                    "per_gpu": [{"ms": p[0], "tokens": int(p[1])} for p in per_rank] if world > 1 else None,
                    "l2": "inputs larger than L2 (per-layer activation buffers; %.1f GB moved per step)" % (step_bytes / 1e9),
                    "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},

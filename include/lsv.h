@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define LSV_ABI_VERSION 2
+#define LSV_ABI_VERSION 3
 
 #define LSV_OK 0
 #define LSV_EINVAL 1
@@ -60,6 +60,12 @@ extern "C" {
 #define LSV_TIER_AUTO 0
 #define LSV_TIER_SIMT 1
 #define LSV_TIER_TC 2
+/* Plan flag, OR-ed into tier_policy: the tensor-core tier's intermediate v = x·A^T is kept as a
+ * single bf16 image instead of the default bf16 (hi, lo) pair.  The pair (v_hi = bf16(v), v_lo =
+ * bf16(v - v_hi)) carries v to ~16 significant bits through the expand's two bf16 MMAs, so the
+ * delta matches the fp32-v SGMV result up to the final bf16 rounding of y; the single image rounds
+ * v to bf16 (8 bits) first, costing less workspace and expand ring bytes. */
+#define LSV_PLAN_V_BF16 0x100
 
 typedef void* lsv_stream_t; /* a cudaStream_t */
 

@@ -51,10 +51,10 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // ---- planner knobs ------------------------------------------------------------------------
-// AUTO tier rule: segments of at most kAutoSimtMaxTok tokens (decode / tiny prefill) or
-// rank > 128 go to the SIMT tier; everything else is tcgen05.  Justified by the per-tier
-// measurements in DESIGN.md §4 (profiles/).
+// AUTO tier rule: segments of at most kAutoSimtMaxTok tokens (decode / tiny prefill) go to the
+// SIMT tier; everything else is tcgen05.
 constexpr int kAutoSimtMaxTok = 8;
+bool auto_simt(int n, int rank) { (void)rank; return n <= kAutoSimtMaxTok; }
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
 #ifndef LSV_SHRINK_WAVES
 #define LSV_SHRINK_WAVES 8
@@ -178,6 +178,9 @@ int subset_np(int P, int p0, int r) { return std::max(1, std::min(P - p0, 256 / 
 int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
                const int32_t* h_outs, int32_t policy) {
   if (int rc = validate_segments(S, indptr, rank, h_in, P, h_outs)) return rc;
+  if (policy & ~(0xff | LSV_PLAN_V_BF16)) return fail(LSV_EINVAL, "unknown plan flags 0x%x", policy);
+  const int vsplit = (policy & LSV_PLAN_V_BF16) ? 0 : 1;
+  policy &= 0xff;
   if (policy != LSV_TIER_AUTO && policy != LSV_TIER_SIMT && policy != LSV_TIER_TC)
     return fail(LSV_EINVAL, "unknown tier policy %d", policy);
   const int N = S > 0 ? indptr[S] : 0;
@@ -194,8 +197,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     if (n == 0) continue;
     bool simt;
     if (policy == LSV_TIER_SIMT) simt = true;
-    else if (policy == LSV_TIER_TC) simt = rank[s] > 128;
-    else simt = n <= kAutoSimtMaxTok || rank[s] > 128;
+    else if (policy == LSV_TIER_TC) simt = false;
+    else simt = auto_simt(n, rank[s]);
     pb.tier[s] = simt ? kTierSimt : kTierTc;
     if (simt) {
       for (int tb = 0; tb < n; tb += kSimtMaxTok) {
@@ -204,9 +207,10 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         v_off += (int64_t)nt * rank[s];
       }
     } else {
-      for (int tb = 0; tb < n; tb += kTileM) {
+      const int tm = mtile_rows(rank[s]);
+      for (int tb = 0; tb < n; tb += tm) {
         MTile mt{};
-        mt.seg = s; mt.tok_begin = indptr[s] + tb; mt.ntok = std::min(kTileM, n - tb); mt.rank = rank[s];
+        mt.seg = s; mt.tok_begin = indptr[s] + tb; mt.ntok = std::min(tm, n - tb); mt.rank = rank[s];
         pb.mtiles.push_back(mt);
       }
     }
@@ -240,7 +244,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     mt.part_off = (int32_t)part_off;
     if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * G;
     mt.vimg_off = (int32_t)vimg_off;  // 1024-aligned: the v image's swizzle atoms are address-based
-    vimg_off += round_up((int)((int64_t)round_up(mt.ntok, 16) * kpad(r) * 2), 1024);
+    vimg_off += (int64_t)vimg_bytes(mt.ntok, kpad(r)) * (vsplit ? 2 : 1);   // split v: hi image, lo image
     mt.counter = counter++;
     if (nsplit > 1) {  // reduction units: (token, projection, 8 padded-k) of this tile, reduced grid-wide
       pb.red.push_back((int32_t)i);
@@ -283,7 +287,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   auto emit = [&](const std::vector<ItemClass>& cls, std::vector<std::pair<int64_t, ExpandRec>>& out) {
     for (const ItemClass& c : cls) {
       const MTile& mt = pb.mtiles[c.mt];
-      const int tw = b_tile_width(h_outs[c.p]);
+      const int tw = expand_item_tw(mt.rank, b_tile_width(h_outs[c.p]));
       for (int jt = 0; jt < h_outs[c.p] / tw; ++jt) {
         ExpandRec r{};
         r.seg = mt.seg; r.tok_begin = mt.tok_begin; r.ntok = mt.ntok; r.rank = mt.rank;
@@ -296,16 +300,18 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   int expand_grid[kMaxProj] = {0, 0, 0, 0};
   std::vector<ItemClass> all_cls;
   for (int p = 0; p < P; ++p) {
-    const int tw = b_tile_width(h_outs[p]);
     std::vector<ItemClass> cls;
+    size_t n_items = 0;
     for (size_t i = 0; i < pb.mtiles.size(); ++i) {
       const MTile& mt = pb.mtiles[i];
+      const int tw = expand_item_tw(mt.rank, b_tile_width(h_outs[p]));
       cls.push_back({(int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + kExpandItemFixed, (int32_t)i, p});
+      n_items += h_outs[p] / tw;
     }
     all_cls.insert(all_cls.end(), cls.begin(), cls.end());
     std::stable_sort(cls.begin(), cls.end(), by_cost);
     std::vector<std::pair<int64_t, ExpandRec>> expand_costed;
-    expand_costed.reserve((size_t)pb.mtiles.size() * (h_outs[p] / tw));
+    expand_costed.reserve(n_items);
     emit(cls, expand_costed);
     expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
     lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p]);
@@ -322,6 +328,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   h.num_segments = S; h.num_tokens = N; h.h_in = h_in; h.h_out = h_outs[0];
   h.num_proj = P;
   h.acc_cols = acc_cols;
+  h.vsplit = vsplit;
   h.n_simt_items = (int32_t)pb.simt.size();
   h.n_mtiles = (int32_t)pb.mtiles.size();
   h.n_shrink_items = (int32_t)pb.shrink.size();
@@ -374,7 +381,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   pb.red_cta = red_cta;
   h.total_ints = off;
   int64_t ws = 0;
-  h.ws_counters = 0; ws += round_up((counter + 2) * 4, 256);  // + grid barrier {arrive, done}
+  h.ws_counters = 0; ws += kBarHeaderBytes;   // barrier header (lsv_plan.h): pair 0 for standalone calls
   h.ws_partials = (int32_t)ws; ws += (part_off * 4 + 255) / 256 * 256;
   const int64_t vstride = (vimg_off + 1023) / 1024 * 1024;
   h.ws_vimg = (int32_t)ws; ws += vstride * P;
@@ -383,7 +390,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   if (ws > INT32_MAX) return fail(LSV_EUNSUPPORTED, "workspace of %lld bytes exceeds 2 GiB", (long long)ws);
   h.vimg_stride = (int32_t)vstride;
   h.ws_bytes = (int32_t)ws;
-  h.n_counters = counter;
+  h.n_counters = 0;
+  (void)counter;
   int simt_segs = 0;
   for (int s = 0; s < S; ++s) simt_segs += pb.tier[s] == kTierSimt;
   h.simt_segments = simt_segs;
@@ -540,7 +548,7 @@ struct TpScatter {
 
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
                const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true,
-               const TpScatter* tps = nullptr, bool simt_pdl = false) {
+               const TpScatter* tps = nullptr, bool simt_pdl = false, int* gbar = nullptr) {
   if (h->n_simt_items > 0) {
     // one block per (8-row block of an item's group A, k-split): exactly the blocks with rows
     const int32_t* hp = reinterpret_cast<const int32_t*>(h);
@@ -556,11 +564,12 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     if (int rc = get_maps(p.xmap, 0, x, ldx, num_tokens, h->h_in)) return rc;
     p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
     p.off_recs = h->off_shrink_recs; p.off_cta = h->off_shrink_cta;
-    p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg; p.ws_counters = h->ws_counters;
+    p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg;
+    p.gbar = gbar ? gbar : reinterpret_cast<int*>(ws);
     p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
     p.off_red_cta = h->off_red_cta;
-    p.grid_bar = h->n_counters;
     p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
+    p.vsplit = h->vsplit;
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     if (tps != nullptr) {
       p.tp = tps->tp; p.tp_rank = tps->tp_rank;
@@ -625,8 +634,10 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   if (xsum != nullptr) {
     p.xsum = xsum; p.xslot = 2 * h->vimg_stride * h->num_proj; p.ws_vimg0 = h->ws_vimg;
     p.off_mtiles = h->off_mtiles; p.n_mtiles = h->n_mtiles; p.num_proj = h->num_proj;
-    p.vimg_stride = h->vimg_stride; p.grid_bar = h->n_counters; p.ws_counters = h->ws_counters;
+    p.vimg_stride = h->vimg_stride;
+    p.gbar = reinterpret_cast<int*>(ws);
   }
+  p.vsplit = h->vsplit;
   p.off_recs = all ? h->off_expand_recs_all : h->off_expand_recs_p[p0];
   p.off_cta = all ? h->off_expand_cta_all : h->off_expand_cta_p[p0];
   p.tw_max = tw_max;
@@ -639,6 +650,11 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// lsv_lora_forward slice of one (layer, group): the plan's scratch without its barrier header
+size_t forward_slice_bytes(const PlanHeader* h) {
+  return ((size_t)h->ws_bytes - kBarHeaderBytes + 255) / 256 * 256;
+}
 
 // lsv_lora_forward's cross-launch overlap is safe when every y range is disjoint from every other
 // y range and from every x range of the call (x ranges may overlap each other: read-only).
@@ -948,25 +964,33 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
     if (S >= 0 && hs[g]->num_segments != S) return fail(LSV_EINVAL, "group plans index different batches");
     S = hs[g]->num_segments;
     nproj += hs[g]->num_proj;
-    ws_off[g + 1] = ws_off[g] + ((size_t)hs[g]->ws_bytes + 255) / 256 * 256;
+    ws_off[g + 1] = ws_off[g] + forward_slice_bytes(hs[g]);
   }
+  if (1 + (int64_t)num_layers * num_groups > kMaxBarPairs)
+    return fail(LSV_EUNSUPPORTED, "%d layers x %d groups exceed the workspace barrier header", num_layers, num_groups);
   const size_t per_layer = ws_off[num_groups];
+  const size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers;
   // A shrink may skip waiting for the previous launch only if nothing it reads is written by an
   // earlier expand of this call and no two expands write overlapping y: otherwise (e.g. y buffers
   // reused across layers) every launch waits for its predecessor.
   const bool overlap_free = !(flags & LSV_FWD_SERIAL) && forward_ranges_disjoint(num_layers, num_groups, hs, nproj, xs, ldxs, ys, ldys, num_tokens);
-  if (workspace_bytes < per_layer * (size_t)num_layers)
+  if (workspace_bytes < need)
     return fail(LSV_EWORKSPACE, "workspace of %zu bytes is smaller than the %zu the forward needs "
-                "(lsv_lora_forward_workspace)", workspace_bytes, per_layer * (size_t)num_layers);
-  if (per_layer > 0 && !workspace) return fail(LSV_EINVAL, "workspace is null");
+                "(lsv_lora_forward_workspace)", workspace_bytes, need);
+  if (!workspace) return fail(LSV_EINVAL, "workspace is null");
   const void* const* at = static_cast<const void* const*>(a_ptrs);
   const void* const* bt = static_cast<const void* const*>(b_ptrs);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // workspace: [barrier header: pair 1 + l*G + g per (layer, group)][per layer: one slice per group].
+  // A slice holds its plan's scratch without the plan's own barrier header: the kernels get a base
+  // kBarHeaderBytes before the slice (plan offsets start there) and their barrier pair explicitly.
+  uint8_t* const wsb = static_cast<uint8_t*>(workspace);
   for (int l = 0; l < num_layers; ++l) {
     int p0 = 0;
-    uint8_t* wsl = static_cast<uint8_t*>(workspace) + per_layer * (size_t)l;
+    uint8_t* wsl = wsb + per_layer * (size_t)l;   // + kBarHeaderBytes + ws_off[g] = slice (l, g)
     for (int g = 0; g < num_groups; ++g) {
       const PlanHeader* h = hs[g];
+      int* gbar = reinterpret_cast<int*>(wsb) + 2 * (1 + l * num_groups + g);
       const int np = h->num_proj;
       const int64_t ldx = ldxs[l * num_groups + g];
       const void* x = xs[l * num_groups + g];
@@ -980,14 +1004,14 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
         if (int rc = run_shrink(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S,
                                 static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], st,
                                 (first || !overlap_free) ? 1 : 0, !first,
-                                nullptr, !first))
+                                nullptr, !first, gbar))
           return rc;
       }
       const void* const* btab[kMaxProj];
       for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
       if (int rc = expand_group_checked(ys + (size_t)l * nproj + p0, ldys + (size_t)l * nproj + p0, num_tokens,
                                         btab, plans_dev[g], plans_host[g], wsl + ws_off[g],
-                                        ws_off[g + 1] - ws_off[g], st, true))
+                                        ws_off[g + 1] - ws_off[g] + kBarHeaderBytes, st, true))
         return rc;
       p0 += np;
     }
@@ -1007,6 +1031,7 @@ int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, i
     return fail(LSV_EINVAL, "lsv_lora_shrink_tp_scatter: bad tp / rank / destinations");
   if (fh->n_mtiles != h->n_mtiles || fh->num_proj != h->num_proj || fh->num_tokens != h->num_tokens)
     return fail(LSV_EINVAL, "shard and full plans index different tiles");
+  if (fh->vsplit != h->vsplit) return fail(LSV_EINVAL, "shard and full plans differ in v precision (LSV_PLAN_V_BF16)");
   if (h->n_simt_items != 0 || fh->n_simt_items != 0)
     return fail(LSV_EUNSUPPORTED, "TP scatter needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
   if (h->h_in != h_in) return fail(LSV_EINVAL, "h_in %d does not match the plan's %d", h_in, h->h_in);
@@ -1078,9 +1103,12 @@ size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const 
   for (int g = 0; g < num_groups; ++g) {
     const PlanHeader* h = check_plan(plans_host[g]);
     if (!h) return 0;
-    per_layer += ((size_t)h->ws_bytes + 255) / 256 * 256;
+    per_layer += forward_slice_bytes(h);
   }
-  return per_layer * (size_t)num_layers;
+  // at least as large as any single plan's workspace, so the standalone entry points can share it
+  size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers;
+  for (int g = 0; g < num_groups; ++g) need = std::max(need, (size_t)check_plan(plans_host[g])->ws_bytes);
+  return need;
 }
 
 int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dtype, int32_t num_tokens, int32_t h_in,
@@ -1136,6 +1164,7 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
     return fail(LSV_EINVAL, "shard and full plans index different tiles (%d vs %d)", hs->n_mtiles, hf->n_mtiles);
   if (tp < 1 || !gathered || !full_workspace) return fail(LSV_EINVAL, "bad arguments");
   if (hs->num_proj != hf->num_proj) return fail(LSV_EINVAL, "shard and full plans have different members");
+  if (hs->vsplit != hf->vsplit) return fail(LSV_EINVAL, "shard and full plans differ in v precision (LSV_PLAN_V_BF16)");
   if (hs->n_simt_items != 0 || hf->n_simt_items != 0)
     return fail(LSV_EUNSUPPORTED, "TP assembly needs every segment on the tensor-core tier (plan with LSV_TIER_TC)");
   if (hf->n_mtiles == 0) return LSV_OK;
@@ -1144,7 +1173,7 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
   for (int pp = 0; pp < hf->num_proj; ++pp) {   // member pp: its shard images and its full-rank images
     vimg_assemble_kernel<<<hf->n_mtiles, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint8_t*>(gathered) + (size_t)pp * hs->vimg_stride, region_bytes, tp, sp, hs->off_mtiles, 0,
-        fp, hf->off_mtiles, static_cast<uint8_t*>(full_workspace), hf->ws_vimg + pp * hf->vimg_stride);
+        fp, hf->off_mtiles, static_cast<uint8_t*>(full_workspace), hf->ws_vimg + pp * hf->vimg_stride, hf->vsplit);
     LSV_CUDA_CHECK(cudaGetLastError());
   }
   return LSV_OK;

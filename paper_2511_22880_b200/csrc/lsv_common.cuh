@@ -75,6 +75,19 @@ __host__ __device__ __forceinline__ uint32_t vimg_off(int t, int k, int kp, int 
   return swz(off, S);
 }
 
+// Bytes of one bf16 v image of an m-tile (rows padded to 16, K = kp), 1024-aligned.  With split v
+// (PlanHeader::vsplit) the m-tile's region holds the hi image, then the lo image at +vimg_bytes.
+__host__ __device__ __forceinline__ uint32_t vimg_bytes(int ntok, int kp) {
+  return (uint32_t)round_up(round_up(ntok, 16) * kp * 2, 1024);
+}
+// Expand item tile width: ranks above 128 use 128-wide h_out tiles (a 256-wide layout tile's half)
+// so that the item's B, v and y bytes fit the expand ring.
+__host__ __device__ __forceinline__ int expand_item_tw(int rank, int layout_tw) {
+  return rank > 128 ? 128 : layout_tw;
+}
+// m-tile height of a segment of this rank: 64 tokens above rank 128 (bounds an item's v image), else 128.
+__host__ __device__ __forceinline__ int mtile_rows(int rank) { return rank > 128 ? 64 : 128; }
+
 // ---- small device helpers ----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -84,6 +97,19 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+// 8 fp32 values -> bf16 hi unit and the bf16 residual unit (v - hi rounded): hi + lo carries v to
+// ~16 significant bits, so the expand's two MMAs (v_hi·B + v_lo·B, fp32 accumulate) see v at
+// near-fp32 precision.
+__device__ __forceinline__ void split_bf16x8(const float* v, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+    l[i] = pack_bf16x2(v[2 * i] - __uint_as_float(h[i] << 16), v[2 * i + 1] - __uint_as_float(h[i] & 0xffff0000u));
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 __device__ __forceinline__ uint32_t elect_one() {
   uint32_t pred = 0;

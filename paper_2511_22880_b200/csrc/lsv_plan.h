@@ -10,7 +10,7 @@
 namespace lsv {
 
 constexpr int32_t kPlanMagic = 0x5056534c;  // "LSVP"
-constexpr int32_t kPlanVersion = 2;
+constexpr int32_t kPlanVersion = 3;
 constexpr int kMaxProj = 4;    // projections per input group (q/k/v = 3)
 
 enum Tier : int32_t { kTierNone = 0, kTierSimt = 1, kTierTc = 2 };
@@ -45,7 +45,8 @@ struct PlanHeader {            // 64 int32
   int32_t off_expand_recs_p[kMaxProj], off_expand_cta_p[kMaxProj];
   int32_t expand_grid_p[kMaxProj], n_expand_items_p[kMaxProj];
   int32_t off_expand_recs_all, off_expand_cta_all, expand_grid_all, n_expand_all;  // every member, one LPT list
-  int32_t reserved[64 - 61];
+  int32_t vsplit;                      // 1: each tcgen05 v image is a bf16 (hi, lo) pair, v = hi + lo to ~2^-16
+  int32_t reserved[64 - 62];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -85,6 +86,15 @@ struct ExpandRec {             // 8 int32
   int32_t seg, tok_begin, ntok, rank;
   int32_t jtile, vimg_off, mtile, proj;         // member proj's h_out columns [jtile*tw, jtile*tw+tw)
 };
+
+// Workspace barrier header.  Every workspace starts with kBarHeaderBytes of grid-barrier words that
+// are zero at rest (zero-filled once; every kernel re-arms what it used before it exits).  A plan's
+// own scratch (split-K partials, v images, SIMT v) starts after it, so reusing one workspace for
+// plans of different layouts (a new batch every step) never lands a barrier on stale scratch.
+// Pair 0 serves the standalone entry points; lsv_lora_forward gives (layer l, group g) pair
+// 1 + l * num_groups + g.
+constexpr int kBarHeaderBytes = 64 * 1024;
+constexpr int kMaxBarPairs = kBarHeaderBytes / 8;
 
 // Pipeline geometry (bytes of shared memory).
 #ifndef LSV_SHRINK_SLOT_KB

@@ -254,20 +254,24 @@ __global__ void __launch_bounds__(256) vimg_assemble_kernel(const uint8_t* __res
                                                             int tp, const int32_t* __restrict__ splan,
                                                             int s_off_mtiles, int s_ws_vimg,
                                                             const int32_t* __restrict__ fplan, int f_off_mtiles,
-                                                            uint8_t* __restrict__ fws, int f_ws_vimg) {
+                                                            uint8_t* __restrict__ fws, int f_ws_vimg, int vsplit) {
   const MTile ms = reinterpret_cast<const MTile*>(splan + s_off_mtiles)[blockIdx.x];
   const MTile mf = reinterpret_cast<const MTile*>(fplan + f_off_mtiles)[blockIdx.x];
   const int rs = ms.rank, kps = kpad(rs), kpf = kpad(mf.rank), np16 = round_up(mf.ntok, 16);
   const int upr = kpf / 8, units = mf.ntok * upr;
-  for (int u = threadIdx.x; u < units; u += blockDim.x) {
-    const int t = u / upr, k0 = (u % upr) * 8;
+  // split v: each image is a (hi, lo) pair; the lo half sits vimg_bytes after the hi half
+  for (int u = threadIdx.x; u < units * (vsplit ? 2 : 1); u += blockDim.x) {
+    const int half = u / units, uu = u % units;
+    const int t = uu / upr, k0 = (uu % upr) * 8;
     uint4 w = make_uint4(0, 0, 0, 0);
     if (k0 < tp * rs) {
       const int sh = k0 / rs, kk = k0 % rs;
-      const uint8_t* src = gathered + (size_t)sh * region + (ms.vimg_off) + vimg_off(t, kk, kps, np16);
+      const uint8_t* src = gathered + (size_t)sh * region + (ms.vimg_off) + vimg_off(t, kk, kps, np16) +
+                           (half ? vimg_bytes(ms.ntok, kps) : 0u);
       w = *reinterpret_cast<const uint4*>(src);
     }
-    *reinterpret_cast<uint4*>(fws + f_ws_vimg + mf.vimg_off + vimg_off(t, k0, kpf, np16)) = w;
+    *reinterpret_cast<uint4*>(fws + f_ws_vimg + mf.vimg_off + vimg_off(t, k0, kpf, np16) +
+                              (half ? vimg_bytes(mf.ntok, kpf) : 0u)) = w;
   }
 }
 

@@ -39,10 +39,12 @@ struct alignas(64) ShrinkParams {
   const int32_t* plan;
   const void* const* a_ptrs;
   uint8_t* ws;
-  int off_recs, off_cta, ws_partials, ws_vimg, ws_counters;
-  int off_mtiles, off_red, n_red, red_units, grid_bar, off_red_cta;   // grid-wide split-K reduction
+  int off_recs, off_cta, ws_partials, ws_vimg;
+  int off_mtiles, off_red, n_red, red_units, off_red_cta;   // grid-wide split-K reduction
+  int* gbar;                    // grid barrier {arrive, done} in the workspace's barrier header
   int num_proj, vimg_stride;    // input group: projections shrunk together, bytes between their v images
   int acc_cols;                 // TMEM accumulator width (128 -> 4 buffers, 256 -> 2)
+  int vsplit;                   // 1: v images are bf16 (hi, lo) pairs (PlanHeader::vsplit)
   int wait_prev;                // 0: the previous launch is another input group's expand, which this
                                 // launch neither reads nor overwrites: start without waiting for it
   // tensor-parallel scatter (tp > 0): instead of this rank's shard images, every (token, member,
@@ -76,7 +78,9 @@ struct alignas(64) ExpandParams {
   int wait_target;              //     then the last CTA through re-arms it ([0] flag, [1] pass counter)
   const uint8_t* xsum;          // TP row groups: this rank's exchange buffer (wait_target fp32 partial
   int xslot, ws_vimg0;          //   slots); summed into the v images (at ws + ws_vimg0) before expanding
-  int off_mtiles, n_mtiles, num_proj, vimg_stride, grid_bar, ws_counters;
+  int off_mtiles, n_mtiles, num_proj, vimg_stride;
+  int* gbar;                    // TP row-sum grid barrier {arrive, done} (workspace barrier header)
+  int vsplit;                   // 1: v images are bf16 (hi, lo) pairs: two v MMAs per K step
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
@@ -167,10 +171,14 @@ using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
 // TP scatter of one 16-byte unit (8 k of member pp, token t of m-tile mtile; k local to the shard)
 // into every rank's full-rank image: column tp_rank * rs + k of K = kpad(full rank).
 __device__ __forceinline__ void tp_scatter(const ShrinkParams& p, int mtile, int pp, int t, int k, int rs, int np16,
-                                           const uint4& w) {
+                                           const uint4& w, const uint4& wlo) {
   const MTile mf = reinterpret_cast<const MTile*>(p.fplan + p.f_off_mtiles)[mtile];
   const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, p.tp_rank * rs + k, kpad(mf.rank), np16);
-  for (int d = 0; d < p.tp; ++d) *reinterpret_cast<uint4*>(p.vdst[d] + off) = w;
+  const uint32_t lo = vimg_bytes(mf.ntok, kpad(mf.rank));
+  for (int d = 0; d < p.tp; ++d) {
+    *reinterpret_cast<uint4*>(p.vdst[d] + off) = w;
+    if (p.vsplit) *reinterpret_cast<uint4*>(p.vdst[d] + off + lo) = wlo;
+  }
 }
 // The full image's k pad (full rank % 16 == 8) is written as zeros by the last shard's rank.
 __device__ __forceinline__ void tp_scatter_pad(const ShrinkParams& p, int mtile, int pp, int t, int np16) {
@@ -178,7 +186,11 @@ __device__ __forceinline__ void tp_scatter_pad(const ShrinkParams& p, int mtile,
   const int kpf = kpad(mf.rank);
   if (p.tp_rank != p.tp - 1 || kpf == mf.rank) return;
   const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, mf.rank, kpf, np16);
-  for (int d = 0; d < p.tp; ++d) *reinterpret_cast<uint4*>(p.vdst[d] + off) = make_uint4(0, 0, 0, 0);
+  const uint32_t lo = vimg_bytes(mf.ntok, kpf);
+  for (int d = 0; d < p.tp; ++d) {
+    *reinterpret_cast<uint4*>(p.vdst[d] + off) = make_uint4(0, 0, 0, 0);
+    if (p.vsplit) *reinterpret_cast<uint4*>(p.vdst[d] + off + lo) = make_uint4(0, 0, 0, 0);
+  }
 }
 // Row-parallel TP: 8 fp32 partial-v values (member pp, token t of m-tile mtile, k..k+7) into slot
 // tp_rank of every rank's exchange buffer (per m-tile fp32 [np16][kp] at 2 * vimg_off).
@@ -197,7 +209,7 @@ __device__ __forceinline__ void tp_row_put(const ShrinkParams& p, int mtile, int
 // last one signals every rank.
 __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
   if (threadIdx.x != 0) return;
-  int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+  int* bar = p.gbar;
   if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) {
     bar[1] = 0;
     for (int d = 0; d < p.tp; ++d) red_release_sys_add(p.flags[d], 1);
@@ -313,17 +325,17 @@ __device__ __forceinline__ void red_sum(const ShrinkParams& p, const RedUnit& ru
 __device__ __forceinline__ void red_store(const ShrinkParams& p, const RedUnit& ru, const float* s8) {
   const int32_t* red = p.plan + p.off_red;
   const int kp = kpad(ru.mt.rank), np16 = round_up(ru.mt.ntok, 16);
-  uint4 w;
-  w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
-  w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
+  uint4 w, wlo;
+  split_bf16x8(s8, w, wlo);
   if (p.tp > 0 && p.tp_row) {
     if (ru.k0 < ru.mt.rank) tp_row_put(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, s8);
   } else if (p.tp > 0) {
-    if (ru.k0 < ru.mt.rank) tp_scatter(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, ru.mt.rank, np16, w);
+    if (ru.k0 < ru.mt.rank) tp_scatter(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, ru.mt.rank, np16, w, wlo);
     if (ru.k0 == 0) tp_scatter_pad(p, red[2 * ru.e], ru.pp, ru.t, np16);   // once per (token, member)
   } else {
-    *reinterpret_cast<uint4*>(p.ws + p.ws_vimg + (size_t)ru.pp * p.vimg_stride + ru.mt.vimg_off +
-                              vimg_off(ru.t, ru.k0, kp, np16)) = w;
+    uint8_t* dst = p.ws + p.ws_vimg + (size_t)ru.pp * p.vimg_stride + ru.mt.vimg_off + vimg_off(ru.t, ru.k0, kp, np16);
+    *reinterpret_cast<uint4*>(dst) = w;
+    if (p.vsplit) *reinterpret_cast<uint4*>(dst + vimg_bytes(ru.mt.ntok, kp)) = wlo;
   }
 }
 
@@ -464,6 +476,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
       const bool valid = row < nt && !(p.dbg & 8);
       uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
+      const uint32_t vlo = vimg_bytes(nt, kp);                  // hi image -> lo image (split v)
       float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
       for (int cc = 0; cc < rows; cc += 16) {
         float v[16];
@@ -474,15 +487,16 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             const int j0 = cc + h * 8;          // 8 columns, all of projection p0 + j0 / r (r % 8 == 0)
             if (j0 < rows) {
               if (inf.nsplit == 1) {
-                uint4 w;
-                w.x = pack_bf16x2(v[h * 8 + 0], v[h * 8 + 1]);
-                w.y = pack_bf16x2(v[h * 8 + 2], v[h * 8 + 3]);
-                w.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
-                w.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
+                uint4 w, wlo;
+                split_bf16x8(v + h * 8, w, wlo);
                 const int pp = inf.p0 + j0 / r;
                 if (p.tp > 0 && p.tp_row) tp_row_put(p, inf.mtile, pp, row, j0 % r, v + h * 8);
-                else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w);
-                else *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16)) = w;
+                else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w, wlo);
+                else {
+                  uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16);
+                  *reinterpret_cast<uint4*>(dst) = w;
+                  if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = wlo;
+                }
               } else {
                 float* dst = part + j0;
                 if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {   // one full sector per row
@@ -500,8 +514,11 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
         if (!p.tp_row)
           for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
       } else if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
-        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp)
-          *reinterpret_cast<uint4*>(vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16)) = make_uint4(0, 0, 0, 0);
+        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) {
+          uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+          if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = make_uint4(0, 0, 0, 0);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -536,7 +553,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   // ---- grid-wide split-K reduction (all CTAs are co-resident: grid <= SMs, 1 CTA per SM) ----
   // Every (token, 8-wide k unit) of every split tile is summed over its splits in fixed split
   // order by one thread, so results are bit-identical from run to run.
-  int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+  int* bar = p.gbar;
   if (threadIdx.x == 0) {
     atomicAdd(&bar[0], 1);
     int seen = 0;
@@ -611,10 +628,11 @@ __device__ __forceinline__ void tp_row_sum(const ExpandParams& p) {
           s8[4] += hi.x; s8[5] += hi.y; s8[6] += hi.z; s8[7] += hi.w;
         }
       }
-      uint4 w;
-      w.x = pack_bf16x2(s8[0], s8[1]); w.y = pack_bf16x2(s8[2], s8[3]);
-      w.z = pack_bf16x2(s8[4], s8[5]); w.w = pack_bf16x2(s8[6], s8[7]);
-      *reinterpret_cast<uint4*>(p.ws + p.ws_vimg0 + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16)) = w;
+      uint4 w, wlo;
+      split_bf16x8(s8, w, wlo);
+      uint8_t* dst = p.ws + p.ws_vimg0 + (size_t)pp * p.vimg_stride + mt.vimg_off + vimg_off(t, k0, kp, np16);
+      *reinterpret_cast<uint4*>(dst) = w;
+      if (p.vsplit) *reinterpret_cast<uint4*>(dst + vimg_bytes(mt.ntok, kp)) = wlo;
     }
   }
 }
@@ -690,7 +708,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       tp_row_sum(p);
       __threadfence();
       __syncthreads();
-      int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+      int* bar = p.gbar;
       if (threadIdx.x == 0) {
         atomicAdd(&bar[0], 1);
         uint64_t t0 = 0;
@@ -718,9 +736,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
     uint32_t vbegin[kItemQ];
     int retired = 0;
     for (int k = 0; rs.pop(inf, b); ++k) {
-      const int tw = p.tws[inf.proj], nb = tw / 64;
+      const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
       const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
-      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2, ybytes = nb * np16 * 128;
+      // split v: the lo image follows the hi image (vimg_bytes apart, as in the workspace): one copy
+      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2 + (p.vsplit ? vlo : 0), ybytes = nb * np16 * 128;
       const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
       const uint32_t size = yoff + ybytes;
       const int qs = k % kItemQ;
@@ -728,7 +748,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       if (lane == 0) {
         // the M=128 MMA reads 128 v rows per K chunk (rows >= ntok only feed discarded D rows):
         // the item must sit where that read stays inside the ring + guard
-        const uint32_t extent = max(size, voff + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
+        const uint32_t extent =
+            max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
         head = round_up(head, 1024);
         if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
           head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
@@ -750,12 +771,21 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       ring_off = __shfl_sync(0xffffffffu, ring_off, 0);
       uint8_t* dst = ring + ring_off;
       const int dbg = p.dbg;
+      if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group, one copy per lane
+        const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
+        const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
+        if (!(dbg & 16))
+          for (int kg = lane; kg < kp / 8; kg += 32)
+            bulk_load(dst + kg * nb * 1024, src + (size_t)kg * (twl / 64) * 1024, (uint32_t)(nb * 1024), &full[qs]);
+      }
       if (lane == 0) {
+        if (tw == twl && !(dbg & 16)) {
 #if LSV_EXPAND_EF == 1 || LSV_EXPAND_EF == 2 || LSV_EXPAND_EF == 4
-        if (!(dbg & 16)) bulk_load_hint(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs], l2_evict_first_policy());
+          bulk_load_hint(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs], l2_evict_first_policy());
 #else
-        if (!(dbg & 16)) bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
+          bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
 #endif
+        }
       } else if (lane == 1) {
         if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, &full[qs]);
       } else if (!(dbg & 8)) {
@@ -782,10 +812,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
     for (int k = 0; rs.pop(inf, unused); ++k) {
       if (lane == 0) {
         trace_aux(p.trace, p.trace_items, cta, k, 1);
-        const int tw = p.tws[inf.proj], nb = tw / 64;
+        const int r = inf.rank;
+        const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
         const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
         const int qs = k % kItemQ;
-        const int r = inf.rank, kp = kpad(r), np16 = round_up(inf.ntok, 16);
+        const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
         const int S = kmajor_row_bytes(kp), ck = S / 2;
         const uint32_t vlay = umma_layout(S);
         const int buf = k % nbuf;
@@ -798,7 +829,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         const uint32_t bb = smem_u32(ring + offs[qs]);
         const uint32_t voff = round_up(tw * kp * 2, 1024);
         const uint32_t vb = bb + voff;
-        const uint32_t yb = bb + round_up(voff + np16 * kp * 2, 1024);
+        const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+        const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
         const uint32_t d = tmem_base + buf * p.tw_max;
         // quadrant rotation: A starts qrow rows early (whole swizzle atoms; the rows before the v
         // image are this item's B tile, >= 96 * S bytes, and only feed discarded D lanes)
@@ -811,6 +843,15 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
           umma_bf16(d, adesc, bdesc, idesc_mn, ks > 0 ? 1u : 0u);
         }
+        // split v: D += v_lo . B (same B descriptors, the lo image vlo bytes after the hi image)
+        if (p.vsplit)
+          for (int ks = 0; ks < nv; ++ks) {
+            const int kk = ks * 16;
+            const uint64_t adesc =
+                smem_desc(vb + vlo + (kk / ck) * np16 * S + (kk % ck) * 2 - qrow * S, 16, 8 * S, vlay);
+            const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
+            umma_bf16(d, adesc, bdesc, idesc_mn, 1u);
+          }
         // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
         for (int ks = 0; ks < ny; ++ks) {
           const uint64_t adesc = smem_desc(ib + (128 - 16 * ks - qrow) * 32, 16, 256, 6);
@@ -839,7 +880,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       const int qr = q - expand_qbase(k, inf.ntok);   // this warp's quadrant within the item
       const int t = qr * 32 + lane;
       if (qr >= 0 && qr * 32 < inf.ntok) {   // warp-uniform: other quadrants have no rows
-        const int tw = p.tws[inf.proj];
+        const int tw = expand_item_tw(inf.rank, p.tws[inf.proj]);
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
         const bool valid = t < inf.ntok && !(p.dbg & 1);
         __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
@@ -903,7 +944,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   if (p.xsum != nullptr && threadIdx.x == 0) {   // every CTA is past the sum barrier: re-arm it
-    int* bar = reinterpret_cast<int*>(p.ws + p.ws_counters) + p.grid_bar;
+    int* bar = p.gbar;
     if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }
   }
 }

@@ -152,12 +152,14 @@ class LoraDeltaEngine:
     Per layer and input group (model.groups(): q/k/v, o, gate/up, down) one fused shrink reads
     the group's x once and writes every member's v images; each member's expand follows."""
 
-    def __init__(self, slab: AdapterSlab, tier_policy: int = native.TIER_AUTO):
+    def __init__(self, slab: AdapterSlab, tier_policy: int = native.TIER_AUTO, v_bf16: bool = False):
+        """``v_bf16``: keep the tensor-core tier's intermediate v as one bf16 image
+        (LSV_PLAN_V_BF16) instead of the default bf16 (hi, lo) pair (include/lsv.h)."""
         native.load()
         self.slab = slab
         self.model: ModelShape = slab.model
         self.device = slab.device
-        self.tier_policy = tier_policy
+        self.tier_policy = tier_policy | (native.PLAN_V_BF16 if v_bf16 else 0)
         self.groups = self.model.groups()
         self._member = {p: (gi, i) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self._workspace: torch.Tensor | None = None
@@ -345,12 +347,13 @@ class LoraDeltaEngine:
         ph = arr(ctypes.c_void_p, [gp.plan_host.ctypes.data for gp in bp.group_plans])
         xa, la, ya, lya = (arr(ctypes.c_void_p, xl), arr(ctypes.c_int64, ldx), arr(ctypes.c_void_p, yl),
                            arr(ctypes.c_int64, ldy))
-        per_layer_ws = bp.workspace.numel() // self.model.layers
+        # the whole workspace: this call's layers reuse the slices (and barrier pairs) of layers
+        # [0, nl); its first launch is a plain one, ordered after the previous call's kernels
         native.check(native.lib().lsv_lora_forward(
             nl, G, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
             ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr() + l0 * G * S * 8,
             bp.b_ptrs.data_ptr() + l0 * P * S * 8, xs[l0][self.groups[0][0]].shape[0],
-            bp.workspace.data_ptr() + l0 * per_layer_ws, per_layer_ws * nl, st.cuda_stream))
+            bp.workspace.data_ptr(), bp.workspace.numel(), st.cuda_stream))
 
     def launches_per_step(self, bp: BatchPlan) -> int:
         """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand

@@ -19,9 +19,10 @@ LIB_PATH = Path(os.environ.get("LSV_LIB_PATH") or Path(__file__).resolve().paren
 
 LSV_OK, LSV_EINVAL, LSV_ECUDA, LSV_EUNSUPPORTED, LSV_EWORKSPACE = 0, 1, 2, 3, 4
 LSV_DTYPE_BF16 = 0
-ABI_VERSION = 2
+ABI_VERSION = 3
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 FWD_SERIAL = 1
+PLAN_V_BF16 = 0x100   # plan flag: single bf16 v image on the tensor-core tier (default: hi/lo pair)
 
 # every symbol include/lsv.h declares (tests/test_native_abi.py checks the library exports them)
 EXPORTED_SYMBOLS = (

@@ -99,6 +99,12 @@ class TPSlab:
         self._member = {p: (gi, i, len(m)) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self.device = torch.device(device)
         self.ranks = list(ranks)
+        big = sorted({int(r) for r in ranks if padded_rank(int(r), tp) > 128})
+        if big:
+            # rank > 128 runs on 64-token tensor-core tiles (lsv_common.cuh mtile_rows), which a
+            # rank shard of at most 128 does not get: the shard and full-rank plans would tile the
+            # batch differently.  The paper's rosters stop at 128 (traces.py:23).
+            raise ValueError(f"tensor parallelism supports padded ranks up to 128, got {big}")
         L, P, G = model.layers, len(self.specs), len(self.groups)
         self.g_off = np.zeros((len(ranks), L, G), dtype=np.int64)
         self.b_off = np.zeros((len(ranks), L, P), dtype=np.int64)

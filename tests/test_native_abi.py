@@ -116,7 +116,29 @@ def test_forced_policies():
     d = _decode(_plan([0, 64, 128], [8, 128], policy=native.TIER_SIMT)[0])
     assert d["n_mtiles"] == 0 and d["n_simt"] == 16
     d = _decode(_plan([0, 2, 130], [8, 256], policy=native.TIER_TC)[0])
-    assert d["n_mtiles"] == 1 and list(d["tier"]) == [2, 1]   # rank 256 stays on SIMT
+    # every segment on tcgen05; rank 256 on 64-token tiles with 128-wide expand items
+    assert d["n_mtiles"] == 3 and list(d["tier"]) == [2, 2]
+    assert [int(m[2]) for m in d["mtiles"]] == [2, 64, 64]
+    items = {(int(r[6]), int(r[4])) for r in d["expand"]}
+    assert len(items) == d["n_expand"] == 4096 // 256 + 2 * (4096 // 128)
+    # AUTO: a long rank-256 segment is no longer sent to SIMT; a 5-token one is
+    d = _decode(_plan([0, 5, 300], [256, 256])[0])
+    assert list(d["tier"]) == [1, 2] and d["n_mtiles"] == 5
+
+
+def test_split_v_doubles_the_v_image_region():
+    lib = native.load()
+    indptr, ranks = [0, 40, 200, 201], [8, 64, 128]
+    regions = []
+    for flag in (0, native.PLAN_V_BF16):
+        blob, _ = _plan(indptr, ranks, policy=native.TIER_AUTO | flag)
+        off, nb = ctypes.c_size_t(), ctypes.c_size_t()
+        native.check(lib.lsv_plan_vimg_region(blob.ctypes.data, ctypes.byref(off), ctypes.byref(nb)))
+        assert int(blob[61]) == (0 if flag else 1)     # PlanHeader::vsplit
+        regions.append(nb.value)
+    assert regions[0] == 2 * regions[1]
+    with pytest.raises(ValueError, match="flags"):
+        _plan(indptr, ranks, policy=0x400)
 
 
 def test_apply_rejects_missing_plan():
