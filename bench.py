@@ -52,6 +52,7 @@ def parse_args(argv=None):
     ap.add_argument("--v-bf16", action="store_true",
                     help="tensor-core tier keeps v as one bf16 image (LSV_PLAN_V_BF16) instead of the hi/lo pair")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the N=1 dp-workload and config-1 lines")
     ap.add_argument("--tp-adapters", type=int, default=0,
                     help="config tp: roster size (default 1000 at TP8, scaled by TP/8 below that to fit HBM)")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -280,6 +281,10 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = ms_local
+    # the same step with every launch waiting for its predecessor (no group shrink starting under the
+    # previous group's expand): what a model whose next input depends on the previous output gets
+    ms_serial = time_graph(torch, eng, bp, xs, ys, stream, args.steps, args.warmup, dev,
+                           step_fn=lambda: eng.forward(bp, xs, ys, stream, serial=True))
     tokens_all = N * world
     per_rank = [[ms_local, N]]
     if world > 1:
@@ -350,7 +355,10 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e through the public API with host buffers ----
     from paper_2511_22880_b200.segments import index_tokens as _ix
-    tok_slots_host = np.repeat(seg.seg_slot, seg.lengths())   # the batch as the host sees it
+    # E2E_BATCHES distinct batches of the same workload family (seeds 0..3 of the token -> adapter
+    # draw), each in arrival order (tokens unsorted: the indexer computes a real permutation), fed
+    # round robin so every step pays indexing and planning of a batch it has not just planned
+    tok_batches = e2e_token_batches(config, wl, world, rank)
     x_host = torch.empty((N, model.projections[0].h_in), dtype=torch.bfloat16, pin_memory=True)
     x_host.copy_(xs[0][input_group(model.projections[0].name)].cpu())
     last = model.projections[-1]
@@ -378,8 +386,8 @@ def run_ours(args, rank, world, local_rank):
         so the host work of step k+1 overlaps the GPU work of step k (a serving loop), and the
         copies of neighbouring steps overlap step k's kernels."""
         b = step_no[0] & 1
+        seg_i = _ix(tok_batches[step_no[0] % len(tok_batches)], wl.ranks)   # host segment indexing
         step_no[0] += 1
-        seg_i = _ix(tok_slots_host, wl.ranks)                      # host segment indexing
         bp_i = eng.prepare(seg_i, stream=stream)                   # host planning + async plan/pointer upload
         h2d_st.wait_event(ev_fwd[b])                               # step k-2 done reading this x buffer
         with torch.cuda.stream(h2d_st):
@@ -433,6 +441,15 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"layer 0 of {model.layers} (all {len(model.projections)} projections, {N} tokens), "
                          f"median of {reps_cpu} reps, extrapolated x{model.layers}"}
 
+    # N = 1 extras: the data-parallel workload of one server (like for like with the N > 1 lines)
+    # and config 1 (launch-bound per-call time by CUDA-graph replay, the full CPU oracle beside it)
+    extra = {}
+    if world == 1 and config == "c2" and not args.no_extras:
+        del graph
+        torch.cuda.synchronize(dev)
+        extra["dp_like_for_like"] = dp_one_server(args, torch, dev)
+        extra["c1"] = c1_line(args, torch, dev)
+
     if rank != 0:
         return None
     line = {
@@ -465,11 +482,135 @@ def run_ours(args, rank, world, local_rank):
                 "path": "per step: index_tokens -> LoraDeltaEngine.prepare (async uploads) -> H2D x -> forward "
                         "(one lsv_lora_forward call) -> D2H y; steps issued back to back (host planning of step k+1 "
                         "overlaps the GPU work of step k; H2D/D2H on their own streams with double-buffered "
-                        "x/y overlap neighbouring steps' kernels), wall clock over all steps after one final sync"},
+                        "x/y overlap neighbouring steps' kernels), wall clock over all steps after one final sync",
+                "batches": f"{len(tok_batches)} distinct seeded batches round robin, tokens in arrival order "
+                           "(the indexer's stable sort by adapter slot is a real permutation); the host batch "
+                           "former lays x out in segment order before the H2D"},
         "gpu_launches": launches * args.steps,
+        "serial_step": {"ms_per_step": ms_serial, "value": tokens_all / (ms_serial / 1e3) if world == 1 else None,
+                        "note": "the same step with every launch waiting for its predecessor (lsv_lora_forward_ex "
+                                "LSV_FWD_SERIAL): no group shrink under the previous group's expand"},
         "clocks": clocks,
     }
+    if extra:
+        line.update(extra)
     return line
+
+
+def e2e_token_batches(config, wl, world, rank, n=4):
+    """Per-token adapter slots of ``n`` distinct batches of the workload, in arrival order (shuffled).
+    c2: seeds 0..n-1 of its token -> adapter draw (same roster); other configs: batches resampled
+    from this GPU's batch (same resident adapters, same per-adapter token distribution)."""
+    from paper_2511_22880_b200 import synth
+    base = np.repeat(wl.segments.seg_slot, wl.segments.lengths())
+    out = []
+    for k in range(n):
+        rng = np.random.default_rng(100 + k)
+        if config == "c2":
+            w = synth.c2_llama2_7b(seed=k)
+            slots = np.repeat(w.segments.seg_slot, w.segments.lengths())
+        else:
+            slots = rng.choice(base, size=len(base), replace=True) if k > 0 else base
+        out.append(rng.permutation(slots))
+    return out
+
+
+def dp_one_server(args, torch, dev):
+    """The data-parallel workload (LoRAServe placement + routing) with one server: what the N > 1
+    lines run per GPU, so the 1 -> N curve is like for like."""
+    import zlib
+    from paper_2511_22880_b200 import synth
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, input_group
+    from paper_2511_22880_b200.slab import AdapterSlab
+    wl = synth.dp_workloads(1)[0]
+    model, seg = wl.model, wl.segments
+    N = seg.num_tokens
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, wl.ranks), dev)
+    for aid, r in zip(wl.adapter_ids, wl.ranks):
+        slab.fill_random(slab.allocate(aid, r), 1000 + zlib.crc32(aid.encode()) % 100000)
+    eng = LoraDeltaEngine(slab, v_bf16=args.v_bf16)
+    bp = eng.prepare(seg)
+    g = torch.Generator(device=dev).manual_seed(11)
+    groups = {}
+    for pr in model.projections:
+        groups.setdefault(input_group(pr.name), pr.h_in)
+    xs = [{k: torch.randn(N, h, device=dev, generator=g).to(torch.bfloat16) for k, h in groups.items()}
+          for _ in range(model.layers)]
+    ys = [{pr.name: torch.randn(N, pr.h_out, device=dev, generator=g).to(torch.bfloat16) for pr in model.projections}
+          for _ in range(model.layers)]
+    stream = torch.cuda.Stream(dev)
+    ms = time_graph(torch, eng, bp, xs, ys, stream, args.steps, args.warmup, dev)
+    out = {"workload": wl.description, "value": N / (ms / 1e3), "ms_per_step": ms, "tokens": N,
+           "note": "synth.dp_workloads(1): the per-GPU workload family of the N > 1 lines with one server"}
+    del eng, bp, slab, xs, ys
+    torch.cuda.synchronize(dev)
+    return out
+
+
+def c1_line(args, torch, dev, replays=1000):
+    """BASELINE config 1 (q_proj 4096x4096, 4 adapters r=8/16/64/128, 4 x 64 tokens): per-call time
+    of one lsv_lora_apply by CUDA-graph replay (launch-bound), and the full (not extrapolated) CPU
+    oracle on the same inputs."""
+    from oracle import oracle
+    from paper_2511_22880_b200 import synth
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.slab import AdapterSlab
+    wl = synth.c1_qproj()
+    pr = wl.model.projections[0]
+    seg = wl.segments
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(seg.num_tokens, pr.h_in, generator=g).to(torch.bfloat16)
+    slab = AdapterSlab(wl.model, AdapterSlab.capacity_for(wl.model, wl.ranks), dev)
+    a_bits, b_bits = [], []
+    for i, r in enumerate(wl.ranks):
+        ga = torch.Generator().manual_seed(1000 + i)
+        a = (torch.randn(r, pr.h_in, generator=ga) / pr.h_in ** 0.5).to(torch.bfloat16)
+        b = (torch.randn(pr.h_out, r, generator=ga) / r ** 0.5).to(torch.bfloat16)
+        slab.load(slab.allocate(wl.adapter_ids[i], r), 0, 0, a.to(dev), b.to(dev))
+        a_bits.append(a.view(torch.int16).numpy().view(np.uint16))
+        b_bits.append(b.view(torch.int16).numpy().view(np.uint16))
+    eng = LoraDeltaEngine(slab, v_bf16=args.v_bf16)
+    bp = eng.prepare(seg)
+    xd = x.to(dev)
+    y = torch.zeros(seg.num_tokens, pr.h_out, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        eng.apply(bp, 0, 0, xd, y, stream)
+    torch.cuda.synchronize(dev)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=stream):
+        for _ in range(10):
+            eng.apply(bp, 0, 0, xd, y, stream)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(replays // 10):
+            gr.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    us = e0.elapsed_time(e1) * 1e3 / replays
+    from paper_2511_22880_b200.lora import algorithmic_bytes
+    nbytes = algorithmic_bytes(seg, pr.h_in, pr.h_out)
+    # the CPU oracle on all of config 1 (no extrapolation), all host threads
+    xb = x.view(torch.int16).numpy().view(np.uint16)
+    a_l = [a_bits[s] for s in seg.seg_slot]
+    b_l = [b_bits[s] for s in seg.seg_slot]
+    oracle.delta_c(xb, seg.seg_indptr, seg.seg_rank, a_l, b_l, pr.h_out)
+    reps, t0 = 0, time.perf_counter()
+    while reps < 200 and time.perf_counter() - t0 < 5.0:
+        oracle.delta_c(xb, seg.seg_indptr, seg.seg_rank, a_l, b_l, pr.h_out)
+        reps += 1
+    cpu_us = (time.perf_counter() - t0) / reps * 1e6
+    return {"workload": wl.description, "us_per_call": us, "tokens_per_s": seg.num_tokens / (us * 1e-6),
+            "hbm_frac": nbytes / (us * 1e-6) / 1e9 / peaks()[0], "algorithmic_bytes": nbytes,
+            "timing": f"CUDA graph of 10 lsv_lora_apply calls replayed {replays // 10}x (shrink + expand launches "
+                      "back to back), CUDA events",
+            "cpu": {"us_per_call": cpu_us, "tokens_per_s": seg.num_tokens / (cpu_us * 1e-6),
+                    "cores": oracle.cpu_threads(), "kind": "port",
+                    "sample": f"all of config 1, {reps} calls, no extrapolation"}}
 
 
 def measured_traffic(config, label):
