@@ -51,10 +51,24 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // ---- planner knobs ------------------------------------------------------------------------
-// AUTO tier rule: segments of at most kAutoSimtMaxTok tokens (decode / tiny prefill) go to the
-// SIMT tier; everything else is tcgen05.
-constexpr int kAutoSimtMaxTok = 8;
-bool auto_simt(int n, int rank) { (void)rank; return n <= kAutoSimtMaxTok; }
+// AUTO tier rule: a segment of n tokens and rank r goes to the SIMT tier iff n <= simt_max_tok(r),
+// else to tcgen05.  From the (n, r) sweep in profiles/r2_tier_sweep.txt (tools/tier_sweep.py:
+// batches of S equal segments, gate 4096->11008 and down 11008->4096, both tiers forced, CUDA-event
+// time; ncu dram% / tensor-pipe% beside it): the threshold is the largest n at which the SIMT
+// tier's summed gate + down time is lower.  The SIMT expand re-reads each B tile per 2-token pass,
+// so its cost grows with n; the tcgen05 tier's per-item cost is flat in n up to a 128-row tile, so
+// its advantage comes earlier the higher the rank.  Rank 256 runs on 64-token tiles with 128-wide
+// expand items (mtile_rows, expand_item_tw), which moves its crossover back up by one step.
+//     r:        8   16   32   64   128   256
+//     SIMT n <= 4    4    2    1    0     1
+int simt_max_tok(int rank) {
+  if (rank <= 16) return 4;
+  if (rank <= 32) return 2;
+  if (rank <= 64) return 1;
+  if (rank <= 128) return 0;
+  return 1;
+}
+bool auto_simt(int n, int rank) { return n <= simt_max_tok(rank); }
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
 #ifndef LSV_SHRINK_WAVES
 #define LSV_SHRINK_WAVES 8

@@ -49,7 +49,7 @@ class Case:
         return oracle.delta_f64(bf16_bits(self.x), self.seg.seg_indptr, self.seg.seg_rank,
                                 [bf16_bits(a) for a in self.a], [bf16_bits(b) for b in self.b], self.h_out)
 
-    def run_gpu(self, tier_policy=0, device="cuda:0", repeat=1):
+    def run_gpu(self, tier_policy=0, device="cuda:0", repeat=1, v_bf16=False):
         from paper_2511_22880_b200.lora import LoraDeltaEngine
         from paper_2511_22880_b200.slab import AdapterSlab
         slab_bytes = AdapterSlab.capacity_for(self.model, self.ranks)
@@ -57,7 +57,7 @@ class Case:
         for s, r in enumerate(self.ranks):
             slot = slab.allocate(f"a{s}", r)
             slab.load(slot, 0, 0, self.a[s].to(device), self.b[s].to(device))
-        eng = LoraDeltaEngine(slab, tier_policy=tier_policy)
+        eng = LoraDeltaEngine(slab, tier_policy=tier_policy, v_bf16=v_bf16)
         bp = eng.prepare(self.seg)
         x = self.x.to(device)
         outs = []
@@ -107,7 +107,7 @@ class LayerCase:
         return oracle.delta_c(bf16_bits(x), self.seg.seg_indptr, self.seg.seg_rank,
                               [bf16_bits(t) for t in a], [bf16_bits(t) for t in b], self.model.projections[p].h_out)
 
-    def run_gpu(self, tier_policy=0, device="cuda:0"):
+    def run_gpu(self, tier_policy=0, device="cuda:0", v_bf16=False):
         """The product path: every projection of the layer through one LoraDeltaEngine.forward
         (fused input-group shrinks + group expands), y_in = 0.  Returns {proj name: y (CPU bf16)}."""
         from paper_2511_22880_b200.lora import LoraDeltaEngine
@@ -124,7 +124,7 @@ class LayerCase:
         seg = Segments(self.seg.perm, self.seg.seg_indptr, np.asarray([slot_of[int(s)] for s in self.seg.seg_slot],
                                                                       dtype=np.int32),
                        self.seg.seg_rank, self.seg.request_order)
-        eng = LoraDeltaEngine(slab, tier_policy=tier_policy)
+        eng = LoraDeltaEngine(slab, tier_policy=tier_policy, v_bf16=v_bf16)
         bp = eng.prepare(seg)
         n = self.seg.num_tokens
         xs = [{g: t.to(device) for g, t in self.x.items()}]

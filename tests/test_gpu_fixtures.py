@@ -45,3 +45,23 @@ def test_c2_layer_matches_sgmv(request, tier):
     for pr in case.model.projections:
         m = _record(request, compare_to_fixture(ys[pr.name].float().numpy(), f"c2_layer/{pr.name}"), tier)
         assert m["max_rel_err"] <= TOL, m
+
+
+@pytest.mark.parametrize("name", ["c1", "ragged", "rank_256", "one_adapter_8192"])
+def test_split_v_is_within_one_ulp(request, name):
+    """The tensor-core tier's default (hi, lo) v carries v to ~16 bits, so the bf16 output is the
+    fp32 SGMV delta correctly rounded up to accumulation noise: at most one bf16 ulp of the
+    reference anywhere (floored at max|ref| / 256, tests/_cases.compare_to_fixture)."""
+    case = fixture_case(name)
+    y, _ = case.run_gpu(tier_policy=TC)
+    m = _record(request, compare_to_fixture(y.float().numpy()[:case.seg.num_tokens], name), TC)
+    assert m["max_ulps"] <= 1.0 and m["frac_rn_exact"] >= 0.99, m
+
+
+@pytest.mark.parametrize("name", ["c1", "token_budget_8192"])
+def test_bf16_v_mode_within_contract(request, name):
+    """LSV_PLAN_V_BF16 (v rounded to one bf16 image before the expand): still inside the contract."""
+    case = fixture_case(name)
+    y, _ = case.run_gpu(tier_policy=TC, v_bf16=True)
+    m = _record(request, compare_to_fixture(y.float().numpy()[:case.seg.num_tokens], name), "tc/v_bf16")
+    assert m["max_rel_err"] <= TOL, m

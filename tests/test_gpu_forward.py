@@ -138,7 +138,7 @@ def test_decode_groups_simt_ksplit_against_oracle():
     tok = np.concatenate([np.full(n, s) for s, n in enumerate([1, 2, 5, 1, 3, 1, 2, 4])])
     np.random.default_rng(3).shuffle(tok)
     seg = index_tokens(tok, ranks)
-    eng = LoraDeltaEngine(slab)
+    eng = LoraDeltaEngine(slab, tier_policy=1)       # forced SIMT (AUTO sends rank >= 128 / n > 4 to tcgen05)
     bp = eng.prepare(seg)
     assert all(gp.summary[5] == 0 for gp in bp.group_plans)   # every segment on the SIMT tier
     N = seg.num_tokens

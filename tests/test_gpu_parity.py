@@ -2,7 +2,7 @@
 
 Tolerance (north star): max|Δ_gpu − Δ_cpu| / max|Δ_cpu| ≤ 1e-2 per projection,
 with y_in = 0 so the bf16 output IS the delta.  Operands are bf16, accumulation fp32; the
-tcgen05 tier additionally rounds the intermediate v to bf16 before the expand MMA.
+tcgen05 tier carries v as a bf16 (hi, lo) pair (~16 bits; LSV_PLAN_V_BF16 rounds it to bf16).
 """
 
 import numpy as np
@@ -131,16 +131,16 @@ def test_shrink_expand_split_equals_apply():
 
 @pytest.mark.parametrize("h_in,h_out", [(11008, 4096), (4096, 11008), (1024, 2816)])
 def test_decode_regime_simt(h_in, h_out):
-    """Decode-shaped batches on the SIMT tier: 1-8-token segments (the expand's 2-token passes,
-    odd counts), ranks 8..256 (r > 128 is SIMT at any length), and h_in up to 11008 (several
-    shrink k-splits whose partials the expand sums in split order)."""
+    """Decode-shaped batches forced onto the SIMT tier: 1-8-token segments (the expand's 2-token
+    passes, odd counts), ranks 8..256, and h_in up to 11008 (several shrink k-splits whose partials
+    the expand sums in split order)."""
     lengths = [1, 2, 3, 1, 5, 8, 1, 2, 7, 4, 1, 6, 2, 1]
     ranks = [8, 16, 32, 64, 128, 256, 8, 200, 24, 40, 136, 16, 64, 8]
     case = Case(h_in, h_out, lengths, ranks, seed=12)
-    err, bp = _check(case)
+    err, bp = _check(case, SIMT)
     s = bp.shape_plans[(h_in, h_out)].summary
     assert s[5] == 0   # every segment on the SIMT tier
-    outs, _ = case.run_gpu(repeat=2)
+    outs, _ = case.run_gpu(tier_policy=SIMT, repeat=2)
     assert torch.equal(outs[0], outs[1])   # deterministic k-split sums
 
 

@@ -121,9 +121,17 @@ def test_forced_policies():
     assert [int(m[2]) for m in d["mtiles"]] == [2, 64, 64]
     items = {(int(r[6]), int(r[4])) for r in d["expand"]}
     assert len(items) == d["n_expand"] == 4096 // 256 + 2 * (4096 // 128)
-    # AUTO: a long rank-256 segment is no longer sent to SIMT; a 5-token one is
-    d = _decode(_plan([0, 5, 300], [256, 256])[0])
+    # AUTO: a long rank-256 segment is no longer sent to SIMT; a 1-token one is
+    d = _decode(_plan([0, 1, 300], [256, 256])[0])
     assert list(d["tier"]) == [1, 2] and d["n_mtiles"] == 5
+
+
+@pytest.mark.parametrize("n,r,tier", [(4, 8, 1), (5, 8, 2), (4, 16, 1), (8, 16, 2), (2, 32, 1), (3, 32, 2),
+                                      (1, 64, 1), (2, 64, 2), (1, 128, 2), (1, 256, 1), (2, 256, 2)])
+def test_auto_rule_follows_the_tier_sweep(n, r, tier):
+    """The AUTO thresholds of profiles/r2_tier_sweep.txt (lsv_api.cu simt_max_tok)."""
+    d = _decode(_plan([0, n], [r])[0])
+    assert int(d["tier"][0]) == tier
 
 
 def test_split_v_doubles_the_v_image_region():
@@ -232,7 +240,8 @@ def test_simt_tail_row_block_map(P):
     ranks = [8, 24, 128, 256, 40, 16]
     lens = [1, 3, 8, 2, 5, 1]
     indptr = np.concatenate(([0], np.cumsum(lens)))
-    blob, _ = _plan_group(indptr, ranks, 4096, [1024] * P) if P > 1 else _plan(indptr, ranks, 4096, 1024)
+    blob, _ = (_plan_group(indptr, ranks, 4096, [1024] * P, policy=native.TIER_SIMT) if P > 1
+               else _plan(indptr, ranks, 4096, 1024, policy=native.TIER_SIMT))
     d = _decode(blob)
     n = d["n_simt"]
     assert n == len(ranks) and d["n_mtiles"] == 0
