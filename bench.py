@@ -449,6 +449,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         extra["dp_like_for_like"] = dp_one_server(args, torch, dev)
         extra["c1"] = c1_line(args, torch, dev)
+        extra["fused_linear"] = fused_linear_line(args, torch, dev, wl)
 
     if rank != 0:
         return None
@@ -611,6 +612,95 @@ def c1_line(args, torch, dev, replays=1000):
             "cpu": {"us_per_call": cpu_us, "tokens_per_s": seg.num_tokens / (cpu_us * 1e-6),
                     "cores": oracle.cpu_threads(), "kind": "port",
                     "sample": f"all of config 1, {reps} calls, no extrapolation"}}
+
+
+def fused_linear_line(args, torch, dev, wl, layers=4):
+    """a LoRA linear layer = base projection GEMM + the adapter delta, on C2's
+    batch and shapes (Llama-2-7B, 4096 tokens, 100 adapters), ``layers`` distinct layers per step
+    (weights and activations beyond L2).  Three ways on the same box, CUDA-graph replay:
+      base      cuBLAS (torch.matmul) base GEMMs only, the floor the delta adds to
+      separate  cuBLAS base GEMMs + the delta path (fused group shrink + group expand: y += delta)
+      fused     lsv_lora_fused_linear: group shrink + one GEMM whose TMEM tile also accumulates v·B
+    Tensor roofline: (base + LoRA) FLOPs / time against MEASURED_PEAKS.json bf16_tflops_sustained."""
+    import zlib
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, algorithmic_flops, input_group
+    from paper_2511_22880_b200.shapes import ModelShape
+    from paper_2511_22880_b200.slab import AdapterSlab
+    model = ModelShape("llama-2-7b-%d-layers" % layers, layers, wl.model.projections)
+    seg = wl.segments
+    N = seg.num_tokens
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, wl.ranks), dev)
+    for aid, r in zip(wl.adapter_ids, wl.ranks):
+        slab.fill_random(slab.allocate(aid, r), 1000 + zlib.crc32(aid.encode()) % 100000)
+    eng = LoraDeltaEngine(slab, v_bf16=args.v_bf16)
+    bp_sep = eng.prepare(seg)
+    bp_fus = eng.prepare(seg, fused_linear=True)
+    g = torch.Generator(device=dev).manual_seed(5)
+    projs = model.projections
+    W = [[(torch.randn(pr.h_out, pr.h_in, device=dev, generator=g) / pr.h_in ** 0.5).to(torch.bfloat16)
+          for pr in projs] for _ in range(layers)]
+    xs = [{input_group(pr.name): torch.randn(N, pr.h_in, device=dev, generator=g).to(torch.bfloat16)
+           for pr in projs} for _ in range(layers)]
+    ys = [[torch.empty(N, pr.h_out, device=dev, dtype=torch.bfloat16) for pr in projs] for _ in range(layers)]
+    stream = torch.cuda.Stream(dev)
+
+    def base():
+        for l in range(layers):
+            for p, pr in enumerate(projs):
+                torch.matmul(xs[l][input_group(pr.name)], W[l][p].t(), out=ys[l][p])
+
+    def separate():
+        base()
+        for l in range(layers):
+            for gi, (gname, members) in enumerate(eng.groups):
+                eng.shrink(bp_sep, l, members[0], xs[l][gname], stream)
+                eng.expand_group(bp_sep, l, gi, [ys[l][p] for p in members], stream)
+
+    def fused():
+        for l in range(layers):
+            for gi, (gname, members) in enumerate(eng.groups):
+                eng.linear_group(bp_fus, l, gi, xs[l][gname], [W[l][p] for p in members], [ys[l][p] for p in members],
+                                 stream)
+
+    res = {}
+    for name, fn in (("base", base), ("separate", separate), ("fused", fused)):
+        res[name] = time_graph(torch, eng, None, None, None, stream, max(args.steps, 10), args.warmup, dev,
+                               step_fn=fn) / layers
+    # parity of the fused layer against the separate path on one projection (both bf16 outputs)
+    y_ref = torch.matmul(xs[0]["attn_in"], W[0][0].t())
+    y_sep = y_ref.clone()
+    eng.shrink(bp_sep, 0, 0, xs[0]["attn_in"])
+    eng.expand(bp_sep, 0, 0, y_sep)
+    fused()
+    torch.cuda.synchronize(dev)
+    agree = float((ys[0][0].float() - y_sep.float()).abs().max() / y_sep.float().abs().max())
+    base_flops = sum(2 * N * pr.h_in * pr.h_out for pr in projs)
+    lora_flops = sum(algorithmic_flops(seg, pr.h_in, pr.h_out) for pr in projs)
+    peak = tflops_peak()
+    out = {"workload": f"{wl.description.split(',')[0].replace('32 layers', '%d layers' % layers)}; base GEMMs "
+                       f"{N}x{{4096,11008}}, per layer", "layers_timed": layers,
+           "tokens": N, "peak_tflops": peak[0], "peak_source": peak[1],
+           "agreement_vs_separate": agree,
+           "timing": "CUDA-graph replay of the whole multi-layer step, CUDA events, per layer"}
+    for name, ms in res.items():
+        fl = base_flops + (lora_flops if name != "base" else 0)
+        out[name] = {"ms_per_layer": ms, "tokens_per_s": N / (ms * 1e-3), "tflops": fl / (ms * 1e-3) / 1e12,
+                     "tensor_frac": fl / (ms * 1e-3) / 1e12 / peak[0]}
+    out["fused_vs_separate_speedup"] = res["separate"] / res["fused"]
+    out["delta_overhead_separate"] = res["separate"] / res["base"] - 1
+    out["delta_overhead_fused"] = res["fused"] / res["base"] - 1
+    del eng, bp_sep, bp_fus, slab, W, xs, ys
+    torch.cuda.synchronize(dev)
+    return out
+
+
+def tflops_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["bf16_tflops_sustained"]), "measured sustained (MEASURED_PEAKS.json)"
+    except Exception:
+        return 2250.0 * 0.6, "fallback"
 
 
 def measured_traffic(config, label):

@@ -66,6 +66,11 @@ extern "C" {
  * delta matches the fp32-v SGMV result up to the final bf16 rounding of y; the single image rounds
  * v to bf16 (8 bits) first, costing less workspace and expand ring bytes. */
 #define LSV_PLAN_V_BF16 0x100
+/* Plan flag: tile-aligned v images for lsv_lora_fused_linear (the base projection GEMM with the
+ * LoRA expand accumulated in its TMEM tile).  Every segment is split at the batch's 128-token tile
+ * boundaries and each piece's v image spans its whole tile (zero rows outside the piece), so an
+ * M=128 MMA adds v·B into exactly the piece's rows.  Tensor-core tier only. */
+#define LSV_PLAN_TILE_ALIGNED 0x200
 
 typedef void* lsv_stream_t; /* a cudaStream_t */
 
@@ -205,6 +210,23 @@ size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const 
 int lsv_lora_expand_proj(void* y, int64_t ldy, int32_t num_tokens, int32_t h_out, int32_t proj,
                          const void* const* b_ptrs, const void* plan_dev, const void* plan_host,
                          void* workspace, size_t workspace_bytes, lsv_stream_t stream);
+
+/* ---- base projection GEMM with the LoRA delta fused -------------------
+ * One LoRA linear layer for an input group, y_p = x · W_p^T + delta_p for every member p, with the
+ * delta accumulated into the base GEMM's TMEM tile (no y read-modify-write): the prices
+ * costmodel.prefill_time (costmodel.py:104-105) puts on "base GEMM + adapter" as one batch cost.
+ *   x      : [num_tokens][h_in] bf16 (device), row stride ldx
+ *   a_ptrs : device table [S] of the segments' group A tiles; runs the shrink of the plan first.
+ *            NULL: the v images are already in the workspace (a previous lsv_lora_shrink).
+ *   w, ldw : HOST arrays [num_proj]: base weight W_p [h_out_p][h_in] bf16 (nn.Linear layout, device)
+ *   ys     : HOST array [num_proj] of outputs [num_tokens][h_out_p] bf16, written (not accumulated);
+ *            32-byte aligned rows (ldy % 16 == 0)
+ *   b_ptrs : HOST array [num_proj] of device tables [S] of B tile pointers
+ * The plan must be built with LSV_PLAN_TILE_ALIGNED; every h_out must be a multiple of 256. */
+int lsv_lora_fused_linear(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in, const void* const* a_ptrs,
+                          const void* const* w, const int64_t* ldw, void* const* ys, const int64_t* ldys,
+                          const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host,
+                          void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
 /* ---- tensor parallelism -------------------------------------------------------------------
  * Column-parallel projections shard each adapter's rank over the TP group: rank t's shrink

@@ -18,6 +18,7 @@
 
 #include "../../include/lsv.h"
 #include "lsv_common.cuh"
+#include "lsv_fused.cuh"
 #include "lsv_plan.h"
 #include "lsv_simt.cuh"
 #include "lsv_tc.cuh"
@@ -119,6 +120,7 @@ struct PlanBuilder {
   std::vector<int32_t> red;          // {mtile, first unit} per split tile
   int32_t red_units = 0;
   std::vector<int32_t> red_cta;
+  std::vector<int32_t> tile_mt;      // tile-aligned plans: [n_gemm_tiles + 1] first piece per tile
 };
 
 // LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
@@ -192,11 +194,16 @@ int subset_np(int P, int p0, int r) { return std::max(1, std::min(P - p0, 256 / 
 int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
                const int32_t* h_outs, int32_t policy) {
   if (int rc = validate_segments(S, indptr, rank, h_in, P, h_outs)) return rc;
-  if (policy & ~(0xff | LSV_PLAN_V_BF16)) return fail(LSV_EINVAL, "unknown plan flags 0x%x", policy);
+  if (policy & ~(0xff | LSV_PLAN_V_BF16 | LSV_PLAN_TILE_ALIGNED))
+    return fail(LSV_EINVAL, "unknown plan flags 0x%x", policy);
   const int vsplit = (policy & LSV_PLAN_V_BF16) ? 0 : 1;
+  const bool tile_aligned = (policy & LSV_PLAN_TILE_ALIGNED) != 0;
   policy &= 0xff;
   if (policy != LSV_TIER_AUTO && policy != LSV_TIER_SIMT && policy != LSV_TIER_TC)
     return fail(LSV_EINVAL, "unknown tier policy %d", policy);
+  if (tile_aligned && policy == LSV_TIER_SIMT)
+    return fail(LSV_EINVAL, "tile-aligned plans (LSV_PLAN_TILE_ALIGNED) are tensor-core tier only");
+  if (tile_aligned) policy = LSV_TIER_TC;   // every segment's v feeds the fused GEMM's M=128 tiles
   const int N = S > 0 ? indptr[S] : 0;
   pb.indptr.assign(indptr, indptr + S + 1);
   if (S == 0) pb.indptr.assign(1, 0);
@@ -219,6 +226,14 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         const int nt = std::min(kSimtMaxTok, n - tb);
         pb.simt.push_back(SimtItem{s, indptr[s] + tb, nt | rank[s] << 16, (int32_t)v_off});
         v_off += (int64_t)nt * rank[s];
+      }
+    } else if (tile_aligned) {   // pieces of the segment inside each 128-token tile of the batch
+      for (int t = indptr[s]; t < indptr[s + 1];) {
+        const int e = std::min(indptr[s + 1], (t / kTileM + 1) * kTileM);
+        MTile mt{};
+        mt.seg = s; mt.tok_begin = t; mt.ntok = e - t; mt.rank = rank[s];
+        pb.mtiles.push_back(mt);
+        t = e;
       }
     } else {
       const int tm = mtile_rows(rank[s]);
@@ -258,12 +273,13 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     mt.part_off = (int32_t)part_off;
     if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * G;
     mt.vimg_off = (int32_t)vimg_off;  // 1024-aligned: the v image's swizzle atoms are address-based
-    vimg_off += (int64_t)vimg_bytes(mt.ntok, kpad(r)) * (vsplit ? 2 : 1);   // split v: hi image, lo image
+    // split v: hi image, lo image; tile-aligned images span the whole 128-row tile
+    vimg_off += (int64_t)vimg_bytes(tile_aligned ? kTileM : mt.ntok, kpad(r)) * (vsplit ? 2 : 1);
     mt.counter = counter++;
     if (nsplit > 1) {  // reduction units: (token, projection, 8 padded-k) of this tile, reduced grid-wide
       pb.red.push_back((int32_t)i);
       pb.red.push_back(pb.red_units);
-      pb.red_units += mt.ntok * P * (kpad(r) / 8);
+      pb.red_units += (tile_aligned ? kTileM : mt.ntok) * P * (kpad(r) / 8);   // tile-aligned: zero rows too
     }
     for (int p0 = 0; p0 < P; p0 += subset_np(P, p0, r)) {
       const int np = subset_np(P, p0, r), rows = np * r;
@@ -393,6 +409,17 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   }
   h.off_red_cta = off; off += (int32_t)red_cta.size();
   pb.red_cta = red_cta;
+  h.tile_aligned = tile_aligned ? 1 : 0;
+  if (tile_aligned) {   // [n_gemm_tiles + 1] first piece of every 128-token tile (pieces are in token order)
+    const int nt = (N + kTileM - 1) / kTileM;
+    pb.tile_mt.assign(nt + 1, 0);
+    size_t i = 0;
+    for (int t = 0; t <= nt; ++t) {
+      while (i < pb.mtiles.size() && pb.mtiles[i].tok_begin < t * kTileM) ++i;
+      pb.tile_mt[t] = (int32_t)i;
+    }
+    off += nt + 1;
+  }
   h.total_ints = off;
   int64_t ws = 0;
   h.ws_counters = 0; ws += kBarHeaderBytes;   // barrier header (lsv_plan.h): pair 0 for standalone calls
@@ -458,9 +485,10 @@ std::unordered_map<MapKey, std::vector<CUtensorMap>, MapKeyHash> g_map_cache;
 
 // kind 0: x maps (5 boxes of 64 cols x 8<<b rows, SWIZZLE_128B)
 // kind 1: y maps (8 boxes of 128 cols x 1<<b rows, no swizzle)
+// kind 2: base-weight maps (1 box of 64 cols x 256 rows, SWIZZLE_128B)
 int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t rows, int32_t cols) {
   const MapKey key{reinterpret_cast<uintptr_t>(ptr), ld, rows, cols, kind};
-  const int nmaps = kind == 0 ? 5 : 8;
+  const int nmaps = kind == 0 ? 5 : kind == 1 ? 8 : 1;
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_map_cache.find(key);
@@ -475,12 +503,12 @@ int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t ro
   for (int b = 0; b < nmaps; ++b) {
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)kChunk : (cuuint32_t)128,
-                               kind == 0 ? (cuuint32_t)(8 << b) : (cuuint32_t)(1 << b)};
+    const cuuint32_t box[2] = {kind == 1 ? (cuuint32_t)128 : (cuuint32_t)kChunk,
+                               kind == 0 ? (cuuint32_t)(8 << b) : kind == 1 ? (cuuint32_t)(1 << b) : (cuuint32_t)kFusedTileN};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     kind == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) kind %d box %d", (int)r, kind, b);
@@ -500,6 +528,9 @@ int ensure_smem_attrs() {
                                           shrink_smem_bytes());
     cudaError_t e2 = cudaFuncSetAttribute(expand_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           expand_smem_bytes());
+    cudaError_t e3 = cudaFuncSetAttribute(fused_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          fused_smem_bytes());
+    if (e2 == cudaSuccess) e2 = e3;
     rc = (e1 == cudaSuccess && e2 == cudaSuccess) ? LSV_OK : LSV_ECUDA;
     if (rc) fail(LSV_ECUDA, "cudaFuncSetAttribute(smem) failed: %s / %s", cudaGetErrorString(e1), cudaGetErrorString(e2));
   });
@@ -584,6 +615,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.off_red_cta = h->off_red_cta;
     p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
     p.vsplit = h->vsplit;
+    p.tile_aligned = h->tile_aligned;
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     if (tps != nullptr) {
       p.tp = tps->tp; p.tp_rank = tps->tp_rank;
@@ -607,6 +639,8 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
                const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws, cudaStream_t st,
                const uint8_t* vimg_base = nullptr, int32_t* wait_flag = nullptr, int32_t wait_target = 0,
                const uint8_t* xsum = nullptr, bool simt_pdl = false) {
+  if (h->tile_aligned)
+    return fail(LSV_EINVAL, "a tile-aligned plan (LSV_PLAN_TILE_ALIGNED) feeds lsv_lora_fused_linear, not the expand");
   if (h->n_simt_items > 0) {   // every member in one launch per token class (grid.z = member)
     SimtExpandArgs a{};
     int max_tiles = 0;
@@ -802,6 +836,7 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   std::copy(pb.expand_all_cta.begin(), pb.expand_all_cta.end(), out + h.off_expand_cta_all);
   std::copy(pb.red.begin(), pb.red.end(), out + h.off_red);
   std::copy(pb.red_cta.begin(), pb.red_cta.end(), out + h.off_red_cta);
+  if (h.tile_aligned) std::copy(pb.tile_mt.begin(), pb.tile_mt.end(), out + h.total_ints - (int32_t)pb.tile_mt.size());
   return LSV_OK;
 }
 
@@ -1053,6 +1088,7 @@ int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, i
   if (!x || !a_ptrs || !aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "bad x / a_ptrs");
   for (int d = 0; d < tp; ++d)
     if (!vfull_dst[d] || !flags[d]) return fail(LSV_EINVAL, "rank %d: null destination or flag", d);
+  if (h->tile_aligned || fh->tile_aligned) return fail(LSV_EUNSUPPORTED, "TP scatter with a tile-aligned plan");
   TpScatter tps;
   tps.tp = tp; tps.tp_rank = tp_rank; tps.fh = fh; tps.fplan = static_cast<const int32_t*>(full_plan_dev);
   tps.vdst = vfull_dst; tps.flags = flags;
@@ -1088,6 +1124,7 @@ int lsv_lora_shrink_tp_partials(const void* x, int64_t ldx, int32_t num_tokens, 
   if (!x || !a_ptrs || !aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "bad x / a_ptrs");
   for (int d = 0; d < tp; ++d)
     if (!xdst[d] || !flags[d]) return fail(LSV_EINVAL, "rank %d: null destination or flag", d);
+  if (h->tile_aligned) return fail(LSV_EUNSUPPORTED, "TP partial exchange with a tile-aligned plan");
   TpScatter tps;
   tps.tp = tp; tps.tp_rank = tp_rank; tps.row = 1; tps.fh = h; tps.fplan = static_cast<const int32_t*>(plan_dev);
   tps.vdst = xdst; tps.flags = flags;
@@ -1133,6 +1170,67 @@ int lsv_lora_apply(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t dty
                                stream))
     return rc;
   return lsv_lora_expand(y, ldy, num_tokens, h_out, b_ptrs, plan_dev, plan_host, workspace, workspace_bytes, stream);
+}
+
+int lsv_lora_fused_linear(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in, const void* const* a_ptrs,
+                          const void* const* w, const int64_t* ldw, void* const* ys, const int64_t* ldys,
+                          const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host, void* workspace,
+                          size_t workspace_bytes, lsv_stream_t stream) {
+  const PlanHeader* h = check_plan(plan_host);
+  if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
+  if (!h->tile_aligned) return fail(LSV_EINVAL, "lsv_lora_fused_linear needs a plan built with LSV_PLAN_TILE_ALIGNED");
+  if (h->h_in != h_in) return fail(LSV_EINVAL, "h_in %d does not match the plan's %d", h_in, h->h_in);
+  if (num_tokens < h->num_tokens)
+    return fail(LSV_EINVAL, "num_tokens %d is smaller than the plan's %d", num_tokens, h->num_tokens);
+  if (!x || !aligned16(x) || ldx % 8 || ldx < h_in) return fail(LSV_EINVAL, "x must be 16-byte aligned with ldx %% 8 == 0, ldx >= h_in");
+  if (!w || !ldw || !ys || !ldys || !b_ptrs) return fail(LSV_EINVAL, "w / ldw / ys / ldys / b_ptrs must be non-null host arrays");
+  const int P = h->num_proj;
+  for (int pp = 0; pp < P; ++pp) {
+    if (h->h_outs[pp] % kFusedTileN)
+      return fail(LSV_EUNSUPPORTED, "member %d: h_out %d is not a multiple of %d", pp, h->h_outs[pp], kFusedTileN);
+    if (!w[pp] || !aligned16(w[pp]) || ldw[pp] % 8 || ldw[pp] < h_in)
+      return fail(LSV_EINVAL, "member %d: W must be [h_out][h_in] bf16, 16-byte aligned, ldw %% 8 == 0", pp);
+    if (!ys[pp] || (reinterpret_cast<uintptr_t>(ys[pp]) & 31) || ldys[pp] % 16 || ldys[pp] < h->h_outs[pp])
+      return fail(LSV_EINVAL, "member %d: y must be 32-byte aligned with ldy %% 16 == 0, ldy >= h_out", pp);
+    if (!b_ptrs[pp]) return fail(LSV_EINVAL, "member %d: b_ptrs is null", pp);
+  }
+  if (num_tokens == 0) return LSV_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  // the shrink of the tile-aligned plan (skipped when a_ptrs is NULL: v images already in ws)
+  if (a_ptrs && h->num_tokens > 0)
+    if (int rc = run_shrink(h, x, ldx, num_tokens, a_ptrs, static_cast<const int32_t*>(plan_dev), ws, st)) return rc;
+  if (int rc = ensure_smem_attrs()) return rc;
+  FusedParams p{};
+  CUtensorMap xm[5];
+  if (int rc = get_maps(xm, 0, x, ldx, num_tokens, h_in)) return rc;
+  p.xmap = xm[4];   // 64 cols x 128 rows
+  int items = 0;
+  const int mt = (num_tokens + kTileM - 1) / kTileM;
+  for (int pp = 0; pp < P; ++pp) {
+    if (int rc = get_maps(&p.wmap[pp], 2, w[pp], ldw[pp], h->h_outs[pp], h_in)) return rc;
+    p.b_ptrs[pp] = b_ptrs[pp];
+    p.y[pp] = static_cast<__nv_bfloat16*>(ys[pp]);
+    p.ldy[pp] = ldys[pp];
+    p.ws_vimg[pp] = h->ws_vimg + pp * h->vimg_stride;
+    p.n_ntiles[pp] = h->h_outs[pp] / kFusedTileN;
+    p.item_base[pp] = items;
+    items += mt * p.n_ntiles[pp];
+  }
+  for (int pp = P; pp <= kMaxProj; ++pp) p.item_base[pp] = items;
+  // tokens past the plan's batch (num_tokens > plan tokens) get the base GEMM only: tiles past the
+  // plan's last tile see no pieces (their tile_mt range is empty)
+  if (mt > (h->num_tokens + kTileM - 1) / kTileM)
+    return fail(LSV_EINVAL, "num_tokens %d spans more 128-token tiles than the plan's %d tokens", num_tokens,
+                h->num_tokens);
+  p.plan = static_cast<const int32_t*>(plan_dev);
+  p.ws = ws;
+  p.num_tokens = num_tokens; p.h_in = h_in; p.vsplit = h->vsplit; p.n_mtiles = mt;
+  p.off_mtiles = h->off_mtiles;
+  p.off_tile_mt = h->total_ints - ((h->num_tokens + kTileM - 1) / kTileM + 1);
+  LSV_CUDA_CHECK(launch_pdl(fused_linear_kernel, std::min(items, num_sms_cached()), fused_smem_bytes(), st, p, true,
+                            kFusedThreads));
+  return LSV_OK;
 }
 
 // Debug only (not part of include/lsv.h): route per-item globaltimer stamps of the tcgen05

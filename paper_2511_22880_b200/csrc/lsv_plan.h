@@ -46,7 +46,11 @@ struct PlanHeader {            // 64 int32
   int32_t expand_grid_p[kMaxProj], n_expand_items_p[kMaxProj];
   int32_t off_expand_recs_all, off_expand_cta_all, expand_grid_all, n_expand_all;  // every member, one LPT list
   int32_t vsplit;                      // 1: each tcgen05 v image is a bf16 (hi, lo) pair, v = hi + lo to ~2^-16
-  int32_t reserved[64 - 62];
+  // tile-aligned plans (LSV_PLAN_TILE_ALIGNED, for the fused base-GEMM kernel): m-tiles are the
+  // pieces of segments inside each 128-token tile of the batch; a piece's v image has 128 rows (the
+  // tile's) with the piece at rows [tok_begin % 128, +ntok) and zeros elsewhere
+  int32_t tile_aligned;
+  int32_t reserved[64 - 63];
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 
@@ -61,6 +65,8 @@ struct SimtItem {              // 4 int32
 constexpr int kSimtShrRows = LSV_SIMT_SHR_ROWS;   // group-A rows per SIMT shrink block (8 or 16)
 __host__ __device__ inline int simt_nt(const SimtItem& it) { return it.nt_rank & 0xffff; }
 __host__ __device__ inline int simt_rank(const SimtItem& it) { return it.nt_rank >> 16; }
+// Tile-aligned plans append [n_gemm_tiles + 1] first-piece indices after the split-K tables
+// (off_tile_mt = total_ints - n_gemm_tiles - 1; n_gemm_tiles = ceil(num_tokens / 128)).
 // The SIMT tail of a plan, after the items: the shrink's row-block prefix [n + 1] over the items
 // (8-row blocks of each item's group A), then one int per row block: item << 8 | row block.
 

@@ -45,6 +45,7 @@ struct alignas(64) ShrinkParams {
   int num_proj, vimg_stride;    // input group: projections shrunk together, bytes between their v images
   int acc_cols;                 // TMEM accumulator width (128 -> 4 buffers, 256 -> 2)
   int vsplit;                   // 1: v images are bf16 (hi, lo) pairs (PlanHeader::vsplit)
+  int tile_aligned;             // 1: 128-row tile-aligned images, zero rows outside the piece
   int wait_prev;                // 0: the previous launch is another input group's expand, which this
                                 // launch neither reads nor overwrites: start without waiting for it
   // tensor-parallel scatter (tp > 0): instead of this rank's shard images, every (token, member,
@@ -310,7 +311,7 @@ __device__ __forceinline__ RedUnit red_unit(const ShrinkParams& p, int u, int e)
 __device__ __forceinline__ void red_sum(const ShrinkParams& p, const RedUnit& ru, float* s8) {
 #pragma unroll
   for (int q8 = 0; q8 < 8; ++q8) s8[q8] = 0.f;
-  if (ru.k0 >= ru.mt.rank) return;
+  if (ru.k0 >= ru.mt.rank || ru.t >= ru.mt.ntok) return;   // k pad / tile-aligned zero rows
   const float* partials = reinterpret_cast<const float*>(p.ws + p.ws_partials);
   const int G = p.num_proj * ru.mt.rank;
   const size_t stride = (size_t)ru.mt.ntok * G;
@@ -333,9 +334,12 @@ __device__ __forceinline__ void red_store(const ShrinkParams& p, const RedUnit& 
     if (ru.k0 < ru.mt.rank) tp_scatter(p, red[2 * ru.e], ru.pp, ru.t, ru.k0, ru.mt.rank, np16, w, wlo);
     if (ru.k0 == 0) tp_scatter_pad(p, red[2 * ru.e], ru.pp, ru.t, np16);   // once per (token, member)
   } else {
-    uint8_t* dst = p.ws + p.ws_vimg + (size_t)ru.pp * p.vimg_stride + ru.mt.vimg_off + vimg_off(ru.t, ru.k0, kp, np16);
+    // tile-aligned: the piece's rows sit at its offset inside the 128-row tile image
+    const int irow = p.tile_aligned ? ((ru.mt.tok_begin + ru.t) & (kTileM - 1)) : ru.t;
+    const int rpad = p.tile_aligned ? kTileM : np16;
+    uint8_t* dst = p.ws + p.ws_vimg + (size_t)ru.pp * p.vimg_stride + ru.mt.vimg_off + vimg_off(irow, ru.k0, kp, rpad);
     *reinterpret_cast<uint4*>(dst) = w;
-    if (p.vsplit) *reinterpret_cast<uint4*>(dst + vimg_bytes(ru.mt.ntok, kp)) = wlo;
+    if (p.vsplit) *reinterpret_cast<uint4*>(dst + vimg_bytes(rpad, kp)) = wlo;
   }
 }
 
@@ -476,12 +480,17 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
       const bool valid = row < nt && !(p.dbg & 8);
       uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
-      const uint32_t vlo = vimg_bytes(nt, kp);                  // hi image -> lo image (split v)
+      // tile-aligned images (fused base GEMM): 128 rows, this piece at rows tok_begin % 128 + row,
+      // every other row zero; each thread writes image row (tok_begin + row) % 128, zeros if !valid
+      const bool ta = p.tile_aligned != 0;
+      const int irow = ta ? ((inf.tok_begin + row) & (kTileM - 1)) : row, rpad = ta ? kTileM : np16;
+      const bool wimg = ta ? !(p.dbg & 8) : valid;              // writes an image row (nsplit == 1)
+      const uint32_t vlo = vimg_bytes(rpad, kp);                // hi image -> lo image (split v)
       float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
       for (int cc = 0; cc < rows; cc += 16) {
         float v[16];
         tmem_ld_32x32b_x16(taddr + cc, v);
-        if (valid) {
+        if (valid || (wimg && inf.nsplit == 1)) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int j0 = cc + h * 8;          // 8 columns, all of projection p0 + j0 / r (r % 8 == 0)
@@ -489,11 +498,12 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
               if (inf.nsplit == 1) {
                 uint4 w, wlo;
                 split_bf16x8(v + h * 8, w, wlo);
+                if (!valid) w = wlo = make_uint4(0, 0, 0, 0);   // tile-aligned zero row
                 const int pp = inf.p0 + j0 / r;
                 if (p.tp > 0 && p.tp_row) tp_row_put(p, inf.mtile, pp, row, j0 % r, v + h * 8);
                 else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w, wlo);
                 else {
-                  uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(row, j0 % r, kp, np16);
+                  uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, j0 % r, kp, rpad);
                   *reinterpret_cast<uint4*>(dst) = w;
                   if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = wlo;
                 }
@@ -513,9 +523,9 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       if (valid && inf.nsplit == 1 && p.tp > 0) {
         if (!p.tp_row)
           for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
-      } else if (valid && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
+      } else if (wimg && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
         for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) {
-          uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(row, r, kp, np16);
+          uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, r, kp, rpad);
           *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
           if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = make_uint4(0, 0, 0, 0);
         }

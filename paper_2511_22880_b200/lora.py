@@ -168,16 +168,19 @@ class LoraDeltaEngine:
 
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
-                peer_slabs: dict[int, AdapterSlab] | None = None, stream=None) -> BatchPlan:
+                peer_slabs: dict[int, AdapterSlab] | None = None, stream=None,
+                fused_linear: bool = False) -> BatchPlan:
         """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
         uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
-        k+1 on the host while batch k still runs there."""
+        k+1 on the host while batch k still runs there.  ``fused_linear``: tile-aligned plans for
+        ``linear_group`` (base GEMM with the delta fused, LSV_PLAN_TILE_ALIGNED; tensor-core tier)."""
         ws_need = 0
         projs = self.model.projections
         # the group plans are independent host work; ctypes drops the GIL inside the C++ planner,
         # so they build in parallel
+        policy = self.tier_policy | (native.PLAN_TILE_ALIGNED if fused_linear else 0)
         futs = [self._pool.submit(build_group_plan, seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
-                                  self.tier_policy, self.device, members, stream is None)
+                                  policy, self.device, members, stream is None)
                 for _, members in self.groups]
         plans = [f.result() for f in futs]
         # forward: one workspace slice per (layer, group) (lsv_lora_forward_workspace)
@@ -194,7 +197,7 @@ class LoraDeltaEngine:
             for gp, t in zip(plans, up):
                 gp.plan_dev = t
             a_dev, b_dev = up[-2], up[-1]
-        bp = BatchPlan(seg, plans, a_dev, b_dev, self._workspace, self.tier_policy)
+        bp = BatchPlan(seg, plans, a_dev, b_dev, self._workspace, policy)
         if stream is not None:
             bp.extra["ring_tag"] = tag
         return bp
@@ -309,6 +312,38 @@ class LoraDeltaEngine:
             ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr(), bp.b_ptrs.data_ptr(),
             xs[0][self.groups[0][0]].shape[0], bp.workspace.data_ptr(), bp.workspace.numel(),
             native.FWD_SERIAL if serial else 0, st.cuda_stream))
+
+    def linear_group(self, bp: BatchPlan, layer: int, gi: int, x: torch.Tensor, weights: list[torch.Tensor],
+                     ys: list[torch.Tensor], stream=None) -> None:
+        """One LoRA linear layer for input group gi: ys[i] = x · weights[i]^T + delta_i for every member
+        (weights[i]: the base projection's nn.Linear weight [h_out, h_in] bf16), with the delta
+        accumulated into the base GEMM's TMEM tile (lsv_lora_fused_linear: the group's shrink, then
+        one fused GEMM launch for every member).  ``bp`` from ``prepare(seg, fused_linear=True)``."""
+        self._live(bp)
+        if not (bp.tier_policy & native.PLAN_TILE_ALIGNED):
+            raise ValueError("linear_group needs a plan from prepare(seg, fused_linear=True)")
+        gp = bp.group_plans[gi]
+        members = self.groups[gi][1]
+        n = len(members)
+        if len(weights) != n or len(ys) != n:
+            raise ValueError(f"input group {self.groups[gi][0]} has {n} members")
+        projs = self.model.projections
+        for w, y, p in zip(weights, ys, members):
+            self._check_io(x, y, projs[p].h_in, projs[p].h_out, bp.num_tokens)
+            if w.dtype != torch.bfloat16 or tuple(w.shape) != (projs[p].h_out, projs[p].h_in) or w.stride(1) != 1:
+                raise ValueError(f"weight of {projs[p].name} must be bf16 [{projs[p].h_out}, {projs[p].h_in}]")
+        S = bp.segments.num_segments
+        P = len(projs)
+        st = stream or torch.cuda.current_stream(self.device)
+        arr = lambda t, v: (t * len(v))(*v)   # noqa: E731
+        wa, lw = arr(ctypes.c_void_p, [w.data_ptr() for w in weights]), arr(ctypes.c_int64, [w.stride(0) for w in weights])
+        ya, ly = arr(ctypes.c_void_p, [y.data_ptr() for y in ys]), arr(ctypes.c_int64, [y.stride(0) for y in ys])
+        ba = arr(ctypes.c_void_p, [bp.b_ptrs.data_ptr() + (layer * P + p) * S * 8 for p in members])
+        native.check(native.lib().lsv_lora_fused_linear(
+            x.data_ptr(), x.stride(0), x.shape[0], gp.h_in, bp.a_ptrs.data_ptr() + (layer * len(self.groups) + gi) * S * 8,
+            ctypes.addressof(wa), ctypes.addressof(lw), ctypes.addressof(ya), ctypes.addressof(ly), ctypes.addressof(ba),
+            gp.plan_dev.data_ptr(), gp.plan_host.ctypes.data, bp.workspace.data_ptr(), bp.workspace.numel(),
+            st.cuda_stream))
 
     def forward_prefetch(self, bp: BatchPlan, pf: "RemotePrefetch", xs, ys, stream=None) -> None:
         """``forward`` with peer-owned adapters fetched one layer ahead into local staging buffers by

@@ -22,6 +22,7 @@ LSV_DTYPE_BF16 = 0
 ABI_VERSION = 3
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 FWD_SERIAL = 1
+PLAN_TILE_ALIGNED = 0x200   # plan flag: tile-aligned v images for lsv_lora_fused_linear
 PLAN_V_BF16 = 0x100   # plan flag: single bf16 v image on the tensor-core tier (default: hi/lo pair)
 
 # every symbol include/lsv.h declares (tests/test_native_abi.py checks the library exports them)
@@ -36,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "lsv_lora_forward", "lsv_lora_forward_ex", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
     "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum", "lsv_debug_set_trace",
+    "lsv_lora_fused_linear",
 )
 
 _lib = None
@@ -85,6 +87,8 @@ _SIGNATURES = {
     "lsv_lora_shrink_tp_partials": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
                                                    _vp, _vp, _vp]),
     "lsv_lora_expand_group_tp_sum": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp, _i32, _vp, _vp]),
+    "lsv_lora_fused_linear": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                             _vp]),
 }
 
 

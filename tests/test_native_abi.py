@@ -254,3 +254,35 @@ def test_simt_tail_row_block_map(P):
     rbmap = blob[d["off_simt"] + 5 * n + 1:d["off_simt"] + 5 * n + 1 + int(pre[-1])]
     want = [i << 8 | rb for i in range(n) for rb in range(nrb[i])]
     assert list(rbmap) == want
+
+
+def test_tile_aligned_plan_pieces():
+    """LSV_PLAN_TILE_ALIGNED: segments are cut at the batch's 128-token tile boundaries, every piece
+    is a tensor-core m-tile with a 128-row v image, and the tail [tiles + 1] indexes each tile's
+    first piece."""
+    lens = [5, 100, 60, 1, 90, 44]
+    ranks = [8, 64, 128, 16, 24, 256]
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    blob, _ = _plan(indptr, ranks, 1024, 512, policy=native.TIER_AUTO | native.PLAN_TILE_ALIGNED)
+    d = _decode(blob)
+    assert int(blob[62]) == 1 and d["n_simt"] == 0          # PlanHeader::tile_aligned; no SIMT items
+    mts = d["mtiles"]
+    for seg, tb, nt, r, *_ in mts:
+        assert tb // 128 == (tb + nt - 1) // 128            # never crosses a tile boundary
+    covered = np.zeros(int(indptr[-1]), dtype=int)
+    for seg, tb, nt, *_ in mts:
+        covered[tb:tb + nt] += 1
+    assert np.all(covered == 1)
+    ntiles = -(-int(indptr[-1]) // 128)
+    tail = blob[d["total_ints"] - ntiles - 1:d["total_ints"]]
+    assert tail[0] == 0 and tail[-1] == len(mts)
+    for t in range(ntiles):
+        for j in range(tail[t], tail[t + 1]):
+            assert int(mts[j][1]) // 128 == t
+    # v images: 128 rows x kpad(rank), hi + lo
+    offs = [int(m[6]) for m in mts]
+    kp = [max(16, -(-int(m[3]) // 16) * 16) for m in mts]
+    sizes = [(-(-128 * k * 2 // 1024) * 1024) * 2 for k in kp]
+    assert offs == list(np.concatenate(([0], np.cumsum(sizes)[:-1])))
+    with pytest.raises(ValueError, match="tile-aligned"):
+        _plan(indptr, ranks, 1024, 512, policy=native.TIER_SIMT | native.PLAN_TILE_ALIGNED)
