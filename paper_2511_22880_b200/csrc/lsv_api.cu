@@ -35,6 +35,7 @@ thread_local uint64_t* g_trace = nullptr;
 thread_local int g_trace_items = 0;
 const int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
 const int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
+const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -1228,6 +1229,8 @@ int lsv_lora_fused_linear(const void* x, int64_t ldx, int32_t num_tokens, int32_
   p.num_tokens = num_tokens; p.h_in = h_in; p.vsplit = h->vsplit; p.n_mtiles = mt;
   p.off_mtiles = h->off_mtiles;
   p.off_tile_mt = h->total_ints - ((h->num_tokens + kTileM - 1) / kTileM + 1);
+  p.dbg = g_debug_fused;
+  p.trace = g_trace; p.trace_items = g_trace_items;
   LSV_CUDA_CHECK(launch_pdl(fused_linear_kernel, std::min(items, num_sms_cached()), fused_smem_bytes(), st, p, true,
                             kFusedThreads));
   return LSV_OK;
