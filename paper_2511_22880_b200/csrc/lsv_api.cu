@@ -71,6 +71,16 @@ int simt_max_tok(int rank) {
   return 1;
 }
 bool auto_simt(int n, int rank) { return n <= simt_max_tok(rank); }
+// Batch level: a decode-shaped batch (no segment longer than kSimtMaxTok tokens) runs entirely on
+// the SIMT tier.  The sweep's thresholds compare batches of one (n, r) class; in a decode batch
+// the few segments they would move to tcgen05 bring that tier's launches (shrink + expand per
+// input group) for little work: C2's decode step (128 requests x 1 token, 100 adapters) measured
+// 7.32 ms per-segment vs 5.79 ms all-SIMT (profiles/r2_tier_sweep.txt, batch-level note).
+bool decode_shaped(int32_t S, const int32_t* indptr) {
+  for (int s = 0; s < S; ++s)
+    if (indptr[s + 1] - indptr[s] > kSimtMaxTok) return false;
+  return true;
+}
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
 #ifndef LSV_SHRINK_WAVES
 #define LSV_SHRINK_WAVES 8
@@ -213,6 +223,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int nsm = num_sms_cached();
 
   // tier per segment
+  const bool all_simt = policy == LSV_TIER_AUTO && decode_shaped(S, indptr);
   int64_t v_off = 0;
   for (int s = 0; s < S; ++s) {
     const int n = indptr[s + 1] - indptr[s];
@@ -220,7 +231,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     bool simt;
     if (policy == LSV_TIER_SIMT) simt = true;
     else if (policy == LSV_TIER_TC) simt = false;
-    else simt = auto_simt(n, rank[s]);
+    else simt = all_simt || auto_simt(n, rank[s]);
     pb.tier[s] = simt ? kTierSimt : kTierTc;
     if (simt) {
       for (int tb = 0; tb < n; tb += kSimtMaxTok) {

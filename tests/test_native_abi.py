@@ -123,15 +123,22 @@ def test_forced_policies():
     assert len(items) == d["n_expand"] == 4096 // 256 + 2 * (4096 // 128)
     # AUTO: a long rank-256 segment is no longer sent to SIMT; a 1-token one is
     d = _decode(_plan([0, 1, 300], [256, 256])[0])
-    assert list(d["tier"]) == [1, 2] and d["n_mtiles"] == 5
+    assert list(d["tier"]) == [1, 2] and d["n_mtiles"] == 5   # 1-token rank 256: SIMT (sweep)
 
 
 @pytest.mark.parametrize("n,r,tier", [(4, 8, 1), (5, 8, 2), (4, 16, 1), (8, 16, 2), (2, 32, 1), (3, 32, 2),
                                       (1, 64, 1), (2, 64, 2), (1, 128, 2), (1, 256, 1), (2, 256, 2)])
 def test_auto_rule_follows_the_tier_sweep(n, r, tier):
-    """The AUTO thresholds of profiles/r2_tier_sweep.txt (lsv_api.cu simt_max_tok)."""
-    d = _decode(_plan([0, n], [r])[0])
-    assert int(d["tier"][0]) == tier
+    """The AUTO thresholds of profiles/r2_tier_sweep.txt (lsv_api.cu simt_max_tok), in a batch that
+    launches the tensor-core tier anyway (a 64-token segment beside the probe)."""
+    d = _decode(_plan([0, n, n + 64], [r, 8])[0])
+    assert int(d["tier"][0]) == tier and int(d["tier"][1]) == 2
+
+
+def test_decode_shaped_batches_stay_on_simt():
+    """No segment longer than 8 tokens: the whole batch on the SIMT tier (no tcgen05 launches)."""
+    d = _decode(_plan([0, 1, 3, 8, 9], [128, 64, 8, 256])[0])
+    assert list(d["tier"]) == [1, 1, 1, 1] and d["n_mtiles"] == 0
 
 
 def test_split_v_doubles_the_v_image_region():

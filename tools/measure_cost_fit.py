@@ -25,12 +25,14 @@ RANKS = (8, 16, 32, 64, 128)
 
 
 def fit(rows, with_tok=True):
-    """Least squares; decode (one token per request) fits without the token term, which is
+    """Least squares on relative residuals (rows weighted by 1/t: the fit is judged per sample as
+    |pred - t| / t); decode (one token per request) fits without the token term, which is
     collinear with sum(ranks) there and carries no bytes of its own worth resolving."""
     a = np.array([[1.0, r["sum_len"] if with_tok else 0.0, r["sum_rank"]] for r in rows])
     t = np.array([r["seconds"] for r in rows])
     cols = [0, 1, 2] if with_tok else [0, 2]
-    coef_sub, *_ = np.linalg.lstsq(a[:, cols], t, rcond=None)
+    w = 1.0 / t
+    coef_sub, *_ = np.linalg.lstsq(a[:, cols] * w[:, None], t * w, rcond=None)
     coef = np.zeros(3)
     coef[cols] = coef_sub
     pred = a @ coef
