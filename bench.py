@@ -762,7 +762,8 @@ def run_remote(args, rank, world, local_rank):
     peers = {r: AdapterSlab.open_peer(model, handles[r], roster, dev) for r in range(world) if r != rank}
     eng = LoraDeltaEngine(slab)
     bp_local = eng.prepare(seg)
-    bp_remote = eng.prepare(seg, seg_owner=owner, peer_slabs=peers)
+    bp_remote = eng.prepare(seg, seg_owner=owner, peer_slabs=peers)              # NVLink-aware LPT plan
+    bp_remote_plain = eng.prepare(seg, seg_owner=owner, peer_slabs=peers, remote_aware=False)
     pf = RemotePrefetch(eng, seg, owner, peers)
     bp_pf = pf.plan()
     g = torch.Generator(device=dev).manual_seed(1 + rank)
@@ -791,16 +792,20 @@ def run_remote(args, rank, world, local_rank):
     identical_pf = all(torch.equal(ys_a[l][k], ys_b[l][k]) for l in range(model.layers) for k in ys_a[l])
     del ys_a, ys_b
     stream = torch.cuda.Stream(dev)
-    torch.distributed.barrier()
-    ms_local = time_graph(torch, eng, bp_local, xs, ys, stream, args.steps, args.warmup, dev)
-    torch.distributed.barrier()
-    ms_pf = time_graph(torch, eng, bp_pf, xs, ys, stream, args.steps, args.warmup, dev,
-                       step_fn=lambda: eng.forward_prefetch(bp_pf, pf, xs, ys, stream))
-    torch.distributed.barrier()
-    sampler = ClockSampler(dev.index)
-    sampler.start()
-    ms_direct = time_graph(torch, eng, bp_remote, xs, ys, stream, args.steps, args.warmup, dev)
-    clocks = sampler.stop()
+    arm_clocks = {}
+
+    def timed(name, bp_, fn=None):
+        torch.distributed.barrier()
+        smp = ClockSampler(dev.index)
+        smp.start()
+        ms_ = time_graph(torch, eng, bp_, xs, ys, stream, args.steps, args.warmup, dev, step_fn=fn)
+        arm_clocks[name] = smp.stop()
+        return ms_
+    ms_local = timed("all_local", bp_local)
+    ms_pf = timed("prefetch", bp_pf, lambda: eng.forward_prefetch(bp_pf, pf, xs, ys, stream))
+    ms_plain = timed("direct_plain_plan", bp_remote_plain)
+    ms_direct = timed("direct", bp_remote)
+    clocks = arm_clocks["direct"]
     # copy-on-first-use (the reference's commit_migration): every peer-owned adapter this GPU's
     # batch uses, copied once into a local slab by the copy engines; afterwards the batch runs
     # all-local (ms_local).  Break-even: how many steps of direct peer loads the copy costs.
@@ -824,13 +829,15 @@ def run_remote(args, rank, world, local_rank):
     mig_identical = all(_same(a) for a, _ in peer_aids[:4])
     del mig
     t = torch.tensor([ms_local, ms_direct, float(identical and identical_pf and mig_identical), ms_pf, ms_mig,
-                      float(mig_bytes)], device=dev, dtype=torch.float64)
+                      float(mig_bytes), ms_plain], device=dev, dtype=torch.float64)
     per = [torch.zeros_like(t) for _ in range(world)]
     torch.distributed.all_gather(per, t)
     per = [p.tolist() for p in per]
     ms_l = max(p[0] for p in per)
     ms_r = max(p[1] for p in per)      # headline: in-kernel NVLink peer loads
     ms_p = max(p[3] for p in per)
+    ms_pl = max(p[6] for p in per)
+    lens = seg.lengths()
     remote_frac = float(np.sum(seg.lengths()[owner != rank])) / N
     step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
     hbm_peak, peak_src = peaks()
@@ -846,18 +853,26 @@ def run_remote(args, rank, world, local_rank):
                                 "bit_identical": bool(p[2])} for p in per],
                    "timing": "CUDA-graph replay, CUDA events, max over ranks"},
         "remote_overhead": ms_r / ms_l - 1.0,
+        "remote_plain_plan": {"ms_per_step": ms_pl, "overhead": ms_pl / ms_l - 1.0,
+                              "note": "the same peer reads with the plan built without LSV_SEG_REMOTE (bytes-only LPT, "
+                                      "remote and local records in LPT order)"},
+        "batch_shape": {"segments": int(seg.num_segments), "mean_tokens_per_segment": float(np.mean(lens)),
+                        "segments_under_32_tokens": int(np.sum(lens < 32)),
+                        "note": "70% of the GPU's tokens on its 100/N own adapters, 30% spread over the others' "
+                                "(synth.remote_workload): smaller segments than C2's (41 tokens each) as N grows"},
         "remote_prefetch": {"ms_per_step": ms_p, "value": N * world / (ms_p / 1e3), "overhead": ms_p / ms_l - 1.0,
                             "mode": "copy-engine fetch (lsv_copy_blocks) of the next layer's peer-owned tiles into "
                                     f"local staging while the current layer computes; {pf.bytes_per_layer / 1e6:.1f} "
                                     f"MB/layer over NVLink on GPU {rank}"},
-        "all_local": {"ms_per_step": ms_l, "value": N * world / (ms_l / 1e3)},
+        "all_local": {"ms_per_step": ms_l, "value": N * world / (ms_l / 1e3),
+                      "hbm_frac": step_bytes / (ms_l * 1e-3) / 1e9 / hbm_peak},
         "remote_migration": {"mode": "copy-on-first-use: every peer-owned adapter of the batch copied once into a "
                                      "local slot (AdapterSlab.migrate_from_peer, lsv_copy_blocks over NVLink)",
                              "ms": max(p[4] for p in per), "bytes_per_gpu": [int(p[5]) for p in per],
                              "GBps": min(p[5] / (p[4] * 1e-3) / 1e9 for p in per),
                              "break_even_steps": max(p[4] for p in per) / max(ms_r - ms_l, 1e-9)},
         "step_hbm": {"frac_local_bytes": step_bytes / (ms_r * 1e-3) / 1e9 / hbm_peak},
-        "clocks": clocks,
+        "clocks": clocks, "clocks_per_arm": arm_clocks,
     }
 
 

@@ -142,6 +142,18 @@ int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const 
                          int32_t h_in, int32_t num_proj, const int32_t* h_outs, int32_t tier_policy,
                          void* plan_host, size_t plan_bytes);
 
+/* Group plan with per-segment flags (HOST array [S], or NULL = lsv_plan_*_group).  LSV_SEG_REMOTE:
+ * the segment's adapter lives in an NVLink peer's slab (the reference's fetch_remote,
+ * pool.py:101-132); the planner weighs its A/B bytes by the HBM/NVLink bandwidth ratio and
+ * interleaves remote and local work in every CTA's list so peer reads overlap local HBM traffic. */
+#define LSV_SEG_REMOTE 1
+int lsv_plan_size_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                           const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
+                           int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes);
+int lsv_plan_build_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                            const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
+                            int32_t tier_policy, void* plan_host, size_t plan_bytes);
+
 /* Fill out[0..7] from a host plan: {num_segments, num_tokens, h_in, h_out,
  * n_simt_segments, n_tc_mtiles, n_shrink_items, n_expand_items}. */
 int lsv_plan_summary(const void* plan_host, int32_t* out8);

@@ -100,6 +100,11 @@ constexpr int64_t kShrinkRecFixed = (int64_t)LSV_SHRINK_REC_FIXED_KB * 1024;
 #define LSV_SHRINK_STAGE_FIXED_KB 96
 #endif
 constexpr int64_t kShrinkStageFixed = (int64_t)LSV_SHRINK_STAGE_FIXED_KB * 1024;
+// Remote segments (adapter owned by an NVLink peer, LSV_SEG_REMOTE): their A/B bytes weigh
+// kRemoteWeight local bytes in the LPT cost (HBM ~6.5 TB/s against ~0.9 TB/s of NVLink ingress per
+// GPU), so the peer reads spread evenly over the CTAs; each CTA's list then alternates remote and
+// local records, keeping NVLink and HBM busy together instead of one after the other.
+const int kRemoteWeight = [] { const char* e = std::getenv("LSV_REMOTE_WEIGHT"); return e ? std::atoi(e) : 7; }();
 
 int num_sms_cached() {
   static int sms = -1;
@@ -162,7 +167,7 @@ struct LoadTree {
 // CTA's list keeps that order.  Returns records regrouped per CTA and the [grid+1] offsets.
 template <typename Rec>
 void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, std::vector<Rec>& out,
-                std::vector<int32_t>& cta_off) {
+                std::vector<int32_t>& cta_off, const std::vector<uint8_t>* remote = nullptr) {
   std::vector<int32_t> owner(costed.size());
   LoadTree tree(grid);
   for (size_t i = 0; i < costed.size(); ++i) {
@@ -176,6 +181,17 @@ void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, st
   out.resize(costed.size());
   std::vector<int32_t> fill(cta_off.begin(), cta_off.end() - 1);
   for (size_t i = 0; i < costed.size(); ++i) out[fill[owner[i]]++] = costed[i].second;   // keeps LPT order per CTA
+  if (remote == nullptr) return;
+  // per CTA: remote and local records alternate (each kind in LPT order), remote first
+  std::vector<Rec> rem, loc;
+  for (int c = 0; c < grid; ++c) {
+    rem.clear();
+    loc.clear();
+    for (int i = cta_off[c]; i < cta_off[c + 1]; ++i) ((*remote)[out[i].seg] ? rem : loc).push_back(out[i]);
+    size_t a = 0, b = 0;
+    for (int i = cta_off[c]; i < cta_off[c + 1]; ++i)
+      out[i] = (a < rem.size() && (b >= loc.size() || a <= b)) ? rem[a++] : loc[b++];
+  }
 }
 
 int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
@@ -203,7 +219,7 @@ int validate_segments(int32_t S, const int32_t* indptr, const int32_t* rank, int
 int subset_np(int P, int p0, int r) { return std::max(1, std::min(P - p0, 256 / r)); }
 
 int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
-               const int32_t* h_outs, int32_t policy) {
+               const int32_t* h_outs, int32_t policy, const int32_t* seg_flags = nullptr) {
   if (int rc = validate_segments(S, indptr, rank, h_in, P, h_outs)) return rc;
   if (policy & ~(0xff | LSV_PLAN_V_BF16 | LSV_PLAN_TILE_ALIGNED))
     return fail(LSV_EINVAL, "unknown plan flags 0x%x", policy);
@@ -220,6 +236,13 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   if (S == 0) pb.indptr.assign(1, 0);
   pb.rank.assign(rank, rank + S);
   pb.tier.assign(S, kTierNone);
+  std::vector<uint8_t> remote(S, 0);
+  bool any_remote = false;
+  for (int s = 0; s < S && seg_flags; ++s) {
+    remote[s] = (seg_flags[s] & LSV_SEG_REMOTE) ? 1 : 0;
+    any_remote |= remote[s] != 0;
+  }
+  const std::vector<uint8_t>* rem = any_remote ? &remote : nullptr;
   const int nsm = num_sms_cached();
 
   // tier per segment
@@ -311,7 +334,8 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         // predict a CTA's time better than its bytes.
         const int nstage = (rc.chunk_end - rc.chunk_begin + kch - 1) / kch;
         const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + kShrinkRecFixed +
-                             kShrinkStageFixed * nstage + (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0);
+                             kShrinkStageFixed * nstage + (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0) +
+                             (remote[mt.seg] ? (int64_t)(kRemoteWeight - 1) * rows * 128 * (rc.chunk_end - rc.chunk_begin) : 0);
         shrink_costed.push_back({cost, rc});
       }
     }
@@ -319,7 +343,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   std::stable_sort(shrink_costed.begin(), shrink_costed.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
   const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
-  lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta);
+  lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta, rem);
 
   // expand: per projection, items = (m-tile, tw-wide h_out tile); plus all members in one list.
   // An item's cost depends only on (m-tile, member), so the (m-tile, member) classes are sorted
@@ -347,7 +371,9 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     for (size_t i = 0; i < pb.mtiles.size(); ++i) {
       const MTile& mt = pb.mtiles[i];
       const int tw = expand_item_tw(mt.rank, b_tile_width(h_outs[p]));
-      cls.push_back({(int64_t)tw * kpad(mt.rank) * 2 + (int64_t)mt.ntok * tw * 4 + kExpandItemFixed, (int32_t)i, p});
+      const int64_t bbytes = (int64_t)tw * kpad(mt.rank) * 2;
+      cls.push_back({bbytes * (remote[mt.seg] ? kRemoteWeight : 1) + (int64_t)mt.ntok * tw * 4 + kExpandItemFixed,
+                     (int32_t)i, p});
       n_items += h_outs[p] / tw;
     }
     all_cls.insert(all_cls.end(), cls.begin(), cls.end());
@@ -356,13 +382,13 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     expand_costed.reserve(n_items);
     emit(cls, expand_costed);
     expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
-    lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p]);
+    lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p], rem);
   }
   std::stable_sort(all_cls.begin(), all_cls.end(), by_cost);
   std::vector<std::pair<int64_t, ExpandRec>> all_costed;
   emit(all_cls, all_costed);
   const int expand_grid_all = (int)std::min<size_t>(all_costed.size(), (size_t)nsm);
-  lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta);
+  lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta, rem);
 
   // header + workspace layout
   PlanHeader& h = pb.h;
@@ -858,12 +884,13 @@ struct PlanKey {
   std::vector<int32_t> v;
   PlanKey() = default;
   PlanKey(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P, const int32_t* h_outs,
-          int32_t policy) {
-    v = {S, h_in, P, policy, num_sms_cached()};
+          int32_t policy, const int32_t* flags) {
+    v = {S, h_in, P, policy, num_sms_cached(), flags ? 1 : 0};
     if (h_outs) v.insert(v.end(), h_outs, h_outs + std::max(0, std::min(P, kMaxProj)));
     if (S > 0 && indptr && rank) {
       v.insert(v.end(), indptr, indptr + S + 1);
       v.insert(v.end(), rank, rank + S);
+      if (flags) v.insert(v.end(), flags, flags + S);
     }
   }
 };
@@ -871,14 +898,14 @@ thread_local PlanKey g_last_key;
 thread_local std::unique_ptr<PlanBuilder> g_last_plan;
 
 int plan_cached(int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P, const int32_t* h_outs,
-                int32_t policy, const PlanBuilder** out) {
-  PlanKey key(S, indptr, rank, h_in, P, h_outs, policy);
+                int32_t policy, const PlanBuilder** out, const int32_t* flags = nullptr) {
+  PlanKey key(S, indptr, rank, h_in, P, h_outs, policy, flags);
   if (g_last_plan && key.v == g_last_key.v) {
     *out = g_last_plan.get();
     return LSV_OK;
   }
   auto pb = std::make_unique<PlanBuilder>();
-  if (int rc = build_plan(*pb, S, indptr, rank, h_in, P, h_outs, policy)) return rc;
+  if (int rc = build_plan(*pb, S, indptr, rank, h_in, P, h_outs, policy, flags)) return rc;
   g_last_key = std::move(key);
   g_last_plan = std::move(pb);
   *out = g_last_plan.get();
@@ -900,6 +927,26 @@ int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const 
                          size_t plan_bytes) {
   const PlanBuilder* pb = nullptr;
   if (int rc = plan_cached(num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy, &pb)) return rc;
+  return plan_write(*pb, plan_host, plan_bytes);
+}
+
+int lsv_plan_size_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                           const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
+                           int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes) {
+  const PlanBuilder* pb = nullptr;
+  if (int rc = plan_cached(num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy, &pb, seg_flags))
+    return rc;
+  if (plan_bytes) *plan_bytes = (size_t)pb->h.total_ints * 4;
+  if (workspace_bytes) *workspace_bytes = (size_t)pb->h.ws_bytes;
+  return LSV_OK;
+}
+
+int lsv_plan_build_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
+                            const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
+                            int32_t tier_policy, void* plan_host, size_t plan_bytes) {
+  const PlanBuilder* pb = nullptr;
+  if (int rc = plan_cached(num_segments, seg_indptr, seg_rank, h_in, num_proj, h_outs, tier_policy, &pb, seg_flags))
+    return rc;
   return plan_write(*pb, plan_host, plan_bytes);
 }
 

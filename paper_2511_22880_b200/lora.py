@@ -121,19 +121,23 @@ class _UploadRing:
 
 
 def build_group_plan(seg: Segments, h_in: int, h_outs, tier_policy: int, device: torch.device,
-                     members: tuple[int, ...] = (), upload: bool = True) -> ShapePlan:
+                     members: tuple[int, ...] = (), upload: bool = True,
+                     seg_flags: np.ndarray | None = None) -> ShapePlan:
+    """``seg_flags`` [S] int32 (LSV_SEG_REMOTE for peer-owned adapters) or None."""
     lib = native.lib()
     S = seg.num_segments
     indptr = np.ascontiguousarray(seg.seg_indptr, dtype=np.int32)
     ranks = np.ascontiguousarray(seg.seg_rank, dtype=np.int32)
     hs = np.ascontiguousarray(h_outs, dtype=np.int32)
+    fl = None if seg_flags is None else np.ascontiguousarray(seg_flags, dtype=np.int32)
+    fptr = None if fl is None else fl.ctypes.data
     pb = ctypes.c_size_t()
     wb = ctypes.c_size_t()
-    native.check(lib.lsv_plan_size_group(S, indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs), hs.ctypes.data,
-                                         tier_policy, ctypes.byref(pb), ctypes.byref(wb)))
+    native.check(lib.lsv_plan_size_group_ex(S, indptr.ctypes.data, ranks.ctypes.data, fptr, h_in, len(hs),
+                                            hs.ctypes.data, tier_policy, ctypes.byref(pb), ctypes.byref(wb)))
     blob = np.zeros(pb.value // 4, dtype=np.int32)
-    native.check(lib.lsv_plan_build_group(S, indptr.ctypes.data, ranks.ctypes.data, h_in, len(hs), hs.ctypes.data,
-                                          tier_policy, blob.ctypes.data, pb.value))
+    native.check(lib.lsv_plan_build_group_ex(S, indptr.ctypes.data, ranks.ctypes.data, fptr, h_in, len(hs),
+                                             hs.ctypes.data, tier_policy, blob.ctypes.data, pb.value))
     summ = np.zeros(8, dtype=np.int32)
     native.check(lib.lsv_plan_summary(blob.ctypes.data, summ.ctypes.data))
     dev = torch.from_numpy(blob).to(device) if upload else None
@@ -169,7 +173,7 @@ class LoraDeltaEngine:
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
                 peer_slabs: dict[int, AdapterSlab] | None = None, stream=None,
-                fused_linear: bool = False) -> BatchPlan:
+                fused_linear: bool = False, remote_aware: bool = True) -> BatchPlan:
         """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
         uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
         k+1 on the host while batch k still runs there.  ``fused_linear``: tile-aligned plans for
@@ -179,8 +183,15 @@ class LoraDeltaEngine:
         # the group plans are independent host work; ctypes drops the GIL inside the C++ planner,
         # so they build in parallel
         policy = self.tier_policy | (native.PLAN_TILE_ALIGNED if fused_linear else 0)
+        flags = None
+        if seg_owner is not None and peer_slabs and remote_aware:
+            me = self.device.index or 0
+            own = np.asarray(seg_owner)
+            remote = (own != me) & np.isin(own, list(peer_slabs))
+            if remote.any():   # NVLink-aware LPT cost + remote/local interleaving (lsv_plan_build_group_ex)
+                flags = np.where(remote, native.SEG_REMOTE, 0).astype(np.int32)
         futs = [self._pool.submit(build_group_plan, seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
-                                  policy, self.device, members, stream is None)
+                                  policy, self.device, members, stream is None, flags)
                 for _, members in self.groups]
         plans = [f.result() for f in futs]
         # forward: one workspace slice per (layer, group) (lsv_lora_forward_workspace)

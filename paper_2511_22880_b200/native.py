@@ -22,6 +22,7 @@ LSV_DTYPE_BF16 = 0
 ABI_VERSION = 3
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 FWD_SERIAL = 1
+SEG_REMOTE = 1      # per-segment plan flag: adapter resident in an NVLink peer's slab
 PLAN_TILE_ALIGNED = 0x200   # plan flag: tile-aligned v images for lsv_lora_fused_linear
 PLAN_V_BF16 = 0x100   # plan flag: single bf16 v image on the tensor-core tier (default: hi/lo pair)
 
@@ -37,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "lsv_lora_forward", "lsv_lora_forward_ex", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
     "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum", "lsv_debug_set_trace",
-    "lsv_lora_fused_linear",
+    "lsv_lora_fused_linear", "lsv_plan_size_group_ex", "lsv_plan_build_group_ex",
 )
 
 _lib = None
@@ -87,6 +88,9 @@ _SIGNATURES = {
     "lsv_lora_shrink_tp_partials": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
                                                    _vp, _vp, _vp]),
     "lsv_lora_expand_group_tp_sum": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp, _i32, _vp, _vp]),
+    "lsv_plan_size_group_ex": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _i32, ctypes.POINTER(_sz),
+                                              ctypes.POINTER(_sz)]),
+    "lsv_plan_build_group_ex": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _sz]),
     "lsv_lora_fused_linear": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                                              _vp]),
 }

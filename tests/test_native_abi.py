@@ -293,3 +293,45 @@ def test_tile_aligned_plan_pieces():
     assert offs == list(np.concatenate(([0], np.cumsum(sizes)[:-1])))
     with pytest.raises(ValueError, match="tile-aligned"):
         _plan(indptr, ranks, 1024, 512, policy=native.TIER_SIMT | native.PLAN_TILE_ALIGNED)
+
+
+def _plan_group_flags(indptr, ranks, flags, h_in=4096, h_outs=(4096,)):
+    lib = native.load()
+    indptr = np.asarray(indptr, dtype=np.int32)
+    ranks = np.asarray(ranks, dtype=np.int32)
+    fl = None if flags is None else np.asarray(flags, dtype=np.int32)
+    hs = np.asarray(h_outs, dtype=np.int32)
+    pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
+    fp = None if fl is None else fl.ctypes.data
+    native.check(lib.lsv_plan_size_group_ex(len(ranks), indptr.ctypes.data, ranks.ctypes.data, fp, h_in, len(hs),
+                                            hs.ctypes.data, 0, ctypes.byref(pb), ctypes.byref(wb)))
+    blob = np.zeros(pb.value // 4, dtype=np.int32)
+    native.check(lib.lsv_plan_build_group_ex(len(ranks), indptr.ctypes.data, ranks.ctypes.data, fp, h_in, len(hs),
+                                             hs.ctypes.data, 0, blob.ctypes.data, pb.value))
+    return blob
+
+
+def test_remote_segments_spread_and_interleave():
+    """LSV_SEG_REMOTE: the same work items (coverage unchanged), remote expand items spread over the
+    CTAs (no CTA carries far more than its share) and alternating with local ones in each list."""
+    rng = np.random.default_rng(5)
+    ranks = [8] * 44 + [16] * 22 + [32] * 14 + [64] * 11 + [128] * 9
+    lens = np.bincount(rng.integers(0, 100, 4096), minlength=100)
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    flags = (np.arange(100) % 3 == 0).astype(np.int32)      # a third of the adapters on a peer
+    d0 = _decode(_plan_group_flags(indptr, ranks, None))
+    d1 = _decode(_plan_group_flags(indptr, ranks, flags))
+    key = lambda d: sorted(map(tuple, d["expand"].tolist()))   # noqa: E731
+    assert key(d0) == key(d1) and sorted(map(tuple, d0["shrink"].tolist())) == sorted(map(tuple, d1["shrink"].tolist()))
+    off = d1["expand_cta"]
+    rem_bytes = []
+    for c in range(d1["expand_grid"]):
+        recs = d1["expand"][off[c]:off[c + 1]]
+        isrem = [bool(flags[int(r[0])]) for r in recs]
+        rem_bytes.append(sum(int(r[3]) for r, f in zip(recs, isrem) if f))
+        # alternation: no two remote records in a row while local ones remain later in the list
+        for i in range(len(isrem) - 1):
+            if isrem[i] and isrem[i + 1]:
+                assert not any(not f for f in isrem[i + 1:])
+    rem_bytes = np.array(rem_bytes, dtype=float)
+    assert rem_bytes.max() <= 2.5 * rem_bytes.mean() + 256
