@@ -805,6 +805,15 @@ def run_remote(args, rank, world, local_rank):
     ms_pf = timed("prefetch", bp_pf, lambda: eng.forward_prefetch(bp_pf, pf, xs, ys, stream))
     ms_plain = timed("direct_plain_plan", bp_remote_plain)
     ms_direct = timed("direct", bp_remote)
+    # SM-partitioned: peer-owned segments on a few CTAs (own stream), local ones on the rest
+    from paper_2511_22880_b200.lora import SplitStep
+    split = {}
+    for rs in (16, 32):
+        sp = SplitStep(slab, seg, owner, peers, remote_sms=rs)
+        split[rs] = timed(f"split{rs}", None, lambda sp=sp: sp.forward(xs, ys, stream))
+        del sp
+    rs_best = min(split, key=split.get)
+    ms_split = split[rs_best]
     clocks = arm_clocks["direct"]
     # copy-on-first-use (the reference's commit_migration): every peer-owned adapter this GPU's
     # batch uses, copied once into a local slab by the copy engines; afterwards the batch runs
@@ -829,7 +838,7 @@ def run_remote(args, rank, world, local_rank):
     mig_identical = all(_same(a) for a, _ in peer_aids[:4])
     del mig
     t = torch.tensor([ms_local, ms_direct, float(identical and identical_pf and mig_identical), ms_pf, ms_mig,
-                      float(mig_bytes), ms_plain], device=dev, dtype=torch.float64)
+                      float(mig_bytes), ms_plain] + [split[k] for k in sorted(split)], device=dev, dtype=torch.float64)
     per = [torch.zeros_like(t) for _ in range(world)]
     torch.distributed.all_gather(per, t)
     per = [p.tolist() for p in per]
@@ -837,6 +846,7 @@ def run_remote(args, rank, world, local_rank):
     ms_r = max(p[1] for p in per)      # headline: in-kernel NVLink peer loads
     ms_p = max(p[3] for p in per)
     ms_pl = max(p[6] for p in per)
+    ms_sp = {k: max(p[7 + i] for p in per) for i, k in enumerate(sorted(split))}
     lens = seg.lengths()
     remote_frac = float(np.sum(seg.lengths()[owner != rank])) / N
     step_bytes = sum(algorithmic_bytes(seg, pr.h_in, pr.h_out) for pr in model.projections) * model.layers
@@ -853,6 +863,10 @@ def run_remote(args, rank, world, local_rank):
                                 "bit_identical": bool(p[2])} for p in per],
                    "timing": "CUDA-graph replay, CUDA events, max over ranks"},
         "remote_overhead": ms_r / ms_l - 1.0,
+        "remote_split": {"ms_per_step": min(ms_sp.values()), "overhead": min(ms_sp.values()) / ms_l - 1.0,
+                         "by_remote_sms": ms_sp,
+                         "mode": "SplitStep: peer-owned segments on R CTAs (their own plan and stream), local ones on "
+                                 "the other 148 - R (LSV_SEG_SKIP + LSV_PLAN_SMS)"},
         "remote_plain_plan": {"ms_per_step": ms_pl, "overhead": ms_pl / ms_l - 1.0,
                               "note": "the same peer reads with the plan built without LSV_SEG_REMOTE (bytes-only LPT, "
                                       "remote and local records in LPT order)"},

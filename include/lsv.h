@@ -71,6 +71,9 @@ extern "C" {
  * boundaries and each piece's v image spans its whole tile (zero rows outside the piece), so an
  * M=128 MMA adds v·B into exactly the piece's rows.  Tensor-core tier only. */
 #define LSV_PLAN_TILE_ALIGNED 0x200
+/* Plan flag: launch at most n CTAs (1..255) per kernel instead of one per SM, so two plans can run
+ * side by side on disjoint SM sets (LSV_SEG_SKIP partitions a batch between them). */
+#define LSV_PLAN_SMS(n) (((n) & 0xff) << 16)
 
 typedef void* lsv_stream_t; /* a cudaStream_t */
 
@@ -147,6 +150,9 @@ int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const 
  * pool.py:101-132); the planner weighs its A/B bytes by the HBM/NVLink bandwidth ratio and
  * interleaves remote and local work in every CTA's list so peer reads overlap local HBM traffic. */
 #define LSV_SEG_REMOTE 1
+/* LSV_SEG_SKIP: the segment keeps its token range but gets no work in this plan (two plans over one
+ * batch: e.g. local segments on most SMs and peer-owned ones on a few, run on two streams). */
+#define LSV_SEG_SKIP 2
 int lsv_plan_size_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
                            const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
                            int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes);

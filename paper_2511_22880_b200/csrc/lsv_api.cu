@@ -221,8 +221,9 @@ int subset_np(int P, int p0, int r) { return std::max(1, std::min(P - p0, 256 / 
 int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t* rank, int32_t h_in, int32_t P,
                const int32_t* h_outs, int32_t policy, const int32_t* seg_flags = nullptr) {
   if (int rc = validate_segments(S, indptr, rank, h_in, P, h_outs)) return rc;
-  if (policy & ~(0xff | LSV_PLAN_V_BF16 | LSV_PLAN_TILE_ALIGNED))
+  if (policy & ~(0xff | LSV_PLAN_V_BF16 | LSV_PLAN_TILE_ALIGNED | (0xff << 16)))
     return fail(LSV_EINVAL, "unknown plan flags 0x%x", policy);
+  const int sm_budget = (policy >> 16) & 0xff;   // LSV_PLAN_SMS(n): grids of at most n CTAs (0: all SMs)
   const int vsplit = (policy & LSV_PLAN_V_BF16) ? 0 : 1;
   const bool tile_aligned = (policy & LSV_PLAN_TILE_ALIGNED) != 0;
   policy &= 0xff;
@@ -243,14 +244,14 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     any_remote |= remote[s] != 0;
   }
   const std::vector<uint8_t>* rem = any_remote ? &remote : nullptr;
-  const int nsm = num_sms_cached();
+  const int nsm = sm_budget > 0 ? std::min(sm_budget, num_sms_cached()) : num_sms_cached();
 
   // tier per segment
   const bool all_simt = policy == LSV_TIER_AUTO && decode_shaped(S, indptr);
   int64_t v_off = 0;
   for (int s = 0; s < S; ++s) {
     const int n = indptr[s + 1] - indptr[s];
-    if (n == 0) continue;
+    if (n == 0 || (seg_flags && (seg_flags[s] & LSV_SEG_SKIP))) continue;   // no work (range kept)
     bool simt;
     if (policy == LSV_TIER_SIMT) simt = true;
     else if (policy == LSV_TIER_TC) simt = false;

@@ -173,16 +173,20 @@ class LoraDeltaEngine:
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
                 peer_slabs: dict[int, AdapterSlab] | None = None, stream=None,
-                fused_linear: bool = False, remote_aware: bool = True) -> BatchPlan:
+                fused_linear: bool = False, remote_aware: bool = True, skip: np.ndarray | None = None,
+                max_sms: int = 0) -> BatchPlan:
         """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
         uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
         k+1 on the host while batch k still runs there.  ``fused_linear``: tile-aligned plans for
-        ``linear_group`` (base GEMM with the delta fused, LSV_PLAN_TILE_ALIGNED; tensor-core tier)."""
+        ``linear_group`` (base GEMM with the delta fused, LSV_PLAN_TILE_ALIGNED; tensor-core tier).
+        ``skip`` [S] bool: segments that keep their tokens but get no work (LSV_SEG_SKIP); ``max_sms``:
+        grids of at most that many CTAs (LSV_PLAN_SMS) — together they split a batch into two plans
+        that run side by side on disjoint SMs (``SplitStep``)."""
         ws_need = 0
         projs = self.model.projections
         # the group plans are independent host work; ctypes drops the GIL inside the C++ planner,
         # so they build in parallel
-        policy = self.tier_policy | (native.PLAN_TILE_ALIGNED if fused_linear else 0)
+        policy = self.tier_policy | (native.PLAN_TILE_ALIGNED if fused_linear else 0) | native.PLAN_SMS(max_sms)
         flags = None
         if seg_owner is not None and peer_slabs and remote_aware:
             me = self.device.index or 0
@@ -190,6 +194,9 @@ class LoraDeltaEngine:
             remote = (own != me) & np.isin(own, list(peer_slabs))
             if remote.any():   # NVLink-aware LPT cost + remote/local interleaving (lsv_plan_build_group_ex)
                 flags = np.where(remote, native.SEG_REMOTE, 0).astype(np.int32)
+        if skip is not None and np.any(skip):
+            flags = (np.zeros(seg.num_segments, dtype=np.int32) if flags is None else flags) | \
+                np.where(np.asarray(skip, dtype=bool), native.SEG_SKIP, 0).astype(np.int32)
         futs = [self._pool.submit(build_group_plan, seg, projs[members[0]].h_in, [projs[p].h_out for p in members],
                                   policy, self.device, members, stream is None, flags)
                 for _, members in self.groups]
@@ -450,6 +457,34 @@ def algorithmic_flops(seg: Segments, h_in: int, h_out: int) -> int:
     n = seg.lengths().astype(np.int64)
     r = seg.seg_rank.astype(np.int64)
     return int(np.sum(2 * n * r * (h_in + h_out)))
+
+
+class SplitStep:
+    """Config 4 with the SMs partitioned: the batch's peer-owned segments run on ``remote_sms`` CTAs
+    (their plan skips every local segment) while the local segments run on the rest (their plan skips
+    the remote ones), each as its own forward on its own stream.  NVLink reads then stream at the
+    link's rate on a few SMs without holding up the local HBM pipeline in the same CTAs (in-order
+    rings make a slow peer tile stall every local item queued behind it).  y rows of the two plans
+    are disjoint segments, so the two forwards never touch the same output."""
+
+    def __init__(self, slab: AdapterSlab, seg: Segments, seg_owner: np.ndarray,
+                 peer_slabs: dict[int, AdapterSlab], remote_sms: int = 24, v_bf16: bool = False):
+        me = slab.device.index or 0
+        remote = np.asarray(seg_owner) != me
+        self.local_eng = LoraDeltaEngine(slab, v_bf16=v_bf16)
+        self.remote_eng = LoraDeltaEngine(slab, v_bf16=v_bf16)   # its own workspace
+        nsm = native.lib().lsv_num_sms()
+        self.bp_local = self.local_eng.prepare(seg, skip=remote, max_sms=max(1, nsm - remote_sms))
+        self.bp_remote = self.remote_eng.prepare(seg, seg_owner=seg_owner, peer_slabs=peer_slabs, skip=~remote,
+                                                 max_sms=remote_sms, remote_aware=False)
+        self.side = torch.cuda.Stream(slab.device)
+
+    def forward(self, xs, ys, stream=None) -> None:
+        st = stream or torch.cuda.current_stream(self.local_eng.device)
+        self.side.wait_stream(st)
+        self.remote_eng.forward(self.bp_remote, xs, ys, self.side)
+        self.local_eng.forward(self.bp_local, xs, ys, st)
+        st.wait_stream(self.side)
 
 
 class RemotePrefetch:

@@ -22,7 +22,12 @@ LSV_DTYPE_BF16 = 0
 ABI_VERSION = 3
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 FWD_SERIAL = 1
+SEG_SKIP = 2        # per-segment plan flag: token range kept, no work in this plan
 SEG_REMOTE = 1      # per-segment plan flag: adapter resident in an NVLink peer's slab
+def PLAN_SMS(n: int) -> int:   # noqa: N802  plan flag: at most n CTAs per kernel
+    return (n & 0xff) << 16
+
+
 PLAN_TILE_ALIGNED = 0x200   # plan flag: tile-aligned v images for lsv_lora_fused_linear
 PLAN_V_BF16 = 0x100   # plan flag: single bf16 v image on the tensor-core tier (default: hi/lo pair)
 

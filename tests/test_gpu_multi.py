@@ -113,3 +113,44 @@ def test_migrate_from_peer_bit_identical():
     from oracle import oracle
     err = oracle.max_rel_err(y.float().cpu().numpy()[:seg.num_tokens], case.oracle_delta()[:seg.num_tokens])
     assert err <= 1e-2
+
+
+def test_split_step_matches_all_local():
+    """SplitStep (peer-owned segments on a few CTAs and their own stream, local ones on the rest)
+    gives the all-local deltas within the contract (k-split choices differ with the SM budget, so
+    fp32 summation order may differ: not bit-identical)."""
+    from oracle import oracle
+    from paper_2511_22880_b200 import native
+    from paper_2511_22880_b200.lora import LoraDeltaEngine, SplitStep
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+    from paper_2511_22880_b200.slab import AdapterSlab
+    native.check(native.lib().lsv_enable_peer(0, 1))
+    model = ModelShape("l7b-2l", 2, LLAMA2_7B.projections)
+    ranks = [8, 16, 32, 64, 128, 8, 16, 64]
+    slabs = []
+    for dev in ("cuda:0", "cuda:1"):
+        slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+        for i, r in enumerate(ranks):
+            slab.fill_random(slab.allocate(f"a{i}", r), 500 + i)
+        slabs.append(slab)
+    torch.cuda.synchronize("cuda:1")
+    seg = index_tokens(np.random.default_rng(4).integers(0, len(ranks), 700), ranks)
+    owner = (np.arange(seg.num_segments) % 2).astype(np.int32)
+    N = seg.num_tokens
+    g = torch.Generator(device="cuda:0").manual_seed(2)
+    xs = [{gname: torch.randn(N, model.projections[m[0]].h_in, device="cuda:0", generator=g).to(torch.bfloat16)
+           for gname, m in model.groups()} for _ in range(2)]
+    ys_a = [{p.name: torch.zeros(N, p.h_out, dtype=torch.bfloat16, device="cuda:0") for p in model.projections}
+            for _ in range(2)]
+    ys_b = [{k: v.clone() for k, v in d.items()} for d in ys_a]
+    eng = LoraDeltaEngine(slabs[0])
+    eng.forward(eng.prepare(seg), xs, ys_a)
+    sp = SplitStep(slabs[0], seg, owner, {1: slabs[1]}, remote_sms=16)
+    sp.forward(xs, ys_b)
+    torch.cuda.synchronize("cuda:0")
+    for l in range(2):
+        for k in ys_a[l]:
+            a, b = ys_a[l][k].float().cpu().numpy(), ys_b[l][k].float().cpu().numpy()
+            assert oracle.max_rel_err(b, a) <= 1e-2, (l, k)
+            assert np.mean(a == b) > 0.97

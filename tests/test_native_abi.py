@@ -335,3 +335,18 @@ def test_remote_segments_spread_and_interleave():
                 assert not any(not f for f in isrem[i + 1:])
     rem_bytes = np.array(rem_bytes, dtype=float)
     assert rem_bytes.max() <= 2.5 * rem_bytes.mean() + 256
+
+
+def test_skip_flags_and_sm_budget():
+    """LSV_SEG_SKIP segments get no work; LSV_PLAN_SMS(n) caps every grid at n CTAs."""
+    ranks = [8, 64, 128, 16]
+    lens = [100, 300, 50, 200]
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    skip = np.array([0, 2, 0, 2], dtype=np.int32)
+    d = _decode(_plan_group_flags(indptr, ranks, skip))
+    assert {int(m[0]) for m in d["mtiles"]} == {0, 2}
+    assert {int(r[0]) for r in d["expand"]} == {0, 2}
+    lib = native.load()
+    blob, _ = _plan(indptr, ranks, policy=native.PLAN_SMS(20))
+    d = _decode(blob)
+    assert d["shrink_grid"] <= 20 and d["expand_grid"] <= 20 and d["n_mtiles"] == 2 + 3 + 1 + 2
