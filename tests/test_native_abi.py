@@ -349,4 +349,4 @@ def test_skip_flags_and_sm_budget():
     lib = native.load()
     blob, _ = _plan(indptr, ranks, policy=native.PLAN_SMS(20))
     d = _decode(blob)
-    assert d["shrink_grid"] <= 20 and d["expand_grid"] <= 20 and d["n_mtiles"] == 2 + 3 + 1 + 2
+    assert d["shrink_grid"] <= 20 and d["expand_grid"] <= 20 and d["n_mtiles"] == 1 + 3 + 1 + 2
