@@ -34,21 +34,26 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
-        return OUT
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES), "-ldl", "-lpthread", "-lrt"]
+CHECKED = PKG / "liblsv_checked.so"   # LSV_DEVICE_CHECKS=1: device-side bounds checks (tools/gpu_checked.sh)
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    out = CHECKED if checked else OUT
+    if not force and out.exists() and not any(p.stat().st_mtime > out.stat().st_mtime for p in DEPS):
+        return out
+    tmp = out.with_suffix(".so.tmp")
+    extra = ["-DLSV_DEVICE_CHECKS=1"] if checked else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES), "-ldl", "-lpthread", "-lrt"]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = PKG / "build.log"
+    log = PKG / ("build_checked.log" if checked else "build.log")
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(res.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

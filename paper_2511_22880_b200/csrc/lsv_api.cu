@@ -667,6 +667,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     }
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
+    p.num_tokens = num_tokens; p.h_in = h->h_in; p.ws_bytes = h->ws_bytes;
     LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl, kShrinkThreads));
   }
   return LSV_OK;
@@ -730,6 +731,8 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   p.tw_max = tw_max;
   p.dbg = g_debug_expand;
   p.trace = g_trace; p.trace_items = g_trace_items;
+  p.num_tokens = num_tokens; p.ws_bytes = vimg_base ? INT64_MAX : h->ws_bytes;
+  for (int pp = 0; pp < h->num_proj; ++pp) p.h_outs[pp] = h->h_outs[pp];
   LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, all ? h->expand_grid_all : h->expand_grid_p[p0], expand_smem_bytes(),
                             st, p, true, kExpandThreads));
   LSV_CUDA_CHECK(cudaGetLastError());

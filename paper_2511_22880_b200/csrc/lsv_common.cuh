@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace lsv {
 
@@ -32,6 +33,27 @@ constexpr int kSimtMaxTok = 8;      // tokens per SIMT item
 constexpr int kSimtSmallTok = LSV_SIMT_SMALL_TOK;    // SIMT items up to this many tokens use the small expand accumulator
 
 __host__ __device__ __forceinline__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Device-side bounds checks (the checked build, LSV_DEVICE_CHECKS=1: liblsv_checked.so, run by
+// tools/gpu_checked.sh over the GPU test suite).  compute-sanitizer is not available on the GPU
+// pool, so every kernel asserts its own invariants instead: plan records inside the batch, ring
+// allocations inside shared memory, workspace writes inside the planned workspace.  A failed check
+// prints the condition and traps (the launch fails loudly).  No-ops in the production build.
+#ifndef LSV_DEVICE_CHECKS
+#define LSV_DEVICE_CHECKS 0
+#endif
+#if LSV_DEVICE_CHECKS
+#define LSV_DCHECK(cond)                                                                              \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("lsv device check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                      \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define LSV_DCHECK(cond) do { } while (0)
+#endif
 
 // ---- layout address functions (byte offsets) -------------------------------------------
 // Hardware swizzle of a byte offset inside a region aligned to the pattern period

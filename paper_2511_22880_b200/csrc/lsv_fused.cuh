@@ -219,6 +219,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_linear_kernel(const __
             lora_unit(cache, at, p.vsplit, u);
             const uint8_t* vimg = p.ws + p.ws_vimg[pp] + u.mt.vimg_off;
             const uint32_t vb = kTileM * u.S, bb = u.ck / 8 * 4096, lo = vimg_bytes(kTileM, u.kp);
+            LSV_DCHECK(u.mt.tok_begin / kTileM == m && u.mt.tok_begin + u.mt.ntok <= p.num_tokens);
+            LSV_DCHECK(bytes <= (uint32_t)kFusedSlotBytes && at.c * u.ck < u.kp);
             const uint8_t* bt = static_cast<const uint8_t*>(p.b_ptrs[pp][u.mt.seg]) + (size_t)n * kFusedTileN * u.kp * 2;
             bulk_load(dst, vimg + (at.h ? lo : 0u) + (size_t)at.c * vb, vb, &full[slot]);
             if (u.both) bulk_load(dst + vb, vimg + lo + (size_t)at.c * vb, vb, &full[slot]);

@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   const int rb = m & 255;
   const int r = simt_rank(it), G = nproj * r;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  LSV_DCHECK(simt_nt(it) >= 1 && simt_nt(it) <= kSimtMaxTok && r >= 8 && r <= 256 && rb * kSimtShrRows < G);
+  LSV_DCHECK(it.v_off + simt_nt(it) * r <= simt_stride);
   const int rl = lane >> 2, k = rb * kSimtShrRows + rl, q4 = lane & 3;
   const uint8_t* arow = static_cast<const uint8_t*>(a_ptrs[it.seg]) + (size_t)k * 128;
   // row k + 8h has the same swizzle phase as row k

@@ -61,6 +61,8 @@ struct alignas(64) ShrinkParams {
   uint64_t* trace;              // debug timeline (nullptr = off): [cta][item][8] globaltimer stamps
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
+  int num_tokens, h_in;         // bounds for the checked build (LSV_DCHECK)
+  int64_t ws_bytes;
 };
 
 struct alignas(64) ExpandParams {
@@ -85,6 +87,9 @@ struct alignas(64) ExpandParams {
   uint64_t* trace;
   int trace_items;
   int dbg;                      // debug ablations (0 in production)
+  int num_tokens;               // bounds for the checked build (LSV_DCHECK)
+  int h_outs[kMaxProj];
+  int64_t ws_bytes;
 };
 
 __device__ __forceinline__ void trace_stamp(uint64_t* trace, int trace_items, int cta, int i, int k) {
@@ -382,6 +387,10 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       // rows [p0*r, (p0+np)*r) of the group A tile (G = num_proj*r rows per 64-column chunk)
       const int r = inf.rank, G = p.num_proj * r, rows = inf.np * r, np8 = round_up(inf.ntok, 8), kch = inf.kch;
       const uint8_t* asub = a + (size_t)inf.p0 * r * 128;
+      LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin >= 0 && inf.tok_begin + inf.ntok <= p.num_tokens);
+      LSV_DCHECK(r >= 8 && r <= 256 && r % 8 == 0 && rows <= 256 && inf.p0 + inf.np <= p.num_proj);
+      LSV_DCHECK(inf.chunk_begin >= 0 && inf.chunk_begin < inf.chunk_end && inf.chunk_end * kChunk <= p.h_in);
+      LSV_DCHECK(kch >= 1 && kch * (np8 + rows) * 128 <= kShrinkSlotBytes && a != nullptr);
       const int m = np8 >> 3, pc = __popc(m);   // x boxes per chunk: one per set bit of np8/8
       for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
         const int kc = min(kch, inf.chunk_end - g);
@@ -486,6 +495,10 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       const int irow = ta ? ((inf.tok_begin + row) & (kTileM - 1)) : row, rpad = ta ? kTileM : np16;
       const bool wimg = ta ? !(p.dbg & 8) : valid;              // writes an image row (nsplit == 1)
       const uint32_t vlo = vimg_bytes(rpad, kp);                // hi image -> lo image (split v)
+      LSV_DCHECK(p.tp > 0 || (int64_t)p.ws_vimg + (int64_t)(p.num_proj - 1) * p.vimg_stride + inf.vimg_off +
+                                   (int64_t)vlo * (p.vsplit ? 2 : 1) <= p.ws_bytes);
+      LSV_DCHECK(inf.nsplit == 1 || (int64_t)p.ws_partials + 4 * ((int64_t)inf.part_off +
+                                   (int64_t)inf.nsplit * nt * G) <= p.ws_bytes);
       float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
       for (int cc = 0; cc < rows; cc += 16) {
         float v[16];
@@ -763,6 +776,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         head = round_up(head, 1024);
         if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
           head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
+        LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
+        LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
+        LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
+        LSV_DCHECK(p.wait_flag != nullptr ||
+                   (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
         trace_stamp(p.trace, p.trace_items, cta, k, 0);
         // retire in FIFO order until an allocation slot and the ring bytes are free
         while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
