@@ -320,6 +320,11 @@ int lsv_ipc_close_handle(void* dev_ptr);
 int lsv_copy_blocks(int32_t n, const void* const* src, void* const* dst, const size_t* bytes,
                     lsv_stream_t stream);
 
+/* Build flags of this library: LSV_BUILD_DEVICE_CHECKS if compiled with device-side bounds checks
+ * (liblsv_checked.so, the test-only build whose kernels trap on out-of-range records). */
+#define LSV_BUILD_DEVICE_CHECKS 1
+int lsv_build_info(void);
+
 /* Number of SMs the planner assumes (queried from device 0 once; 148 on B200). */
 int lsv_num_sms(void);
 

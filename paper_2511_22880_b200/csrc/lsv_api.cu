@@ -787,6 +787,7 @@ extern "C" {
 int lsv_version(void) { return LSV_ABI_VERSION; }
 const char* lsv_last_error(void) { return g_err; }
 int lsv_num_sms(void) { return num_sms_cached(); }
+int lsv_build_info(void) { return LSV_DEVICE_CHECKS ? LSV_BUILD_DEVICE_CHECKS : 0; }
 
 size_t lsv_adapter_a_bytes(int32_t rank, int32_t h_in) {
   return (rank > 0 && h_in > 0) ? (size_t)rank * h_in * 2 : 0;

@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "lsv_lora_forward", "lsv_lora_forward_ex", "lsv_lora_forward_workspace", "lsv_copy_blocks",
     "lsv_lora_shrink_tp_scatter", "lsv_lora_expand_group_tp",
     "lsv_lora_shrink_tp_partials", "lsv_lora_expand_group_tp_sum", "lsv_debug_set_trace",
-    "lsv_lora_fused_linear", "lsv_plan_size_group_ex", "lsv_plan_build_group_ex",
+    "lsv_lora_fused_linear", "lsv_plan_size_group_ex", "lsv_plan_build_group_ex", "lsv_build_info",
 )
 
 _lib = None
@@ -53,6 +53,7 @@ _SIGNATURES = {
     "lsv_version": (ctypes.c_int, []),
     "lsv_last_error": (ctypes.c_char_p, []),
     "lsv_num_sms": (ctypes.c_int, []),
+    "lsv_build_info": (ctypes.c_int, []),
     "lsv_debug_set_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "lsv_adapter_a_bytes": (_sz, [_i32, _i32]),
     "lsv_adapter_b_bytes": (_sz, [_i32, _i32]),

@@ -98,3 +98,14 @@ def test_forward_writes_only_its_outputs():
     torch.cuda.synchronize()
     assert all(_guard_intact(b, v) for b, v in bufs)
     assert bool(torch.all(bp.workspace[:64 * 1024] == 0))
+
+
+def test_checked_library_when_requested():
+    """tools/gpu_checked.sh sets LSV_EXPECT_CHECKED=1: the loaded library must be the checked build."""
+    import os
+    from paper_2511_22880_b200 import native
+    info = native.lib().lsv_build_info()
+    if os.environ.get("LSV_EXPECT_CHECKED") == "1":
+        assert info & 1, "expected liblsv_checked.so (LSV_DEVICE_CHECKS)"
+    else:
+        assert info in (0, 1)
