@@ -471,7 +471,7 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "launch_us": exp_us,
                      "algorithmic_bytes_per_launch": exp_bytes,
-                     "traffic_source": "profiles/traffic_r1.json: dram__bytes_read.sum + dram__bytes_write.sum of the "
+                     "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of the "
                                        "same launch from one ncu --set full capture (tools/prof_one.py)",
                      "shrink": {"kernel": (f"simt_shrink_kernel ({names}, one launch)" if simt_only else
                                            f"shrink_tc_kernel (fused {len(members)}-projection group {names})"),
@@ -705,7 +705,7 @@ def tflops_peak():
 
 def measured_traffic(config, label):
     """DRAM bytes per launch of the roofline kernel, from the committed ncu capture (or None)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r1.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get(config, {}).get(label)

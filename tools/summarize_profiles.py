@@ -3,7 +3,7 @@
     python tools/summarize_profiles.py TAG      # reads gpurun_out/launches_TAG.csv, full_TAG.ncu-rep
 
 writes profiles/<TAG>_launch_summary.txt, profiles/<TAG>_launches_c2_step.csv (the launch list),
-profiles/<TAG>_ncu_full_mlp_in.txt and updates profiles/traffic_r1.json (dram bytes per launch of the
+profiles/<TAG>_ncu_full_mlp_in.txt and updates profiles/traffic.json (dram bytes per launch of the
 roofline kernel, read by bench.py)."""
 import csv
 import io
@@ -17,8 +17,8 @@ OUT = sys.argv[2] if len(sys.argv) > 2 else TAG
 DECODE = len(sys.argv) > 3 and sys.argv[3] == "decode"
 WL = ("decode (C2 roster, 128 requests x 1 token, 73 active adapters; SIMT tier)" if DECODE else
       "config 2 (Llama-2-7B shapes, 100 adapters, 4096 tokens)")
-CMD = "python bench.py --config decode --steps 1 --warmup 3 --no-cpu-baseline" if DECODE else \
-      "python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+CMD = "python bench.py --config decode --steps 1 --warmup 3 --no-cpu-baseline --no-extras" if DECODE else \
+      "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras"
 GROUPS = ["attn_in (q/k/v fused)", "attn_out (o)", "mlp_in (gate/up fused)", "mlp_mid (down)"]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
@@ -104,14 +104,14 @@ def full():
     print("\n".join(lines))
     if DECODE:
         return
-    tj = json.load(open("profiles/traffic_r1.json"))
+    tj = json.load(open("profiles/traffic.json"))
     for k in tj["c2"]:
         kern = k.split(" ")[0]
         if kern in traffic:
             tj["c2"][k] = traffic[kern]
     tj["note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/{OUT}_ncu_full_mlp_in.txt. "
                   "Writes land in L2 and are partly evicted after the launch, so write bytes undercount.")
-    json.dump(tj, open("profiles/traffic_r1.json", "w"), indent=1)
+    json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
 
 
 if __name__ == "__main__":
