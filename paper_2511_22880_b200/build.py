@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
         return out
     tmp = out.with_suffix(".so.tmp")
     extra = ["-DLSV_DEVICE_CHECKS=1"] if checked else []
+    extra += os.environ.get("LSV_NVCC_DEFINES", "").split()   # development variants (A/B builds)
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES), "-ldl", "-lpthread", "-lrt"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / ("build_checked.log" if checked else "build.log")

@@ -35,6 +35,8 @@ thread_local uint64_t* g_trace = nullptr;
 thread_local int g_trace_items = 0;
 const int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
 const int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
+// LSV_SIMT_WAIT=1: SIMT shrinks always wait for the previous launch (A/B timing of the overlap)
+const bool g_simt_wait = [] { const char* e = std::getenv("LSV_SIMT_WAIT"); return e && std::atoi(e) != 0; }();
 const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
@@ -640,7 +642,8 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     LSV_CUDA_CHECK(launch_pdl_any(simt_shrink_kernel, dim3(n_rb, 1, simt_ksplit(h->h_in)), 256, st, simt_pdl,
                                   static_cast<const __nv_bfloat16*>(x), ldx, (int)h->h_in, plan,
                                   (int)h->off_simt_items, (int)h->n_simt_items, a_ptrs,
-                                  reinterpret_cast<float*>(ws + h->ws_simt_v), (int)h->num_proj, (int)h->simt_stride));
+                                  reinterpret_cast<float*>(ws + h->ws_simt_v), (int)h->num_proj, (int)h->simt_stride,
+                                  (wait_prev || !simt_pdl || g_simt_wait) ? 1 : 0));
   }
   if (h->n_shrink_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;

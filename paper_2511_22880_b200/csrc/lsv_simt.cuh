@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
                                                           int h_in, const int32_t* __restrict__ plan,
                                                           int off_items, int n_items,
                                                           const void* const* __restrict__ a_ptrs,
-                                                          float* __restrict__ simt_v, int nproj, int simt_stride) {
+                                                          float* __restrict__ simt_v, int nproj, int simt_stride,
+                                                          int wait_prev) {
   __shared__ float red[8][kSimtShrRows][kSimtMaxTok];   // [warp][row][token]
   const int m = plan[off_items + 5 * n_items + 1 + blockIdx.x];   // row-block map: item << 8 | row block
   const SimtItem it = reinterpret_cast<const SimtItem*>(plan + off_items)[m >> 8];
@@ -83,7 +84,9 @@ __global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* _
   load(cbeg + warp);
   // PDL (lsv_lora_forward): the first A loads above may overlap the previous kernel's tail; x and
   // the v partials are touched only after it has completed.  A no-op for a normal launch.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // wait_prev = 0: the previous launch is another input group's expand, which neither writes this
+  // group's x nor reads its workspace slice (lsv_lora_forward's overlap rule): no wait at all.
+  if (wait_prev) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int c0 = cbeg + warp; c0 < chunks; c0 += 8 * kShrU) {
     if (c0 != cbeg + warp) load(c0);
