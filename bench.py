@@ -56,6 +56,8 @@ def parse_args(argv=None):
     ap.add_argument("--tp-adapters", type=int, default=0,
                     help="config tp: roster size (default 1000 at TP8, scaled by TP/8 below that to fit HBM)")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--tp-padded", action="store_true",
+                    help="config tp: column-group ranks padded to 8*TP (equal shards) instead of balanced shards")
     return ap.parse_args(argv)
 
 
@@ -908,7 +910,7 @@ def run_tp(args, rank, world, local_rank):
     rng = np.random.default_rng(0)
     tok = rng.integers(0, n_ad, 4096)
     seg = index_tokens(tok, ranks)
-    slab = TPSlab(model, world, rank, ranks, dev)
+    slab = TPSlab(model, world, rank, ranks, dev, balanced=not args.tp_padded)
     for s_, r in enumerate(ranks):
         slab.fill_random_shards(s_, 1000 + s_)
     eng = TPLoraDeltaEngine(slab)
@@ -1009,13 +1011,16 @@ def run_tp(args, rank, world, local_rank):
         "config": {"workload": f"llama-3-70b 80 layers x 7 proj, TP{world} (S-LoRA sharding), {n_ad} adapters "
                                f"{traces.assign_power_law_counts(n_ad, traces.DEFAULT_RANKS, 1.0)}, {N} tokens, "
                                f"{seg.num_segments} active", "config": "tp",
+                   "shards": "padded to 8*TP" if args.tp_padded else "balanced (round-robin 8-row groups)",
                    "timing": timing},
         "nccl_ms_per_step": coll_ms, "nccl_share": coll_ms / ms,
         "step_hbm": {"algorithmic_bytes_per_gpu": gpu_bytes, "achieved_GBs_per_gpu": gpu_bytes / (ms * 1e-3) / 1e9,
                      "peak": hbm_peak, "peak_source": peak_src,
                      "frac": gpu_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
-                     "note": "ideal S-LoRA sharding with unpadded ranks; the implementation pads column-group "
-                             "ranks to a multiple of 8*TP (DESIGN.md section 8, item 5)"},
+                     "note": "ideal S-LoRA sharding with unpadded ranks" + (
+                         "; this run pads column-group ranks to a multiple of 8*TP (--tp-padded)" if args.tp_padded else
+                         "; column groups use balanced shards (round-robin 8-row groups, LSV_TP_ROUND_ROBIN): "
+                         "the kernels move the unpadded bytes")},
         "exchange": ("column groups (q/k/v, gate/up): shrink epilogue stores each shard into every rank's full-rank "
                      "v image over NVLink + flag (no NCCL); row groups (o, down): NCCL all-reduce") if fused
                     else "NCCL all-gather (column groups) / all-reduce (row groups)",

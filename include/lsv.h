@@ -153,6 +153,10 @@ int lsv_plan_build_group(int32_t num_segments, const int32_t* seg_indptr, const 
 /* LSV_SEG_SKIP: the segment keeps its token range but gets no work in this plan (two plans over one
  * batch: e.g. local segments on most SMs and peer-owned ones on a few, run on two streams). */
 #define LSV_SEG_SKIP 2
+/* LSV_SEG_NOSHRINK: the segment keeps its m-tiles (so the plan's tile list matches a full-rank plan of
+ * the same batch) but gets no shrink work: a tensor-parallel rank that holds none of the adapter's
+ * rows under balanced sharding (LSV_TP_ROUND_ROBIN).  Pass any valid rank for it. */
+#define LSV_SEG_NOSHRINK 4
 int lsv_plan_size_group_ex(int32_t num_segments, const int32_t* seg_indptr, const int32_t* seg_rank,
                            const int32_t* seg_flags, int32_t h_in, int32_t num_proj, const int32_t* h_outs,
                            int32_t tier_policy, size_t* plan_bytes, size_t* workspace_bytes);
@@ -264,6 +268,11 @@ int lsv_vimg_assemble(const void* gathered, size_t region_bytes, int32_t tp, con
  * lsv_ipc_open_handle; member p at p * full vimg_stride, m-tile at the full plan's offsets), then
  * its last CTA adds 1 to flags[d] on every rank (system-scope release).  full_plan: the full-rank
  * plan (same segments and members).  Tensor-core tier only (LSV_TIER_TC plans). */
+/* OR-ed into lsv_lora_shrink_tp_scatter's tp: balanced shards.  Rank t holds the 8-row groups g of
+ * each adapter's A with g % tp == t (possibly none: LSV_SEG_NOSHRINK), instead of a contiguous
+ * 1/tp of the rank padded to a multiple of 8·tp; its local column k lands at full column
+ * 8·(t + tp·(k/8)) + k%8.  The expand's B keeps the true rank. */
+#define LSV_TP_ROUND_ROBIN 0x100
 int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, int32_t h_in,
                                const void* const* a_ptrs, const void* plan_dev, const void* plan_host,
                                void* workspace, size_t workspace_bytes, int32_t tp, int32_t tp_rank,

@@ -246,6 +246,10 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     any_remote |= remote[s] != 0;
   }
   const std::vector<uint8_t>* rem = any_remote ? &remote : nullptr;
+  // LSV_SEG_NOSHRINK: the segment's m-tiles stay in the plan (indices match a full-rank plan of the
+  // same batch) but this plan shrinks nothing for it (a TP rank holding no rows of its adapter)
+  std::vector<uint8_t> noshrink(S, 0);
+  for (int s = 0; s < S && seg_flags; ++s) noshrink[s] = (seg_flags[s] & LSV_SEG_NOSHRINK) ? 1 : 0;
   const int nsm = sm_budget > 0 ? std::min(sm_budget, num_sms_cached()) : num_sms_cached();
 
   // tier per segment
@@ -307,6 +311,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     int cps = (chunks + nsplit - 1) / nsplit;          // chunks per split, whole 4-chunk stages
     if (nsplit > 1) cps = std::min(chunks, round_up(cps, kShrinkMaxKch));
     nsplit = (chunks + cps - 1) / cps;
+    if (noshrink[mt.seg]) nsplit = 1;
     mt.nsplit = nsplit;
     mt.part_off = (int32_t)part_off;
     if (nsplit > 1) part_off += (int64_t)nsplit * mt.ntok * G;
@@ -314,6 +319,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     // split v: hi image, lo image; tile-aligned images span the whole 128-row tile
     vimg_off += (int64_t)vimg_bytes(tile_aligned ? kTileM : mt.ntok, kpad(r)) * (vsplit ? 2 : 1);
     mt.counter = counter++;
+    if (noshrink[mt.seg]) continue;
     if (nsplit > 1) {  // reduction units: (token, projection, 8 padded-k) of this tile, reduced grid-wide
       pb.red.push_back((int32_t)i);
       pb.red.push_back(pb.red_units);
@@ -625,7 +631,7 @@ int check_common(const PlanHeader* h, size_t workspace_bytes, const void* plan_d
 // writes (lsv_lora_forward's per-(layer, group) workspace slices), so it need not wait for it;
 // pdl = false: a plain launch, ordered after all earlier work in the stream.
 struct TpScatter {
-  int tp = 0, tp_rank = 0, row = 0;
+  int tp = 0, tp_rank = 0, row = 0, rr = 0;
   const PlanHeader* fh = nullptr;
   const int32_t* fplan = nullptr;
   void* const* vdst = nullptr;
@@ -660,7 +666,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
     p.tile_aligned = h->tile_aligned;
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     if (tps != nullptr) {
-      p.tp = tps->tp; p.tp_rank = tps->tp_rank;
+      p.tp = tps->tp; p.tp_rank = tps->tp_rank; p.tp_rr = tps->rr;
       p.tp_row = tps->row; p.xslot = 2 * h->vimg_stride * h->num_proj;
       p.fplan = tps->fplan; p.f_off_mtiles = tps->fh->off_mtiles; p.vstride_f = tps->fh->vimg_stride;
       for (int d = 0; d < tps->tp; ++d) {
@@ -1143,6 +1149,8 @@ int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, i
   const PlanHeader* fh = check_plan(full_plan_host);
   if (int rc = check_common(h, workspace_bytes, plan_dev, workspace)) return rc;
   if (!fh || !full_plan_dev) return fail(LSV_EINVAL, "full_plan is not a liblsv plan");
+  const int rr = (tp & LSV_TP_ROUND_ROBIN) ? 1 : 0;   // shard = 8-row groups g with g % tp == tp_rank
+  tp &= 0xff;
   if (tp < 1 || tp > kMaxTp || tp_rank < 0 || tp_rank >= tp || !vfull_dst || !flags)
     return fail(LSV_EINVAL, "lsv_lora_shrink_tp_scatter: bad tp / rank / destinations");
   if (fh->n_mtiles != h->n_mtiles || fh->num_proj != h->num_proj || fh->num_tokens != h->num_tokens)
@@ -1157,7 +1165,7 @@ int lsv_lora_shrink_tp_scatter(const void* x, int64_t ldx, int32_t num_tokens, i
     if (!vfull_dst[d] || !flags[d]) return fail(LSV_EINVAL, "rank %d: null destination or flag", d);
   if (h->tile_aligned || fh->tile_aligned) return fail(LSV_EUNSUPPORTED, "TP scatter with a tile-aligned plan");
   TpScatter tps;
-  tps.tp = tp; tps.tp_rank = tp_rank; tps.fh = fh; tps.fplan = static_cast<const int32_t*>(full_plan_dev);
+  tps.tp = tp; tps.tp_rank = tp_rank; tps.rr = rr; tps.fh = fh; tps.fplan = static_cast<const int32_t*>(full_plan_dev);
   tps.vdst = vfull_dst; tps.flags = flags;
   return run_shrink(h, x, ldx, num_tokens, a_ptrs, static_cast<const int32_t*>(plan_dev),
                     static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream), 1, true, &tps);

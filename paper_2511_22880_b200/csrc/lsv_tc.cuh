@@ -53,6 +53,8 @@ struct alignas(64) ShrinkParams {
   // (vdst[d]: rank d's image base for this layer/group, CUDA-IPC-mapped); the last CTA then bumps
   // every rank's flag.  fplan: the full-rank plan (same m-tiles) on the device.
   int tp, tp_rank, vstride_f, f_off_mtiles;
+  int tp_rr;                    // 1: shard = the 8-row groups g of the full rank with g % tp == tp_rank
+                                //    (balanced shards, no padding); 0: contiguous rows [tp_rank*rs, +rs)
   const int32_t* fplan;
   uint8_t* vdst[kMaxTp];
   int* flags[kMaxTp];
@@ -174,12 +176,17 @@ constexpr int kExpandRecCh = LSV_EXPAND_RECCH;
 using ShrinkRecBuf = WarpRecBuf<ShrinkRec, kShrinkRecCh>;
 using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
 
+// Full-rank image column of local shard column k (a multiple of 8): contiguous shards put it at
+// tp_rank * rs + k; round-robin shards own every tp-th 8-row group, starting at group tp_rank.
+__device__ __forceinline__ int tp_full_col(const ShrinkParams& p, int k, int rs) {
+  return p.tp_rr ? 8 * (p.tp_rank + p.tp * (k >> 3)) + (k & 7) : p.tp_rank * rs + k;
+}
 // TP scatter of one 16-byte unit (8 k of member pp, token t of m-tile mtile; k local to the shard)
-// into every rank's full-rank image: column tp_rank * rs + k of K = kpad(full rank).
+// into every rank's full-rank image at column tp_full_col of K = kpad(full rank).
 __device__ __forceinline__ void tp_scatter(const ShrinkParams& p, int mtile, int pp, int t, int k, int rs, int np16,
                                            const uint4& w, const uint4& wlo) {
   const MTile mf = reinterpret_cast<const MTile*>(p.fplan + p.f_off_mtiles)[mtile];
-  const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, p.tp_rank * rs + k, kpad(mf.rank), np16);
+  const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, tp_full_col(p, k, rs), kpad(mf.rank), np16);
   const uint32_t lo = vimg_bytes(mf.ntok, kpad(mf.rank));
   for (int d = 0; d < p.tp; ++d) {
     *reinterpret_cast<uint4*>(p.vdst[d] + off) = w;
@@ -190,7 +197,9 @@ __device__ __forceinline__ void tp_scatter(const ShrinkParams& p, int mtile, int
 __device__ __forceinline__ void tp_scatter_pad(const ShrinkParams& p, int mtile, int pp, int t, int np16) {
   const MTile mf = reinterpret_cast<const MTile*>(p.fplan + p.f_off_mtiles)[mtile];
   const int kpf = kpad(mf.rank);
-  if (p.tp_rank != p.tp - 1 || kpf == mf.rank) return;
+  // written by the rank holding the last real 8-row group (contiguous: the last rank)
+  const int writer = p.tp_rr ? (mf.rank / 8 - 1) % p.tp : p.tp - 1;
+  if (p.tp_rank != writer || kpf == mf.rank) return;
   const uint32_t off = (uint32_t)pp * p.vstride_f + mf.vimg_off + vimg_off(t, mf.rank, kpf, np16);
   const uint32_t lo = vimg_bytes(mf.ntok, kpf);
   for (int d = 0; d < p.tp; ++d) {

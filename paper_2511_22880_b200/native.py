@@ -22,6 +22,8 @@ LSV_DTYPE_BF16 = 0
 ABI_VERSION = 3
 TIER_AUTO, TIER_SIMT, TIER_TC = 0, 1, 2
 FWD_SERIAL = 1
+SEG_NOSHRINK = 4    # per-segment plan flag: m-tiles kept, no shrink work (balanced TP shard with no rows)
+TP_ROUND_ROBIN = 0x100   # lsv_lora_shrink_tp_scatter: balanced round-robin 8-row-group shards
 SEG_SKIP = 2        # per-segment plan flag: token range kept, no work in this plan
 SEG_REMOTE = 1      # per-segment plan flag: adapter resident in an NVLink peer's slab
 def PLAN_SMS(n: int) -> int:   # noqa: N802  plan flag: at most n CTAs per kernel

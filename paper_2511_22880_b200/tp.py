@@ -40,6 +40,15 @@ def padded_rank(rank: int, tp: int) -> int:
     return max(q, (rank + q - 1) // q * q)
 
 
+def balanced_rows(rank: int, tp: int, t: int) -> np.ndarray:
+    """Balanced shard (LSV_TP_ROUND_ROBIN): rank t's rows of a column-parallel adapter, the 8-row
+    groups g with g % tp == t, in order.  Rank 8 at TP4 puts its one group on rank 0 and none on
+    the others, instead of padding every adapter to 8*tp rows (+47% of the column groups' adapter
+    bytes at TP4 for the 500-adapter roster)."""
+    groups = np.arange(t, rank // 8, tp)
+    return (groups[:, None] * 8 + np.arange(8)[None, :]).reshape(-1)
+
+
 @dataclass(frozen=True)
 class ShardSpec:
     name: str
@@ -47,11 +56,13 @@ class ShardSpec:
     h_in: int        # this rank's input width
     h_out: int       # this rank's output width
 
-    def a_rank(self, rank: int, tp: int) -> int:
-        return padded_rank(rank, tp) // tp if self.column else rank
+    def a_rank(self, rank: int, tp: int, t: int = 0, balanced: bool = False) -> int:
+        if not self.column:
+            return rank
+        return len(balanced_rows(rank, tp, t)) if balanced else padded_rank(rank, tp) // tp
 
-    def b_rank(self, rank: int, tp: int) -> int:
-        return padded_rank(rank, tp) if self.column else rank
+    def b_rank(self, rank: int, tp: int, balanced: bool = False) -> int:
+        return (rank if balanced else padded_rank(rank, tp)) if self.column else rank
 
 
 def shard_specs(model: ModelShape, tp: int) -> list[ShardSpec]:
@@ -64,7 +75,8 @@ def shard_specs(model: ModelShape, tp: int) -> list[ShardSpec]:
     return out
 
 
-def shard_adapter(lora_a: torch.Tensor, lora_b: torch.Tensor, sp: ShardSpec, tp: int, t: int):
+def shard_adapter(lora_a: torch.Tensor, lora_b: torch.Tensor, sp: ShardSpec, tp: int, t: int,
+                  balanced: bool = False):
     """Rank t's (A_t, B_t) of a full PEFT-layout adapter (lora_A [r, h_in], lora_B [h_out, r]).
 
     Column-parallel: the rank is zero-padded to padded_rank(r, tp); A_t is rank rows
@@ -72,6 +84,10 @@ def shard_adapter(lora_a: torch.Tensor, lora_b: torch.Tensor, sp: ShardSpec, tp:
     the all-gathered v is full rank).  Row-parallel: A_t is the h_in column slice, B_t the h_out
     row slice, both at the full rank (v is a partial sum, all-reduced)."""
     r = lora_a.shape[0]
+    if sp.column and balanced:   # rank t's 8-row groups of A; B at the true rank
+        rows = torch.as_tensor(balanced_rows(r, tp, t), dtype=torch.long, device=lora_a.device)
+        return (lora_a.index_select(0, rows).contiguous(),
+                lora_b[t * sp.h_out:(t + 1) * sp.h_out].contiguous())
     if sp.column:
         rp = padded_rank(r, tp)
         a_pad = lora_a.new_zeros((rp, lora_a.shape[1]))
@@ -92,14 +108,17 @@ class TPSlab:
 
     ALIGN = 1024
 
-    def __init__(self, model: ModelShape, tp: int, rank: int, ranks: list[int], device):
+    def __init__(self, model: ModelShape, tp: int, rank: int, ranks: list[int], device, balanced: bool = False):
+        """``balanced``: column-parallel A shards are round-robin 8-row groups (no padding; only the
+        in-kernel NVLink exchange path consumes them, tp.TPLoraDeltaEngine.forward(fused=True))."""
         self.model, self.tp, self.rank = model, tp, rank
+        self.balanced = balanced
         self.specs = shard_specs(model, tp)
         self.groups = model.groups()
         self._member = {p: (gi, i, len(m)) for gi, (_, m) in enumerate(self.groups) for i, p in enumerate(m)}
         self.device = torch.device(device)
         self.ranks = list(ranks)
-        big = sorted({int(r) for r in ranks if padded_rank(int(r), tp) > 128})
+        big = sorted({int(r) for r in ranks if (int(r) if balanced else padded_rank(int(r), tp)) > 128})
         if big:
             # rank > 128 runs on 64-token tensor-core tiles (lsv_common.cuh mtile_rows), which a
             # rank shard of at most 128 does not get: the shard and full-rank plans would tile the
@@ -115,11 +134,11 @@ class TPSlab:
                 for gi, (_, members) in enumerate(self.groups):
                     sp0 = self.specs[members[0]]
                     self.g_off[s, l, gi] = cur
-                    cur += 2 * len(members) * sp0.a_rank(r, tp) * sp0.h_in
+                    cur += 2 * len(members) * sp0.a_rank(r, tp, rank, balanced) * sp0.h_in
                     for p in members:
                         sp = self.specs[p]
                         self.b_off[s, l, p] = cur
-                        cur += 2 * kpad(sp.b_rank(r, tp)) * sp.h_out
+                        cur += 2 * kpad(sp.b_rank(r, tp, balanced)) * sp.h_out
         self.capacity = cur + self.ALIGN
         ptr = ctypes.c_void_p()
         native.check(native.lib().lsv_slab_alloc(self.capacity, self.device.index or 0, ctypes.byref(ptr)))
@@ -135,10 +154,11 @@ class TPSlab:
         sp = self.specs[proj]
         r = self.ranks[slot]
         gi, idx, nproj = self._member[proj]
-        ra, rb = sp.a_rank(r, self.tp), sp.b_rank(r, self.tp)
+        ra, rb = sp.a_rank(r, self.tp, self.rank, self.balanced), sp.b_rank(r, self.tp, self.balanced)
         lib = native.lib()
-        native.check(lib.lsv_pack_adapter_group(a_sh.data_ptr(), nproj, idx, ra, sp.h_in,
-                                                self.base + int(self.g_off[slot, layer, gi]), st))
+        if ra > 0:   # a balanced shard may hold no rows of this adapter
+            native.check(lib.lsv_pack_adapter_group(a_sh.data_ptr(), nproj, idx, ra, sp.h_in,
+                                                    self.base + int(self.g_off[slot, layer, gi]), st))
         native.check(lib.lsv_pack_adapter(None, b_sh.data_ptr(), rb, sp.h_in, sp.h_out, None,
                                           self.base + int(self.b_off[slot, layer, proj]), st))
 
@@ -147,7 +167,8 @@ class TPSlab:
         """Pack this rank's shard of a full PEFT-layout adapter (lora_A [r, h_in], lora_B [h_out, r])."""
         sp = self.specs[proj]
         st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        a_sh, b_sh = shard_adapter(lora_a.to(self.device), lora_b.to(self.device), sp, self.tp, self.rank)
+        a_sh, b_sh = shard_adapter(lora_a.to(self.device), lora_b.to(self.device), sp, self.tp, self.rank,
+                                   self.balanced)
         self._pack(slot, layer, proj, a_sh.contiguous(), b_sh.contiguous(), st)
 
     def fill_random_full(self, slot: int, seed: int, full: ModelShape) -> None:
@@ -169,8 +190,8 @@ class TPSlab:
         st = torch.cuda.current_stream(self.device).cuda_stream
         for l in range(self.model.layers):
             for p, sp in enumerate(self.specs):
-                ra, rb = sp.a_rank(r, self.tp), sp.b_rank(r, self.tp)
-                a = (torch.randn((ra, sp.h_in), generator=g, device=self.device) * 0.02).to(torch.bfloat16)
+                ra, rb = sp.a_rank(r, self.tp, self.rank, self.balanced), sp.b_rank(r, self.tp, self.balanced)
+                a = (torch.randn((max(ra, 8), sp.h_in), generator=g, device=self.device) * 0.02).to(torch.bfloat16)
                 b = (torch.randn((sp.h_out, rb), generator=g, device=self.device) * 0.1).to(torch.bfloat16)
                 self._pack(slot, l, p, a, b, st)
 
@@ -202,14 +223,20 @@ class TPLoraDeltaEngine:
         tp = self.tp
         plans = {}
         ws_a_need = ws_b_need = 0
+        bal = self.slab.balanced
         for gi, (_, members) in enumerate(self.groups):
             sp0 = self.specs[members[0]]
-            ra = np.array([sp0.a_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
-            rb = np.array([sp0.b_rank(int(r), tp) for r in seg.seg_rank], dtype=np.int32)
+            ra = np.array([sp0.a_rank(int(r), tp, self.rank, bal) for r in seg.seg_rank], dtype=np.int32)
+            rb = np.array([sp0.b_rank(int(r), tp, bal) for r in seg.seg_rank], dtype=np.int32)
+            # a balanced shard with no rows of an adapter: keep its m-tiles (same tiles as the full-rank
+            # plan), no shrink work (LSV_SEG_NOSHRINK; the rank passed is a placeholder)
+            flags = np.where(ra == 0, native.SEG_NOSHRINK, 0).astype(np.int32) if (ra == 0).any() else None
+            ra = np.maximum(ra, 8)
             h_outs = [self.specs[p].h_out for p in members]
-            mk = lambda rr: build_group_plan(Segments(seg.perm, seg.seg_indptr, seg.seg_slot, rr, seg.request_order),  # noqa: E731
-                                             sp0.h_in, h_outs, native.TIER_TC, self.device, members)
-            plan_a = mk(ra)
+            mk = lambda rr, fl=None: build_group_plan(  # noqa: E731
+                Segments(seg.perm, seg.seg_indptr, seg.seg_slot, rr, seg.request_order),
+                sp0.h_in, h_outs, native.TIER_TC, self.device, members, seg_flags=fl)
+            plan_a = mk(ra, flags)
             plan_b = mk(rb) if sp0.column else plan_a
             plans[gi] = (plan_a, plan_b)
             ws_a_need = max(ws_a_need, plan_a.workspace_bytes)
@@ -302,6 +329,8 @@ class TPLoraDeltaEngine:
         lib = native.lib()
         members = self.groups[gi][1]
         sp0 = self.specs[members[0]]
+        if sp0.column and self.slab.balanced:
+            raise ValueError("the NCCL all-gather path needs equal (padded) shards: TPSlab(balanced=False)")
         plan_a, plan_b = st["plans"][gi]
         S = st["seg"].num_segments
         row = layer * len(self.groups) + gi
@@ -399,7 +428,8 @@ class TPLoraDeltaEngine:
                 native.check(lib.lsv_lora_shrink_tp_scatter(
                     x.data_ptr(), x.stride(0), x.shape[0], sp0.h_in,
                     st["a_ptrs"].data_ptr() + (layer * G + gi) * S * 8, plan_a.plan_dev.data_ptr(),
-                    plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(), self.tp, self.rank,
+                    plan_a.plan_host.ctypes.data, ws_a.data_ptr(), ws_a.numel(),
+                    self.tp | (native.TP_ROUND_ROBIN if self.slab.balanced else 0), self.rank,
                     ctypes.addressof(vdst), plan_b.plan_dev.data_ptr(), plan_b.plan_host.ctypes.data,
                     ctypes.addressof(flags), strm.cuda_stream))
                 native.check(lib.lsv_lora_expand_group_tp(
@@ -409,6 +439,8 @@ class TPLoraDeltaEngine:
     def _forward_nccl(self, st: dict, xs, ys, stream=None) -> None:
         """Every layer and group, software-pipelined: the shrink of group g and its NCCL collective
         (side stream) overlap the assembly + expand of group g-1 on the compute stream."""
+        if self.slab.balanced:
+            raise ValueError("the NCCL all-gather path needs equal (padded) shards: TPSlab(balanced=False)")
         lib = native.lib()
         comp = stream or torch.cuda.current_stream(self.device)
         comm = st["comm"]

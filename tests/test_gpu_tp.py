@@ -87,7 +87,7 @@ def test_tp2_column_and_row_parallel():
     assert oracle.max_rel_err(yo, refo) <= TOL
 
 
-def _worker_groups(rank, world, port, q):
+def _worker_groups(rank, world, port, q, balanced=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     torch.cuda.set_device(rank)
@@ -115,7 +115,7 @@ def _worker_groups(rank, world, port, q):
                 for p, pr in enumerate(model.projections):
                     full[(s_, l, p)] = ((torch.randn(r, pr.h_in, generator=g) / pr.h_in ** 0.5).to(torch.bfloat16),
                                         (torch.randn(pr.h_out, r, generator=g) / r ** 0.5).to(torch.bfloat16))
-        slab = TPSlab(model, world, rank, ranks, dev)
+        slab = TPSlab(model, world, rank, ranks, dev, balanced=balanced)
         for (s_, l, p), (a, b) in full.items():
             slab.load_full(s_, l, p, a, b)
         eng = TPLoraDeltaEngine(slab)
@@ -135,7 +135,8 @@ def _worker_groups(rank, world, port, q):
             ys.append(yd)
         eng.forward(st, xs, ys)                      # fused column-group exchange (NVLink stores)
         ys2 = [{k: torch.zeros_like(v) for k, v in yd.items()} for yd in ys]
-        eng.forward(st, xs, ys2, fused=False)        # every group through NCCL
+        if not balanced:
+            eng.forward(st, xs, ys2, fused=False)    # every group through NCCL (equal padded shards only)
         ys3 = [{k: torch.zeros_like(v) for k, v in yd.items()} for yd in ys]
         eng.forward(st, xs, ys3, row_fused=True)     # row groups' all-reduce in the kernels too
         torch.cuda.synchronize()
@@ -143,7 +144,7 @@ def _worker_groups(rank, world, port, q):
         # column groups: the fused exchange moves the same bf16 units NCCL's all-gather moves (identical
         # bits); row groups: fp32 partials summed once vs NCCL's bf16 all-reduce (both within tolerance)
         col = {model.projections[p].name for n, m in model.groups() for p in m if slab.specs[p].column}
-        same = all(torch.equal(ys[l][k], ys2[l][k]) for l in range(model.layers) for k in ys[l] if k in col)
+        same = balanced or all(torch.equal(ys[l][k], ys2[l][k]) for l in range(model.layers) for k in ys[l] if k in col)
         errs = [("fused == nccl", same)]
         for l in range(model.layers):
             for p, pr in enumerate(model.projections):
@@ -168,16 +169,18 @@ def _worker_groups(rank, world, port, q):
 
 
 @pytest.mark.timeout(600)
-def test_tp2_forward_input_groups():
+@pytest.mark.parametrize("balanced", [False, True])
+def test_tp2_forward_input_groups(balanced):
     """TP2 forward over every input group of a 2-layer mini Llama with every exchange inside the
     kernels over NVLink: fused q/k/v and gate/up shrinks store each rank-shard of v into every rank's
     full-rank image (bit-identical to the NCCL all-gather path); o/down shrinks store fp32 partial v
     into every rank's slot and the expands sum them — every projection within the bf16 tolerance of
-    the unsharded oracle."""
+    the unsharded oracle.  ``balanced``: round-robin 8-row-group shards (LSV_TP_ROUND_ROBIN, ranks
+    with no rows of an adapter skip it via LSV_SEG_NOSHRINK) instead of ranks padded to 16."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker_groups, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker_groups, args=(r, 2, port, q, balanced)) for r in range(2)]
     for p in procs:
         p.start()
     import queue as _queue

@@ -92,3 +92,30 @@ def test_tp2_shard_math_gloo():
         assert len(rows) == 6
         for r, name, err in rows:
             assert err < 1e-9, (r, name, err)
+
+
+def test_balanced_shards_cover_every_row_once_and_reassemble():
+    """Balanced (round-robin 8-row group) shards: every row of A on exactly one rank, no padding, and
+    the kernels' column map (full column 8*(t + tp*(k//8)) + k%8 of rank t's local column k) rebuilds
+    v = x·A^T exactly from the per-rank shrinks."""
+    from paper_2511_22880_b200.tp import ShardSpec, balanced_rows, shard_adapter
+    g = torch.Generator().manual_seed(3)
+    for tp in (2, 4, 8):
+        for r in (8, 16, 24, 40, 64, 128):
+            rows = [balanced_rows(r, tp, t) for t in range(tp)]
+            allr = sorted(int(i) for rr in rows for i in rr)
+            assert allr == list(range(r))
+            sp = ShardSpec("q_proj", True, 256, 128 // tp * tp // tp)
+            a = torch.randn(r, 256, generator=g)
+            b = torch.randn(sp.h_out * tp, r, generator=g)
+            x = torch.randn(5, 256, generator=g)
+            v = torch.zeros(5, r)
+            for t in range(tp):
+                a_t, b_t = shard_adapter(a, b, sp, tp, t, balanced=True)
+                assert a_t.shape[0] == len(rows[t]) and b_t.shape[1] == r      # B keeps the true rank
+                assert sp.a_rank(r, tp, t, balanced=True) == a_t.shape[0]
+                v_t = x @ a_t.T
+                for k in range(0, a_t.shape[0], 8):
+                    col = 8 * (t + tp * (k // 8))
+                    v[:, col:col + 8] = v_t[:, k:k + 8]
+            assert torch.allclose(v, x @ a.T, atol=1e-5)
