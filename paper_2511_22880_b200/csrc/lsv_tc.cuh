@@ -236,6 +236,10 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 #ifndef LSV_SHRINK_LAYOUT
 #define LSV_SHRINK_LAYOUT 1
 #endif
+// Shrink producer: 1 = converged warp, elected-lane copies; 0 = lanes issue the x boxes in parallel.
+#ifndef LSV_SHRINK_PROD_WARP
+#define LSV_SHRINK_PROD_WARP 1
+#endif
 #if LSV_SHRINK_LAYOUT
 constexpr int kShrProdWarp = 2, kShrMmaWarp = 3, kShrinkThreads = 256;
 __device__ __forceinline__ bool shrink_epi_warp(int w) { return w < 2 || w >= 6; }
@@ -274,6 +278,17 @@ __device__ __forceinline__ int expand_qbase(int k, int ntok) {
 // 4 B evict-first and y evict-last.
 #ifndef LSV_EXPAND_EF
 #define LSV_EXPAND_EF 0
+#endif
+// Expand MMA issue: 1 = the whole MMA warp runs the item loop (election inside the MMA asm,
+// descriptors advanced by constant steps); 0 = lane 0 alone (ptxas wraps each MMA in a
+// uniformization loop).
+#ifndef LSV_EXPAND_MMA_WARP
+#define LSV_EXPAND_MMA_WARP 1
+#endif
+// Expand producer: 1 = the whole warp runs the loop converged and each copy is issued by an
+// elected lane; 0 = lane 0 allocates, lanes issue the item's copies in parallel.
+#ifndef LSV_EXPAND_PROD_WARP
+#define LSV_EXPAND_PROD_WARP 1
 #endif
 #ifndef LSV_EXPAND_EPI_WARPS
 #define LSV_EXPAND_EPI_WARPS 4
@@ -401,6 +416,39 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       LSV_DCHECK(inf.chunk_begin >= 0 && inf.chunk_begin < inf.chunk_end && inf.chunk_end * kChunk <= p.h_in);
       LSV_DCHECK(kch >= 1 && kch * (np8 + rows) * 128 <= kShrinkSlotBytes && a != nullptr);
       const int m = np8 >> 3, pc = __popc(m);   // x boxes per chunk: one per set bit of np8/8
+#if LSV_SHRINK_PROD_WARP
+      // converged: every lane computes the same operands, an elected lane issues each copy (no
+      // per-lane uniformization loop around the TMA instructions)
+      const uint32_t ring_base = smem_u32(ring);
+      for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
+        const int kc = min(kch, inf.chunk_end - g);
+        mbar_wait(&empty[slot], phase ^ 1);
+        const uint32_t fb = smem_u32(&full[slot]);
+        mbar_arrive_expect_tx_elect(fb, (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : rows)) * 128));
+        const uint32_t dst = ring_base + slot * kShrinkSlotBytes;
+        if (!(p.dbg & 2)) {
+          if (rows == G) {       // whole group: the kc chunks are one contiguous run
+            bulk_load_elect(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), fb);
+          } else {               // projection subset: one copy per chunk
+            for (int c = 0; c < kc; ++c)
+              bulk_load_elect(dst + (kc * np8 + c * rows) * 128, asub + (size_t)(g + c) * G * 128, (uint32_t)(rows * 128), fb);
+          }
+        }
+        if (!(p.dbg & 4)) {
+          for (int c = 0; c < kc; ++c) {
+            int mm = m, row = 0;
+            while (mm) {
+              const int bb = 31 - __clz(mm);
+              tma_load_2d_elect(dst + (c * np8 + row) * 128, &p.xmap[bb], fb, (g + c) * kChunk, inf.tok_begin + row);
+              row += 8 << bb;
+              mm &= ~(1 << bb);
+            }
+          }
+        }
+        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
+      }
+      (void)pc;
+#else
       for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
         const int kc = min(kch, inf.chunk_end - g);
         if (lane == 0) {
@@ -433,6 +481,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
         }
         if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
+#endif
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
       __syncwarp();
     }
@@ -760,7 +809,77 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == kExpProdWarp) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
+  if (warp == kExpProdWarp && LSV_EXPAND_PROD_WARP) {  // ---------------- producer (whole warp, converged)
+    // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
+    // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
+    // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
+    ExpandRec inf;
+    const uint8_t* b;
+    uint32_t head = 0, tail = 0;
+    uint32_t vbegin[kItemQ];
+    int retired = 0;
+    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+    for (int k = 0; rs.pop(inf, b); ++k) {
+      const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
+      const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
+      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2 + (p.vsplit ? vlo : 0), ybytes = nb * np16 * 128;
+      const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
+      const uint32_t size = yoff + ybytes;
+      const int qs = k % kItemQ;
+      const uint32_t extent =
+          max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
+      head = round_up(head, 1024);
+      if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
+        head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
+      LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
+      LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
+      LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
+      LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+      while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
+        mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
+        ++retired;
+        tail = retired < k ? vbegin[retired % kItemQ] : head;
+      }
+      vbegin[qs] = head;
+      const uint32_t ring_off = head % kExpandRingBytes;
+      if (lane == 0) offs[qs] = ring_off;
+      head += size;
+      const int dbg = p.dbg;
+      const uint32_t fb = smem_u32(&full[qs]);
+      mbar_arrive_expect_tx_elect(fb, ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) + ((dbg & 8) ? 0 : ybytes));
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+      const uint32_t dst = ring_base + ring_off;
+      if (!(dbg & 16)) {
+        if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group
+          const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
+          const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
+          for (int kg = 0; kg < kp / 8; ++kg)
+            bulk_load_elect(dst + kg * nb * 1024, src + (size_t)kg * (twl / 64) * 1024, (uint32_t)(nb * 1024), fb);
+        } else {
+          bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
+        }
+      }
+      if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
+      if (!(dbg & 8)) {
+        // y rows [tok_begin, +np16) of each 64-column block: one box per set bit of np16 / 8
+        const int m = np16 >> 3;
+        for (int h = 0; h < nb; ++h) {
+          int mm = m, row = 0;
+          while (mm) {
+            const int bbit = 31 - __clz(mm);
+            tma_load_2d_elect(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bbit], fb,
+                              inf.jtile * tw + h * 64, inf.tok_begin + row);
+            row += 8 << bbit;
+            mm &= ~(1 << bbit);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == kExpProdWarp) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
     ExpandRec inf;
     const uint8_t* b;
@@ -839,6 +958,64 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
                       inf.jtile * tw + h * 64, inf.tok_begin + row);
 #endif
       }
+      __syncwarp();
+    }
+  } else if (warp == kExpMmaWarp && LSV_EXPAND_MMA_WARP) {  // ---------------- MMA issuer (whole warp)
+    // Every lane runs the loop and computes the same descriptors; the election happens inside the
+    // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
+    // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
+    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+    ExpandRec inf;
+    const uint8_t* unused;
+    const uint32_t ib = smem_u32(ident);
+    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+    for (int k = 0; rs.pop(inf, unused); ++k) {
+      const int r = inf.rank;
+      const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
+      const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
+      const int qs = k % kItemQ;
+      const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
+      const int S = kmajor_row_bytes(kp), ck = S / 2;
+      const uint32_t vlay = umma_layout(S);
+      const int buf = k % nbuf;
+      mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
+      mbar_wait(&full[qs], (k / kItemQ) & 1);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 6);
+      tc_fence_after();
+      const uint32_t bb = ring_base + offs[qs];
+      const uint32_t voff = round_up(tw * kp * 2, 1024);
+      const uint32_t vb = bb + voff;
+      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+      const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
+      const uint32_t d = tmem_base + buf * p.tw_max;
+      const int qrow = 32 * expand_qbase(k, inf.ntok);
+      const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
+      // D = v . B (+ v_lo . B): A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128).
+      // K step ks: A advances 32 B inside a swizzle row, np16 rows of S bytes per ck-element chunk;
+      // B advances one 2 * nb KB group of 16 k.
+      const uint64_t a0 = smem_desc(vb - qrow * S, 16, 8 * S, vlay);
+      const uint64_t b0 = smem_desc(bb, 1024, nb * 1024, 2);
+      const uint32_t bstep = (2 * nb * 1024) >> 4, cstep = (np16 * S) >> 4;
+      for (int h = 0; h < (p.vsplit ? 2 : 1); ++h) {
+        uint64_t arow = a0 + (h ? (vlo >> 4) : 0u), bd = b0;
+        for (int ks = 0; ks < nv; ++ks) {
+          const uint32_t in_row = (uint32_t)((ks * 16) % ck) * 2 >> 4;
+          umma_bf16_elect(d, arow + in_row, bd, idesc_mn, (h | ks) ? 1u : 0u);
+          bd += bstep;
+          if (((ks + 1) * 16) % ck == 0) arow += cstep;
+        }
+      }
+      // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
+      uint64_t ai = smem_desc(ib + (128 - qrow) * 32, 16, 256, 6), by = smem_desc(yb, np16 * 128, 1024, 2);
+      for (int ks = 0; ks < ny; ++ks) {
+        umma_bf16_elect(d, ai, by, idesc_mn, 1u);
+        ai -= 32;          // 16 rows x 32 B
+        by += 128;         // 2048 B
+      }
+      umma_commit_elect(&empty[qs]);   // ring bytes free once these MMAs have read them
+      umma_commit_elect(&tfull[buf]);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
       __syncwarp();
     }
   } else if (warp == kExpMmaWarp) {  // ---------------- MMA issuer (lane 0)
