@@ -531,11 +531,12 @@ std::mutex g_map_mu;
 std::unordered_map<MapKey, std::vector<CUtensorMap>, MapKeyHash> g_map_cache;
 
 // kind 0: x maps (5 boxes of 64 cols x 8<<b rows, SWIZZLE_128B)
-// kind 1: y maps (8 boxes of 128 cols x 1<<b rows, no swizzle)
+// kind 1: expand y maps, 3D {64 cols, rows, cols/64 blocks} (strides ld*2, 128 B): 10 boxes
+//         {64, 8<<b rows, 4 blocks} (b = 0..4) then {64, 8<<b, 2 blocks}, SWIZZLE_128B
 // kind 2: base-weight maps (1 box of 64 cols x 256 rows, SWIZZLE_128B)
 int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t rows, int32_t cols) {
   const MapKey key{reinterpret_cast<uintptr_t>(ptr), ld, rows, cols, kind};
-  const int nmaps = kind == 0 ? 5 : kind == 1 ? 8 : 1;
+  const int nmaps = kind == 0 ? 5 : kind == 1 ? 10 : 1;
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_map_cache.find(key);
@@ -547,15 +548,25 @@ int get_maps(CUtensorMap* out, int kind, const void* ptr, int64_t ld, int32_t ro
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   std::vector<CUtensorMap> maps(nmaps);
-  for (int b = 0; b < nmaps; ++b) {
+  for (int b = 0; b < nmaps && kind == 1; ++b) {
+    if (cols % 64) return fail(LSV_EINVAL, "y width %d is not a multiple of 64", cols);
+    const cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+    const cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128};
+    const cuuint32_t box[3] = {64, (cuuint32_t)(8 << (b % 5)), b < 5 ? 4u : 2u};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) for a 3D y map, box %d", (int)r, b);
+  }
+  for (int b = 0; b < nmaps && kind != 1; ++b) {
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    const cuuint32_t box[2] = {kind == 1 ? (cuuint32_t)128 : (cuuint32_t)kChunk,
-                               kind == 0 ? (cuuint32_t)(8 << b) : kind == 1 ? (cuuint32_t)(1 << b) : (cuuint32_t)kFusedTileN};
+    const cuuint32_t box[2] = {(cuuint32_t)kChunk, kind == 0 ? (cuuint32_t)(8 << b) : (cuuint32_t)kFusedTileN};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&maps[b], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     kind == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return fail(LSV_ECUDA, "cuTensorMapEncodeTiled failed (%d) kind %d box %d", (int)r, kind, b);
@@ -717,7 +728,10 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   for (int pp = 0; pp < h->num_proj; ++pp) {
     const int i = all ? pp : (pp == p0 ? 0 : -1);
     if (i < 0) continue;
-    if (int rc = get_maps(p.ymap[pp], 0, ys[i], ldys[i], num_tokens, h->h_outs[pp])) return rc;
+    CUtensorMap ym[10];
+    if (int rc = get_maps(ym, 1, ys[i], ldys[i], num_tokens, h->h_outs[pp])) return rc;
+    std::memcpy(p.ymap[pp], ym, sizeof(CUtensorMap) * 5);
+    std::memcpy(p.ymap2[pp], ym + 5, sizeof(CUtensorMap) * 5);
     p.y[pp] = static_cast<__nv_bfloat16*>(ys[i]);
     p.ldy[pp] = ldys[i];
     p.b_ptrs[pp] = b_ptrs[i];

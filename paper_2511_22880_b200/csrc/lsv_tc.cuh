@@ -68,7 +68,11 @@ struct alignas(64) ShrinkParams {
 };
 
 struct alignas(64) ExpandParams {
-  CUtensorMap ymap[kMaxProj][5];   // per member: y [num_tokens][h_out], boxes {64 cols x 8<<b rows}, SW128
+  // per member: y [num_tokens][h_out] as 3D {64 cols, rows, h_out/64 blocks} (strides 2 B, ldy*2 B,
+  // 128 B), SWIZZLE_128B boxes {64, 8<<b rows, 4 blocks} (256-wide items) / {64, 8<<b, 2} (128-wide):
+  // one copy lands a row range of every 64-column block of the item as [block][rows][64]
+  CUtensorMap ymap[kMaxProj][5];
+  CUtensorMap ymap2[kMaxProj][5];
   const int32_t* plan;
   const void* const* b_ptrs[kMaxProj];
   uint8_t* ws;
@@ -274,22 +278,6 @@ __device__ __forceinline__ int expand_qbase(int k, int ntok) {
   return 0;
 #endif
 }
-// L2 hints on the expand's loads: 0 off; 1 B evict-first; 2 B and y evict-first; 3 y evict-last;
-// 4 B evict-first and y evict-last.
-#ifndef LSV_EXPAND_EF
-#define LSV_EXPAND_EF 0
-#endif
-// Expand MMA issue: 1 = the whole MMA warp runs the item loop (election inside the MMA asm,
-// descriptors advanced by constant steps); 0 = lane 0 alone (ptxas wraps each MMA in a
-// uniformization loop).
-#ifndef LSV_EXPAND_MMA_WARP
-#define LSV_EXPAND_MMA_WARP 1
-#endif
-// Expand producer: 1 = the whole warp runs the loop converged and each copy is issued by an
-// elected lane; 0 = lane 0 allocates, lanes issue the item's copies in parallel.
-#ifndef LSV_EXPAND_PROD_WARP
-#define LSV_EXPAND_PROD_WARP 1
-#endif
 #ifndef LSV_EXPAND_EPI_WARPS
 #define LSV_EXPAND_EPI_WARPS 4
 #endif
@@ -765,7 +753,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
     fence_mbar_init();
     for (int pp = 0; pp < kMaxProj; ++pp)
       if (p.y[pp])
-        for (int b = 0; b < 5; ++b) prefetch_tmap(&p.ymap[pp][b]);
+        for (int b = 0; b < 5; ++b) { prefetch_tmap(&p.ymap[pp][b]); prefetch_tmap(&p.ymap2[pp][b]); }
   }
   if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
@@ -809,7 +797,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  if (warp == kExpProdWarp && LSV_EXPAND_PROD_WARP) {  // ---------------- producer (whole warp, converged)
+  if (warp == kExpProdWarp) {  // ---------------- producer (whole warp, converged)
     // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
     // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
     // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
@@ -863,104 +851,23 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         }
       }
       if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
+      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 3);
       if (!(dbg & 8)) {
-        // y rows [tok_begin, +np16) of each 64-column block: one box per set bit of np16 / 8
-        const int m = np16 >> 3;
-        for (int h = 0; h < nb; ++h) {
-          int mm = m, row = 0;
-          while (mm) {
-            const int bbit = 31 - __clz(mm);
-            tma_load_2d_elect(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bbit], fb,
-                              inf.jtile * tw + h * 64, inf.tok_begin + row);
-            row += 8 << bbit;
-            mm &= ~(1 << bbit);
-          }
+        // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
+        // [nb blocks][R rows][64] at yoff + row * nb * 128
+        const CUtensorMap* ym = nb == 4 ? p.ymap[inf.proj] : p.ymap2[inf.proj];
+        int mm = np16 >> 3, row = 0;
+        while (mm) {
+          const int bbit = 31 - __clz(mm);
+          tma_load_3d_elect(dst + yoff + row * nb * 128, &ym[bbit], fb, 0, inf.tok_begin + row, inf.jtile * nb);
+          row += 8 << bbit;
+          mm &= ~(1 << bbit);
         }
       }
+      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 4);
       __syncwarp();
     }
-  } else if (warp == kExpProdWarp) {  // ---------------- producer: lane 0 allocates ring bytes, lanes issue copies
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
-    ExpandRec inf;
-    const uint8_t* b;
-    uint32_t head = 0, tail = 0;
-    uint32_t vbegin[kItemQ];
-    int retired = 0;
-    for (int k = 0; rs.pop(inf, b); ++k) {
-      const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
-      const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
-      // split v: the lo image follows the hi image (vimg_bytes apart, as in the workspace): one copy
-      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
-      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2 + (p.vsplit ? vlo : 0), ybytes = nb * np16 * 128;
-      const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
-      const uint32_t size = yoff + ybytes;
-      const int qs = k % kItemQ;
-      uint32_t ring_off = 0;
-      if (lane == 0) {
-        // the M=128 MMA reads 128 v rows per K chunk (rows >= ntok only feed discarded D rows):
-        // the item must sit where that read stays inside the ring + guard
-        const uint32_t extent =
-            max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
-        head = round_up(head, 1024);
-        if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
-          head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
-        LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
-        LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
-        LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
-        LSV_DCHECK(p.wait_flag != nullptr ||
-                   (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
-        trace_stamp(p.trace, p.trace_items, cta, k, 0);
-        // retire in FIFO order until an allocation slot and the ring bytes are free
-        while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
-          mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
-          ++retired;
-          tail = retired < k ? vbegin[retired % kItemQ] : head;
-        }
-        vbegin[qs] = head;
-        ring_off = head % kExpandRingBytes;
-        offs[qs] = ring_off;
-        head += size;
-        const int dbg = p.dbg;
-        mbar_arrive_expect_tx(&full[qs], ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) + ((dbg & 8) ? 0 : ybytes));
-        trace_stamp(p.trace, p.trace_items, cta, k, 1);
-      }
-      ring_off = __shfl_sync(0xffffffffu, ring_off, 0);
-      uint8_t* dst = ring + ring_off;
-      const int dbg = p.dbg;
-      if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group, one copy per lane
-        const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
-        const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
-        if (!(dbg & 16))
-          for (int kg = lane; kg < kp / 8; kg += 32)
-            bulk_load(dst + kg * nb * 1024, src + (size_t)kg * (twl / 64) * 1024, (uint32_t)(nb * 1024), &full[qs]);
-      }
-      if (lane == 0) {
-        if (tw == twl && !(dbg & 16)) {
-#if LSV_EXPAND_EF == 1 || LSV_EXPAND_EF == 2 || LSV_EXPAND_EF == 4
-          bulk_load_hint(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs], l2_evict_first_policy());
-#else
-          bulk_load(dst, b + (size_t)inf.jtile * bbytes, bbytes, &full[qs]);
-#endif
-        }
-      } else if (lane == 1) {
-        if (!(dbg & 32)) bulk_load(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, &full[qs]);
-      } else if (!(dbg & 8)) {
-        int h, row, bb;
-        if (y_box(np16, nb, lane - 2, h, row, bb))
-#if LSV_EXPAND_EF >= 3
-          tma_load_2d_hint(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
-                           inf.jtile * tw + h * 64, inf.tok_begin + row, l2_evict_last_policy());
-#elif LSV_EXPAND_EF == 2
-          tma_load_2d_hint(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
-                           inf.jtile * tw + h * 64, inf.tok_begin + row, l2_evict_first_policy());
-#else
-          tma_load_2d(dst + yoff + h * np16 * 128 + row * 128, &p.ymap[inf.proj][bb], &full[qs],
-                      inf.jtile * tw + h * 64, inf.tok_begin + row);
-#endif
-      }
-      __syncwarp();
-    }
-  } else if (warp == kExpMmaWarp && LSV_EXPAND_MMA_WARP) {  // ---------------- MMA issuer (whole warp)
+  } else if (warp == kExpMmaWarp) {  // ---------------- MMA issuer (whole warp)
     // Every lane runs the loop and computes the same descriptors; the election happens inside the
     // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
     // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
@@ -1007,78 +914,27 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
         }
       }
       // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
-      uint64_t ai = smem_desc(ib + (128 - qrow) * 32, 16, 256, 6), by = smem_desc(yb, np16 * 128, 1024, 2);
-      for (int ks = 0; ks < ny; ++ks) {
-        umma_bf16_elect(d, ai, by, idesc_mn, 1u);
-        ai -= 32;          // 16 rows x 32 B
-        by += 128;         // 2048 B
+      // y sits in boxes of R = 8 << b rows (largest first), box at yb + row0 * nb * 128 with block
+      // stride R * 128; every box holds whole 16-row K steps (np16 / 8 is even)
+      uint64_t ai = smem_desc(ib + (128 - qrow) * 32, 16, 256, 6);
+      {
+        int mm = np16 >> 3, row0 = 0, ks = 0;
+        while (mm && ks < ny) {
+          const int bbit = 31 - __clz(mm), R = 8 << bbit;
+          uint64_t by = smem_desc(yb + row0 * nb * 128, R * 128, 1024, 2);
+          for (int r = 0; r < R && ks < ny; r += 16, ++ks) {
+            umma_bf16_elect(d, ai, by, idesc_mn, 1u);
+            ai -= 32;      // 16 identity rows x 32 B
+            by += 128;     // 16 y rows x 128 B
+          }
+          row0 += R;
+          mm &= ~(1 << bbit);
+        }
       }
       umma_commit_elect(&empty[qs]);   // ring bytes free once these MMAs have read them
       umma_commit_elect(&tfull[buf]);
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
       __syncwarp();
-    }
-  } else if (warp == kExpMmaWarp) {  // ---------------- MMA issuer (lane 0)
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
-    ExpandRec inf;
-    const uint8_t* unused;
-    const uint32_t ib = smem_u32(ident);
-    for (int k = 0; rs.pop(inf, unused); ++k) {
-      if (lane == 0) {
-        trace_aux(p.trace, p.trace_items, cta, k, 1);
-        const int r = inf.rank;
-        const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
-        const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
-        const int qs = k % kItemQ;
-        const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
-        const int S = kmajor_row_bytes(kp), ck = S / 2;
-        const uint32_t vlay = umma_layout(S);
-        const int buf = k % nbuf;
-        trace_aux(p.trace, p.trace_items, cta, k, 2);
-        mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
-        trace_stamp(p.trace, p.trace_items, cta, k, 5);
-        mbar_wait(&full[qs], (k / kItemQ) & 1);
-        trace_stamp(p.trace, p.trace_items, cta, k, 6);
-        tc_fence_after();
-        const uint32_t bb = smem_u32(ring + offs[qs]);
-        const uint32_t voff = round_up(tw * kp * 2, 1024);
-        const uint32_t vb = bb + voff;
-        const uint32_t vlo = vimg_bytes(inf.ntok, kp);
-        const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
-        const uint32_t d = tmem_base + buf * p.tw_max;
-        // quadrant rotation: A starts qrow rows early (whole swizzle atoms; the rows before the v
-        // image are this item's B tile, >= 96 * S bytes, and only feed discarded D lanes)
-        const int qrow = 32 * expand_qbase(k, inf.ntok);
-        // D = v . B : A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128)
-        const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
-        for (int ks = 0; ks < nv; ++ks) {
-          const int kk = ks * 16;
-          const uint64_t adesc = smem_desc(vb + (kk / ck) * np16 * S + (kk % ck) * 2 - qrow * S, 16, 8 * S, vlay);
-          const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
-          umma_bf16(d, adesc, bdesc, idesc_mn, ks > 0 ? 1u : 0u);
-        }
-        // split v: D += v_lo . B (same B descriptors, the lo image vlo bytes after the hi image)
-        if (p.vsplit)
-          for (int ks = 0; ks < nv; ++ks) {
-            const int kk = ks * 16;
-            const uint64_t adesc =
-                smem_desc(vb + vlo + (kk / ck) * np16 * S + (kk % ck) * 2 - qrow * S, 16, 8 * S, vlay);
-            const uint64_t bdesc = smem_desc(bb + ks * 2 * nb * 1024, 1024, nb * 1024, 2);
-            umma_bf16(d, adesc, bdesc, idesc_mn, 1u);
-          }
-        // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
-        for (int ks = 0; ks < ny; ++ks) {
-          const uint64_t adesc = smem_desc(ib + (128 - 16 * ks - qrow) * 32, 16, 256, 6);
-          const uint64_t bdesc = smem_desc(yb + ks * 2048, np16 * 128, 1024, 2);
-          umma_bf16(d, adesc, bdesc, idesc_mn, 1u);
-        }
-        trace_stamp(p.trace, p.trace_items, cta, k, 7);
-        umma_commit(&empty[qs]);   // ring bytes free once these MMAs have read them
-        umma_commit(&tfull[buf]);
-        trace_stamp(p.trace, p.trace_items, cta, k, 2);
-      }
-      __syncwarp();
-      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 0);
     }
   } else if (expand_epi_warp(warp)) {  // ---------------- epilogue: thread = token row of quadrant q
     const int q = warp & 3;

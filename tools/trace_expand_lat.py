@@ -171,3 +171,15 @@ for k in range(min(n, 30)):
     held = sum(int(size[j]) for j in range(k) if e[j] > p0s[k]) / 1024
     print(f"  {k:2d} {recs[k, 3]:4d} {recs[k, 2]:4d} {size[k] / 1024:6.1f} {held:7.1f} {a[k] - p0s[k]:6d} | "
           f"{p0s[k] - t0:7d} {a[k] - t0:7d} {l[k] - t0:7d} {e[k] - t0:7d}")
+if (aux[:, 1:, 3] > 0).any():
+    pr = {k: [] for k in ("alloc->bulk_issued", "bulk->y_issued", "y_issued->next_p0")}
+    for c in range(148):
+        n = int((cyc[c, :ITEMS - 1, 0] > 0).sum())
+        for i in range(n - 1):
+            pr["alloc->bulk_issued"].append(aux[c, i, 3] - cyc[c, i, 1])
+            pr["bulk->y_issued"].append(aux[c, i, 4] - aux[c, i, 3])
+            pr["y_issued->next_p0"].append(cyc[c, i + 1, 0] - aux[c, i, 4])
+    print("producer per item (cycles):")
+    for k, v in pr.items():
+        v = np.array(v)
+        print(f"  {k:20s} mean {v.mean():7.0f}  p50 {np.median(v):7.0f}  p90 {np.percentile(v, 90):7.0f}")
