@@ -37,6 +37,9 @@ const int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK");
 const int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
 // LSV_SIMT_WAIT=1: SIMT shrinks always wait for the previous launch (A/B timing of the overlap)
 const bool g_simt_wait = [] { const char* e = std::getenv("LSV_SIMT_WAIT"); return e && std::atoi(e) != 0; }();
+// LSV_GROUP_KERNEL=0: lsv_lora_forward runs each group as a shrink launch + an expand launch
+// instead of one group kernel (A/B timing)
+const bool g_group_kernel = [] { const char* e = std::getenv("LSV_GROUP_KERNEL"); return !e || std::atoi(e) != 0; }();
 const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
@@ -318,7 +321,10 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     mt.vimg_off = (int32_t)vimg_off;  // 1024-aligned: the v image's swizzle atoms are address-based
     // split v: hi image, lo image; tile-aligned images span the whole 128-row tile
     vimg_off += (int64_t)vimg_bytes(tile_aligned ? kTileM : mt.ntok, kpad(r)) * (vsplit ? 2 : 1);
-    mt.counter = counter++;
+    int nsub = 0;
+    for (int p0 = 0; p0 < P; p0 += subset_np(P, p0, r)) ++nsub;
+    mt.counter = noshrink[mt.seg] ? 0 : nsplit * nsub;   // shrink records of the tile (group kernel's ready target)
+    ++counter;
     if (noshrink[mt.seg]) continue;
     if (nsplit > 1) {  // reduction units: (token, projection, 8 padded-k) of this tile, reduced grid-wide
       pb.red.push_back((int32_t)i);
@@ -588,7 +594,10 @@ int ensure_smem_attrs() {
                                           expand_smem_bytes());
     cudaError_t e3 = cudaFuncSetAttribute(fused_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           fused_smem_bytes());
+    cudaError_t e4 = cudaFuncSetAttribute(group_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          group_smem_bytes());
     if (e2 == cudaSuccess) e2 = e3;
+    if (e2 == cudaSuccess) e2 = e4;
     rc = (e1 == cudaSuccess && e2 == cudaSuccess) ? LSV_OK : LSV_ECUDA;
     if (rc) fail(LSV_ECUDA, "cudaFuncSetAttribute(smem) failed: %s / %s", cudaGetErrorString(e1), cudaGetErrorString(e2));
   });
@@ -649,6 +658,12 @@ struct TpScatter {
   int32_t* const* flags = nullptr;
 };
 
+int fill_shrink_params(ShrinkParams& p, const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens,
+                       const void* const* a_ptrs, const int32_t* plan, uint8_t* ws, int* gbar);
+int fill_expand_params(ExpandParams& p, const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys,
+                       int32_t num_tokens, const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws,
+                       const uint8_t* vimg_base);
+
 int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
                const int32_t* plan, uint8_t* ws, cudaStream_t st, int wait_prev = 1, bool pdl = true,
                const TpScatter* tps = nullptr, bool simt_pdl = false, int* gbar = nullptr) {
@@ -665,16 +680,7 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
   if (h->n_shrink_items > 0) {
     if (int rc = ensure_smem_attrs()) return rc;
     ShrinkParams p{};
-    if (int rc = get_maps(p.xmap, 0, x, ldx, num_tokens, h->h_in)) return rc;
-    p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
-    p.off_recs = h->off_shrink_recs; p.off_cta = h->off_shrink_cta;
-    p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg;
-    p.gbar = gbar ? gbar : reinterpret_cast<int*>(ws);
-    p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
-    p.off_red_cta = h->off_red_cta;
-    p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
-    p.vsplit = h->vsplit;
-    p.tile_aligned = h->tile_aligned;
+    if (int rc = fill_shrink_params(p, h, x, ldx, num_tokens, a_ptrs, plan, ws, gbar)) return rc;
     p.wait_prev = (wait_prev || h->n_simt_items > 0) ? 1 : 0;   // a SIMT launch in between is not PDL
     if (tps != nullptr) {
       p.tp = tps->tp; p.tp_rank = tps->tp_rank; p.tp_rr = tps->rr;
@@ -685,10 +691,27 @@ int run_shrink(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_toke
         p.flags[d] = tps->flags[d];
       }
     }
+    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl, kShrinkThreads));
+  }
+  return LSV_OK;
+}
+
+int fill_shrink_params(ShrinkParams& p, const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens,
+                       const void* const* a_ptrs, const int32_t* plan, uint8_t* ws, int* gbar) {
+  {
+    if (int rc = get_maps(p.xmap, 0, x, ldx, num_tokens, h->h_in)) return rc;
+    p.plan = plan; p.a_ptrs = a_ptrs; p.ws = ws;
+    p.off_recs = h->off_shrink_recs; p.off_cta = h->off_shrink_cta;
+    p.ws_partials = h->ws_partials; p.ws_vimg = h->ws_vimg;
+    p.gbar = gbar ? gbar : reinterpret_cast<int*>(ws);
+    p.off_mtiles = h->off_mtiles; p.off_red = h->off_red; p.n_red = h->n_red; p.red_units = h->red_units;
+    p.off_red_cta = h->off_red_cta;
+    p.num_proj = h->num_proj; p.vimg_stride = h->vimg_stride; p.acc_cols = h->acc_cols;
+    p.vsplit = h->vsplit;
+    p.tile_aligned = h->tile_aligned;
     p.dbg = g_debug_shrink;
     p.trace = g_trace; p.trace_items = g_trace_items;
     p.num_tokens = num_tokens; p.h_in = h->h_in; p.ws_bytes = h->ws_bytes;
-    LSV_CUDA_CHECK(launch_pdl(shrink_tc_kernel, h->shrink_grid, shrink_smem_bytes(), st, p, pdl, kShrinkThreads));
   }
   return LSV_OK;
 }
@@ -724,6 +747,25 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
   if (n_items == 0) return LSV_OK;
   if (int rc = ensure_smem_attrs()) return rc;
   ExpandParams p{};
+  if (int rc = fill_expand_params(p, h, p0, np, ys, ldys, num_tokens, b_ptrs, plan, ws, vimg_base)) return rc;
+  p.wait_flag = wait_flag; p.wait_target = wait_target;
+  if (xsum != nullptr) {
+    p.xsum = xsum; p.xslot = 2 * h->vimg_stride * h->num_proj; p.ws_vimg0 = h->ws_vimg;
+    p.off_mtiles = h->off_mtiles; p.n_mtiles = h->n_mtiles; p.num_proj = h->num_proj;
+    p.vimg_stride = h->vimg_stride;
+    p.gbar = reinterpret_cast<int*>(ws);
+  }
+  LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, all ? h->expand_grid_all : h->expand_grid_p[p0], expand_smem_bytes(),
+                            st, p, true, kExpandThreads));
+  LSV_CUDA_CHECK(cudaGetLastError());
+  return LSV_OK;
+}
+
+// Expand parameters of members [p0, p0 + np) (np == num_proj > 1: the combined list).
+int fill_expand_params(ExpandParams& p, const PlanHeader* h, int p0, int np, void* const* ys, const int64_t* ldys,
+                       int32_t num_tokens, const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws,
+                       const uint8_t* vimg_base) {
+  const bool all = np == h->num_proj && np > 1;
   int tw_max = 0;
   for (int pp = 0; pp < h->num_proj; ++pp) {
     const int i = all ? pp : (pp == p0 ? 0 : -1);
@@ -741,28 +783,51 @@ int run_expand(const PlanHeader* h, int p0, int np, void* const* ys, const int64
     tw_max = std::max(tw_max, p.tws[pp]);
   }
   p.plan = plan; p.ws = vimg_base ? const_cast<uint8_t*>(vimg_base) : ws;
-  p.wait_flag = wait_flag; p.wait_target = wait_target;
-  if (xsum != nullptr) {
-    p.xsum = xsum; p.xslot = 2 * h->vimg_stride * h->num_proj; p.ws_vimg0 = h->ws_vimg;
-    p.off_mtiles = h->off_mtiles; p.n_mtiles = h->n_mtiles; p.num_proj = h->num_proj;
-    p.vimg_stride = h->vimg_stride;
-    p.gbar = reinterpret_cast<int*>(ws);
-  }
   p.vsplit = h->vsplit;
   p.off_recs = all ? h->off_expand_recs_all : h->off_expand_recs_p[p0];
   p.off_cta = all ? h->off_expand_cta_all : h->off_expand_cta_p[p0];
+  p.off_mtiles = h->off_mtiles;
   p.tw_max = tw_max;
   p.dbg = g_debug_expand;
   p.trace = g_trace; p.trace_items = g_trace_items;
   p.num_tokens = num_tokens; p.ws_bytes = vimg_base ? INT64_MAX : h->ws_bytes;
   for (int pp = 0; pp < h->num_proj; ++pp) p.h_outs[pp] = h->h_outs[pp];
-  LSV_CUDA_CHECK(launch_pdl(expand_tc_kernel, all ? h->expand_grid_all : h->expand_grid_p[p0], expand_smem_bytes(),
-                            st, p, true, kExpandThreads));
-  LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// One input group's shrink + expand as one group kernel (tensor-core plans without SIMT items):
+// ready / split_done are the group's [n_mtiles] counters, zero at launch.
+bool group_kernel_eligible(const PlanHeader* h) {
+  return g_group_kernel && h->n_simt_items == 0 && !h->tile_aligned && h->n_shrink_items > 0 &&
+         (h->num_proj > 1 ? h->n_expand_all : h->n_expand_items_p[0]) > 0;
+}
+int run_group(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
+              void* const* ys, const int64_t* ldys, const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws,
+              int* gbar, int* ready, int wait_prev, bool pdl, cudaStream_t st) {
+  if (int rc = ensure_smem_attrs()) return rc;
+  GroupParams gp{};
+  if (int rc = fill_shrink_params(gp.s, h, x, ldx, num_tokens, a_ptrs, plan, ws, gbar)) return rc;
+  if (int rc = fill_expand_params(gp.e, h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, plan, ws, nullptr)) return rc;
+  gp.ready = ready;
+  gp.split_done = ready + h->n_mtiles;
+  gp.s_grid = h->shrink_grid;
+  gp.e_grid = h->num_proj > 1 ? h->expand_grid_all : h->expand_grid_p[0];
+  gp.wait_prev = wait_prev;
+  LSV_CUDA_CHECK(launch_pdl(group_tc_kernel, std::max(gp.s_grid, gp.e_grid), group_smem_bytes(), st, gp, pdl,
+                            kExpandThreads));
+  LSV_CUDA_CHECK(cudaGetLastError());
+  return LSV_OK;
+}
+// lsv_lora_forward's group-kernel counters: 2 * n_mtiles ints per (layer, group), after the slices
+size_t forward_counter_bytes(int L, int G, const PlanHeader* const* hs) {
+  size_t n = 0;
+  for (int g = 0; g < G; ++g) n += 2 * (size_t)hs[g]->n_mtiles;
+  return (n * 4 * (size_t)L + 255) / 256 * 256;
+}
+
+
 
 // lsv_lora_forward slice of one (layer, group): the plan's scratch without its barrier header
 size_t forward_slice_bytes(const PlanHeader* h) {
@@ -1105,7 +1170,7 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
   if (1 + (int64_t)num_layers * num_groups > kMaxBarPairs)
     return fail(LSV_EUNSUPPORTED, "%d layers x %d groups exceed the workspace barrier header", num_layers, num_groups);
   const size_t per_layer = ws_off[num_groups];
-  const size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers;
+  const size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers + forward_counter_bytes(num_layers, num_groups, hs);
   // A shrink may skip waiting for the previous launch only if nothing it reads is written by an
   // earlier expand of this call and no two expands write overlapping y: otherwise (e.g. y buffers
   // reused across layers) every launch waits for its predecessor.
@@ -1121,6 +1186,14 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
   // A slice holds its plan's scratch without the plan's own barrier header: the kernels get a base
   // kBarHeaderBytes before the slice (plan offsets start there) and their barrier pair explicitly.
   uint8_t* const wsb = static_cast<uint8_t*>(workspace);
+  // group-kernel counters (after the slices): zero-filled by this call, ordered after everything
+  // earlier in the stream (a memset is never overlapped by a programmatic launch)
+  int* const counters = reinterpret_cast<int*>(wsb + kBarHeaderBytes + per_layer * (size_t)num_layers);
+  bool any_group = false;
+  for (int g = 0; g < num_groups; ++g) any_group |= group_kernel_eligible(hs[g]) && hs[g]->num_tokens > 0;
+  if (any_group && num_layers > 0)
+    LSV_CUDA_CHECK(cudaMemsetAsync(counters, 0, forward_counter_bytes(num_layers, num_groups, hs), st));
+  size_t cnt_off = 0;
   for (int l = 0; l < num_layers; ++l) {
     int p0 = 0;
     uint8_t* wsl = wsb + per_layer * (size_t)l;   // + kBarHeaderBytes + ws_off[g] = slice (l, g)
@@ -1131,6 +1204,26 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       const int64_t ldx = ldxs[l * num_groups + g];
       const void* x = xs[l * num_groups + g];
       const bool first = l == 0 && g == 0;
+      int* const ready = counters + cnt_off;
+      cnt_off += 2 * (size_t)h->n_mtiles;
+      if (h->num_tokens > 0 && group_kernel_eligible(h)) {
+        if (!x || !aligned16(x) || ldx % 8 || ldx < h->h_in || num_tokens < h->num_tokens)
+          return fail(LSV_EINVAL, "layer %d group %d: bad x", l, g);
+        void* const* yg = ys + (size_t)l * nproj + p0;
+        const int64_t* ldg = ldys + (size_t)l * nproj + p0;
+        for (int i = 0; i < np; ++i)
+          if (!yg[i] || !aligned16(yg[i]) || ldg[i] % 8 || ldg[i] < h->h_outs[i])
+            return fail(LSV_EINVAL, "layer %d group %d member %d: bad y", l, g, i);
+        const void* const* btab[kMaxProj];
+        for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
+        // an overlap-free call's group kernels touch disjoint buffers: none waits for its predecessor
+        if (int rc = run_group(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S, yg, ldg, btab,
+                               static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], gbar, ready,
+                               (first || !overlap_free) ? 1 : 0, !first, st))
+          return rc;
+        p0 += np;
+        continue;
+      }
       if (h->num_tokens > 0) {
         if (!x || !aligned16(x) || ldx % 8 || ldx < h->h_in || num_tokens < h->num_tokens)
           return fail(LSV_EINVAL, "layer %d group %d: bad x", l, g);
@@ -1246,7 +1339,10 @@ size_t lsv_lora_forward_workspace(int32_t num_layers, int32_t num_groups, const 
     per_layer += forward_slice_bytes(h);
   }
   // at least as large as any single plan's workspace, so the standalone entry points can share it
-  size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers;
+  const PlanHeader* hs[64];
+  if (num_groups > 64) return 0;
+  for (int g = 0; g < num_groups; ++g) hs[g] = check_plan(plans_host[g]);
+  size_t need = kBarHeaderBytes + per_layer * (size_t)num_layers + forward_counter_bytes(num_layers, num_groups, hs);
   for (int g = 0; g < num_groups; ++g) need = std::max(need, (size_t)check_plan(plans_host[g])->ws_bytes);
   return need;
 }

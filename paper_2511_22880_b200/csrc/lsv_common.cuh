@@ -208,6 +208,27 @@ __device__ __forceinline__ void red_release_sys_add(int* p, int v) {
   asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Bounded wait on a device-scope counter written by other CTAs of the same grid (traps after ~4 s).
+__device__ __forceinline__ void wait_geq_gpu(const int* flag, int target) {
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0; ld_acquire_gpu(flag) < target; ++spin) {
+    __nanosleep(20);
+    if ((spin & 1023u) == 1023u) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+}
 // Bounded cross-GPU wait: traps after ~4 s instead of hanging the GPU on a missing signal.
 __device__ __forceinline__ void wait_flag_geq(const int* flag, int target) {
   uint64_t t0 = 0;

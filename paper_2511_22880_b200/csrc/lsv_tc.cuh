@@ -240,10 +240,6 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 #ifndef LSV_SHRINK_LAYOUT
 #define LSV_SHRINK_LAYOUT 1
 #endif
-// Shrink producer: 1 = converged warp, elected-lane copies; 0 = lanes issue the x boxes in parallel.
-#ifndef LSV_SHRINK_PROD_WARP
-#define LSV_SHRINK_PROD_WARP 1
-#endif
 #if LSV_SHRINK_LAYOUT
 constexpr int kShrProdWarp = 2, kShrMmaWarp = 3, kShrinkThreads = 256;
 __device__ __forceinline__ bool shrink_epi_warp(int w) { return w < 2 || w >= 6; }
@@ -360,42 +356,30 @@ __device__ __forceinline__ void red_store(const ShrinkParams& p, const RedUnit& 
   }
 }
 
-__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  ShrinkRecBuf* recbuf = reinterpret_cast<ShrinkRecBuf*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + kShrinkRecBufs);
-  uint64_t* empty = full + kShrinkSlots;
-  uint64_t* tfull = empty + kShrinkSlots;
-  uint64_t* tempty = tfull + kAccBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
-    fence_mbar_init();
-    for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
-  }
-  if (warp == kShrMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int cta = blockIdx.x;
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
-  if (p.wait_prev) pdl_wait();   // x, workspace and counters are written by earlier launches
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
-
-  if (warp == kShrProdWarp) {  // ---------------- producer: lane 0 owns the slot ring, lanes issue the copies
+// ---- shrink roles (shrink_tc_kernel and the group kernel) ---------------------------------
+struct ShrinkSm {
+  uint8_t* ring;
+  ShrinkRecBuf* recbuf;   // indexed by warp
+  uint64_t *full, *empty, *tfull, *tempty;
+};
+struct RingPos {
+  int slot;
+  uint32_t phase;
+};
+// Producer: streams every record's stages into the slot ring; returns the ring position after
+// the last stage (the group kernel drains the ring from there).
+__device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane) {
+  uint8_t* ring = sm.ring;
+  ShrinkRecBuf* recbuf = sm.recbuf;
+  uint64_t* full = sm.full;
+  uint64_t* empty = sm.empty;
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
     ShrinkRec inf;
     const uint8_t* a;
     int slot = 0; uint32_t phase = 0;
+    int pstage = 0;   // debug stage stamps (LSV_DEBUG_SHRINK bit 16)
     for (int k = 0; rs.pop(inf, a); ++k) {
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
       // rows [p0*r, (p0+np)*r) of the group A tile (G = num_proj*r rows per 64-column chunk)
       const int r = inf.rank, G = p.num_proj * r, rows = inf.np * r, np8 = round_up(inf.ntok, 8), kch = inf.kch;
       const uint8_t* asub = a + (size_t)inf.p0 * r * 128;
@@ -403,14 +387,15 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       LSV_DCHECK(r >= 8 && r <= 256 && r % 8 == 0 && rows <= 256 && inf.p0 + inf.np <= p.num_proj);
       LSV_DCHECK(inf.chunk_begin >= 0 && inf.chunk_begin < inf.chunk_end && inf.chunk_end * kChunk <= p.h_in);
       LSV_DCHECK(kch >= 1 && kch * (np8 + rows) * 128 <= kShrinkSlotBytes && a != nullptr);
-      const int m = np8 >> 3, pc = __popc(m);   // x boxes per chunk: one per set bit of np8/8
-#if LSV_SHRINK_PROD_WARP
+      const int m = np8 >> 3;   // x boxes per chunk: one per set bit of np8/8
       // converged: every lane computes the same operands, an elected lane issues each copy (no
       // per-lane uniformization loop around the TMA instructions)
       const uint32_t ring_base = smem_u32(ring);
       for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
         const int kc = min(kch, inf.chunk_end - g);
+        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage, 3);
         mbar_wait(&empty[slot], phase ^ 1);
+        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage, 4);
         const uint32_t fb = smem_u32(&full[slot]);
         mbar_arrive_expect_tx_elect(fb, (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : rows)) * 128));
         const uint32_t dst = ring_base + slot * kShrinkSlotBytes;
@@ -433,47 +418,24 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             }
           }
         }
+        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage++, 5);
         if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
-      (void)pc;
-#else
-      for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
-        const int kc = min(kch, inf.chunk_end - g);
-        if (lane == 0) {
-          mbar_wait(&empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&full[slot], (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : rows)) * 128));
-        }
-        __syncwarp();
-        uint8_t* dst = ring + slot * kShrinkSlotBytes;
-        if (lane == 0) {
-          if (!(p.dbg & 2)) {
-            if (rows == G) {       // whole group: the kc chunks are one contiguous run
-              bulk_load(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), &full[slot]);
-            } else {               // projection subset: one copy per chunk
-              for (int c = 0; c < kc; ++c)
-                bulk_load(dst + (kc * np8 + c * rows) * 128, asub + (size_t)(g + c) * G * 128, (uint32_t)(rows * 128),
-                          &full[slot]);
-            }
-          }
-        } else if (!(p.dbg & 4)) {
-          for (int bx = lane - 1; bx < kc * pc; bx += 31) {   // kc * pc may exceed the 31 lanes
-            const int c = bx / pc, i = bx % pc;
-            int mm = m, row = 0, bb = -1;
-            for (int s2 = 0; s2 <= i; ++s2) {       // i-th set bit from the top
-              bb = 31 - __clz(mm);
-              if (s2 < i) { row += 8 << bb; mm &= ~(1 << bb); }
-            }
-            tma_load_2d(dst + (c * np8 + row) * 128, &p.xmap[bb], &full[slot], (g + c) * kChunk,
-                        inf.tok_begin + row);
-          }
-        }
-        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
-      }
-#endif
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
       __syncwarp();
     }
-  } else if (warp == kShrMmaWarp) {  // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+  return RingPos{slot, phase};
+}
+// MMA issuer: the whole warp runs the loop (warp-uniform values stay in uniform registers, so each
+// MMA costs a few uniform adds), one lane issues.  Returns the number of records.
+__device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm& sm, uint32_t tmem_base, int cta, int warp,
+                                          int lane) {
+  uint8_t* ring = sm.ring;
+  ShrinkRecBuf* recbuf = sm.recbuf;
+  uint64_t* full = sm.full;
+  uint64_t* empty = sm.empty;
+  uint64_t* tfull = sm.tfull;
+  uint64_t* tempty = sm.tempty;
     // values stay in uniform registers, so each MMA costs a few uniform adds), one lane issues
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
@@ -482,7 +444,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     int dbg_stage = 0;
     const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
     const int nbuf = kTmemCols / p.acc_cols;
-    for (int k = 0; rs.pop(inf, unused); ++k) {
+    int k = 0;
+    for (; rs.pop(inf, unused); ++k) {
       const int rows = __shfl_sync(0xffffffffu, inf.rank * inf.np, 0);
       const int np8 = round_up(__shfl_sync(0xffffffffu, inf.ntok, 0), 8);
       const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
@@ -518,7 +481,15 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       umma_commit_elect(&tfull[buf]);
       if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
     }
-  } else if (shrink_epi_warp(warp)) {  // ---------------- epilogue: thread = token row of quadrant q
+  return k;
+}
+// Epilogue: thread = token row of quadrant q.  In the group kernel (ready != nullptr) every record
+// publishes its images (ready[mtile]) or its split partials (split_done[mtile]) when stored.
+__device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const ShrinkSm& sm, uint32_t tmem_base, int cta,
+                                                int warp, int lane, int* ready, int* split_done) {
+  ShrinkRecBuf* recbuf = sm.recbuf;
+  uint64_t* tfull = sm.tfull;
+  uint64_t* tempty = sm.tempty;
     const int q = warp & 3, row = q * 32 + lane;
     float* partials = reinterpret_cast<float*>(p.ws + p.ws_partials);
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
@@ -531,7 +502,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       const int buf = k % nbuf;
       mbar_wait(&tfull[buf], (k / nbuf) & 1);
       tc_fence_after();
-      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
+      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
       const bool valid = row < nt && !(p.dbg & 8);
       uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
@@ -592,10 +563,50 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
-      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
+      if (ready != nullptr) {   // group kernel: publish this record's v images (or split partials)
+        named_bar_sync(1, 128);   // the four epilogue warps' stores of this record are done
+        if (warp == 0 && lane == 0) {
+          fence_proxy_async_global();   // the expand reads the images with bulk copies (async proxy)
+          red_release_gpu_add(inf.nsplit > 1 ? &split_done[inf.mtile] : &ready[inf.mtile], 1);
+        }
+      }
+      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
   }
+
+__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  ShrinkRecBuf* recbuf = reinterpret_cast<ShrinkRecBuf*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + kShrinkRecBufs);
+  uint64_t* empty = full + kShrinkSlots;
+  uint64_t* tfull = empty + kShrinkSlots;
+  uint64_t* tempty = tfull + kAccBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    fence_mbar_init();
+    for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
+  }
+  if (warp == kShrMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cta = blockIdx.x;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
+  if (p.wait_prev) pdl_wait();   // x, workspace and counters are written by earlier launches
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
+  const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty};
+  if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane);
+  else if (warp == kShrMmaWarp) shrink_mma(p, sm, tmem_base, cta, warp, lane);
+  else if (shrink_epi_warp(warp)) shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr, nullptr);
   // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
   // recorded the table entry holding its first unit.  Each thread resolves its first two units
   // (static plan data, dependent loads) now, while other warps finish, so that after the grid
@@ -724,80 +735,27 @@ __device__ __forceinline__ bool y_box(int np16, int nb, int box, int& h, int& ro
   return true;
 }
 
-__global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                    // 8 KB
-  ExpandRecBuf* recbuf = reinterpret_cast<ExpandRecBuf*>(ident + kIdentRows * 16 * 2);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + kExpRecBufs);     // [kItemQ]
-  uint64_t* full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
-  uint64_t* empty = full + kItemQ;
-  uint64_t* tfull = empty + kItemQ;
-  uint64_t* tempty = tfull + kAccBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
-  const int nbuf = kTmemCols / p.tw_max;     // TMEM accumulators in flight
-  // No ring zeroing is needed: B tiles are stored padded to kp rows (zeros past the rank) and
-  // every other over-read (v rows past the tile's tokens) only feeds discarded D rows.
-  // identity A tile, K-major SWIZZLE_32B [256 rows][16 k]: 1.0 at (128 + k, k)
-  for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {
-    const int t = i / 16, k = i % 16;
-    reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
-  }
-  fence_proxy_async_smem();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
-    fence_mbar_init();
-    for (int pp = 0; pp < kMaxProj; ++pp)
-      if (p.y[pp])
-        for (int b = 0; b < 5; ++b) { prefetch_tmap(&p.ymap[pp][b]); prefetch_tmap(&p.ymap2[pp][b]); }
-  }
-  if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int cta = blockIdx.x;
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
-  pdl_wait();                 // v images come from the shrink launch; y from earlier work
-  if (p.wait_flag != nullptr) {   // TP: the peers' shards of the v images have landed here too
-    if (threadIdx.x == 0) {
-      wait_flag_geq(p.wait_flag, p.wait_target);
-      fence_proxy_async_global();
-      if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
-        p.wait_flag[1] = 0;
-        p.wait_flag[0] = 0;
-      }
-    }
-    __syncthreads();
-    if (p.xsum != nullptr) {      // row group: v = sum of every rank's fp32 partial, fixed rank order
-      tp_row_sum(p);
-      __threadfence();
-      __syncthreads();
-      int* bar = p.gbar;
-      if (threadIdx.x == 0) {
-        atomicAdd(&bar[0], 1);
-        uint64_t t0 = 0;
-        for (uint32_t spin = 0; ld_acquire_sys(&bar[0]) < (int)gridDim.x; ++spin) {
-          __nanosleep(32);
-          if ((spin & 1023u) == 1023u) {
-            const uint64_t now = globaltimer_ns();
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 4000000000ull) __trap();
-          }
-        }
-        fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
-      }
-      __syncthreads();
-    }
-  }
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
-
-  if (warp == kExpProdWarp) {  // ---------------- producer (whole warp, converged)
+// ---- expand roles (expand_tc_kernel and the group kernel) ---------------------------------
+constexpr int kVQ = 16;   // group kernel: v-ready queue between the ready checker and the producer
+struct ExpandSm {
+  uint8_t* ring;
+  uint8_t* ident;
+  ExpandRecBuf* recbuf;   // indexed by warp
+  uint32_t* offs;
+  uint64_t *full, *empty, *tfull, *tempty;
+};
+// Producer (whole warp, converged): every lane keeps the same ring bookkeeping and computes the
+// same copy operands; each copy is issued by one elected lane inside its asm (issuing the y
+// boxes from different lanes made ptxas serialise them through a per-lane uniformization loop,
+// ~1800 cycles per item).  B and y are issued first; in the group kernel (vfull != nullptr) the
+// v copy waits until the ready checker has seen the item's m-tile complete.
+__device__ __forceinline__ void expand_producer(const ExpandParams& p, const ExpandSm& sm, int cta, int warp, int lane,
+                                                uint64_t* vfull, uint64_t* vempty) {
+  uint8_t* ring = sm.ring;
+  ExpandRecBuf* recbuf = sm.recbuf;
+  uint32_t* offs = sm.offs;
+  uint64_t* full = sm.full;
+  uint64_t* empty = sm.empty;
     // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
     // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
     // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
@@ -850,7 +808,6 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
         }
       }
-      if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
       if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 3);
       if (!(dbg & 8)) {
         // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
@@ -864,10 +821,29 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
           mm &= ~(1 << bbit);
         }
       }
+      if (vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
+        mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
+        if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
+      }
+      if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
       if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 4);
       __syncwarp();
     }
-  } else if (warp == kExpMmaWarp) {  // ---------------- MMA issuer (whole warp)
+}
+// MMA issuer (whole warp): the election happens inside the MMA asm, so ptxas emits no per-MMA
+// uniformization loop; descriptors advance by constant steps (start address field = byte
+// address >> 4, below 2^14 in shared memory).
+__device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm& sm, uint32_t tmem_base, int cta, int warp,
+                                           int lane) {
+  uint8_t* ring = sm.ring;
+  uint8_t* ident = sm.ident;
+  ExpandRecBuf* recbuf = sm.recbuf;
+  uint32_t* offs = sm.offs;
+  uint64_t* full = sm.full;
+  uint64_t* empty = sm.empty;
+  uint64_t* tfull = sm.tfull;
+  uint64_t* tempty = sm.tempty;
+    const int nbuf = kTmemCols / p.tw_max;     // TMEM accumulators in flight
     // Every lane runs the loop and computes the same descriptors; the election happens inside the
     // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
     // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
@@ -936,7 +912,14 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
       __syncwarp();
     }
-  } else if (expand_epi_warp(warp)) {  // ---------------- epilogue: thread = token row of quadrant q
+}
+// Epilogue: thread = token row of quadrant q.
+__device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const ExpandSm& sm, uint32_t tmem_base, int cta,
+                                                int warp, int lane) {
+  ExpandRecBuf* recbuf = sm.recbuf;
+  uint64_t* tfull = sm.tfull;
+  uint64_t* tempty = sm.tempty;
+    const int nbuf = kTmemCols / p.tw_max;
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
@@ -1009,6 +992,83 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
     }
   }
+
+__global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                    // 8 KB
+  ExpandRecBuf* recbuf = reinterpret_cast<ExpandRecBuf*>(ident + kIdentRows * 16 * 2);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + kExpRecBufs);     // [kItemQ]
+  uint64_t* full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
+  uint64_t* empty = full + kItemQ;
+  uint64_t* tfull = empty + kItemQ;
+  uint64_t* tempty = tfull + kAccBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
+  // No ring zeroing is needed: B tiles are stored padded to kp rows (zeros past the rank) and
+  // every other over-read (v rows past the tile's tokens) only feeds discarded D rows.
+  // identity A tile, K-major SWIZZLE_32B [256 rows][16 k]: 1.0 at (128 + k, k)
+  for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {
+    const int t = i / 16, k = i % 16;
+    reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
+    fence_mbar_init();
+    for (int pp = 0; pp < kMaxProj; ++pp)
+      if (p.y[pp])
+        for (int b = 0; b < 5; ++b) { prefetch_tmap(&p.ymap[pp][b]); prefetch_tmap(&p.ymap2[pp][b]); }
+  }
+  if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cta = blockIdx.x;
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
+  pdl_wait();                 // v images come from the shrink launch; y from earlier work
+  if (p.wait_flag != nullptr) {   // TP: the peers' shards of the v images have landed here too
+    if (threadIdx.x == 0) {
+      wait_flag_geq(p.wait_flag, p.wait_target);
+      fence_proxy_async_global();
+      if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
+        p.wait_flag[1] = 0;
+        p.wait_flag[0] = 0;
+      }
+    }
+    __syncthreads();
+    if (p.xsum != nullptr) {      // row group: v = sum of every rank's fp32 partial, fixed rank order
+      tp_row_sum(p);
+      __threadfence();
+      __syncthreads();
+      int* bar = p.gbar;
+      if (threadIdx.x == 0) {
+        atomicAdd(&bar[0], 1);
+        uint64_t t0 = 0;
+        for (uint32_t spin = 0; ld_acquire_sys(&bar[0]) < (int)gridDim.x; ++spin) {
+          __nanosleep(32);
+          if ((spin & 1023u) == 1023u) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) __trap();
+          }
+        }
+        fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
+      }
+      __syncthreads();
+    }
+  }
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
+
+  const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty};
+  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr);
+  else if (warp == kExpMmaWarp) expand_mma(p, sm, tmem_base, cta, warp, lane);
+  else if (expand_epi_warp(warp)) expand_epilogue(p, sm, tmem_base, cta, warp, lane);
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
@@ -1017,6 +1077,178 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
     int* bar = p.gbar;
     if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }
   }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// Group kernel: one input group's shrink and expand in one persistent launch.  Each CTA runs its
+// shrink records, then its expand items; an item's v copy waits only for its own m-tile:
+//   ready[mt]      = records of the tile whose v images are written (split tiles: whose share of
+//                    the split-K reduction is written), target MTile::counter (= its records);
+//   split_done[mt] = split records of the tile whose fp32 partials are written.
+// Warp 4 reduces the CTA's split records (tokens split, split + nsplit, ... of the record's
+// members) once every split of the tile is in; warp 5 walks the CTA's expand list ahead of the
+// producer and releases each item's v copy when its tile is complete.  There is no grid barrier
+// and no second launch; CTAs that finish their shrink early expand the tiles already complete.
+struct alignas(64) GroupParams {
+  ShrinkParams s;
+  ExpandParams e;
+  int* ready;          // [n_mtiles], zero at launch (lsv_lora_forward zero-fills them per call)
+  int* split_done;     // [n_mtiles]
+  int s_grid, e_grid;  // CTAs with shrink records / expand items
+  int wait_prev;       // 1: griddepcontrol.wait first (the previous launch may touch our buffers)
+};
+union RecBufU {
+  ShrinkRecBuf s;
+  ExpandRecBuf e;
+};
+__host__ __device__ constexpr int group_smem_bytes() {
+  return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 8 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
+         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ) + 16 + 1024;
+}
+static_assert(kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes <=
+                  kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2,
+              "the shrink ring (and its MMA over-read guard) must lie below the group kernel's record buffers");
+
+// Warp 4: this CTA's share of the split-K reduction of its split records.
+__device__ __forceinline__ void group_reducer(const ShrinkParams& p, ShrinkRecBuf* rb, int cta, int lane, int* ready,
+                                              const int* split_done) {
+  WarpRecStream<ShrinkRec, kShrinkRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ShrinkRec inf;
+  const uint8_t* unused;
+  const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
+  while (rs.pop(inf, unused)) {
+    if (inf.nsplit == 1) continue;
+    if (lane == 0) wait_geq_gpu(&split_done[inf.mtile], inf.counter);   // every split record of the tile
+    __syncwarp();
+    RedUnit ru;
+    ru.mt = mts[inf.mtile];
+    ru.e = 0;
+    const int upr = kpad(inf.rank) / 8, per_tok = inf.np * upr;
+    const int ntk = (inf.ntok - inf.split + inf.nsplit - 1) / inf.nsplit;   // tokens split, split + nsplit, ...
+    for (int u = lane; u < ntk * per_tok; u += 32) {
+      ru.t = inf.split + (u / per_tok) * inf.nsplit;
+      ru.pp = inf.p0 + (u % per_tok) / upr;
+      ru.k0 = (u % upr) * 8;
+      float s8[8];
+      red_sum(p, ru, s8);
+      red_store(p, ru, s8);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_global();
+      red_release_gpu_add(&ready[inf.mtile], 1);
+    }
+  }
+}
+// Warp 5: walks the expand list ahead of the producer; releases item k's v copy (vfull) once its
+// m-tile is complete.  The acquire + proxy fence make the images (generic-proxy stores of other
+// CTAs) visible to the producer's bulk copy.
+__device__ __forceinline__ void group_ready_checker(const ExpandParams& p, ExpandRecBuf* rb, int cta, int lane,
+                                                    const int* ready, uint64_t* vfull, uint64_t* vempty) {
+  WarpRecStream<ExpandRec, kExpandRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ExpandRec inf;
+  const uint8_t* unused;
+  const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
+  int last = -1;
+  for (int k = 0; rs.pop(inf, unused); ++k) {
+    mbar_wait(&vempty[k % kVQ], ((k / kVQ) & 1) ^ 1);
+    if (inf.mtile != last) {
+      if (lane == 0) {
+        wait_geq_gpu(&ready[inf.mtile], mts[inf.mtile].counter);
+        fence_proxy_async_global();
+      }
+      last = inf.mtile;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&vfull[k % kVQ]);
+  }
+}
+
+__global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __grid_constant__ GroupParams gp) {
+  static_assert(kShrinkThreads == kExpandThreads && kShrProdWarp == kExpProdWarp && kShrMmaWarp == kExpMmaWarp,
+                "the group kernel runs both pipelines with one warp layout");
+  const ShrinkParams& sp = gp.s;
+  const ExpandParams& ep = gp.e;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // shrink slots / expand ring
+  uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                     // 8 KB
+  RecBufU* recbuf = reinterpret_cast<RecBufU*>(ident + kIdentRows * 16 * 2);       // one per warp, both phases
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 8);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
+  uint64_t* s_empty = s_full + kShrinkSlots;
+  uint64_t* s_tfull = s_empty + kShrinkSlots;
+  uint64_t* s_tempty = s_tfull + kAccBufs;
+  uint64_t* e_full = s_tempty + kAccBufs;
+  uint64_t* e_empty = e_full + kItemQ;
+  uint64_t* e_tfull = e_empty + kItemQ;
+  uint64_t* e_tempty = e_tfull + kAccBufs;
+  uint64_t* vfull = e_tempty + kAccBufs;
+  uint64_t* vempty = vfull + kVQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + kVQ);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {   // identity A tile (expand y add)
+    const int t = i / 16, k = i % 16;
+    reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&s_tfull[b], 1); mbar_init(&s_tempty[b], 4); }
+    for (int s = 0; s < kItemQ; ++s) { mbar_init(&e_full[s], 1); mbar_init(&e_empty[s], 1); }
+    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&e_tfull[b], 1); mbar_init(&e_tempty[b], kExpandEpiWarps); }
+    for (int q = 0; q < kVQ; ++q) { mbar_init(&vfull[q], 1); mbar_init(&vempty[q], 1); }
+    fence_mbar_init();
+    for (int b = 0; b < 5; ++b) prefetch_tmap(&sp.xmap[b]);
+    for (int pp = 0; pp < kMaxProj; ++pp)
+      if (ep.y[pp])
+        for (int b = 0; b < 5; ++b) { prefetch_tmap(&ep.ymap[pp][b]); prefetch_tmap(&ep.ymap2[pp][b]); }
+  }
+  if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (gp.wait_prev) pdl_wait();
+  pdl_launch_dependents();
+  const bool shr = cta < gp.s_grid, exp = cta < gp.e_grid;
+  const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty};
+  const ExpandSm esm{ring, ident, &recbuf[0].e, offs, e_full, e_empty, e_tfull, e_tempty};
+  // the role functions index recbuf by warp: give each a pointer whose [warp] is this warp's union slot
+  ShrinkSm ssw = ssm;
+  ssw.recbuf = reinterpret_cast<ShrinkRecBuf*>(&recbuf[warp]) - warp;
+  ExpandSm esw = esm;
+  esw.recbuf = reinterpret_cast<ExpandRecBuf*>(&recbuf[warp]) - warp;
+  if (warp == kExpProdWarp) {
+    if (shr) {
+      RingPos rp = shrink_producer(sp, ssw, cta, warp, lane);
+      for (int i = 0; i < kShrinkSlots; ++i) {   // every stage consumed: the ring is the expand's now
+        mbar_wait(&s_empty[rp.slot], rp.phase ^ 1);
+        if (++rp.slot == kShrinkSlots) { rp.slot = 0; rp.phase ^= 1; }
+      }
+    }
+    if (exp) expand_producer(ep, esw, cta, warp, lane, vfull, vempty);
+  } else if (warp == kExpMmaWarp) {
+    if (shr) {
+      const int n = shrink_mma(sp, ssw, tmem_base, cta, warp, lane);
+      const int nbs = kTmemCols / sp.acc_cols;
+      for (int k = n; k < n + nbs; ++k) mbar_wait(&s_tempty[k % nbs], ((k / nbs) & 1) ^ 1);   // accumulators drained
+      tc_fence_after();
+    }
+    if (exp) expand_mma(ep, esw, tmem_base, cta, warp, lane);
+  } else if (expand_epi_warp(warp)) {
+    if (shr) shrink_epilogue(sp, ssw, tmem_base, cta, warp, lane, gp.ready, gp.split_done);
+    if (exp) expand_epilogue(ep, esw, tmem_base, cta, warp, lane);
+  } else if (warp == 4) {
+    if (shr) group_reducer(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done);
+  } else if (warp == 5) {
+    if (exp) group_ready_checker(ep, &recbuf[warp].e, cta, lane, gp.ready, vfull, vempty);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
 }
 
 }  // namespace lsv
