@@ -88,9 +88,9 @@ bool decode_shaped(int32_t S, const int32_t* indptr) {
 }
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
 #ifndef LSV_SHRINK_WAVES
-#define LSV_SHRINK_WAVES 8
+#define LSV_SHRINK_WAVES 4
 #endif
-constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost)
+constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost; 4 measured best with the group kernel: 9.58 vs 9.70 ms at 8, 9.79 at 2)
 // LPT cost of an item = its bytes + a fixed per-item cost (pipeline fill, barrier round trips,
 // epilogue), in byte-equivalents
 #ifndef LSV_EXPAND_ITEM_FIXED_KB
@@ -815,6 +815,8 @@ int run_group(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_token
   gp.s_grid = h->shrink_grid;
   gp.e_grid = h->num_proj > 1 ? h->expand_grid_all : h->expand_grid_p[0];
   gp.wait_prev = wait_prev;
+  if (gp.e.trace != nullptr)   // development trace: the expand's stamps in a second buffer half
+    gp.e.trace += (size_t)num_sms_cached() * gp.e.trace_items * 16;
   LSV_CUDA_CHECK(launch_pdl(group_tc_kernel, std::max(gp.s_grid, gp.e_grid), group_smem_bytes(), st, gp, pdl,
                             kExpandThreads));
   LSV_CUDA_CHECK(cudaGetLastError());

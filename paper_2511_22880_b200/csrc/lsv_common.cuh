@@ -216,10 +216,18 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // Bounded wait on a device-scope counter written by other CTAs of the same grid (traps after ~4 s).
+// Spins with relaxed loads and acquires once at the end: an ld.acquire.gpu compiles to a load plus
+// an invalidation of the SM's whole L1 (CCTL.IVALL); a fence.acq_rel.gpu to a full MEMBAR.GPU.
 __device__ __forceinline__ void wait_geq_gpu(const int* flag, int target) {
   uint64_t t0 = 0;
-  for (uint32_t spin = 0; ld_acquire_gpu(flag) < target; ++spin) {
+  for (uint32_t spin = 0; ld_relaxed_gpu(flag) < target; ++spin) {
     __nanosleep(20);
     if ((spin & 1023u) == 1023u) {
       uint64_t now;
@@ -228,11 +236,17 @@ __device__ __forceinline__ void wait_geq_gpu(const int* flag, int target) {
       else if (now - t0 > 4000000000ull) __trap();
     }
   }
+  (void)ld_acquire_gpu(flag);   // one acquire (load + L1 invalidate) once the count is reached
 }
 // Bounded cross-GPU wait: traps after ~4 s instead of hanging the GPU on a missing signal.
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void wait_flag_geq(const int* flag, int target) {
   uint64_t t0 = 0;
-  for (uint32_t spin = 0; ld_acquire_sys(flag) < target; ++spin) {
+  for (uint32_t spin = 0; ld_relaxed_sys(flag) < target; ++spin) {   // relaxed spin, one acquire fence
     __nanosleep(32);
     if ((spin & 1023u) == 1023u) {
       uint64_t now;
@@ -241,6 +255,7 @@ __device__ __forceinline__ void wait_flag_geq(const int* flag, int target) {
       else if (now - t0 > 4000000000ull) __trap();
     }
   }
+  (void)ld_acquire_sys(flag);
 }
 
 // ---- async copies (TMA / bulk) -------------------------------------------------------------

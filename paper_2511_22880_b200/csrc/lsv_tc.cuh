@@ -483,10 +483,12 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
     }
   return k;
 }
-// Epilogue: thread = token row of quadrant q.  In the group kernel (ready != nullptr) every record
-// publishes its images (ready[mtile]) or its split partials (split_done[mtile]) when stored.
+// Epilogue: thread = token row of quadrant q.  In the group kernel (recdone != nullptr) each warp
+// arrives on recdone[k % kRecQ] once its rows of record k are stored; the signal warp publishes
+// (and counts the records it has published in the int after the barriers: back-pressure).
+constexpr int kRecQ = 16;   // recdone barriers, then the signal warp's progress counter
 __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const ShrinkSm& sm, uint32_t tmem_base, int cta,
-                                                int warp, int lane, int* ready, int* split_done) {
+                                                int warp, int lane, uint64_t* recdone) {
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
@@ -563,12 +565,10 @@ __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const Shr
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (ready != nullptr) {   // group kernel: publish this record's v images (or split partials)
-        named_bar_sync(1, 128);   // the four epilogue warps' stores of this record are done
-        if (warp == 0 && lane == 0) {
-          fence_proxy_async_global();   // the expand reads the images with bulk copies (async proxy)
-          red_release_gpu_add(inf.nsplit > 1 ? &split_done[inf.mtile] : &ready[inf.mtile], 1);
-        }
+      if (recdone != nullptr && lane == 0) {   // group kernel: stored (the signal warp is < kRecQ behind)
+        const volatile int* sigc = reinterpret_cast<const volatile int*>(recdone + kRecQ);
+        while (k >= kRecQ && *sigc <= k - kRecQ) __nanosleep(32);
+        mbar_arrive(&recdone[k % kRecQ]);
       }
       if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
       if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty};
   if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane);
   else if (warp == kShrMmaWarp) shrink_mma(p, sm, tmem_base, cta, warp, lane);
-  else if (shrink_epi_warp(warp)) shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr, nullptr);
+  else if (shrink_epi_warp(warp)) shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr);
   // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
   // recorded the table entry holding its first unit.  Each thread resolves its first two units
   // (static plan data, dependent loads) now, while other warps finish, so that after the grid
@@ -639,8 +639,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     int seen = 0;
     uint64_t t0 = 0;
     for (uint32_t spin = 0;; ++spin) {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(&bar[0]) : "memory");
-      if (seen >= (int)gridDim.x) break;
+      seen = ld_relaxed_gpu(&bar[0]);
+      if (seen >= (int)gridDim.x) { (void)ld_acquire_gpu(&bar[0]); break; }
       __nanosleep(64);
       if ((spin & 1023u) == 1023u) {   // bounded: trap after ~4 s instead of hanging the GPU
         const uint64_t now = globaltimer_ns();
@@ -822,7 +822,9 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
         }
       }
       if (vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
+        if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 5);
         mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
+        if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 6);
         if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
       }
       if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
@@ -1049,7 +1051,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
       if (threadIdx.x == 0) {
         atomicAdd(&bar[0], 1);
         uint64_t t0 = 0;
-        for (uint32_t spin = 0; ld_acquire_sys(&bar[0]) < (int)gridDim.x; ++spin) {
+        for (uint32_t spin = 0; ld_relaxed_sys(&bar[0]) < (int)gridDim.x; ++spin) {
           __nanosleep(32);
           if ((spin & 1023u) == 1023u) {
             const uint64_t now = globaltimer_ns();
@@ -1057,6 +1059,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
             else if (now - t0 > 4000000000ull) __trap();
           }
         }
+        (void)ld_acquire_sys(&bar[0]);
         fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
       }
       __syncthreads();
@@ -1086,9 +1089,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
 //   ready[mt]      = records of the tile whose v images are written (split tiles: whose share of
 //                    the split-K reduction is written), target MTile::counter (= its records);
 //   split_done[mt] = split records of the tile whose fp32 partials are written.
-// Warp 4 reduces the CTA's split records (tokens split, split + nsplit, ... of the record's
-// members) once every split of the tile is in; warp 5 walks the CTA's expand list ahead of the
-// producer and releases each item's v copy when its tile is complete.  There is no grid barrier
+// Warp 4 publishes each stored record, then walks the CTA's expand list ahead of the producer and
+// releases each item's v copy when its tile is complete; warp 5 reduces the CTA's split records
+// (tokens split, split + nsplit, ... of the record's members) once every split of the tile is in.  There is no grid barrier
 // and no second launch; CTAs that finish their shrink early expand the tiles already complete.
 struct alignas(64) GroupParams {
   ShrinkParams s;
@@ -1104,13 +1107,13 @@ union RecBufU {
 };
 __host__ __device__ constexpr int group_smem_bytes() {
   return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 8 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
-         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ) + 16 + 1024;
+         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 + 1024;
 }
 static_assert(kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes <=
                   kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2,
               "the shrink ring (and its MMA over-read guard) must lie below the group kernel's record buffers");
 
-// Warp 4: this CTA's share of the split-K reduction of its split records.
+// Warp 5: this CTA's share of the split-K reduction of its split records.
 __device__ __forceinline__ void group_reducer(const ShrinkParams& p, ShrinkRecBuf* rb, int cta, int lane, int* ready,
                                               const int* split_done) {
   WarpRecStream<ShrinkRec, kShrinkRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
@@ -1141,7 +1144,26 @@ __device__ __forceinline__ void group_reducer(const ShrinkParams& p, ShrinkRecBu
     }
   }
 }
-// Warp 5: walks the expand list ahead of the producer; releases item k's v copy (vfull) once its
+// Warp 4, shrink phase: publishes each of the CTA's records once its four epilogue warps have
+// stored it (recdone): ready[mt] for a whole tile's images, split_done[mt] for split partials.
+// It never waits on other CTAs, so every record's signal goes out whatever the reducers wait on.
+// The release is cumulative over the epilogue warps' stores it acquired through the mbarrier.
+__device__ __forceinline__ void group_signaler(const ShrinkParams& p, ShrinkRecBuf* rb, int cta, int lane, int* ready,
+                                               int* split_done, uint64_t* recdone) {
+  WarpRecStream<ShrinkRec, kShrinkRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ShrinkRec inf;
+  const uint8_t* unused;
+  for (int k = 0; rs.pop(inf, unused); ++k) {
+    mbar_wait(&recdone[k % kRecQ], (k / kRecQ) & 1);
+    if (lane == 0) {
+      fence_proxy_async_global();   // the expand reads the images with bulk copies (async proxy)
+      red_release_gpu_add(inf.nsplit > 1 ? &split_done[inf.mtile] : &ready[inf.mtile], 1);
+      *reinterpret_cast<volatile int*>(recdone + kRecQ) = k + 1;
+    }
+    __syncwarp();
+  }
+}
+// Warp 4, expand phase: walks the expand list ahead of the producer; releases item k's v copy (vfull) once its
 // m-tile is complete.  The acquire + proxy fence make the images (generic-proxy stores of other
 // CTAs) visible to the producer's bulk copy.
 __device__ __forceinline__ void group_ready_checker(const ExpandParams& p, ExpandRecBuf* rb, int cta, int lane,
@@ -1185,7 +1207,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
   uint64_t* e_tempty = e_tfull + kAccBufs;
   uint64_t* vfull = e_tempty + kAccBufs;
   uint64_t* vempty = vfull + kVQ;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + kVQ);
+  uint64_t* recdone = vempty + kVQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recdone + kRecQ) + 1;   // [0]: published-record count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -1200,6 +1223,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
     for (int s = 0; s < kItemQ; ++s) { mbar_init(&e_full[s], 1); mbar_init(&e_empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&e_tfull[b], 1); mbar_init(&e_tempty[b], kExpandEpiWarps); }
     for (int q = 0; q < kVQ; ++q) { mbar_init(&vfull[q], 1); mbar_init(&vempty[q], 1); }
+    for (int q = 0; q < kRecQ; ++q) mbar_init(&recdone[q], 4);
+    *reinterpret_cast<volatile int*>(recdone + kRecQ) = 0;
     fence_mbar_init();
     for (int b = 0; b < 5; ++b) prefetch_tmap(&sp.xmap[b]);
     for (int pp = 0; pp < kMaxProj; ++pp)
@@ -1211,6 +1236,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) phase_stamp(sp.trace, sp.trace_items, cta, 0);
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
   const bool shr = cta < gp.s_grid, exp = cta < gp.e_grid;
@@ -1229,6 +1255,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
         if (++rp.slot == kShrinkSlots) { rp.slot = 0; rp.phase ^= 1; }
       }
     }
+    if (lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 2);   // shrink stages consumed
     if (exp) expand_producer(ep, esw, cta, warp, lane, vfull, vempty);
   } else if (warp == kExpMmaWarp) {
     if (shr) {
@@ -1239,12 +1266,16 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
     }
     if (exp) expand_mma(ep, esw, tmem_base, cta, warp, lane);
   } else if (expand_epi_warp(warp)) {
-    if (shr) shrink_epilogue(sp, ssw, tmem_base, cta, warp, lane, gp.ready, gp.split_done);
+    if (shr) shrink_epilogue(sp, ssw, tmem_base, cta, warp, lane, recdone);
+    if (warp == 0 && lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 1);   // shrink records stored
     if (exp) expand_epilogue(ep, esw, tmem_base, cta, warp, lane);
+    if (warp == 0 && lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 4);   // expand items stored
   } else if (warp == 4) {
-    if (shr) group_reducer(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done);
-  } else if (warp == 5) {
+    if (shr) group_signaler(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done, recdone);
     if (exp) group_ready_checker(ep, &recbuf[warp].e, cta, lane, gp.ready, vfull, vempty);
+  } else if (warp == 5) {
+    if (shr) group_reducer(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done);
+    if (lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 3);   // split-K shares reduced
   }
   tc_fence_before();
   __syncthreads();
