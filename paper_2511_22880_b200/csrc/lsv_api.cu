@@ -40,6 +40,9 @@ const bool g_simt_wait = [] { const char* e = std::getenv("LSV_SIMT_WAIT"); retu
 // LSV_GROUP_KERNEL=0: lsv_lora_forward runs each group as a shrink launch + an expand launch
 // instead of one group kernel (A/B timing)
 const bool g_group_kernel = [] { const char* e = std::getenv("LSV_GROUP_KERNEL"); return !e || std::atoi(e) != 0; }();
+// LSV_READY_ORDER=0: keep each CTA's expand items in LPT order instead of estimated m-tile
+// readiness order (A/B timing)
+const bool g_ready_order = [] { const char* e = std::getenv("LSV_READY_ORDER"); return !e || std::atoi(e) != 0; }();
 const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
 int fail(int code, const char* fmt, ...) {
@@ -170,22 +173,30 @@ struct LoadTree {
 
 // LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
 // CTA's list keeps that order.  Returns records regrouped per CTA and the [grid+1] offsets.
+// finish (optional): each record's estimated completion, its CTA's load once it is done.
 template <typename Rec>
 void lpt_assign(const std::vector<std::pair<int64_t, Rec>>& costed, int grid, std::vector<Rec>& out,
-                std::vector<int32_t>& cta_off, const std::vector<uint8_t>* remote = nullptr) {
+                std::vector<int32_t>& cta_off, const std::vector<uint8_t>* remote = nullptr,
+                std::vector<int64_t>* finish = nullptr) {
   std::vector<int32_t> owner(costed.size());
+  std::vector<int64_t> done(costed.size());
   LoadTree tree(grid);
   for (size_t i = 0; i < costed.size(); ++i) {
     const int c = tree.top();
     owner[i] = c;
     tree.add(c, costed[i].first);
+    done[i] = tree.load[c];
   }
   cta_off.assign(grid + 1, 0);
   for (int32_t o : owner) ++cta_off[o + 1];
   for (int c = 0; c < grid; ++c) cta_off[c + 1] += cta_off[c];
   out.resize(costed.size());
+  if (finish) finish->resize(costed.size());
   std::vector<int32_t> fill(cta_off.begin(), cta_off.end() - 1);
-  for (size_t i = 0; i < costed.size(); ++i) out[fill[owner[i]]++] = costed[i].second;   // keeps LPT order per CTA
+  for (size_t i = 0; i < costed.size(); ++i) {   // keeps LPT order per CTA
+    if (finish) (*finish)[fill[owner[i]]] = done[i];
+    out[fill[owner[i]]++] = costed[i].second;
+  }
   if (remote == nullptr) return;
   // per CTA: remote and local records alternate (each kind in LPT order), remote first
   std::vector<Rec> rem, loc;
@@ -358,7 +369,21 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   std::stable_sort(shrink_costed.begin(), shrink_costed.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
   const int shrink_grid = (int)std::min<size_t>(shrink_costed.size(), (size_t)nsm);
-  lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta, rem);
+  std::vector<int64_t> shrink_finish;
+  lpt_assign(shrink_costed, std::max(shrink_grid, 1), pb.shrink, pb.shrink_cta, rem, &shrink_finish);
+  // estimated time each m-tile's v images are complete (its last shrink record; split tiles also
+  // wait for their reduction): the group kernel's CTAs take their expand items in this order
+  std::vector<int64_t> tile_ready(pb.mtiles.size(), 0);
+  for (size_t i = 0; i < pb.shrink.size(); ++i) {
+    const ShrinkRec& rc = pb.shrink[i];
+    tile_ready[rc.mtile] = std::max(tile_ready[rc.mtile], shrink_finish[i] + (rc.nsplit > 1 ? kShrinkRecFixed : 0));
+  }
+  auto ready_order = [&](std::vector<ExpandRec>& recs, const std::vector<int32_t>& off) {
+    for (size_t c = 0; c + 1 < off.size(); ++c)
+      std::stable_sort(recs.begin() + off[c], recs.begin() + off[c + 1], [&](const ExpandRec& a, const ExpandRec& b) {
+        return tile_ready[a.mtile] < tile_ready[b.mtile];
+      });
+  };
 
   // expand: per projection, items = (m-tile, tw-wide h_out tile); plus all members in one list.
   // An item's cost depends only on (m-tile, member), so the (m-tile, member) classes are sorted
@@ -398,12 +423,14 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
     emit(cls, expand_costed);
     expand_grid[p] = (int)std::min<size_t>(expand_costed.size(), (size_t)nsm);
     lpt_assign(expand_costed, std::max(expand_grid[p], 1), pb.expand[p], pb.expand_cta[p], rem);
+    if (g_ready_order && !rem) ready_order(pb.expand[p], pb.expand_cta[p]);
   }
   std::stable_sort(all_cls.begin(), all_cls.end(), by_cost);
   std::vector<std::pair<int64_t, ExpandRec>> all_costed;
   emit(all_cls, all_costed);
   const int expand_grid_all = (int)std::min<size_t>(all_costed.size(), (size_t)nsm);
   lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta, rem);
+  if (g_ready_order && !rem) ready_order(pb.expand_all, pb.expand_all_cta);
 
   // header + workspace layout
   PlanHeader& h = pb.h;
