@@ -845,7 +845,7 @@ int run_group(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_token
   if (gp.e.trace != nullptr)   // development trace: the expand's stamps in a second buffer half
     gp.e.trace += (size_t)num_sms_cached() * gp.e.trace_items * 16;
   LSV_CUDA_CHECK(launch_pdl(group_tc_kernel, std::max(gp.s_grid, gp.e_grid), group_smem_bytes(), st, gp, pdl,
-                            kExpandThreads));
+                            kGroupThreads));
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }

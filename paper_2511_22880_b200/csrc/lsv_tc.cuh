@@ -235,6 +235,14 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
   }
 }
 
+// Copy-issuing warps per pipeline: a warp spends ~130 cycles issuing each bulk / TMA copy
+// (tools/tma_issue.cu), two warps issue twice as many.  The second part runs on warp 4 in the
+// standalone kernels (idle otherwise) and on warp 8 in the group kernel.
+#ifndef LSV_PROD_PARTS
+#define LSV_PROD_PARTS 2
+#endif
+constexpr int kProdParts = LSV_PROD_PARTS;
+constexpr int kProdWarp2 = 4;
 // Shrink warp roles: as the expand's (below), layout 1 keeps the producer and the MMA issuer off
 // the sub-partitions of the busy epilogue quadrants 0 and 1.
 #ifndef LSV_SHRINK_LAYOUT
@@ -242,7 +250,7 @@ __device__ __forceinline__ void tp_signal(const ShrinkParams& p) {
 #endif
 #if LSV_SHRINK_LAYOUT
 constexpr int kShrProdWarp = 2, kShrMmaWarp = 3, kShrinkThreads = 256;
-__device__ __forceinline__ bool shrink_epi_warp(int w) { return w < 2 || w >= 6; }
+__device__ __forceinline__ bool shrink_epi_warp(int w) { return w < 2 || w == 6 || w == 7; }
 #else
 constexpr int kShrProdWarp = 0, kShrMmaWarp = 1, kShrinkThreads = 192;
 __device__ __forceinline__ bool shrink_epi_warp(int w) { return w >= 2; }
@@ -290,7 +298,7 @@ constexpr int kExpandEpiWarps = LSV_EXPAND_EPI_WARPS;   // 4: one per TMEM lane 
 #if LSV_EXPAND_LAYOUT
 static_assert(LSV_EXPAND_EPI_WARPS == 4, "layout 1 has one epilogue warp per quadrant");
 constexpr int kExpProdWarp = 2, kExpMmaWarp = 3, kExpandThreads = 256;
-__device__ __forceinline__ bool expand_epi_warp(int w) { return w < 2 || w >= 6; }
+__device__ __forceinline__ bool expand_epi_warp(int w) { return w < 2 || w == 6 || w == 7; }
 #else
 constexpr int kExpProdWarp = 0, kExpMmaWarp = 1, kExpandThreads = 64 + 32 * kExpandEpiWarps;
 __device__ __forceinline__ bool expand_epi_warp(int w) { return w >= 2; }
@@ -368,62 +376,68 @@ struct RingPos {
 };
 // Producer: streams every record's stages into the slot ring; returns the ring position after
 // the last stage (the group kernel drains the ring from there).
-__device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane) {
+__device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane,
+                                                   int part = 0, int nparts = 1) {
+  // nparts warps run this loop with the same slot bookkeeping; a stage's copies (A first, then the
+  // x boxes) go round-robin to the parts, each arriving on full[slot] with its own bytes: one
+  // warp spends ~130 cycles issuing each copy, so copies from two warps double the issue rate.
   uint8_t* ring = sm.ring;
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* full = sm.full;
   uint64_t* empty = sm.empty;
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
-    ShrinkRec inf;
-    const uint8_t* a;
-    int slot = 0; uint32_t phase = 0;
-    int pstage = 0;   // debug stage stamps (LSV_DEBUG_SHRINK bit 16)
-    for (int k = 0; rs.pop(inf, a); ++k) {
-      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
-      // rows [p0*r, (p0+np)*r) of the group A tile (G = num_proj*r rows per 64-column chunk)
-      const int r = inf.rank, G = p.num_proj * r, rows = inf.np * r, np8 = round_up(inf.ntok, 8), kch = inf.kch;
-      const uint8_t* asub = a + (size_t)inf.p0 * r * 128;
-      LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin >= 0 && inf.tok_begin + inf.ntok <= p.num_tokens);
-      LSV_DCHECK(r >= 8 && r <= 256 && r % 8 == 0 && rows <= 256 && inf.p0 + inf.np <= p.num_proj);
-      LSV_DCHECK(inf.chunk_begin >= 0 && inf.chunk_begin < inf.chunk_end && inf.chunk_end * kChunk <= p.h_in);
-      LSV_DCHECK(kch >= 1 && kch * (np8 + rows) * 128 <= kShrinkSlotBytes && a != nullptr);
-      const int m = np8 >> 3;   // x boxes per chunk: one per set bit of np8/8
-      // converged: every lane computes the same operands, an elected lane issues each copy (no
-      // per-lane uniformization loop around the TMA instructions)
-      const uint32_t ring_base = smem_u32(ring);
-      for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
-        const int kc = min(kch, inf.chunk_end - g);
-        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage, 3);
-        mbar_wait(&empty[slot], phase ^ 1);
-        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage, 4);
-        const uint32_t fb = smem_u32(&full[slot]);
-        mbar_arrive_expect_tx_elect(fb, (uint32_t)(kc * (((p.dbg & 4) ? 0 : np8) + ((p.dbg & 2) ? 0 : rows)) * 128));
-        const uint32_t dst = ring_base + slot * kShrinkSlotBytes;
-        if (!(p.dbg & 2)) {
-          if (rows == G) {       // whole group: the kc chunks are one contiguous run
-            bulk_load_elect(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), fb);
-          } else {               // projection subset: one copy per chunk
-            for (int c = 0; c < kc; ++c)
-              bulk_load_elect(dst + (kc * np8 + c * rows) * 128, asub + (size_t)(g + c) * G * 128, (uint32_t)(rows * 128), fb);
-          }
+  WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
+  ShrinkRec inf;
+  const uint8_t* a;
+  int slot = 0; uint32_t phase = 0;
+  int pstage = 0;   // debug stage stamps (LSV_DEBUG_SHRINK bit 16)
+  const bool stamp = part == 0 && lane == 0;
+  const uint32_t ring_base = smem_u32(ring);
+  for (int k = 0; rs.pop(inf, a); ++k) {
+    if (!(p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+    // rows [p0*r, (p0+np)*r) of the group A tile (G = num_proj*r rows per 64-column chunk)
+    const int r = inf.rank, G = p.num_proj * r, rows = inf.np * r, np8 = round_up(inf.ntok, 8), kch = inf.kch;
+    const uint8_t* asub = a + (size_t)inf.p0 * r * 128;
+    LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin >= 0 && inf.tok_begin + inf.ntok <= p.num_tokens);
+    LSV_DCHECK(r >= 8 && r <= 256 && r % 8 == 0 && rows <= 256 && inf.p0 + inf.np <= p.num_proj);
+    LSV_DCHECK(inf.chunk_begin >= 0 && inf.chunk_begin < inf.chunk_end && inf.chunk_end * kChunk <= p.h_in);
+    LSV_DCHECK(kch >= 1 && kch * (np8 + rows) * 128 <= kShrinkSlotBytes && a != nullptr);
+    const int m = np8 >> 3;   // x boxes per chunk: one per set bit of np8/8
+    for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
+      const int kc = min(kch, inf.chunk_end - g);
+      if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage, 3);
+      mbar_wait(&empty[slot], phase ^ 1);
+      if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage, 4);
+      const uint32_t fb = smem_u32(&full[slot]);
+      // part 0 copies A; chunk c's x boxes belong to part (c + 1) % nparts
+      const bool do_a = part == 0 && !(p.dbg & 2), do_x = !(p.dbg & 4);
+      const int my_chunks = do_x ? (kc + nparts - 1 - (part + nparts - 1) % nparts) / nparts : 0;
+      mbar_arrive_expect_tx_elect(fb, (uint32_t)((do_a ? kc * rows : 0) + my_chunks * np8) * 128);
+      const uint32_t dst = ring_base + slot * kShrinkSlotBytes;
+      if (do_a) {
+        if (rows == G) {       // whole group: the kc chunks are one contiguous run
+          bulk_load_elect(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), fb);
+        } else {               // projection subset: one copy per chunk
+          for (int c = 0; c < kc; ++c)
+            bulk_load_elect(dst + (kc * np8 + c * rows) * 128, asub + (size_t)(g + c) * G * 128, (uint32_t)(rows * 128), fb);
         }
-        if (!(p.dbg & 4)) {
-          for (int c = 0; c < kc; ++c) {
-            int mm = m, row = 0;
-            while (mm) {
-              const int bb = 31 - __clz(mm);
-              tma_load_2d_elect(dst + (c * np8 + row) * 128, &p.xmap[bb], fb, (g + c) * kChunk, inf.tok_begin + row);
-              row += 8 << bb;
-              mm &= ~(1 << bb);
-            }
-          }
-        }
-        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, pstage++, 5);
-        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
-      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
-      __syncwarp();
+      if (do_x) {
+        for (int c = (part + nparts - 1) % nparts; c < kc; c += nparts) {
+          int mm = m, row = 0;
+          while (mm) {
+            const int bb = 31 - __clz(mm);
+            tma_load_2d_elect(dst + (c * np8 + row) * 128, &p.xmap[bb], fb, (g + c) * kChunk, inf.tok_begin + row);
+            row += 8 << bb;
+            mm &= ~(1 << bb);
+          }
+        }
+      }
+      if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage++, 5);
+      if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
     }
+    if (!(p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+    __syncwarp();
+  }
   return RingPos{slot, phase};
 }
 // MMA issuer: the whole warp runs the loop (warp-uniform values stay in uniform registers, so each
@@ -588,7 +602,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_mbar_init();
     for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
@@ -604,7 +618,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
   const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty};
-  if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane);
+  if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane, 0, kProdParts);
+  else if (warp == kProdWarp2 && kProdParts == 2) shrink_producer(p, sm, cta, warp, lane, 1, kProdParts);
   else if (warp == kShrMmaWarp) shrink_mma(p, sm, tmem_base, cta, warp, lane);
   else if (shrink_epi_warp(warp)) shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr);
   // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
@@ -750,7 +765,9 @@ struct ExpandSm {
 // ~1800 cycles per item).  B and y are issued first; in the group kernel (vfull != nullptr) the
 // v copy waits until the ready checker has seen the item's m-tile complete.
 __device__ __forceinline__ void expand_producer(const ExpandParams& p, const ExpandSm& sm, int cta, int warp, int lane,
-                                                uint64_t* vfull, uint64_t* vempty) {
+                                                uint64_t* vfull, uint64_t* vempty, int part = 0, int nparts = 1) {
+  // nparts (1 or 2) warps run this loop with the same ring bookkeeping: part 0 copies B and v
+  // (and y when alone), part 1 the y boxes; each arrives on full[] with its own bytes.
   uint8_t* ring = sm.ring;
   ExpandRecBuf* recbuf = sm.recbuf;
   uint32_t* offs = sm.offs;
@@ -783,7 +800,8 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
       LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
       LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
       LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+      const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
+      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k, 0);
       while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
         mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
         ++retired;
@@ -791,14 +809,15 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
       }
       vbegin[qs] = head;
       const uint32_t ring_off = head % kExpandRingBytes;
-      if (lane == 0) offs[qs] = ring_off;
+      if (stamp) offs[qs] = ring_off;
       head += size;
       const int dbg = p.dbg;
       const uint32_t fb = smem_u32(&full[qs]);
-      mbar_arrive_expect_tx_elect(fb, ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) + ((dbg & 8) ? 0 : ybytes));
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+      mbar_arrive_expect_tx_elect(fb, (p0 ? ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) : 0u) +
+                                          (do_y ? ((dbg & 8) ? 0 : ybytes) : 0u));
+      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k, 1);
       const uint32_t dst = ring_base + ring_off;
-      if (!(dbg & 16)) {
+      if (p0 && !(dbg & 16)) {
         if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group
           const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
           const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
@@ -808,8 +827,8 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
           bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
         }
       }
-      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 3);
-      if (!(dbg & 8)) {
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 3);
+      if (do_y && !(dbg & 8)) {
         // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
         // [nb blocks][R rows][64] at yoff + row * nb * 128
         const CUtensorMap* ym = nb == 4 ? p.ymap[inf.proj] : p.ymap2[inf.proj];
@@ -821,14 +840,14 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
           mm &= ~(1 << bbit);
         }
       }
-      if (vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
-        if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 5);
+      if (p0 && vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
+        if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 5);
         mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
-        if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 6);
+        if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 6);
         if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
       }
-      if (!(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
-      if (lane == 0) trace_aux(p.trace, p.trace_items, cta, k, 4);
+      if (p0 && !(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 4);
       __syncwarp();
     }
 }
@@ -1018,7 +1037,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   }
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
     fence_mbar_init();
     for (int pp = 0; pp < kMaxProj; ++pp)
@@ -1069,7 +1088,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
   const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty};
-  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr);
+  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 0, kProdParts);
+  else if (warp == kProdWarp2 && kProdParts == 2) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 1, kProdParts);
   else if (warp == kExpMmaWarp) expand_mma(p, sm, tmem_base, cta, warp, lane);
   else if (expand_epi_warp(warp)) expand_epilogue(p, sm, tmem_base, cta, warp, lane);
   tc_fence_before();
@@ -1106,7 +1126,7 @@ union RecBufU {
   ExpandRecBuf e;
 };
 __host__ __device__ constexpr int group_smem_bytes() {
-  return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 8 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
+  return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
          8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 + 1024;
 }
 static_assert(kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes <=
@@ -1187,7 +1207,8 @@ __device__ __forceinline__ void group_ready_checker(const ExpandParams& p, Expan
   }
 }
 
-__global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __grid_constant__ GroupParams gp) {
+constexpr int kGroupThreads = 288;   // the standalone layout + warp 8 (second copy-issuing part)
+__global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid_constant__ GroupParams gp) {
   static_assert(kShrinkThreads == kExpandThreads && kShrProdWarp == kExpProdWarp && kShrMmaWarp == kExpMmaWarp,
                 "the group kernel runs both pipelines with one warp layout");
   const ShrinkParams& sp = gp.s;
@@ -1196,7 +1217,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // shrink slots / expand ring
   uint8_t* ident = ring + kExpandRingBytes + kExpandGuardBytes;                     // 8 KB
   RecBufU* recbuf = reinterpret_cast<RecBufU*>(ident + kIdentRows * 16 * 2);       // one per warp, both phases
-  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + 8);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + kGroupThreads / 32);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
   uint64_t* s_empty = s_full + kShrinkSlots;
   uint64_t* s_tfull = s_empty + kShrinkSlots;
@@ -1218,9 +1239,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
   }
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); }
+    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&s_full[s], kProdParts); mbar_init(&s_empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&s_tfull[b], 1); mbar_init(&s_tempty[b], 4); }
-    for (int s = 0; s < kItemQ; ++s) { mbar_init(&e_full[s], 1); mbar_init(&e_empty[s], 1); }
+    for (int s = 0; s < kItemQ; ++s) { mbar_init(&e_full[s], kProdParts); mbar_init(&e_empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&e_tfull[b], 1); mbar_init(&e_tempty[b], kExpandEpiWarps); }
     for (int q = 0; q < kVQ; ++q) { mbar_init(&vfull[q], 1); mbar_init(&vempty[q], 1); }
     for (int q = 0; q < kRecQ; ++q) mbar_init(&recdone[q], 4);
@@ -1247,16 +1268,17 @@ __global__ void __launch_bounds__(kExpandThreads, 1) group_tc_kernel(const __gri
   ssw.recbuf = reinterpret_cast<ShrinkRecBuf*>(&recbuf[warp]) - warp;
   ExpandSm esw = esm;
   esw.recbuf = reinterpret_cast<ExpandRecBuf*>(&recbuf[warp]) - warp;
-  if (warp == kExpProdWarp) {
+  if (warp == kExpProdWarp || (warp == 8 && kProdParts == 2)) {
+    const int part = warp == 8 ? 1 : 0;
     if (shr) {
-      RingPos rp = shrink_producer(sp, ssw, cta, warp, lane);
+      RingPos rp = shrink_producer(sp, ssw, cta, warp, lane, part, kProdParts);
       for (int i = 0; i < kShrinkSlots; ++i) {   // every stage consumed: the ring is the expand's now
         mbar_wait(&s_empty[rp.slot], rp.phase ^ 1);
         if (++rp.slot == kShrinkSlots) { rp.slot = 0; rp.phase ^= 1; }
       }
     }
-    if (lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 2);   // shrink stages consumed
-    if (exp) expand_producer(ep, esw, cta, warp, lane, vfull, vempty);
+    if (lane == 0 && part == 0) phase_stamp(sp.trace, sp.trace_items, cta, 2);   // shrink stages consumed
+    if (exp) expand_producer(ep, esw, cta, warp, lane, vfull, vempty, part, kProdParts);
   } else if (warp == kExpMmaWarp) {
     if (shr) {
       const int n = shrink_mma(sp, ssw, tmem_base, cta, warp, lane);

@@ -81,3 +81,26 @@ if int(os.environ.get("LSV_DEBUG_SHRINK", "0")) & 16:   # per-stage shrink stamp
                 st["stage_period"].append(v[5] - sc[c, s - 1, 5])
     for k, v in st.items():
         pct(k, v)
+# expand items inside the group kernel: where an item's time goes (clock-only stamps)
+es = {k: [] for k in ("ring_wait", "alloc->B_issued", "B->y_issued", "y->v_issued(vready wait)", "v_issued->next",
+                      "load(alloc->landed)", "mma_full_wait", "mma_issue", "epi", "item_period")}
+for c in range(148):
+    n = int(ne[c])
+    for i in range(n):
+        v, a = ec[c, i], eaux[c, i]
+        es["ring_wait"].append(v[1] - v[0])
+        es["alloc->B_issued"].append(a[3] - v[1])
+        if a[5] > 0:
+            es["B->y_issued"].append(a[5] - a[3])
+            es["y->v_issued(vready wait)"].append(a[4] - a[5])
+        if i + 1 < n:
+            es["v_issued->next"].append(ec[c, i + 1, 0] - a[4])
+        es["load(alloc->landed)"].append(v[6] - v[1])
+        es["mma_full_wait"].append(v[6] - v[5])
+        es["mma_issue"].append(v[2] - v[6])
+        es["epi"].append(v[4] - v[3])
+        if i > 0:
+            es["item_period"].append(v[4] - ec[c, i - 1, 4])
+for k, v in es.items():
+    if v:
+        pct(k, v)
