@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import concurrent.futures
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -408,16 +409,51 @@ class LoraDeltaEngine:
             bp.b_ptrs.data_ptr() + l0 * P * S * 8, xs[l0][self.groups[0][0]].shape[0],
             bp.workspace.data_ptr(), bp.workspace.numel(), st.cuda_stream))
 
+    @staticmethod
+    def group_kernel_eligible(gp) -> bool:
+        """Whether ``forward`` runs this group plan as one group kernel (lsv_api.cu
+        group_kernel_eligible: tcgen05 tier only, not tile-aligned, LSV_GROUP_KERNEL not 0)."""
+        h = gp.plan_host[:64]
+        n_exp = int(h[60]) if int(h[33]) > 1 else int(h[53])
+        return (os.environ.get("LSV_GROUP_KERNEL", "1") != "0" and int(h[6]) == 0 and int(h[62]) == 0
+                and int(h[8]) > 0 and n_exp > 0)
+
     def launches_per_step(self, bp: BatchPlan) -> int:
-        """Kernels one ``forward`` launches (SIMT + tcgen05 shrink per group, SIMT + tcgen05 expand
-        per member)."""
+        """Kernels one ``forward`` launches: one group kernel per tcgen05-only group; otherwise SIMT +
+        tcgen05 shrink per group and SIMT (per member) + tcgen05 expand."""
         n = 0
         for gp in bp.group_plans:
+            if self.group_kernel_eligible(gp):
+                n += 1
+                continue
             simt = 1 if gp.summary[4] else 0
             h = gp.plan_host[:64]
             n += simt + (1 if gp.summary[6] else 0)                     # shrink
             n += simt * len(gp.h_outs) + (1 if int(h[60]) else 0)       # expand: SIMT per member + one tcgen05
         return n * self.model.layers
+
+    def forward_group(self, bp: BatchPlan, layer: int, gi: int, x: torch.Tensor, ys: list[torch.Tensor],
+                      stream=None) -> None:
+        """Input group gi of one layer through lsv_lora_forward_ex (one layer, one group): the group
+        kernel when the plan is eligible (bench.py times the dominant kernel with it)."""
+        self._live(bp)
+        gp = bp.group_plans[gi]
+        members = self.groups[gi][1]
+        S = bp.segments.num_segments
+        P = len(self.model.projections)
+        G = len(self.groups)
+        arr = lambda t, v: (t * len(v))(*v)   # noqa: E731
+        pd, ph = arr(ctypes.c_void_p, [gp.plan_dev.data_ptr()]), arr(ctypes.c_void_p, [gp.plan_host.ctypes.data])
+        xa, la = arr(ctypes.c_void_p, [x.data_ptr()]), arr(ctypes.c_int64, [x.stride(0)])
+        ya, lya = arr(ctypes.c_void_p, [y.data_ptr() for y in ys]), arr(ctypes.c_int64, [y.stride(0) for y in ys])
+        # a_ptrs rows are (layer, group), b_ptrs rows (layer, projection): this group's rows only
+        a_tab = bp.a_ptrs.data_ptr() + (layer * G + gi) * S * 8
+        b_tab = bp.b_ptrs.data_ptr() + (layer * P + members[0]) * S * 8
+        st = stream or torch.cuda.current_stream(self.device)
+        native.check(native.lib().lsv_lora_forward_ex(
+            1, 1, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
+            ctypes.addressof(ya), ctypes.addressof(lya), a_tab, b_tab, x.shape[0], bp.workspace.data_ptr(),
+            bp.workspace.numel(), 0, st.cuda_stream))
 
     @staticmethod
     def _check_io(x: torch.Tensor, y: torch.Tensor, h_in: int, h_out: int, n: int) -> None:

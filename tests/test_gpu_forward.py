@@ -158,3 +158,35 @@ def test_decode_groups_simt_ksplit_against_oracle():
         ref = oracle.delta_c(bf16_bits(x.cpu()), seg.seg_indptr, seg.seg_rank, a_list, b_list, pr.h_out)
         err = oracle.max_rel_err(ys[0][pr.name].float().cpu().numpy()[:N], ref[:N])
         assert err <= TOL, (pr.name, err)
+
+
+def test_group_kernel_full_layer_bit_identical_to_split_launches():
+    """One full Llama-2-7B layer at C2 scale (100 adapters, 4096 tokens, every group kernel path:
+    split tiles, member subsets of rank 128, down_proj's long split-K) through lsv_lora_forward
+    (one group kernel per input group) and through the separate shrink / expand launches: the
+    outputs are bit-identical (same split-K summation order, same v images)."""
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+    from paper_2511_22880_b200.slab import AdapterSlab
+    dev = torch.device("cuda:0")
+    model = ModelShape("l7b-1l", 1, LLAMA2_7B.projections)
+    ranks = [8] * 44 + [16] * 22 + [32] * 14 + [64] * 11 + [128] * 9
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+    for i, r in enumerate(ranks):
+        slab.fill_random(slab.allocate(f"a{i}", r), 700 + i)
+    seg = index_tokens(np.random.default_rng(3).integers(0, 100, 4096), ranks)
+    eng = LoraDeltaEngine(slab)
+    bp = eng.prepare(seg)
+    g = torch.Generator().manual_seed(4)
+    xs = [{name: (torch.randn(4096, model.projections[m[0]].h_in, generator=g) * 2).to(torch.bfloat16).to(dev)
+           for name, m in model.groups()}]
+    ys = [{p.name: torch.randn(4096, p.h_out, generator=g).to(torch.bfloat16).to(dev) for p in model.projections}]
+    ys2 = [{k: v.clone() for k, v in ys[0].items()}]
+    eng.forward(bp, xs, ys)
+    for gi, (name, members) in enumerate(model.groups()):
+        eng.shrink(bp, 0, members[0], xs[0][name])
+        eng.expand_group(bp, 0, gi, [ys2[0][model.projections[p].name] for p in members])
+    torch.cuda.synchronize()
+    for pr in model.projections:
+        assert torch.equal(ys[0][pr.name], ys2[0][pr.name]), pr.name
