@@ -3,5 +3,5 @@
 VAR=$1; VALS=$2; shift 2
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for i in 1 2; do for v in $VALS; do
-  echo -n "$VAR=$v: "; env $VAR=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step'],3), 'serial', round(d['serial_step']['ms_per_step'],3), 'expand', round(d['roofline']['launch_us'],1), 'shrink', round(d['roofline']['shrink']['launch_us'],1), 'e2e', round(d['e2e']['value']))"
+  echo -n "$VAR=$v: "; env $VAR=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" 2>/dev/null | python tools/ab_summary.py
 done; done
