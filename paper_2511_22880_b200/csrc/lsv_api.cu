@@ -32,7 +32,8 @@ thread_local char g_err[512] = "";
 // (lsv_debug_set_trace: launches issued from the calling thread stamp it) and ablation bits read
 // once from the environment (0 in production).
 thread_local uint64_t* g_trace = nullptr;
-thread_local int g_trace_items = 0;
+thread_local int g_trace_items = 0;   // < 0: group-kernel timeline mode, -(launches) records
+thread_local int g_tl_launch = 0;
 const int g_debug_shrink = [] { const char* e = std::getenv("LSV_DEBUG_SHRINK"); return e ? std::atoi(e) : 0; }();
 const int g_debug_expand = [] { const char* e = std::getenv("LSV_DEBUG_EXPAND"); return e ? std::atoi(e) : 0; }();
 // LSV_SIMT_WAIT=1: SIMT shrinks always wait for the previous launch (A/B timing of the overlap)
@@ -737,7 +738,7 @@ int fill_shrink_params(ShrinkParams& p, const PlanHeader* h, const void* x, int6
     p.vsplit = h->vsplit;
     p.tile_aligned = h->tile_aligned;
     p.dbg = g_debug_shrink;
-    p.trace = g_trace; p.trace_items = g_trace_items;
+    p.trace = g_trace_items > 0 ? g_trace : nullptr; p.trace_items = std::max(0, g_trace_items);
     p.num_tokens = num_tokens; p.h_in = h->h_in; p.ws_bytes = h->ws_bytes;
   }
   return LSV_OK;
@@ -816,7 +817,7 @@ int fill_expand_params(ExpandParams& p, const PlanHeader* h, int p0, int np, voi
   p.off_mtiles = h->off_mtiles;
   p.tw_max = tw_max;
   p.dbg = g_debug_expand;
-  p.trace = g_trace; p.trace_items = g_trace_items;
+  p.trace = g_trace_items > 0 ? g_trace : nullptr; p.trace_items = std::max(0, g_trace_items);
   p.num_tokens = num_tokens; p.ws_bytes = vimg_base ? INT64_MAX : h->ws_bytes;
   for (int pp = 0; pp < h->num_proj; ++pp) p.h_outs[pp] = h->h_outs[pp];
   return LSV_OK;
@@ -842,8 +843,13 @@ int run_group(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_token
   gp.s_grid = h->shrink_grid;
   gp.e_grid = h->num_proj > 1 ? h->expand_grid_all : h->expand_grid_p[0];
   gp.wait_prev = wait_prev;
-  if (gp.e.trace != nullptr)   // development trace: the expand's stamps in a second buffer half
+  if (g_trace != nullptr && g_trace_items < 0) {   // timeline mode: one [cta][4] record per launch
+    gp.s.trace = gp.e.trace = nullptr;
+    gp.s.trace_items = gp.e.trace_items = 0;
+    gp.tl = g_trace + (size_t)(g_tl_launch++ % -g_trace_items) * num_sms_cached() * 4;
+  } else if (gp.e.trace != nullptr) {   // development trace: the expand's stamps in a second buffer half
     gp.e.trace += (size_t)num_sms_cached() * gp.e.trace_items * 16;
+  }
   LSV_CUDA_CHECK(launch_pdl(group_tc_kernel, std::max(gp.s_grid, gp.e_grid), group_smem_bytes(), st, gp, pdl,
                             kGroupThreads));
   LSV_CUDA_CHECK(cudaGetLastError());
@@ -1454,6 +1460,7 @@ int lsv_lora_fused_linear(const void* x, int64_t ldx, int32_t num_tokens, int32_
 int lsv_debug_set_trace(void* buf, int32_t items_per_cta) {
   g_trace = static_cast<uint64_t*>(buf);
   g_trace_items = buf ? items_per_cta : 0;
+  g_tl_launch = 0;
   return LSV_OK;
 }
 

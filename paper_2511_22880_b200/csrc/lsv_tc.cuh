@@ -1120,6 +1120,7 @@ struct alignas(64) GroupParams {
   int* split_done;     // [n_mtiles]
   int s_grid, e_grid;  // CTAs with shrink records / expand items
   int wait_prev;       // 1: griddepcontrol.wait first (the previous launch may touch our buffers)
+  uint64_t* tl;        // development timeline (nullptr = off): [cta][4] = {entry, setup done, exit, SM id}
 };
 union RecBufU {
   ShrinkRecBuf s;
@@ -1233,6 +1234,12 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+  if (gp.tl != nullptr && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    gp.tl[cta * 4 + 0] = globaltimer_ns();
+    gp.tl[cta * 4 + 3] = smid;
+  }
   for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {   // identity A tile (expand y add)
     const int t = i / 16, k = i % 16;
     reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
@@ -1258,6 +1265,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) phase_stamp(sp.trace, sp.trace_items, cta, 0);
+  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 4 + 1] = globaltimer_ns();
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
   const bool shr = cta < gp.s_grid, exp = cta < gp.e_grid;
@@ -1302,6 +1310,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   tc_fence_before();
   __syncthreads();
   if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 4 + 2] = globaltimer_ns();
 }
 
 }  // namespace lsv
