@@ -22,6 +22,12 @@ if timeout 300 python tools/prof_one.py 2 > gpurun_out/prof_one_$TAG.log 2>&1; t
     -o gpurun_out/full_$TAG -f python tools/prof_one.py 2 > gpurun_out/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?"
 fi
+if timeout 300 python tools/prof_group.py > gpurun_out/prof_group_$TAG.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:group -s 8 -c 4 \
+    -o gpurun_out/group_full_$TAG -f python tools/prof_group.py > gpurun_out/ncu_group_$TAG.log 2>&1
+  echo "ncu group rc=$?"
+fi
+timeout 300 python tools/timeline_step.py 4 > gpurun_out/timeline_$TAG.txt 2>&1; echo "timeline rc=$?"
 if timeout 300 python tools/prof_fused.py 0 > gpurun_out/prof_fused_$TAG.log 2>&1; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fused" -s 2 -c 1 \
     -o gpurun_out/fused_full_$TAG -f python tools/prof_fused.py 0 > gpurun_out/ncu_fused_$TAG.log 2>&1
@@ -30,6 +36,6 @@ fi
 lscpu | head -20 > gpurun_out/lscpu_$TAG.txt
 python -c "
 import json; d=json.load(open('gpurun_out/bench_$TAG.json'))
-print('value', round(d['value']), 'ms', round(d['ms_per_step'],3), 'frac', round(d['step_hbm']['frac'],3), 'roof', round(d['roofline']['frac'],3))
+print('value', round(d['value']), 'ms', round(d['ms_per_step'],3), 'frac', round(d['step_hbm']['frac'],3), 'roof', round(d['roofline']['frac'],3), d['roofline']['kernel'])
 print('serial', d['serial_step']['ms_per_step'], 'e2e', round(d['e2e']['value']), 'cpu', d['cpu_baseline']['value'])
 print('dp1', round(d['dp_like_for_like']['value']), 'c1 us', round(d['c1']['us_per_call'],2), 'fused', d['fused_linear']['fused']['ms_per_layer'], d['fused_linear']['separate']['ms_per_layer'], d['fused_linear']['base']['ms_per_layer'])"

@@ -55,15 +55,20 @@ def launches():
     for k, (n, t) in agg.items():
         lines.append(f"{k:20s} {n:8d} {t:10.1f} {t / n:9.2f} {t / total:7.3f}")
     lines += ["", "per layer (first 3 layers of the capture, us):"]
+    grouped = out and out[0][0].endswith("group_tc_kernel")
+    per = 4 if grouped else 8
     for layer in range(3):
-        seg = out[layer * 8:(layer + 1) * 8]
+        seg = out[layer * per:(layer + 1) * per]
         parts = []
         for g in range(4):
-            parts.append(f"shrink {GROUPS[g]} {seg[2 * g][1]:.1f}")
-            parts.append(f"expand {GROUPS[g].split(' ')[0]} (one launch) {seg[2 * g + 1][1]:.1f}")
+            if grouped:
+                parts.append(f"group kernel {GROUPS[g]} {seg[g][1]:.1f}")
+            else:
+                parts.append(f"shrink {GROUPS[g]} {seg[2 * g][1]:.1f}")
+                parts.append(f"expand {GROUPS[g].split(' ')[0]} (one launch) {seg[2 * g + 1][1]:.1f}")
         lines.append("  " + ", ".join(parts))
-    step = out[:8 * 32]
-    lines += ["", f"one step = 32 layers x 8 launches = {len(step)} launches, sum {sum(u for _, u in step):.1f} us "
+    step = out[:per * 32]
+    lines += ["", f"one step = 32 layers x {per} launches = {len(step)} launches, sum {sum(u for _, u in step):.1f} us "
               "(serialised, cold caches)"]
     open(f"profiles/{OUT}_launch_summary.txt", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
@@ -109,11 +114,50 @@ def full():
         kern = k.split(" ")[0]
         if kern in traffic:
             tj["c2"][k] = traffic[kern]
-    tj["note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/{OUT}_ncu_full_mlp_in.txt. "
+    tj["note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch: split launches from "
+                  f"profiles/{OUT}_ncu_full_mlp_in.txt, the group kernel from profiles/{OUT}_ncu_group.txt. "
                   "Writes land in L2 and are partly evicted after the launch, so write bytes undercount.")
     json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
+
+
+def group():
+    """The four group kernels of one layer (tools/prof_group.py capture) -> profiles/<OUT>_ncu_group.txt,
+    and the mlp_in launch's DRAM bytes into traffic.json (bench.py's group-kernel roofline)."""
+    import os
+    rep = f"gpurun_out/group_full_{TAG}.ncu-rep"
+    if not os.path.exists(rep):
+        return
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw[raw.index('"ID"'):])))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    lines = ["# ncu --set full --clock-control none --import-source on -k regex:group -s 8 -c 4 python tools/prof_group.py",
+             "# config 2, one Llama-2-7B layer through lsv_lora_forward: the four group kernels in order (attn_in q/k/v,",
+             "# attn_out o, mlp_in gate/up, mlp_mid down); run only after `python tools/prof_group.py` exited 0 without",
+             "# ncu.  Cold-cache, serialised replay (no PDL overlap between the four).", ""]
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    traffic = []
+    for g, r in enumerate(data):
+        lines.append(f"== group_tc_kernel {GROUPS[g] if g < 4 else g}")
+        for m in METRICS:
+            if m in col:
+                lines.append(f"  {m:60s} {r[col[m]]:>20s} {units[col[m]]}")
+        b = float(r[col["dram__bytes_read.sum"]].replace(",", "")) * mult[units[col["dram__bytes_read.sum"]]] + \
+            float(r[col["dram__bytes_write.sum"]].replace(",", "")) * mult[units[col["dram__bytes_write.sum"]]]
+        lines.append(f"  dram read+write bytes per launch: {b / 1e6:.1f} MB")
+        lines.append("")
+        traffic.append(b)
+    open(f"profiles/{OUT}_ncu_group.txt", "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if len(traffic) >= 3:
+        tj = json.load(open("profiles/traffic.json"))
+        for k in tj["c2"]:
+            if k.startswith("group_tc_kernel (mlp_in"):
+                tj["c2"][k] = traffic[2]
+        json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
 
 
 if __name__ == "__main__":
     launches()
     full()
+    group()
