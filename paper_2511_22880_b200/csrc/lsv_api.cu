@@ -41,6 +41,8 @@ const bool g_simt_wait = [] { const char* e = std::getenv("LSV_SIMT_WAIT"); retu
 // LSV_GROUP_KERNEL=0: lsv_lora_forward runs each group as a shrink launch + an expand launch
 // instead of one group kernel (A/B timing)
 const bool g_group_kernel = [] { const char* e = std::getenv("LSV_GROUP_KERNEL"); return !e || std::atoi(e) != 0; }();
+// LSV_LAYER_KERNEL=0: one group kernel per (layer, group) instead of one layer kernel per layer
+const bool g_layer_kernel = [] { const char* e = std::getenv("LSV_LAYER_KERNEL"); return !e || std::atoi(e) != 0; }();
 // LSV_READY_ORDER=0: keep each CTA's expand items in LPT order instead of estimated m-tile
 // readiness order (A/B timing)
 const bool g_ready_order = [] { const char* e = std::getenv("LSV_READY_ORDER"); return !e || std::atoi(e) != 0; }();
@@ -622,8 +624,10 @@ int ensure_smem_attrs() {
                                           expand_smem_bytes());
     cudaError_t e3 = cudaFuncSetAttribute(fused_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           fused_smem_bytes());
-    cudaError_t e4 = cudaFuncSetAttribute(group_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e4 = cudaFuncSetAttribute(group_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           group_smem_bytes());
+    if (e4 == cudaSuccess)
+      e4 = cudaFuncSetAttribute(group_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, group_smem_bytes());
     if (e2 == cudaSuccess) e2 = e3;
     if (e2 == cudaSuccess) e2 = e4;
     rc = (e1 == cudaSuccess && e2 == cudaSuccess) ? LSV_OK : LSV_ECUDA;
@@ -831,27 +835,68 @@ bool group_kernel_eligible(const PlanHeader* h) {
   return g_group_kernel && h->n_simt_items == 0 && !h->tile_aligned && h->n_shrink_items > 0 &&
          (h->num_proj > 1 ? h->n_expand_all : h->n_expand_items_p[0]) > 0;
 }
-int run_group(const PlanHeader* h, const void* x, int64_t ldx, int32_t num_tokens, const void* const* a_ptrs,
-              void* const* ys, const int64_t* ldys, const void* const* const* b_ptrs, const int32_t* plan, uint8_t* ws,
-              int* gbar, int* ready, int wait_prev, bool pdl, cudaStream_t st) {
-  if (int rc = ensure_smem_attrs()) return rc;
-  GroupParams gp{};
-  if (int rc = fill_shrink_params(gp.s, h, x, ldx, num_tokens, a_ptrs, plan, ws, gbar)) return rc;
-  if (int rc = fill_expand_params(gp.e, h, 0, h->num_proj, ys, ldys, num_tokens, b_ptrs, plan, ws, nullptr)) return rc;
-  gp.ready = ready;
-  gp.split_done = ready + h->n_mtiles;
+// One group's parameters (its plan, x, A table, ys, B tables, workspace slice and counters).
+struct GroupArgs {
+  const PlanHeader* h;
+  const void* x;
+  int64_t ldx;
+  const void* const* a_ptrs;
+  void* const* ys;
+  const int64_t* ldys;
+  const void* const* const* b_ptrs;   // [num_proj] member tables
+  const int32_t* plan;
+  uint8_t* ws;
+  int* gbar;
+  int* ready;
+};
+int fill_group_params(GroupParams& gp, const GroupArgs& a, int32_t num_tokens, int wait_prev) {
+  const PlanHeader* h = a.h;
+  if (int rc = fill_shrink_params(gp.s, h, a.x, a.ldx, num_tokens, a.a_ptrs, a.plan, a.ws, a.gbar)) return rc;
+  if (int rc = fill_expand_params(gp.e, h, 0, h->num_proj, a.ys, a.ldys, num_tokens, a.b_ptrs, a.plan, a.ws, nullptr))
+    return rc;
+  gp.ready = a.ready;
+  gp.split_done = a.ready + h->n_mtiles;
   gp.s_grid = h->shrink_grid;
   gp.e_grid = h->num_proj > 1 ? h->expand_grid_all : h->expand_grid_p[0];
   gp.wait_prev = wait_prev;
-  if (g_trace != nullptr && g_trace_items < 0) {   // timeline mode: one [cta][4] record per launch
+  return LSV_OK;
+}
+// Development traces: timeline mode gives each launch its own [cta][4] record; item traces put the
+// expand's stamps in a second buffer half.
+void group_trace(GroupParams& gp) {
+  if (g_trace != nullptr && g_trace_items < 0) {
     gp.s.trace = gp.e.trace = nullptr;
     gp.s.trace_items = gp.e.trace_items = 0;
     gp.tl = g_trace + (size_t)(g_tl_launch++ % -g_trace_items) * num_sms_cached() * 4;
-  } else if (gp.e.trace != nullptr) {   // development trace: the expand's stamps in a second buffer half
+  } else if (gp.e.trace != nullptr) {
     gp.e.trace += (size_t)num_sms_cached() * gp.e.trace_items * 16;
   }
-  LSV_CUDA_CHECK(launch_pdl(group_tc_kernel, std::max(gp.s_grid, gp.e_grid), group_smem_bytes(), st, gp, pdl,
-                            kGroupThreads));
+}
+int run_group(const GroupArgs& a, int32_t num_tokens, int wait_prev, bool pdl, cudaStream_t st) {
+  if (int rc = ensure_smem_attrs()) return rc;
+  LayerParams<1> lp{};
+  if (int rc = fill_group_params(lp.g[0], a, num_tokens, wait_prev)) return rc;
+  lp.ngroups = 1;
+  group_trace(lp.g[0]);
+  LSV_CUDA_CHECK(launch_pdl(group_tc_kernel<1>, std::max(lp.g[0].s_grid, lp.g[0].e_grid), group_smem_bytes(), st, lp,
+                            pdl, kGroupThreads));
+  LSV_CUDA_CHECK(cudaGetLastError());
+  return LSV_OK;
+}
+// A layer kernel: n (<= kLayerGroups) overlap-free groups back to back in one launch.
+constexpr int kLayerGroups = 4;
+int run_layer(const GroupArgs* a, int n, int32_t num_tokens, int wait_prev, bool pdl, cudaStream_t st) {
+  if (int rc = ensure_smem_attrs()) return rc;
+  LayerParams<kLayerGroups> lp{};
+  int grid = 0;
+  for (int i = 0; i < n; ++i) {
+    if (int rc = fill_group_params(lp.g[i], a[i], num_tokens, wait_prev)) return rc;
+    grid = std::max(grid, std::max(lp.g[i].s_grid, lp.g[i].e_grid));
+  }
+  lp.ngroups = n;
+  group_trace(lp.g[0]);
+  for (int i = 1; i < n; ++i) lp.g[i].s.trace = lp.g[i].e.trace = nullptr;
+  LSV_CUDA_CHECK(launch_pdl(group_tc_kernel<kLayerGroups>, grid, group_smem_bytes(), st, lp, pdl, kGroupThreads));
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
@@ -1229,9 +1274,15 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
   if (any_group && num_layers > 0)
     LSV_CUDA_CHECK(cudaMemsetAsync(counters, 0, forward_counter_bytes(num_layers, num_groups, hs), st));
   size_t cnt_off = 0;
+  // layer kernels: an overlap-free call whose groups all run as group kernels issues one launch per
+  // layer (every group of the layer back to back in each CTA)
+  bool layer_kernel = g_layer_kernel && overlap_free && num_groups <= kLayerGroups;
+  for (int g = 0; g < num_groups; ++g) layer_kernel &= hs[g]->num_tokens > 0 && group_kernel_eligible(hs[g]);
   for (int l = 0; l < num_layers; ++l) {
     int p0 = 0;
     uint8_t* wsl = wsb + per_layer * (size_t)l;   // + kBarHeaderBytes + ws_off[g] = slice (l, g)
+    GroupArgs la[kLayerGroups];
+    const void* const* lbt[kLayerGroups][kMaxProj];
     for (int g = 0; g < num_groups; ++g) {
       const PlanHeader* h = hs[g];
       int* gbar = reinterpret_cast<int*>(wsb) + 2 * (1 + l * num_groups + g);
@@ -1249,14 +1300,17 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
         for (int i = 0; i < np; ++i)
           if (!yg[i] || !aligned16(yg[i]) || ldg[i] % 8 || ldg[i] < h->h_outs[i])
             return fail(LSV_EINVAL, "layer %d group %d member %d: bad y", l, g, i);
-        const void* const* btab[kMaxProj];
+        const void* const** btab = lbt[layer_kernel ? g : 0];
         for (int i = 0; i < np; ++i) btab[i] = bt + ((size_t)l * nproj + p0 + i) * S;
-        // an overlap-free call's group kernels touch disjoint buffers: none waits for its predecessor
-        if (int rc = run_group(h, x, ldx, num_tokens, at + ((size_t)l * num_groups + g) * S, yg, ldg, btab,
-                               static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], gbar, ready,
-                               (first || !overlap_free) ? 1 : 0, !first, st))
-          return rc;
+        const GroupArgs ga{h, x, ldx, at + ((size_t)l * num_groups + g) * S, yg, ldg, btab,
+                           static_cast<const int32_t*>(plans_dev[g]), wsl + ws_off[g], gbar, ready};
         p0 += np;
+        if (layer_kernel) {
+          la[g] = ga;
+          continue;
+        }
+        // an overlap-free call's group kernels touch disjoint buffers: none waits for its predecessor
+        if (int rc = run_group(ga, num_tokens, (first || !overlap_free) ? 1 : 0, !first, st)) return rc;
         continue;
       }
       if (h->num_tokens > 0) {
@@ -1279,6 +1333,8 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
         return rc;
       p0 += np;
     }
+    if (layer_kernel)
+      if (int rc = run_layer(la, num_groups, num_tokens, l == 0 ? 1 : 0, l > 0, st)) return rc;
   }
   return LSV_OK;
 }

@@ -374,10 +374,22 @@ struct RingPos {
   int slot;
   uint32_t phase;
 };
+// Pipeline position that carries over when one CTA runs several input groups back to back (the
+// layer kernel): every barrier's parity follows from these running counts.  Each role keeps its
+// own copy of the fields it uses (producer parts and MMA: the slot ring and the item count; MMA and
+// epilogue: the TMEM buffers' parity bits; epilogue and signal warp: the record count).
+struct PipeState {
+  int s_slot = 0;
+  uint32_t s_phase = 0;     // shrink slot ring position
+  uint32_t s_tbits = 0;     // shrink TMEM buffers: bit b = parity of buffer b's next tfull wait
+  int s_rec = 0;            // shrink records so far (recdone queue)
+  int e_item = 0;           // expand items so far (ring allocations, v-ready queue)
+  uint32_t e_tbits = 0;     // expand TMEM buffers: bit b = parity of buffer b's next tfull wait
+};
 // Producer: streams every record's stages into the slot ring; returns the ring position after
 // the last stage (the group kernel drains the ring from there).
 __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane,
-                                                   int part = 0, int nparts = 1) {
+                                                   int part = 0, int nparts = 1, RingPos start = RingPos{0, 0u}) {
   // nparts warps run this loop with the same slot bookkeeping; a stage's copies (A first, then the
   // x boxes) go round-robin to the parts, each arriving on full[slot] with its own bytes: one
   // warp spends ~130 cycles issuing each copy, so copies from two warps double the issue rate.
@@ -388,7 +400,7 @@ __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const 
   WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
   ShrinkRec inf;
   const uint8_t* a;
-  int slot = 0; uint32_t phase = 0;
+  int slot = start.slot; uint32_t phase = start.phase;
   int pstage = 0;   // debug stage stamps (LSV_DEBUG_SHRINK bit 16)
   const bool stamp = part == 0 && lane == 0;
   const uint32_t ring_base = smem_u32(ring);
@@ -443,7 +455,7 @@ __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const 
 // MMA issuer: the whole warp runs the loop (warp-uniform values stay in uniform registers, so each
 // MMA costs a few uniform adds), one lane issues.  Returns the number of records.
 __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm& sm, uint32_t tmem_base, int cta, int warp,
-                                          int lane) {
+                                          int lane, PipeState& st) {
   uint8_t* ring = sm.ring;
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* full = sm.full;
@@ -454,7 +466,7 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
     WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
     ShrinkRec inf;
     const uint8_t* unused;
-    int slot = 0; uint32_t phase = 0;
+    int slot = st.s_slot; uint32_t phase = st.s_phase;
     int dbg_stage = 0;
     const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
     const int nbuf = kTmemCols / p.acc_cols;
@@ -465,7 +477,7 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
       const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
       const int cb = __shfl_sync(0xffffffffu, inf.chunk_begin, 0), ce = __shfl_sync(0xffffffffu, inf.chunk_end, 0);
       const int buf = k % nbuf;
-      mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
+      mbar_wait(&tempty[buf], ((st.s_tbits >> buf) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + buf * p.acc_cols;
       const uint32_t idesc = idesc_bf16(128, max(16, round_up(rows, 16)));
@@ -493,8 +505,11 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
         if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
       }
       umma_commit_elect(&tfull[buf]);
+      st.s_tbits ^= 1u << buf;
       if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
     }
+  st.s_slot = slot;
+  st.s_phase = phase;
   return k;
 }
 // Epilogue: thread = token row of quadrant q.  In the group kernel (recdone != nullptr) each warp
@@ -502,7 +517,7 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
 // (and counts the records it has published in the int after the barriers: back-pressure).
 constexpr int kRecQ = 16;   // recdone barriers, then the signal warp's progress counter
 __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const ShrinkSm& sm, uint32_t tmem_base, int cta,
-                                                int warp, int lane, uint64_t* recdone) {
+                                                int warp, int lane, uint64_t* recdone, PipeState& st) {
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
@@ -512,11 +527,13 @@ __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const Shr
     ShrinkRec inf;
     const uint8_t* unused;
     const int nbuf = kTmemCols / p.acc_cols;
-    for (int k = 0; rs.pop(inf, unused); ++k) {
+    int k = 0;
+    for (; rs.pop(inf, unused); ++k) {
       const int r = inf.rank, nt = inf.ntok, kp = kpad(r), np16 = round_up(nt, 16);
       const int G = p.num_proj * r, rows = inf.np * r;
       const int buf = k % nbuf;
-      mbar_wait(&tfull[buf], (k / nbuf) & 1);
+      mbar_wait(&tfull[buf], (st.s_tbits >> buf) & 1);
+      st.s_tbits ^= 1u << buf;
       tc_fence_after();
       if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
@@ -581,12 +598,14 @@ __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const Shr
       if (lane == 0) mbar_arrive(&tempty[buf]);
       if (recdone != nullptr && lane == 0) {   // group kernel: stored (the signal warp is < kRecQ behind)
         const volatile int* sigc = reinterpret_cast<const volatile int*>(recdone + kRecQ);
-        while (k >= kRecQ && *sigc <= k - kRecQ) __nanosleep(32);
-        mbar_arrive(&recdone[k % kRecQ]);
+        const int kg = st.s_rec + k;   // record index over every group this CTA has run
+        while (kg >= kRecQ && *sigc <= kg - kRecQ) __nanosleep(32);
+        mbar_arrive(&recdone[kg % kRecQ]);
       }
       if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
       if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
+    st.s_rec += k;
   }
 
 __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
@@ -620,8 +639,13 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty};
   if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane, 0, kProdParts);
   else if (warp == kProdWarp2 && kProdParts == 2) shrink_producer(p, sm, cta, warp, lane, 1, kProdParts);
-  else if (warp == kShrMmaWarp) shrink_mma(p, sm, tmem_base, cta, warp, lane);
-  else if (shrink_epi_warp(warp)) shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr);
+  else if (warp == kShrMmaWarp) {
+    PipeState st;
+    shrink_mma(p, sm, tmem_base, cta, warp, lane, st);
+  } else if (shrink_epi_warp(warp)) {
+    PipeState st;
+    shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr, st);
+  }
   // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
   // recorded the table entry holding its first unit.  Each thread resolves its first two units
   // (static plan data, dependent loads) now, while other warps finish, so that after the grid
@@ -765,7 +789,8 @@ struct ExpandSm {
 // ~1800 cycles per item).  B and y are issued first; in the group kernel (vfull != nullptr) the
 // v copy waits until the ready checker has seen the item's m-tile complete.
 __device__ __forceinline__ void expand_producer(const ExpandParams& p, const ExpandSm& sm, int cta, int warp, int lane,
-                                                uint64_t* vfull, uint64_t* vempty, int part = 0, int nparts = 1) {
+                                                uint64_t* vfull, uint64_t* vempty, int part, int nparts, PipeState& st,
+                                                bool drain = false) {
   // nparts (1 or 2) warps run this loop with the same ring bookkeeping: part 0 copies B and v
   // (and y when alone), part 1 the y boxes; each arrives on full[] with its own bytes.
   uint8_t* ring = sm.ring;
@@ -779,11 +804,13 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
     WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
     ExpandRec inf;
     const uint8_t* b;
-    uint32_t head = 0, tail = 0;
+    uint32_t head = 0, tail = 0;   // ring bytes (the ring is empty when an expand phase starts)
     uint32_t vbegin[kItemQ];
-    int retired = 0;
+    const int k0 = st.e_item;      // allocations before this phase are all retired
+    int retired = k0;
     const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
-    for (int k = 0; rs.pop(inf, b); ++k) {
+    int k = k0;
+    for (; rs.pop(inf, b); ++k) {
       const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
       const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
       const uint32_t vlo = vimg_bytes(inf.ntok, kp);
@@ -801,7 +828,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
       LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
       LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
       const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
-      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k, 0);
+      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 0);
       while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
         mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
         ++retired;
@@ -815,7 +842,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
       const uint32_t fb = smem_u32(&full[qs]);
       mbar_arrive_expect_tx_elect(fb, (p0 ? ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) : 0u) +
                                           (do_y ? ((dbg & 8) ? 0 : ybytes) : 0u));
-      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k, 1);
+      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 1);
       const uint32_t dst = ring_base + ring_off;
       if (p0 && !(dbg & 16)) {
         if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group
@@ -827,7 +854,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
           bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
         }
       }
-      if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 3);
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 3);
       if (do_y && !(dbg & 8)) {
         // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
         // [nb blocks][R rows][64] at yoff + row * nb * 128
@@ -841,21 +868,24 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
         }
       }
       if (p0 && vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
-        if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 5);
+        if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 5);
         mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
-        if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 6);
+        if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 6);
         if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
       }
       if (p0 && !(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
-      if (stamp) trace_aux(p.trace, p.trace_items, cta, k, 4);
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 4);
       __syncwarp();
     }
+    if (drain)   // the next group's shrink reuses the ring bytes: wait until every item's MMAs read them
+      for (; retired < k; ++retired) mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
+    st.e_item = k;
 }
 // MMA issuer (whole warp): the election happens inside the MMA asm, so ptxas emits no per-MMA
 // uniformization loop; descriptors advance by constant steps (start address field = byte
 // address >> 4, below 2^14 in shared memory).
 __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm& sm, uint32_t tmem_base, int cta, int warp,
-                                           int lane) {
+                                           int lane, PipeState& st) {
   uint8_t* ring = sm.ring;
   uint8_t* ident = sm.ident;
   ExpandRecBuf* recbuf = sm.recbuf;
@@ -873,7 +903,9 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
     const uint8_t* unused;
     const uint32_t ib = smem_u32(ident);
     const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
-    for (int k = 0; rs.pop(inf, unused); ++k) {
+    const int k0 = st.e_item;
+    int k = k0;
+    for (; rs.pop(inf, unused); ++k) {
       const int r = inf.rank;
       const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
       const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
@@ -881,11 +913,11 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
       const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
       const int S = kmajor_row_bytes(kp), ck = S / 2;
       const uint32_t vlay = umma_layout(S);
-      const int buf = k % nbuf;
-      mbar_wait(&tempty[buf], ((k / nbuf) & 1) ^ 1);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
+      const int buf = (k - k0) % nbuf;
+      mbar_wait(&tempty[buf], ((st.e_tbits >> buf) & 1) ^ 1);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 5);
       mbar_wait(&full[qs], (k / kItemQ) & 1);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 6);
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 6);
       tc_fence_after();
       const uint32_t bb = ring_base + offs[qs];
       const uint32_t voff = round_up(tw * kp * 2, 1024);
@@ -893,7 +925,7 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
       const uint32_t vlo = vimg_bytes(inf.ntok, kp);
       const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
       const uint32_t d = tmem_base + buf * p.tw_max;
-      const int qrow = 32 * expand_qbase(k, inf.ntok);
+      const int qrow = 32 * expand_qbase(k - k0, inf.ntok);
       const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
       // D = v . B (+ v_lo . B): A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128).
       // K step ks: A advances 32 B inside a swizzle row, np16 rows of S bytes per ck-element chunk;
@@ -930,13 +962,15 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
       }
       umma_commit_elect(&empty[qs]);   // ring bytes free once these MMAs have read them
       umma_commit_elect(&tfull[buf]);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
+      st.e_tbits ^= 1u << buf;
+      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 2);
       __syncwarp();
     }
+    st.e_item = k;
 }
 // Epilogue: thread = token row of quadrant q.
 __device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const ExpandSm& sm, uint32_t tmem_base, int cta,
-                                                int warp, int lane) {
+                                                int warp, int lane, PipeState& st) {
   ExpandRecBuf* recbuf = sm.recbuf;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
@@ -948,7 +982,8 @@ __device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const Exp
     const uint8_t* unused;
     for (int k = 0; rs.pop(inf, unused); ++k) {
       const int buf = k % nbuf;
-      mbar_wait(&tfull[buf], (k / nbuf) & 1);
+      mbar_wait(&tfull[buf], (st.e_tbits >> buf) & 1);
+      st.e_tbits ^= 1u << buf;
       tc_fence_after();
       if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
       const int qr = q - expand_qbase(k, inf.ntok);   // this warp's quadrant within the item
@@ -1088,10 +1123,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
   const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty};
-  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 0, kProdParts);
-  else if (warp == kProdWarp2 && kProdParts == 2) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 1, kProdParts);
-  else if (warp == kExpMmaWarp) expand_mma(p, sm, tmem_base, cta, warp, lane);
-  else if (expand_epi_warp(warp)) expand_epilogue(p, sm, tmem_base, cta, warp, lane);
+  PipeState st;
+  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 0, kProdParts, st);
+  else if (warp == kProdWarp2 && kProdParts == 2) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 1, kProdParts, st);
+  else if (warp == kExpMmaWarp) expand_mma(p, sm, tmem_base, cta, warp, lane, st);
+  else if (expand_epi_warp(warp)) expand_epilogue(p, sm, tmem_base, cta, warp, lane, st);
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
@@ -1121,6 +1157,13 @@ struct alignas(64) GroupParams {
   int s_grid, e_grid;  // CTAs with shrink records / expand items
   int wait_prev;       // 1: griddepcontrol.wait first (the previous launch may touch our buffers)
   uint64_t* tl;        // development timeline (nullptr = off): [cta][4] = {entry, setup done, exit, SM id}
+};
+// A layer kernel runs NG input groups back to back in every CTA (lsv_lora_forward, overlap-free
+// calls): the groups' parameters travel together as kernel parameters (4 groups: ~26 KB).
+template <int NG>
+struct alignas(64) LayerParams {
+  GroupParams g[NG];
+  int ngroups;
 };
 union RecBufU {
   ShrinkRecBuf s;
@@ -1170,11 +1213,12 @@ __device__ __forceinline__ void group_reducer(const ShrinkParams& p, ShrinkRecBu
 // It never waits on other CTAs, so every record's signal goes out whatever the reducers wait on.
 // The release is cumulative over the epilogue warps' stores it acquired through the mbarrier.
 __device__ __forceinline__ void group_signaler(const ShrinkParams& p, ShrinkRecBuf* rb, int cta, int lane, int* ready,
-                                               int* split_done, uint64_t* recdone) {
+                                               int* split_done, uint64_t* recdone, int& rec_base) {
   WarpRecStream<ShrinkRec, kShrinkRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
   ShrinkRec inf;
   const uint8_t* unused;
-  for (int k = 0; rs.pop(inf, unused); ++k) {
+  int k = rec_base;   // record index over every group this CTA has run (recdone queue)
+  for (; rs.pop(inf, unused); ++k) {
     mbar_wait(&recdone[k % kRecQ], (k / kRecQ) & 1);
     if (lane == 0) {
       fence_proxy_async_global();   // the expand reads the images with bulk copies (async proxy)
@@ -1183,18 +1227,20 @@ __device__ __forceinline__ void group_signaler(const ShrinkParams& p, ShrinkRecB
     }
     __syncwarp();
   }
+  rec_base = k;
 }
 // Warp 4, expand phase: walks the expand list ahead of the producer; releases item k's v copy (vfull) once its
 // m-tile is complete.  The acquire + proxy fence make the images (generic-proxy stores of other
 // CTAs) visible to the producer's bulk copy.
 __device__ __forceinline__ void group_ready_checker(const ExpandParams& p, ExpandRecBuf* rb, int cta, int lane,
-                                                    const int* ready, uint64_t* vfull, uint64_t* vempty) {
+                                                    const int* ready, uint64_t* vfull, uint64_t* vempty, int& item_base) {
   WarpRecStream<ExpandRec, kExpandRecCh> rs(rb, p.plan, p.off_recs, p.off_cta, cta, nullptr);
   ExpandRec inf;
   const uint8_t* unused;
   const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
   int last = -1;
-  for (int k = 0; rs.pop(inf, unused); ++k) {
+  int k = item_base;   // item index over every group this CTA has run (v-ready queue)
+  for (; rs.pop(inf, unused); ++k) {
     mbar_wait(&vempty[k % kVQ], ((k / kVQ) & 1) ^ 1);
     if (inf.mtile != last) {
       if (lane == 0) {
@@ -1206,12 +1252,15 @@ __device__ __forceinline__ void group_ready_checker(const ExpandParams& p, Expan
     __syncwarp();
     if (lane == 0) mbar_arrive(&vfull[k % kVQ]);
   }
+  item_base = k;
 }
 
 constexpr int kGroupThreads = 288;   // the standalone layout + warp 8 (second copy-issuing part)
-__global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid_constant__ GroupParams gp) {
+template <int NG>
+__global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid_constant__ LayerParams<NG> lp) {
   static_assert(kShrinkThreads == kExpandThreads && kShrProdWarp == kExpProdWarp && kShrMmaWarp == kExpMmaWarp,
                 "the group kernel runs both pipelines with one warp layout");
+  const GroupParams& gp = lp.g[0];   // launch-wide fields (timeline, wait) and the first group's maps
   const ShrinkParams& sp = gp.s;
   const ExpandParams& ep = gp.e;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1268,7 +1317,6 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 4 + 1] = globaltimer_ns();
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
-  const bool shr = cta < gp.s_grid, exp = cta < gp.e_grid;
   const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty};
   const ExpandSm esm{ring, ident, &recbuf[0].e, offs, e_full, e_empty, e_tfull, e_tempty};
   // the role functions index recbuf by warp: give each a pointer whose [warp] is this warp's union slot
@@ -1276,36 +1324,73 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   ssw.recbuf = reinterpret_cast<ShrinkRecBuf*>(&recbuf[warp]) - warp;
   ExpandSm esw = esm;
   esw.recbuf = reinterpret_cast<ExpandRecBuf*>(&recbuf[warp]) - warp;
+  const int ng = NG == 1 ? 1 : lp.ngroups;
+  // Each role runs every group in order, its pipeline position carried over (PipeState): between a
+  // group's shrink and its expand the copy warps drain the slot ring and the MMA warp the shrink
+  // accumulators; between groups the copy warps drain the expand ring and the MMA warp the expand
+  // accumulators.  No CTA-wide barrier: a CTA moves on while others are still in the last group.
   if (warp == kExpProdWarp || (warp == 8 && kProdParts == 2)) {
     const int part = warp == 8 ? 1 : 0;
-    if (shr) {
-      RingPos rp = shrink_producer(sp, ssw, cta, warp, lane, part, kProdParts);
-      for (int i = 0; i < kShrinkSlots; ++i) {   // every stage consumed: the ring is the expand's now
-        mbar_wait(&s_empty[rp.slot], rp.phase ^ 1);
-        if (++rp.slot == kShrinkSlots) { rp.slot = 0; rp.phase ^= 1; }
+    RingPos rp{0, 0u};
+    PipeState st;
+    for (int g = 0; g < ng; ++g) {
+      const GroupParams& G = lp.g[g];
+      if (g > 0 && part == 0 && lane == 0) {   // the next group's tensor maps
+        for (int b = 0; b < 5; ++b) prefetch_tmap(&G.s.xmap[b]);
+        for (int pp = 0; pp < kMaxProj; ++pp)
+          if (G.e.y[pp])
+            for (int b = 0; b < 5; ++b) { prefetch_tmap(&G.e.ymap[pp][b]); prefetch_tmap(&G.e.ymap2[pp][b]); }
+      }
+      if (cta < G.s_grid) {
+        rp = shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, rp);
+        RingPos d = rp;
+        for (int i = 0; i < kShrinkSlots; ++i) {   // every stage consumed: the ring is the expand's now
+          mbar_wait(&s_empty[d.slot], d.phase ^ 1);
+          if (++d.slot == kShrinkSlots) { d.slot = 0; d.phase ^= 1; }
+        }
+      }
+      if (lane == 0 && part == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 2);   // shrink stages consumed
+      if (cta < G.e_grid) expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, g + 1 < ng);
+    }
+  } else if (warp == kExpMmaWarp) {
+    PipeState st;
+    for (int g = 0; g < ng; ++g) {
+      const GroupParams& G = lp.g[g];
+      if (cta < G.s_grid) {
+        shrink_mma(G.s, ssw, tmem_base, cta, warp, lane, st);
+        for (int b = 0; b < kAccBufs; ++b) mbar_wait(&s_tempty[b], ((st.s_tbits >> b) & 1) ^ 1);   // accumulators drained
+        tc_fence_after();
+      }
+      if (cta < G.e_grid) {
+        expand_mma(G.e, esw, tmem_base, cta, warp, lane, st);
+        if (g + 1 < ng) {
+          for (int b = 0; b < kAccBufs; ++b) mbar_wait(&e_tempty[b], ((st.e_tbits >> b) & 1) ^ 1);
+          tc_fence_after();
+        }
       }
     }
-    if (lane == 0 && part == 0) phase_stamp(sp.trace, sp.trace_items, cta, 2);   // shrink stages consumed
-    if (exp) expand_producer(ep, esw, cta, warp, lane, vfull, vempty, part, kProdParts);
-  } else if (warp == kExpMmaWarp) {
-    if (shr) {
-      const int n = shrink_mma(sp, ssw, tmem_base, cta, warp, lane);
-      const int nbs = kTmemCols / sp.acc_cols;
-      for (int k = n; k < n + nbs; ++k) mbar_wait(&s_tempty[k % nbs], ((k / nbs) & 1) ^ 1);   // accumulators drained
-      tc_fence_after();
-    }
-    if (exp) expand_mma(ep, esw, tmem_base, cta, warp, lane);
   } else if (expand_epi_warp(warp)) {
-    if (shr) shrink_epilogue(sp, ssw, tmem_base, cta, warp, lane, recdone);
-    if (warp == 0 && lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 1);   // shrink records stored
-    if (exp) expand_epilogue(ep, esw, tmem_base, cta, warp, lane);
-    if (warp == 0 && lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 4);   // expand items stored
+    PipeState st;
+    for (int g = 0; g < ng; ++g) {
+      const GroupParams& G = lp.g[g];
+      if (cta < G.s_grid) shrink_epilogue(G.s, ssw, tmem_base, cta, warp, lane, recdone, st);
+      if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 1);   // shrink records stored
+      if (cta < G.e_grid) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
+      if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 4);   // expand items stored
+    }
   } else if (warp == 4) {
-    if (shr) group_signaler(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done, recdone);
-    if (exp) group_ready_checker(ep, &recbuf[warp].e, cta, lane, gp.ready, vfull, vempty);
+    int rec_base = 0, item_base = 0;
+    for (int g = 0; g < ng; ++g) {
+      const GroupParams& G = lp.g[g];
+      if (cta < G.s_grid) group_signaler(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done, recdone, rec_base);
+      if (cta < G.e_grid) group_ready_checker(G.e, &recbuf[warp].e, cta, lane, G.ready, vfull, vempty, item_base);
+    }
   } else if (warp == 5) {
-    if (shr) group_reducer(sp, &recbuf[warp].s, cta, lane, gp.ready, gp.split_done);
-    if (lane == 0) phase_stamp(sp.trace, sp.trace_items, cta, 3);   // split-K shares reduced
+    for (int g = 0; g < ng; ++g) {
+      const GroupParams& G = lp.g[g];
+      if (cta < G.s_grid) group_reducer(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done);
+      if (lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 3);   // split-K shares reduced
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -418,9 +418,13 @@ class LoraDeltaEngine:
         return (os.environ.get("LSV_GROUP_KERNEL", "1") != "0" and int(h[6]) == 0 and int(h[62]) == 0
                 and int(h[8]) > 0 and n_exp > 0)
 
-    def launches_per_step(self, bp: BatchPlan) -> int:
-        """Kernels one ``forward`` launches: one group kernel per tcgen05-only group; otherwise SIMT +
-        tcgen05 shrink per group and SIMT (per member) + tcgen05 expand."""
+    def launches_per_step(self, bp: BatchPlan, serial: bool = False) -> int:
+        """Kernels one ``forward`` launches: one layer kernel per layer when every group runs as a
+        group kernel (overlap-free calls, at most 4 groups); else one group kernel per tcgen05-only
+        group, otherwise SIMT + tcgen05 shrink per group and SIMT (per member) + tcgen05 expand."""
+        if (not serial and os.environ.get("LSV_LAYER_KERNEL", "1") != "0" and len(bp.group_plans) <= 4
+                and all(self.group_kernel_eligible(gp) for gp in bp.group_plans)):
+            return self.model.layers
         n = 0
         for gp in bp.group_plans:
             if self.group_kernel_eligible(gp):

@@ -1,4 +1,5 @@
-"""Per-SM timeline of a multi-layer lsv_lora_forward (C2 shapes, L layers -> 4L group kernels):
+"""Per-SM timeline of a multi-layer lsv_lora_forward (C2 shapes, L layers -> L layer kernels, or 4L
+group kernels with LSV_LAYER_KERNEL=0):
 when each launch's CTA enters, finishes its setup and exits on every SM, and how much SM time
 the launch boundaries cost (exit of one CTA -> entry of the next on the same SM, plus setup).
     python tools/timeline_step.py [layers=4]"""
@@ -43,9 +44,12 @@ e1.record()
 torch.cuda.synchronize()
 lib.lsv_debug_set_trace(None, 0)
 tl = buf.view(n, 148, 4).cpu().numpy().astype(np.int64)
+n = int((tl[:, :, 0].max(axis=1) > 0).sum())   # launches recorded: 4L group kernels or L layer kernels
+tl = tl[:n]
 t0 = tl[:, :, 0][tl[:, :, 0] > 0].min()
-print(f"{L} layers, {n} group kernels: {e0.elapsed_time(e1) * 1e3:.0f} us (events); per launch (us from first entry):")
-names = [g for g, _ in eng.groups] * L
+kind = "group kernels" if n == 4 * L else "layer kernels"
+print(f"{L} layers, {n} {kind}: {e0.elapsed_time(e1) * 1e3:.0f} us (events); per launch (us from first entry):")
+names = [g for g, _ in eng.groups] * L if n == 4 * L else [f"layer {i}" for i in range(n)]
 for i in range(n):
     ent, setup, ext = (tl[i, :, 0] - t0) / 1e3, (tl[i, :, 1] - tl[i, :, 0]) / 1e3, (tl[i, :, 2] - t0) / 1e3
     print(f"  {i:2d} {names[i]:9s} entry {ent.min():7.1f}..{ent.max():7.1f}  setup p50 {np.median(setup):4.2f}  "
