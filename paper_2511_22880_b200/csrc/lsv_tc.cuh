@@ -1325,45 +1325,61 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   ExpandSm esw = esm;
   esw.recbuf = reinterpret_cast<ExpandRecBuf*>(&recbuf[warp]) - warp;
   const int ng = NG == 1 ? 1 : lp.ngroups;
-  // Each role runs every group in order, its pipeline position carried over (PipeState): between a
-  // group's shrink and its expand the copy warps drain the slot ring and the MMA warp the shrink
-  // accumulators; between groups the copy warps drain the expand ring and the MMA warp the expand
-  // accumulators.  No CTA-wide barrier: a CTA moves on while others are still in the last group.
+  // Each role runs the layer's 2*ng phases in the same order, its pipeline position carried over
+  // (PipeState): S0, S1, E0, S2, E1, ..., S(ng-1), E(ng-2), E(ng-1) — the next group's shrink runs
+  // before the previous group's expand, so a group's m-tiles (split-K reductions included) are
+  // complete by the time its expand starts.  After a shrink phase followed by an expand the copy
+  // warps drain the slot ring; after an expand phase they drain the expand ring; the MMA warp drains
+  // a phase's accumulators before the next phase writes TMEM.  No CTA-wide barrier.
+  const int nph = 2 * ng;
+  auto phase_of = [&](int i, int& g) -> bool {   // true: expand phase of group g
+    if (i == 0) { g = 0; return false; }
+    if (i == nph - 1) { g = ng - 1; return true; }
+    g = (i + 1) / 2 - (i % 2 == 0 ? 1 : 0);
+    return i % 2 == 0;
+  };
   if (warp == kExpProdWarp || (warp == 8 && kProdParts == 2)) {
     const int part = warp == 8 ? 1 : 0;
     RingPos rp{0, 0u};
     PipeState st;
-    for (int g = 0; g < ng; ++g) {
+    for (int i = 0; i < nph; ++i) {
+      int g, gn = 0;
+      const bool ex = phase_of(i, g);
+      const bool next_ex = i + 1 < nph && phase_of(i + 1, gn);
       const GroupParams& G = lp.g[g];
-      if (g > 0 && part == 0 && lane == 0) {   // the next group's tensor maps
-        for (int b = 0; b < 5; ++b) prefetch_tmap(&G.s.xmap[b]);
-        for (int pp = 0; pp < kMaxProj; ++pp)
-          if (G.e.y[pp])
-            for (int b = 0; b < 5; ++b) { prefetch_tmap(&G.e.ymap[pp][b]); prefetch_tmap(&G.e.ymap2[pp][b]); }
-      }
-      if (cta < G.s_grid) {
-        rp = shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, rp);
-        RingPos d = rp;
-        for (int i = 0; i < kShrinkSlots; ++i) {   // every stage consumed: the ring is the expand's now
-          mbar_wait(&s_empty[d.slot], d.phase ^ 1);
-          if (++d.slot == kShrinkSlots) { d.slot = 0; d.phase ^= 1; }
+      if (!ex) {
+        if (g > 0 && part == 0 && lane == 0) {   // this group's tensor maps
+          for (int b = 0; b < 5; ++b) prefetch_tmap(&G.s.xmap[b]);
+          for (int pp = 0; pp < kMaxProj; ++pp)
+            if (G.e.y[pp])
+              for (int b = 0; b < 5; ++b) { prefetch_tmap(&G.e.ymap[pp][b]); prefetch_tmap(&G.e.ymap2[pp][b]); }
         }
+        if (cta < G.s_grid) rp = shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, rp);
+        if (next_ex) {
+          RingPos d = rp;
+          for (int j = 0; j < kShrinkSlots; ++j) {   // every stage consumed: the ring is the expand's now
+            mbar_wait(&s_empty[d.slot], d.phase ^ 1);
+            if (++d.slot == kShrinkSlots) { d.slot = 0; d.phase ^= 1; }
+          }
+        }
+        if (lane == 0 && part == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 2);   // shrink stages issued
+      } else if (cta < G.e_grid) {
+        expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, i + 1 < nph);
       }
-      if (lane == 0 && part == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 2);   // shrink stages consumed
-      if (cta < G.e_grid) expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, g + 1 < ng);
     }
   } else if (warp == kExpMmaWarp) {
     PipeState st;
-    for (int g = 0; g < ng; ++g) {
+    for (int i = 0; i < nph; ++i) {
+      int g;
+      const bool ex = phase_of(i, g);
       const GroupParams& G = lp.g[g];
-      if (cta < G.s_grid) {
+      if (!ex && cta < G.s_grid) {
         shrink_mma(G.s, ssw, tmem_base, cta, warp, lane, st);
         for (int b = 0; b < kAccBufs; ++b) mbar_wait(&s_tempty[b], ((st.s_tbits >> b) & 1) ^ 1);   // accumulators drained
         tc_fence_after();
-      }
-      if (cta < G.e_grid) {
+      } else if (ex && cta < G.e_grid) {
         expand_mma(G.e, esw, tmem_base, cta, warp, lane, st);
-        if (g + 1 < ng) {
+        if (i + 1 < nph) {
           for (int b = 0; b < kAccBufs; ++b) mbar_wait(&e_tempty[b], ((st.e_tbits >> b) & 1) ^ 1);
           tc_fence_after();
         }
@@ -1371,22 +1387,27 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
     }
   } else if (expand_epi_warp(warp)) {
     PipeState st;
-    for (int g = 0; g < ng; ++g) {
+    for (int i = 0; i < nph; ++i) {
+      int g;
+      const bool ex = phase_of(i, g);
       const GroupParams& G = lp.g[g];
-      if (cta < G.s_grid) shrink_epilogue(G.s, ssw, tmem_base, cta, warp, lane, recdone, st);
-      if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 1);   // shrink records stored
-      if (cta < G.e_grid) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
-      if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 4);   // expand items stored
+      if (!ex && cta < G.s_grid) shrink_epilogue(G.s, ssw, tmem_base, cta, warp, lane, recdone, st);
+      if (ex && cta < G.e_grid) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
+      if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, ex ? 4 : 1);   // phase stored
     }
   } else if (warp == 4) {
     int rec_base = 0, item_base = 0;
-    for (int g = 0; g < ng; ++g) {
+    for (int i = 0; i < nph; ++i) {
+      int g;
+      const bool ex = phase_of(i, g);
       const GroupParams& G = lp.g[g];
-      if (cta < G.s_grid) group_signaler(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done, recdone, rec_base);
-      if (cta < G.e_grid) group_ready_checker(G.e, &recbuf[warp].e, cta, lane, G.ready, vfull, vempty, item_base);
+      if (!ex && cta < G.s_grid) group_signaler(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done, recdone, rec_base);
+      if (ex && cta < G.e_grid) group_ready_checker(G.e, &recbuf[warp].e, cta, lane, G.ready, vfull, vempty, item_base);
     }
   } else if (warp == 5) {
-    for (int g = 0; g < ng; ++g) {
+    for (int i = 0; i < nph; ++i) {
+      int g;
+      if (phase_of(i, g)) continue;
       const GroupParams& G = lp.g[g];
       if (cta < G.s_grid) group_reducer(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done);
       if (lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 3);   // split-K shares reduced
