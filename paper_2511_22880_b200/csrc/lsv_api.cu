@@ -94,9 +94,9 @@ bool decode_shaped(int32_t S, const int32_t* indptr) {
 }
 constexpr int64_t kMinItemBytes = 64 * 1024;  // smallest shrink k-split worth a pipeline fill
 #ifndef LSV_SHRINK_WAVES
-#define LSV_SHRINK_WAVES 4
+#define LSV_SHRINK_WAVES 2
 #endif
-constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost; 4 measured best with the group kernel: 9.58 vs 9.70 ms at 8, 9.79 at 2)
+constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (balance vs split cost): with the layer kernel's S(g+1)-before-E(g) order 2 measured best (8.67 / 8.95 ms vs 8.76 / 8.94 at 4, 8.93 at 8; 1 within noise)
 // LPT cost of an item = its bytes + a fixed per-item cost (pipeline fill, barrier round trips,
 // epilogue), in byte-equivalents
 #ifndef LSV_EXPAND_ITEM_FIXED_KB
