@@ -41,6 +41,9 @@ const bool g_simt_wait = [] { const char* e = std::getenv("LSV_SIMT_WAIT"); retu
 // LSV_GROUP_KERNEL=0: lsv_lora_forward runs each group as a shrink launch + an expand launch
 // instead of one group kernel (A/B timing)
 const bool g_group_kernel = [] { const char* e = std::getenv("LSV_GROUP_KERNEL"); return !e || std::atoi(e) != 0; }();
+// LSV_FWD_STREAMS=0: an overlap-free forward that cannot use layer kernels (SIMT-tier groups: decode)
+// issues every group on the caller's stream instead of one stream per group index
+const bool g_fwd_streams = [] { const char* e = std::getenv("LSV_FWD_STREAMS"); return !e || std::atoi(e) != 0; }();
 // LSV_LAYER_KERNEL=0: one group kernel per (layer, group) instead of one layer kernel per layer
 const bool g_layer_kernel = [] { const char* e = std::getenv("LSV_LAYER_KERNEL"); return !e || std::atoi(e) != 0; }();
 // LSV_READY_ORDER=0: keep each CTA's expand items in LPT order instead of estimated m-tile
@@ -117,6 +120,33 @@ constexpr int64_t kShrinkStageFixed = (int64_t)LSV_SHRINK_STAGE_FIXED_KB * 1024;
 // local records, keeping NVLink and HBM busy together instead of one after the other.
 const int kRemoteWeight = [] { const char* e = std::getenv("LSV_REMOTE_WEIGHT"); return e ? std::atoi(e) : 7; }();
 
+// Per-device side streams for lsv_lora_forward's group-parallel mode (created once, never freed):
+// the groups of an overlap-free call are independent, so group g's launches go to stream g % 4
+// (forked from and joined back into the caller's stream with events; graph capture records the
+// fork/join as parallel branches).
+constexpr int kFwdStreams = 4;
+struct FwdStreams {
+  cudaStream_t s[kFwdStreams - 1] = {};
+  cudaEvent_t fork = nullptr, join[kFwdStreams - 1] = {};
+  bool ok = false;
+};
+FwdStreams* fwd_streams() {
+  static FwdStreams per_dev[16];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  FwdStreams& f = per_dev[dev];
+  if (!f.ok) {
+    bool good = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < kFwdStreams - 1 && good; ++i)
+      good = cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&f.join[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!good) { cudaGetLastError(); return nullptr; }
+    f.ok = true;
+  }
+  return &f;
+}
 int num_sms_cached() {
   static int sms = -1;
   static std::once_flag once;
@@ -1278,6 +1308,16 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
   // layer (every group of the layer back to back in each CTA)
   bool layer_kernel = g_layer_kernel && overlap_free && num_groups <= kLayerGroups;
   for (int g = 0; g < num_groups; ++g) layer_kernel &= hs[g]->num_tokens > 0 && group_kernel_eligible(hs[g]);
+  // otherwise an overlap-free call spreads its groups over kFwdStreams streams (group g on stream
+  // g % kFwdStreams): independent groups then run concurrently, which the small SIMT-tier launches
+  // of decode batches need to fill the GPU
+  FwdStreams* const fs = (overlap_free && !layer_kernel && g_fwd_streams && num_groups > 1 && num_layers > 0)
+                             ? fwd_streams() : nullptr;
+  if (fs != nullptr) {
+    LSV_CUDA_CHECK(cudaEventRecord(fs->fork, st));
+    for (int i = 0; i < kFwdStreams - 1; ++i) LSV_CUDA_CHECK(cudaStreamWaitEvent(fs->s[i], fs->fork, 0));
+  }
+  const cudaStream_t st_main = st;
   for (int l = 0; l < num_layers; ++l) {
     int p0 = 0;
     uint8_t* wsl = wsb + per_layer * (size_t)l;   // + kBarHeaderBytes + ws_off[g] = slice (l, g)
@@ -1289,7 +1329,9 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       const int np = h->num_proj;
       const int64_t ldx = ldxs[l * num_groups + g];
       const void* x = xs[l * num_groups + g];
-      const bool first = l == 0 && g == 0;
+      // the first launch on each stream of this call is a plain one (waits for the fork / earlier work)
+      const bool first = l == 0 && (fs != nullptr ? g < kFwdStreams : g == 0);
+      const cudaStream_t st = (fs != nullptr && g % kFwdStreams != 0) ? fs->s[g % kFwdStreams - 1] : st_main;
       int* const ready = counters + cnt_off;
       cnt_off += 2 * (size_t)h->n_mtiles;
       if (h->num_tokens > 0 && group_kernel_eligible(h)) {
@@ -1334,8 +1376,13 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       p0 += np;
     }
     if (layer_kernel)
-      if (int rc = run_layer(la, num_groups, num_tokens, l == 0 ? 1 : 0, l > 0, st)) return rc;
+      if (int rc = run_layer(la, num_groups, num_tokens, l == 0 ? 1 : 0, l > 0, st_main)) return rc;
   }
+  if (fs != nullptr)
+    for (int i = 0; i < kFwdStreams - 1; ++i) {
+      LSV_CUDA_CHECK(cudaEventRecord(fs->join[i], fs->s[i]));
+      LSV_CUDA_CHECK(cudaStreamWaitEvent(st_main, fs->join[i], 0));
+    }
   return LSV_OK;
 }
 
