@@ -124,7 +124,10 @@ const int kRemoteWeight = [] { const char* e = std::getenv("LSV_REMOTE_WEIGHT");
 // the groups of an overlap-free call are independent, so group g's launches go to stream g % 4
 // (forked from and joined back into the caller's stream with events; graph capture records the
 // fork/join as parallel branches).
-constexpr int kFwdStreams = 4;
+#ifndef LSV_FWD_NSTREAMS
+#define LSV_FWD_NSTREAMS 4
+#endif
+constexpr int kFwdStreams = LSV_FWD_NSTREAMS;
 struct FwdStreams {
   cudaStream_t s[kFwdStreams - 1] = {};
   cudaEvent_t fork = nullptr, join[kFwdStreams - 1] = {};
@@ -1330,8 +1333,9 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       const int64_t ldx = ldxs[l * num_groups + g];
       const void* x = xs[l * num_groups + g];
       // the first launch on each stream of this call is a plain one (waits for the fork / earlier work)
-      const bool first = l == 0 && (fs != nullptr ? g < kFwdStreams : g == 0);
-      const cudaStream_t st = (fs != nullptr && g % kFwdStreams != 0) ? fs->s[g % kFwdStreams - 1] : st_main;
+      const int si = (l * num_groups + g) % kFwdStreams;   // (layer, group) round robin over the streams
+      const bool first = fs != nullptr ? l * num_groups + g < kFwdStreams : (l == 0 && g == 0);
+      const cudaStream_t st = (fs != nullptr && si != 0) ? fs->s[si - 1] : st_main;
       int* const ready = counters + cnt_off;
       cnt_off += 2 * (size_t)h->n_mtiles;
       if (h->num_tokens > 0 && group_kernel_eligible(h)) {
