@@ -120,13 +120,15 @@ constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past 
 constexpr int kExpandRingBytes = LSV_EXPAND_RING_KB * 1024;   // variable-size items, allocated in issue order
 constexpr int kExpandGuardBytes = 2 * 1024;    // rank-8 K=16 MMA reads one k-core past its tile
 constexpr int kExpandInflight = 8;
-// SIMT shrink k-splits: h_in's 64-column chunks are split into ~16-chunk ranges, one block each, so a
-// decode batch's few rank-row blocks still spread over every SM.  16 measured best once the SIMT
-// shrinks overlap the previous group's expand (decode step 4.24-4.41 ms vs 4.61 at 32, 4.48 at 8,
-// 4.42 at 12, 5.89 at 64; tools/gpu_ab_lib.sh --config decode).  Each split
-// writes its own fp32 partial v; the SIMT expand sums the splits in split order (deterministic).
+// SIMT shrink k-splits: h_in's 64-column chunks are split into ~48-chunk ranges, one block each.
+// With one launch stream, 16-chunk splits measured best (4.24-4.41 ms decode step; the few rank-row
+// blocks of a decode batch need the split to spread over the SMs).  With lsv_lora_forward's groups on
+// concurrent streams the other groups fill the SMs instead, and fewer splits win (decode step 3.04 ms
+// at 48 vs 3.06 at 64, 3.20 at 32, 3.42 at 16, 3.61 at 128; tools/gpu_ab_lib.sh --config decode); the
+// serialised step pays for it (6.6 vs 5.4 ms).  Each split writes its own fp32 partial v; the SIMT
+// expand sums the splits in split order (deterministic).
 #ifndef LSV_SIMT_SPLIT_CHUNKS
-#define LSV_SIMT_SPLIT_CHUNKS 16
+#define LSV_SIMT_SPLIT_CHUNKS 48
 #endif
 __host__ __device__ constexpr int simt_ksplit(int h_in) {
   return h_in / 64 / LSV_SIMT_SPLIT_CHUNKS < 1 ? 1 : h_in / 64 / LSV_SIMT_SPLIT_CHUNKS;
