@@ -436,6 +436,27 @@ class LoraDeltaEngine:
             n += simt * len(gp.h_outs) + (1 if int(h[60]) else 0)       # expand: SIMT per member + one tcgen05
         return n * self.model.layers
 
+    def forward_layer(self, bp: BatchPlan, layer: int, xs_l: dict[str, torch.Tensor], ys_l: dict[str, torch.Tensor],
+                      stream=None) -> None:
+        """Every input group of one layer through lsv_lora_forward_ex (one layer): the layer kernel when
+        every group plan is eligible (bench.py times the dominant kernel with it)."""
+        self._live(bp)
+        projs = self.model.projections
+        G, P, S = len(self.groups), len(projs), bp.segments.num_segments
+        arr = lambda t, v: (t * len(v))(*v)   # noqa: E731
+        xl = [xs_l[g] for g, _ in self.groups]
+        yl = [ys_l[projs[p].name] for _, m in self.groups for p in m]
+        pd = arr(ctypes.c_void_p, [gp.plan_dev.data_ptr() for gp in bp.group_plans])
+        ph = arr(ctypes.c_void_p, [gp.plan_host.ctypes.data for gp in bp.group_plans])
+        xa, la = arr(ctypes.c_void_p, [x.data_ptr() for x in xl]), arr(ctypes.c_int64, [x.stride(0) for x in xl])
+        ya, lya = arr(ctypes.c_void_p, [y.data_ptr() for y in yl]), arr(ctypes.c_int64, [y.stride(0) for y in yl])
+        st = stream or torch.cuda.current_stream(self.device)
+        native.check(native.lib().lsv_lora_forward_ex(
+            1, G, ctypes.addressof(pd), ctypes.addressof(ph), ctypes.addressof(xa), ctypes.addressof(la),
+            ctypes.addressof(ya), ctypes.addressof(lya), bp.a_ptrs.data_ptr() + layer * G * S * 8,
+            bp.b_ptrs.data_ptr() + layer * P * S * 8, xl[0].shape[0], bp.workspace.data_ptr(),
+            bp.workspace.numel(), 0, st.cuda_stream))
+
     def forward_group(self, bp: BatchPlan, layer: int, gi: int, x: torch.Tensor, ys: list[torch.Tensor],
                       stream=None) -> None:
         """Input group gi of one layer through lsv_lora_forward_ex (one layer, one group): the group

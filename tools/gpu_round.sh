@@ -23,9 +23,12 @@ if timeout 300 python tools/prof_one.py 2 > gpurun_out/prof_one_$TAG.log 2>&1; t
   echo "ncu full rc=$?"
 fi
 if timeout 300 python tools/prof_group.py > gpurun_out/prof_group_$TAG.log 2>&1; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:group -s 8 -c 4 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:group -s 3 -c 1 \
     -o gpurun_out/group_full_$TAG -f python tools/prof_group.py > gpurun_out/ncu_group_$TAG.log 2>&1
-  echo "ncu group rc=$?"
+  echo "ncu layer kernel rc=$?"
+  LSV_LAYER_KERNEL=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:group -s 12 -c 4 \
+    -o gpurun_out/group4_full_$TAG -f python tools/prof_group.py > gpurun_out/ncu_group4_$TAG.log 2>&1
+  echo "ncu group kernels rc=$?"
 fi
 timeout 300 python tools/timeline_step.py 4 > gpurun_out/timeline_$TAG.txt 2>&1; echo "timeline rc=$?"
 if timeout 300 python tools/prof_fused.py 0 > gpurun_out/prof_fused_$TAG.log 2>&1; then

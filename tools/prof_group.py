@@ -1,6 +1,6 @@
-"""Minimal C2 one-layer workload for ncu captures of the group kernel: one lsv_lora_forward over a
-1-layer Llama-2-7B (4 input groups -> 4 group-kernel launches), three times; profile the last
-call's four launches with -k regex:group -s 8 -c 4."""
+"""Minimal C2 one-layer workload for ncu captures: one lsv_lora_forward over a 1-layer Llama-2-7B,
+four times.  Default: one layer-kernel launch per call (profile the last with -k regex:group -s 3
+-c 1); with LSV_LAYER_KERNEL=0 four group-kernel launches per call (-s 12 -c 4)."""
 import sys
 
 import numpy as np
@@ -23,7 +23,7 @@ eng = LoraDeltaEngine(slab)
 bp = eng.prepare(seg)
 xs = [{g: torch.randn(4096, model.projections[m[0]].h_in, device=dev).to(torch.bfloat16) for g, m in eng.groups}]
 ys = [{p.name: torch.zeros(4096, p.h_out, device=dev, dtype=torch.bfloat16) for p in model.projections}]
-for _ in range(3):
+for _ in range(4):
     eng.forward(bp, xs, ys)
 torch.cuda.synchronize()
 print("ok")

@@ -50,18 +50,23 @@ def launches():
              f"#          {CMD}   (after the same command exited 0 without ncu)",
              "# ncu serialises launches and replays with cold caches: absolute times run above the CUDA-graph step;",
              "# the per-kernel SHARE of the step is what to compare.  Full list: "
-             f"profiles/{OUT}_launches{'' if DECODE else '_c2'}_step.csv", "",
+             f"profiles/{OUT}_launches{'' if DECODE else '_c2'}_step.csv",
+             "# (the capture also holds bench.py's serialised-step replay and its roofline calls after the step)", "",
              f"{'kernel':20s} {'launches':>8s} {'total_us':>10s} {'mean_us':>9s} {'share':>7s}"]
     for k, (n, t) in agg.items():
         lines.append(f"{k:20s} {n:8d} {t:10.1f} {t / n:9.2f} {t / total:7.3f}")
     lines += ["", "per layer (first 3 layers of the capture, us):"]
-    grouped = out and out[0][0].endswith("group_tc_kernel")
-    per = 4 if grouped else 8
+    first = out[0][0] if out else ""
+    layered = "group_tc_kernel<4>" in first
+    grouped = not layered and "group_tc_kernel" in first
+    per = 1 if layered else 4 if grouped else 8
     for layer in range(3):
         seg = out[layer * per:(layer + 1) * per]
         parts = []
-        for g in range(4):
-            if grouped:
+        for g in range(1 if layered else 4):
+            if layered:
+                parts.append(f"layer kernel (all four groups) {seg[0][1]:.1f}")
+            elif grouped:
                 parts.append(f"group kernel {GROUPS[g]} {seg[g][1]:.1f}")
             else:
                 parts.append(f"shrink {GROUPS[g]} {seg[2 * g][1]:.1f}")
@@ -124,37 +129,45 @@ def group():
     """The four group kernels of one layer (tools/prof_group.py capture) -> profiles/<OUT>_ncu_group.txt,
     and the mlp_in launch's DRAM bytes into traffic.json (bench.py's group-kernel roofline)."""
     import os
-    rep = f"gpurun_out/group_full_{TAG}.ncu-rep"
-    if not os.path.exists(rep):
-        return
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(raw[raw.index('"ID"'):])))
-    hdr, units, data = rows[0], rows[1], rows[2:]
-    col = {h: i for i, h in enumerate(hdr)}
-    lines = ["# ncu --set full --clock-control none --import-source on -k regex:group -s 8 -c 4 python tools/prof_group.py",
-             "# config 2, one Llama-2-7B layer through lsv_lora_forward: the four group kernels in order (attn_in q/k/v,",
-             "# attn_out o, mlp_in gate/up, mlp_mid down); run only after `python tools/prof_group.py` exited 0 without",
-             "# ncu.  Cold-cache, serialised replay (no PDL overlap between the four).", ""]
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    traffic = []
-    for g, r in enumerate(data):
-        lines.append(f"== group_tc_kernel {GROUPS[g] if g < 4 else g}")
-        for m in METRICS:
-            if m in col:
-                lines.append(f"  {m:60s} {r[col[m]]:>20s} {units[col[m]]}")
-        b = float(r[col["dram__bytes_read.sum"]].replace(",", "")) * mult[units[col["dram__bytes_read.sum"]]] + \
-            float(r[col["dram__bytes_write.sum"]].replace(",", "")) * mult[units[col["dram__bytes_write.sum"]]]
-        lines.append(f"  dram read+write bytes per launch: {b / 1e6:.1f} MB")
-        lines.append("")
-        traffic.append(b)
+    lines, traffic = [], []
+    for rep, hdr_lines, names in (
+            (f"gpurun_out/group_full_{TAG}.ncu-rep",
+             ["# ncu --set full --clock-control none --import-source on -k regex:group -s 3 -c 1 python tools/prof_group.py",
+              "# config 2, one Llama-2-7B layer through lsv_lora_forward: the layer kernel (all four groups, one launch)"],
+             ["layer kernel (attn_in, attn_out, mlp_in, mlp_mid)"]),
+            (f"gpurun_out/group4_full_{TAG}.ncu-rep",
+             ["# LSV_LAYER_KERNEL=0 ncu ... -k regex:group -s 12 -c 4 python tools/prof_group.py: the same layer as four",
+              "# group kernels in order"], GROUPS)):
+        if not os.path.exists(rep):
+            continue
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+        rows = list(csv.reader(io.StringIO(raw[raw.index('"ID"'):])))
+        hdr, units, data = rows[0], rows[1], rows[2:]
+        col = {h: i for i, h in enumerate(hdr)}
+        lines += hdr_lines + ["# run only after `python tools/prof_group.py` exited 0 without ncu.  Cold-cache, serialised.", ""]
+        for g, r in enumerate(data):
+            lines.append(f"== group_tc_kernel {names[g] if g < len(names) else g}")
+            for m in METRICS:
+                if m in col:
+                    lines.append(f"  {m:60s} {r[col[m]]:>20s} {units[col[m]]}")
+            b = float(r[col["dram__bytes_read.sum"]].replace(",", "")) * mult[units[col["dram__bytes_read.sum"]]] + \
+                float(r[col["dram__bytes_write.sum"]].replace(",", "")) * mult[units[col["dram__bytes_write.sum"]]]
+            lines.append(f"  dram read+write bytes per launch: {b / 1e6:.1f} MB")
+            lines.append("")
+            traffic.append((names[g] if g < len(names) else str(g), b))
+    if not lines:
+        return
     open(f"profiles/{OUT}_ncu_group.txt", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
-    if len(traffic) >= 3:
-        tj = json.load(open("profiles/traffic.json"))
+    tj = json.load(open("profiles/traffic.json"))
+    for name, b in traffic:
         for k in tj["c2"]:
-            if k.startswith("group_tc_kernel (mlp_in"):
-                tj["c2"][k] = traffic[2]
-        json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
+            if name.startswith("layer kernel") and k.startswith("group_tc_kernel<4> (layer kernel"):
+                tj["c2"][k] = b
+            if name.startswith("mlp_in") and k.startswith("group_tc_kernel (mlp_in"):
+                tj["c2"][k] = b
+    json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
 
 
 if __name__ == "__main__":
