@@ -123,8 +123,9 @@ def test_stream_prepared_plans_ring_and_staleness():
 def test_decode_groups_simt_ksplit_against_oracle():
     """Decode-shaped batch (1-5 tokens per adapter) through lsv_lora_forward on a full-width
     layer (h = 4096, inter = 11008): the SIMT tier's group shrinks (q/k/v: N = 3r rows in 16-row
-    blocks that straddle members) with several k-splits (2 for h_in 4096, 5 for 11008), and the
-    one-launch multi-member expands, against the oracle for every projection."""
+    blocks that straddle members) with k-splits (48-chunk ranges: 1 for h_in 4096, 3 for 11008),
+    the one-launch multi-member expands, and the four groups on concurrent streams (an overlap-free
+    forward without layer kernels), against the oracle for every projection."""
     from paper_2511_22880_b200.lora import LoraDeltaEngine
     from paper_2511_22880_b200.segments import index_tokens
     from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
