@@ -200,24 +200,32 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
                           const void* const* const* b_ptrs, const void* plan_dev, const void* plan_host,
                           void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
-/* A whole model step for one batch: for every layer l and input group g (in order), the group's
- * fused shrink then its one-launch expand.  plans_* [num_groups] (group plans of the same batch),
- * xs/ldxs [num_layers*num_groups], ys/ldys [num_layers*num_projections] (host arrays of device
- * pointers / row strides; projections numbered group by group), a_ptrs [num_layers*num_groups][S]
- * and b_ptrs [num_layers*num_projections][S] device tables.  Equivalent to the per-group calls,
- * with no per-launch host round trips.  The workspace holds one slice per (layer, group)
- * (lsv_lora_forward_workspace bytes, zero-filled once), so each group's shrink may start while
- * the previous group's expand drains. */
+/* A whole model step for one batch: for every layer l and input group g, the group's fused shrink
+ * and its expand.  plans_* [num_groups] (group plans of the same batch), xs/ldxs
+ * [num_layers*num_groups], ys/ldys [num_layers*num_projections] (host arrays of device pointers /
+ * row strides; projections numbered group by group), a_ptrs [num_layers*num_groups][S] and b_ptrs
+ * [num_layers*num_projections][S] device tables.  Equivalent to the per-group calls (bit-identical
+ * results), with no per-launch host round trips.  The workspace holds one slice per (layer, group)
+ * plus per-m-tile counters (lsv_lora_forward_workspace bytes, zero-filled once; the call zero-fills
+ * the counters itself, ordered on `stream`).  How the work is launched:
+ *   - an overlap-free call (below) whose groups are all tensor-core tier: one launch per layer
+ *     (every group's shrink and expand in one persistent kernel, <= 4 groups);
+ *   - otherwise each tensor-core group is one launch (shrink + expand); SIMT-tier groups are a
+ *     shrink and an expand launch;
+ *   - an overlap-free call without layer launches issues group g of layer l on one of 4 streams
+ *     ((l * num_groups + g) % 4, forked from and joined back into `stream` with events), so
+ *     independent groups (decode batches) run concurrently.  Work queued on `stream` after the call
+ *     is ordered after all of it; a graph capture of `stream` records the fork/join. */
 int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
                      const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
                      void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
                      int32_t num_tokens, void* workspace, size_t workspace_bytes, lsv_stream_t stream);
 
-/* lsv_lora_forward with flags.  By default a group's shrink may start while the previous group's
- * expand drains (it reads nothing that expand writes), which is valid only when every y range of the
- * call is disjoint from every other y range and from every x range; the library checks this and
- * falls back to full serialisation otherwise.  LSV_FWD_SERIAL forces every launch to wait for its
- * predecessor (what a model whose next input depends on the previous output gets). */
+/* lsv_lora_forward with flags.  By default the call is overlap-free: groups run concurrently or
+ * reordered (a group's shrink before the previous group's expand), which is valid only when every
+ * y range of the call is disjoint from every other y range and from every x range; the library
+ * checks this and falls back to full serialisation otherwise.  LSV_FWD_SERIAL forces every group
+ * to wait for its predecessor (what a model whose next input depends on the previous output gets). */
 #define LSV_FWD_SERIAL 1
 int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
                         const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
