@@ -1311,11 +1311,15 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
   // layer (every group of the layer back to back in each CTA)
   bool layer_kernel = g_layer_kernel && overlap_free && num_groups <= kLayerGroups;
   for (int g = 0; g < num_groups; ++g) layer_kernel &= hs[g]->num_tokens > 0 && group_kernel_eligible(hs[g]);
-  // otherwise an overlap-free call spreads its groups over kFwdStreams streams (group g on stream
-  // g % kFwdStreams): independent groups then run concurrently, which the small SIMT-tier launches
-  // of decode batches need to fill the GPU
-  FwdStreams* const fs = (overlap_free && !layer_kernel && g_fwd_streams && num_groups > 1 && num_layers > 0)
-                             ? fwd_streams() : nullptr;
+  // otherwise an overlap-free call whose groups are all SIMT tier (decode batches) spreads its
+  // groups over kFwdStreams streams ((layer, group) round robin): independent groups then run
+  // concurrently, which the small SIMT launches need to fill the GPU.  Never with tensor-core work:
+  // its kernels (the group kernel's readiness waits, the standalone shrink's grid barrier) need
+  // every CTA of the grid co-resident, which two concurrent 148-CTA grids could not guarantee.
+  bool all_simt = true;
+  for (int g = 0; g < num_groups; ++g) all_simt &= hs[g]->n_mtiles == 0;
+  FwdStreams* const fs = (overlap_free && !layer_kernel && all_simt && g_fwd_streams && num_groups > 1 &&
+                          num_layers > 0) ? fwd_streams() : nullptr;
   if (fs != nullptr) {
     LSV_CUDA_CHECK(cudaEventRecord(fs->fork, st));
     for (int i = 0; i < kFwdStreams - 1; ++i) LSV_CUDA_CHECK(cudaStreamWaitEvent(fs->s[i], fs->fork, 0));

@@ -1156,7 +1156,8 @@ struct alignas(64) GroupParams {
   int* split_done;     // [n_mtiles]
   int s_grid, e_grid;  // CTAs with shrink records / expand items
   int wait_prev;       // 1: griddepcontrol.wait first (the previous launch may touch our buffers)
-  uint64_t* tl;        // development timeline (nullptr = off): [cta][4] = {entry, setup done, exit, SM id}
+  uint64_t* tl;        // development timeline (nullptr = off): [cta][16] = {entry, setup done, exit, SM id,
+                       // end of phase i (epilogue warp 0) at 4 + i}
 };
 // A layer kernel runs NG input groups back to back in every CTA (lsv_lora_forward, overlap-free
 // calls): the groups' parameters travel together as kernel parameters (4 groups: ~26 KB).
@@ -1286,8 +1287,8 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   if (gp.tl != nullptr && threadIdx.x == 0) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    gp.tl[cta * 4 + 0] = globaltimer_ns();
-    gp.tl[cta * 4 + 3] = smid;
+    gp.tl[cta * 16 + 0] = globaltimer_ns();
+    gp.tl[cta * 16 + 3] = smid;
   }
   for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {   // identity A tile (expand y add)
     const int t = i / 16, k = i % 16;
@@ -1314,7 +1315,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) phase_stamp(sp.trace, sp.trace_items, cta, 0);
-  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 4 + 1] = globaltimer_ns();
+  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 16 + 1] = globaltimer_ns();
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
   const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty};
@@ -1394,6 +1395,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
       if (!ex && cta < G.s_grid) shrink_epilogue(G.s, ssw, tmem_base, cta, warp, lane, recdone, st);
       if (ex && cta < G.e_grid) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
       if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, ex ? 4 : 1);   // phase stored
+      if (gp.tl != nullptr && warp == 0 && lane == 0 && i < 12) gp.tl[cta * 16 + 4 + i] = globaltimer_ns();
     }
   } else if (warp == 4) {
     int rec_base = 0, item_base = 0;
@@ -1416,7 +1418,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   tc_fence_before();
   __syncthreads();
   if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
-  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 4 + 2] = globaltimer_ns();
+  if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 16 + 2] = globaltimer_ns();
 }
 
 }  // namespace lsv

@@ -33,7 +33,7 @@ for _ in range(3):
     eng.forward(bp, xs, ys)
 torch.cuda.synchronize()
 n = 4 * L
-buf = torch.zeros(n * 148 * 4, dtype=torch.int64, device=dev)
+buf = torch.zeros(n * 148 * 16, dtype=torch.int64, device=dev)
 lib = native.lib()
 lib.lsv_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 lib.lsv_debug_set_trace(buf.data_ptr(), -n)
@@ -43,7 +43,7 @@ eng.forward(bp, xs, ys)
 e1.record()
 torch.cuda.synchronize()
 lib.lsv_debug_set_trace(None, 0)
-tl = buf.view(n, 148, 4).cpu().numpy().astype(np.int64)
+tl = buf.view(n, 148, 16).cpu().numpy().astype(np.int64)
 n = int((tl[:, :, 0].max(axis=1) > 0).sum())   # launches recorded: 4L group kernels or L layer kernels
 tl = tl[:n]
 t0 = tl[:, :, 0][tl[:, :, 0] > 0].min()
@@ -70,3 +70,17 @@ for sm in range(148):
 gaps = np.array(gaps)
 print(f"exit -> next entry on the same SM: mean {gaps.mean():.2f} us, p50 {np.median(gaps):.2f}, p90 {np.percentile(gaps, 90):.2f}; "
       f"SM time past setup / span: {busy / (148 * span) * 100:.1f}%")
+
+if kind == "layer kernels":   # phase ends inside each layer kernel (epilogue warp 0 of every CTA)
+    order = ["S0 attn_in", "S1 attn_out", "E0 attn_in", "S2 mlp_in", "E1 attn_out", "S3 mlp_mid", "E2 mlp_in", "E3 mlp_mid"]
+    for i in range(min(n, 2)):
+        ent = tl[i, :, 1]
+        print(f"layer kernel {i}: phase end, us after the CTA's setup (p10 / p50 / max over CTAs)")
+        prev = ent
+        for ph in range(8):
+            e = tl[i, :, 4 + ph]
+            d = (e - ent) / 1e3
+            dur = (e - prev) / 1e3
+            print(f"  {order[ph]:12s} end {np.percentile(d, 10):7.1f} {np.median(d):7.1f} {d.max():7.1f}   "
+                  f"phase length p50 {np.median(dur):6.1f}")
+            prev = e
