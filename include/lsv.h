@@ -215,7 +215,12 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
  *   - an overlap-free call without layer launches issues group g of layer l on one of 4 streams
  *     ((l * num_groups + g) % 4, forked from and joined back into `stream` with events), so
  *     independent groups (decode batches) run concurrently.  Work queued on `stream` after the call
- *     is ordered after all of it; a graph capture of `stream` records the fork/join. */
+ *     is ordered after all of it; a graph capture of `stream` records the fork/join.
+ * Tensor-core launches (group / layer kernels, the standalone shrink's split-K grid barrier) wait
+ * on other CTAs of their own grid, so their grid (at most one CTA per SM) must become co-resident:
+ * kernels of other streams may delay them but must not wait on them.  Two lsv calls on different
+ * streams of one GPU therefore need disjoint SM budgets (LSV_PLAN_SMS in the plans), as
+ * SplitStep does. */
 int lsv_lora_forward(int32_t num_layers, int32_t num_groups, const void* const* plans_dev,
                      const void* const* plans_host, const void* const* xs, const int64_t* ldxs,
                      void* const* ys, const int64_t* ldys, const void* a_ptrs, const void* b_ptrs,
