@@ -462,52 +462,53 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
   uint64_t* empty = sm.empty;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
-    // values stay in uniform registers, so each MMA costs a few uniform adds), one lane issues
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
-    ShrinkRec inf;
-    const uint8_t* unused;
-    int slot = st.s_slot; uint32_t phase = st.s_phase;
-    int dbg_stage = 0;
-    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
-    const int nbuf = kTmemCols / p.acc_cols;
-    int k = 0;
-    for (; rs.pop(inf, unused); ++k) {
-      const int rows = __shfl_sync(0xffffffffu, inf.rank * inf.np, 0);
-      const int np8 = round_up(__shfl_sync(0xffffffffu, inf.ntok, 0), 8);
-      const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
-      const int cb = __shfl_sync(0xffffffffu, inf.chunk_begin, 0), ce = __shfl_sync(0xffffffffu, inf.chunk_end, 0);
-      const int buf = k % nbuf;
-      mbar_wait(&tempty[buf], ((st.s_tbits >> buf) & 1) ^ 1);
+  // the whole warp runs the loop (warp-uniform values stay in uniform registers, so each MMA costs a
+  // few uniform adds); an elected lane issues
+  WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ShrinkRec inf;
+  const uint8_t* unused;
+  int slot = st.s_slot; uint32_t phase = st.s_phase;
+  int dbg_stage = 0;
+  const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+  const int nbuf = kTmemCols / p.acc_cols;
+  int k = 0;
+  for (; rs.pop(inf, unused); ++k) {
+    const int rows = __shfl_sync(0xffffffffu, inf.rank * inf.np, 0);
+    const int np8 = round_up(__shfl_sync(0xffffffffu, inf.ntok, 0), 8);
+    const int kch = __shfl_sync(0xffffffffu, inf.kch, 0);
+    const int cb = __shfl_sync(0xffffffffu, inf.chunk_begin, 0), ce = __shfl_sync(0xffffffffu, inf.chunk_end, 0);
+    const int buf = k % nbuf;
+    mbar_wait(&tempty[buf], ((st.s_tbits >> buf) & 1) ^ 1);
+    tc_fence_after();
+    const uint32_t d = tmem_base + buf * p.acc_cols;
+    const uint32_t idesc = idesc_bf16(128, max(16, round_up(rows, 16)));
+    const uint32_t xstep = (uint32_t)(np8 * 128) >> 4, astep = (uint32_t)(rows * 128) >> 4;  // per chunk, desc units
+    uint32_t accumulate = 0;
+    for (int g = cb; g < ce; g += kch) {
+      const int kc = min(kch, ce - g);
+      if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage, 6);
+      mbar_wait(&full[slot], phase);
       tc_fence_after();
-      const uint32_t d = tmem_base + buf * p.acc_cols;
-      const uint32_t idesc = idesc_bf16(128, max(16, round_up(rows, 16)));
-      const uint32_t xstep = (uint32_t)(np8 * 128) >> 4, astep = (uint32_t)(rows * 128) >> 4;  // per chunk, desc units
-      uint32_t accumulate = 0;
-      for (int g = cb; g < ce; g += kch) {
-        const int kc = min(kch, ce - g);
-        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage, 6);
-        mbar_wait(&full[slot], phase);
-        tc_fence_after();
-        if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage++, 7);
-        const uint32_t xb = ring_base + slot * kShrinkSlotBytes;
-        uint64_t adesc = smem_desc(xb, 16, 1024, 2);
-        uint64_t bdesc = smem_desc(xb + kc * np8 * 128, 16, 1024, 2);
-        for (int c = 0; c < kc; ++c) {
+      if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage++, 7);
+      const uint32_t xb = ring_base + slot * kShrinkSlotBytes;
+      uint64_t adesc = smem_desc(xb, 16, 1024, 2);
+      uint64_t bdesc = smem_desc(xb + kc * np8 * 128, 16, 1024, 2);
+      for (int c = 0; c < kc; ++c) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {   // K=16 steps inside the 128-byte swizzle row: +32 B = +2
-            umma_bf16_elect(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
-            accumulate = 1;
-          }
-          adesc += xstep;
-          bdesc += astep;
+        for (int kk = 0; kk < 4; ++kk) {   // K=16 steps inside the 128-byte swizzle row: +32 B = +2
+          umma_bf16_elect(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, accumulate);
+          accumulate = 1;
         }
-        umma_commit_elect(&empty[slot]);
-        if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
+        adesc += xstep;
+        bdesc += astep;
       }
-      umma_commit_elect(&tfull[buf]);
-      st.s_tbits ^= 1u << buf;
-      if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
+      umma_commit_elect(&empty[slot]);
+      if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
     }
+    umma_commit_elect(&tfull[buf]);
+    st.s_tbits ^= 1u << buf;
+    if (!(p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 2);
+  }
   st.s_slot = slot;
   st.s_phase = phase;
   return k;
@@ -521,91 +522,91 @@ __device__ __forceinline__ void shrink_epilogue(const ShrinkParams& p, const Shr
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
-    const int q = warp & 3, row = q * 32 + lane;
-    float* partials = reinterpret_cast<float*>(p.ws + p.ws_partials);
-    WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
-    ShrinkRec inf;
-    const uint8_t* unused;
-    const int nbuf = kTmemCols / p.acc_cols;
-    int k = 0;
-    for (; rs.pop(inf, unused); ++k) {
-      const int r = inf.rank, nt = inf.ntok, kp = kpad(r), np16 = round_up(nt, 16);
-      const int G = p.num_proj * r, rows = inf.np * r;
-      const int buf = k % nbuf;
-      mbar_wait(&tfull[buf], (st.s_tbits >> buf) & 1);
-      st.s_tbits ^= 1u << buf;
-      tc_fence_after();
-      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
-      const bool valid = row < nt && !(p.dbg & 8);
-      uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
-      // tile-aligned images (fused base GEMM): 128 rows, this piece at rows tok_begin % 128 + row,
-      // every other row zero; each thread writes image row (tok_begin + row) % 128, zeros if !valid
-      const bool ta = p.tile_aligned != 0;
-      const int irow = ta ? ((inf.tok_begin + row) & (kTileM - 1)) : row, rpad = ta ? kTileM : np16;
-      const bool wimg = ta ? !(p.dbg & 8) : valid;              // writes an image row (nsplit == 1)
-      const uint32_t vlo = vimg_bytes(rpad, kp);                // hi image -> lo image (split v)
-      LSV_DCHECK(p.tp > 0 || (int64_t)p.ws_vimg + (int64_t)(p.num_proj - 1) * p.vimg_stride + inf.vimg_off +
-                                   (int64_t)vlo * (p.vsplit ? 2 : 1) <= p.ws_bytes);
-      LSV_DCHECK(inf.nsplit == 1 || (int64_t)p.ws_partials + 4 * ((int64_t)inf.part_off +
-                                   (int64_t)inf.nsplit * nt * G) <= p.ws_bytes);
-      float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
-      for (int cc = 0; cc < rows; cc += 16) {
-        float v[16];
-        tmem_ld_32x32b_x16(taddr + cc, v);
-        if (valid || (wimg && inf.nsplit == 1)) {
+  const int q = warp & 3, row = q * 32 + lane;
+  float* partials = reinterpret_cast<float*>(p.ws + p.ws_partials);
+  WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ShrinkRec inf;
+  const uint8_t* unused;
+  const int nbuf = kTmemCols / p.acc_cols;
+  int k = 0;
+  for (; rs.pop(inf, unused); ++k) {
+    const int r = inf.rank, nt = inf.ntok, kp = kpad(r), np16 = round_up(nt, 16);
+    const int G = p.num_proj * r, rows = inf.np * r;
+    const int buf = k % nbuf;
+    mbar_wait(&tfull[buf], (st.s_tbits >> buf) & 1);
+    st.s_tbits ^= 1u << buf;
+    tc_fence_after();
+    if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
+    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.acc_cols;
+    const bool valid = row < nt && !(p.dbg & 8);
+    uint8_t* vimg = p.ws + p.ws_vimg + inf.vimg_off;          // + projection * vimg_stride
+    // tile-aligned images (fused base GEMM): 128 rows, this piece at rows tok_begin % 128 + row,
+    // every other row zero; each thread writes image row (tok_begin + row) % 128, zeros if !valid
+    const bool ta = p.tile_aligned != 0;
+    const int irow = ta ? ((inf.tok_begin + row) & (kTileM - 1)) : row, rpad = ta ? kTileM : np16;
+    const bool wimg = ta ? !(p.dbg & 8) : valid;              // writes an image row (nsplit == 1)
+    const uint32_t vlo = vimg_bytes(rpad, kp);                // hi image -> lo image (split v)
+    LSV_DCHECK(p.tp > 0 || (int64_t)p.ws_vimg + (int64_t)(p.num_proj - 1) * p.vimg_stride + inf.vimg_off +
+                                 (int64_t)vlo * (p.vsplit ? 2 : 1) <= p.ws_bytes);
+    LSV_DCHECK(inf.nsplit == 1 || (int64_t)p.ws_partials + 4 * ((int64_t)inf.part_off +
+                                 (int64_t)inf.nsplit * nt * G) <= p.ws_bytes);
+    float* part = partials + inf.part_off + ((size_t)inf.split * nt + row) * G + inf.p0 * r;
+    for (int cc = 0; cc < rows; cc += 16) {
+      float v[16];
+      tmem_ld_32x32b_x16(taddr + cc, v);
+      if (valid || (wimg && inf.nsplit == 1)) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j0 = cc + h * 8;          // 8 columns, all of projection p0 + j0 / r (r % 8 == 0)
-            if (j0 < rows) {
-              if (inf.nsplit == 1) {
-                uint4 w, wlo;
-                split_bf16x8(v + h * 8, w, wlo);
-                if (!valid) w = wlo = make_uint4(0, 0, 0, 0);   // tile-aligned zero row
-                const int pp = inf.p0 + j0 / r;
-                if (p.tp > 0 && p.tp_row) tp_row_put(p, inf.mtile, pp, row, j0 % r, v + h * 8);
-                else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w, wlo);
-                else {
-                  uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, j0 % r, kp, rpad);
-                  *reinterpret_cast<uint4*>(dst) = w;
-                  if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = wlo;
-                }
+        for (int h = 0; h < 2; ++h) {
+          const int j0 = cc + h * 8;          // 8 columns, all of projection p0 + j0 / r (r % 8 == 0)
+          if (j0 < rows) {
+            if (inf.nsplit == 1) {
+              uint4 w, wlo;
+              split_bf16x8(v + h * 8, w, wlo);
+              if (!valid) w = wlo = make_uint4(0, 0, 0, 0);   // tile-aligned zero row
+              const int pp = inf.p0 + j0 / r;
+              if (p.tp > 0 && p.tp_row) tp_row_put(p, inf.mtile, pp, row, j0 % r, v + h * 8);
+              else if (p.tp > 0) tp_scatter(p, inf.mtile, pp, row, j0 % r, r, np16, w, wlo);
+              else {
+                uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, j0 % r, kp, rpad);
+                *reinterpret_cast<uint4*>(dst) = w;
+                if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = wlo;
+              }
+            } else {
+              float* dst = part + j0;
+              if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {   // one full sector per row
+                st_global_v8_if(dst, reinterpret_cast<const uint32_t*>(v + h * 8), true);
               } else {
-                float* dst = part + j0;
-                if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {   // one full sector per row
-                  st_global_v8_if(dst, reinterpret_cast<const uint32_t*>(v + h * 8), true);
-                } else {
-                  reinterpret_cast<float4*>(dst)[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
-                  reinterpret_cast<float4*>(dst)[1] = make_float4(v[h * 8 + 4], v[h * 8 + 5], v[h * 8 + 6], v[h * 8 + 7]);
-                }
+                reinterpret_cast<float4*>(dst)[0] = make_float4(v[h * 8 + 0], v[h * 8 + 1], v[h * 8 + 2], v[h * 8 + 3]);
+                reinterpret_cast<float4*>(dst)[1] = make_float4(v[h * 8 + 4], v[h * 8 + 5], v[h * 8 + 6], v[h * 8 + 7]);
               }
             }
           }
         }
       }
-      if (valid && inf.nsplit == 1 && p.tp > 0) {
-        if (!p.tp_row)
-          for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
-      } else if (wimg && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
-        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) {
-          uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, r, kp, rpad);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-          if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = make_uint4(0, 0, 0, 0);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (recdone != nullptr && lane == 0) {   // group kernel: stored (the signal warp is < kRecQ behind)
-        const volatile int* sigc = reinterpret_cast<const volatile int*>(recdone + kRecQ);
-        const int kg = st.s_rec + k;   // record index over every group this CTA has run
-        while (kg >= kRecQ && *sigc <= kg - kRecQ) __nanosleep(32);
-        mbar_arrive(&recdone[kg % kRecQ]);
-      }
-      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
-      if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
     }
-    st.s_rec += k;
+    if (valid && inf.nsplit == 1 && p.tp > 0) {
+      if (!p.tp_row)
+        for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) tp_scatter_pad(p, inf.mtile, pp, row, np16);
+    } else if (wimg && inf.nsplit == 1 && kp != r) {   // the k pad of each v image (r % 16 == 8) is zero
+      for (int pp = inf.p0; pp < inf.p0 + inf.np; ++pp) {
+        uint8_t* dst = vimg + (size_t)pp * p.vimg_stride + vimg_off(irow, r, kp, rpad);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+        if (p.vsplit) *reinterpret_cast<uint4*>(dst + vlo) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[buf]);
+    if (recdone != nullptr && lane == 0) {   // group kernel: stored (the signal warp is < kRecQ behind)
+      const volatile int* sigc = reinterpret_cast<const volatile int*>(recdone + kRecQ);
+      const int kg = st.s_rec + k;   // record index over every group this CTA has run
+      while (kg >= kRecQ && *sigc <= kg - kRecQ) __nanosleep(32);
+      mbar_arrive(&recdone[kg % kRecQ]);
+    }
+    if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+    if (!(p.dbg & 16) && q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 5);
+  }
+  st.s_rec += k;
   }
 
 __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ ShrinkParams p) {
@@ -621,10 +622,10 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
-    fence_mbar_init();
-    for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
+  for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
+  for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+  fence_mbar_init();
+  for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
   }
   if (warp == kShrMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
@@ -640,11 +641,11 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane, 0, kProdParts);
   else if (warp == kProdWarp2 && kProdParts == 2) shrink_producer(p, sm, cta, warp, lane, 1, kProdParts);
   else if (warp == kShrMmaWarp) {
-    PipeState st;
-    shrink_mma(p, sm, tmem_base, cta, warp, lane, st);
+  PipeState st;
+  shrink_mma(p, sm, tmem_base, cta, warp, lane, st);
   } else if (shrink_epi_warp(warp)) {
-    PipeState st;
-    shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr, st);
+  PipeState st;
+  shrink_epilogue(p, sm, tmem_base, cta, warp, lane, nullptr, st);
   }
   // CTA c owns split-K reduce units [c*U/G, (c+1)*U/G) of the concatenated split tiles; the host
   // recorded the table entry holding its first unit.  Each thread resolves its first two units
@@ -655,8 +656,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   const int ua = u0 + threadIdx.x, ub = ua + blockDim.x;
   RedUnit ra{}, rb{};
   if (p.n_red > 0 && ua < u1) {
-    ra = red_unit(p, ua, p.plan[p.off_red_cta + blockIdx.x]);
-    if (ub < u1) rb = red_unit(p, ub, ra.e);
+  ra = red_unit(p, ua, p.plan[p.off_red_cta + blockIdx.x]);
+  if (ub < u1) rb = red_unit(p, ub, ra.e);
   }
   tc_fence_before();
   __threadfence();             // partials visible device-wide before the grid barrier
@@ -665,8 +666,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == kShrMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   if (p.n_red == 0) {
-    if (p.tp > 0) tp_signal(p);
-    return;
+  if (p.tp > 0) tp_signal(p);
+  return;
   }
 
   // ---- grid-wide split-K reduction (all CTAs are co-resident: grid <= SMs, 1 CTA per SM) ----
@@ -674,45 +675,45 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   // order by one thread, so results are bit-identical from run to run.
   int* bar = p.gbar;
   if (threadIdx.x == 0) {
-    atomicAdd(&bar[0], 1);
-    int seen = 0;
-    uint64_t t0 = 0;
-    for (uint32_t spin = 0;; ++spin) {
-      seen = ld_relaxed_gpu(&bar[0]);
-      if (seen >= (int)gridDim.x) { (void)ld_acquire_gpu(&bar[0]); break; }
-      __nanosleep(64);
-      if ((spin & 1023u) == 1023u) {   // bounded: trap after ~4 s instead of hanging the GPU
-        const uint64_t now = globaltimer_ns();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > 4000000000ull) __trap();
-      }
+  atomicAdd(&bar[0], 1);
+  int seen = 0;
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    seen = ld_relaxed_gpu(&bar[0]);
+    if (seen >= (int)gridDim.x) { (void)ld_acquire_gpu(&bar[0]); break; }
+    __nanosleep(64);
+    if ((spin & 1023u) == 1023u) {   // bounded: trap after ~4 s instead of hanging the GPU
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
     }
+  }
   }
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 4);
   if (ua < u1) {
-    float sa[8], sb[8];
-    red_sum(p, ra, sa);                  // both units' loads in flight before either store
-    if (ub < u1) red_sum(p, rb, sb);
-    red_store(p, ra, sa);
-    if (ub < u1) red_store(p, rb, sb);
-    int e = ub < u1 ? rb.e : ra.e;
-    for (int u = ub + blockDim.x; u < u1; u += blockDim.x) {
-      const RedUnit ru = red_unit(p, u, e);
-      e = ru.e;
-      float s8[8];
-      red_sum(p, ru, s8);
-      red_store(p, ru, s8);
-    }
+  float sa[8], sb[8];
+  red_sum(p, ra, sa);                  // both units' loads in flight before either store
+  if (ub < u1) red_sum(p, rb, sb);
+  red_store(p, ra, sa);
+  if (ub < u1) red_store(p, rb, sb);
+  int e = ub < u1 ? rb.e : ra.e;
+  for (int u = ub + blockDim.x; u < u1; u += blockDim.x) {
+    const RedUnit ru = red_unit(p, u, e);
+    e = ru.e;
+    float s8[8];
+    red_sum(p, ru, s8);
+    red_store(p, ru, s8);
+  }
   }
   if (p.tp > 0) __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 5);
   if (threadIdx.x == 0 && atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) {
-    bar[0] = 0;                // every CTA is past the barrier: re-arm it for the next launch
-    bar[1] = 0;
-    if (p.tp > 0)              // the last CTA out: every rank's copy of this group is complete
-      for (int d = 0; d < p.tp; ++d) red_release_sys_add(p.flags[d], 1);
+  bar[0] = 0;                // every CTA is past the barrier: re-arm it for the next launch
+  bar[1] = 0;
+  if (p.tp > 0)              // the last CTA out: every rank's copy of this group is complete
+    for (int d = 0; d < p.tp; ++d) red_release_sys_add(p.flags[d], 1);
   }
 }
 
@@ -798,88 +799,88 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
   uint32_t* offs = sm.offs;
   uint64_t* full = sm.full;
   uint64_t* empty = sm.empty;
-    // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
-    // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
-    // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
-    ExpandRec inf;
-    const uint8_t* b;
-    uint32_t head = 0, tail = 0;   // ring bytes (the ring is empty when an expand phase starts)
-    uint32_t vbegin[kItemQ];
-    const int k0 = st.e_item;      // allocations before this phase are all retired
-    int retired = k0;
-    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
-    int k = k0;
-    for (; rs.pop(inf, b); ++k) {
-      const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
-      const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
-      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
-      const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2 + (p.vsplit ? vlo : 0), ybytes = nb * np16 * 128;
-      const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
-      const uint32_t size = yoff + ybytes;
-      const int qs = k % kItemQ;
-      const uint32_t extent =
-          max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
-      head = round_up(head, 1024);
-      if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
-        head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
-      LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
-      LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
-      LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
-      LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
-      const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
-      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 0);
-      while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
-        mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
-        ++retired;
-        tail = retired < k ? vbegin[retired % kItemQ] : head;
-      }
-      vbegin[qs] = head;
-      const uint32_t ring_off = head % kExpandRingBytes;
-      if (stamp) offs[qs] = ring_off;
-      head += size;
-      const int dbg = p.dbg;
-      const uint32_t fb = smem_u32(&full[qs]);
-      mbar_arrive_expect_tx_elect(fb, (p0 ? ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) : 0u) +
-                                          (do_y ? ((dbg & 8) ? 0 : ybytes) : 0u));
-      if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 1);
-      const uint32_t dst = ring_base + ring_off;
-      if (p0 && !(dbg & 16)) {
-        if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group
-          const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
-          const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
-          for (int kg = 0; kg < kp / 8; ++kg)
-            bulk_load_elect(dst + kg * nb * 1024, src + (size_t)kg * (twl / 64) * 1024, (uint32_t)(nb * 1024), fb);
-        } else {
-          bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
-        }
-      }
-      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 3);
-      if (do_y && !(dbg & 8)) {
-        // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
-        // [nb blocks][R rows][64] at yoff + row * nb * 128
-        const CUtensorMap* ym = nb == 4 ? p.ymap[inf.proj] : p.ymap2[inf.proj];
-        int mm = np16 >> 3, row = 0;
-        while (mm) {
-          const int bbit = 31 - __clz(mm);
-          tma_load_3d_elect(dst + yoff + row * nb * 128, &ym[bbit], fb, 0, inf.tok_begin + row, inf.jtile * nb);
-          row += 8 << bbit;
-          mm &= ~(1 << bbit);
-        }
-      }
-      if (p0 && vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
-        if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 5);
-        mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
-        if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 6);
-        if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
-      }
-      if (p0 && !(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
-      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 4);
-      __syncwarp();
+  // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
+  // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
+  // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
+  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
+  ExpandRec inf;
+  const uint8_t* b;
+  uint32_t head = 0, tail = 0;   // ring bytes (the ring is empty when an expand phase starts)
+  uint32_t vbegin[kItemQ];
+  const int k0 = st.e_item;      // allocations before this phase are all retired
+  int retired = k0;
+  const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+  int k = k0;
+  for (; rs.pop(inf, b); ++k) {
+    const int twl = p.tws[inf.proj], tw = expand_item_tw(inf.rank, twl), nb = tw / 64;
+    const int kp = kpad(inf.rank), np16 = round_up(inf.ntok, 16), S = kmajor_row_bytes(kp);
+    const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+    const uint32_t bbytes = tw * kp * 2, vbytes = np16 * kp * 2 + (p.vsplit ? vlo : 0), ybytes = nb * np16 * 128;
+    const uint32_t voff = round_up(bbytes, 1024), yoff = round_up(voff + vbytes, 1024);
+    const uint32_t size = yoff + ybytes;
+    const int qs = k % kItemQ;
+    const uint32_t extent =
+        max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
+    head = round_up(head, 1024);
+    if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
+      head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
+    LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
+    LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
+    LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
+    LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
+    const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
+    if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 0);
+    while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
+      mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
+      ++retired;
+      tail = retired < k ? vbegin[retired % kItemQ] : head;
     }
-    if (drain)   // the next group's shrink reuses the ring bytes: wait until every item's MMAs read them
-      for (; retired < k; ++retired) mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
-    st.e_item = k;
+    vbegin[qs] = head;
+    const uint32_t ring_off = head % kExpandRingBytes;
+    if (stamp) offs[qs] = ring_off;
+    head += size;
+    const int dbg = p.dbg;
+    const uint32_t fb = smem_u32(&full[qs]);
+    mbar_arrive_expect_tx_elect(fb, (p0 ? ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) : 0u) +
+                                        (do_y ? ((dbg & 8) ? 0 : ybytes) : 0u));
+    if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 1);
+    const uint32_t dst = ring_base + ring_off;
+    if (p0 && !(dbg & 16)) {
+      if (tw < twl) {   // a 128-wide half of a 256-wide layout tile: 2 KB per 8-k group
+        const int halves = twl / tw, jt = inf.jtile / halves, sub = inf.jtile % halves;
+        const uint8_t* src = b + (size_t)jt * twl * kp * 2 + sub * nb * 1024;
+        for (int kg = 0; kg < kp / 8; ++kg)
+          bulk_load_elect(dst + kg * nb * 1024, src + (size_t)kg * (twl / 64) * 1024, (uint32_t)(nb * 1024), fb);
+      } else {
+        bulk_load_elect(dst, b + (size_t)inf.jtile * bbytes, bbytes, fb);
+      }
+    }
+    if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 3);
+    if (do_y && !(dbg & 8)) {
+      // y rows [tok_begin, +np16): one 3D box per set bit of np16 / 8 (largest first), each
+      // [nb blocks][R rows][64] at yoff + row * nb * 128
+      const CUtensorMap* ym = nb == 4 ? p.ymap[inf.proj] : p.ymap2[inf.proj];
+      int mm = np16 >> 3, row = 0;
+      while (mm) {
+        const int bbit = 31 - __clz(mm);
+        tma_load_3d_elect(dst + yoff + row * nb * 128, &ym[bbit], fb, 0, inf.tok_begin + row, inf.jtile * nb);
+        row += 8 << bbit;
+        mm &= ~(1 << bbit);
+      }
+    }
+    if (p0 && vfull != nullptr) {   // group kernel: the tile's v images are complete (ready checker warp)
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 5);
+      mbar_wait(&vfull[k % kVQ], (k / kVQ) & 1);
+      if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 6);
+      if (lane == 0) mbar_arrive(&vempty[k % kVQ]);
+    }
+    if (p0 && !(dbg & 32)) bulk_load_elect(dst + voff, p.ws + p.ws_vimg[inf.proj] + inf.vimg_off, vbytes, fb);
+    if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 4);
+    __syncwarp();
+  }
+  if (drain)   // the next group's shrink reuses the ring bytes: wait until every item's MMAs read them
+    for (; retired < k; ++retired) mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
+  st.e_item = k;
 }
 // MMA issuer (whole warp): the election happens inside the MMA asm, so ptxas emits no per-MMA
 // uniformization loop; descriptors advance by constant steps (start address field = byte
@@ -894,79 +895,79 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
   uint64_t* empty = sm.empty;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
-    const int nbuf = kTmemCols / p.tw_max;     // TMEM accumulators in flight
-    // Every lane runs the loop and computes the same descriptors; the election happens inside the
-    // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
-    // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
-    ExpandRec inf;
-    const uint8_t* unused;
-    const uint32_t ib = smem_u32(ident);
-    const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
-    const int k0 = st.e_item;
-    int k = k0;
-    for (; rs.pop(inf, unused); ++k) {
-      const int r = inf.rank;
-      const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
-      const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
-      const int qs = k % kItemQ;
-      const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
-      const int S = kmajor_row_bytes(kp), ck = S / 2;
-      const uint32_t vlay = umma_layout(S);
-      const int buf = (k - k0) % nbuf;
-      mbar_wait(&tempty[buf], ((st.e_tbits >> buf) & 1) ^ 1);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 5);
-      mbar_wait(&full[qs], (k / kItemQ) & 1);
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 6);
-      tc_fence_after();
-      const uint32_t bb = ring_base + offs[qs];
-      const uint32_t voff = round_up(tw * kp * 2, 1024);
-      const uint32_t vb = bb + voff;
-      const uint32_t vlo = vimg_bytes(inf.ntok, kp);
-      const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
-      const uint32_t d = tmem_base + buf * p.tw_max;
-      const int qrow = 32 * expand_qbase(k - k0, inf.ntok);
-      const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
-      // D = v . B (+ v_lo . B): A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128).
-      // K step ks: A advances 32 B inside a swizzle row, np16 rows of S bytes per ck-element chunk;
-      // B advances one 2 * nb KB group of 16 k.
-      const uint64_t a0 = smem_desc(vb - qrow * S, 16, 8 * S, vlay);
-      const uint64_t b0 = smem_desc(bb, 1024, nb * 1024, 2);
-      const uint32_t bstep = (2 * nb * 1024) >> 4, cstep = (np16 * S) >> 4;
-      for (int h = 0; h < (p.vsplit ? 2 : 1); ++h) {
-        uint64_t arow = a0 + (h ? (vlo >> 4) : 0u), bd = b0;
-        for (int ks = 0; ks < nv; ++ks) {
-          const uint32_t in_row = (uint32_t)((ks * 16) % ck) * 2 >> 4;
-          umma_bf16_elect(d, arow + in_row, bd, idesc_mn, (h | ks) ? 1u : 0u);
-          bd += bstep;
-          if (((ks + 1) * 16) % ck == 0) arow += cstep;
-        }
+  const int nbuf = kTmemCols / p.tw_max;     // TMEM accumulators in flight
+  // Every lane runs the loop and computes the same descriptors; the election happens inside the
+  // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
+  // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
+  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ExpandRec inf;
+  const uint8_t* unused;
+  const uint32_t ib = smem_u32(ident);
+  const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
+  const int k0 = st.e_item;
+  int k = k0;
+  for (; rs.pop(inf, unused); ++k) {
+    const int r = inf.rank;
+    const int tw = expand_item_tw(r, p.tws[inf.proj]), nb = tw / 64;
+    const uint32_t idesc_mn = idesc_bf16(128, tw, 1);
+    const int qs = k % kItemQ;
+    const int kp = kpad(r), np16 = round_up(inf.ntok, 16);
+    const int S = kmajor_row_bytes(kp), ck = S / 2;
+    const uint32_t vlay = umma_layout(S);
+    const int buf = (k - k0) % nbuf;
+    mbar_wait(&tempty[buf], ((st.e_tbits >> buf) & 1) ^ 1);
+    if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 5);
+    mbar_wait(&full[qs], (k / kItemQ) & 1);
+    if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 6);
+    tc_fence_after();
+    const uint32_t bb = ring_base + offs[qs];
+    const uint32_t voff = round_up(tw * kp * 2, 1024);
+    const uint32_t vb = bb + voff;
+    const uint32_t vlo = vimg_bytes(inf.ntok, kp);
+    const uint32_t yb = bb + round_up(voff + np16 * kp * 2 + (p.vsplit ? vlo : 0u), 1024);
+    const uint32_t d = tmem_base + buf * p.tw_max;
+    const int qrow = 32 * expand_qbase(k - k0, inf.ntok);
+    const int nv = (p.dbg & 128) ? 1 : kp / 16, ny = (p.dbg & 64) ? 0 : np16 / 16;
+    // D = v . B (+ v_lo . B): A = v image (K-major, swizzled by kp), B = B tile (MN-major SW128).
+    // K step ks: A advances 32 B inside a swizzle row, np16 rows of S bytes per ck-element chunk;
+    // B advances one 2 * nb KB group of 16 k.
+    const uint64_t a0 = smem_desc(vb - qrow * S, 16, 8 * S, vlay);
+    const uint64_t b0 = smem_desc(bb, 1024, nb * 1024, 2);
+    const uint32_t bstep = (2 * nb * 1024) >> 4, cstep = (np16 * S) >> 4;
+    for (int h = 0; h < (p.vsplit ? 2 : 1); ++h) {
+      uint64_t arow = a0 + (h ? (vlo >> 4) : 0u), bd = b0;
+      for (int ks = 0; ks < nv; ++ks) {
+        const uint32_t in_row = (uint32_t)((ks * 16) % ck) * 2 >> 4;
+        umma_bf16_elect(d, arow + in_row, bd, idesc_mn, (h | ks) ? 1u : 0u);
+        bd += bstep;
+        if (((ks + 1) * 16) % ck == 0) arow += cstep;
       }
-      // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
-      // y sits in boxes of R = 8 << b rows (largest first), box at yb + row0 * nb * 128 with block
-      // stride R * 128; every box holds whole 16-row K steps (np16 / 8 is even)
-      uint64_t ai = smem_desc(ib + (128 - qrow) * 32, 16, 256, 6);
-      {
-        int mm = np16 >> 3, row0 = 0, ks = 0;
-        while (mm && ks < ny) {
-          const int bbit = 31 - __clz(mm), R = 8 << bbit;
-          uint64_t by = smem_desc(yb + row0 * nb * 128, R * 128, 1024, 2);
-          for (int r = 0; r < R && ks < ny; r += 16, ++ks) {
-            umma_bf16_elect(d, ai, by, idesc_mn, 1u);
-            ai -= 32;      // 16 identity rows x 32 B
-            by += 128;     // 16 y rows x 128 B
-          }
-          row0 += R;
-          mm &= ~(1 << bbit);
-        }
-      }
-      umma_commit_elect(&empty[qs]);   // ring bytes free once these MMAs have read them
-      umma_commit_elect(&tfull[buf]);
-      st.e_tbits ^= 1u << buf;
-      if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 2);
-      __syncwarp();
     }
-    st.e_item = k;
+    // D += I . y : A = identity rows shifted by 16*ks (K-major SW32), B = y (MN-major SW128)
+    // y sits in boxes of R = 8 << b rows (largest first), box at yb + row0 * nb * 128 with block
+    // stride R * 128; every box holds whole 16-row K steps (np16 / 8 is even)
+    uint64_t ai = smem_desc(ib + (128 - qrow) * 32, 16, 256, 6);
+    {
+      int mm = np16 >> 3, row0 = 0, ks = 0;
+      while (mm && ks < ny) {
+        const int bbit = 31 - __clz(mm), R = 8 << bbit;
+        uint64_t by = smem_desc(yb + row0 * nb * 128, R * 128, 1024, 2);
+        for (int r = 0; r < R && ks < ny; r += 16, ++ks) {
+          umma_bf16_elect(d, ai, by, idesc_mn, 1u);
+          ai -= 32;      // 16 identity rows x 32 B
+          by += 128;     // 16 y rows x 128 B
+        }
+        row0 += R;
+        mm &= ~(1 << bbit);
+      }
+    }
+    umma_commit_elect(&empty[qs]);   // ring bytes free once these MMAs have read them
+    umma_commit_elect(&tfull[buf]);
+    st.e_tbits ^= 1u << buf;
+    if (lane == 0) trace_stamp(p.trace, p.trace_items, cta, k - k0, 2);
+    __syncwarp();
+  }
+  st.e_item = k;
 }
 // Epilogue: thread = token row of quadrant q.
 __device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const ExpandSm& sm, uint32_t tmem_base, int cta,
@@ -974,79 +975,79 @@ __device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const Exp
   ExpandRecBuf* recbuf = sm.recbuf;
   uint64_t* tfull = sm.tfull;
   uint64_t* tempty = sm.tempty;
-    const int nbuf = kTmemCols / p.tw_max;
-    const int q = warp & 3;
-    const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
-    WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
-    ExpandRec inf;
-    const uint8_t* unused;
-    for (int k = 0; rs.pop(inf, unused); ++k) {
-      const int buf = k % nbuf;
-      mbar_wait(&tfull[buf], (st.e_tbits >> buf) & 1);
-      st.e_tbits ^= 1u << buf;
-      tc_fence_after();
-      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
-      const int qr = q - expand_qbase(k, inf.ntok);   // this warp's quadrant within the item
-      const int t = qr * 32 + lane;
-      if (qr >= 0 && qr * 32 < inf.ntok) {   // warp-uniform: other quadrants have no rows
-        const int tw = expand_item_tw(inf.rank, p.tws[inf.proj]);
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
-        const bool valid = t < inf.ntok && !(p.dbg & 1);
-        __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
-        const int c_lo = kExpandEpiWarps == 8 ? half * (tw / 2) : 0, c_hi = kExpandEpiWarps == 8 ? c_lo + tw / 2 : tw;
-        // each lane writes its own token row: 32-byte stores are one full sector per row and half
-        // the store wavefronts of 16-byte ones; streaming (evict-first) since y is not re-read here
-        const bool st32 = LSV_EXPAND_ST32 && p.st32[inf.proj];
+  const int nbuf = kTmemCols / p.tw_max;
+  const int q = warp & 3;
+  const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
+  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ExpandRec inf;
+  const uint8_t* unused;
+  for (int k = 0; rs.pop(inf, unused); ++k) {
+    const int buf = k % nbuf;
+    mbar_wait(&tfull[buf], (st.e_tbits >> buf) & 1);
+    st.e_tbits ^= 1u << buf;
+    tc_fence_after();
+    if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 3);
+    const int qr = q - expand_qbase(k, inf.ntok);   // this warp's quadrant within the item
+    const int t = qr * 32 + lane;
+    if (qr >= 0 && qr * 32 < inf.ntok) {   // warp-uniform: other quadrants have no rows
+      const int tw = expand_item_tw(inf.rank, p.tws[inf.proj]);
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + buf * p.tw_max;
+      const bool valid = t < inf.ntok && !(p.dbg & 1);
+      __nv_bfloat16* yrow = p.y[inf.proj] + (int64_t)(inf.tok_begin + (valid ? t : 0)) * p.ldy[inf.proj] + inf.jtile * tw;
+      const int c_lo = kExpandEpiWarps == 8 ? half * (tw / 2) : 0, c_hi = kExpandEpiWarps == 8 ? c_lo + tw / 2 : tw;
+      // each lane writes its own token row: 32-byte stores are one full sector per row and half
+      // the store wavefronts of 16-byte ones; streaming (evict-first) since y is not re-read here
+      const bool st32 = LSV_EXPAND_ST32 && p.st32[inf.proj];
 #if LSV_EXPAND_EPI_PIPE
-        // two 32-column chunks in flight: chunk i+1's TMEM load overlaps chunk i's convert + stores
-        auto put = [&](const uint32_t* r, int cc) {
-          uint32_t w[16];
+      // two 32-column chunks in flight: chunk i+1's TMEM load overlaps chunk i's convert + stores
+      auto put = [&](const uint32_t* r, int cc) {
+        uint32_t w[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-          if (st32) {
+        for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+        if (st32) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
-          } else {
+          for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
+        } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
-          }
-        };
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32_nowait(taddr + c_lo, ra);
-#pragma unroll 1
-        for (int cc = c_lo; cc < c_hi; cc += 64) {   // (c_hi - c_lo) is a multiple of 64
-          tmem_wait_ld_regs(ra);
-          tmem_ld_32x32b_x32_nowait(taddr + cc + 32, rb);
-          put(ra, cc);
-          tmem_wait_ld_regs(rb);
-          if (cc + 64 < c_hi) tmem_ld_32x32b_x32_nowait(taddr + cc + 64, ra);
-          put(rb, cc + 32);
+          for (int u = 0; u < 4; ++u)
+            st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
         }
+      };
+      uint32_t ra[32], rb[32];
+      tmem_ld_32x32b_x32_nowait(taddr + c_lo, ra);
+#pragma unroll 1
+      for (int cc = c_lo; cc < c_hi; cc += 64) {   // (c_hi - c_lo) is a multiple of 64
+        tmem_wait_ld_regs(ra);
+        tmem_ld_32x32b_x32_nowait(taddr + cc + 32, rb);
+        put(ra, cc);
+        tmem_wait_ld_regs(rb);
+        if (cc + 64 < c_hi) tmem_ld_32x32b_x32_nowait(taddr + cc + 64, ra);
+        put(rb, cc + 32);
+      }
 #else
 #pragma unroll 1
-        for (int cc = c_lo; cc < c_hi; cc += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + cc, r);
-          uint32_t w[16];
+      for (int cc = c_lo; cc < c_hi; cc += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + cc, r);
+        uint32_t w[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-          if (st32) {
+        for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+        if (st32) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
-          } else {
+          for (int u = 0; u < 2; ++u) st_global_v8_cs_if(yrow + cc + u * 16, &w[8 * u], valid);
+        } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
-          }
+          for (int u = 0; u < 4; ++u)
+            st_global_v4_if(yrow + cc + u * 8, w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3], valid);
         }
-#endif
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+#endif
     }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[buf]);
+    if (q == 0 && lane == 0) trace_stamp(p.trace, p.trace_items, cta, k, 4);
+  }
   }
 
 __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __grid_constant__ ExpandParams p) {
@@ -1067,17 +1068,17 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   // every other over-read (v rows past the tile's tokens) only feeds discarded D rows.
   // identity A tile, K-major SWIZZLE_32B [256 rows][16 k]: 1.0 at (128 + k, k)
   for (int i = threadIdx.x; i < kIdentRows * 16; i += blockDim.x) {
-    const int t = i / 16, k = i % 16;
-    reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
+  const int t = i / 16, k = i % 16;
+  reinterpret_cast<uint16_t*>(ident)[swz(t * 32 + k * 2, 32) / 2] = (t == 128 + k) ? 0x3F80u : 0u;
   }
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
-    fence_mbar_init();
-    for (int pp = 0; pp < kMaxProj; ++pp)
-      if (p.y[pp])
-        for (int b = 0; b < 5; ++b) { prefetch_tmap(&p.ymap[pp][b]); prefetch_tmap(&p.ymap2[pp][b]); }
+  for (int s = 0; s < kItemQ; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
+  for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kExpandEpiWarps); }
+  fence_mbar_init();
+  for (int pp = 0; pp < kMaxProj; ++pp)
+    if (p.y[pp])
+      for (int b = 0; b < 5; ++b) { prefetch_tmap(&p.ymap[pp][b]); prefetch_tmap(&p.ymap2[pp][b]); }
   }
   if (warp == kExpMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
@@ -1088,36 +1089,36 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 1);
   pdl_wait();                 // v images come from the shrink launch; y from earlier work
   if (p.wait_flag != nullptr) {   // TP: the peers' shards of the v images have landed here too
+  if (threadIdx.x == 0) {
+    wait_flag_geq(p.wait_flag, p.wait_target);
+    fence_proxy_async_global();
+    if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
+      p.wait_flag[1] = 0;
+      p.wait_flag[0] = 0;
+    }
+  }
+  __syncthreads();
+  if (p.xsum != nullptr) {      // row group: v = sum of every rank's fp32 partial, fixed rank order
+    tp_row_sum(p);
+    __threadfence();
+    __syncthreads();
+    int* bar = p.gbar;
     if (threadIdx.x == 0) {
-      wait_flag_geq(p.wait_flag, p.wait_target);
-      fence_proxy_async_global();
-      if (atomicAdd(p.wait_flag + 1, 1) == (int)gridDim.x - 1) {   // last CTA through: re-arm
-        p.wait_flag[1] = 0;
-        p.wait_flag[0] = 0;
+      atomicAdd(&bar[0], 1);
+      uint64_t t0 = 0;
+      for (uint32_t spin = 0; ld_relaxed_sys(&bar[0]) < (int)gridDim.x; ++spin) {
+        __nanosleep(32);
+        if ((spin & 1023u) == 1023u) {
+          const uint64_t now = globaltimer_ns();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 4000000000ull) __trap();
+        }
       }
+      (void)ld_acquire_sys(&bar[0]);
+      fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
     }
     __syncthreads();
-    if (p.xsum != nullptr) {      // row group: v = sum of every rank's fp32 partial, fixed rank order
-      tp_row_sum(p);
-      __threadfence();
-      __syncthreads();
-      int* bar = p.gbar;
-      if (threadIdx.x == 0) {
-        atomicAdd(&bar[0], 1);
-        uint64_t t0 = 0;
-        for (uint32_t spin = 0; ld_relaxed_sys(&bar[0]) < (int)gridDim.x; ++spin) {
-          __nanosleep(32);
-          if ((spin & 1023u) == 1023u) {
-            const uint64_t now = globaltimer_ns();
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 4000000000ull) __trap();
-          }
-        }
-        (void)ld_acquire_sys(&bar[0]);
-        fence_proxy_async_global();   // generic-proxy v writes -> the bulk copies that read them
-      }
-      __syncthreads();
-    }
+  }
   }
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
@@ -1133,8 +1134,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 3);
   if (warp == kExpMmaWarp) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   if (p.xsum != nullptr && threadIdx.x == 0) {   // every CTA is past the sum barrier: re-arm it
-    int* bar = p.gbar;
-    if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }
+  int* bar = p.gbar;
+  if (atomicAdd(&bar[1], 1) == (int)gridDim.x - 1) { bar[0] = 0; bar[1] = 0; }
   }
 }
 
