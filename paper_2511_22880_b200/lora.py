@@ -174,7 +174,7 @@ class LoraDeltaEngine:
     # -- planning ----------------------------------------------------------------------
     def prepare(self, seg: Segments, seg_owner: np.ndarray | None = None,
                 peer_slabs: dict[int, AdapterSlab] | None = None, stream=None,
-                fused_linear: bool = False, remote_aware: bool = True, skip: np.ndarray | None = None,
+                fused_linear: bool = False, remote_aware: bool = False, skip: np.ndarray | None = None,
                 max_sms: int = 0) -> BatchPlan:
         """Plan a batch: one liblsv plan per input group + pointer tables.  With ``stream`` the
         uploads are asynchronous on that stream (pinned staging), so a serving loop can plan batch
@@ -182,7 +182,9 @@ class LoraDeltaEngine:
         ``linear_group`` (base GEMM with the delta fused, LSV_PLAN_TILE_ALIGNED; tensor-core tier).
         ``skip`` [S] bool: segments that keep their tokens but get no work (LSV_SEG_SKIP); ``max_sms``:
         grids of at most that many CTAs (LSV_PLAN_SMS) — together they split a batch into two plans
-        that run side by side on disjoint SMs (``SplitStep``)."""
+        that run side by side on disjoint SMs (``SplitStep``).  ``remote_aware``: mark peer-owned
+        segments LSV_SEG_REMOTE (NVLink-weighted LPT cost, remote/local interleaving); off by default
+        (the bytes-only plan measured faster with the layer kernel: 12.53 vs 12.95 ms on 2 GPUs)."""
         ws_need = 0
         projs = self.model.projections
         # the group plans are independent host work; ctypes drops the GIL inside the C++ planner,
