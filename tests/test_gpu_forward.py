@@ -191,3 +191,46 @@ def test_group_kernel_full_layer_bit_identical_to_split_launches():
     torch.cuda.synchronize()
     for pr in model.projections:
         assert torch.equal(ys[0][pr.name], ys2[0][pr.name]), pr.name
+
+
+@pytest.mark.parametrize("names", [("q_proj", "k_proj", "v_proj", "o_proj"),            # 2 groups: layer kernel
+                                   ("q_proj", "o_proj", "gate_proj", "up_proj", "down_proj", "k_proj")])   # 5 groups
+def test_forward_group_counts_bit_identical(names):
+    """lsv_lora_forward with 2 input groups (one layer kernel per layer, two groups back to back) and
+    with 5 groups (more than a layer kernel holds: one group kernel per group), 3 layers, against
+    the same work issued group by group."""
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import ModelShape, Projection
+    from paper_2511_22880_b200.slab import AdapterSlab
+    dev = torch.device("cuda:0")
+    h, inter, kv = 1024, 2816, 256
+    shapes = {"q_proj": (h, h), "k_proj": (h, kv), "v_proj": (h, kv), "o_proj": (h, h), "gate_proj": (h, inter),
+              "up_proj": (h, inter), "down_proj": (inter, h)}
+    model = ModelShape("mini", 3, tuple(Projection(n, *shapes[n]) for n in names))
+    ranks = [8, 16, 128, 64, 24, 32]
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+    for i, r in enumerate(ranks):
+        slab.fill_random(slab.allocate(f"a{i}", r), 300 + i)
+    tok = np.concatenate([np.full(n, s) for s, n in enumerate([70, 33, 150, 64, 17, 90])])
+    np.random.default_rng(2).shuffle(tok)
+    seg = index_tokens(tok, ranks)
+    eng = LoraDeltaEngine(slab, tier_policy=2)
+    bp = eng.prepare(seg)
+    N = seg.num_tokens
+    g = torch.Generator().manual_seed(6)
+    xs = [{name: torch.randn(N, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16).to(dev)
+           for name, m in model.groups()} for _ in range(model.layers)]
+    ys = [{p.name: torch.randn(N, p.h_out, generator=g).to(torch.bfloat16).to(dev) for p in model.projections}
+          for _ in range(model.layers)]
+    ys2 = [{k: v.clone() for k, v in d.items()} for d in ys]
+    eng.forward(bp, xs, ys)
+    for layer in range(model.layers):
+        for gi, (name, members) in enumerate(model.groups()):
+            eng.shrink(bp, layer, members[0], xs[layer][name])
+            eng.expand_group(bp, layer, gi, [ys2[layer][model.projections[p].name] for p in members])
+    torch.cuda.synchronize()
+    assert len(model.groups()) == (2 if len(names) == 4 else 5)
+    for layer in range(model.layers):
+        for pr in model.projections:
+            assert torch.equal(ys[layer][pr.name], ys2[layer][pr.name]), (layer, pr.name)
