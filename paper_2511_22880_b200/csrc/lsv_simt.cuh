@@ -36,7 +36,17 @@ constexpr int kSimtUnroll = 4;
 #endif
 constexpr int kShrRH = kSimtShrRows / 8;          // 8-row halves per block; a lane owns row rl of each
 constexpr int kShrU = LSV_SIMT_SHR_UNROLL;        // chunks in flight per warp
-__global__ void __launch_bounds__(256) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
+// Resident blocks per SM the compiler must allow (register cap): 4 shrink blocks (64 registers) and
+// 8 expand blocks (64 registers) instead of the 3 and 6 that 77-79 registers allow; with the decode
+// batch's groups on concurrent streams the occupancy wins over the few spills (decode step 3.0 vs
+// 3.6 ms for the unconstrained build, whose 91-register shrink fits 2 blocks).
+#ifndef LSV_SIMT_SHR_MINB
+#define LSV_SIMT_SHR_MINB 4
+#endif
+#ifndef LSV_SIMT_EXP_MINB
+#define LSV_SIMT_EXP_MINB 8
+#endif
+__global__ void __launch_bounds__(256, LSV_SIMT_SHR_MINB) simt_shrink_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                           int h_in, const int32_t* __restrict__ plan,
                                                           int off_items, int n_items,
                                                           const void* const* __restrict__ a_ptrs,
@@ -162,7 +172,7 @@ struct SimtExpandArgs {          // every member of an input group (grid.z = mem
 constexpr int kSimtExpCols = LSV_SIMT_EXP_COLS;            // h_out columns per block (64 per warp)
 constexpr int kSimtExpThreads = kSimtExpCols / 64 * 32;
 template <int NT>                // accumulator rows: tokens per pass over the item's B tile
-__global__ void __launch_bounds__(kSimtExpThreads) simt_expand_kernel(const __grid_constant__ SimtExpandArgs a) {
+__global__ void __launch_bounds__(kSimtExpThreads, LSV_SIMT_EXP_MINB) simt_expand_kernel(const __grid_constant__ SimtExpandArgs a) {
   __shared__ float vs[kSimtMaxTok * 256];
   const int m = blockIdx.z, h_out = a.h_out[m];
   if ((int)blockIdx.y * kSimtExpCols >= h_out) return;    // block-uniform: past this member's columns
