@@ -1,21 +1,25 @@
 // lsv_tc.cuh — tcgen05 (5th-gen tensor core) tier of the mixed-rank LoRA delta.
 //
-// Shrink  D[128 tok × N=rank16] += x_tile[128 × 64k] · A_s^T            (TMEM accumulator)
+// Shrink  D[128 tok × N = members·rank] += x_tile[128 × 64k] · A_s^T     (TMEM accumulator)
 //   x tile: TMA (cp.async.bulk.tensor, SWIZZLE_128B) of exactly ceil8(n) token rows per
 //   64-column chunk, composed from 128/64/32/16/8-row boxes; A_s: one cp.async.bulk of a
-//   pre-swizzled [kch chunks][rank][64] slab run.  Rows past the segment / columns past the
+//   pre-swizzled [kch chunks][rows][64] slab run.  Rows past the segment / columns past the
 //   rank are garbage in, garbage out (row i of D only reads row i of x; column j only
-//   row j of A) and are never stored.  k-split partials are reduced after a grid barrier by
-//   all CTAs in parallel (fixed summation order per element) into the bf16 "v image".
-// Expand  D[128 tok × 128 h_out] = v·B_s^T + I·y                         (y added on the tensor core)
-//   B tile and v image: one cp.async.bulk each; the item's y rows: TMA into an MN-major
-//   SWIZZLE_128B operand; the epilogue is LDTM -> cvt -> 16-byte row stores.
+//   row j of A) and are never stored.  k-split partials are summed in split order (bit-
+//   reproducible) into the v images: after a grid barrier in the standalone kernel, per tile by
+//   the reducer warp in the group kernel.
+// Expand  D[128 tok × 256 h_out] = v_hi·B_s^T + v_lo·B_s^T + I·y          (y added on the tensor core)
+//   B tile and v image pair: one cp.async.bulk each; the item's y rows: one 3D TMA box per row
+//   range into an MN-major SWIZZLE_128B operand; the epilogue is LDTM -> cvt -> 32-byte stores.
 //
-// Both kernels: 192 threads, one persistent CTA per SM, each streaming its own list of fully
-// decoded work records (the host planner assigns records to CTAs LPT-greedy on estimated bytes,
-// so there are no device atomics and no dependent descriptor loads on the critical path).
-// warp 0 = producer (one lane), warp 1 = MMA issuer (one lane) and TMEM owner, warps 2..5 =
-// epilogue (warp w reads TMEM lanes 32*(w%4)..+31).  Launched with programmatic dependent
+// Kernels: shrink_tc_kernel and expand_tc_kernel (standalone entry points, TP) and
+// group_tc_kernel<NG> (lsv_lora_forward: NG input groups' shrinks and expands in one launch,
+// per-m-tile readiness instead of a grid barrier).  One persistent CTA per SM streams its own
+// lists of fully decoded records (host LPT assignment: no device atomics on the critical path).
+// Warp roles (256 threads; the group kernel adds warp 8): 0, 1, 6, 7 epilogue (warp w reads TMEM
+// lanes 32*(w%4)..+31), 2 (+ 4 / 8) copy issue, 3 MMA issue and TMEM owner; in the group kernel
+// 4 publishes stored records and checks expand readiness, 5 reduces split-K shares.  Every copy
+// and MMA is issued by an elected lane of a converged warp.  Launched with programmatic dependent
 // launch: the prologue (barrier init, TMEM alloc) overlaps the previous kernel's tail.
 #pragma once
 #include <cuda.h>
