@@ -894,13 +894,13 @@ int fill_group_params(GroupParams& gp, const GroupArgs& a, int32_t num_tokens, i
   gp.wait_prev = wait_prev;
   return LSV_OK;
 }
-// Development traces: timeline mode gives each launch its own [cta][4] record; item traces put the
+// Development traces: timeline mode gives each launch its own [cta][16] record; item traces put the
 // expand's stamps in a second buffer half.
 void group_trace(GroupParams& gp) {
   if (g_trace != nullptr && g_trace_items < 0) {
     gp.s.trace = gp.e.trace = nullptr;
     gp.s.trace_items = gp.e.trace_items = 0;
-    gp.tl = g_trace + (size_t)(g_tl_launch++ % -g_trace_items) * num_sms_cached() * 4;
+    gp.tl = g_trace + (size_t)(g_tl_launch++ % -g_trace_items) * num_sms_cached() * 16;
   } else if (gp.e.trace != nullptr) {
     gp.e.trace += (size_t)num_sms_cached() * gp.e.trace_items * 16;
   }
