@@ -48,6 +48,8 @@ const bool g_fwd_streams = [] { const char* e = std::getenv("LSV_FWD_STREAMS"); 
 const bool g_layer_kernel = [] { const char* e = std::getenv("LSV_LAYER_KERNEL"); return !e || std::atoi(e) != 0; }();
 // LSV_READY_ORDER=0: keep each CTA's expand items in LPT order instead of estimated m-tile
 // readiness order (A/B timing)
+// layer kernel phase order (lsv_tc.cuh group_tc_kernel): group g's expand after the shrinks of groups <= g + d
+const int g_phase_lookahead = [] { const char* e = std::getenv("LSV_PHASE_LOOKAHEAD"); return e ? std::atoi(e) : 3; }();
 const bool g_ready_order = [] { const char* e = std::getenv("LSV_READY_ORDER"); return !e || std::atoi(e) != 0; }();
 const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
@@ -927,6 +929,7 @@ int run_layer(const GroupArgs* a, int n, int32_t num_tokens, int wait_prev, bool
     grid = std::max(grid, std::max(lp.g[i].s_grid, lp.g[i].e_grid));
   }
   lp.ngroups = n;
+  lp.lookahead = g_phase_lookahead;
   group_trace(lp.g[0]);
   for (int i = 1; i < n; ++i) lp.g[i].s.trace = lp.g[i].e.trace = nullptr;
   LSV_CUDA_CHECK(launch_pdl(group_tc_kernel<kLayerGroups>, grid, group_smem_bytes(), st, lp, pdl, kGroupThreads));

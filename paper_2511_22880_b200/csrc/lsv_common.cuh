@@ -179,8 +179,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 // Bounded wait: traps after ~4 s instead of hanging the GPU forever on a pipeline bug.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
   uint32_t done = 0;
   uint64_t t0 = 0;
   for (uint32_t spin = 0;; ++spin) {
@@ -197,6 +196,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_addr(smem_u32(bar), parity); }
 
 // ---- cross-GPU signalling (NVLink peers, CUDA-IPC-mapped memory) -------------------------
 __device__ __forceinline__ int ld_acquire_sys(const int* p) {

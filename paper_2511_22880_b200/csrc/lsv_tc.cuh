@@ -373,10 +373,7 @@ struct ShrinkSm {
   uint8_t* ring;
   ShrinkRecBuf* recbuf;   // indexed by warp
   uint64_t *full, *empty, *tfull, *tempty;
-};
-struct RingPos {
-  int slot;
-  uint32_t phase;
+  uint32_t* offs;         // [kShrinkSlots] ring offset of the stage behind each full barrier
 };
 // Pipeline position that carries over when one CTA runs several input groups back to back (the
 // layer kernel): every barrier's parity follows from these running counts.  Each role keeps its
@@ -390,13 +387,66 @@ struct PipeState {
   int e_item = 0;           // expand items so far (ring allocations, v-ready queue)
   uint32_t e_tbits = 0;     // expand TMEM buffers: bit b = parity of buffer b's next tfull wait
 };
-// Producer: streams every record's stages into the slot ring; returns the ring position after
-// the last stage (the group kernel drains the ring from there).
-__device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane,
-                                                   int part = 0, int nparts = 1, RingPos start = RingPos{0, 0u}) {
-  // nparts warps run this loop with the same slot bookkeeping; a stage's copies (A first, then the
-  // x boxes) go round-robin to the parts, each arriving on full[slot] with its own bytes: one
-  // warp spends ~130 cycles issuing each copy, so copies from two warps double the issue rate.
+// Byte ring shared by every pipeline a CTA runs (the layer kernel: shrink stages and expand items
+// of consecutive phases back to back).  Allocations are contiguous, 1024-byte aligned and released
+// in allocation order (the MMA warp consumes them in that order, across phases), each when its
+// release barrier completes the recorded phase; a phase's first copies therefore go out while the
+// previous phase's last items are still landing — there is no drain between phases.  Every
+// producer part keeps an identical copy of this bookkeeping.
+// An allocation's barriers (shrink slot or expand queue entry) are reused only after the FIFO has
+// released their previous allocation, so every FIFO wait names an unambiguous phase.
+constexpr int kRingQ = 16;   // allocations in flight, both pipelines (>= kShrinkSlots + kItemQ)
+constexpr int kRingBars = 16;   // barrier ids: shrink slot s -> s, expand queue entry q -> kShrinkSlots + q
+constexpr int kRingTableWords = 2 * kRingQ + kRingBars;   // per producer part, in shared memory
+// The counters stay in registers; the tables live in shared memory (local-memory tables queue
+// behind the epilogue's global stores in L1 and slowed the producers by ~15%).
+struct RingAlloc {
+  uint32_t head = 0, tail = 0;   // bytes allocated / start of the oldest live allocation (monotone)
+  int n = 0, r = 0;              // allocations made / released
+  uint32_t* beg;                 // [kRingQ] start of allocation i % kRingQ
+  uint32_t* bar;                 // [kRingQ] its release barrier: shared address | phase parity
+  int* last;                     // [kRingBars] per barrier id: index of its latest allocation (-1: none)
+  // tab: this part's kRingTableWords words; the whole warp calls this
+  __device__ explicit RingAlloc(uint32_t* tab, int lane)
+      : beg(tab), bar(tab + kRingQ), last(reinterpret_cast<int*>(tab + 2 * kRingQ)) {
+    if (lane < kRingBars) last[lane] = -1;
+    __syncwarp();
+  }
+};
+__device__ __forceinline__ void ring_release_one(RingAlloc& ra) {
+  const uint32_t b = ra.bar[ra.r % kRingQ];
+  mbar_wait_addr(b & ~1u, b & 1u);
+  ++ra.r;
+  ra.tail = ra.r < ra.n ? ra.beg[ra.r % kRingQ] : ra.head;
+}
+// size bytes once they are free.  The allocation ends before ring_bytes + spill (free shared
+// memory past the ring) and `extent` bytes from its start (the MMAs over-read past short tiles)
+// before ring_bytes + guard (shared memory the over-read may touch: garbage there only reaches
+// accumulator rows/columns nobody stores); else it starts at the next wrap.  Returns the offset.
+__device__ __forceinline__ uint32_t ring_alloc(RingAlloc& ra, uint32_t size, uint32_t extent, uint32_t ring_bytes,
+                                               uint32_t spill, uint32_t guard, int bar_id, uint32_t bar_addr,
+                                               uint32_t parity) {
+  uint32_t head = (ra.head + 1023u) & ~1023u;
+  const uint32_t off = head % ring_bytes;
+  if (off + size > ring_bytes + spill || off + extent > ring_bytes + guard) head = (head / ring_bytes + 1) * ring_bytes;
+  ra.head = head;
+  if (ra.r == ra.n) ra.tail = head;
+  const int prev = ra.last[bar_id];   // the barriers' previous allocation must be released first
+  while (ra.r <= prev || ra.n - ra.r == kRingQ || head + size - ra.tail > ring_bytes) ring_release_one(ra);
+  ra.last[bar_id] = ra.n;
+  ra.beg[ra.n % kRingQ] = head;
+  ra.bar[ra.n % kRingQ] = bar_addr | parity;
+  ++ra.n;
+  ra.head = head + size;
+  return head % ring_bytes;
+}
+// Producer: streams every record's stages into the byte ring (stage slot = barrier pair + offset).
+__device__ __forceinline__ void shrink_producer(const ShrinkParams& p, const ShrinkSm& sm, int cta, int warp, int lane,
+                                                int part, int nparts, PipeState& st, RingAlloc& ra, uint32_t ring_bytes,
+                                                uint32_t spill) {
+  // nparts warps run this loop with the same slot and ring bookkeeping; a stage's copies (A first,
+  // then the x boxes) go round-robin to the parts, each arriving on full[slot] with its own bytes:
+  // one warp spends ~130 cycles issuing each copy, so copies from two warps double the issue rate.
   uint8_t* ring = sm.ring;
   ShrinkRecBuf* recbuf = sm.recbuf;
   uint64_t* full = sm.full;
@@ -404,7 +454,7 @@ __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const 
   WarpRecStream<ShrinkRec, kShrinkRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, &p.a_ptrs);
   ShrinkRec inf;
   const uint8_t* a;
-  int slot = start.slot; uint32_t phase = start.phase;
+  int slot = st.s_slot; uint32_t phase = st.s_phase;
   int pstage = 0;   // debug stage stamps (LSV_DEBUG_SHRINK bit 16)
   const bool stamp = part == 0 && lane == 0;
   const uint32_t ring_base = smem_u32(ring);
@@ -421,14 +471,21 @@ __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const 
     for (int g = inf.chunk_begin; g < inf.chunk_end; g += kch) {
       const int kc = min(kch, inf.chunk_end - g);
       if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage, 3);
-      mbar_wait(&empty[slot], phase ^ 1);
+      // x chunks [kc][np8 rows], then A [kc][rows]; the M=128 MMA reads 16 KB from each x chunk and
+      // N = round_up(rows, 16) A rows
+      // (the standalone kernel's ring holds kShrinkSlots whole slots: fixed-size stages, no wrap waste)
+      const uint32_t size = ring_bytes == kShrinkSlots * kShrinkSlotBytes ? kShrinkSlotBytes : (uint32_t)(kc * (np8 + rows) * 128);
+      const uint32_t extent = max(size + (uint32_t)((round_up(rows, 16) - rows) * 128),
+                                  (uint32_t)((kc - 1) * np8 * 128 + kTileM * 128));
+      const uint32_t off = ring_alloc(ra, size, extent, ring_bytes, spill, kShrinkGuardBytes, slot, smem_u32(&empty[slot]), phase);
+      if (part == 0) sm.offs[slot] = off;   // every lane: the elected arriving lane's own store
       if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage, 4);
       const uint32_t fb = smem_u32(&full[slot]);
       // part 0 copies A; chunk c's x boxes belong to part (c + 1) % nparts
       const bool do_a = part == 0 && !(p.dbg & 2), do_x = !(p.dbg & 4);
       const int my_chunks = do_x ? (kc + nparts - 1 - (part + nparts - 1) % nparts) / nparts : 0;
       mbar_arrive_expect_tx_elect(fb, (uint32_t)((do_a ? kc * rows : 0) + my_chunks * np8) * 128);
-      const uint32_t dst = ring_base + slot * kShrinkSlotBytes;
+      const uint32_t dst = ring_base + off;
       if (do_a) {
         if (rows == G) {       // whole group: the kc chunks are one contiguous run
           bulk_load_elect(dst + kc * np8 * 128, a + (size_t)g * G * 128, (uint32_t)(kc * G * 128), fb);
@@ -454,7 +511,8 @@ __device__ __forceinline__ RingPos shrink_producer(const ShrinkParams& p, const 
     if (!(p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, k, 1);
     __syncwarp();
   }
-  return RingPos{slot, phase};
+  st.s_slot = slot;
+  st.s_phase = phase;
 }
 // MMA issuer: the whole warp runs the loop (warp-uniform values stay in uniform registers, so each
 // MMA costs a few uniform adds), one lane issues.  Returns the number of records.
@@ -494,7 +552,7 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
       mbar_wait(&full[slot], phase);
       tc_fence_after();
       if ((p.dbg & 16) && lane == 0) trace_stamp(p.trace, p.trace_items, cta, dbg_stage++, 7);
-      const uint32_t xb = ring_base + slot * kShrinkSlotBytes;
+      const uint32_t xb = ring_base + sm.offs[slot];
       uint64_t adesc = smem_desc(xb, 16, 1024, 2);
       uint64_t bdesc = smem_desc(xb + kc * np8 * 128, 16, 1024, 2);
       for (int c = 0; c < kc; ++c) {
@@ -622,6 +680,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   uint64_t* tfull = empty + kShrinkSlots;
   uint64_t* tempty = tfull + kAccBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+  uint32_t* offs = tmem_slot + 1;
+  uint32_t* ring_tab = offs + kShrinkSlots;   // [kProdParts][kRingTableWords]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
@@ -641,10 +701,13 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   if (p.wait_prev) pdl_wait();   // x, workspace and counters are written by earlier launches
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
-  const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty};
-  if (warp == kShrProdWarp) shrink_producer(p, sm, cta, warp, lane, 0, kProdParts);
-  else if (warp == kProdWarp2 && kProdParts == 2) shrink_producer(p, sm, cta, warp, lane, 1, kProdParts);
-  else if (warp == kShrMmaWarp) {
+  const ShrinkSm sm{ring, recbuf, full, empty, tfull, tempty, offs};
+  if (warp == kShrProdWarp || (warp == kProdWarp2 && kProdParts == 2)) {
+  PipeState st;
+  RingAlloc ra(ring_tab + (warp == kShrProdWarp ? 0 : kRingTableWords), lane);
+  shrink_producer(p, sm, cta, warp, lane, warp == kShrProdWarp ? 0 : 1, kProdParts, st, ra, kShrinkSlots * kShrinkSlotBytes,
+                  kShrinkGuardBytes);
+  } else if (warp == kShrMmaWarp) {
   PipeState st;
   shrink_mma(p, sm, tmem_base, cta, warp, lane, st);
   } else if (shrink_epi_warp(warp)) {
@@ -795,7 +858,7 @@ struct ExpandSm {
 // v copy waits until the ready checker has seen the item's m-tile complete.
 __device__ __forceinline__ void expand_producer(const ExpandParams& p, const ExpandSm& sm, int cta, int warp, int lane,
                                                 uint64_t* vfull, uint64_t* vempty, int part, int nparts, PipeState& st,
-                                                bool drain = false) {
+                                                RingAlloc& ra) {
   // nparts (1 or 2) warps run this loop with the same ring bookkeeping: part 0 copies B and v
   // (and y when alone), part 1 the y boxes; each arrives on full[] with its own bytes.
   uint8_t* ring = sm.ring;
@@ -809,10 +872,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
   WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
   ExpandRec inf;
   const uint8_t* b;
-  uint32_t head = 0, tail = 0;   // ring bytes (the ring is empty when an expand phase starts)
-  uint32_t vbegin[kItemQ];
-  const int k0 = st.e_item;      // allocations before this phase are all retired
-  int retired = k0;
+  const int k0 = st.e_item;
   const uint32_t ring_base = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
   int k = k0;
   for (; rs.pop(inf, b); ++k) {
@@ -825,24 +885,15 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
     const int qs = k % kItemQ;
     const uint32_t extent =
         max(size, voff + (p.vsplit ? vlo : 0u) + (uint32_t)((kp * 2 / S - 1) * np16 * S + 128 * S));
-    head = round_up(head, 1024);
-    if ((head % kExpandRingBytes) + extent > kExpandRingBytes + kExpandGuardBytes)
-      head = (head / kExpandRingBytes + 1) * kExpandRingBytes;
     LSV_DCHECK(extent <= (uint32_t)(kExpandRingBytes + kExpandGuardBytes) && size <= (uint32_t)kExpandRingBytes);
     LSV_DCHECK(inf.ntok >= 1 && inf.ntok <= kTileM && inf.tok_begin + inf.ntok <= p.num_tokens);
     LSV_DCHECK(inf.proj >= 0 && inf.proj < kMaxProj && (inf.jtile + 1) * tw <= p.h_outs[inf.proj]);
     LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
     const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
     if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 0);
-    while (k - retired == kItemQ || head + size - tail > (uint32_t)kExpandRingBytes) {
-      mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
-      ++retired;
-      tail = retired < k ? vbegin[retired % kItemQ] : head;
-    }
-    vbegin[qs] = head;
-    const uint32_t ring_off = head % kExpandRingBytes;
+    const uint32_t ring_off = ring_alloc(ra, size, extent, kExpandRingBytes, kExpandGuardBytes, kExpandGuardBytes, kShrinkSlots + qs,
+                                         smem_u32(&empty[qs]), (k / kItemQ) & 1);
     if (stamp) offs[qs] = ring_off;
-    head += size;
     const int dbg = p.dbg;
     const uint32_t fb = smem_u32(&full[qs]);
     mbar_arrive_expect_tx_elect(fb, (p0 ? ((dbg & 16) ? 0 : bbytes) + ((dbg & 32) ? 0 : vbytes) : 0u) +
@@ -882,8 +933,6 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
     if (stamp) trace_aux(p.trace, p.trace_items, cta, k - k0, 4);
     __syncwarp();
   }
-  if (drain)   // the next group's shrink reuses the ring bytes: wait until every item's MMAs read them
-    for (; retired < k; ++retired) mbar_wait(&empty[retired % kItemQ], (retired / kItemQ) & 1);
   st.e_item = k;
 }
 // MMA issuer (whole warp): the election happens inside the MMA asm, so ptxas emits no per-MMA
@@ -1065,6 +1114,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   uint64_t* tfull = empty + kItemQ;
   uint64_t* tempty = tfull + kAccBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+  uint32_t* ring_tab = tmem_slot + 1;   // [kProdParts][kRingTableWords]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
@@ -1129,8 +1179,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
 
   const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty};
   PipeState st;
-  if (warp == kExpProdWarp) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 0, kProdParts, st);
-  else if (warp == kProdWarp2 && kProdParts == 2) expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, 1, kProdParts, st);
+  if (warp == kExpProdWarp || (warp == kProdWarp2 && kProdParts == 2)) {
+    const int part = warp == kExpProdWarp ? 0 : 1;
+    RingAlloc ra(ring_tab + part * kRingTableWords, lane);
+    expand_producer(p, sm, cta, warp, lane, nullptr, nullptr, part, kProdParts, st, ra);
+  }
   else if (warp == kExpMmaWarp) expand_mma(p, sm, tmem_base, cta, warp, lane, st);
   else if (expand_epi_warp(warp)) expand_epilogue(p, sm, tmem_base, cta, warp, lane, st);
   tc_fence_before();
@@ -1170,6 +1223,7 @@ template <int NG>
 struct alignas(64) LayerParams {
   GroupParams g[NG];
   int ngroups;
+  int lookahead;       // phase order: group g's expand runs after the shrinks of groups <= g + lookahead
 };
 union RecBufU {
   ShrinkRecBuf s;
@@ -1177,11 +1231,17 @@ union RecBufU {
 };
 __host__ __device__ constexpr int group_smem_bytes() {
   return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
-         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 + 1024;
+         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 +
+         2 * kRingTableWords * 4 + 1024;
 }
-static_assert(kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes <=
-                  kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2,
-              "the shrink ring (and its MMA over-read guard) must lie below the group kernel's record buffers");
+static_assert(kShrinkGuardBytes <= kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU),
+              "a shrink stage's MMA over-read past the ring end stays inside the group kernel's shared memory");
+static_assert(kShrinkSlots <= kItemQ, "the shrink stage offsets live in the second half of offs[]");
+static_assert(8 * (2 * kShrinkSlots + 2 * kAccBufs) + 4 + 4 * kShrinkSlots + 2 * 4 * kRingTableWords <= 1024 &&
+                  4 * 2 * kItemQ + 8 * (2 * kItemQ + 2 * kAccBufs) + 4 + 2 * 4 * kRingTableWords <= 1024,
+              "the standalone kernels' barriers, offsets and ring tables fit their last 1 KB of shared memory");
+static_assert(kShrinkSlots + kItemQ <= kRingQ && kShrinkSlots + kItemQ <= kRingBars,
+              "ring allocations in flight across a phase boundary: at most one per barrier pair");
 
 // Warp 5: this CTA's share of the split-K reduction of its split records.
 __device__ __forceinline__ void group_reducer(const ShrinkParams& p, ShrinkRecBuf* rb, int cta, int lane, int* ready,
@@ -1286,6 +1346,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   uint64_t* vempty = vfull + kVQ;
   uint64_t* recdone = vempty + kVQ;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recdone + kRecQ) + 1;   // [0]: published-record count
+  uint32_t* ring_tab = tmem_slot + 1;                                          // [kProdParts][kRingTableWords]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -1323,7 +1384,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   if (gp.tl != nullptr && threadIdx.x == 0) gp.tl[cta * 16 + 1] = globaltimer_ns();
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
-  const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty};
+  const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty, offs + kItemQ};
   const ExpandSm esm{ring, ident, &recbuf[0].e, offs, e_full, e_empty, e_tfull, e_tempty};
   // the role functions index recbuf by warp: give each a pointer whose [warp] is this warp's union slot
   ShrinkSm ssw = ssm;
@@ -1332,26 +1393,33 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   esw.recbuf = reinterpret_cast<ExpandRecBuf*>(&recbuf[warp]) - warp;
   const int ng = NG == 1 ? 1 : lp.ngroups;
   // Each role runs the layer's 2*ng phases in the same order, its pipeline position carried over
-  // (PipeState): S0, S1, E0, S2, E1, ..., S(ng-1), E(ng-2), E(ng-1) — the next group's shrink runs
-  // before the previous group's expand, so a group's m-tiles (split-K reductions included) are
-  // complete by the time its expand starts.  After a shrink phase followed by an expand the copy
-  // warps drain the slot ring; after an expand phase they drain the expand ring; the MMA warp drains
-  // a phase's accumulators before the next phase writes TMEM.  No CTA-wide barrier.
+  // (PipeState).  Default order (lookahead 3): every shrink, then every expand — a group's m-tiles
+  // (split-K reductions included) on other CTAs have the later shrinks' time to complete before
+  // its expand asks for them, which absorbs the start skew of back-to-back layer launches
+  // (lookahead 1, S0 S1 E0 S2 E1 S3 E2 E3, measured 9.1 vs 8.73 ms per C2 step).  Shrink stages and expand items share one byte ring
+  // (RingAlloc): the copy warps start a phase's loads behind the previous phase's last items; the
+  // MMA warp drains a phase's accumulators before the next phase writes TMEM.  No CTA-wide barrier.
   const int nph = 2 * ng;
+  // lookahead d: S0 .. Sd, then E0 S(d+1) E1 S(d+2) ..., then the remaining expands
+  // (d = 1: S0 S1 E0 S2 E1 S3 E2 E3; d = 3: S0 S1 S2 S3 E0 E1 E2 E3)
+  const int npre = min(ng, (NG == 1 ? 1 : max(lp.lookahead, 1)) + 1), m = ng - npre;
   auto phase_of = [&](int i, int& g) -> bool {   // true: expand phase of group g
-    if (i == 0) { g = 0; return false; }
-    if (i == nph - 1) { g = ng - 1; return true; }
-    g = (i + 1) / 2 - (i % 2 == 0 ? 1 : 0);
-    return i % 2 == 0;
+    if (i < npre) { g = i; return false; }
+    const int j = i - npre;
+    if (j < 2 * m) {
+      g = j / 2 + (j % 2 ? npre : 0);
+      return j % 2 == 0;
+    }
+    g = m + (j - 2 * m);
+    return true;
   };
   if (warp == kExpProdWarp || (warp == 8 && kProdParts == 2)) {
     const int part = warp == 8 ? 1 : 0;
-    RingPos rp{0, 0u};
     PipeState st;
+    RingAlloc ra(ring_tab + part * kRingTableWords, lane);
     for (int i = 0; i < nph; ++i) {
-      int g, gn = 0;
+      int g;
       const bool ex = phase_of(i, g);
-      const bool next_ex = i + 1 < nph && phase_of(i + 1, gn);
       const GroupParams& G = lp.g[g];
       if (!ex) {
         if (g > 0 && part == 0 && lane == 0) {   // this group's tensor maps
@@ -1360,17 +1428,11 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
             if (G.e.y[pp])
               for (int b = 0; b < 5; ++b) { prefetch_tmap(&G.e.ymap[pp][b]); prefetch_tmap(&G.e.ymap2[pp][b]); }
         }
-        if (cta < G.s_grid) rp = shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, rp);
-        if (next_ex) {
-          RingPos d = rp;
-          for (int j = 0; j < kShrinkSlots; ++j) {   // every stage consumed: the ring is the expand's now
-            mbar_wait(&s_empty[d.slot], d.phase ^ 1);
-            if (++d.slot == kShrinkSlots) { d.slot = 0; d.phase ^= 1; }
-          }
-        }
+        if (cta < G.s_grid) shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, st, ra, kExpandRingBytes,
+                                            kExpandGuardBytes);
         if (lane == 0 && part == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 2);   // shrink stages issued
       } else if (cta < G.e_grid) {
-        expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, i + 1 < nph);
+        expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, ra);
       }
     }
   } else if (warp == kExpMmaWarp) {

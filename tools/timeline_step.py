@@ -72,7 +72,21 @@ print(f"exit -> next entry on the same SM: mean {gaps.mean():.2f} us, p50 {np.me
       f"SM time past setup / span: {busy / (148 * span) * 100:.1f}%")
 
 if kind == "layer kernels":   # phase ends inside each layer kernel (epilogue warp 0 of every CTA)
-    order = ["S0 attn_in", "S1 attn_out", "E0 attn_in", "S2 mlp_in", "E1 attn_out", "S3 mlp_mid", "E2 mlp_in", "E3 mlp_mid"]
+    import os
+    la = int(os.environ.get("LSV_PHASE_LOOKAHEAD", "3"))   # lsv_tc.cuh group_tc_kernel phase_of
+    names4 = ["attn_in", "attn_out", "mlp_in", "mlp_mid"]
+    npre, order = min(4, max(la, 1) + 1), []
+    for i in range(8):
+        if i < npre:
+            order.append(f"S{i} {names4[i]}")
+            continue
+        j = i - npre
+        if j < 2 * (4 - npre):
+            g = j // 2 + (npre if j % 2 else 0)
+            order.append(f"{'S' if j % 2 else 'E'}{g} {names4[g]}")
+        else:
+            g = (4 - npre) + j - 2 * (4 - npre)
+            order.append(f"E{g} {names4[g]}")
     for i in range(min(n, 2)):
         ent = tl[i, :, 1]
         print(f"layer kernel {i}: phase end, us after the CTA's setup (p10 / p50 / max over CTAs)")
@@ -84,3 +98,5 @@ if kind == "layer kernels":   # phase ends inside each layer kernel (epilogue wa
             print(f"  {order[ph]:12s} end {np.percentile(d, 10):7.1f} {np.median(d):7.1f} {d.max():7.1f}   "
                   f"phase length p50 {np.median(dur):6.1f}")
             prev = e
+if len(sys.argv) > 2:   # raw [launch][cta][16] globaltimer stamps for offline analysis
+    np.save(sys.argv[2], tl)
