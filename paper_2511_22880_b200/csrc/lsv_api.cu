@@ -107,13 +107,16 @@ constexpr int kShrinkWaves = LSV_SHRINK_WAVES;  // target shrink items per SM (b
 #ifndef LSV_EXPAND_ITEM_FIXED_KB
 #define LSV_EXPAND_ITEM_FIXED_KB 8
 #endif
+// Fixed costs per shrink record / stage: with the layer kernel's byte ring (no pipeline refill per
+// phase) small ones balance the CTAs best (C2 8.38-8.48 ms at 16 / 8 KB vs 8.61-8.75 at the
+// standalone-kernel-era 64 / 96 KB; 0-16 KB all within noise of each other)
 #ifndef LSV_SHRINK_REC_FIXED_KB
-#define LSV_SHRINK_REC_FIXED_KB 64
+#define LSV_SHRINK_REC_FIXED_KB 16
 #endif
 constexpr int64_t kExpandItemFixed = (int64_t)LSV_EXPAND_ITEM_FIXED_KB * 1024;
 constexpr int64_t kShrinkRecFixed = (int64_t)LSV_SHRINK_REC_FIXED_KB * 1024;
 #ifndef LSV_SHRINK_STAGE_FIXED_KB
-#define LSV_SHRINK_STAGE_FIXED_KB 96
+#define LSV_SHRINK_STAGE_FIXED_KB 8
 #endif
 constexpr int64_t kShrinkStageFixed = (int64_t)LSV_SHRINK_STAGE_FIXED_KB * 1024;
 // Remote segments (adapter owned by an NVLink peer, LSV_SEG_REMOTE): their A/B bytes weigh
@@ -392,10 +395,10 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
         rc.kch = kch; rc.split = sp;
         rc.nsplit = nsplit; rc.part_off = mt.part_off; rc.vimg_off = mt.vimg_off; rc.counter = mt.counter;
         rc.mtile = (int32_t)i; rc.p0 = p0; rc.np = np;
-        // bytes moved + a fixed cost per pipeline stage and per record (pipeline fill, epilogue,
-        // split partials).  Measured per CTA (tools/shrink_balance.py), a stage costs a near
-        // fixed share of the load latency whatever its size (the ring holds 3), so stage counts
-        // predict a CTA's time better than its bytes.
+        // bytes moved + a fixed cost per pipeline stage and per record (epilogue, split partials).
+        // The standalone shrink (round-2 start, tools/shrink_balance.py) paid a near fixed share of
+        // the load latency per stage; the layer kernel streams stages back to back across phases,
+        // and bytes predict a CTA's time (tools/timeline_step.py per-CTA phase ends vs its plan).
         const int nstage = (rc.chunk_end - rc.chunk_begin + kch - 1) / kch;
         const int64_t cost = row_bytes * (rc.chunk_end - rc.chunk_begin) + kShrinkRecFixed +
                              kShrinkStageFixed * nstage + (nsplit > 1 ? (int64_t)mt.ntok * rows * 8 : 0) +

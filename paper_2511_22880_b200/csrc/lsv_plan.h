@@ -112,7 +112,11 @@ constexpr int kMaxBarPairs = kBarHeaderBytes / 8;
 #endif
 constexpr int kShrinkMaxKch = LSV_SHRINK_MAX_KCH;   // 64-column chunks per pipeline stage, at most
 constexpr int kShrinkSlotBytes = LSV_SHRINK_SLOT_KB * 1024;
-constexpr int kShrinkSlots = LSV_SHRINK_SLOTS;
+constexpr int kShrinkSlots = LSV_SHRINK_SLOTS;     // the standalone shrink kernel's ring: whole slots
+#ifndef LSV_SHRINK_STAGES
+#define LSV_SHRINK_STAGES LSV_SHRINK_SLOTS
+#endif
+constexpr int kShrinkStages = LSV_SHRINK_STAGES;   // stage barrier pairs (stages in flight), both kernels
 constexpr int kShrinkGuardBytes = 16 * 1024;   // the M=128 MMA over-reads past short token tiles
 #ifndef LSV_EXPAND_RING_KB
 #define LSV_EXPAND_RING_KB 200

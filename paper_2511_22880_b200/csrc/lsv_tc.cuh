@@ -373,7 +373,7 @@ struct ShrinkSm {
   uint8_t* ring;
   ShrinkRecBuf* recbuf;   // indexed by warp
   uint64_t *full, *empty, *tfull, *tempty;
-  uint32_t* offs;         // [kShrinkSlots] ring offset of the stage behind each full barrier
+  uint32_t* offs;         // [kShrinkStages] ring offset of the stage behind each full barrier
 };
 // Pipeline position that carries over when one CTA runs several input groups back to back (the
 // layer kernel): every barrier's parity follows from these running counts.  Each role keeps its
@@ -395,8 +395,8 @@ struct PipeState {
 // producer part keeps an identical copy of this bookkeeping.
 // An allocation's barriers (shrink slot or expand queue entry) are reused only after the FIFO has
 // released their previous allocation, so every FIFO wait names an unambiguous phase.
-constexpr int kRingQ = 16;   // allocations in flight, both pipelines (>= kShrinkSlots + kItemQ)
-constexpr int kRingBars = 16;   // barrier ids: shrink slot s -> s, expand queue entry q -> kShrinkSlots + q
+constexpr int kRingQ = 16;   // allocations in flight, both pipelines (>= kShrinkStages + kItemQ)
+constexpr int kRingBars = 16;   // barrier ids: shrink slot s -> s, expand queue entry q -> kShrinkStages + q
 constexpr int kRingTableWords = 2 * kRingQ + kRingBars;   // per producer part, in shared memory
 // The counters stay in registers; the tables live in shared memory (local-memory tables queue
 // behind the epilogue's global stores in L1 and slowed the producers by ~15%).
@@ -506,7 +506,7 @@ __device__ __forceinline__ void shrink_producer(const ShrinkParams& p, const Shr
         }
       }
       if ((p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, pstage++, 5);
-      if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
+      if (++slot == kShrinkStages) { slot = 0; phase ^= 1; }
     }
     if (!(p.dbg & 16) && stamp) trace_stamp(p.trace, p.trace_items, cta, k, 1);
     __syncwarp();
@@ -565,7 +565,7 @@ __device__ __forceinline__ int shrink_mma(const ShrinkParams& p, const ShrinkSm&
         bdesc += astep;
       }
       umma_commit_elect(&empty[slot]);
-      if (++slot == kShrinkSlots) { slot = 0; phase ^= 1; }
+      if (++slot == kShrinkStages) { slot = 0; phase ^= 1; }
     }
     umma_commit_elect(&tfull[buf]);
     st.s_tbits ^= 1u << buf;
@@ -676,17 +676,17 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ShrinkRecBuf* recbuf = reinterpret_cast<ShrinkRecBuf*>(ring + kShrinkSlots * kShrinkSlotBytes + kShrinkGuardBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(recbuf + kShrinkRecBufs);
-  uint64_t* empty = full + kShrinkSlots;
-  uint64_t* tfull = empty + kShrinkSlots;
+  uint64_t* empty = full + kShrinkStages;
+  uint64_t* tfull = empty + kShrinkStages;
   uint64_t* tempty = tfull + kAccBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
   uint32_t* offs = tmem_slot + 1;
-  uint32_t* ring_tab = offs + kShrinkSlots;   // [kProdParts][kRingTableWords]
+  uint32_t* ring_tab = offs + kShrinkStages;   // [kProdParts][kRingTableWords]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, blockIdx.x, 0);
   if (threadIdx.x == 0) {
-  for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
+  for (int s = 0; s < kShrinkStages; ++s) { mbar_init(&full[s], kProdParts); mbar_init(&empty[s], 1); }
   for (int b = 0; b < kAccBufs; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
   fence_mbar_init();
   for (int b = 0; b < 5; ++b) prefetch_tmap(&p.xmap[b]);
@@ -891,7 +891,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
     LSV_DCHECK(p.wait_flag != nullptr || (int64_t)p.ws_vimg[inf.proj] + inf.vimg_off + vbytes <= p.ws_bytes);
     const bool p0 = part == 0, stamp = p0 && lane == 0, do_y = nparts == 1 || part == 1;
     if (stamp) trace_stamp(p.trace, p.trace_items, cta, k - k0, 0);
-    const uint32_t ring_off = ring_alloc(ra, size, extent, kExpandRingBytes, kExpandGuardBytes, kExpandGuardBytes, kShrinkSlots + qs,
+    const uint32_t ring_off = ring_alloc(ra, size, extent, kExpandRingBytes, kExpandGuardBytes, kExpandGuardBytes, kShrinkStages + qs,
                                          smem_u32(&empty[qs]), (k / kItemQ) & 1);
     if (stamp) offs[qs] = ring_off;
     const int dbg = p.dbg;
@@ -1231,16 +1231,16 @@ union RecBufU {
 };
 __host__ __device__ constexpr int group_smem_bytes() {
   return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
-         8 * (2 * kShrinkSlots + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 +
+         8 * (2 * kShrinkStages + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 +
          2 * kRingTableWords * 4 + 1024;
 }
 static_assert(kShrinkGuardBytes <= kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU),
               "a shrink stage's MMA over-read past the ring end stays inside the group kernel's shared memory");
-static_assert(kShrinkSlots <= kItemQ, "the shrink stage offsets live in the second half of offs[]");
-static_assert(8 * (2 * kShrinkSlots + 2 * kAccBufs) + 4 + 4 * kShrinkSlots + 2 * 4 * kRingTableWords <= 1024 &&
+static_assert(kShrinkStages <= kItemQ, "the shrink stage offsets live in the second half of offs[]");
+static_assert(8 * (2 * kShrinkStages + 2 * kAccBufs) + 4 + 4 * kShrinkStages + 2 * 4 * kRingTableWords <= 1024 &&
                   4 * 2 * kItemQ + 8 * (2 * kItemQ + 2 * kAccBufs) + 4 + 2 * 4 * kRingTableWords <= 1024,
               "the standalone kernels' barriers, offsets and ring tables fit their last 1 KB of shared memory");
-static_assert(kShrinkSlots + kItemQ <= kRingQ && kShrinkSlots + kItemQ <= kRingBars,
+static_assert(kShrinkStages + kItemQ <= kRingQ && kShrinkStages + kItemQ <= kRingBars,
               "ring allocations in flight across a phase boundary: at most one per barrier pair");
 
 // Warp 5: this CTA's share of the split-K reduction of its split records.
@@ -1335,8 +1335,8 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   RecBufU* recbuf = reinterpret_cast<RecBufU*>(ident + kIdentRows * 16 * 2);       // one per warp, both phases
   uint32_t* offs = reinterpret_cast<uint32_t*>(recbuf + kGroupThreads / 32);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(offs + 2 * kItemQ);
-  uint64_t* s_empty = s_full + kShrinkSlots;
-  uint64_t* s_tfull = s_empty + kShrinkSlots;
+  uint64_t* s_empty = s_full + kShrinkStages;
+  uint64_t* s_tfull = s_empty + kShrinkStages;
   uint64_t* s_tempty = s_tfull + kAccBufs;
   uint64_t* e_full = s_tempty + kAccBufs;
   uint64_t* e_empty = e_full + kItemQ;
@@ -1362,7 +1362,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   }
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkSlots; ++s) { mbar_init(&s_full[s], kProdParts); mbar_init(&s_empty[s], 1); }
+    for (int s = 0; s < kShrinkStages; ++s) { mbar_init(&s_full[s], kProdParts); mbar_init(&s_empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&s_tfull[b], 1); mbar_init(&s_tempty[b], 4); }
     for (int s = 0; s < kItemQ; ++s) { mbar_init(&e_full[s], kProdParts); mbar_init(&e_empty[s], 1); }
     for (int b = 0; b < kAccBufs; ++b) { mbar_init(&e_tfull[b], 1); mbar_init(&e_tempty[b], kExpandEpiWarps); }

@@ -98,5 +98,7 @@ if kind == "layer kernels":   # phase ends inside each layer kernel (epilogue wa
             print(f"  {order[ph]:12s} end {np.percentile(d, 10):7.1f} {np.median(d):7.1f} {d.max():7.1f}   "
                   f"phase length p50 {np.median(dur):6.1f}")
             prev = e
-if len(sys.argv) > 2:   # raw [launch][cta][16] globaltimer stamps for offline analysis
+if len(sys.argv) > 2:   # raw [launch][cta][16] globaltimer stamps (+ each group's plan) for offline analysis
     np.save(sys.argv[2], tl)
+    np.savez(sys.argv[2].replace(".npy", "_plans.npz"),
+             **{g: np.asarray(gp.plan_host) for (g, _), gp in zip(eng.groups, bp.group_plans)})
