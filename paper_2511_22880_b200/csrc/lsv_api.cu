@@ -50,6 +50,12 @@ const bool g_layer_kernel = [] { const char* e = std::getenv("LSV_LAYER_KERNEL")
 // readiness order (A/B timing)
 // layer kernel phase order (lsv_tc.cuh group_tc_kernel): group g's expand after the shrinks of groups <= g + d
 const int g_phase_lookahead = [] { const char* e = std::getenv("LSV_PHASE_LOOKAHEAD"); return e ? std::atoi(e) : 3; }();
+// layer kernel: expand items by dynamic dispatch from a per-group global cursor (lsv_tc.cuh group_dispatcher)
+// in calls of several layers (C2 8.43-8.57 ms vs 8.91-9.05 with each CTA's static LPT list, same box:
+// the static lists let the CTAs drift apart over a step's back-to-back layer launches, up to ~100 µs
+// by layer 8); a one-layer call keeps the static lists (no drift to absorb; 134 vs 142 µs for mlp_in)
+const bool g_dyn_expand = [] { const char* e = std::getenv("LSV_DYN_EXPAND"); return !e || std::atoi(e) != 0; }();
+const int g_dyn_order = [] { const char* e = std::getenv("LSV_DYN_ORDER"); return e ? std::atoi(e) : 1; }();
 const bool g_ready_order = [] { const char* e = std::getenv("LSV_READY_ORDER"); return !e || std::atoi(e) != 0; }();
 const int g_debug_fused = [] { const char* e = std::getenv("LSV_DEBUG_FUSED"); return e ? std::atoi(e) : 0; }();
 
@@ -186,6 +192,7 @@ struct PlanBuilder {
   int32_t red_units = 0;
   std::vector<int32_t> red_cta;
   std::vector<int32_t> tile_mt;      // tile-aligned plans: [n_gemm_tiles + 1] first piece per tile
+  std::vector<int32_t> dyn;          // dynamic expand dispatch order (PlanHeader::off_dyn)
 };
 
 // LPT greedy: items (already sorted by non-increasing cost) go to the least-loaded CTA; each
@@ -472,6 +479,32 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   const int expand_grid_all = (int)std::min<size_t>(all_costed.size(), (size_t)nsm);
   lpt_assign(all_costed, std::max(expand_grid_all, 1), pb.expand_all, pb.expand_all_cta, rem);
   if (g_ready_order && !rem) ready_order(pb.expand_all, pb.expand_all_cta);
+  {   // dynamic dispatch order over the group kernel's list: estimated tile readiness, then larger first
+    const std::vector<ExpandRec>& gl = P > 1 ? pb.expand_all : pb.expand[0];
+    std::vector<int64_t> key(gl.size());
+    for (size_t i = 0; i < gl.size(); ++i) {
+      const ExpandRec& r = gl[i];
+      const int tw = expand_item_tw(r.rank, b_tile_width(h_outs[r.proj]));
+      key[i] = (int64_t)tw * kpad(r.rank) * 2 + (int64_t)r.ntok * tw * 4;
+    }
+    pb.dyn.resize(gl.size());
+    for (size_t i = 0; i < gl.size(); ++i) pb.dyn[i] = (int32_t)i;
+    int64_t max_ready = 1;
+    for (int64_t t : tile_ready) max_ready = std::max(max_ready, t);
+    const int nb = g_dyn_order == 1 ? 8 : 1;   // 1: readiness in 8 buckets, h_out tiles interleaved inside each
+    std::stable_sort(pb.dyn.begin(), pb.dyn.end(), [&](int32_t a, int32_t b) {
+      const ExpandRec &x = gl[a], &y = gl[b];
+      if (g_dyn_order == 2) {   // h_out-tile major: consecutive items from different m-tiles
+        if (x.jtile != y.jtile) return x.jtile < y.jtile;
+      } else if (g_dyn_order == 1) {
+        const int64_t ba = tile_ready[x.mtile] * nb / (max_ready + 1), bb = tile_ready[y.mtile] * nb / (max_ready + 1);
+        if (ba != bb) return ba < bb;
+        if (x.jtile != y.jtile) return x.jtile < y.jtile;
+      }
+      const int64_t ra = tile_ready[x.mtile], rb = tile_ready[y.mtile];
+      return ra != rb ? ra < rb : key[a] > key[b];
+    });
+  }
 
   // header + workspace layout
   PlanHeader& h = pb.h;
@@ -530,6 +563,7 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
   }
   h.off_red_cta = off; off += (int32_t)red_cta.size();
   pb.red_cta = red_cta;
+  h.off_dyn = off; off += (int32_t)pb.dyn.size();
   h.tile_aligned = tile_aligned ? 1 : 0;
   if (tile_aligned) {   // [n_gemm_tiles + 1] first piece of every 128-token tile (pieces are in token order)
     const int nt = (N + kTileM - 1) / kTileM;
@@ -923,7 +957,8 @@ int run_group(const GroupArgs& a, int32_t num_tokens, int wait_prev, bool pdl, c
 }
 // A layer kernel: n (<= kLayerGroups) overlap-free groups back to back in one launch.
 constexpr int kLayerGroups = 4;
-int run_layer(const GroupArgs* a, int n, int32_t num_tokens, int wait_prev, bool pdl, cudaStream_t st) {
+// dyn: expand items by dynamic dispatch (calls of several layers: back-to-back layer launches)
+int run_layer(const GroupArgs* a, int n, int32_t num_tokens, int wait_prev, bool pdl, bool dyn, cudaStream_t st) {
   if (int rc = ensure_smem_attrs()) return rc;
   LayerParams<kLayerGroups> lp{};
   int grid = 0;
@@ -933,16 +968,24 @@ int run_layer(const GroupArgs* a, int n, int32_t num_tokens, int wait_prev, bool
   }
   lp.ngroups = n;
   lp.lookahead = g_phase_lookahead;
+  lp.dyn = dyn ? 1 : 0;
+  for (int i = 0; i < n && dyn; ++i) {   // cursor: the int after the group's 2 * n_mtiles counters
+    const PlanHeader* h = a[i].h;
+    lp.g[i].e.cursor = lp.g[i].ready + 2 * h->n_mtiles;
+    lp.g[i].e.off_dyn = h->off_dyn;
+    lp.g[i].e.n_dyn = h->num_proj > 1 ? h->n_expand_all : h->n_expand_items_p[0];
+  }
   group_trace(lp.g[0]);
   for (int i = 1; i < n; ++i) lp.g[i].s.trace = lp.g[i].e.trace = nullptr;
   LSV_CUDA_CHECK(launch_pdl(group_tc_kernel<kLayerGroups>, grid, group_smem_bytes(), st, lp, pdl, kGroupThreads));
   LSV_CUDA_CHECK(cudaGetLastError());
   return LSV_OK;
 }
-// lsv_lora_forward's group-kernel counters: 2 * n_mtiles ints per (layer, group), after the slices
+// lsv_lora_forward's group-kernel counters: 2 * n_mtiles ints per (layer, group) + the dynamic
+// dispatch cursor, after the slices
 size_t forward_counter_bytes(int L, int G, const PlanHeader* const* hs) {
   size_t n = 0;
-  for (int g = 0; g < G; ++g) n += 2 * (size_t)hs[g]->n_mtiles;
+  for (int g = 0; g < G; ++g) n += 2 * (size_t)hs[g]->n_mtiles + 1;
   return (n * 4 * (size_t)L + 255) / 256 * 256;
 }
 
@@ -1086,6 +1129,7 @@ static int plan_write(const PlanBuilder& pb, void* plan_host, size_t plan_bytes)
   std::copy(pb.expand_all_cta.begin(), pb.expand_all_cta.end(), out + h.off_expand_cta_all);
   std::copy(pb.red.begin(), pb.red.end(), out + h.off_red);
   std::copy(pb.red_cta.begin(), pb.red_cta.end(), out + h.off_red_cta);
+  std::copy(pb.dyn.begin(), pb.dyn.end(), out + h.off_dyn);
   if (h.tile_aligned) std::copy(pb.tile_mt.begin(), pb.tile_mt.end(), out + h.total_ints - (int32_t)pb.tile_mt.size());
   return LSV_OK;
 }
@@ -1347,7 +1391,7 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       const bool first = fs != nullptr ? l * num_groups + g < kFwdStreams : (l == 0 && g == 0);
       const cudaStream_t st = (fs != nullptr && si != 0) ? fs->s[si - 1] : st_main;
       int* const ready = counters + cnt_off;
-      cnt_off += 2 * (size_t)h->n_mtiles;
+      cnt_off += 2 * (size_t)h->n_mtiles + 1;
       if (h->num_tokens > 0 && group_kernel_eligible(h)) {
         if (!x || !aligned16(x) || ldx % 8 || ldx < h->h_in || num_tokens < h->num_tokens)
           return fail(LSV_EINVAL, "layer %d group %d: bad x", l, g);
@@ -1390,7 +1434,7 @@ int lsv_lora_forward_ex(int32_t num_layers, int32_t num_groups, const void* cons
       p0 += np;
     }
     if (layer_kernel)
-      if (int rc = run_layer(la, num_groups, num_tokens, l == 0 ? 1 : 0, l > 0, st_main)) return rc;
+      if (int rc = run_layer(la, num_groups, num_tokens, l == 0 ? 1 : 0, l > 0, g_dyn_expand && num_layers > 1, st_main)) return rc;
   }
   if (fs != nullptr)
     for (int i = 0; i < kFwdStreams - 1; ++i) {

@@ -50,7 +50,9 @@ struct PlanHeader {            // 64 int32
   // pieces of segments inside each 128-token tile of the batch; a piece's v image has 128 rows (the
   // tile's) with the piece at rows [tok_begin % 128, +ntok) and zeros elsewhere
   int32_t tile_aligned;
-  int32_t reserved[64 - 63];
+  // [n] int32: the group kernel's expand list (all members when num_proj > 1, else member 0's) in
+  // global readiness order, for the layer kernel's dynamic expand dispatch (0: none)
+  int32_t off_dyn;
 };
 static_assert(sizeof(PlanHeader) == 64 * 4, "plan header size");
 

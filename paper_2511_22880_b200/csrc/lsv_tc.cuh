@@ -100,6 +100,10 @@ struct alignas(64) ExpandParams {
   int num_tokens;               // bounds for the checked build (LSV_DCHECK)
   int h_outs[kMaxProj];
   int64_t ws_bytes;
+  // layer kernel, dynamic dispatch (cursor != nullptr): CTAs take items of the list in the plan's
+  // off_dyn order from a global cursor instead of walking their own LPT lists
+  int* cursor;
+  int off_dyn, n_dyn;
 };
 
 __device__ __forceinline__ void trace_stamp(uint64_t* trace, int trace_items, int cta, int i, int k) {
@@ -183,6 +187,45 @@ constexpr int kShrinkRecCh = 16;
 constexpr int kExpandRecCh = LSV_EXPAND_RECCH;
 using ShrinkRecBuf = WarpRecBuf<ShrinkRec, kShrinkRecCh>;
 using ExpandRecBuf = WarpRecBuf<ExpandRec, kExpandRecCh>;
+
+// Dynamic expand dispatch (layer kernel): the dispatcher warp takes the next item index from the
+// group's global cursor and publishes its record here; every expand role reads the records in
+// publication order.  A record with ntok == 0 ends the CTA's phase.  Slot reuse: the dispatcher
+// leads the copy warp by at most kVQ items (v-ready queue), which leads the MMA by kItemQ and the
+// epilogue by the TMEM buffers, plus one end record per phase: fewer than kDynQ positions.
+constexpr int kDynQ = 48;
+struct DynRing {
+  ExpandRec rec[kDynQ];
+  const uint8_t* ptr[kDynQ];
+  int published;                 // records published (monotone over the launch)
+};
+__device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// An expand role's record source: its CTA's static list, or the dynamic ring (dyn != nullptr;
+// q = the role's ring position, carried over phases).
+struct ExpSrc {
+  WarpRecStream<ExpandRec, kExpandRecCh> rs;
+  DynRing* dyn;
+  int* q;
+  __device__ __forceinline__ ExpSrc(ExpandRecBuf* b, const int32_t* plan, int off_recs, int off_cta, int cta,
+                                    const void* const* const* tables, DynRing* d, int* qpos)
+      : rs(b, plan, off_recs, off_cta, cta, tables), dyn(d), q(qpos) {}
+  __device__ __forceinline__ bool pop(ExpandRec& r, const uint8_t*& ptr) {
+    if (dyn == nullptr) return rs.pop(r, ptr);
+    const int pos = *q;
+    while (ld_acquire_cta_shared(&dyn->published) <= pos) {}
+    r = dyn->rec[pos % kDynQ];
+    ptr = dyn->ptr[pos % kDynQ];
+    *q = pos + 1;
+    return r.ntok != 0;
+  }
+};
 
 // Full-rank image column of local shard column k (a multiple of 8): contiguous shards put it at
 // tp_rank * rs + k; round-robin shards own every tp-th 8-row group, starting at group tp_rank.
@@ -385,6 +428,7 @@ struct PipeState {
   uint32_t s_tbits = 0;     // shrink TMEM buffers: bit b = parity of buffer b's next tfull wait
   int s_rec = 0;            // shrink records so far (recdone queue)
   int e_item = 0;           // expand items so far (ring allocations, v-ready queue)
+  int e_q = 0;              // dynamic dispatch ring position (items + end records)
   uint32_t e_tbits = 0;     // expand TMEM buffers: bit b = parity of buffer b's next tfull wait
 };
 // Byte ring shared by every pipeline a CTA runs (the layer kernel: shrink stages and expand items
@@ -850,6 +894,7 @@ struct ExpandSm {
   ExpandRecBuf* recbuf;   // indexed by warp
   uint32_t* offs;
   uint64_t *full, *empty, *tfull, *tempty;
+  DynRing* dyn;           // dynamic dispatch (layer kernel) or nullptr
 };
 // Producer (whole warp, converged): every lane keeps the same ring bookkeeping and computes the
 // same copy operands; each copy is issued by one elected lane inside its asm (issuing the y
@@ -869,7 +914,7 @@ __device__ __forceinline__ void expand_producer(const ExpandParams& p, const Exp
   // Every lane keeps the same ring bookkeeping and computes the same copy operands; each copy
   // is issued by one elected lane inside its asm.  (Issuing the y boxes from different lanes
   // made ptxas serialise them through a per-lane uniformization loop: ~1800 cycles per item.)
-  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs);
+  ExpSrc rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, p.b_ptrs, sm.dyn, &st.e_q);
   ExpandRec inf;
   const uint8_t* b;
   const int k0 = st.e_item;
@@ -952,7 +997,7 @@ __device__ __forceinline__ void expand_mma(const ExpandParams& p, const ExpandSm
   // Every lane runs the loop and computes the same descriptors; the election happens inside the
   // MMA asm, so ptxas emits no per-MMA uniformization loop.  Descriptors advance by constant
   // steps (start address field = byte address >> 4, which stays below 2^14 in shared memory).
-  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ExpSrc rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr, sm.dyn, &st.e_q);
   ExpandRec inf;
   const uint8_t* unused;
   const uint32_t ib = smem_u32(ident);
@@ -1031,7 +1076,7 @@ __device__ __forceinline__ void expand_epilogue(const ExpandParams& p, const Exp
   const int nbuf = kTmemCols / p.tw_max;
   const int q = warp & 3;
   const int half = (warp - 2) >> 2;          // with 8 epilogue warps: which half of the columns
-  WarpRecStream<ExpandRec, kExpandRecCh> rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr);
+  ExpSrc rs(&recbuf[warp], p.plan, p.off_recs, p.off_cta, cta, nullptr, sm.dyn, &st.e_q);
   ExpandRec inf;
   const uint8_t* unused;
   for (int k = 0; rs.pop(inf, unused); ++k) {
@@ -1177,7 +1222,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_tc_kernel(const __gr
   pdl_launch_dependents();
   if (threadIdx.x == 0) phase_stamp(p.trace, p.trace_items, cta, 2);
 
-  const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty};
+  const ExpandSm sm{ring, ident, recbuf, offs, full, empty, tfull, tempty, nullptr};
   PipeState st;
   if (warp == kExpProdWarp || (warp == kProdWarp2 && kProdParts == 2)) {
     const int part = warp == kExpProdWarp ? 0 : 1;
@@ -1224,6 +1269,7 @@ struct alignas(64) LayerParams {
   GroupParams g[NG];
   int ngroups;
   int lookahead;       // phase order: group g's expand runs after the shrinks of groups <= g + lookahead
+  int dyn;             // 1: expand items by dynamic dispatch (every group's e.cursor set)
 };
 union RecBufU {
   ShrinkRecBuf s;
@@ -1232,7 +1278,7 @@ union RecBufU {
 __host__ __device__ constexpr int group_smem_bytes() {
   return 1024 + kExpandRingBytes + kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU) + 2 * kItemQ * 4 +
          8 * (2 * kShrinkStages + 2 * kAccBufs + 2 * kItemQ + 2 * kAccBufs + 2 * kVQ + kRecQ) + 32 +
-         2 * kRingTableWords * 4 + 1024;
+         2 * kRingTableWords * 4 + (int)sizeof(DynRing) + 16 + 1024;
 }
 static_assert(kShrinkGuardBytes <= kExpandGuardBytes + kIdentRows * 16 * 2 + 9 * (int)sizeof(RecBufU),
               "a shrink stage's MMA over-read past the ring end stays inside the group kernel's shared memory");
@@ -1320,6 +1366,66 @@ __device__ __forceinline__ void group_ready_checker(const ExpandParams& p, Expan
   }
   item_base = k;
 }
+// Warp 4, expand phase with dynamic dispatch: takes the group's items in batches of kDynBatch
+// (one atomicAdd on the cursor; the lanes load the records and adapter pointers in parallel),
+// publishes them to the CTA's expand roles, then releases each item's v copy once its m-tile is
+// complete.  A batch is taken only when the copy warp has taken item k - kDynLead, so every CTA
+// holds about the same few items when the list runs out (the phase ends together on every SM).
+// The end record goes out when the list is exhausted.
+#ifndef LSV_DYN_BATCH
+#define LSV_DYN_BATCH 4
+#endif
+#ifndef LSV_DYN_LEAD
+#define LSV_DYN_LEAD 4
+#endif
+constexpr int kDynBatch = LSV_DYN_BATCH;
+constexpr int kDynLead = LSV_DYN_LEAD;
+static_assert(kDynBatch - 1 + kDynLead < kVQ && kDynLead + kDynBatch + kVQ + kItemQ + 4 + 4 < kDynQ,
+              "dynamic dispatch lead within the v-ready queue and the record ring");
+__device__ __forceinline__ void group_dispatcher(const ExpandParams& p, DynRing* dr, int lane, const int* ready,
+                                                 uint64_t* vfull, uint64_t* vempty, int& item_base, int& q_base) {
+  const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
+  const ExpandRec* recs = reinterpret_cast<const ExpandRec*>(p.plan + p.off_recs);
+  const int32_t* order = p.plan + p.off_dyn;
+  int k = item_base, q = q_base, last = -1;
+  for (bool done = false; !done;) {
+    const int j = k - kDynLead;   // the copy warp took item j: bounded lead (and v-queue slots free)
+    if (j >= 0) mbar_wait(&vempty[j % kVQ], (j / kVQ) & 1);
+    int base = 0;
+    if (lane == 0) base = atomicAdd(p.cursor, kDynBatch);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int nvalid = max(0, min(kDynBatch, p.n_dyn - base));
+    done = nvalid < kDynBatch;
+    const int npub = nvalid + (done ? 1 : 0);   // + the end record
+    if (lane < npub) {
+      ExpandRec r{};
+      const uint8_t* ptr = nullptr;
+      if (lane < nvalid) {
+        r = recs[order[base + lane]];
+        ptr = static_cast<const uint8_t*>(p.b_ptrs[r.proj][r.seg]);
+      }
+      dr->rec[(q + lane) % kDynQ] = r;
+      dr->ptr[(q + lane) % kDynQ] = ptr;
+    }
+    __syncwarp();
+    if (lane == 0) st_release_cta_shared(&dr->published, q + npub);
+    for (int i = 0; i < nvalid; ++i, ++k) {
+      const int mt = dr->rec[(q + i) % kDynQ].mtile;
+      if (lane == 0) {
+        if (mt != last) {
+          wait_geq_gpu(&ready[mt], mts[mt].counter);
+          fence_proxy_async_global();
+          last = mt;
+        }
+        mbar_arrive(&vfull[k % kVQ]);
+      }
+    }
+    __syncwarp();
+    q += npub;
+  }
+  item_base = k;
+  q_base = q;
+}
 
 constexpr int kGroupThreads = 288;   // the standalone layout + warp 8 (second copy-issuing part)
 template <int NG>
@@ -1347,6 +1453,8 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   uint64_t* recdone = vempty + kVQ;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recdone + kRecQ) + 1;   // [0]: published-record count
   uint32_t* ring_tab = tmem_slot + 1;                                          // [kProdParts][kRingTableWords]
+  DynRing* dyn = reinterpret_cast<DynRing*>(
+      (reinterpret_cast<uintptr_t>(ring_tab + kProdParts * kRingTableWords) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -1369,6 +1477,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
     for (int q = 0; q < kVQ; ++q) { mbar_init(&vfull[q], 1); mbar_init(&vempty[q], 1); }
     for (int q = 0; q < kRecQ; ++q) mbar_init(&recdone[q], 4);
     *reinterpret_cast<volatile int*>(recdone + kRecQ) = 0;
+    dyn->published = 0;
     fence_mbar_init();
     for (int b = 0; b < 5; ++b) prefetch_tmap(&sp.xmap[b]);
     for (int pp = 0; pp < kMaxProj; ++pp)
@@ -1385,7 +1494,11 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
   if (gp.wait_prev) pdl_wait();
   pdl_launch_dependents();
   const ShrinkSm ssm{ring, &recbuf[0].s, s_full, s_empty, s_tfull, s_tempty, offs + kItemQ};
-  const ExpandSm esm{ring, ident, &recbuf[0].e, offs, e_full, e_empty, e_tfull, e_tempty};
+  const bool dyn_on = NG > 1 && lp.dyn;
+  const ExpandSm esm{ring, ident, &recbuf[0].e, offs, e_full, e_empty, e_tfull, e_tempty, dyn_on ? dyn : nullptr};
+  // dynamic dispatch: every CTA of the launch runs every expand phase (it takes items until the
+  // group's list is exhausted)
+  auto runs_expand = [&](const GroupParams& G) { return dyn_on || cta < G.e_grid; };
   // the role functions index recbuf by warp: give each a pointer whose [warp] is this warp's union slot
   ShrinkSm ssw = ssm;
   ssw.recbuf = reinterpret_cast<ShrinkRecBuf*>(&recbuf[warp]) - warp;
@@ -1431,7 +1544,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
         if (cta < G.s_grid) shrink_producer(G.s, ssw, cta, warp, lane, part, kProdParts, st, ra, kExpandRingBytes,
                                             kExpandGuardBytes);
         if (lane == 0 && part == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, 2);   // shrink stages issued
-      } else if (cta < G.e_grid) {
+      } else if (runs_expand(G)) {
         expand_producer(G.e, esw, cta, warp, lane, vfull, vempty, part, kProdParts, st, ra);
       }
     }
@@ -1445,7 +1558,7 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
         shrink_mma(G.s, ssw, tmem_base, cta, warp, lane, st);
         for (int b = 0; b < kAccBufs; ++b) mbar_wait(&s_tempty[b], ((st.s_tbits >> b) & 1) ^ 1);   // accumulators drained
         tc_fence_after();
-      } else if (ex && cta < G.e_grid) {
+      } else if (ex && runs_expand(G)) {
         expand_mma(G.e, esw, tmem_base, cta, warp, lane, st);
         if (i + 1 < nph) {
           for (int b = 0; b < kAccBufs; ++b) mbar_wait(&e_tempty[b], ((st.e_tbits >> b) & 1) ^ 1);
@@ -1460,18 +1573,19 @@ __global__ void __launch_bounds__(kGroupThreads, 1) group_tc_kernel(const __grid
       const bool ex = phase_of(i, g);
       const GroupParams& G = lp.g[g];
       if (!ex && cta < G.s_grid) shrink_epilogue(G.s, ssw, tmem_base, cta, warp, lane, recdone, st);
-      if (ex && cta < G.e_grid) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
+      if (ex && runs_expand(G)) expand_epilogue(G.e, esw, tmem_base, cta, warp, lane, st);
       if (warp == 0 && lane == 0) phase_stamp(G.s.trace, G.s.trace_items, cta, ex ? 4 : 1);   // phase stored
       if (gp.tl != nullptr && warp == 0 && lane == 0 && i < 12) gp.tl[cta * 16 + 4 + i] = globaltimer_ns();
     }
   } else if (warp == 4) {
-    int rec_base = 0, item_base = 0;
+    int rec_base = 0, item_base = 0, q_base = 0;
     for (int i = 0; i < nph; ++i) {
       int g;
       const bool ex = phase_of(i, g);
       const GroupParams& G = lp.g[g];
       if (!ex && cta < G.s_grid) group_signaler(G.s, &recbuf[warp].s, cta, lane, G.ready, G.split_done, recdone, rec_base);
-      if (ex && cta < G.e_grid) group_ready_checker(G.e, &recbuf[warp].e, cta, lane, G.ready, vfull, vempty, item_base);
+      if (ex && dyn_on) group_dispatcher(G.e, dyn, lane, G.ready, vfull, vempty, item_base, q_base);
+      else if (ex && cta < G.e_grid) group_ready_checker(G.e, &recbuf[warp].e, cta, lane, G.ready, vfull, vempty, item_base);
     }
   } else if (warp == 5) {
     for (int i = 0; i < nph; ++i) {
