@@ -1387,7 +1387,7 @@ __device__ __forceinline__ void group_dispatcher(const ExpandParams& p, DynRing*
   const MTile* mts = reinterpret_cast<const MTile*>(p.plan + p.off_mtiles);
   const ExpandRec* recs = reinterpret_cast<const ExpandRec*>(p.plan + p.off_recs);
   const int32_t* order = p.plan + p.off_dyn;
-  int k = item_base, q = q_base, last = -1;
+  int k = item_base, q = q_base;
   for (bool done = false; !done;) {
     const int j = k - kDynLead;   // the copy warp took item j: bounded lead (and v-queue slots free)
     if (j >= 0) mbar_wait(&vempty[j % kVQ], (j / kVQ) & 1);
@@ -1409,18 +1409,14 @@ __device__ __forceinline__ void group_dispatcher(const ExpandParams& p, DynRing*
     }
     __syncwarp();
     if (lane == 0) st_release_cta_shared(&dr->published, q + npub);
-    for (int i = 0; i < nvalid; ++i, ++k) {
-      const int mt = dr->rec[(q + i) % kDynQ].mtile;
-      if (lane == 0) {
-        if (mt != last) {
-          wait_geq_gpu(&ready[mt], mts[mt].counter);
-          fence_proxy_async_global();
-          last = mt;
-        }
-        mbar_arrive(&vfull[k % kVQ]);
-      }
+    if (lane < nvalid) {   // each lane releases its item's v copy when the m-tile is complete (any order)
+      const int mt = dr->rec[(q + lane) % kDynQ].mtile;
+      wait_geq_gpu(&ready[mt], mts[mt].counter);
+      fence_proxy_async_global();
+      mbar_arrive(&vfull[(k + lane) % kVQ]);
     }
     __syncwarp();
+    k += nvalid;
     q += npub;
   }
   item_base = k;
