@@ -507,6 +507,13 @@ def run_ours(args, rank, world, local_rank):
                                 "stream (each call: a ~4 KB counter memset + the kernel)",
                       "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of the "
                                         "same launch from one ncu --set full capture (tools/prof_group.py)",
+                      # inside the step the layer kernels run back to back (PDL, dynamic expand dispatch):
+                      # the step time over its launches is their average duration there
+                      "in_step": ({"launch_us": ms * 1e3 / launches,
+                                   "frac": lay_bytes / (ms * 1e-3 / launches) / 1e9 / hbm_peak,
+                                   "note": "step time / layer-kernel launches per step (the step is only these "
+                                           "launches and one counter memset)"}
+                                  if launches == wl.model.layers and world == 1 else None),
                       "group_kernel": {"kernel": grp_label, "launch_us": grp_us, "algorithmic_bytes_per_launch": grp_bytes,
                                        "achieved": grp_bytes / (grp_us * 1e-6) / 1e9,
                                        "frac": grp_bytes / (grp_us * 1e-6) / 1e9 / hbm_peak},
