@@ -38,10 +38,26 @@ lib = native.lib()
 lib.lsv_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 lib.lsv_debug_set_trace(buf.data_ptr(), -n)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-eng.forward(bp, xs, ys)
-e1.record()
-torch.cuda.synchronize()
+import os
+if os.environ.get("TL_GRAPH"):   # the step as bench.py runs it: one CUDA graph replay
+    st = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        eng.forward(bp, xs, ys, st)
+    lib.lsv_debug_set_trace(None, 0)
+    with torch.cuda.stream(st):
+        graph.replay()          # warm
+        torch.cuda.synchronize()
+        buf.zero_()
+        e0.record(st)
+        graph.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+else:
+    e0.record()
+    eng.forward(bp, xs, ys)
+    e1.record()
+    torch.cuda.synchronize()
 lib.lsv_debug_set_trace(None, 0)
 tl = buf.view(n, 148, 16).cpu().numpy().astype(np.int64)
 n = int((tl[:, :, 0].max(axis=1) > 0).sum())   # launches recorded: 4L group kernels or L layer kernels
