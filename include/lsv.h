@@ -209,7 +209,9 @@ int lsv_lora_expand_group(void* const* ys, const int64_t* ldys, int32_t num_toke
  * plus per-m-tile counters (lsv_lora_forward_workspace bytes, zero-filled once; the call zero-fills
  * the counters itself, ordered on `stream`).  How the work is launched:
  *   - an overlap-free call (below) whose groups are all tensor-core tier: one launch per layer
- *     (every group's shrink and expand in one persistent kernel, <= 4 groups);
+ *     (every group's shrink and expand in one persistent kernel, <= 4 groups); with more than one
+ *     layer its CTAs take expand items from a per-(layer, group) cursor in the counter area
+ *     (dynamic dispatch; the result bits do not depend on which CTA computes an item);
  *   - otherwise each tensor-core group is one launch (shrink + expand); SIMT-tier groups are a
  *     shrink and an expand launch;
  *   - an overlap-free call without layer launches issues group g of layer l on one of 4 streams
