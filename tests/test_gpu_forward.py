@@ -193,6 +193,45 @@ def test_group_kernel_full_layer_bit_identical_to_split_launches():
         assert torch.equal(ys[0][pr.name], ys2[0][pr.name]), pr.name
 
 
+def test_layer_kernel_dynamic_dispatch_c2_three_layers_bit_identical():
+    """Three Llama-2-7B layers of the C2 batch through lsv_lora_forward — one layer kernel per
+    layer: all four input groups' shrink stages and expand items through one shared-memory byte
+    ring, every shrink before any expand, expand items taken from per-(layer, group) global cursors
+    (dynamic dispatch, multi-layer calls) — against the separate shrink / expand launches of the
+    same work: bit-identical (which CTA computes an item does not change its bits)."""
+    from paper_2511_22880_b200.lora import LoraDeltaEngine
+    from paper_2511_22880_b200.segments import index_tokens
+    from paper_2511_22880_b200.shapes import LLAMA2_7B, ModelShape
+    from paper_2511_22880_b200.slab import AdapterSlab
+    dev = torch.device("cuda:0")
+    model = ModelShape("l7b-3l", 3, LLAMA2_7B.projections)
+    ranks = [8] * 44 + [16] * 22 + [32] * 14 + [64] * 11 + [128] * 9
+    slab = AdapterSlab(model, AdapterSlab.capacity_for(model, ranks), dev)
+    for i, r in enumerate(ranks):
+        slab.fill_random(slab.allocate(f"a{i}", r), 900 + i)
+    seg = index_tokens(np.random.default_rng(11).integers(0, 100, 4096), ranks)
+    eng = LoraDeltaEngine(slab)
+    bp = eng.prepare(seg)
+    assert eng.launches_per_step(bp) == model.layers     # one layer kernel per layer
+    g = torch.Generator().manual_seed(12)
+    xs = [{name: torch.randn(4096, model.projections[m[0]].h_in, generator=g).to(torch.bfloat16).to(dev)
+           for name, m in model.groups()} for _ in range(model.layers)]
+    ys = [{p.name: torch.randn(4096, p.h_out, generator=g).to(torch.bfloat16).to(dev) for p in model.projections}
+          for _ in range(model.layers)]
+    ys2 = [{k: v.clone() for k, v in d.items()} for d in ys]
+    eng.forward(bp, xs, ys)
+    eng.forward(bp, xs, ys)                                  # twice: the cursors are re-armed per call
+    for _ in range(2):
+        for layer in range(model.layers):
+            for gi, (name, members) in enumerate(model.groups()):
+                eng.shrink(bp, layer, members[0], xs[layer][name])
+                eng.expand_group(bp, layer, gi, [ys2[layer][model.projections[p].name] for p in members])
+    torch.cuda.synchronize()
+    for layer in range(model.layers):
+        for pr in model.projections:
+            assert torch.equal(ys[layer][pr.name], ys2[layer][pr.name]), (layer, pr.name)
+
+
 @pytest.mark.parametrize("names", [("q_proj", "k_proj", "v_proj", "o_proj"),            # 2 groups: layer kernel
                                    ("q_proj", "o_proj", "gate_proj", "up_proj", "down_proj", "k_proj")])   # 5 groups
 def test_forward_group_counts_bit_identical(names):
