@@ -504,6 +504,24 @@ int build_plan(PlanBuilder& pb, int32_t S, const int32_t* indptr, const int32_t*
       const int64_t ra = tile_ready[x.mtile], rb = tile_ready[y.mtile];
       return ra != rb ? ra < rb : key[a] > key[b];
     });
+    if (rem) {   // peer-owned items (NVLink) and local ones (HBM) merged by their estimated time on
+                 // each link, so both stay busy to the end of the list (~8x HBM / NVLink bandwidth)
+      std::vector<int32_t> loc, rmt;
+      for (int32_t i : pb.dyn) (remote[gl[i].seg] ? rmt : loc).push_back(i);
+      pb.dyn.clear();
+      int64_t tl = 0, tr = 0;
+      size_t il = 0, ir = 0;
+      while (il < loc.size() || ir < rmt.size()) {
+        if (ir < rmt.size() && (il == loc.size() || tr <= tl)) {
+          const ExpandRec& r = gl[rmt[ir]];
+          tr += (int64_t)expand_item_tw(r.rank, b_tile_width(h_outs[r.proj])) * kpad(r.rank) * 2 * 8;
+          pb.dyn.push_back(rmt[ir++]);
+        } else {
+          tl += key[loc[il]];
+          pb.dyn.push_back(loc[il++]);
+        }
+      }
+    }
   }
 
   // header + workspace layout
