@@ -219,7 +219,14 @@ struct ExpSrc {
   __device__ __forceinline__ bool pop(ExpandRec& r, const uint8_t*& ptr) {
     if (dyn == nullptr) return rs.pop(r, ptr);
     const int pos = *q;
-    while (ld_acquire_cta_shared(&dyn->published) <= pos) {}
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; ld_acquire_cta_shared(&dyn->published) <= pos; ++spin) {
+      if ((spin & 1023u) == 1023u) {   // bounded like every other wait: trap after ~4 s instead of hanging
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 4000000000ull) __trap();
+      }
+    }
     r = dyn->rec[pos % kDynQ];
     ptr = dyn->ptr[pos % kDynQ];
     *q = pos + 1;
