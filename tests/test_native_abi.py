@@ -350,3 +350,20 @@ def test_skip_flags_and_sm_budget():
     blob, _ = _plan(indptr, ranks, policy=native.PLAN_SMS(20))
     d = _decode(blob)
     assert d["shrink_grid"] <= 20 and d["expand_grid"] <= 20 and d["n_mtiles"] == 1 + 3 + 1 + 2
+
+
+def test_dynamic_dispatch_order_is_a_permutation_of_the_group_list():
+    """PlanHeader::off_dyn (the layer kernel's dynamic expand dispatch order) lists every item of
+    the group kernel's expand list (all members when num_proj > 1, else member 0's) exactly once."""
+    rng = np.random.default_rng(5)
+    ranks = [8] * 30 + [16] * 10 + [32] * 8 + [64] * 6 + [128] * 6
+    lens = rng.integers(9, 120, len(ranks))
+    indptr = np.concatenate(([0], np.cumsum(lens)))
+    for h_in, h_outs in ((4096, [11008, 11008]), (4096, [4096, 1024, 1024]), (11008, [4096])):
+        blob, _ = _plan_group(indptr, ranks, h_in, h_outs)
+        h = blob[:64]
+        P, off_dyn = int(h[33]), int(h[63])
+        n = int(h[60]) if P > 1 else int(h[53])
+        assert off_dyn > 0 and off_dyn + n <= int(h[21])
+        order = blob[off_dyn:off_dyn + n]
+        assert np.array_equal(np.sort(order), np.arange(n))
